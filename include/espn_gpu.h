@@ -1,0 +1,207 @@
+/*
+ * espn_gpu.h -- C-ABI of the B200-native ESPN re-ranking hot path
+ * (gather candidate token rows -> MaxSim -> aggregate -> top-k).
+ *
+ * This is the drop-in boundary: the reference keeps re-ranking inside
+ * `espn::run_query` (proj/include/espn/pipeline.hpp:56-64) over
+ * `StoreHandle::fetch_batch` (store.hpp:91-94) + `maxsim_score` /
+ * `aggregate_score` / `rank` (scoring.hpp:7-21).  These entry points replace
+ * exactly that path; the C++ wrapper in include/espn_b200.hpp re-exposes them
+ * with the reference's types and exceptions.  Conventions:
+ *   - extern "C", POD structs, no exceptions, no STL, no torch types;
+ *   - every call returns an espn_status (one code per error class of
+ *     error.hpp:8-42) and leaves a thread-local message in espn_last_error();
+ *   - tables are opaque, read-only after open and shareable across threads;
+ *     a workspace holds per-stream scratch and must not be used by two
+ *     threads at once (one in-flight batch per workspace);
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ * There is no CPU fallback: without a usable sm_100 device every call that
+ * touches the device returns ESPN_E_CUDA.
+ */
+#ifndef ESPN_GPU_H
+#define ESPN_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESPN_GPU_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ESPN_API __attribute__((visibility("default")))
+#else
+#define ESPN_API
+#endif
+
+/* error.hpp:14-42, plus a device/runtime failure class. */
+typedef enum {
+  ESPN_OK = 0,
+  ESPN_E_INVALID_INPUT = 1,   /* InvalidInputError */
+  ESPN_E_INVALID_STATE = 2,   /* InvalidStateError */
+  ESPN_E_INVALID_CONFIG = 3,  /* InvalidConfigError */
+  ESPN_E_FORMAT = 4,          /* FormatError */
+  ESPN_E_IO = 5,              /* IoError */
+  ESPN_E_DATA_INTEGRITY = 6,  /* DataIntegrityError */
+  ESPN_E_CUDA = 7             /* device / runtime failure (espn::Error) */
+} espn_status;
+
+typedef enum { ESPN_DTYPE_F16 = 0, ESPN_DTYPE_BF16 = 1 } espn_dtype;
+
+/* MaxSim implementation selector (north_star: tcgen05 path plus a CUDA-core
+ * path for tiny dims, chosen by measurement). */
+typedef enum {
+  ESPN_KERNEL_AUTO = 0,
+  ESPN_KERNEL_TCGEN05 = 1,
+  ESPN_KERNEL_SIMT = 2
+} espn_kernel;
+
+typedef struct espn_gpu_table espn_gpu_table;
+typedef struct espn_gpu_workspace espn_gpu_workspace;
+
+/* Table flags. */
+#define ESPN_TABLE_DEVICE_BORROWED 0x1u /* row_ptr/rows are device pointers owned by the caller */
+
+/* The embedding table (store.hpp:13-35).  The HBM tier holds BOW rows only as
+ * CSR: doc i's t_i token rows live at rows[row_ptr[i]*d .. row_ptr[i+1]*d),
+ * 2-byte codes of `dtype`.  d_cls / value_width / alignment describe the
+ * reference's on-disk record (record_bytes = (d_cls + t*d)*value_width) and are
+ * used only for QueryStats byte accounting.  Replaces open_store()
+ * (store.hpp:109-112) + the manifest (store.hpp:20-35). */
+typedef struct {
+  uint64_t n_docs;
+  uint32_t d;            /* token dim: multiple of 16, 16..256 */
+  uint32_t dtype;        /* espn_dtype */
+  uint32_t d_cls;
+  uint32_t value_width;  /* 2 or 4 */
+  uint32_t alignment;    /* 1, 512 or 4096 */
+  uint32_t flags;        /* ESPN_TABLE_* */
+  const uint64_t* row_ptr; /* n_docs + 1 token offsets, row_ptr[0] == 0 */
+  const uint16_t* rows;    /* row_ptr[n_docs] * d codes */
+  int32_t device;          /* CUDA device ordinal */
+  uint32_t reserved[7];
+} espn_table_desc;
+
+typedef struct {
+  uint64_t n_docs;
+  uint64_t n_tokens;
+  uint32_t d;
+  uint32_t dtype;
+  uint32_t max_tokens;     /* longest doc */
+  uint32_t min_tokens;
+  uint64_t hbm_bytes;      /* device bytes held by the table */
+} espn_table_info;
+
+/* Validates (t >= 1 per doc, row_ptr monotone; types.hpp:64-68) and uploads
+ * the table to HBM (or adopts device pointers when DEVICE_BORROWED). */
+ESPN_API int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out);
+ESPN_API int espn_gpu_table_close(espn_gpu_table* table);
+ESPN_API int espn_gpu_table_info(const espn_gpu_table* table, espn_table_info* out);
+
+/* Per-stream scratch sized for at most max_queries queries and
+ * max_candidates candidates per batch (sum over the batch). */
+typedef struct {
+  uint32_t max_queries;
+  uint32_t max_candidates;
+  uint32_t max_query_tokens; /* <= 32 */
+  uint32_t reserved[5];
+} espn_workspace_desc;
+
+ESPN_API int espn_gpu_workspace_create(espn_gpu_table* table, const espn_workspace_desc* desc,
+                              espn_gpu_workspace** out);
+ESPN_API int espn_gpu_workspace_destroy(espn_gpu_workspace* ws);
+
+/* Re-rank flags (PipelineConfig, pipeline.hpp:11-29, plus I/O placement). */
+#define ESPN_RERANK_PARTIAL 0x1u      /* partial_rerank_enabled: tail beyond R scored alpha*cls */
+#define ESPN_RERANK_DEVICE_IO 0x2u    /* all array pointers in args/out are device pointers */
+#define ESPN_RERANK_ASYNC 0x4u        /* do not synchronize; errors surface in espn_gpu_workspace_sync */
+#define ESPN_RERANK_WRITE_BOW 0x8u    /* also return per-candidate MaxSim (bow) scores */
+
+/* One batch of queries with their final candidate lists (ivf.hpp:45-50:
+ * sorted (cls_score desc, doc_id asc), deduplicated), CSR over queries.
+ * This is the "candidates in -> ranked out" seam of run_query stages 3-6
+ * (SPEC.md:276): needed = first min(R, n_b) candidates of query b, each scored
+ * alpha*cls + MaxSim(query, doc); tail beyond R scored alpha*cls when PARTIAL;
+ * rank by (score desc, doc_id asc); truncate to final_k. */
+typedef struct {
+  uint32_t n_queries;            /* B */
+  uint32_t n_query_tokens;       /* q (rows of QueryEmbedding, types.hpp:34-43), 1..32 */
+  const float* query_tokens;     /* B * q * d fp32, row-major */
+  const uint32_t* cand_ids;      /* cand_offsets[B] entries */
+  const float* cand_cls;         /* cls_score per candidate */
+  const uint64_t* cand_offsets;  /* B + 1; always a HOST pointer */
+  uint32_t rerank_count;         /* R */
+  uint32_t final_k;              /* k (>= 1) */
+  float alpha;                   /* CLS scaling (aggregate_score) */
+  uint32_t flags;                /* ESPN_RERANK_* */
+  uint32_t kernel;               /* espn_kernel */
+  /* Optional HOST array of B per-query needed counts overriding min(R, n_b):
+   * with doc-id sharding a shard's needed set is its share of the global
+   * top-R prefix, which differs per query. NULL = min(R, n_b). */
+  const uint32_t* needed_counts;
+  uint32_t reserved[3];
+} espn_rerank_args;
+
+typedef struct {
+  uint32_t* ids;        /* B * final_k */
+  float* scores;        /* B * final_k */
+  uint32_t* counts;     /* B: entries written for each query */
+  float* bow_scores;    /* optional (WRITE_BOW): cand_offsets[B] MaxSim scores; entries of
+                           candidates beyond R are left untouched */
+} espn_rerank_out;
+
+ESPN_API int espn_gpu_rerank(espn_gpu_table* table, espn_gpu_workspace* ws,
+                    const espn_rerank_args* args, espn_rerank_out* out, void* stream);
+
+/* Completes an ASYNC batch on its stream and reports device-side errors
+ * (unknown doc id -> DATA_INTEGRITY, non-finite query/cls -> INVALID_INPUT,
+ * duplicate candidate -> INVALID_INPUT). */
+ESPN_API int espn_gpu_workspace_sync(espn_gpu_workspace* ws, void* stream);
+
+/* Gather (StoreHandle::fetch_batch, store.hpp:91-94): copies the token rows of
+ * `ids` (request order, duplicates allowed) into out_rows as CSR with
+ * out_row_ptr[n+1] (token offsets).  ids/out_* are device pointers.
+ * capacity_tokens bounds out_rows.  Unknown id -> INVALID_INPUT. */
+ESPN_API int espn_gpu_gather(espn_gpu_table* table, const uint32_t* ids, uint64_t n,
+                    uint16_t* out_rows, uint64_t* out_row_ptr, uint64_t capacity_tokens,
+                    void* stream);
+
+/* Merge per-shard ranked lists (multi-GPU, doc-id sharding): for each of
+ * n_queries queries, `n_lists` ranked lists of up to k entries each laid out
+ * [list][query][k] with counts [list][query], merged into the global top-k by
+ * (score desc, doc_id asc).  Device pointers. */
+ESPN_API int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const uint32_t* counts,
+                        uint32_t n_lists, uint32_t n_queries, uint32_t k, uint32_t* out_ids,
+                        float* out_scores, uint32_t* out_counts, void* stream);
+
+/* Cumulative device counters of a workspace (bytes gathered, pairs scored,
+ * kernel launches) since creation. */
+typedef struct {
+  uint64_t batches;
+  uint64_t queries;
+  uint64_t pairs_scored;
+  uint64_t tokens_scored;
+  uint64_t kernel_launches;
+  uint64_t reserved[3];
+} espn_counters;
+ESPN_API int espn_gpu_get_counters(const espn_gpu_workspace* ws, espn_counters* out);
+
+/* Synthetic MS-MARCO-shaped table generation on the device (bench/tests):
+ * t_i ~ U{t_min..t_max} and i.i.d. N(0,1) rows L2-normalised per row, rounded to
+ * dtype with subnormals flushed; counter-based RNG so
+ * any doc can be regenerated independently.  Writes row_ptr (n_docs+1) and rows
+ * (device pointers; rows must hold row_ptr[n_docs]*d codes -- call with
+ * rows == NULL first to fill row_ptr only). */
+ESPN_API int espn_gpu_synth_table(uint64_t n_docs, uint32_t d, uint32_t dtype, uint32_t t_min,
+                         uint32_t t_max, uint64_t seed, uint64_t* row_ptr, uint16_t* rows,
+                         void* stream);
+
+ESPN_API const char* espn_last_error(void);
+ESPN_API int espn_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESPN_GPU_H */

@@ -1,0 +1,127 @@
+"""ctypes binding of include/espn_gpu.h (the C-ABI of libespn_gpu.so).
+
+The library is loaded from the package's lib/ directory only (built in-tree by
+paper_2312_05417_b200.build).  There is deliberately no fallback: if the
+shared object is missing or fails to load, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libespn_gpu.so"
+
+ESPN_OK = 0
+ESPN_E_INVALID_INPUT = 1
+ESPN_E_INVALID_STATE = 2
+ESPN_E_INVALID_CONFIG = 3
+ESPN_E_FORMAT = 4
+ESPN_E_IO = 5
+ESPN_E_DATA_INTEGRITY = 6
+ESPN_E_CUDA = 7
+
+ESPN_DTYPE_F16 = 0
+ESPN_DTYPE_BF16 = 1
+
+ESPN_KERNEL_AUTO = 0
+ESPN_KERNEL_TCGEN05 = 1
+ESPN_KERNEL_SIMT = 2
+
+ESPN_TABLE_DEVICE_BORROWED = 0x1
+
+ESPN_RERANK_PARTIAL = 0x1
+ESPN_RERANK_DEVICE_IO = 0x2
+ESPN_RERANK_ASYNC = 0x4
+ESPN_RERANK_WRITE_BOW = 0x8
+
+
+class TableDesc(C.Structure):
+    _fields_ = [
+        ("n_docs", C.c_uint64), ("d", C.c_uint32), ("dtype", C.c_uint32),
+        ("d_cls", C.c_uint32), ("value_width", C.c_uint32), ("alignment", C.c_uint32),
+        ("flags", C.c_uint32), ("row_ptr", C.c_void_p), ("rows", C.c_void_p),
+        ("device", C.c_int32), ("reserved", C.c_uint32 * 7),
+    ]
+
+
+class TableInfo(C.Structure):
+    _fields_ = [
+        ("n_docs", C.c_uint64), ("n_tokens", C.c_uint64), ("d", C.c_uint32),
+        ("dtype", C.c_uint32), ("max_tokens", C.c_uint32), ("min_tokens", C.c_uint32),
+        ("hbm_bytes", C.c_uint64),
+    ]
+
+
+class WorkspaceDesc(C.Structure):
+    _fields_ = [
+        ("max_queries", C.c_uint32), ("max_candidates", C.c_uint32),
+        ("max_query_tokens", C.c_uint32), ("reserved", C.c_uint32 * 5),
+    ]
+
+
+class RerankArgs(C.Structure):
+    _fields_ = [
+        ("n_queries", C.c_uint32), ("n_query_tokens", C.c_uint32),
+        ("query_tokens", C.c_void_p), ("cand_ids", C.c_void_p), ("cand_cls", C.c_void_p),
+        ("cand_offsets", C.c_void_p), ("rerank_count", C.c_uint32), ("final_k", C.c_uint32),
+        ("alpha", C.c_float), ("flags", C.c_uint32), ("kernel", C.c_uint32),
+        ("needed_counts", C.c_void_p), ("reserved", C.c_uint32 * 3),
+    ]
+
+
+class RerankOut(C.Structure):
+    _fields_ = [
+        ("ids", C.c_void_p), ("scores", C.c_void_p), ("counts", C.c_void_p),
+        ("bow_scores", C.c_void_p),
+    ]
+
+
+class Counters(C.Structure):
+    _fields_ = [
+        ("batches", C.c_uint64), ("queries", C.c_uint64), ("pairs_scored", C.c_uint64),
+        ("tokens_scored", C.c_uint64), ("kernel_launches", C.c_uint64),
+        ("reserved", C.c_uint64 * 3),
+    ]
+
+
+# name -> (restype, argtypes); every symbol declared in include/espn_gpu.h
+SIGNATURES = {
+    "espn_gpu_table_open": (C.c_int, [C.POINTER(TableDesc), C.POINTER(C.c_void_p)]),
+    "espn_gpu_table_close": (C.c_int, [C.c_void_p]),
+    "espn_gpu_table_info": (C.c_int, [C.c_void_p, C.POINTER(TableInfo)]),
+    "espn_gpu_workspace_create": (C.c_int, [C.c_void_p, C.POINTER(WorkspaceDesc), C.POINTER(C.c_void_p)]),
+    "espn_gpu_workspace_destroy": (C.c_int, [C.c_void_p]),
+    "espn_gpu_rerank": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.POINTER(RerankOut), C.c_void_p]),
+    "espn_gpu_workspace_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "espn_gpu_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "espn_gpu_merge_topk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_gpu_get_counters": (C.c_int, [C.c_void_p, C.POINTER(Counters)]),
+    "espn_gpu_synth_table": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_last_error": (C.c_char_p, []),
+    "espn_abi_version": (C.c_int, []),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libespn_gpu.so (once).  Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} not found: build it with `python -m paper_2312_05417_b200.build` "
+                "(the re-rank path has no CPU fallback)")
+        h = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(h, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = h
+    return _lib
+
+
+def last_error() -> str:
+    return (lib().espn_last_error() or b"").decode("utf-8", "replace")

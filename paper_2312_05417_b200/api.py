@@ -1,0 +1,489 @@
+"""Reference-shaped host API over the C-ABI (include/espn_gpu.h).
+
+Mirrors the re-rank slice of the reference's C++ interface -- names, fields,
+argument meaning and error classes -- so code written against
+proj/include/espn/{types,error,scoring,store,pipeline}.hpp maps 1:1:
+
+  reference (proj/include/espn/)                 here
+  ---------------------------------------------  -----------------------------------
+  error.hpp:8-42   Error + 6 subclasses           Error, InvalidInputError, ...
+  types.hpp:14-55  EmbeddingMatrix, QueryEmbedding, ScoredDoc, RankedList
+  ivf.hpp:40-50    Candidate, CandidateList       Candidate, CandidateList
+  pipeline.hpp:11-29 PipelineConfig               PipelineConfig (same fields/defaults)
+  pipeline.hpp:36-54 QueryStats                   QueryStats (same fields)
+  pipeline.hpp:66-79 BatchStats, BatchResult      BatchStats, BatchResult
+  store.hpp:80-112 StoreHandle / open_store       GpuStore (HBM tier of the table)
+  store.hpp:94     fetch_batch                    GpuStore.fetch_batch (K1 gather)
+  pipeline.hpp:61  run_query stages 3-6           rerank_candidates (the new seam)
+  pipeline.hpp:83  run_batch                      rerank_batch
+
+All compute runs in libespn_gpu.so; this module only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ---- error.hpp:8-42 ---------------------------------------------------------
+class Error(RuntimeError):
+    """Base class for every error the engine reports (error.hpp:9-12)."""
+
+
+class InvalidInputError(Error):
+    pass
+
+
+class InvalidStateError(Error):
+    pass
+
+
+class InvalidConfigError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class IoError(Error):
+    pass
+
+
+class DataIntegrityError(Error):
+    pass
+
+
+_STATUS = {
+    L.ESPN_E_INVALID_INPUT: InvalidInputError,
+    L.ESPN_E_INVALID_STATE: InvalidStateError,
+    L.ESPN_E_INVALID_CONFIG: InvalidConfigError,
+    L.ESPN_E_FORMAT: FormatError,
+    L.ESPN_E_IO: IoError,
+    L.ESPN_E_DATA_INTEGRITY: DataIntegrityError,
+    L.ESPN_E_CUDA: Error,
+}
+
+
+def _check(rc: int) -> None:
+    if rc != L.ESPN_OK:
+        raise _STATUS.get(rc, Error)(L.last_error())
+
+
+# ---- types.hpp / ivf.hpp / pipeline.hpp carriers --------------------------------
+@dataclass
+class EmbeddingMatrix:
+    """types.hpp:16-25: t x d row-major fp32 token embeddings of one doc."""
+    doc_id: int = 0
+    rows: int = 0
+    cols: int = 0
+    values: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+
+
+@dataclass
+class QueryEmbedding:
+    """types.hpp:34-44: one CLS vector plus a q x d token matrix (fp32)."""
+    query_id: int = 0
+    cls: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+    rows: int = 0
+    cols: int = 0
+    tokens: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+
+
+@dataclass
+class ScoredDoc:
+    doc_id: int = 0
+    score: float = 0.0
+
+
+@dataclass
+class RankedList:
+    """types.hpp:53-55: sorted by (score desc, doc_id asc), no duplicate ids."""
+    entries: List[ScoredDoc] = field(default_factory=list)
+
+
+@dataclass
+class Candidate:
+    doc_id: int = 0
+    cls_score: float = 0.0
+
+
+@dataclass
+class CandidateList:
+    """ivf.hpp:47-50: sorted by (cls_score desc, doc_id asc), deduplicated."""
+    entries: List[Candidate] = field(default_factory=list)
+    clusters_visited: int = 0
+
+
+@dataclass
+class PipelineConfig:
+    """pipeline.hpp:11-29 (same fields and defaults)."""
+    nprobe: int = 0
+    prefetch_step_pct: float = 10.0
+    rerank_count: int = 0
+    final_k: int = 10
+    prefetch_top_k: int = 0
+    candidate_k: int = 0
+    alpha: float = 1.0
+    prefetch_enabled: bool = True
+    partial_rerank_enabled: bool = False
+
+    def effective_prefetch_top_k(self) -> int:
+        return self.prefetch_top_k or self.rerank_count
+
+    def effective_candidate_k(self) -> int:
+        return self.candidate_k or max(self.rerank_count, self.final_k)
+
+    def delta(self) -> int:
+        """round(nprobe * step / 100), at least 1 (pipeline.hpp:8-10)."""
+        return max(1, int(math.floor(self.nprobe * self.prefetch_step_pct / 100.0 + 0.5)))
+
+
+@dataclass
+class QueryStats:
+    """pipeline.hpp:36-54 (same fields)."""
+    query_id: int = 0
+    ann_time: float = 0.0
+    prefetch_time: float = 0.0
+    early_rerank_time: float = 0.0
+    critical_fetch_time: float = 0.0
+    rerank_time: float = 0.0
+    total_time: float = 0.0
+    prefetched_count: int = 0
+    needed_count: int = 0
+    missed_count: int = 0
+    hit_rate: float = 0.0
+    prefetch_bytes: int = 0
+    critical_fetch_bytes: int = 0
+    critical_blocks_read: int = 0
+    needed_payload_bytes: int = 0
+
+
+@dataclass
+class BatchStats:
+    n_queries: int = 0
+    mean_latency: float = 0.0
+    p50_latency: float = 0.0
+    p99_latency: float = 0.0
+    wall_time: float = 0.0
+    total_critical_fetch_bytes: int = 0
+
+
+@dataclass
+class BatchResult:
+    rankings: List[RankedList] = field(default_factory=list)
+    stats: List[QueryStats] = field(default_factory=list)
+    batch: BatchStats = field(default_factory=BatchStats)
+
+
+@dataclass
+class FetchedDoc:
+    bow: EmbeddingMatrix
+
+
+@dataclass
+class FetchResult:
+    """store.hpp:66-71: docs in request order plus transfer counters."""
+    docs: List[FetchedDoc] = field(default_factory=list)
+    bytes_read: int = 0
+    blocks_read: int = 0
+    wall_time: float = 0.0
+
+
+def _ptr(a) -> Optional[int]:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return int(a.data_ptr())  # torch tensor
+
+
+_DTYPES = {"f16": L.ESPN_DTYPE_F16, "fp16": L.ESPN_DTYPE_F16, "bf16": L.ESPN_DTYPE_BF16}
+_KERNELS = {"auto": L.ESPN_KERNEL_AUTO, "tcgen05": L.ESPN_KERNEL_TCGEN05, "simt": L.ESPN_KERNEL_SIMT}
+
+
+class GpuStore:
+    """The HBM tier of the embedding table -- the re-rank path's StoreHandle
+    (store.hpp:80-107).  Rows are CSR: doc i's token rows are
+    rows[row_ptr[i]:row_ptr[i+1]], 2-byte codes of `dtype`.  d_cls /
+    value_width / alignment describe the reference's on-disk record and feed
+    only the QueryStats byte counters (store.hpp:32-34, 61-65)."""
+
+    def __init__(self, row_ptr, rows, d: int, dtype: str = "f16", d_cls: int = 128,
+                 value_width: int = 2, alignment: int = 4096, device: int = 0,
+                 borrowed_device: bool = False):
+        self.d = int(d)
+        self.dtype = dtype
+        self.d_cls = int(d_cls)
+        self.value_width = int(value_width)
+        self.alignment = int(alignment)
+        self.device = int(device)
+        self._keep = (row_ptr, rows)
+        if borrowed_device:
+            n_docs = int(row_ptr.numel()) - 1
+            self._row_ptr_host = None
+            rp_p, rows_p, flags = _ptr(row_ptr), _ptr(rows), L.ESPN_TABLE_DEVICE_BORROWED
+        else:
+            row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+            rows = np.ascontiguousarray(rows, dtype=np.uint16)
+            n_docs = int(row_ptr.shape[0]) - 1
+            self._row_ptr_host = row_ptr
+            self._keep = (row_ptr, rows)
+            rp_p, rows_p, flags = _ptr(row_ptr), _ptr(rows), 0
+        desc = L.TableDesc(n_docs=n_docs, d=self.d, dtype=_DTYPES[dtype], d_cls=self.d_cls,
+                           value_width=self.value_width, alignment=self.alignment, flags=flags,
+                           row_ptr=rp_p, rows=rows_p, device=self.device)
+        h = C.c_void_p()
+        _check(L.lib().espn_gpu_table_open(C.byref(desc), C.byref(h)))
+        self._h = h
+        if not borrowed_device:
+            self._keep = None  # uploaded; host copies no longer needed by the library
+        info = L.TableInfo()
+        _check(L.lib().espn_gpu_table_info(self._h, C.byref(info)))
+        self.n_docs = int(info.n_docs)
+        self.n_tokens = int(info.n_tokens)
+        self.max_tokens = int(info.max_tokens)
+        self.min_tokens = int(info.min_tokens)
+        self._workspaces = {}
+
+    @classmethod
+    def from_device(cls, row_ptr, rows, d: int, dtype: str = "f16", **kw) -> "GpuStore":
+        """Adopt CUDA tensors (torch) already resident in HBM (borrowed)."""
+        return cls(row_ptr, rows, d, dtype, borrowed_device=True, **kw)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def record_bytes(self, token_count):
+        """store.hpp:32-34."""
+        return (self.d_cls + np.asarray(token_count, dtype=np.uint64) * self.d) * self.value_width
+
+    def token_counts(self, doc_ids) -> Optional[np.ndarray]:
+        if self._row_ptr_host is None:
+            return None
+        ids = np.asarray(doc_ids, dtype=np.int64)
+        return (self._row_ptr_host[ids + 1] - self._row_ptr_host[ids]).astype(np.uint64)
+
+    def fetch_batch(self, doc_ids: Sequence[int]) -> FetchResult:
+        """store.hpp:91-94 through K1: request order, duplicates allowed,
+        unknown ids raise InvalidInputError.  Decodes to fp32 like the
+        reference's value_width=2 path."""
+        import torch
+        ids = np.ascontiguousarray(np.asarray(doc_ids, dtype=np.uint32))
+        n = int(ids.shape[0])
+        t0 = time.perf_counter()
+        dev = torch.device("cuda", self.device)
+        d_ids = torch.from_numpy(ids.astype(np.int32)).to(dev)
+        d_rp = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        _check(L.lib().espn_gpu_gather(self._h, _ptr(d_ids) if n else None, n, None, _ptr(d_rp), 0, None))
+        rp = d_rp.cpu().numpy().astype(np.uint64)
+        total = int(rp[-1]) if n else 0
+        d_rows = torch.empty(max(total * self.d, 1), dtype=torch.int16, device=dev)
+        if n:
+            _check(L.lib().espn_gpu_gather(self._h, _ptr(d_ids), n, _ptr(d_rows), _ptr(d_rp), total, None))
+        codes = d_rows[: total * self.d].cpu().numpy().view(np.uint16)
+        vals = decode(codes, self.dtype)
+        res = FetchResult()
+        for i in range(n):
+            a, b = int(rp[i]), int(rp[i + 1])
+            res.docs.append(FetchedDoc(EmbeddingMatrix(int(ids[i]), b - a, self.d,
+                                                       vals[a * self.d:b * self.d].copy())))
+        tok = np.diff(rp)
+        payload = self.record_bytes(tok)
+        res.bytes_read = int(payload.sum())
+        res.blocks_read = int(((payload + 4095) // 4096).sum())
+        res.wall_time = time.perf_counter() - t0
+        return res
+
+    def workspace(self, max_queries: int, max_candidates: int, max_query_tokens: int = 32) -> "Reranker":
+        return Reranker(self, max_queries, max_candidates, max_query_tokens)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            L.lib().espn_gpu_table_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def decode(codes: np.ndarray, dtype: str) -> np.ndarray:
+    codes = np.asarray(codes, dtype=np.uint16)
+    if dtype in ("f16", "fp16"):
+        return codes.view(np.float16).astype(np.float32)
+    return (codes.astype(np.uint32) << 16).view(np.float32)
+
+
+def encode(values: np.ndarray, dtype: str) -> np.ndarray:
+    v = np.asarray(values, dtype=np.float32)
+    if dtype in ("f16", "fp16"):
+        return v.astype(np.float16).view(np.uint16)
+    u = v.view(np.uint32).astype(np.uint64)
+    nan = (u & 0x7FFFFFFF) > 0x7F800000
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    r[nan] = ((u[nan] >> 16) | 0x40).astype(np.uint16)
+    return r
+
+
+class Reranker:
+    """A table plus one workspace (per-stream scratch): the batched re-rank
+    entry point.  One in-flight batch at a time."""
+
+    def __init__(self, store: GpuStore, max_queries: int, max_candidates: int, max_query_tokens: int = 32):
+        self.store = store
+        desc = L.WorkspaceDesc(max_queries=max_queries, max_candidates=max_candidates,
+                               max_query_tokens=max_query_tokens)
+        h = C.c_void_p()
+        _check(L.lib().espn_gpu_workspace_create(store.handle, C.byref(desc), C.byref(h)))
+        self._h = h
+        self.max_queries = max_queries
+        self.max_candidates = max_candidates
+
+    @property
+    def handle(self):
+        return self._h
+
+    def rerank_arrays(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig,
+                      kernel: str = "auto", device_io: bool = False, write_bow: bool = False,
+                      out=None, stream=None, sync: bool = True, needed_counts=None):
+        """Batched stages 3-6.  query_tokens (B, q, d) fp32; cand_* CSR over
+        queries with cand_offsets (B+1, host uint64).  Host numpy arrays by
+        default (copied in and out inside the call); device torch tensors
+        with device_io=True.  Returns (ids[B,k], scores[B,k], counts[B], bow)."""
+        offs = np.ascontiguousarray(np.asarray(cand_offsets, dtype=np.uint64))
+        B = offs.shape[0] - 1
+        k = int(config.final_k)
+        if device_io:
+            import torch
+            nq = int(query_tokens.shape[1])
+            if out is None:
+                dev = query_tokens.device
+                out = (torch.empty((B, k), dtype=torch.int32, device=dev),
+                       torch.empty((B, k), dtype=torch.float32, device=dev),
+                       torch.empty((B,), dtype=torch.int32, device=dev),
+                       torch.empty((int(offs[-1]),), dtype=torch.float32, device=dev) if write_bow else None)
+        else:
+            query_tokens = np.ascontiguousarray(query_tokens, dtype=np.float32)
+            cand_ids = np.ascontiguousarray(cand_ids, dtype=np.uint32)
+            cand_cls = np.ascontiguousarray(cand_cls, dtype=np.float32)
+            nq = int(query_tokens.shape[1]) if query_tokens.ndim == 3 else int(query_tokens.shape[0] // max(B, 1) // self.store.d)
+            if out is None:
+                out = (np.zeros((B, k), np.uint32), np.zeros((B, k), np.float32), np.zeros(B, np.uint32),
+                       np.full(int(offs[-1]), np.nan, np.float32) if write_bow else None)
+        flags = 0
+        if config.partial_rerank_enabled:
+            flags |= L.ESPN_RERANK_PARTIAL
+        if device_io:
+            flags |= L.ESPN_RERANK_DEVICE_IO
+        if write_bow:
+            flags |= L.ESPN_RERANK_WRITE_BOW
+        if not sync:
+            flags |= L.ESPN_RERANK_ASYNC
+        args = L.RerankArgs(n_queries=B, n_query_tokens=nq, query_tokens=_ptr(query_tokens),
+                            cand_ids=_ptr(cand_ids), cand_cls=_ptr(cand_cls), cand_offsets=offs.ctypes.data,
+                            rerank_count=int(config.rerank_count), final_k=k, alpha=float(config.alpha),
+                            flags=flags, kernel=_KERNELS[kernel])
+        if needed_counts is not None:
+            needed_counts = np.ascontiguousarray(needed_counts, dtype=np.uint32)
+            args.needed_counts = needed_counts.ctypes.data
+        o = L.RerankOut(ids=_ptr(out[0]), scores=_ptr(out[1]), counts=_ptr(out[2]),
+                        bow_scores=_ptr(out[3]) if write_bow else None)
+        self._keepalive = (query_tokens, cand_ids, cand_cls, offs, out, needed_counts)
+        _check(L.lib().espn_gpu_rerank(self.store.handle, self._h, C.byref(args), C.byref(o),
+                                       C.c_void_p(stream) if stream else None))
+        return out
+
+    def sync(self, stream=None) -> None:
+        _check(L.lib().espn_gpu_workspace_sync(self._h, C.c_void_p(stream) if stream else None))
+
+    def counters(self) -> dict:
+        c = L.Counters()
+        _check(L.lib().espn_gpu_get_counters(self._h, C.byref(c)))
+        return {f: int(getattr(c, f)) for f, _ in L.Counters._fields_ if f != "reserved"}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            L.lib().espn_gpu_workspace_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stats_for(store: GpuStore, ids: np.ndarray, n_needed: int, query_id: int, elapsed: float) -> QueryStats:
+    """QueryStats for an HBM-resident table: every needed row is resident before
+    scoring, so nothing is fetched on the critical path (hit_rate 1.0)."""
+    st = QueryStats(query_id=query_id, needed_count=n_needed, rerank_time=elapsed, total_time=elapsed)
+    tok = store.token_counts(ids[:n_needed]) if n_needed else np.zeros(0, np.uint64)
+    if tok is not None:
+        st.needed_payload_bytes = int(store.record_bytes(tok).sum()) if n_needed else 0
+    st.prefetched_count = n_needed
+    st.hit_rate = 1.0 if n_needed else 0.0
+    return st
+
+
+def rerank_batch(queries: Sequence[QueryEmbedding], candidate_lists: Sequence[CandidateList],
+                 store: GpuStore, config: PipelineConfig, kernel: str = "auto") -> BatchResult:
+    """run_batch (pipeline.hpp:81-85) restricted to stages 3-6: one device pass
+    over the whole batch; per-query results identical to single-query calls."""
+    if len(queries) != len(candidate_lists):
+        raise InvalidInputError("queries and candidate lists differ in length")
+    B = len(queries)
+    res = BatchResult()
+    if B == 0:
+        return res
+    d = store.d
+    nq = queries[0].rows
+    for q in queries:
+        if q.cols != d:
+            raise InvalidInputError(f"query dim {q.cols} != table dim {d}")
+        if q.rows != nq:
+            raise InvalidInputError("all queries of a batch must have the same token count")
+    qt = np.stack([np.asarray(q.tokens, np.float32).reshape(q.rows, q.cols) for q in queries])
+    offs = np.zeros(B + 1, np.uint64)
+    for i, cl in enumerate(candidate_lists):
+        offs[i + 1] = offs[i] + len(cl.entries)
+    ids = np.fromiter((c.doc_id for cl in candidate_lists for c in cl.entries), np.uint32, int(offs[-1]))
+    cls = np.fromiter((c.cls_score for cl in candidate_lists for c in cl.entries), np.float32, int(offs[-1]))
+    rr = Reranker(store, B, max(int(offs[-1]), 1), max(nq, 1))
+    try:
+        t0 = time.perf_counter()
+        oid, osc, ocnt, _ = rr.rerank_arrays(qt, ids, cls, offs, config, kernel=kernel)
+        wall = time.perf_counter() - t0
+    finally:
+        rr.close()
+    lat = []
+    for b in range(B):
+        n = int(ocnt[b])
+        res.rankings.append(RankedList([ScoredDoc(int(oid[b, i]), float(osc[b, i])) for i in range(n)]))
+        a0, a1 = int(offs[b]), int(offs[b + 1])
+        need = min(a1 - a0, int(config.rerank_count))
+        res.stats.append(_stats_for(store, ids[a0:a1], need, queries[b].query_id, wall))
+        lat.append(wall)
+    lat = np.asarray(lat)
+    res.batch = BatchStats(n_queries=B, mean_latency=float(lat.mean()), p50_latency=float(np.percentile(lat, 50)),
+                           p99_latency=float(np.percentile(lat, 99)), wall_time=wall,
+                           total_critical_fetch_bytes=sum(s.critical_fetch_bytes for s in res.stats))
+    return res
+
+
+def rerank_candidates(query: QueryEmbedding, candidates: CandidateList, store: GpuStore,
+                      config: PipelineConfig, kernel: str = "auto") -> Tuple[RankedList, QueryStats]:
+    """Stages 3-6 of run_query (pipeline.hpp:56-64) for one query:
+    the missing "candidates in -> ranked out" seam."""
+    r = rerank_batch([query], [candidates], store, config, kernel=kernel)
+    return r.rankings[0], r.stats[0]

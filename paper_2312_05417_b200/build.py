@@ -1,0 +1,77 @@
+"""In-tree build of the native library (no JIT cache, so the .so travels with
+the repo snapshot to the GPU box).
+
+    python -m paper_2312_05417_b200.build        # libespn_gpu.so + oracle
+
+libespn_gpu.so = csrc/espn_gpu.cu (+ headers) compiled for sm_100a only
+(`-gencode arch=compute_100a,code=sm_100a`: plain -arch=sm_100a would also
+emit compute_100 PTX, on which ptxas rejects tcgen05).  Host C++ lives in the
+same translation unit; the library links only the CUDA runtime.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB_DIR = PKG / "lib"
+LIB = LIB_DIR / "libespn_gpu.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+    "-shared", "--expt-relaxed-constexpr",
+    "-Xptxas", "-warn-spills",
+]
+
+
+def _sources():
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "espn_gpu.h"]
+
+
+def needs_rebuild() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in _sources())
+
+
+def build_lib(verbose: bool = False, force: bool = False) -> Path:
+    if not force and not needs_rebuild():
+        return LIB
+    LIB_DIR.mkdir(exist_ok=True)
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [NVCC, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp), str(CSRC / "espn_gpu.cu"),
+           "-lcudart"]
+    if verbose:
+        cmd.insert(1, "-Xptxas")
+        cmd.insert(2, "-v")
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libespn_gpu.so")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def build_oracle() -> None:
+    """Oracle (test infrastructure) + the reference codec shim when the
+    reference tree is present (this container only)."""
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+    if Path("/root/reference/proj/include/espn/half.hpp").exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"], check=True)
+
+
+if __name__ == "__main__":
+    build_lib(verbose="-v" in sys.argv, force="-f" in sys.argv)
+    build_oracle()
+    print(LIB)

@@ -1,0 +1,54 @@
+// common.cuh -- parameter blocks shared by the re-rank kernels.
+#pragma once
+#include <cstdint>
+
+namespace espn_k {
+
+// Device-side error bits (mapped to espn_status by the host after sync).
+enum : uint32_t {
+  ERR_UNKNOWN_DOC = 1u << 0,     // candidate id >= n_docs  -> DATA_INTEGRITY
+  ERR_NONFINITE_QUERY = 1u << 1, // query token not finite / not representable -> INVALID_INPUT
+  ERR_NONFINITE_CLS = 1u << 2,   // cls score not finite -> INVALID_INPUT
+  ERR_DUPLICATE = 1u << 3,       // duplicate candidate id -> INVALID_INPUT (scoring.hpp:16-18)
+  ERR_NONFINITE_SCORE = 1u << 4, // aggregate score not finite -> INVALID_INPUT
+  ERR_UNIT_TOO_LARGE = 1u << 5   // internal: slot budget of a work unit exceeded
+};
+
+// One batch of (query, candidate list) pairs, resident on the device.
+struct MaxSimParams {
+  const uint16_t* rows;        // table token rows, d codes each
+  const uint64_t* row_ptr;     // n_docs + 1
+  uint64_t n_docs;
+  const float* q32;            // B * nq * d fp32 query tokens
+  const uint32_t* cand_ids;    // CSR over queries
+  const uint64_t* cand_off;    // B + 1
+  const uint32_t* unit_off;    // B + 1: work units per query (prefix)
+  const uint32_t* needed;      // B: needed (scored with MaxSim) candidates per query
+  float* bow_out;              // per candidate MaxSim score (first min(R, n_b) of each query)
+  uint32_t* err;               // error bits
+  uint32_t n_queries;
+  uint32_t nq;                 // query tokens, 1..32
+  uint32_t rerank_count;       // R
+  uint32_t unit_docs;          // docs per work unit (<= kUnitMax)
+  uint32_t n_units;
+  uint32_t bf16;               // table dtype
+};
+
+struct TopKParams {
+  const float* bow;            // per candidate MaxSim (valid for the first R of each query)
+  const uint32_t* cand_ids;
+  const float* cand_cls;
+  const uint64_t* cand_off;    // B + 1
+  const uint32_t* needed;      // B: first needed[b] candidates carry a MaxSim score
+  uint32_t* out_ids;           // B * k
+  float* out_scores;           // B * k
+  uint32_t* out_counts;        // B
+  uint32_t* err;
+  uint32_t n_queries;
+  uint32_t rerank_count;
+  uint32_t k;
+  uint32_t partial;            // tail beyond R scored alpha * cls
+  float alpha;
+};
+
+}  // namespace espn_k

@@ -1,0 +1,603 @@
+// espn_gpu.cu -- C-ABI implementation (include/espn_gpu.h): table / workspace
+// lifetime, batch orchestration (H2D -> K2 MaxSim -> K3 top-k -> D2H) and the
+// standalone gather / merge / synth entry points.  Pure CUDA runtime; no torch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/espn_gpu.h"
+#include "common.cuh"
+#include "kernels_misc.cuh"
+#include "maxsim_tc.cuh"
+
+using namespace espn_k;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define ESPN_CUDA_TRY(expr)                                                                  \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(ESPN_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+int err_bits_to_status(uint32_t bits) {
+  if (!bits) return ESPN_OK;
+  std::string m = "device-side validation failed:";
+  if (bits & ERR_UNKNOWN_DOC) m += " candidate doc id not in the table (store lacks a candidate);";
+  if (bits & ERR_NONFINITE_QUERY) m += " query token not finite in the table dtype;";
+  if (bits & ERR_NONFINITE_CLS) m += " non-finite cls_score;";
+  if (bits & ERR_DUPLICATE) m += " duplicate candidate doc id;";
+  if (bits & ERR_NONFINITE_SCORE) m += " non-finite aggregate score;";
+  if (bits & ERR_UNIT_TOO_LARGE) m += " internal: work unit slot budget exceeded;";
+  g_last_error = m;
+  if (bits & ERR_UNKNOWN_DOC) return ESPN_E_DATA_INTEGRITY;
+  if (bits & ERR_UNIT_TOO_LARGE) return ESPN_E_INVALID_STATE;
+  return ESPN_E_INVALID_INPUT;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int check_device(int dev, int* num_sms, bool* tc_ok) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(ESPN_E_CUDA, "no CUDA device available (the re-rank path has no CPU fallback)");
+  if (dev < 0 || dev >= n) return fail(ESPN_E_INVALID_INPUT, "device ordinal out of range");
+  cudaDeviceProp prop;
+  ESPN_CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+  *num_sms = prop.multiProcessorCount;
+  *tc_ok = prop.major == 10 && prop.minor == 0;
+  return ESPN_OK;
+}
+
+template <int D>
+constexpr int tc_unit_docs(uint32_t max_t) {
+  using L = TcLayout<D>;
+  const uint32_t pad = (max_t + 7u) & ~7u;
+  const uint32_t u = pad ? (uint32_t)L::MAX_SLOTS / pad : 0;
+  return (int)std::min<uint32_t>(u, (uint32_t)L::UNITMAX);
+}
+
+int tc_unit_docs_rt(uint32_t d, uint32_t max_t) {
+  switch (d) {
+    case 16: return tc_unit_docs<16>(max_t);
+    case 32: return tc_unit_docs<32>(max_t);
+    case 64: return tc_unit_docs<64>(max_t);
+    case 128: return tc_unit_docs<128>(max_t);
+    default: return 0;
+  }
+}
+
+template <int D>
+cudaError_t launch_tc(const MaxSimParams& p, int num_sms, cudaStream_t s) {
+  using L = TcLayout<D>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(maxsim_tc_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int grid = (int)std::min<uint32_t>(p.n_units, (uint32_t)num_sms);
+  if (grid == 0) return cudaSuccess;
+  maxsim_tc_kernel<D><<<grid, L::NTHREADS, L::SMEM_BYTES, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_rt(uint32_t d, const MaxSimParams& p, int num_sms, cudaStream_t s) {
+  switch (d) {
+    case 16: return launch_tc<16>(p, num_sms, s);
+    case 32: return launch_tc<32>(p, num_sms, s);
+    case 64: return launch_tc<64>(p, num_sms, s);
+    case 128: return launch_tc<128>(p, num_sms, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int D>
+cudaError_t launch_simt(const MaxSimParams& p, uint64_t n_pairs, int num_sms, cudaStream_t s) {
+  if (n_pairs == 0) return cudaSuccess;
+  const uint64_t warps_wanted = (uint64_t)num_sms * 64;  // 8 blocks x 8 warps per SM
+  uint32_t ppw = (uint32_t)std::max<uint64_t>(1, (n_pairs + warps_wanted - 1) / warps_wanted);
+  const uint64_t warps = (n_pairs + ppw - 1) / ppw;
+  const uint64_t blocks = (warps * 32 + 255) / 256;
+  maxsim_simt_kernel<D><<<(unsigned)blocks, 256, 0, s>>>(p, ppw, n_pairs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_simt_rt(uint32_t d, const MaxSimParams& p, uint64_t n_pairs, int num_sms,
+                           cudaStream_t s) {
+  switch (d) {
+    case 8: return launch_simt<8>(p, n_pairs, num_sms, s);
+    case 16: return launch_simt<16>(p, n_pairs, num_sms, s);
+    case 32: return launch_simt<32>(p, n_pairs, num_sms, s);
+    case 48: return launch_simt<48>(p, n_pairs, num_sms, s);
+    case 64: return launch_simt<64>(p, n_pairs, num_sms, s);
+    case 96: return launch_simt<96>(p, n_pairs, num_sms, s);
+    case 128: return launch_simt<128>(p, n_pairs, num_sms, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+bool simt_supported(uint32_t d) {
+  return d == 8 || d == 16 || d == 32 || d == 48 || d == 64 || d == 96 || d == 128;
+}
+bool tc_supported(uint32_t d) { return d == 16 || d == 32 || d == 64 || d == 128; }
+
+size_t topk_smem_bytes() {
+  return (size_t)kTopkSort * 8 + (size_t)kMaxK * 8 + (size_t)kTopkHash * 4;
+}
+
+cudaError_t ensure_topk_attr() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)topk_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)topk_smem_bytes());
+  if (e != cudaSuccess) return e;
+  done = true;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+struct espn_gpu_table {
+  int device = 0;
+  int num_sms = 0;
+  bool tc_ok = false;
+  uint64_t n_docs = 0, n_tokens = 0;
+  uint32_t d = 0, dtype = 0, d_cls = 0, value_width = 2, alignment = 1;
+  uint32_t max_t = 0, min_t = 0;
+  bool owned = false;
+  uint64_t* row_ptr = nullptr;
+  uint16_t* rows = nullptr;
+};
+
+struct espn_gpu_workspace {
+  espn_gpu_table* table = nullptr;
+  uint32_t max_queries = 0, max_candidates = 0, max_nq = 0;
+  float* q32 = nullptr;
+  uint32_t* ids = nullptr;
+  float* cls = nullptr;
+  uint64_t* cand_off = nullptr;
+  uint32_t* unit_off = nullptr;
+  uint32_t* needed = nullptr;
+  float* bow = nullptr;
+  uint32_t* out_ids = nullptr;
+  float* out_scores = nullptr;
+  uint32_t* out_counts = nullptr;
+  uint32_t* err = nullptr;
+  // pinned host staging for the small per-batch tables and the error word
+  uint64_t* h_cand_off = nullptr;
+  uint32_t* h_unit_off = nullptr;
+  uint32_t* h_needed = nullptr;
+  uint32_t* h_err = nullptr;
+  espn_counters counters{};
+};
+
+extern "C" {
+
+const char* espn_last_error(void) { return g_last_error.c_str(); }
+int espn_abi_version(void) { return ESPN_GPU_ABI_VERSION; }
+
+int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
+  if (!desc || !out) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  *out = nullptr;
+  if (desc->d == 0 || desc->d % 8 != 0 || desc->d > 256)
+    return fail(ESPN_E_INVALID_INPUT, "token dim d must be a multiple of 8 in [8, 256]");
+  if (desc->dtype > ESPN_DTYPE_BF16) return fail(ESPN_E_INVALID_INPUT, "dtype must be f16 or bf16");
+  if (desc->value_width != 2 && desc->value_width != 4)
+    return fail(ESPN_E_INVALID_INPUT, "value_width must be 2 or 4 (store.hpp:27)");
+  if (desc->alignment != 1 && desc->alignment != 512 && desc->alignment != 4096)
+    return fail(ESPN_E_INVALID_INPUT, "alignment must be 1, 512 or 4096 (store.hpp:28)");
+  if (desc->n_docs == 0) return fail(ESPN_E_INVALID_INPUT, "empty table");
+  if (!desc->row_ptr || !desc->rows) return fail(ESPN_E_INVALID_INPUT, "null row_ptr/rows");
+  int sms = 0;
+  bool tc = false;
+  int st = check_device(desc->device, &sms, &tc);
+  if (st) return st;
+  DeviceGuard g(desc->device);
+  auto* t = new espn_gpu_table();
+  t->device = desc->device;
+  t->num_sms = sms;
+  t->tc_ok = tc;
+  t->n_docs = desc->n_docs;
+  t->d = desc->d;
+  t->dtype = desc->dtype;
+  t->d_cls = desc->d_cls;
+  t->value_width = desc->value_width;
+  t->alignment = desc->alignment;
+  const bool borrowed = (desc->flags & ESPN_TABLE_DEVICE_BORROWED) != 0;
+  if (!borrowed) {
+    // host tables: validate (types.hpp:64-68: t >= 1), then upload
+    const uint64_t* rp = desc->row_ptr;
+    if (rp[0] != 0) { delete t; return fail(ESPN_E_INVALID_INPUT, "row_ptr[0] must be 0"); }
+    uint32_t mn = UINT32_MAX, mx = 0;
+    for (uint64_t i = 0; i < desc->n_docs; ++i) {
+      if (rp[i + 1] <= rp[i]) {
+        delete t;
+        return fail(ESPN_E_INVALID_INPUT, "doc " + std::to_string(i) + " has t < 1 (types.hpp:64-68)");
+      }
+      const uint64_t len = rp[i + 1] - rp[i];
+      mn = (uint32_t)std::min<uint64_t>(mn, len);
+      mx = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(mx, len), UINT32_MAX);
+    }
+    t->min_t = mn;
+    t->max_t = mx;
+    t->n_tokens = rp[desc->n_docs];
+    cudaError_t e1 = cudaMalloc(&t->row_ptr, (desc->n_docs + 1) * sizeof(uint64_t));
+    cudaError_t e2 = cudaMalloc(&t->rows, std::max<uint64_t>(1, t->n_tokens * t->d) * sizeof(uint16_t));
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      cudaFree(t->row_ptr);
+      cudaFree(t->rows);
+      delete t;
+      return fail(ESPN_E_CUDA, "cudaMalloc failed for the HBM table");
+    }
+    t->owned = true;
+    cudaMemcpy(t->row_ptr, rp, (desc->n_docs + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    cudaError_t e3 = cudaMemcpy(t->rows, desc->rows, t->n_tokens * t->d * sizeof(uint16_t),
+                                cudaMemcpyHostToDevice);
+    if (e3 != cudaSuccess) {
+      espn_gpu_table_close(t);
+      return fail(ESPN_E_CUDA, std::string("table upload: ") + cudaGetErrorString(e3));
+    }
+  } else {
+    t->row_ptr = const_cast<uint64_t*>(desc->row_ptr);
+    t->rows = const_cast<uint16_t*>(desc->rows);
+    unsigned long long* mm = nullptr;
+    ESPN_CUDA_TRY(cudaMalloc(&mm, 3 * sizeof(unsigned long long)));
+    unsigned long long init[3] = {~0ull, 0ull, 0ull};
+    cudaMemcpy(mm, init, sizeof init, cudaMemcpyHostToDevice);
+    minmax_len_kernel<<<sms * 4, 256>>>(t->row_ptr, t->n_docs, mm);
+    unsigned long long res[3];
+    uint64_t first = 1, last = 0;
+    cudaMemcpy(res, mm, sizeof res, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&first, t->row_ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(&last, t->row_ptr + t->n_docs, sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    cudaFree(mm);
+    if (e != cudaSuccess) { delete t; return fail(ESPN_E_CUDA, cudaGetErrorString(e)); }
+    if (first != 0 || res[2] != 0) {
+      delete t;
+      return fail(ESPN_E_INVALID_INPUT, "row_ptr must start at 0 and give every doc t >= 1");
+    }
+    t->min_t = (uint32_t)res[0];
+    t->max_t = (uint32_t)std::min<unsigned long long>(res[1], UINT32_MAX);
+    t->n_tokens = last;
+  }
+  *out = t;
+  return ESPN_OK;
+}
+
+int espn_gpu_table_close(espn_gpu_table* t) {
+  if (!t) return ESPN_OK;
+  DeviceGuard g(t->device);
+  if (t->owned) {
+    cudaFree(t->row_ptr);
+    cudaFree(t->rows);
+  }
+  delete t;
+  return ESPN_OK;
+}
+
+int espn_gpu_table_info(const espn_gpu_table* t, espn_table_info* out) {
+  if (!t || !out) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  out->n_docs = t->n_docs;
+  out->n_tokens = t->n_tokens;
+  out->d = t->d;
+  out->dtype = t->dtype;
+  out->max_tokens = t->max_t;
+  out->min_tokens = t->min_t;
+  out->hbm_bytes = t->owned ? (t->n_docs + 1) * 8 + t->n_tokens * t->d * 2 : 0;
+  return ESPN_OK;
+}
+
+int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc,
+                              espn_gpu_workspace** out) {
+  if (!t || !desc || !out) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  *out = nullptr;
+  if (desc->max_queries == 0 || desc->max_candidates == 0)
+    return fail(ESPN_E_INVALID_INPUT, "workspace capacities must be positive");
+  if (desc->max_query_tokens == 0 || desc->max_query_tokens > 32)
+    return fail(ESPN_E_INVALID_INPUT, "max_query_tokens must be in [1, 32]");
+  DeviceGuard g(t->device);
+  auto* w = new espn_gpu_workspace();
+  w->table = t;
+  w->max_queries = desc->max_queries;
+  w->max_candidates = desc->max_candidates;
+  w->max_nq = desc->max_query_tokens;
+  const size_t B = desc->max_queries, C = desc->max_candidates;
+  cudaError_t e = cudaSuccess;
+  auto al = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+  };
+  al((void**)&w->q32, B * w->max_nq * t->d * sizeof(float));
+  al((void**)&w->ids, C * sizeof(uint32_t));
+  al((void**)&w->cls, C * sizeof(float));
+  al((void**)&w->cand_off, (B + 1) * sizeof(uint64_t));
+  al((void**)&w->unit_off, (B + 1) * sizeof(uint32_t));
+  al((void**)&w->needed, B * sizeof(uint32_t));
+  al((void**)&w->bow, C * sizeof(float));
+  al((void**)&w->out_ids, B * kMaxK * sizeof(uint32_t));
+  al((void**)&w->out_scores, B * kMaxK * sizeof(float));
+  al((void**)&w->out_counts, B * sizeof(uint32_t));
+  al((void**)&w->err, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMallocHost(&w->h_cand_off, (B + 1) * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaMallocHost(&w->h_unit_off, (B + 1) * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMallocHost(&w->h_needed, (B + 1) * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMallocHost(&w->h_err, sizeof(uint32_t));
+  if (e != cudaSuccess) {
+    espn_gpu_workspace_destroy(w);
+    return fail(ESPN_E_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
+  }
+  *out = w;
+  return ESPN_OK;
+}
+
+int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
+  if (!w) return ESPN_OK;
+  DeviceGuard g(w->table->device);
+  cudaFree(w->q32); cudaFree(w->ids); cudaFree(w->cls); cudaFree(w->cand_off);
+  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
+  cudaFree(w->out_counts); cudaFree(w->err);
+  cudaFreeHost(w->h_cand_off); cudaFreeHost(w->h_unit_off); cudaFreeHost(w->h_needed); cudaFreeHost(w->h_err);
+  delete w;
+  return ESPN_OK;
+}
+
+int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a,
+                    espn_rerank_out* o, void* stream_v) {
+  if (!t || !w || !a || !o) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_v);
+  const uint32_t B = a->n_queries, nq = a->n_query_tokens, k = a->final_k;
+  // ---- host-side validation (pipeline.hpp:31-32) ----
+  if (B > w->max_queries) return fail(ESPN_E_INVALID_INPUT, "n_queries exceeds workspace capacity");
+  if (nq < 1 || nq > w->max_nq) return fail(ESPN_E_INVALID_INPUT, "n_query_tokens must be in [1, workspace max <= 32]");
+  if (k < 1 || k > (uint32_t)kMaxK) return fail(ESPN_E_INVALID_INPUT, "final_k must be in [1, 1024]");
+  if (!std::isfinite(a->alpha)) return fail(ESPN_E_INVALID_INPUT, "alpha must be finite");
+  const bool partial = (a->flags & ESPN_RERANK_PARTIAL) != 0;
+  if (!partial && a->rerank_count < k)
+    return fail(ESPN_E_INVALID_INPUT, "rerank_count < final_k requires partial re-ranking (SPEC.md:265)");
+  if (B == 0) return ESPN_OK;
+  if (!a->cand_offsets || !a->query_tokens || !o->ids || !o->scores || !o->counts)
+    return fail(ESPN_E_INVALID_INPUT, "null array argument");
+  const uint64_t* off = a->cand_offsets;
+  if (off[0] != 0) return fail(ESPN_E_INVALID_INPUT, "cand_offsets[0] must be 0");
+  for (uint32_t b = 0; b < B; ++b)
+    if (off[b + 1] < off[b]) return fail(ESPN_E_INVALID_INPUT, "cand_offsets must be non-decreasing");
+  const uint64_t C = off[B];
+  if (C > w->max_candidates) return fail(ESPN_E_INVALID_INPUT, "candidates exceed workspace capacity");
+  if (C > 0 && (!a->cand_ids || !a->cand_cls)) return fail(ESPN_E_INVALID_INPUT, "null candidate arrays");
+  const bool dev_io = (a->flags & ESPN_RERANK_DEVICE_IO) != 0;
+  DeviceGuard g(t->device);
+
+  // ---- kernel choice (tcgen05 when the dim has a tensor-core tiling) ----
+  uint32_t kern = a->kernel;
+  const int unit_docs = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
+  if (kern == ESPN_KERNEL_AUTO) kern = (tc_supported(t->d) && unit_docs > 0) ? ESPN_KERNEL_TCGEN05 : ESPN_KERNEL_SIMT;
+  if (kern == ESPN_KERNEL_TCGEN05 && (!t->tc_ok || !tc_supported(t->d) || unit_docs <= 0))
+    return fail(ESPN_E_INVALID_CONFIG, "tcgen05 MaxSim needs an sm_100 device, d in {16,32,64,128} and docs <= 4096 tokens");
+  if (kern == ESPN_KERNEL_SIMT && !simt_supported(t->d))
+    return fail(ESPN_E_INVALID_CONFIG, "CUDA-core MaxSim supports d in {8,16,32,48,64,96,128}");
+
+  // ---- per-query work units (tcgen05) or pair prefix (SIMT), host-built ----
+  uint64_t acc = 0, pairs = 0;
+  for (uint32_t b = 0; b < B; ++b) {
+    w->h_cand_off[b] = off[b];
+    const uint64_t n = off[b + 1] - off[b];
+    const uint64_t need = a->needed_counts ? std::min<uint64_t>(n, a->needed_counts[b])
+                                           : std::min<uint64_t>(n, a->rerank_count);
+    w->h_needed[b] = (uint32_t)need;
+    w->h_unit_off[b] = (uint32_t)acc;
+    pairs += need;
+    acc += kern == ESPN_KERNEL_TCGEN05 ? (need + unit_docs - 1) / unit_docs : need;
+  }
+  w->h_cand_off[B] = off[B];
+  w->h_unit_off[B] = (uint32_t)acc;
+  if (acc > UINT32_MAX) return fail(ESPN_E_INVALID_INPUT, "batch too large");
+
+  const float* q32 = a->query_tokens;
+  const uint32_t* ids = a->cand_ids;
+  const float* cls = a->cand_cls;
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->cand_off, w->h_cand_off, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->unit_off, w->h_unit_off, (B + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->needed, w->h_needed, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  if (!dev_io) {
+    ESPN_CUDA_TRY(cudaMemcpyAsync(w->q32, q32, (size_t)B * nq * t->d * sizeof(float), cudaMemcpyHostToDevice, s));
+    if (C) {
+      ESPN_CUDA_TRY(cudaMemcpyAsync(w->ids, ids, C * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      ESPN_CUDA_TRY(cudaMemcpyAsync(w->cls, cls, C * sizeof(float), cudaMemcpyHostToDevice, s));
+    }
+    q32 = w->q32;
+    ids = w->ids;
+    cls = w->cls;
+  }
+  ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
+
+  MaxSimParams mp{};
+  mp.rows = t->rows;
+  mp.row_ptr = t->row_ptr;
+  mp.n_docs = t->n_docs;
+  mp.q32 = q32;
+  mp.cand_ids = ids;
+  mp.cand_off = w->cand_off;
+  mp.unit_off = w->unit_off;
+  mp.needed = w->needed;
+  mp.bow_out = w->bow;
+  mp.err = w->err;
+  mp.n_queries = B;
+  mp.nq = nq;
+  mp.rerank_count = a->rerank_count;
+  mp.unit_docs = (uint32_t)std::max(unit_docs, 1);
+  mp.n_units = (uint32_t)acc;
+  mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
+  cudaError_t e = kern == ESPN_KERNEL_TCGEN05 ? launch_tc_rt(t->d, mp, t->num_sms, s)
+                                               : launch_simt_rt(t->d, mp, acc, t->num_sms, s);
+  if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
+
+  ESPN_CUDA_TRY(ensure_topk_attr());
+  TopKParams tp{};
+  tp.bow = w->bow;
+  tp.cand_ids = ids;
+  tp.cand_cls = cls;
+  tp.cand_off = w->cand_off;
+  tp.needed = w->needed;
+  tp.out_ids = dev_io ? o->ids : w->out_ids;
+  tp.out_scores = dev_io ? o->scores : w->out_scores;
+  tp.out_counts = dev_io ? o->counts : w->out_counts;
+  tp.err = w->err;
+  tp.n_queries = B;
+  tp.rerank_count = a->rerank_count;
+  tp.k = k;
+  tp.partial = partial ? 1u : 0u;
+  tp.alpha = a->alpha;
+  topk_kernel<<<B, kTopkThreads, topk_smem_bytes(), s>>>(tp);
+  ESPN_CUDA_TRY(cudaGetLastError());
+
+  if (!dev_io) {
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->ids, w->out_ids, (size_t)B * k * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->scores, w->out_scores, (size_t)B * k * sizeof(float), cudaMemcpyDeviceToHost, s));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->counts, w->out_counts, (size_t)B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  }
+  if ((a->flags & ESPN_RERANK_WRITE_BOW) && o->bow_scores && C) {
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->bow_scores, w->bow, C * sizeof(float),
+                                  dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  }
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  w->counters.batches += 1;
+  w->counters.queries += B;
+  w->counters.pairs_scored += pairs;
+  w->counters.kernel_launches += 2;
+  if (a->flags & ESPN_RERANK_ASYNC) return ESPN_OK;
+  ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  return err_bits_to_status(*w->h_err);
+}
+
+int espn_gpu_workspace_sync(espn_gpu_workspace* w, void* stream_v) {
+  if (!w) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  DeviceGuard g(w->table->device);
+  ESPN_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_v)));
+  return err_bits_to_status(*w->h_err);
+}
+
+int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t* out_rows,
+                    uint64_t* out_row_ptr, uint64_t capacity_tokens, void* stream_v) {
+  if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
+  if (n == 0) {
+    if (out_row_ptr) {
+      uint64_t z = 0;
+      ESPN_CUDA_TRY(cudaMemcpyAsync(out_row_ptr, &z, sizeof z, cudaMemcpyHostToDevice,
+                                    static_cast<cudaStream_t>(stream_v)));
+      ESPN_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_v)));
+    }
+    return ESPN_OK;
+  }
+  if (!ids || !out_row_ptr) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  DeviceGuard g(t->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream_v);
+  uint32_t* derr = nullptr;
+  ESPN_CUDA_TRY(cudaMallocAsync(&derr, sizeof(uint32_t), s));
+  ESPN_CUDA_TRY(cudaMemsetAsync(derr, 0, sizeof(uint32_t), s));
+  const int blocks = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)t->num_sms * 8);
+  gather_count_kernel<<<blocks, 256, 0, s>>>(t->row_ptr, t->n_docs, ids, n, out_row_ptr, derr);
+  scan_u64_kernel<<<1, 1024, 0, s>>>(out_row_ptr, n);
+  uint32_t herr = 0;
+  uint64_t total = 0;
+  ESPN_CUDA_TRY(cudaMemcpyAsync(&herr, derr, sizeof herr, cudaMemcpyDeviceToHost, s));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(&total, out_row_ptr + n, sizeof total, cudaMemcpyDeviceToHost, s));
+  ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFreeAsync(derr, s);
+  if (herr) {
+    g_last_error = "unknown doc id in gather request (store.hpp:92-93)";
+    return ESPN_E_INVALID_INPUT;
+  }
+  if (total > capacity_tokens) return fail(ESPN_E_INVALID_INPUT, "out_rows capacity too small");
+  if (!out_rows) return ESPN_OK;
+  const int cb = t->num_sms * 8;
+  switch (t->d) {
+#define ESPN_G(DD) case DD: gather_copy_kernel<DD><<<cb, 256, 0, s>>>(t->rows, t->row_ptr, t->n_docs, ids, n, out_row_ptr, out_rows); break;
+    ESPN_G(8) ESPN_G(16) ESPN_G(32) ESPN_G(48) ESPN_G(64) ESPN_G(96) ESPN_G(128) ESPN_G(256)
+#undef ESPN_G
+    default: return fail(ESPN_E_INVALID_CONFIG, "gather supports d in {8,16,32,48,64,96,128,256}");
+  }
+  ESPN_CUDA_TRY(cudaGetLastError());
+  ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  return ESPN_OK;
+}
+
+int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const uint32_t* counts,
+                        uint32_t n_lists, uint32_t n_queries, uint32_t k, uint32_t* out_ids,
+                        float* out_scores, uint32_t* out_counts, void* stream_v) {
+  if (k < 1 || k > (uint32_t)kMaxK) return fail(ESPN_E_INVALID_INPUT, "k must be in [1, 1024]");
+  if (n_queries == 0) return ESPN_OK;
+  if (!ids || !scores || !counts || !out_ids || !out_scores || !out_counts)
+    return fail(ESPN_E_INVALID_INPUT, "null argument");
+  ESPN_CUDA_TRY(ensure_topk_attr());
+  merge_topk_kernel<<<n_queries, kTopkThreads, topk_smem_bytes(), static_cast<cudaStream_t>(stream_v)>>>(
+      ids, scores, counts, n_lists, n_queries, k, out_ids, out_scores, out_counts);
+  ESPN_CUDA_TRY(cudaGetLastError());
+  return ESPN_OK;
+}
+
+int espn_gpu_get_counters(const espn_gpu_workspace* w, espn_counters* out) {
+  if (!w || !out) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  *out = w->counters;
+  return ESPN_OK;
+}
+
+int espn_gpu_synth_table(uint64_t n_docs, uint32_t d, uint32_t dtype, uint32_t t_min, uint32_t t_max,
+                         uint64_t seed, uint64_t* row_ptr, uint16_t* rows, void* stream_v) {
+  if (n_docs == 0 || t_min < 1 || t_max < t_min) return fail(ESPN_E_INVALID_INPUT, "bad synth shape");
+  if (!row_ptr) return fail(ESPN_E_INVALID_INPUT, "null row_ptr");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_v);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  ESPN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (!rows) {
+    synth_lengths_kernel<<<sms * 8, 256, 0, s>>>(n_docs, t_min, t_max, seed, row_ptr);
+    scan_u64_kernel<<<1, 1024, 0, s>>>(row_ptr, n_docs);
+    ESPN_CUDA_TRY(cudaGetLastError());
+    ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+    return ESPN_OK;
+  }
+  uint64_t n_rows = 0;
+  ESPN_CUDA_TRY(cudaMemcpyAsync(&n_rows, row_ptr + n_docs, sizeof n_rows, cudaMemcpyDeviceToHost, s));
+  ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  const uint64_t rseed = splitmix64(seed ^ 0x5EEDull);
+  switch (d) {
+#define ESPN_S(DD) case DD: synth_rows_kernel<DD><<<sms * 16, 256, 0, s>>>(n_rows, rseed, dtype == ESPN_DTYPE_BF16, rows); break;
+    ESPN_S(16) ESPN_S(32) ESPN_S(64) ESPN_S(128)
+#undef ESPN_S
+    default: return fail(ESPN_E_INVALID_INPUT, "synth supports d in {16,32,64,128}");
+  }
+  ESPN_CUDA_TRY(cudaGetLastError());
+  ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  return ESPN_OK;
+}
+
+}  // extern "C"

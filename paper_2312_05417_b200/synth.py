@@ -1,0 +1,84 @@
+"""Seeded synthetic MS-MARCO-shaped inputs.
+
+Host-side (numpy) generator for tests and the CPU baseline; the bench builds
+multi-GB tables on the device with espn_gpu_synth_table instead (same shape
+law, counter-based RNG).
+
+  * doc token rows: i.i.d. N(0,1), L2-normalised per row, rounded to the
+    table dtype with subnormals flushed;
+  * t ~ U{t_min..t_max} per doc;
+  * queries: perturbed copies (sigma) of a sampled source doc's rows,
+    resampled to q tokens, normalised;
+  * candidates: the source doc plus K-1 distinct uniform ids, cls scores in
+    (0, 1) sorted (cls desc, id asc) as ivf.hpp:45-46 requires.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .api import decode, encode
+
+
+def flush_subnormals(codes: np.ndarray, dtype: str) -> np.ndarray:
+    codes = codes.copy()
+    if dtype in ("f16", "fp16"):
+        sub = (codes & 0x7C00) == 0
+    else:
+        sub = (codes & 0x7F80) == 0
+    codes[sub] &= 0x8000
+    return codes
+
+
+def make_table(n_docs: int, d: int, t_min: int, t_max: int, dtype: str = "f16", seed: int = 42):
+    rng = np.random.default_rng(seed)
+    t = rng.integers(t_min, t_max + 1, size=n_docs, dtype=np.int64)
+    row_ptr = np.zeros(n_docs + 1, np.uint64)
+    row_ptr[1:] = np.cumsum(t)
+    n_tok = int(row_ptr[-1])
+    x = rng.standard_normal((n_tok, d), dtype=np.float32)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    codes = flush_subnormals(encode(x.ravel(), dtype), dtype)
+    return row_ptr, codes
+
+
+def make_queries(row_ptr, codes, d: int, n_queries: int, nq: int = 32, dtype: str = "f16",
+                 sigma: float = 0.1, seed: int = 7):
+    """Returns (q fp32 [B, nq, d], source doc ids [B])."""
+    rng = np.random.default_rng(seed)
+    n_docs = row_ptr.shape[0] - 1
+    src = rng.integers(0, n_docs, size=n_queries)
+    q = np.empty((n_queries, nq, d), np.float32)
+    for b, s in enumerate(src):
+        a, e = int(row_ptr[s]), int(row_ptr[s + 1])
+        rows = decode(codes[a * d:e * d], dtype).reshape(e - a, d)
+        pick = rng.integers(0, e - a, size=nq)
+        v = rows[pick] + sigma * rng.standard_normal((nq, d), dtype=np.float32)
+        q[b] = v / np.linalg.norm(v, axis=1, keepdims=True)
+    return q, src
+
+
+def make_candidates(n_docs: int, n_queries: int, k: int, src=None, seed: int = 11):
+    """CSR candidate lists: (ids u32, cls f32, offsets u64)."""
+    rng = np.random.default_rng(seed)
+    k = min(k, n_docs)
+    ids = np.empty((n_queries, k), np.uint32)
+    cls = np.empty((n_queries, k), np.float32)
+    for b in range(n_queries):
+        if n_docs <= 4 * k:
+            c = rng.permutation(n_docs)[:k]
+        else:
+            c = np.unique(rng.integers(0, n_docs, size=int(k * 1.2) + 16))
+            c = rng.permutation(c)[:k]
+            while c.size < k:
+                extra = np.setdiff1d(np.unique(rng.integers(0, n_docs, size=k)), c)
+                c = np.concatenate([c, extra])[:k]
+        if src is not None and src[b] not in c:
+            c[0] = src[b]
+        s = rng.random(k, dtype=np.float32)
+        if src is not None:
+            s[c == src[b]] = 1.0
+        order = np.lexsort((c, -s))  # cls desc, id asc
+        ids[b] = c[order]
+        cls[b] = s[order]
+    off = np.arange(n_queries + 1, dtype=np.uint64) * k
+    return ids.ravel(), cls.ravel(), off

@@ -1,0 +1,256 @@
+"""GPU parity: libespn_gpu.so (tcgen05 and CUDA-core MaxSim, top-k, gather,
+merge) against the CPU oracle on the same seeded inputs.  All calls go through
+the C-ABI (ctypes).  Tolerances: tests/helpers.py."""
+import numpy as np
+import pytest
+
+from helpers import RTOL, assert_topk_equivalent, oracle_full_scores, rel_err
+
+pytestmark = pytest.mark.gpu
+
+from paper_2312_05417_b200 import api, synth  # noqa: E402
+
+
+def _dt(name):
+    import oracle_py
+    return oracle_py.F16 if name == "f16" else oracle_py.BF16
+
+
+def build_case(n_docs, d, t_min, t_max, B, K, nq=32, dtype="f16", seed=1):
+    rp, codes = synth.make_table(n_docs, d, t_min, t_max, dtype=dtype, seed=seed)
+    q, src = synth.make_queries(rp, codes, d, B, nq=nq, dtype=dtype, seed=seed + 1)
+    ids, cls, off = synth.make_candidates(n_docs, B, K, src=src, seed=seed + 2)
+    return rp, codes, q, ids, cls, off
+
+
+def run_gpu(rp, codes, d, dtype, q, ids, cls, off, cfg, kernel):
+    store = api.GpuStore(rp, codes, d, dtype=dtype)
+    rr = api.Reranker(store, len(off) - 1, max(int(off[-1]), 1), q.shape[1])
+    out = rr.rerank_arrays(q, ids, cls, off, cfg, kernel=kernel, write_bow=True)
+    rr.close()
+    store.close()
+    return out
+
+
+def check_against_oracle(oracle, rp, codes, d, dtype, q, ids, cls, off, cfg, kernel, bitexact_bow=False):
+    ot = oracle.OracleTable(rp, codes, d, dtype=_dt(dtype))
+    qr = oracle.round_to(q, _dt(dtype))  # the oracle consumes the same rounded query
+    gi, gs, gc, gbow = run_gpu(rp, codes, d, dtype, q, ids, cls, off, cfg, kernel)
+    st, obow = oracle.maxsim_batch(ot, qr, ids, off)
+    assert st == 0
+    st, oi, os_, on = oracle.rerank_batch(ot, qr, ids, cls, off, cfg.rerank_count, cfg.final_k, cfg.alpha,
+                                          cfg.partial_rerank_enabled)
+    assert st == 0
+    B = len(off) - 1
+    for b in range(B):
+        a0, a1 = int(off[b]), int(off[b + 1])
+        need = min(a1 - a0, cfg.rerank_count)
+        g = gbow[a0:a0 + need]
+        o = obow[a0:a0 + need]
+        if bitexact_bow:
+            assert np.array_equal(g.view(np.uint32), o.view(np.uint32)), f"query {b}: SIMT bow not bit-exact"
+        elif need:
+            e = rel_err(g, o)
+            assert e.max() <= RTOL, f"query {b}: max rel err {e.max()} at {int(e.argmax())}"
+        full = oracle_full_scores(obow[a0:a1], cls[a0:a1], cfg.alpha, need, cfg.partial_rerank_enabled)
+        assert int(gc[b]) == int(on[b])
+        n = int(on[b])
+        assert_topk_equivalent(gi[b, :n], gs[b, :n], oi[b, :n], os_[b, :n], ids[a0:a1], full, ctx=f"query {b}")
+    return gbow, obow
+
+
+@pytest.mark.parametrize("kernel", ["tcgen05", "simt"])
+def test_c1_shape_parity(oracle, cuda_ok, kernel):
+    # configs[0]: 100k docs, <=32 tok/doc, d32 fp16, 32 query tok, top-1000 -> top-10 (B=1);
+    # a 20k-doc table keeps the oracle fast; the shape law is the same.
+    rp, codes, q, ids, cls, off = build_case(20000, 32, 1, 32, B=2, K=1000)
+    cfg = api.PipelineConfig(rerank_count=1000, final_k=10)
+    check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, kernel,
+                         bitexact_bow=(kernel == "simt"))
+
+
+@pytest.mark.parametrize("d", [16, 32, 64, 128])
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_tcgen05_dims_dtypes(oracle, cuda_ok, d, dtype):
+    t_max = 100 if d == 128 else 63
+    rp, codes, q, ids, cls, off = build_case(3000, d, 1, t_max, B=3, K=257, dtype=dtype, seed=d)
+    cfg = api.PipelineConfig(rerank_count=257, final_k=10)
+    check_against_oracle(oracle, rp, codes, d, dtype, q, ids, cls, off, cfg, "tcgen05")
+
+
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_simt_bitexact(oracle, cuda_ok, d):
+    rp, codes, q, ids, cls, off = build_case(2000, d, 1, 40, B=3, K=200, seed=3 + d)
+    cfg = api.PipelineConfig(rerank_count=200, final_k=10)
+    check_against_oracle(oracle, rp, codes, d, "f16", q, ids, cls, off, cfg, "simt", bitexact_bow=True)
+
+
+def test_c2_shape_many_units(oracle, cuda_ok):
+    # configs[1] shape law (t ~ U{1..63}, d32, K=R=1000, k=10) at batch 64 on a
+    # 200k-doc table: hundreds of work units, stage/quarter straddling docs.
+    rp, codes, q, ids, cls, off = build_case(200000, 32, 1, 63, B=64, K=1000, seed=5)
+    cfg = api.PipelineConfig(rerank_count=1000, final_k=10)
+    check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
+
+
+@pytest.mark.parametrize("kernel", ["tcgen05", "simt"])
+def test_partial_rerank_and_alpha(oracle, cuda_ok, kernel):
+    rp, codes, q, ids, cls, off = build_case(5000, 32, 1, 63, B=4, K=1000, seed=9)
+    cfg = api.PipelineConfig(rerank_count=64, final_k=10, alpha=0.5, partial_rerank_enabled=True)
+    check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, kernel)
+
+
+def test_partial_with_r_equal_k_matches_full(cuda_ok):
+    # R == candidate-list length => partial == full, bit-exact
+    rp, codes, q, ids, cls, off = build_case(3000, 32, 1, 63, B=3, K=300, seed=21)
+    full = run_gpu(rp, codes, 32, "f16", q, ids, cls, off, api.PipelineConfig(rerank_count=300, final_k=10), "auto")
+    part = run_gpu(rp, codes, 32, "f16", q, ids, cls, off,
+                   api.PipelineConfig(rerank_count=300, final_k=10, partial_rerank_enabled=True), "auto")
+    assert np.array_equal(full[0], part[0]) and np.array_equal(full[1], part[1])
+
+
+def test_short_lists_small_nq_long_docs(oracle, cuda_ok):
+    # ragged: q=5 tokens, candidate lists shorter than final_k and than R,
+    # docs up to 400 tokens (fewer docs per work unit)
+    rp, codes = synth.make_table(1500, 32, 1, 400, seed=31)
+    q, src = synth.make_queries(rp, codes, 32, 5, nq=5, seed=32)
+    ids_l, cls_l, offs = [], [], [0]
+    rng = np.random.default_rng(33)
+    for b, n in enumerate([3, 0, 50, 700, 1]):
+        c = rng.permutation(1500)[:n].astype(np.uint32)
+        s = np.sort(rng.random(n).astype(np.float32))[::-1].copy()
+        o = np.lexsort((c, -s))
+        ids_l.append(c[o]); cls_l.append(s[o]); offs.append(offs[-1] + n)
+    ids = np.concatenate(ids_l).astype(np.uint32)
+    cls = np.concatenate(cls_l).astype(np.float32)
+    off = np.asarray(offs, np.uint64)
+    cfg = api.PipelineConfig(rerank_count=600, final_k=10)
+    check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
+    check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "simt", bitexact_bow=True)
+
+
+def test_single_token_docs_and_large_k(oracle, cuda_ok):
+    rp, codes, q, ids, cls, off = build_case(4000, 32, 1, 1, B=2, K=3000, seed=41)
+    cfg = api.PipelineConfig(rerank_count=3000, final_k=100)
+    check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
+
+
+def test_c5_candidate_count(oracle, cuda_ok):
+    # configs[4]: 4000 candidates per query (top-k over > one sort chunk)
+    rp, codes, q, ids, cls, off = build_case(50000, 32, 1, 63, B=2, K=4000, seed=51)
+    cfg = api.PipelineConfig(rerank_count=4000, final_k=10)
+    check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
+
+
+def test_errors(cuda_ok):
+    rp, codes, q, ids, cls, off = build_case(1000, 32, 1, 20, B=2, K=100, seed=61)
+    store = api.GpuStore(rp, codes, 32)
+    rr = api.Reranker(store, 2, 200, 32)
+    cfg = api.PipelineConfig(rerank_count=100, final_k=10)
+    bad = ids.copy(); bad[5] = 1000  # store lacks a candidate -> DataIntegrityError
+    with pytest.raises(api.DataIntegrityError):
+        rr.rerank_arrays(q, bad, cls, off, cfg)
+    dup = ids.copy(); dup[7] = dup[3]  # rank() rejects duplicates (scoring.hpp:16-18)
+    with pytest.raises(api.InvalidInputError):
+        rr.rerank_arrays(q, dup, cls, off, cfg)
+    nan = cls.copy(); nan[2] = np.nan
+    with pytest.raises(api.InvalidInputError):
+        rr.rerank_arrays(q, ids, nan, off, cfg)
+    with pytest.raises(api.InvalidInputError):  # R < final_k without partial
+        rr.rerank_arrays(q, ids, cls, off, api.PipelineConfig(rerank_count=5, final_k=10))
+    qn = q.copy(); qn[1, 3, 4] = np.inf
+    with pytest.raises(api.InvalidInputError):
+        rr.rerank_arrays(qn, ids, cls, off, cfg)
+    # still usable after errors
+    gi, gs, gc, _ = rr.rerank_arrays(q, ids, cls, off, cfg)
+    assert list(gc) == [10, 10]
+    rr.close(); store.close()
+
+
+def test_gather_bitexact(oracle, cuda_ok):
+    rp, codes = synth.make_table(5000, 32, 1, 63, seed=71)
+    store = api.GpuStore(rp, codes, 32)
+    ot = oracle.OracleTable(rp, codes, 32)
+    rng = np.random.default_rng(72)
+    req = rng.integers(0, 5000, size=1000).astype(np.uint32)
+    req[10] = req[11]  # duplicates allowed (store.hpp:92)
+    res = store.fetch_batch(req)
+    st, orp, orows = oracle.gather(ot, req)
+    assert st == 0
+    assert len(res.docs) == len(req)
+    got = np.concatenate([api.encode(doc.bow.values, "f16") for doc in res.docs])
+    assert np.array_equal(got, orows)
+    assert [doc.bow.rows for doc in res.docs] == list(np.diff(orp).astype(int))
+    assert [doc.bow.doc_id for doc in res.docs] == list(req.astype(int))
+    with pytest.raises(api.InvalidInputError):
+        store.fetch_batch([1, 5000])
+    assert store.fetch_batch([]).docs == []
+    store.close()
+
+
+def test_merge_topk(cuda_ok):
+    import torch
+    from paper_2312_05417_b200 import _lib as L
+    rng = np.random.default_rng(81)
+    G, B, k = 4, 8, 10
+    ids = np.zeros((G, B, k), np.uint32); sc = np.zeros((G, B, k), np.float32); cnt = np.zeros((G, B), np.uint32)
+    allc = [[] for _ in range(B)]
+    for g in range(G):
+        for b in range(B):
+            n = int(rng.integers(0, k + 1))
+            i = rng.choice(100000, size=n, replace=False).astype(np.uint32) * G + g  # disjoint shards
+            s = rng.standard_normal(n).astype(np.float32)
+            s[:n // 2] = 0.25  # exact ties broken by id asc
+            o = np.lexsort((i, -s))
+            ids[g, b, :n] = i[o]; sc[g, b, :n] = s[o]; cnt[g, b] = n
+            allc[b] += list(zip(s[o], i[o]))
+    dev = torch.device("cuda")
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(dev)
+    oi = torch.zeros((B, k), dtype=torch.int32, device=dev)
+    os_ = torch.zeros((B, k), dtype=torch.float32, device=dev)
+    oc = torch.zeros(B, dtype=torch.int32, device=dev)
+    ti, ts, tc = t(ids), t(sc), t(cnt)
+    rc = L.lib().espn_gpu_merge_topk(ti.data_ptr(), ts.data_ptr(), tc.data_ptr(), G, B, k, oi.data_ptr(),
+                                     os_.data_ptr(), oc.data_ptr(), None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    oi, os_, oc = oi.cpu().numpy().view(np.uint32), os_.cpu().numpy(), oc.cpu().numpy()
+    for b in range(B):
+        exp = sorted(allc[b], key=lambda x: (-x[0], x[1]))[:k]
+        assert oc[b] == len(exp)
+        assert list(oi[b, :oc[b]]) == [int(e[1]) for e in exp]
+        assert np.array_equal(os_[b, :oc[b]], np.asarray([e[0] for e in exp], np.float32))
+
+
+def test_api_mirror_rerank_candidates(oracle, cuda_ok):
+    rp, codes, q, ids, cls, off = build_case(3000, 32, 1, 63, B=1, K=200, seed=91)
+    store = api.GpuStore(rp, codes, 32)
+    qe = api.QueryEmbedding(query_id=3, cls=np.zeros(128, np.float32), rows=32, cols=32, tokens=q[0].ravel())
+    cl = api.CandidateList([api.Candidate(int(i), float(c)) for i, c in zip(ids, cls)])
+    ranked, stats = api.rerank_candidates(qe, cl, store, api.PipelineConfig(rerank_count=200, final_k=10))
+    ot = oracle.OracleTable(rp, codes, 32)
+    st, oi, os_, ostats = oracle.rerank_query(ot, oracle.round_to(q[0]), ids, cls, 200, 10)
+    assert st == 0
+    assert [e.doc_id for e in ranked.entries] == list(oi)
+    assert stats.needed_count == 200 and stats.query_id == 3
+    assert stats.needed_payload_bytes == ostats.needed_payload_bytes
+    store.close()
+
+
+def test_synth_table_on_device(cuda_ok):
+    import torch
+    from paper_2312_05417_b200 import _lib as L
+    n, d = 10000, 32
+    rp = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+    assert L.lib().espn_gpu_synth_table(n, d, 0, 1, 63, 42, rp.data_ptr(), None, None) == 0
+    t = torch.diff(rp).cpu().numpy()
+    assert t.min() >= 1 and t.max() <= 63 and abs(t.mean() - 32) < 1.5
+    rows = torch.zeros(int(rp[-1]) * d, dtype=torch.int16, device="cuda")
+    assert L.lib().espn_gpu_synth_table(n, d, 0, 1, 63, 42, rp.data_ptr(), rows.data_ptr(), None) == 0
+    v = rows.cpu().numpy().view(np.float16).astype(np.float32).reshape(-1, d)
+    nrm = np.linalg.norm(v, axis=1)
+    assert np.all(np.isfinite(v)) and np.abs(nrm - 1).max() < 5e-3
+    assert not np.any((rows.cpu().numpy().view(np.uint16) & 0x7C00) == 0) or True
+    codes = rows.cpu().numpy().view(np.uint16)
+    sub = ((codes & 0x7C00) == 0) & ((codes & 0x3FF) != 0)
+    assert not sub.any(), "synthetic table must not contain fp16 subnormals"
