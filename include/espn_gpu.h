@@ -81,7 +81,12 @@ typedef struct {
   const uint64_t* row_ptr; /* n_docs + 1 token offsets, row_ptr[0] == 0 */
   const uint16_t* rows;    /* row_ptr[n_docs] * d codes */
   int32_t device;          /* CUDA device ordinal */
-  uint32_t reserved[7];
+  /* Doc-id sharding (multi-GPU): this table holds the docs with
+   * id % shard_count == shard_index, global id g at local index g / shard_count.
+   * All ids crossing the ABI stay global.  0 or 1 = unsharded. */
+  uint32_t shard_count;
+  uint32_t shard_index;
+  uint32_t reserved[5];
 } espn_table_desc;
 
 typedef struct {
@@ -118,6 +123,8 @@ ESPN_API int espn_gpu_workspace_destroy(espn_gpu_workspace* ws);
 #define ESPN_RERANK_DEVICE_IO 0x2u    /* all array pointers in args/out are device pointers */
 #define ESPN_RERANK_ASYNC 0x4u        /* do not synchronize; errors surface in espn_gpu_workspace_sync */
 #define ESPN_RERANK_WRITE_BOW 0x8u    /* also return per-candidate MaxSim (bow) scores */
+#define ESPN_RERANK_PROFILE 0x10u     /* time the MaxSim and top-k kernels with CUDA events on
+                                         `stream` (accumulated into espn_counters) */
 
 /* One batch of queries with their final candidate lists (ivf.hpp:45-50:
  * sorted (cls_score desc, doc_id asc), deduplicated), CSR over queries.
@@ -169,34 +176,49 @@ ESPN_API int espn_gpu_gather(espn_gpu_table* table, const uint32_t* ids, uint64_
                     void* stream);
 
 /* Merge per-shard ranked lists (multi-GPU, doc-id sharding): for each of
- * n_queries queries, `n_lists` ranked lists of up to k entries each laid out
- * [list][query][k] with counts [list][query], merged into the global top-k by
- * (score desc, doc_id asc).  Device pointers. */
+ * n_queries queries, `n_lists` ranked lists of up to k entries, merged into
+ * the global top-k by (score desc, doc_id asc).  List l's arrays start at
+ * ids + l*list_stride, scores + l*list_stride, counts + l*list_stride
+ * (list_stride in 4-byte elements; ids/scores are [query][k], counts [query]),
+ * so one packed all-gather buffer can be merged in place.  Device pointers. */
 ESPN_API int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const uint32_t* counts,
-                        uint32_t n_lists, uint32_t n_queries, uint32_t k, uint32_t* out_ids,
-                        float* out_scores, uint32_t* out_counts, void* stream);
+                        uint32_t n_lists, uint64_t list_stride, uint32_t n_queries, uint32_t k,
+                        uint32_t* out_ids, float* out_scores, uint32_t* out_counts, void* stream);
 
-/* Cumulative device counters of a workspace (bytes gathered, pairs scored,
- * kernel launches) since creation. */
+/* Cumulative counters of a workspace since creation.  Reading them completes
+ * any PROFILE events still in flight (synchronizes on them). */
 typedef struct {
   uint64_t batches;
   uint64_t queries;
-  uint64_t pairs_scored;
-  uint64_t tokens_scored;
-  uint64_t kernel_launches;
-  uint64_t reserved[3];
+  uint64_t pairs_scored;       /* (query, candidate) MaxSim evaluations */
+  uint64_t kernel_launches;    /* kernels of this library launched by the workspace */
+  uint64_t profiled_batches;   /* batches run with ESPN_RERANK_PROFILE */
+  double maxsim_ms;            /* summed CUDA-event time of the MaxSim kernel (PROFILE) */
+  double topk_ms;              /* summed CUDA-event time of the top-k kernel (PROFILE) */
+  uint64_t reserved;
 } espn_counters;
 ESPN_API int espn_gpu_get_counters(const espn_gpu_workspace* ws, espn_counters* out);
 
 /* Synthetic MS-MARCO-shaped table generation on the device (bench/tests):
- * t_i ~ U{t_min..t_max} and i.i.d. N(0,1) rows L2-normalised per row, rounded to
- * dtype with subnormals flushed; counter-based RNG so
- * any doc can be regenerated independently.  Writes row_ptr (n_docs+1) and rows
- * (device pointers; rows must hold row_ptr[n_docs]*d codes -- call with
- * rows == NULL first to fill row_ptr only). */
-ESPN_API int espn_gpu_synth_table(uint64_t n_docs, uint32_t d, uint32_t dtype, uint32_t t_min,
-                         uint32_t t_max, uint64_t seed, uint64_t* row_ptr, uint16_t* rows,
-                         void* stream);
+ * t ~ U{t_min..t_max} per doc and i.i.d. N(0,1) rows L2-normalised per row,
+ * rounded to dtype with subnormals flushed.  The RNG
+ * is counter-based and keyed by the GLOBAL doc id (and token index), so the
+ * corpus is identical for every shard count and any doc can be regenerated
+ * independently (paper_2312_05417_b200/synth.py mirrors it on the host).
+ * Generates shard `shard_index` of `shard_count` (local doc i = global id
+ * i*shard_count + shard_index) with n_local_docs docs.  Writes row_ptr
+ * (n_local_docs+1) and rows (device pointers; rows must hold
+ * row_ptr[n_local_docs]*d codes -- call with rows == NULL first to fill
+ * row_ptr only). */
+ESPN_API int espn_gpu_synth_table(uint64_t n_local_docs, uint32_t d, uint32_t dtype, uint32_t t_min,
+                         uint32_t t_max, uint64_t seed, uint32_t shard_count, uint32_t shard_index,
+                         uint64_t* row_ptr, uint16_t* rows, void* stream);
+
+/* K1 copy stage only, asynchronous on `stream` (for kernel timing / ncu):
+ * out_row_ptr must already hold the request-order token offsets (as produced by
+ * espn_gpu_gather with out_rows == NULL); ids must be known.  Device pointers. */
+ESPN_API int espn_gpu_gather_rows(espn_gpu_table* table, const uint32_t* ids, uint64_t n,
+                         const uint64_t* out_row_ptr, uint16_t* out_rows, void* stream);
 
 ESPN_API const char* espn_last_error(void);
 ESPN_API int espn_abi_version(void);

@@ -33,6 +33,7 @@ ESPN_RERANK_PARTIAL = 0x1
 ESPN_RERANK_DEVICE_IO = 0x2
 ESPN_RERANK_ASYNC = 0x4
 ESPN_RERANK_WRITE_BOW = 0x8
+ESPN_RERANK_PROFILE = 0x10
 
 
 class TableDesc(C.Structure):
@@ -40,7 +41,8 @@ class TableDesc(C.Structure):
         ("n_docs", C.c_uint64), ("d", C.c_uint32), ("dtype", C.c_uint32),
         ("d_cls", C.c_uint32), ("value_width", C.c_uint32), ("alignment", C.c_uint32),
         ("flags", C.c_uint32), ("row_ptr", C.c_void_p), ("rows", C.c_void_p),
-        ("device", C.c_int32), ("reserved", C.c_uint32 * 7),
+        ("device", C.c_int32), ("shard_count", C.c_uint32), ("shard_index", C.c_uint32),
+        ("reserved", C.c_uint32 * 5),
     ]
 
 
@@ -79,8 +81,8 @@ class RerankOut(C.Structure):
 class Counters(C.Structure):
     _fields_ = [
         ("batches", C.c_uint64), ("queries", C.c_uint64), ("pairs_scored", C.c_uint64),
-        ("tokens_scored", C.c_uint64), ("kernel_launches", C.c_uint64),
-        ("reserved", C.c_uint64 * 3),
+        ("kernel_launches", C.c_uint64), ("profiled_batches", C.c_uint64),
+        ("maxsim_ms", C.c_double), ("topk_ms", C.c_double), ("reserved", C.c_uint64),
     ]
 
 
@@ -94,11 +96,12 @@ SIGNATURES = {
     "espn_gpu_rerank": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.POINTER(RerankOut), C.c_void_p]),
     "espn_gpu_workspace_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
     "espn_gpu_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
-    "espn_gpu_merge_topk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
-                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_gpu_merge_topk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32,
+                                      C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "espn_gpu_get_counters": (C.c_int, [C.c_void_p, C.POINTER(Counters)]),
     "espn_gpu_synth_table": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
-                                       C.c_void_p, C.c_void_p, C.c_void_p]),
+                                       C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_gpu_gather_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "espn_last_error": (C.c_char_p, []),
     "espn_abi_version": (C.c_int, []),
 }

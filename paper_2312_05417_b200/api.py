@@ -218,7 +218,7 @@ class GpuStore:
 
     def __init__(self, row_ptr, rows, d: int, dtype: str = "f16", d_cls: int = 128,
                  value_width: int = 2, alignment: int = 4096, device: int = 0,
-                 borrowed_device: bool = False):
+                 borrowed_device: bool = False, shard_count: int = 1, shard_index: int = 0):
         self.d = int(d)
         self.dtype = dtype
         self.d_cls = int(d_cls)
@@ -239,7 +239,10 @@ class GpuStore:
             rp_p, rows_p, flags = _ptr(row_ptr), _ptr(rows), 0
         desc = L.TableDesc(n_docs=n_docs, d=self.d, dtype=_DTYPES[dtype], d_cls=self.d_cls,
                            value_width=self.value_width, alignment=self.alignment, flags=flags,
-                           row_ptr=rp_p, rows=rows_p, device=self.device)
+                           row_ptr=rp_p, rows=rows_p, device=self.device, shard_count=int(shard_count),
+                           shard_index=int(shard_index))
+        self.shard_count = max(int(shard_count), 1)
+        self.shard_index = int(shard_index) if self.shard_count > 1 else 0
         h = C.c_void_p()
         _check(L.lib().espn_gpu_table_open(C.byref(desc), C.byref(h)))
         self._h = h

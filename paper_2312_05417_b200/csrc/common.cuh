@@ -4,6 +4,18 @@
 
 namespace espn_k {
 
+// Global doc id -> local row index of this shard, or UINT64_MAX if the id is
+// not stored here (unknown id / wrong shard -> DataIntegrityError).
+__device__ __forceinline__ uint64_t shard_local(uint32_t id, uint32_t count, uint32_t index,
+                                                uint64_t n_docs) {
+  uint64_t local = id;
+  if (count > 1) {
+    if (id % count != index) return ~0ull;
+    local = id / count;
+  }
+  return local < n_docs ? local : ~0ull;
+}
+
 // Device-side error bits (mapped to espn_status by the host after sync).
 enum : uint32_t {
   ERR_UNKNOWN_DOC = 1u << 0,     // candidate id >= n_docs  -> DATA_INTEGRITY
@@ -18,7 +30,9 @@ enum : uint32_t {
 struct MaxSimParams {
   const uint16_t* rows;        // table token rows, d codes each
   const uint64_t* row_ptr;     // n_docs + 1
-  uint64_t n_docs;
+  uint64_t n_docs;             // local docs of this shard
+  uint32_t shard_count;        // doc-id sharding: id % shard_count == shard_index
+  uint32_t shard_index;        //   lives at local index id / shard_count
   const float* q32;            // B * nq * d fp32 query tokens
   const uint32_t* cand_ids;    // CSR over queries
   const uint64_t* cand_off;    // B + 1

@@ -173,6 +173,7 @@ struct espn_gpu_table {
   uint64_t n_docs = 0, n_tokens = 0;
   uint32_t d = 0, dtype = 0, d_cls = 0, value_width = 2, alignment = 1;
   uint32_t max_t = 0, min_t = 0;
+  uint32_t shard_count = 1, shard_index = 0;
   bool owned = false;
   uint64_t* row_ptr = nullptr;
   uint16_t* rows = nullptr;
@@ -192,13 +193,44 @@ struct espn_gpu_workspace {
   float* out_scores = nullptr;
   uint32_t* out_counts = nullptr;
   uint32_t* err = nullptr;
-  // pinned host staging for the small per-batch tables and the error word
-  uint64_t* h_cand_off = nullptr;
-  uint32_t* h_unit_off = nullptr;
-  uint32_t* h_needed = nullptr;
+  // Pinned host staging for the small per-batch tables, as a ring: an ASYNC
+  // caller may enqueue batch n+1 before batch n's H2D copies ran, so each
+  // call stages into its own slot, reused only after its copy-done event.
+  static constexpr int kSlots = 8;
+  struct Slot {
+    uint64_t* cand_off = nullptr;
+    uint32_t* unit_off = nullptr;
+    uint32_t* needed = nullptr;
+    cudaEvent_t copied = nullptr;
+    bool used = false;
+  } slots[kSlots];
+  uint64_t calls = 0;
   uint32_t* h_err = nullptr;
+  bool async_pending = false;  // device err word carries bits of un-synced ASYNC calls
+  // PROFILE: event triples around MaxSim / top-k, drained lazily
+  static constexpr int kProf = 64;
+  struct Prof {
+    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+    bool pending = false;
+  } prof[kProf];
+  uint64_t prof_calls = 0;
   espn_counters counters{};
 };
+
+namespace {
+void drain_prof(espn_gpu_workspace* w, int i) {
+  auto& p = w->prof[i];
+  if (!p.pending) return;
+  cudaEventSynchronize(p.e[2]);
+  float a = 0.f, b = 0.f;
+  cudaEventElapsedTime(&a, p.e[0], p.e[1]);
+  cudaEventElapsedTime(&b, p.e[1], p.e[2]);
+  w->counters.maxsim_ms += a;
+  w->counters.topk_ms += b;
+  w->counters.profiled_batches += 1;
+  p.pending = false;
+}
+}  // namespace
 
 extern "C" {
 
@@ -232,6 +264,9 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
   t->d_cls = desc->d_cls;
   t->value_width = desc->value_width;
   t->alignment = desc->alignment;
+  t->shard_count = desc->shard_count > 1 ? desc->shard_count : 1;
+  t->shard_index = desc->shard_count > 1 ? desc->shard_index : 0;
+  if (t->shard_index >= t->shard_count) { delete t; return fail(ESPN_E_INVALID_INPUT, "shard_index >= shard_count"); }
   const bool borrowed = (desc->flags & ESPN_TABLE_DEVICE_BORROWED) != 0;
   if (!borrowed) {
     // host tables: validate (types.hpp:64-68: t >= 1), then upload
@@ -346,9 +381,15 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   al((void**)&w->out_scores, B * kMaxK * sizeof(float));
   al((void**)&w->out_counts, B * sizeof(uint32_t));
   al((void**)&w->err, sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMallocHost(&w->h_cand_off, (B + 1) * sizeof(uint64_t));
-  if (e == cudaSuccess) e = cudaMallocHost(&w->h_unit_off, (B + 1) * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMallocHost(&w->h_needed, (B + 1) * sizeof(uint32_t));
+  for (auto& sl : w->slots) {
+    if (e == cudaSuccess) e = cudaMallocHost(&sl.cand_off, (B + 1) * sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMallocHost(&sl.unit_off, (B + 1) * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMallocHost(&sl.needed, (B + 1) * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming);
+  }
+  for (auto& pr : w->prof)
+    for (auto& ev : pr.e)
+      if (e == cudaSuccess) e = cudaEventCreate(&ev);
   if (e == cudaSuccess) e = cudaMallocHost(&w->h_err, sizeof(uint32_t));
   if (e != cudaSuccess) {
     espn_gpu_workspace_destroy(w);
@@ -364,7 +405,15 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   cudaFree(w->q32); cudaFree(w->ids); cudaFree(w->cls); cudaFree(w->cand_off);
   cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
   cudaFree(w->out_counts); cudaFree(w->err);
-  cudaFreeHost(w->h_cand_off); cudaFreeHost(w->h_unit_off); cudaFreeHost(w->h_needed); cudaFreeHost(w->h_err);
+  for (auto& sl : w->slots) {
+    if (sl.copied) cudaEventSynchronize(sl.copied);
+    cudaFreeHost(sl.cand_off); cudaFreeHost(sl.unit_off); cudaFreeHost(sl.needed);
+    if (sl.copied) cudaEventDestroy(sl.copied);
+  }
+  for (auto& pr : w->prof)
+    for (auto& ev : pr.e)
+      if (ev) { cudaEventSynchronize(ev); cudaEventDestroy(ev); }
+  cudaFreeHost(w->h_err);
   delete w;
   return ESPN_OK;
 }
@@ -406,27 +455,35 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     return fail(ESPN_E_INVALID_CONFIG, "CUDA-core MaxSim supports d in {8,16,32,48,64,96,128}");
 
   // ---- per-query work units (tcgen05) or pair prefix (SIMT), host-built ----
+  auto& sl = w->slots[w->calls % espn_gpu_workspace::kSlots];
+  if (sl.used) ESPN_CUDA_TRY(cudaEventSynchronize(sl.copied));  // slot's previous H2D done
   uint64_t acc = 0, pairs = 0;
   for (uint32_t b = 0; b < B; ++b) {
-    w->h_cand_off[b] = off[b];
+    sl.cand_off[b] = off[b];
     const uint64_t n = off[b + 1] - off[b];
     const uint64_t need = a->needed_counts ? std::min<uint64_t>(n, a->needed_counts[b])
                                            : std::min<uint64_t>(n, a->rerank_count);
-    w->h_needed[b] = (uint32_t)need;
-    w->h_unit_off[b] = (uint32_t)acc;
+    sl.needed[b] = (uint32_t)need;
+    sl.unit_off[b] = (uint32_t)acc;
     pairs += need;
     acc += kern == ESPN_KERNEL_TCGEN05 ? (need + unit_docs - 1) / unit_docs : need;
   }
-  w->h_cand_off[B] = off[B];
-  w->h_unit_off[B] = (uint32_t)acc;
+  sl.cand_off[B] = off[B];
+  sl.unit_off[B] = (uint32_t)acc;
   if (acc > UINT32_MAX) return fail(ESPN_E_INVALID_INPUT, "batch too large");
+  const bool profile = (a->flags & ESPN_RERANK_PROFILE) != 0;
+  const int pslot = (int)(w->prof_calls % espn_gpu_workspace::kProf);
+  if (profile) drain_prof(w, pslot);
 
   const float* q32 = a->query_tokens;
   const uint32_t* ids = a->cand_ids;
   const float* cls = a->cand_cls;
-  ESPN_CUDA_TRY(cudaMemcpyAsync(w->cand_off, w->h_cand_off, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-  ESPN_CUDA_TRY(cudaMemcpyAsync(w->unit_off, w->h_unit_off, (B + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-  ESPN_CUDA_TRY(cudaMemcpyAsync(w->needed, w->h_needed, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->cand_off, sl.cand_off, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->unit_off, sl.unit_off, (B + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->needed, sl.needed, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  ESPN_CUDA_TRY(cudaEventRecord(sl.copied, s));
+  sl.used = true;
+  ++w->calls;
   if (!dev_io) {
     ESPN_CUDA_TRY(cudaMemcpyAsync(w->q32, q32, (size_t)B * nq * t->d * sizeof(float), cudaMemcpyHostToDevice, s));
     if (C) {
@@ -437,12 +494,15 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     ids = w->ids;
     cls = w->cls;
   }
-  ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
+  // the device error word is sticky across un-synced ASYNC batches
+  if (!w->async_pending) ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
 
   MaxSimParams mp{};
   mp.rows = t->rows;
   mp.row_ptr = t->row_ptr;
   mp.n_docs = t->n_docs;
+  mp.shard_count = t->shard_count;
+  mp.shard_index = t->shard_index;
   mp.q32 = q32;
   mp.cand_ids = ids;
   mp.cand_off = w->cand_off;
@@ -456,9 +516,11 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   mp.unit_docs = (uint32_t)std::max(unit_docs, 1);
   mp.n_units = (uint32_t)acc;
   mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
+  if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
   cudaError_t e = kern == ESPN_KERNEL_TCGEN05 ? launch_tc_rt(t->d, mp, t->num_sms, s)
                                                : launch_simt_rt(t->d, mp, acc, t->num_sms, s);
   if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
+  if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[1], s));
 
   ESPN_CUDA_TRY(ensure_topk_attr());
   TopKParams tp{};
@@ -478,6 +540,11 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   tp.alpha = a->alpha;
   topk_kernel<<<B, kTopkThreads, topk_smem_bytes(), s>>>(tp);
   ESPN_CUDA_TRY(cudaGetLastError());
+  if (profile) {
+    ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[2], s));
+    w->prof[pslot].pending = true;
+    ++w->prof_calls;
+  }
 
   if (!dev_io) {
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->ids, w->out_ids, (size_t)B * k * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -488,20 +555,27 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->bow_scores, w->bow, C * sizeof(float),
                                   dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   }
-  ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   w->counters.batches += 1;
   w->counters.queries += B;
   w->counters.pairs_scored += pairs;
   w->counters.kernel_launches += 2;
-  if (a->flags & ESPN_RERANK_ASYNC) return ESPN_OK;
+  if (a->flags & ESPN_RERANK_ASYNC) {
+    w->async_pending = true;
+    return ESPN_OK;
+  }
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  w->async_pending = false;
   return err_bits_to_status(*w->h_err);
 }
 
 int espn_gpu_workspace_sync(espn_gpu_workspace* w, void* stream_v) {
   if (!w) return fail(ESPN_E_INVALID_INPUT, "null argument");
   DeviceGuard g(w->table->device);
-  ESPN_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_v)));
+  cudaStream_t s = static_cast<cudaStream_t>(stream_v);
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  w->async_pending = false;
   return err_bits_to_status(*w->h_err);
 }
 
@@ -524,7 +598,7 @@ int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t
   ESPN_CUDA_TRY(cudaMallocAsync(&derr, sizeof(uint32_t), s));
   ESPN_CUDA_TRY(cudaMemsetAsync(derr, 0, sizeof(uint32_t), s));
   const int blocks = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)t->num_sms * 8);
-  gather_count_kernel<<<blocks, 256, 0, s>>>(t->row_ptr, t->n_docs, ids, n, out_row_ptr, derr);
+  gather_count_kernel<<<blocks, 256, 0, s>>>(t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, derr);
   scan_u64_kernel<<<1, 1024, 0, s>>>(out_row_ptr, n);
   uint32_t herr = 0;
   uint64_t total = 0;
@@ -536,11 +610,11 @@ int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t
     g_last_error = "unknown doc id in gather request (store.hpp:92-93)";
     return ESPN_E_INVALID_INPUT;
   }
+  if (!out_rows) return ESPN_OK;  // offsets only
   if (total > capacity_tokens) return fail(ESPN_E_INVALID_INPUT, "out_rows capacity too small");
-  if (!out_rows) return ESPN_OK;
   const int cb = t->num_sms * 8;
   switch (t->d) {
-#define ESPN_G(DD) case DD: gather_copy_kernel<DD><<<cb, 256, 0, s>>>(t->rows, t->row_ptr, t->n_docs, ids, n, out_row_ptr, out_rows); break;
+#define ESPN_G(DD) case DD: gather_copy_kernel<DD><<<cb, 256, 0, s>>>(t->rows, t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, out_rows); break;
     ESPN_G(8) ESPN_G(16) ESPN_G(32) ESPN_G(48) ESPN_G(64) ESPN_G(96) ESPN_G(128) ESPN_G(256)
 #undef ESPN_G
     default: return fail(ESPN_E_INVALID_CONFIG, "gather supports d in {8,16,32,48,64,96,128,256}");
@@ -551,46 +625,68 @@ int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t
 }
 
 int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const uint32_t* counts,
-                        uint32_t n_lists, uint32_t n_queries, uint32_t k, uint32_t* out_ids,
-                        float* out_scores, uint32_t* out_counts, void* stream_v) {
+                        uint32_t n_lists, uint64_t list_stride, uint32_t n_queries, uint32_t k,
+                        uint32_t* out_ids, float* out_scores, uint32_t* out_counts, void* stream_v) {
   if (k < 1 || k > (uint32_t)kMaxK) return fail(ESPN_E_INVALID_INPUT, "k must be in [1, 1024]");
   if (n_queries == 0) return ESPN_OK;
   if (!ids || !scores || !counts || !out_ids || !out_scores || !out_counts)
     return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (n_lists > 1 && list_stride < (uint64_t)n_queries * k)
+    return fail(ESPN_E_INVALID_INPUT, "list_stride smaller than one list");
   ESPN_CUDA_TRY(ensure_topk_attr());
   merge_topk_kernel<<<n_queries, kTopkThreads, topk_smem_bytes(), static_cast<cudaStream_t>(stream_v)>>>(
-      ids, scores, counts, n_lists, n_queries, k, out_ids, out_scores, out_counts);
+      ids, scores, counts, n_lists, list_stride, n_queries, k, out_ids, out_scores, out_counts);
+  ESPN_CUDA_TRY(cudaGetLastError());
+  return ESPN_OK;
+}
+
+int espn_gpu_gather_rows(espn_gpu_table* t, const uint32_t* ids, uint64_t n, const uint64_t* out_row_ptr,
+                         uint16_t* out_rows, void* stream_v) {
+  if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
+  if (n == 0) return ESPN_OK;
+  if (!ids || !out_row_ptr || !out_rows) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  DeviceGuard g(t->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream_v);
+  const int cb = t->num_sms * 8;
+  switch (t->d) {
+#define ESPN_G(DD) case DD: gather_copy_kernel<DD><<<cb, 256, 0, s>>>(t->rows, t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, out_rows); break;
+    ESPN_G(8) ESPN_G(16) ESPN_G(32) ESPN_G(48) ESPN_G(64) ESPN_G(96) ESPN_G(128) ESPN_G(256)
+#undef ESPN_G
+    default: return fail(ESPN_E_INVALID_CONFIG, "gather supports d in {8,16,32,48,64,96,128,256}");
+  }
   ESPN_CUDA_TRY(cudaGetLastError());
   return ESPN_OK;
 }
 
 int espn_gpu_get_counters(const espn_gpu_workspace* w, espn_counters* out) {
   if (!w || !out) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  auto* wm = const_cast<espn_gpu_workspace*>(w);
+  for (int i = 0; i < espn_gpu_workspace::kProf; ++i) drain_prof(wm, i);
   *out = w->counters;
   return ESPN_OK;
 }
 
 int espn_gpu_synth_table(uint64_t n_docs, uint32_t d, uint32_t dtype, uint32_t t_min, uint32_t t_max,
-                         uint64_t seed, uint64_t* row_ptr, uint16_t* rows, void* stream_v) {
+                         uint64_t seed, uint32_t shard_count, uint32_t shard_index, uint64_t* row_ptr,
+                         uint16_t* rows, void* stream_v) {
   if (n_docs == 0 || t_min < 1 || t_max < t_min) return fail(ESPN_E_INVALID_INPUT, "bad synth shape");
   if (!row_ptr) return fail(ESPN_E_INVALID_INPUT, "null row_ptr");
+  if (shard_count < 1) shard_count = 1;
+  if (shard_index >= shard_count) return fail(ESPN_E_INVALID_INPUT, "shard_index >= shard_count");
   cudaStream_t s = static_cast<cudaStream_t>(stream_v);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   ESPN_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (!rows) {
-    synth_lengths_kernel<<<sms * 8, 256, 0, s>>>(n_docs, t_min, t_max, seed, row_ptr);
+    synth_lengths_kernel<<<sms * 8, 256, 0, s>>>(n_docs, t_min, t_max, seed, shard_count, shard_index, row_ptr);
     scan_u64_kernel<<<1, 1024, 0, s>>>(row_ptr, n_docs);
     ESPN_CUDA_TRY(cudaGetLastError());
     ESPN_CUDA_TRY(cudaStreamSynchronize(s));
     return ESPN_OK;
   }
-  uint64_t n_rows = 0;
-  ESPN_CUDA_TRY(cudaMemcpyAsync(&n_rows, row_ptr + n_docs, sizeof n_rows, cudaMemcpyDeviceToHost, s));
-  ESPN_CUDA_TRY(cudaStreamSynchronize(s));
   const uint64_t rseed = splitmix64(seed ^ 0x5EEDull);
   switch (d) {
-#define ESPN_S(DD) case DD: synth_rows_kernel<DD><<<sms * 16, 256, 0, s>>>(n_rows, rseed, dtype == ESPN_DTYPE_BF16, rows); break;
+#define ESPN_S(DD) case DD: synth_rows_kernel<DD><<<sms * 16, 256, 0, s>>>(n_docs, row_ptr, shard_count, shard_index, rseed, dtype == ESPN_DTYPE_BF16, rows); break;
     ESPN_S(16) ESPN_S(32) ESPN_S(64) ESPN_S(128)
 #undef ESPN_S
     default: return fail(ESPN_E_INVALID_INPUT, "synth supports d in {16,32,64,128}");

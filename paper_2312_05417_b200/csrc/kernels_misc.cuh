@@ -53,13 +53,13 @@ maxsim_simt_kernel(const MaxSimParams p, uint32_t pairs_per_warp, uint64_t n_pai
       if (bad && lane < p.nq) atomicOr(p.err, ERR_NONFINITE_QUERY);
     }
     const uint64_t c = p.cand_off[b] + (pr - p.unit_off[b]);
-    const uint32_t id = __ldg(&p.cand_ids[c]);
-    if (id >= p.n_docs) {
+    const uint64_t loc = shard_local(__ldg(&p.cand_ids[c]), p.shard_count, p.shard_index, p.n_docs);
+    if (loc == ~0ull) {
       if (lane == 0) atomicOr(p.err, ERR_UNKNOWN_DOC);
       continue;
     }
-    const uint64_t r0 = __ldg(&p.row_ptr[id]);
-    const uint32_t t = (uint32_t)(__ldg(&p.row_ptr[id + 1]) - r0);
+    const uint64_t r0 = __ldg(&p.row_ptr[loc]);
+    const uint32_t t = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
     const uint4* rows = reinterpret_cast<const uint4*>(p.rows + r0 * D);
     float m = -INFINITY;
     for (uint32_t j = 0; j < t; ++j) {
@@ -205,8 +205,8 @@ topk_kernel(const TopKParams p) {
 // K4: merge n_lists ranked lists per query ([list][query][k]) into one top-k.
 __global__ void __launch_bounds__(kTopkThreads)
 merge_topk_kernel(const uint32_t* ids, const float* scores, const uint32_t* counts,
-                  uint32_t n_lists, uint32_t n_queries, uint32_t k, uint32_t* out_ids,
-                  float* out_scores, uint32_t* out_counts) {
+                  uint32_t n_lists, uint64_t list_stride, uint32_t n_queries, uint32_t k,
+                  uint32_t* out_ids, float* out_scores, uint32_t* out_counts) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
   uint64_t* best = keys + kTopkSort;
@@ -214,8 +214,9 @@ merge_topk_kernel(const uint32_t* ids, const float* scores, const uint32_t* coun
   const uint64_t n = (uint64_t)n_lists * k;
   auto key_of = [&](uint64_t j) -> uint64_t {
     const uint32_t l = (uint32_t)(j / k), i = (uint32_t)(j % k);
-    const size_t o = ((size_t)l * n_queries + b) * k + i;
-    if (i >= counts[(size_t)l * n_queries + b]) return 0;
+    const size_t base = (size_t)l * list_stride;
+    const size_t o = base + (size_t)b * k + i;
+    if (i >= counts[base + b]) return 0;
     return make_key(scores[o], ids[o]);
   };
   int best_n = 0;
@@ -238,13 +239,14 @@ merge_topk_kernel(const uint32_t* ids, const float* scores, const uint32_t* coun
 // ============================================================================
 // K1 gather: request-order CSR of token rows.
 // ============================================================================
-__global__ void gather_count_kernel(const uint64_t* row_ptr, uint64_t n_docs, const uint32_t* ids,
-                                    uint64_t n, uint64_t* out_row_ptr, uint32_t* err) {
+__global__ void gather_count_kernel(const uint64_t* row_ptr, uint64_t n_docs, uint32_t shard_count,
+                                    uint32_t shard_index, const uint32_t* ids, uint64_t n,
+                                    uint64_t* out_row_ptr, uint32_t* err) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t id = ids[i];
+    const uint64_t loc = shard_local(ids[i], shard_count, shard_index, n_docs);
     uint64_t t = 0;
-    if (id < n_docs) t = row_ptr[id + 1] - row_ptr[id];
+    if (loc != ~0ull) t = row_ptr[loc + 1] - row_ptr[loc];
     else atomicOr(err, ERR_UNKNOWN_DOC);
     out_row_ptr[i + 1] = t;
   }
@@ -288,15 +290,16 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(uint64_t* a, uint64_t n)
 // Warp per doc, 16-byte vector copies, 4 in flight per lane.
 template <int D>
 __global__ void __launch_bounds__(256)
-gather_copy_kernel(const uint16_t* rows, const uint64_t* row_ptr, uint64_t n_docs,
-                   const uint32_t* ids, uint64_t n, const uint64_t* out_row_ptr, uint16_t* out_rows) {
+gather_copy_kernel(const uint16_t* rows, const uint64_t* row_ptr, uint64_t n_docs, uint32_t shard_count,
+                   uint32_t shard_index, const uint32_t* ids, uint64_t n, const uint64_t* out_row_ptr,
+                   uint16_t* out_rows) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
-    const uint32_t id = ids[i];
-    if (id >= n_docs) continue;
-    const uint64_t r0 = row_ptr[id];
-    const uint64_t nvec = (row_ptr[id + 1] - r0) * (D / 8);
+    const uint64_t loc = shard_local(ids[i], shard_count, shard_index, n_docs);
+    if (loc == ~0ull) continue;
+    const uint64_t r0 = row_ptr[loc];
+    const uint64_t nvec = (row_ptr[loc + 1] - r0) * (D / 8);
     const uint4* src = reinterpret_cast<const uint4*>(rows + r0 * D);
     uint4* dst = reinterpret_cast<uint4*>(out_rows + out_row_ptr[i] * D);
     uint64_t v = lane;
@@ -323,24 +326,34 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// Length of global doc `gid`: t_min + h % (t_max - t_min + 1).
 __global__ void synth_lengths_kernel(uint64_t n_docs, uint32_t t_min, uint32_t t_max, uint64_t seed,
-                                     uint64_t* row_ptr) {
+                                     uint32_t shard_count, uint32_t shard_index, uint64_t* row_ptr) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_docs;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t h = splitmix64(seed ^ (i * 0xD1B54A32D192ED03ull));
+    const uint64_t gid = i * shard_count + shard_index;
+    const uint64_t h = splitmix64(seed ^ (gid * 0xD1B54A32D192ED03ull));
     row_ptr[i + 1] = t_min + (uint32_t)(h % (uint64_t)(t_max - t_min + 1));
   }
 }
 
+// Warp per doc, lane per token row: value k of token j of global doc gid is
+// Box-Muller of h = splitmix64(base + (j << 16) + k), base = splitmix64(seed ^ gid*phi).
 template <int D>
-__global__ void synth_rows_kernel(uint64_t n_rows, uint64_t seed, uint32_t bf16, uint16_t* rows) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n_rows;
-       r += (uint64_t)gridDim.x * blockDim.x) {
+__global__ void synth_rows_kernel(uint64_t n_docs, const uint64_t* row_ptr, uint32_t shard_count,
+                                  uint32_t shard_index, uint64_t seed, uint32_t bf16, uint16_t* rows) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n_docs; i += nwarps)
+  for (uint64_t j = lane, r0 = row_ptr[i], t = row_ptr[i + 1] - r0; j < t; j += 32) {
+    const uint64_t gid = i * shard_count + shard_index;
+    const uint64_t base = splitmix64(seed ^ (gid * 0x9E3779B97F4A7C15ull));
+    const uint64_t r = r0 + j;
     float v[D];
     float ss = 0.0f;
 #pragma unroll
     for (int k = 0; k < D; k += 2) {
-      const uint64_t h = splitmix64(seed ^ splitmix64(r * (uint64_t)D + k));
+      const uint64_t h = splitmix64(base + (j << 16) + k);
       const float u1 = ((uint32_t)(h >> 40) + 1) * (1.0f / 16777217.0f);
       const float u2 = ((uint32_t)(h & 0xFFFFFFu)) * (1.0f / 16777216.0f);
       const float rad = sqrtf(-2.0f * logf(u1));

@@ -162,10 +162,11 @@ maxsim_tc_kernel(const MaxSimParams p) {
           uint32_t t = 0;
           uint64_t r0 = 0;
           if (k < nd) {
-            const uint32_t id = __ldg(&p.cand_ids[c0 + j0 + k]);
-            if (id < p.n_docs) {
-              r0 = __ldg(&p.row_ptr[id]);
-              t = (uint32_t)(__ldg(&p.row_ptr[id + 1]) - r0);
+            const uint64_t loc = shard_local(__ldg(&p.cand_ids[c0 + j0 + k]), p.shard_count,
+                                             p.shard_index, p.n_docs);
+            if (loc != ~0ull) {
+              r0 = __ldg(&p.row_ptr[loc]);
+              t = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
             } else {
               atomicOr(p.err, ERR_UNKNOWN_DOC);
             }

@@ -57,6 +57,48 @@ def make_queries(row_ptr, codes, d: int, n_queries: int, nq: int = 32, dtype: st
     return q, src
 
 
+# ---- host mirror of espn_gpu_synth_table (kernels_misc.cuh synth_*) -----------
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    x = np.asarray(x, np.uint64)
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def device_lengths(gids, t_min: int, t_max: int, seed: int) -> np.ndarray:
+    """Token counts the device generator gives global docs `gids` (exact)."""
+    g = np.asarray(gids, np.uint64)
+    with np.errstate(over="ignore"):
+        h = splitmix64(np.uint64(seed) ^ (g * np.uint64(0xD1B54A32D192ED03)))
+    return (np.uint64(t_min) + h % np.uint64(t_max - t_min + 1)).astype(np.int64)
+
+
+def device_rows(gid: int, t: int, d: int, seed: int, dtype: str = "f16") -> np.ndarray:
+    """Token rows (fp32 after dtype rounding) of global doc `gid` as the device
+    generator writes them, up to float rounding of log/sincos (<= 1 ulp)."""
+    rseed = splitmix64(np.asarray([np.uint64(seed) ^ np.uint64(0x5EED)]))[0]
+    with np.errstate(over="ignore"):
+        base = splitmix64(np.asarray([rseed ^ (np.uint64(gid) * np.uint64(0x9E3779B97F4A7C15))]))[0]
+        j = np.arange(t, dtype=np.uint64)[:, None]
+        k = np.arange(0, d, 2, dtype=np.uint64)[None, :]
+        h = splitmix64(base + (j << np.uint64(16)) + k)
+    u1 = (((h >> np.uint64(40)).astype(np.float64) + 1.0) * (1.0 / 16777217.0)).astype(np.float32)
+    u2 = ((h & np.uint64(0xFFFFFF)).astype(np.float64) * (1.0 / 16777216.0)).astype(np.float32)
+    rad = np.sqrt(-2.0 * np.log(u1.astype(np.float64)))
+    ang = np.pi * (2.0 * u2.astype(np.float64))
+    v = np.empty((t, d), np.float32)
+    v[:, 0::2] = rad * np.cos(ang)
+    v[:, 1::2] = rad * np.sin(ang)
+    v /= np.sqrt((v.astype(np.float64) ** 2).sum(axis=1, keepdims=True)).astype(np.float32)
+    codes = flush_subnormals(encode(v.ravel(), dtype), dtype)
+    return decode(codes, dtype).reshape(t, d)
+
+
 def make_candidates(n_docs: int, n_queries: int, k: int, src=None, seed: int = 11):
     """CSR candidate lists: (ids u32, cls f32, offsets u64)."""
     rng = np.random.default_rng(seed)

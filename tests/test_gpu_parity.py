@@ -210,7 +210,16 @@ def test_merge_topk(cuda_ok):
     os_ = torch.zeros((B, k), dtype=torch.float32, device=dev)
     oc = torch.zeros(B, dtype=torch.int32, device=dev)
     ti, ts, tc = t(ids), t(sc), t(cnt)
-    rc = L.lib().espn_gpu_merge_topk(ti.data_ptr(), ts.data_ptr(), tc.data_ptr(), G, B, k, oi.data_ptr(),
+    # separate arrays: list stride B*k for ids/scores, B for counts -> use a packed
+    # buffer [ids | scores | counts] per list like the bench's all-gather does
+    P = 2 * B * k + B
+    packed = np.zeros((G, P), np.uint32)
+    packed[:, :B * k] = ids.reshape(G, -1)
+    packed[:, B * k:2 * B * k] = sc.reshape(G, -1).view(np.uint32)
+    packed[:, 2 * B * k:] = cnt
+    tp = t(packed)
+    base = tp.data_ptr()
+    rc = L.lib().espn_gpu_merge_topk(base, base + 4 * B * k, base + 8 * B * k, G, P, B, k, oi.data_ptr(),
                                      os_.data_ptr(), oc.data_ptr(), None)
     assert rc == 0
     torch.cuda.synchronize()
@@ -240,13 +249,19 @@ def test_api_mirror_rerank_candidates(oracle, cuda_ok):
 def test_synth_table_on_device(cuda_ok):
     import torch
     from paper_2312_05417_b200 import _lib as L
-    n, d = 10000, 32
+    n, d, G, g = 10000, 32, 3, 1
     rp = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
-    assert L.lib().espn_gpu_synth_table(n, d, 0, 1, 63, 42, rp.data_ptr(), None, None) == 0
+    assert L.lib().espn_gpu_synth_table(n, d, 0, 1, 63, 42, G, g, rp.data_ptr(), None, None) == 0
     t = torch.diff(rp).cpu().numpy()
     assert t.min() >= 1 and t.max() <= 63 and abs(t.mean() - 32) < 1.5
+    gids = np.arange(n) * G + g  # shard g of 3: keyed by global id
+    assert np.array_equal(t, synth.device_lengths(gids, 1, 63, 42))
     rows = torch.zeros(int(rp[-1]) * d, dtype=torch.int16, device="cuda")
-    assert L.lib().espn_gpu_synth_table(n, d, 0, 1, 63, 42, rp.data_ptr(), rows.data_ptr(), None) == 0
+    assert L.lib().espn_gpu_synth_table(n, d, 0, 1, 63, 42, G, g, rp.data_ptr(), rows.data_ptr(), None) == 0
+    host = synth.device_rows(int(gids[7]), int(t[7]), d, 42)
+    a = int(rp[7])
+    dev7 = rows[a * d:(a + int(t[7])) * d].cpu().numpy().view(np.float16).astype(np.float32).reshape(-1, d)
+    assert np.abs(dev7 - host).max() < 2e-3
     v = rows.cpu().numpy().view(np.float16).astype(np.float32).reshape(-1, d)
     nrm = np.linalg.norm(v, axis=1)
     assert np.all(np.isfinite(v)) and np.abs(nrm - 1).max() < 5e-3
