@@ -63,10 +63,18 @@ typedef struct espn_gpu_workspace espn_gpu_workspace;
 
 /* Table flags. */
 #define ESPN_TABLE_DEVICE_BORROWED 0x1u /* row_ptr/rows are device pointers owned by the caller */
+#define ESPN_TABLE_ROWS_TILED 0x2u      /* rows are already in the HBM tile layout,
+                                           e.g. written by espn_gpu_synth_table; otherwise rows are
+                                           plain row-major and the library tiles them at open (a
+                                           borrowed plain table gets a library-owned tiled copy) */
 
 /* The embedding table (store.hpp:13-35).  The HBM tier holds BOW rows only as
  * CSR: doc i's t_i token rows live at rows[row_ptr[i]*d .. row_ptr[i+1]*d),
- * 2-byte codes of `dtype`.  d_cls / value_width / alignment describe the
+ * 2-byte codes of `dtype`.  Callers pass plain row-major rows; in HBM the
+ * library keeps each document in the "tile layout" (d in {16,32,64,128}: K-panels
+ * of <=128-byte rows with the UMMA swizzle applied per document)
+ * so one bulk copy per document feeds the tensor cores.  Every read-back path
+ * (espn_gpu_gather) returns plain rows.  d_cls / value_width / alignment describe the
  * reference's on-disk record (record_bytes = (d_cls + t*d)*value_width) and are
  * used only for QueryStats byte accounting.  Replaces open_store()
  * (store.hpp:109-112) + the manifest (store.hpp:20-35). */
@@ -205,6 +213,7 @@ ESPN_API int espn_gpu_get_counters(const espn_gpu_workspace* ws, espn_counters* 
  * is counter-based and keyed by the GLOBAL doc id (and token index), so the
  * corpus is identical for every shard count and any doc can be regenerated
  * independently (paper_2312_05417_b200/synth.py mirrors it on the host).
+ * Rows are written in the HBM tile layout: open with ESPN_TABLE_ROWS_TILED.
  * Generates shard `shard_index` of `shard_count` (local doc i = global id
  * i*shard_count + shard_index) with n_local_docs docs.  Writes row_ptr
  * (n_local_docs+1) and rows (device pointers; rows must hold

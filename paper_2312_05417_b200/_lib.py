@@ -28,6 +28,7 @@ ESPN_KERNEL_TCGEN05 = 1
 ESPN_KERNEL_SIMT = 2
 
 ESPN_TABLE_DEVICE_BORROWED = 0x1
+ESPN_TABLE_ROWS_TILED = 0x2
 
 ESPN_RERANK_PARTIAL = 0x1
 ESPN_RERANK_DEVICE_IO = 0x2

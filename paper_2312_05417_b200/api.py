@@ -218,7 +218,8 @@ class GpuStore:
 
     def __init__(self, row_ptr, rows, d: int, dtype: str = "f16", d_cls: int = 128,
                  value_width: int = 2, alignment: int = 4096, device: int = 0,
-                 borrowed_device: bool = False, shard_count: int = 1, shard_index: int = 0):
+                 borrowed_device: bool = False, shard_count: int = 1, shard_index: int = 0,
+                 rows_tiled: bool = False):
         self.d = int(d)
         self.dtype = dtype
         self.d_cls = int(d_cls)
@@ -230,6 +231,8 @@ class GpuStore:
             n_docs = int(row_ptr.numel()) - 1
             self._row_ptr_host = None
             rp_p, rows_p, flags = _ptr(row_ptr), _ptr(rows), L.ESPN_TABLE_DEVICE_BORROWED
+            if rows_tiled:
+                flags |= L.ESPN_TABLE_ROWS_TILED
         else:
             row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
             rows = np.ascontiguousarray(rows, dtype=np.uint16)
@@ -258,7 +261,9 @@ class GpuStore:
 
     @classmethod
     def from_device(cls, row_ptr, rows, d: int, dtype: str = "f16", **kw) -> "GpuStore":
-        """Adopt CUDA tensors (torch) already resident in HBM (borrowed)."""
+        """Adopt CUDA tensors (torch) already resident in HBM (borrowed).  Pass
+        rows_tiled=True for rows already in the HBM tile layout (synth output);
+        plain rows get a library-owned tiled copy."""
         return cls(row_ptr, rows, d, dtype, borrowed_device=True, **kw)
 
     @property

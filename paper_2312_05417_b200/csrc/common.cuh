@@ -16,6 +16,33 @@ __device__ __forceinline__ uint64_t shard_local(uint32_t id, uint32_t count, uin
   return local < n_docs ? local : ~0ull;
 }
 
+// HBM tile layout of the table rows.  For the tensor-core dims
+// (d in {16, 32, 64, 128}) each document's t token rows are stored as
+// NP = max(1, 2d/128) K-panels of t rows x PW bytes (PW = min(2d, 128)), and
+// inside a panel the 16-byte chunks of row j are XOR-permuted by
+// sw(j) = ((j * PW) >> 7) & (PW/16 - 1) -- exactly the UMMA K-major
+// SWIZZLE_{32,64,128}B pattern of a row sitting at an 8-row-aligned shared
+// memory slot.  A document (or a panel of it) is therefore ONE contiguous
+// byte range that a single cp.async.bulk drops into the MMA operand layout.
+// Other dims keep plain row-major rows.  Doc boundaries come from row_ptr, so
+// the layout is doc-relative: row j of a doc is its j-th token.
+template <int D>
+struct RowLayout {
+  static constexpr bool TILED = (D == 16 || D == 32 || D == 64 || D == 128);
+  static constexpr int ROWB = 2 * D;
+  static constexpr int PW = TILED ? (ROWB < 128 ? ROWB : 128) : ROWB;
+  static constexpr int NP = ROWB / PW;
+  static constexpr int CPP = PW / 16;  // 16-byte chunks per panel row
+  static constexpr int CH = ROWB / 16; // 16-byte chunks per row
+  // byte offset (inside a doc of t rows) of 16-byte chunk c of row j
+  __host__ __device__ static __forceinline__ uint32_t off(uint32_t t, uint32_t j, uint32_t c) {
+    if (!TILED) return j * (uint32_t)ROWB + c * 16u;
+    const uint32_t p = c / CPP, cc = c % CPP;
+    const uint32_t sw = ((j * (uint32_t)PW) >> 7) & (uint32_t)(CPP - 1);
+    return (p * t + j) * (uint32_t)PW + ((cc ^ sw) << 4);
+  }
+};
+
 // Device-side error bits (mapped to espn_status by the host after sync).
 enum : uint32_t {
   ERR_UNKNOWN_DOC = 1u << 0,     // candidate id >= n_docs  -> DATA_INTEGRITY
@@ -36,7 +63,8 @@ struct MaxSimParams {
   const float* q32;            // B * nq * d fp32 query tokens
   const uint32_t* cand_ids;    // CSR over queries
   const uint64_t* cand_off;    // B + 1
-  const uint32_t* unit_off;    // B + 1: work units per query (prefix)
+  const uint32_t* unit_off;    // B + 1: SIMT path: per-query pair prefix
+  const uint4* unit_tab;       // tcgen05 path: per work unit {b, n_docs, first candidate (u64 lo, hi)}
   const uint32_t* needed;      // B: needed (scored with MaxSim) candidates per query
   float* bow_out;              // per candidate MaxSim score (first min(R, n_b) of each query)
   uint32_t* err;               // error bits
@@ -46,6 +74,7 @@ struct MaxSimParams {
   uint32_t unit_docs;          // docs per work unit (<= kUnitMax)
   uint32_t n_units;
   uint32_t bf16;               // table dtype
+  uint32_t dbg;                // profiling knobs (ESPN_DEBUG env; 0 in production)
 };
 
 struct TopKParams {

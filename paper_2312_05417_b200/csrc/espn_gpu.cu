@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -164,6 +165,24 @@ cudaError_t ensure_topk_attr() {
   return cudaSuccess;
 }
 
+bool layout_tiled(uint32_t d) { return d == 16 || d == 32 || d == 64 || d == 128; }
+
+// plain CSR rows (device) -> HBM tile layout (device), both n_tokens * d codes
+cudaError_t tile_rows(uint32_t d, const uint16_t* plain, const uint64_t* row_ptr, uint64_t n_docs,
+                      uint16_t* tiled, int num_sms) {
+  const int blocks = num_sms * 8;
+  switch (d) {
+    case 16: tile_rows_kernel<16><<<blocks, 256>>>(plain, row_ptr, n_docs, tiled); break;
+    case 32: tile_rows_kernel<32><<<blocks, 256>>>(plain, row_ptr, n_docs, tiled); break;
+    case 64: tile_rows_kernel<64><<<blocks, 256>>>(plain, row_ptr, n_docs, tiled); break;
+    case 128: tile_rows_kernel<128><<<blocks, 256>>>(plain, row_ptr, n_docs, tiled); break;
+    default: return cudaSuccess;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cudaDeviceSynchronize();
+}
+
 }  // namespace
 
 struct espn_gpu_table {
@@ -174,7 +193,8 @@ struct espn_gpu_table {
   uint32_t d = 0, dtype = 0, d_cls = 0, value_width = 2, alignment = 1;
   uint32_t max_t = 0, min_t = 0;
   uint32_t shard_count = 1, shard_index = 0;
-  bool owned = false;
+  bool owned = false;       // row_ptr owned
+  bool owned_rows = false;  // rows owned
   uint64_t* row_ptr = nullptr;
   uint16_t* rows = nullptr;
 };
@@ -188,6 +208,8 @@ struct espn_gpu_workspace {
   uint64_t* cand_off = nullptr;
   uint32_t* unit_off = nullptr;
   uint32_t* needed = nullptr;
+  uint4* unit_tab = nullptr;    // tcgen05 work units {b, n_docs, first candidate}
+  uint64_t max_units = 0;
   float* bow = nullptr;
   uint32_t* out_ids = nullptr;
   float* out_scores = nullptr;
@@ -201,6 +223,7 @@ struct espn_gpu_workspace {
     uint64_t* cand_off = nullptr;
     uint32_t* unit_off = nullptr;
     uint32_t* needed = nullptr;
+    uint4* unit_tab = nullptr;
     cudaEvent_t copied = nullptr;
     bool used = false;
   } slots[kSlots];
@@ -294,9 +317,20 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
       return fail(ESPN_E_CUDA, "cudaMalloc failed for the HBM table");
     }
     t->owned = true;
+    t->owned_rows = true;
     cudaMemcpy(t->row_ptr, rp, (desc->n_docs + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice);
-    cudaError_t e3 = cudaMemcpy(t->rows, desc->rows, t->n_tokens * t->d * sizeof(uint16_t),
-                                cudaMemcpyHostToDevice);
+    const size_t row_bytes = t->n_tokens * t->d * sizeof(uint16_t);
+    cudaError_t e3;
+    if (layout_tiled(t->d) && !(desc->flags & ESPN_TABLE_ROWS_TILED)) {
+      // upload plain rows to a staging buffer, then tile into the table
+      uint16_t* plain = nullptr;
+      e3 = cudaMalloc(&plain, std::max<size_t>(row_bytes, 16));
+      if (e3 == cudaSuccess) e3 = cudaMemcpy(plain, desc->rows, row_bytes, cudaMemcpyHostToDevice);
+      if (e3 == cudaSuccess) e3 = tile_rows(t->d, plain, t->row_ptr, t->n_docs, t->rows, t->num_sms);
+      cudaFree(plain);
+    } else {
+      e3 = cudaMemcpy(t->rows, desc->rows, row_bytes, cudaMemcpyHostToDevice);
+    }
     if (e3 != cudaSuccess) {
       espn_gpu_table_close(t);
       return fail(ESPN_E_CUDA, std::string("table upload: ") + cudaGetErrorString(e3));
@@ -323,6 +357,19 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
     t->min_t = (uint32_t)res[0];
     t->max_t = (uint32_t)std::min<unsigned long long>(res[1], UINT32_MAX);
     t->n_tokens = last;
+    if (layout_tiled(t->d) && !(desc->flags & ESPN_TABLE_ROWS_TILED)) {
+      // borrowed plain rows: the table keeps its own tiled copy
+      uint16_t* tiled = nullptr;
+      cudaError_t e4 = cudaMalloc(&tiled, std::max<size_t>(t->n_tokens * t->d * sizeof(uint16_t), 16));
+      if (e4 == cudaSuccess) e4 = tile_rows(t->d, t->rows, t->row_ptr, t->n_docs, tiled, t->num_sms);
+      if (e4 != cudaSuccess) {
+        cudaFree(tiled);
+        delete t;
+        return fail(ESPN_E_CUDA, std::string("table tiling: ") + cudaGetErrorString(e4));
+      }
+      t->rows = tiled;
+      t->owned_rows = true;
+    }
   }
   *out = t;
   return ESPN_OK;
@@ -331,10 +378,8 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
 int espn_gpu_table_close(espn_gpu_table* t) {
   if (!t) return ESPN_OK;
   DeviceGuard g(t->device);
-  if (t->owned) {
-    cudaFree(t->row_ptr);
-    cudaFree(t->rows);
-  }
+  if (t->owned) cudaFree(t->row_ptr);
+  if (t->owned_rows) cudaFree(t->rows);
   delete t;
   return ESPN_OK;
 }
@@ -347,7 +392,7 @@ int espn_gpu_table_info(const espn_gpu_table* t, espn_table_info* out) {
   out->dtype = t->dtype;
   out->max_tokens = t->max_t;
   out->min_tokens = t->min_t;
-  out->hbm_bytes = t->owned ? (t->n_docs + 1) * 8 + t->n_tokens * t->d * 2 : 0;
+  out->hbm_bytes = (t->owned ? (t->n_docs + 1) * 8 : 0) + (t->owned_rows ? t->n_tokens * t->d * 2 : 0);
   return ESPN_OK;
 }
 
@@ -376,6 +421,12 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   al((void**)&w->cand_off, (B + 1) * sizeof(uint64_t));
   al((void**)&w->unit_off, (B + 1) * sizeof(uint32_t));
   al((void**)&w->needed, B * sizeof(uint32_t));
+  // work-unit table capacity: every query may end in a partial unit
+  {
+    const int ud = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
+    w->max_units = ud > 0 ? (C + ud - 1) / ud + B : 0;
+  }
+  al((void**)&w->unit_tab, w->max_units * sizeof(uint4));
   al((void**)&w->bow, C * sizeof(float));
   al((void**)&w->out_ids, B * kMaxK * sizeof(uint32_t));
   al((void**)&w->out_scores, B * kMaxK * sizeof(float));
@@ -385,6 +436,7 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     if (e == cudaSuccess) e = cudaMallocHost(&sl.cand_off, (B + 1) * sizeof(uint64_t));
     if (e == cudaSuccess) e = cudaMallocHost(&sl.unit_off, (B + 1) * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMallocHost(&sl.needed, (B + 1) * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMallocHost(&sl.unit_tab, std::max<uint64_t>(w->max_units, 1) * sizeof(uint4));
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming);
   }
   for (auto& pr : w->prof)
@@ -403,11 +455,11 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   if (!w) return ESPN_OK;
   DeviceGuard g(w->table->device);
   cudaFree(w->q32); cudaFree(w->ids); cudaFree(w->cls); cudaFree(w->cand_off);
-  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
+  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
   cudaFree(w->out_counts); cudaFree(w->err);
   for (auto& sl : w->slots) {
     if (sl.copied) cudaEventSynchronize(sl.copied);
-    cudaFreeHost(sl.cand_off); cudaFreeHost(sl.unit_off); cudaFreeHost(sl.needed);
+    cudaFreeHost(sl.cand_off); cudaFreeHost(sl.unit_off); cudaFreeHost(sl.needed); cudaFreeHost(sl.unit_tab);
     if (sl.copied) cudaEventDestroy(sl.copied);
   }
   for (auto& pr : w->prof)
@@ -466,7 +518,16 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     sl.needed[b] = (uint32_t)need;
     sl.unit_off[b] = (uint32_t)acc;
     pairs += need;
-    acc += kern == ESPN_KERNEL_TCGEN05 ? (need + unit_docs - 1) / unit_docs : need;
+    if (kern == ESPN_KERNEL_TCGEN05) {
+      for (uint64_t j = 0; j < need; j += unit_docs) {
+        if (acc >= w->max_units) return fail(ESPN_E_INVALID_STATE, "work-unit table overflow");
+        const uint64_t c = off[b] + j;
+        sl.unit_tab[acc++] = make_uint4(b, (uint32_t)std::min<uint64_t>(unit_docs, need - j), (uint32_t)c,
+                                        (uint32_t)(c >> 32));
+      }
+    } else {
+      acc += need;
+    }
   }
   sl.cand_off[B] = off[B];
   sl.unit_off[B] = (uint32_t)acc;
@@ -481,6 +542,8 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   ESPN_CUDA_TRY(cudaMemcpyAsync(w->cand_off, sl.cand_off, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   ESPN_CUDA_TRY(cudaMemcpyAsync(w->unit_off, sl.unit_off, (B + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
   ESPN_CUDA_TRY(cudaMemcpyAsync(w->needed, sl.needed, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  if (kern == ESPN_KERNEL_TCGEN05 && acc)
+    ESPN_CUDA_TRY(cudaMemcpyAsync(w->unit_tab, sl.unit_tab, acc * sizeof(uint4), cudaMemcpyHostToDevice, s));
   ESPN_CUDA_TRY(cudaEventRecord(sl.copied, s));
   sl.used = true;
   ++w->calls;
@@ -507,6 +570,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   mp.cand_ids = ids;
   mp.cand_off = w->cand_off;
   mp.unit_off = w->unit_off;
+  mp.unit_tab = w->unit_tab;
   mp.needed = w->needed;
   mp.bow_out = w->bow;
   mp.err = w->err;
@@ -516,6 +580,13 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   mp.unit_docs = (uint32_t)std::max(unit_docs, 1);
   mp.n_units = (uint32_t)acc;
   mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
+  {
+    static const uint32_t dbg = [] {
+      const char* e = getenv("ESPN_DEBUG");
+      return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
+    }();
+    mp.dbg = dbg;
+  }
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
   cudaError_t e = kern == ESPN_KERNEL_TCGEN05 ? launch_tc_rt(t->d, mp, t->num_sms, s)
                                                : launch_simt_rt(t->d, mp, acc, t->num_sms, s);

@@ -60,13 +60,13 @@ maxsim_simt_kernel(const MaxSimParams p, uint32_t pairs_per_warp, uint64_t n_pai
     }
     const uint64_t r0 = __ldg(&p.row_ptr[loc]);
     const uint32_t t = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
-    const uint4* rows = reinterpret_cast<const uint4*>(p.rows + r0 * D);
+    const uint8_t* doc = reinterpret_cast<const uint8_t*>(p.rows + r0 * D);
     float m = -INFINITY;
     for (uint32_t j = 0; j < t; ++j) {
       float acc = 0.0f;
 #pragma unroll
       for (int k8 = 0; k8 < D / 8; ++k8) {
-        const uint4 v = __ldg(&rows[(size_t)j * (D / 8) + k8]);
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(doc + RowLayout<D>::off(t, j, k8)));
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -287,31 +287,53 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(uint64_t* a, uint64_t n)
   }
 }
 
-// Warp per doc, 16-byte vector copies, 4 in flight per lane.
+// Warp per doc, 16-byte vector copies, 4 in flight per lane.  Reads the HBM
+// tile layout (RowLayout) and writes plain row-major rows in request order.
 template <int D>
 __global__ void __launch_bounds__(256)
 gather_copy_kernel(const uint16_t* rows, const uint64_t* row_ptr, uint64_t n_docs, uint32_t shard_count,
                    uint32_t shard_index, const uint32_t* ids, uint64_t n, const uint64_t* out_row_ptr,
                    uint16_t* out_rows) {
+  using RL = RowLayout<D>;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
     const uint64_t loc = shard_local(ids[i], shard_count, shard_index, n_docs);
     if (loc == ~0ull) continue;
     const uint64_t r0 = row_ptr[loc];
-    const uint64_t nvec = (row_ptr[loc + 1] - r0) * (D / 8);
-    const uint4* src = reinterpret_cast<const uint4*>(rows + r0 * D);
+    const uint32_t t = (uint32_t)(row_ptr[loc + 1] - r0);
+    const uint32_t nvec = t * RL::CH;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(rows + r0 * D);
     uint4* dst = reinterpret_cast<uint4*>(out_rows + out_row_ptr[i] * D);
-    uint64_t v = lane;
+    auto at = [&](uint32_t v) {
+      return __ldcs(reinterpret_cast<const uint4*>(src + RL::off(t, v / RL::CH, v % RL::CH)));
+    };
+    uint32_t v = lane;
     for (; v + 96 < nvec; v += 128) {
-      const uint4 a0 = __ldcs(src + v), a1 = __ldcs(src + v + 32), a2 = __ldcs(src + v + 64),
-                  a3 = __ldcs(src + v + 96);
+      const uint4 a0 = at(v), a1 = at(v + 32), a2 = at(v + 64), a3 = at(v + 96);
       __stcs(dst + v, a0);
       __stcs(dst + v + 32, a1);
       __stcs(dst + v + 64, a2);
       __stcs(dst + v + 96, a3);
     }
-    for (; v < nvec; v += 32) __stcs(dst + v, __ldcs(src + v));
+    for (; v < nvec; v += 32) __stcs(dst + v, at(v));
+  }
+}
+
+// Plain row-major CSR rows -> HBM tile layout (table open).  Warp per doc.
+template <int D>
+__global__ void __launch_bounds__(256)
+tile_rows_kernel(const uint16_t* plain, const uint64_t* row_ptr, uint64_t n_docs, uint16_t* tiled) {
+  using RL = RowLayout<D>;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n_docs; i += nwarps) {
+    const uint64_t r0 = row_ptr[i];
+    const uint32_t t = (uint32_t)(row_ptr[i + 1] - r0);
+    const uint4* src = reinterpret_cast<const uint4*>(plain + r0 * D);
+    uint8_t* dst = reinterpret_cast<uint8_t*>(tiled + r0 * D);
+    for (uint32_t v = lane; v < t * RL::CH; v += 32)
+      *reinterpret_cast<uint4*>(dst + RL::off(t, v / RL::CH, v % RL::CH)) = __ldcs(src + v);
   }
 }
 
@@ -348,7 +370,6 @@ __global__ void synth_rows_kernel(uint64_t n_docs, const uint64_t* row_ptr, uint
   for (uint64_t j = lane, r0 = row_ptr[i], t = row_ptr[i + 1] - r0; j < t; j += 32) {
     const uint64_t gid = i * shard_count + shard_index;
     const uint64_t base = splitmix64(seed ^ (gid * 0x9E3779B97F4A7C15ull));
-    const uint64_t r = r0 + j;
     float v[D];
     float ss = 0.0f;
 #pragma unroll
@@ -379,10 +400,12 @@ __global__ void synth_rows_kernel(uint64_t n_docs, const uint64_t* row_ptr, uint
       }
       packed[k / 2] = (uint32_t)c0 | ((uint32_t)c1 << 16);
     }
-    uint4* dst = reinterpret_cast<uint4*>(rows + r * D);
+    // HBM tile layout (RowLayout): chunk k of row j of this doc
+    uint8_t* dst = reinterpret_cast<uint8_t*>(rows + r0 * D);
 #pragma unroll
     for (int k = 0; k < D / 8; ++k)
-      dst[k] = make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3]);
+      *reinterpret_cast<uint4*>(dst + RowLayout<D>::off((uint32_t)t, (uint32_t)j, k)) =
+          make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3]);
   }
 }
 

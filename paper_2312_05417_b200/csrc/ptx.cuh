@@ -24,14 +24,39 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware until
+// the phase completes (or the hint expires) instead of spinning on issue slots
+// shared with the compute warps of its SM sub-partition.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra LAB_WAIT;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
+}
+// Arrive and add `bytes` to the barrier's expected transaction count.
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                   smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA engine (UBLKCP); completion is
+// signalled as `bytes` transactions on `bar`.  16-byte aligned, size % 16 == 0.
+// L2 policy evict_first: table rows are streamed once per batch.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst_smem),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 // Arrive (without pending-count increment) once all prior cp.async of this
 // thread have landed in shared memory.
@@ -108,6 +133,22 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, float (&v)[32
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int W>
+__device__ __forceinline__ void tmem_ld_32x32b(uint32_t taddr, float (&v)[W]) {
+  if constexpr (W == 32) tmem_ld_32x32b_x32(taddr, v);
+  else tmem_ld_32x32b_x16(taddr, v);
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -123,6 +164,20 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lb
   d |= static_cast<uint64_t>(1) << 46;  // descriptor version 1 (sm_100)
   return d;
 }
+// UMMA shared-memory descriptor, K-major, swizzled (layout code: 2 = 128B,
+// 4 = 64B, 6 = 32B).  SBO = byte distance between 8-row groups (8 x row
+// pitch); LBO is unused for swizzled K-major operands.  K advance inside the
+// swizzle atom is a plain start-address offset (the swizzle is applied to
+// absolute address bits, so atoms must be 8-row aligned).
+__device__ __forceinline__ uint64_t umma_desc_sw(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(layout & 7u) << 61;
+  return d;
+}
 // Instruction descriptor for kind::f16: fp32 accumulate, A/B K-major,
 // a_fmt/b_fmt 0 = f16, 1 = bf16.
 __host__ __device__ __forceinline__ uint32_t umma_idesc_f16(uint32_t m, uint32_t n, uint32_t bf16) {
@@ -130,6 +185,22 @@ __host__ __device__ __forceinline__ uint32_t umma_idesc_f16(uint32_t m, uint32_t
 }
 
 // ---- numeric helpers ----------------------------------------------------------
+// (n > j) ? a : b as a forced SETP+SELP pair (keeps masked maxima branch-free;
+// plain ternaries on a runtime count get compiled into decision trees).
+__device__ __forceinline__ float sel_gt(uint32_t n, uint32_t j, float a, float b) {
+  float r;
+  asm("{\n\t.reg .pred q;\n\tsetp.gt.u32 q, %1, %2;\n\tselp.f32 %0, %3, %4, q;\n\t}"
+      : "=f"(r)
+      : "r"(n), "r"(j), "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+// Order-preserving float <-> int key (non-NaN): signed int compare == float compare.
+__device__ __forceinline__ int ord_key(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float key_ord(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7FFFFFFF); }
 __device__ __forceinline__ uint16_t f32_to_code(float x, uint32_t bf16) {
   if (bf16) return __bfloat16_as_ushort(__float2bfloat16_rn(x));
   return __half_as_ushort(__float2half_rn(x));

@@ -124,3 +124,34 @@ def make_candidates(n_docs: int, n_queries: int, k: int, src=None, seed: int = 1
         cls[b] = s[order]
     off = np.arange(n_queries + 1, dtype=np.uint64) * k
     return ids.ravel(), cls.ravel(), off
+
+
+# ---- host mirror of the HBM tile layout (common.cuh RowLayout) ----------------
+def tile_chunk_offsets(t: int, d: int) -> np.ndarray:
+    """[t, 2d/16] byte offsets, inside a doc of t rows, of each 16-byte chunk of
+    each plain row in the HBM tile layout (identity for non-tensor-core dims)."""
+    rowb = 2 * d
+    ch = rowb // 16
+    j = np.arange(t, dtype=np.int64)[:, None]
+    c = np.arange(ch, dtype=np.int64)[None, :]
+    if d not in (16, 32, 64, 128):
+        return j * rowb + c * 16
+    pw = min(rowb, 128)
+    cpp = pw // 16
+    p, cc = c // cpp, c % cpp
+    sw = ((j * pw) >> 7) & (cpp - 1)
+    return (p * t + j) * pw + ((cc ^ sw) << 4)
+
+
+def untile_rows(row_ptr, tiled_codes, d: int) -> np.ndarray:
+    """HBM tile layout -> plain row-major codes (test helper)."""
+    b = np.asarray(tiled_codes, np.uint16).view(np.uint8)
+    out = np.empty_like(b)
+    rp = np.asarray(row_ptr, np.int64)
+    rowb = 2 * d
+    for i in range(rp.shape[0] - 1):
+        a, t = int(rp[i]) * rowb, int(rp[i + 1] - rp[i])
+        off = tile_chunk_offsets(t, d).ravel()
+        chunks = np.stack([b[a + o:a + o + 16] for o in off]) if t else np.zeros((0, 16), np.uint8)
+        out[a:a + t * rowb] = chunks.ravel()
+    return out.view(np.uint16)

@@ -260,7 +260,10 @@ def test_synth_table_on_device(cuda_ok):
     assert L.lib().espn_gpu_synth_table(n, d, 0, 1, 63, 42, G, g, rp.data_ptr(), rows.data_ptr(), None) == 0
     host = synth.device_rows(int(gids[7]), int(t[7]), d, 42)
     a = int(rp[7])
-    dev7 = rows[a * d:(a + int(t[7])) * d].cpu().numpy().view(np.float16).astype(np.float32).reshape(-1, d)
+    # the generator writes the HBM tile layout; untile doc 7 on the host
+    doc7 = rows[a * d:(a + int(t[7])) * d].cpu().numpy().view(np.uint16)
+    doc7 = synth.untile_rows(np.array([0, int(t[7])]), doc7, d)
+    dev7 = doc7.view(np.float16).astype(np.float32).reshape(-1, d)
     assert np.abs(dev7 - host).max() < 2e-3
     v = rows.cpu().numpy().view(np.float16).astype(np.float32).reshape(-1, d)
     nrm = np.linalg.norm(v, axis=1)
