@@ -119,7 +119,9 @@ typedef struct {
   uint32_t max_queries;
   uint32_t max_candidates;
   uint32_t max_query_tokens; /* <= 32 */
-  uint32_t reserved[5];
+  uint32_t max_list;         /* longest candidate list of a query (sizes the top-k duplicate
+                                check when offsets are device-resident); 0 = min(max_candidates, 4096) */
+  uint32_t reserved[4];
 } espn_workspace_desc;
 
 ESPN_API int espn_gpu_workspace_create(espn_gpu_table* table, const espn_workspace_desc* desc,
@@ -133,6 +135,10 @@ ESPN_API int espn_gpu_workspace_destroy(espn_gpu_workspace* ws);
 #define ESPN_RERANK_WRITE_BOW 0x8u    /* also return per-candidate MaxSim (bow) scores */
 #define ESPN_RERANK_PROFILE 0x10u     /* time the MaxSim and top-k kernels with CUDA events on
                                          `stream` (accumulated into espn_counters) */
+#define ESPN_RERANK_DEVICE_OFFSETS 0x20u /* cand_offsets / needed_counts are DEVICE pointers (needs
+                                         DEVICE_IO): the batch is planned on the device, the call has
+                                         no host-side loop, no host sync with ASYNC, and is CUDA-graph
+                                         capturable; validation errors surface at sync */
 
 /* One batch of queries with their final candidate lists (ivf.hpp:45-50:
  * sorted (cls_score desc, doc_id asc), deduplicated), CSR over queries.
@@ -146,7 +152,7 @@ typedef struct {
   const float* query_tokens;     /* B * q * d fp32, row-major */
   const uint32_t* cand_ids;      /* cand_offsets[B] entries */
   const float* cand_cls;         /* cls_score per candidate */
-  const uint64_t* cand_offsets;  /* B + 1; always a HOST pointer */
+  const uint64_t* cand_offsets;  /* B + 1; HOST pointer unless ESPN_RERANK_DEVICE_OFFSETS */
   uint32_t rerank_count;         /* R */
   uint32_t final_k;              /* k (>= 1) */
   float alpha;                   /* CLS scaling (aggregate_score) */

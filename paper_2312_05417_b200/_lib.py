@@ -35,6 +35,7 @@ ESPN_RERANK_DEVICE_IO = 0x2
 ESPN_RERANK_ASYNC = 0x4
 ESPN_RERANK_WRITE_BOW = 0x8
 ESPN_RERANK_PROFILE = 0x10
+ESPN_RERANK_DEVICE_OFFSETS = 0x20
 
 
 class TableDesc(C.Structure):
@@ -58,7 +59,7 @@ class TableInfo(C.Structure):
 class WorkspaceDesc(C.Structure):
     _fields_ = [
         ("max_queries", C.c_uint32), ("max_candidates", C.c_uint32),
-        ("max_query_tokens", C.c_uint32), ("reserved", C.c_uint32 * 5),
+        ("max_query_tokens", C.c_uint32), ("max_list", C.c_uint32), ("reserved", C.c_uint32 * 4),
     ]
 
 

@@ -50,7 +50,28 @@ enum : uint32_t {
   ERR_NONFINITE_CLS = 1u << 2,   // cls score not finite -> INVALID_INPUT
   ERR_DUPLICATE = 1u << 3,       // duplicate candidate id -> INVALID_INPUT (scoring.hpp:16-18)
   ERR_NONFINITE_SCORE = 1u << 4, // aggregate score not finite -> INVALID_INPUT
-  ERR_UNIT_TOO_LARGE = 1u << 5   // internal: slot budget of a work unit exceeded
+  ERR_UNIT_TOO_LARGE = 1u << 5,  // internal: slot budget of a work unit exceeded
+  ERR_BAD_OFFSETS = 1u << 6,     // cand_offsets not starting at 0 / decreasing -> INVALID_INPUT
+  ERR_CAPACITY = 1u << 7         // batch exceeds workspace capacity -> INVALID_INPUT
+};
+
+// Device-side batch planning (plan_kernel): per-query needed counts, work
+// units of the MaxSim kernel, all from device-resident candidate offsets, so
+// a whole re-rank batch is a fixed launch sequence (CUDA-graph capturable).
+struct PlanParams {
+  const uint64_t* cand_off;    // B + 1
+  const uint32_t* needed_in;   // optional B: per-query needed override (sharding)
+  uint32_t* needed;            // out B
+  uint32_t* unit_off;          // out B + 1: prefix of work units (SIMT: of pairs)
+  uint4* unit_tab;             // out: tcgen05 work units {b, n_docs, first candidate lo, hi}
+  uint32_t* n_units;           // out: total work units
+  uint32_t* err;
+  uint64_t max_candidates;
+  uint64_t max_units;
+  uint32_t n_queries;
+  uint32_t rerank_count;
+  uint32_t unit_docs;          // docs per unit (tcgen05); 1 for SIMT (units = pairs)
+  uint32_t write_tab;          // 1: tcgen05 (fill unit_tab)
 };
 
 // One batch of (query, candidate list) pairs, resident on the device.
@@ -72,7 +93,7 @@ struct MaxSimParams {
   uint32_t nq;                 // query tokens, 1..32
   uint32_t rerank_count;       // R
   uint32_t unit_docs;          // docs per work unit (<= kUnitMax)
-  uint32_t n_units;
+  const uint32_t* n_units;     // device: total work units (written by plan_kernel)
   uint32_t bf16;               // table dtype
   uint32_t dbg;                // profiling knobs (ESPN_DEBUG env; 0 in production)
 };
@@ -92,6 +113,7 @@ struct TopKParams {
   uint32_t k;
   uint32_t partial;            // tail beyond R scored alpha * cls
   float alpha;
+  uint32_t dbg;                // profiling knobs (ESPN_DEBUG env; 0 in production)
 };
 
 }  // namespace espn_k

@@ -43,6 +43,8 @@ int err_bits_to_status(uint32_t bits) {
   if (bits & ERR_DUPLICATE) m += " duplicate candidate doc id;";
   if (bits & ERR_NONFINITE_SCORE) m += " non-finite aggregate score;";
   if (bits & ERR_UNIT_TOO_LARGE) m += " internal: work unit slot budget exceeded;";
+  if (bits & ERR_BAD_OFFSETS) m += " cand_offsets must start at 0 and be non-decreasing;";
+  if (bits & ERR_CAPACITY) m += " batch exceeds workspace capacity;";
   g_last_error = m;
   if (bits & ERR_UNKNOWN_DOC) return ESPN_E_DATA_INTEGRITY;
   if (bits & ERR_UNIT_TOO_LARGE) return ESPN_E_INVALID_STATE;
@@ -102,9 +104,8 @@ cudaError_t launch_tc(const MaxSimParams& p, int num_sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int grid = (int)std::min<uint32_t>(p.n_units, (uint32_t)num_sms);
-  if (grid == 0) return cudaSuccess;
-  maxsim_tc_kernel<D><<<grid, L::NTHREADS, L::SMEM_BYTES, s>>>(p);
+  // persistent: one CTA per SM; the unit count is read on the device
+  maxsim_tc_kernel<D><<<num_sms, L::NTHREADS, L::SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -119,26 +120,20 @@ cudaError_t launch_tc_rt(uint32_t d, const MaxSimParams& p, int num_sms, cudaStr
 }
 
 template <int D>
-cudaError_t launch_simt(const MaxSimParams& p, uint64_t n_pairs, int num_sms, cudaStream_t s) {
-  if (n_pairs == 0) return cudaSuccess;
-  const uint64_t warps_wanted = (uint64_t)num_sms * 64;  // 8 blocks x 8 warps per SM
-  uint32_t ppw = (uint32_t)std::max<uint64_t>(1, (n_pairs + warps_wanted - 1) / warps_wanted);
-  const uint64_t warps = (n_pairs + ppw - 1) / ppw;
-  const uint64_t blocks = (warps * 32 + 255) / 256;
-  maxsim_simt_kernel<D><<<(unsigned)blocks, 256, 0, s>>>(p, ppw, n_pairs);
+cudaError_t launch_simt(const MaxSimParams& p, int num_sms, cudaStream_t s) {
+  maxsim_simt_kernel<D><<<num_sms * 8, 256, 0, s>>>(p);  // 64 warps per SM, grid-stride
   return cudaGetLastError();
 }
 
-cudaError_t launch_simt_rt(uint32_t d, const MaxSimParams& p, uint64_t n_pairs, int num_sms,
-                           cudaStream_t s) {
+cudaError_t launch_simt_rt(uint32_t d, const MaxSimParams& p, int num_sms, cudaStream_t s) {
   switch (d) {
-    case 8: return launch_simt<8>(p, n_pairs, num_sms, s);
-    case 16: return launch_simt<16>(p, n_pairs, num_sms, s);
-    case 32: return launch_simt<32>(p, n_pairs, num_sms, s);
-    case 48: return launch_simt<48>(p, n_pairs, num_sms, s);
-    case 64: return launch_simt<64>(p, n_pairs, num_sms, s);
-    case 96: return launch_simt<96>(p, n_pairs, num_sms, s);
-    case 128: return launch_simt<128>(p, n_pairs, num_sms, s);
+    case 8: return launch_simt<8>(p, num_sms, s);
+    case 16: return launch_simt<16>(p, num_sms, s);
+    case 32: return launch_simt<32>(p, num_sms, s);
+    case 48: return launch_simt<48>(p, num_sms, s);
+    case 64: return launch_simt<64>(p, num_sms, s);
+    case 96: return launch_simt<96>(p, num_sms, s);
+    case 128: return launch_simt<128>(p, num_sms, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -210,6 +205,9 @@ struct espn_gpu_workspace {
   uint32_t* needed = nullptr;
   uint4* unit_tab = nullptr;    // tcgen05 work units {b, n_docs, first candidate}
   uint64_t max_units = 0;
+  uint32_t* needed_in = nullptr;  // staged needed_counts (host-offset mode)
+  uint32_t* n_units = nullptr;    // planned unit count (device)
+  uint32_t max_list = 0;          // longest candidate list the top-k hash is sized for
   float* bow = nullptr;
   uint32_t* out_ids = nullptr;
   float* out_scores = nullptr;
@@ -221,9 +219,7 @@ struct espn_gpu_workspace {
   static constexpr int kSlots = 8;
   struct Slot {
     uint64_t* cand_off = nullptr;
-    uint32_t* unit_off = nullptr;
     uint32_t* needed = nullptr;
-    uint4* unit_tab = nullptr;
     cudaEvent_t copied = nullptr;
     bool used = false;
   } slots[kSlots];
@@ -427,22 +423,24 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     w->max_units = ud > 0 ? (C + ud - 1) / ud + B : 0;
   }
   al((void**)&w->unit_tab, w->max_units * sizeof(uint4));
+  al((void**)&w->needed_in, B * sizeof(uint32_t));
+  al((void**)&w->n_units, sizeof(uint32_t));
+  w->max_list = desc->max_list ? desc->max_list : (uint32_t)std::min<size_t>(C, 4096);
   al((void**)&w->bow, C * sizeof(float));
   al((void**)&w->out_ids, B * kMaxK * sizeof(uint32_t));
   al((void**)&w->out_scores, B * kMaxK * sizeof(float));
   al((void**)&w->out_counts, B * sizeof(uint32_t));
-  al((void**)&w->err, sizeof(uint32_t));
+  al((void**)&w->err, 4 * sizeof(uint32_t));
   for (auto& sl : w->slots) {
     if (e == cudaSuccess) e = cudaMallocHost(&sl.cand_off, (B + 1) * sizeof(uint64_t));
-    if (e == cudaSuccess) e = cudaMallocHost(&sl.unit_off, (B + 1) * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMallocHost(&sl.needed, (B + 1) * sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMallocHost(&sl.unit_tab, std::max<uint64_t>(w->max_units, 1) * sizeof(uint4));
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming);
   }
   for (auto& pr : w->prof)
     for (auto& ev : pr.e)
       if (e == cudaSuccess) e = cudaEventCreate(&ev);
   if (e == cudaSuccess) e = cudaMallocHost(&w->h_err, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(w->err, 0, 4 * sizeof(uint32_t));
   if (e != cudaSuccess) {
     espn_gpu_workspace_destroy(w);
     return fail(ESPN_E_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
@@ -455,11 +453,11 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   if (!w) return ESPN_OK;
   DeviceGuard g(w->table->device);
   cudaFree(w->q32); cudaFree(w->ids); cudaFree(w->cls); cudaFree(w->cand_off);
-  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
+  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->needed_in); cudaFree(w->n_units); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
   cudaFree(w->out_counts); cudaFree(w->err);
   for (auto& sl : w->slots) {
     if (sl.copied) cudaEventSynchronize(sl.copied);
-    cudaFreeHost(sl.cand_off); cudaFreeHost(sl.unit_off); cudaFreeHost(sl.needed); cudaFreeHost(sl.unit_tab);
+    cudaFreeHost(sl.cand_off); cudaFreeHost(sl.needed);
     if (sl.copied) cudaEventDestroy(sl.copied);
   }
   for (auto& pr : w->prof)
@@ -487,14 +485,26 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   if (B == 0) return ESPN_OK;
   if (!a->cand_offsets || !a->query_tokens || !o->ids || !o->scores || !o->counts)
     return fail(ESPN_E_INVALID_INPUT, "null array argument");
-  const uint64_t* off = a->cand_offsets;
-  if (off[0] != 0) return fail(ESPN_E_INVALID_INPUT, "cand_offsets[0] must be 0");
-  for (uint32_t b = 0; b < B; ++b)
-    if (off[b + 1] < off[b]) return fail(ESPN_E_INVALID_INPUT, "cand_offsets must be non-decreasing");
-  const uint64_t C = off[B];
-  if (C > w->max_candidates) return fail(ESPN_E_INVALID_INPUT, "candidates exceed workspace capacity");
-  if (C > 0 && (!a->cand_ids || !a->cand_cls)) return fail(ESPN_E_INVALID_INPUT, "null candidate arrays");
   const bool dev_io = (a->flags & ESPN_RERANK_DEVICE_IO) != 0;
+  const bool dev_off = (a->flags & ESPN_RERANK_DEVICE_OFFSETS) != 0;
+  if (dev_off && !dev_io) return fail(ESPN_E_INVALID_INPUT, "DEVICE_OFFSETS requires DEVICE_IO");
+  uint64_t C = 0;          // total candidates (host-offset mode only)
+  uint64_t max_list = 0;   // longest scored list (hash sizing)
+  if (!dev_off) {
+    const uint64_t* off = a->cand_offsets;
+    if (off[0] != 0) return fail(ESPN_E_INVALID_INPUT, "cand_offsets[0] must be 0");
+    for (uint32_t b = 0; b < B; ++b) {
+      if (off[b + 1] < off[b]) return fail(ESPN_E_INVALID_INPUT, "cand_offsets must be non-decreasing");
+      const uint64_t n = off[b + 1] - off[b];
+      const uint64_t need = std::min<uint64_t>(n, a->needed_counts ? a->needed_counts[b] : a->rerank_count);
+      max_list = std::max<uint64_t>(max_list, partial ? n : need);
+    }
+    C = off[B];
+    if (C > w->max_candidates) return fail(ESPN_E_INVALID_INPUT, "candidates exceed workspace capacity");
+    if (C > 0 && (!a->cand_ids || !a->cand_cls)) return fail(ESPN_E_INVALID_INPUT, "null candidate arrays");
+  } else {
+    max_list = w->max_list;  // device offsets: the workspace's declared bound
+  }
   DeviceGuard g(t->device);
 
   // ---- kernel choice (tcgen05 when the dim has a tensor-core tiling) ----
@@ -505,48 +515,39 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     return fail(ESPN_E_INVALID_CONFIG, "tcgen05 MaxSim needs an sm_100 device, d in {16,32,64,128} and docs <= 4096 tokens");
   if (kern == ESPN_KERNEL_SIMT && !simt_supported(t->d))
     return fail(ESPN_E_INVALID_CONFIG, "CUDA-core MaxSim supports d in {8,16,32,48,64,96,128}");
+  const bool tc = kern == ESPN_KERNEL_TCGEN05;
 
-  // ---- per-query work units (tcgen05) or pair prefix (SIMT), host-built ----
-  auto& sl = w->slots[w->calls % espn_gpu_workspace::kSlots];
-  if (sl.used) ESPN_CUDA_TRY(cudaEventSynchronize(sl.copied));  // slot's previous H2D done
-  uint64_t acc = 0, pairs = 0;
-  for (uint32_t b = 0; b < B; ++b) {
-    sl.cand_off[b] = off[b];
-    const uint64_t n = off[b + 1] - off[b];
-    const uint64_t need = a->needed_counts ? std::min<uint64_t>(n, a->needed_counts[b])
-                                           : std::min<uint64_t>(n, a->rerank_count);
-    sl.needed[b] = (uint32_t)need;
-    sl.unit_off[b] = (uint32_t)acc;
-    pairs += need;
-    if (kern == ESPN_KERNEL_TCGEN05) {
-      for (uint64_t j = 0; j < need; j += unit_docs) {
-        if (acc >= w->max_units) return fail(ESPN_E_INVALID_STATE, "work-unit table overflow");
-        const uint64_t c = off[b] + j;
-        sl.unit_tab[acc++] = make_uint4(b, (uint32_t)std::min<uint64_t>(unit_docs, need - j), (uint32_t)c,
-                                        (uint32_t)(c >> 32));
-      }
-    } else {
-      acc += need;
-    }
-  }
-  sl.cand_off[B] = off[B];
-  sl.unit_off[B] = (uint32_t)acc;
-  if (acc > UINT32_MAX) return fail(ESPN_E_INVALID_INPUT, "batch too large");
+  static const uint32_t dbg = [] {
+    const char* e = getenv("ESPN_DEBUG");
+    return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
+  }();
   const bool profile = (a->flags & ESPN_RERANK_PROFILE) != 0;
   const int pslot = (int)(w->prof_calls % espn_gpu_workspace::kProf);
   if (profile) drain_prof(w, pslot);
 
+  // ---- inputs -> device ----
+  const uint64_t* cand_off = a->cand_offsets;
+  const uint32_t* needed_in = a->needed_counts;
   const float* q32 = a->query_tokens;
   const uint32_t* ids = a->cand_ids;
   const float* cls = a->cand_cls;
-  ESPN_CUDA_TRY(cudaMemcpyAsync(w->cand_off, sl.cand_off, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-  ESPN_CUDA_TRY(cudaMemcpyAsync(w->unit_off, sl.unit_off, (B + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-  ESPN_CUDA_TRY(cudaMemcpyAsync(w->needed, sl.needed, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-  if (kern == ESPN_KERNEL_TCGEN05 && acc)
-    ESPN_CUDA_TRY(cudaMemcpyAsync(w->unit_tab, sl.unit_tab, acc * sizeof(uint4), cudaMemcpyHostToDevice, s));
-  ESPN_CUDA_TRY(cudaEventRecord(sl.copied, s));
-  sl.used = true;
-  ++w->calls;
+  if (!dev_off) {
+    // stage the small per-batch tables in a pinned slot (ring: an ASYNC caller
+    // may enqueue batch n+1 before batch n's copies ran)
+    auto& sl = w->slots[w->calls % espn_gpu_workspace::kSlots];
+    if (sl.used) ESPN_CUDA_TRY(cudaEventSynchronize(sl.copied));
+    std::memcpy(sl.cand_off, a->cand_offsets, (B + 1) * sizeof(uint64_t));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(w->cand_off, sl.cand_off, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    if (a->needed_counts) {
+      std::memcpy(sl.needed, a->needed_counts, B * sizeof(uint32_t));
+      ESPN_CUDA_TRY(cudaMemcpyAsync(w->needed_in, sl.needed, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      needed_in = w->needed_in;
+    }
+    ESPN_CUDA_TRY(cudaEventRecord(sl.copied, s));
+    sl.used = true;
+    ++w->calls;
+    cand_off = w->cand_off;
+  }
   if (!dev_io) {
     ESPN_CUDA_TRY(cudaMemcpyAsync(w->q32, q32, (size_t)B * nq * t->d * sizeof(float), cudaMemcpyHostToDevice, s));
     if (C) {
@@ -557,9 +558,28 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     ids = w->ids;
     cls = w->cls;
   }
-  // the device error word is sticky across un-synced ASYNC batches
-  if (!w->async_pending) ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
+  // the device error word is sticky across un-synced ASYNC batches; it is
+  // read and cleared by the synchronising call (or espn_gpu_workspace_sync)
 
+  // ---- K0: batch plan on the device ----
+  PlanParams pp{};
+  pp.cand_off = cand_off;
+  pp.needed_in = needed_in;
+  pp.needed = w->needed;
+  pp.unit_off = w->unit_off;
+  pp.unit_tab = w->unit_tab;
+  pp.n_units = w->n_units;
+  pp.err = w->err;
+  pp.max_candidates = w->max_candidates;
+  pp.max_units = tc ? w->max_units : ~0ull;
+  pp.n_queries = B;
+  pp.rerank_count = a->rerank_count;
+  pp.unit_docs = tc ? (uint32_t)unit_docs : 1u;
+  pp.write_tab = tc ? 1u : 0u;
+  plan_kernel<<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp);
+  ESPN_CUDA_TRY(cudaGetLastError());
+
+  // ---- K2: MaxSim ----
   MaxSimParams mp{};
   mp.rows = t->rows;
   mp.row_ptr = t->row_ptr;
@@ -568,7 +588,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   mp.shard_index = t->shard_index;
   mp.q32 = q32;
   mp.cand_ids = ids;
-  mp.cand_off = w->cand_off;
+  mp.cand_off = cand_off;
   mp.unit_off = w->unit_off;
   mp.unit_tab = w->unit_tab;
   mp.needed = w->needed;
@@ -578,27 +598,21 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   mp.nq = nq;
   mp.rerank_count = a->rerank_count;
   mp.unit_docs = (uint32_t)std::max(unit_docs, 1);
-  mp.n_units = (uint32_t)acc;
+  mp.n_units = w->n_units;
   mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
-  {
-    static const uint32_t dbg = [] {
-      const char* e = getenv("ESPN_DEBUG");
-      return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
-    }();
-    mp.dbg = dbg;
-  }
+  mp.dbg = dbg;
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
-  cudaError_t e = kern == ESPN_KERNEL_TCGEN05 ? launch_tc_rt(t->d, mp, t->num_sms, s)
-                                               : launch_simt_rt(t->d, mp, acc, t->num_sms, s);
+  cudaError_t e = tc ? launch_tc_rt(t->d, mp, t->num_sms, s) : launch_simt_rt(t->d, mp, t->num_sms, s);
   if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[1], s));
 
+  // ---- K3: aggregate + top-k ----
   ESPN_CUDA_TRY(ensure_topk_attr());
   TopKParams tp{};
   tp.bow = w->bow;
   tp.cand_ids = ids;
   tp.cand_cls = cls;
-  tp.cand_off = w->cand_off;
+  tp.cand_off = cand_off;
   tp.needed = w->needed;
   tp.out_ids = dev_io ? o->ids : w->out_ids;
   tp.out_scores = dev_io ? o->scores : w->out_scores;
@@ -609,8 +623,38 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   tp.k = k;
   tp.partial = partial ? 1u : 0u;
   tp.alpha = a->alpha;
-  topk_kernel<<<B, kTopkThreads, topk_smem_bytes(), s>>>(tp);
-  ESPN_CUDA_TRY(cudaGetLastError());
+  tp.dbg = dbg;
+  {
+    // CTA-per-query fast path when final_k <= 32 and the dedup hash fits;
+    // launched as a programmatic dependent of MaxSim (its id-only dedup
+    // prologue overlaps the MaxSim tail)
+    uint32_t hs = 64;
+    while (hs < 2 * max_list) hs <<= 1;
+    if (k <= 32 && hs <= 8192) {
+      const size_t smem = (size_t)hs * 8 + 8 * 32 * 8;
+      static bool attr = false;
+      if (!attr) {
+        ESPN_CUDA_TRY(cudaFuncSetAttribute(topk_cta_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8 + 8 * 32 * 8));
+        ESPN_CUDA_TRY(cudaFuncSetAttribute(topk_cta_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8 + 8 * 32 * 8));
+        attr = true;
+      }
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(B);
+      lc.blockDim = dim3(kTopkCtaThreads);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      ESPN_CUDA_TRY(k <= 16 ? cudaLaunchKernelEx(&lc, topk_cta_kernel<16>, tp, hs)
+                            : cudaLaunchKernelEx(&lc, topk_cta_kernel<32>, tp, hs));
+    } else {
+      topk_kernel<<<B, kTopkThreads, topk_smem_bytes(), s>>>(tp);
+      ESPN_CUDA_TRY(cudaGetLastError());
+    }
+  }
   if (profile) {
     ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[2], s));
     w->prof[pslot].pending = true;
@@ -622,20 +666,22 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->scores, w->out_scores, (size_t)B * k * sizeof(float), cudaMemcpyDeviceToHost, s));
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->counts, w->out_counts, (size_t)B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   }
-  if ((a->flags & ESPN_RERANK_WRITE_BOW) && o->bow_scores && C) {
-    ESPN_CUDA_TRY(cudaMemcpyAsync(o->bow_scores, w->bow, C * sizeof(float),
-                                  dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if ((a->flags & ESPN_RERANK_WRITE_BOW) && o->bow_scores) {
+    if (dev_off) return fail(ESPN_E_INVALID_INPUT, "WRITE_BOW needs host cand_offsets (total size)");
+    if (C)
+      ESPN_CUDA_TRY(cudaMemcpyAsync(o->bow_scores, w->bow, C * sizeof(float),
+                                    dev_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   }
   w->counters.batches += 1;
   w->counters.queries += B;
-  w->counters.pairs_scored += pairs;
-  w->counters.kernel_launches += 2;
+  w->counters.kernel_launches += 3;
   if (a->flags & ESPN_RERANK_ASYNC) {
     w->async_pending = true;
     return ESPN_OK;
   }
   ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
   w->async_pending = false;
   return err_bits_to_status(*w->h_err);
 }
@@ -646,6 +692,7 @@ int espn_gpu_workspace_sync(espn_gpu_workspace* w, void* stream_v) {
   cudaStream_t s = static_cast<cudaStream_t>(stream_v);
   ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
   w->async_pending = false;
   return err_bits_to_status(*w->h_err);
 }

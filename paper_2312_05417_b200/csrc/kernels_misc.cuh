@@ -22,14 +22,17 @@ namespace espn_k {
 // ============================================================================
 template <int D>
 __global__ void __launch_bounds__(256)
-maxsim_simt_kernel(const MaxSimParams p, uint32_t pairs_per_warp, uint64_t n_pairs_total) {
+maxsim_simt_kernel(const MaxSimParams p) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  uint64_t pr = gw * pairs_per_warp;
-  const uint64_t pr_end = min(pr + pairs_per_warp, n_pairs_total);
-  if (pr >= pr_end) return;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   // pairs are enumerated over needed candidates only: query b contributes
-  // min(R, n_b) pairs; unit_off carries the per-query pair prefix here.
+  // needed[b] pairs; unit_off (plan_kernel, unit_docs = 1) is the pair prefix.
+  const uint64_t n_pairs_total = p.unit_off[p.n_queries];
+  const uint64_t per = (n_pairs_total + nw - 1) / nw;  // contiguous range per warp
+  uint64_t pr = gw * per;
+  const uint64_t pr_end = min(pr + per, n_pairs_total);
+  if (pr >= pr_end) return;
   uint32_t lo = 0, hi = p.n_queries;
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
@@ -81,6 +84,88 @@ maxsim_simt_kernel(const MaxSimParams p, uint32_t pairs_per_warp, uint64_t n_pai
     float s = 0.0f;
     for (uint32_t i = 0; i < p.nq; ++i) s = __fadd_rn(s, __shfl_sync(0xffffffffu, m, i));
     if (lane == 0) p.bow_out[c] = s;
+  }
+}
+
+// ============================================================================
+// Batch plan (device side).  CTA c owns queries [256c, 256c+256): it sums the
+// work units of all earlier queries (block reduction over <= B offsets, cheap
+// next to the batch), scans its own, and writes needed[], unit_off[] and the
+// tcgen05 unit table.  Validates the offsets (start 0, non-decreasing, total
+// within the workspace); on error the plan is empty (n_units = 0) so no kernel
+// touches memory through a bad offset.
+// ============================================================================
+constexpr int kPlanThreads = 256;
+__device__ __forceinline__ uint64_t plan_units(const PlanParams& q, uint32_t b, uint32_t* need_out, bool* bad) {
+  const uint64_t a = q.cand_off[b], e = q.cand_off[b + 1];
+  if (e < a) { *bad = true; return 0; }
+  const uint64_t n = e - a;
+  const uint64_t cap = q.needed_in ? (uint64_t)q.needed_in[b] : (uint64_t)q.rerank_count;
+  const uint64_t need = n < cap ? n : cap;
+  *need_out = (uint32_t)need;
+  return q.write_tab ? (need + q.unit_docs - 1) / q.unit_docs : need;
+}
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q) {
+  __shared__ uint64_t wsum[kPlanThreads / 32];
+  __shared__ uint64_t base_sh;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t q0 = blockIdx.x * kPlanThreads;
+  bool bad = false;
+  uint32_t dummy;
+  // units of queries [0, q0)
+  uint64_t pre = 0;
+  for (uint32_t b = tid; b < q0; b += kPlanThreads) pre += plan_units(q, b, &dummy, &bad);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if (lane == 0) wsum[wid] = pre;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t t = 0;
+    for (int i = 0; i < kPlanThreads / 32; ++i) t += wsum[i];
+    base_sh = t;
+  }
+  __syncthreads();
+  const uint64_t base = base_sh;
+  // own query: exclusive block scan of its units
+  const uint32_t b = q0 + tid;
+  uint32_t need = 0;
+  const uint64_t u = b < q.n_queries ? plan_units(q, b, &need, &bad) : 0;
+  uint64_t incl = u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  uint64_t woff = 0;
+  for (uint32_t i = 0; i < wid; ++i) woff += wsum[i];
+  const uint64_t excl = base + woff + incl - u;
+  if (tid == 0 && q.cand_off[0] != 0) bad = true;
+  const bool last = b + 1 == q.n_queries;
+  bool over = false;
+  if (last && (q.cand_off[q.n_queries] > q.max_candidates || excl + u > q.max_units)) over = true;
+  // the last CTA has seen every query (prefix loop + its own): its verdict is global
+  const bool any_bad = __syncthreads_or(bad);
+  if (any_bad && tid == 0) atomicOr(q.err, ERR_BAD_OFFSETS);
+  if (over) atomicOr(q.err, ERR_CAPACITY);
+  if (b < q.n_queries) {
+    q.needed[b] = need;
+    q.unit_off[b] = (uint32_t)excl;
+    if (q.write_tab && excl + u <= q.max_units) {
+      const uint64_t c0 = q.cand_off[b];
+      for (uint64_t j = 0; j < u; ++j) {
+        const uint64_t c = c0 + j * q.unit_docs;
+        const uint32_t nd = (uint32_t)min((uint64_t)q.unit_docs, (uint64_t)need - j * q.unit_docs);
+        q.unit_tab[excl + j] = make_uint4(b, nd, (uint32_t)c, (uint32_t)(c >> 32));
+      }
+    }
+  }
+  if (last) {
+    q.unit_off[q.n_queries] = (uint32_t)(excl + u);
+    // read by the MaxSim kernel; an invalid batch gets an empty plan
+    *q.n_units = (any_bad || over) ? 0u : (uint32_t)(excl + u);
   }
 }
 
@@ -160,6 +245,7 @@ topk_kernel(const TopKParams p) {
   uint64_t* best = keys + kTopkSort;
   uint32_t* hash = reinterpret_cast<uint32_t*>(best + kMaxK);
   const uint32_t b = blockIdx.x;
+  if (*p.err & (ERR_BAD_OFFSETS | ERR_CAPACITY)) return;  // plan rejected the batch
   const uint64_t c0 = p.cand_off[b];
   const uint64_t n = p.cand_off[b + 1] - c0;
   const uint64_t n_needed = min((uint64_t)p.needed[b], n);
@@ -200,6 +286,161 @@ topk_kernel(const TopKParams p) {
     }
   }
   if (threadIdx.x == 0) p.out_counts[b] = (uint32_t)best_n;
+}
+
+// K3 fast path (final_k <= KMAX <= 32): one 256-thread CTA per query, no
+// sort.  (1) Duplicate detection (rank() rejects duplicate ids,
+// scoring.hpp:16-18) over the scored ids in a shared-memory open-addressing
+// table WITHOUT atomics: entries are (id << 32 | index); each round every
+// pending id is written to its probe slot if the slot looks empty, then read
+// back after a barrier -- own entry = placed, same id with another index =
+// duplicate, other id = probe on.  This phase reads only candidate ids, so it
+// runs before the programmatic-dependent-launch wait and overlaps the MaxSim
+// kernel's tail.  (2) Each thread keeps its best KMAX keys in registers;
+// k rounds of warp max-reduction produce per-warp lists, merged the same way
+// by warp 0.  Keys are (orderable score << 32 | ~doc_id): larger key =
+// (score desc, doc_id asc), exactly rank()'s comparator.
+constexpr int kTopkCtaThreads = 256;
+template <int KMAX>
+__global__ void __launch_bounds__(kTopkCtaThreads)
+topk_cta_kernel(const TopKParams p, uint32_t hash_slots) {
+  extern __shared__ __align__(16) uint64_t tk_smem[];
+  uint64_t* hash = tk_smem;                          // hash_slots entries
+  uint64_t* wl = tk_smem + hash_slots;               // 8 warps x KMAX merged lists
+  __shared__ int any_pending;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t b = blockIdx.x;
+  if (*p.err & (ERR_BAD_OFFSETS | ERR_CAPACITY)) return;  // plan rejected the batch
+  const uint64_t c0 = p.cand_off[b];
+  const uint64_t n = p.cand_off[b + 1] - c0;
+  const uint64_t n_needed = min((uint64_t)p.needed[b], n);
+  const uint64_t n_scored = p.partial ? n : n_needed;
+  constexpr uint64_t EMPTY = ~0ull;
+  if (n_scored * 2 <= hash_slots && !(p.dbg & 128u)) {
+    for (uint32_t i = tid; i < hash_slots; i += kTopkCtaThreads) hash[i] = EMPTY;
+    uint32_t dup = 0;
+    for (uint64_t j0 = 0; j0 < n_scored; j0 += kTopkCtaThreads * 4) {
+      uint32_t idv[4], hpos[4], pend = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t j = j0 + u * kTopkCtaThreads + tid;
+        idv[u] = j < n_scored ? __ldg(&p.cand_ids[c0 + j]) : 0u;
+        if (j < n_scored) pend |= 1u << u;
+        hpos[u] = ((idv[u] * 2654435761u) >> 7) & (hash_slots - 1);
+      }
+      __syncthreads();  // table initialised / previous batch settled
+      for (;;) {
+        uint32_t wrote = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (pend & (1u << u)) {
+            const uint64_t e = hash[hpos[u]];
+            if (e == EMPTY) {
+              hash[hpos[u]] = ((uint64_t)idv[u] << 32) | (uint32_t)(j0 + u * kTopkCtaThreads + tid);
+              wrote |= 1u << u;
+            } else if ((uint32_t)(e >> 32) == idv[u]) {
+              dup = 1;
+              pend &= ~(1u << u);
+            } else {
+              hpos[u] = (hpos[u] + 1) & (hash_slots - 1);
+            }
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (wrote & (1u << u)) {
+            const uint64_t mine = ((uint64_t)idv[u] << 32) | (uint32_t)(j0 + u * kTopkCtaThreads + tid);
+            const uint64_t e = hash[hpos[u]];
+            if (e == mine) {
+              pend &= ~(1u << u);
+            } else if ((uint32_t)(e >> 32) == idv[u]) {
+              dup = 1;
+              pend &= ~(1u << u);
+            } else {
+              hpos[u] = (hpos[u] + 1) & (hash_slots - 1);
+            }
+          }
+        }
+        if (!__syncthreads_or(pend != 0)) break;
+      }
+    }
+    if (dup) atomicOr(p.err, ERR_DUPLICATE);
+  }
+  (void)any_pending;
+  // bow scores come from the preceding MaxSim kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const float alpha = p.alpha;
+  uint64_t best[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) best[i] = 0;
+  uint32_t bad = 0;
+  for (uint64_t j0 = 0; j0 < n_scored; j0 += kTopkCtaThreads * 4) {
+    uint32_t idv[4];
+    float clv[4], bwv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // batch the loads
+      const uint64_t j = j0 + u * kTopkCtaThreads + tid;
+      idv[u] = j < n_scored ? __ldg(&p.cand_ids[c0 + j]) : 0u;
+      clv[u] = j < n_scored ? __ldg(&p.cand_cls[c0 + j]) : 0.0f;
+      bwv[u] = j < n_needed ? p.bow[c0 + j] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (j0 + u * kTopkCtaThreads + tid >= n_scored) continue;
+      const float sc = __fadd_rn(__fmul_rn(alpha, clv[u]), bwv[u]);
+      bad |= !isfinite(clv[u]) ? ERR_NONFINITE_CLS : (!isfinite(sc) ? ERR_NONFINITE_SCORE : 0u);
+      const uint64_t key = make_key(sc, idv[u]);
+      if (key > best[KMAX - 1]) {
+        best[KMAX - 1] = key;
+#pragma unroll
+        for (int i = KMAX - 1; i > 0; --i) {
+          const uint64_t a = best[i - 1], c = best[i];
+          best[i - 1] = a > c ? a : c;
+          best[i] = a > c ? c : a;
+        }
+      }
+    }
+  }
+  if (bad) atomicOr(p.err, bad);
+  const uint32_t k = p.k;
+  // per-warp merge: k rounds of warp max over the lanes' list heads
+  for (uint32_t r = 0; r < k; ++r) {
+    uint64_t m = best[0];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
+      m = x > m ? x : m;
+    }
+    if (best[0] == m && m != 0) {
+#pragma unroll
+      for (int i = 0; i < KMAX - 1; ++i) best[i] = best[i + 1];
+      best[KMAX - 1] = 0;
+    }
+    if (lane == 0) wl[wid * KMAX + r] = m;
+  }
+  __syncthreads();
+  // block merge by warp 0: lane l < 8 walks warp l's sorted list
+  if (wid == 0) {
+    uint32_t pos = 0;
+    uint32_t r = 0;
+    for (; r < k; ++r) {
+      uint64_t h = (lane < kTopkCtaThreads / 32 && pos < k) ? wl[lane * KMAX + pos] : 0;
+      uint64_t m = h;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
+        m = x > m ? x : m;
+      }
+      if (m == 0) break;  // fewer than k scored candidates
+      if (h == m) ++pos;
+      if (lane == 0) {
+        p.out_ids[(size_t)b * k + r] = ~(uint32_t)(m & 0xFFFFFFFFu);
+        p.out_scores[(size_t)b * k + r] = order_float((uint32_t)(m >> 32));
+      }
+    }
+    if (lane == 0) p.out_counts[b] = r;
+  }
 }
 
 // K4: merge n_lists ranked lists per query ([list][query][k]) into one top-k.

@@ -63,7 +63,7 @@ struct TcLayout {
   static constexpr int MAXW = NG / 32;             // bitmap words (one bit per group)
   static constexpr int MAX_STAGES = MAX_SLOTS / STAGE_SLOTS;  // stages of a full unit
   static constexpr int PM_STRIDE = UNITMAX + 1;    // padded: conflict-free emits and combine
-  static constexpr int PM_FLOATS = 4 * 32 * PM_STRIDE;
+  static constexpr int PM_FLOATS = NU * 32 * PM_STRIDE;  // per unit slot: [query token][doc] keys
   static constexpr int NBUF = (512 / NQC) < 4 ? (512 / NQC) : 4;
   static constexpr uint32_t TMEM_COLS = NBUF * NQC <= 32 ? 32 : NBUF * NQC <= 64 ? 64
                                       : NBUF * NQC <= 128 ? 128 : NBUF * NQC <= 256 ? 256 : 512;
@@ -72,7 +72,8 @@ struct TcLayout {
   static constexpr int MMA_WARP = NEPI;
   static constexpr int PROD_WARP0 = NEPI + 1;
   static constexpr int LOADER_WARP = PROD_WARP0 + NPROD;
-  static constexpr int NWARPS = LOADER_WARP + 1;
+  static constexpr int COMBINE_WARP = LOADER_WARP + 1;
+  static constexpr int NWARPS = COMBINE_WARP + 1;
   static constexpr int HALF = NQC / 2;             // columns per epilogue warp per stage
   static constexpr int LW = HALF < 32 ? HALF : 32; // tcgen05.ld width (columns)
   static constexpr int NLD = HALF / LW;            // loads per epilogue warp per stage
@@ -97,7 +98,7 @@ struct TcLayout {
   static constexpr int OFF_PM = OFF_A + A_BYTES;
   static constexpr int OFF_UNIT = OFF_PM + PM_FLOATS * 4;
   static constexpr int OFF_BAR = (OFF_UNIT + NU * (int)sizeof(Unit) + 7) / 8 * 8;
-  static constexpr int N_BARS = 2 * NS + 2 * NBUF + 2 * NU;
+  static constexpr int N_BARS = 2 * NS + 2 * NBUF + 3 * NU;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
@@ -139,7 +140,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
   uint64_t* tfull_bar = bars + 2 * L::NS;          // [NBUF] MMA commit -> epilogue
   uint64_t* tempty_bar = tfull_bar + L::NBUF;      // [NBUF] epilogue -> MMA
   uint64_t* ufull_bar = tempty_bar + L::NBUF;      // [NU] loader -> producer, MMA, epilogue
-  uint64_t* uempty_bar = ufull_bar + L::NU;        // [NU] epilogue -> loader
+  uint64_t* uempty_bar = ufull_bar + L::NU;        // [NU] combine -> loader
+  uint64_t* edone_bar = uempty_bar + L::NU;        // [NU] epilogue (all lanes) -> combine
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
   const int tid = threadIdx.x;
@@ -152,6 +154,10 @@ maxsim_tc_kernel(const MaxSimParams p) {
     uint4* z = reinterpret_cast<uint4*>(smem);
     const int n16 = (L::OFF_PM) / 16;
     for (int i = tid; i < n16; i += L::NTHREADS) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  {
+    int* pmk = reinterpret_cast<int*>(smem + L::OFF_PM);
+    for (int i = tid; i < L::PM_FLOATS; i += L::NTHREADS) pmk[i] = ord_key(-INFINITY);
   }
   fence_proxy_async_smem();
   if (tid == 0) {
@@ -166,6 +172,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
     for (int i = 0; i < L::NU; ++i) {
       mbar_init(&ufull_bar[i], 1);
       mbar_init(&uempty_bar[i], 1);
+      mbar_init(&edone_bar[i], 32 * L::NEPI);
     }
     mbar_fence_init();
   }
@@ -175,8 +182,11 @@ maxsim_tc_kernel(const MaxSimParams p) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const uint64_t t_start = gtimer();
+  // let the dependent top-k grid launch now: its dedup prologue reads only
+  // candidate ids and then waits (griddepcontrol.wait) for this grid to finish
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  const uint32_t n_units = p.n_units;
+  const uint32_t n_units = *p.n_units;  // planned on the device (plan_kernel)
 
   if (warp == L::LOADER_WARP) {
     // ============================ UNIT LOADER ===================================
@@ -312,7 +322,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
       __syncwarp();
       if (lane == 0) { ESPN_TRACE(2, it); mbar_arrive(&ufull_bar[us]); }
     }
-  } else if (warp >= L::PROD_WARP0) {
+  } else if (warp >= L::PROD_WARP0 && warp < L::PROD_WARP0 + L::NPROD) {
     // ====================== BULK-COPY PRODUCERS (NPROD warps) ======================
     // Producer pw takes docs kbeg + pw*32 + lane, stride 32*NPROD; each warp
     // arrives on the stage's full barrier with its own expect_tx byte count.
@@ -410,15 +420,13 @@ maxsim_tc_kernel(const MaxSimParams p) {
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp < L::NEPI) {
     // ==================== EPILOGUE (warps 0..NEPI-1) ===========================
     // warp = h*4 + w: TMEM lane quarter w (== query-token quarter), column half h.
     // pm holds order-preserving int keys of the per-doc partial maxima; the two
     // halves of a quarter may both flush a doc straddling the split, so
     // flushes are shared-memory atomicMax (a few per stage).
     const int w = warp & 3, h = warp >> 2;
-    int* my_pm = reinterpret_cast<int*>(pm) + (w * 32 + lane) * L::PM_STRIDE;
-    const uint32_t etid = tid;  // 0 .. 32*NEPI-1
     uint32_t gs = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t ug = blockIdx.x + it * gridDim.x;
@@ -427,11 +435,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
       const typename L::Unit& U = units[us];
       mbar_wait(&ufull_bar[us], (it / L::NU) & 1);
       if (tid == 0) ESPN_TRACE(4, it);
-      const uint32_t S = U.S, nd = U.nd;
-      const uint64_t j0 = U.cfirst;
-      if (h == 0)
-        for (uint32_t k = 0; k < nd; ++k) my_pm[k] = ord_key(-INFINITY);
-      named_bar_sync(2, 32 * L::NEPI);
+      const uint32_t S = U.S;
+      int* my_pm = reinterpret_cast<int*>(pm) + (us * 32 + lane) * L::PM_STRIDE;
       const uint32_t n_st = (S + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t buf = gs % L::NBUF;
@@ -509,23 +514,34 @@ maxsim_tc_kernel(const MaxSimParams p) {
           if (lane == 0) mbar_arrive(&tempty_bar[buf]);
         }
       }
-      // ---- combine: bow(doc) = sum_i max_w pm[w][i][doc], i ascending ----
+      // all lanes' flushes of this unit are done: hand the slot to the combiner
       if (tid == 0) ESPN_TRACE(5, it);
-      named_bar_sync(2, 32 * L::NEPI);
-      const int* pmi = reinterpret_cast<const int*>(pm);
-      for (uint32_t k = etid; k < nd; k += 32 * L::NEPI) {
+      mbar_arrive(&edone_bar[us]);
+    }
+  } else if (warp == L::COMBINE_WARP) {
+    // ============================ COMBINE ========================================
+    // bow(doc) = sum_i pm[us][i][doc] (max over the doc's tokens, reduced by the
+    // epilogue's atomicMax), i ascending (the oracle's summation order); then
+    // the slot's keys are reset and the unit slot is released to the loader.
+    // Runs concurrently with the epilogue of the next units.
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t ug = blockIdx.x + it * gridDim.x;
+      if (ug >= n_units) break;
+      const uint32_t us = it % L::NU;
+      const typename L::Unit& U = units[us];
+      mbar_wait(&edone_bar[us], (it / L::NU) & 1);
+      const uint32_t nd = U.nd;
+      const uint64_t j0 = U.cfirst;
+      int* pmu = reinterpret_cast<int*>(pm) + us * 32 * L::PM_STRIDE;
+      for (uint32_t k = lane; k < nd; k += 32) {
         float s = 0.0f;
-        for (uint32_t i = 0; i < p.nq; ++i) {
-          const int a0 = pmi[(0 * 32 + i) * L::PM_STRIDE + k];
-          const int a1 = pmi[(1 * 32 + i) * L::PM_STRIDE + k];
-          const int a2 = pmi[(2 * 32 + i) * L::PM_STRIDE + k];
-          const int a3 = pmi[(3 * 32 + i) * L::PM_STRIDE + k];
-          s = __fadd_rn(s, key_ord(max(max(a0, a1), max(a2, a3))));
-        }
+        for (uint32_t i = 0; i < p.nq; ++i) s = __fadd_rn(s, key_ord(pmu[i * L::PM_STRIDE + k]));
         p.bow_out[j0 + k] = s;
+#pragma unroll 8
+        for (uint32_t i = 0; i < 32; ++i) pmu[i * L::PM_STRIDE + k] = ord_key(-INFINITY);
       }
-      named_bar_sync(2, 32 * L::NEPI);
-      if (tid == 0) { ESPN_TRACE(6, it); mbar_arrive(&uempty_bar[us]); }
+      __syncwarp();
+      if (lane == 0) { ESPN_TRACE(6, it); mbar_arrive(&uempty_bar[us]); }
     }
   }
 

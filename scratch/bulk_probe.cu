@@ -47,7 +47,7 @@ prod(const __grid_constant__ Maps maps, const uint8_t* __restrict__ rows, const 
   __shared__ uint64_t full[NS], empty[NS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], W); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], MODE == 5 ? W * 32 : W); mbar_init(&empty[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
@@ -75,6 +75,26 @@ prod(const __grid_constant__ Maps maps, const uint8_t* __restrict__ rows, const 
       bytes = nb(cur) + nb(cur2);
       for (int o = 16; o; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
       mbar_wait(&empty[s], ((st / NS) & 1) ^ 1);
+      if (MODE == 5) {
+        const uint32_t sbase5 = su32(sm + s * 32768);
+        // docs of this warp: lanes hold (row0, t, slot); copy each doc cooperatively
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const uint4 dd = h2 ? cur2 : cur;
+          const uint32_t act = __ballot_sync(0xffffffffu, dd.y != 0);
+          for (uint32_t m = act; m; m &= m - 1) {
+            const int src_l = __ffs(m) - 1;
+            const uint32_t r0 = __shfl_sync(0xffffffffu, dd.x, src_l), t = __shfl_sync(0xffffffffu, dd.y, src_l),
+                           sl = __shfl_sync(0xffffffffu, dd.z, src_l);
+            const uint8_t* src = rows + (size_t)r0 * 64;
+            const uint32_t dst = sbase5 + sl * 64;
+            for (uint32_t c = lane; c < t * 4; c += 32)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(src + c * 16) : "memory");
+          }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[s])) : "memory");
+        cur = nxt; cur2 = nxt2;
+        continue;
+      }
       if (lane == 0) mbar_arrive_tx(&full[s], bytes);
       __syncwarp();
       const uint32_t sbase = su32(sm + s * 32768);
@@ -172,12 +192,10 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 5;
     printf("%-34s NS=%d W=%d %7.3f ms  useful %6.0f GB/s\n", name, ns, W, ms, bytes / ms / 1e6);
   };
-  run("bulk1d evict_first", prod<0, 4, 1>, 4, 1);
   run("bulk1d evict_first", prod<0, 4, 2>, 4, 2);
-  run("bulk1d evict_first", prod<0, 4, 3>, 4, 3);
-  run("bulk1d evict_first", prod<0, 6, 2>, 6, 2);
-  run("bulk1d nohint", prod<1, 4, 2>, 4, 2);
-  run("tma tile8 (ceil8 rows)", prod<2, 4, 2>, 4, 2);
-  run("tma 8/4/2/1 exact", prod<3, 4, 2>, 4, 2);
+  run("cp.async per doc", prod<5, 4, 1>, 4, 1);
+  run("cp.async per doc", prod<5, 4, 2>, 4, 2);
+  run("cp.async per doc", prod<5, 4, 4>, 4, 4);
+  run("cp.async per doc", prod<5, 6, 4>, 6, 4);
   return 0;
 }
