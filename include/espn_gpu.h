@@ -199,8 +199,8 @@ ESPN_API int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const
                         uint32_t n_lists, uint64_t list_stride, uint32_t n_queries, uint32_t k,
                         uint32_t* out_ids, float* out_scores, uint32_t* out_counts, void* stream);
 
-/* Cumulative counters of a workspace since creation.  Reading them completes
- * any PROFILE events still in flight (synchronizes on them). */
+/* Cumulative counters of a workspace since creation.  Reading them
+ * synchronizes the device (completes PROFILE timings still in flight). */
 typedef struct {
   uint64_t batches;
   uint64_t queries;
@@ -209,7 +209,10 @@ typedef struct {
   uint64_t profiled_batches;   /* batches run with ESPN_RERANK_PROFILE */
   double maxsim_ms;            /* summed CUDA-event time of the MaxSim kernel (PROFILE) */
   double topk_ms;              /* summed CUDA-event time of the top-k kernel (PROFILE) */
-  uint64_t reserved;
+  uint64_t maxsim_device_ns;   /* PROFILE, tcgen05 path: device-timed MaxSim duration summed over
+                                  launches (globaltimer, first CTA start -> last CTA end); also
+                                  counts launches replayed from CUDA graphs */
+  uint64_t maxsim_device_launches;
 } espn_counters;
 ESPN_API int espn_gpu_get_counters(const espn_gpu_workspace* ws, espn_counters* out);
 

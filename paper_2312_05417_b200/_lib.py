@@ -84,7 +84,8 @@ class Counters(C.Structure):
     _fields_ = [
         ("batches", C.c_uint64), ("queries", C.c_uint64), ("pairs_scored", C.c_uint64),
         ("kernel_launches", C.c_uint64), ("profiled_batches", C.c_uint64),
-        ("maxsim_ms", C.c_double), ("topk_ms", C.c_double), ("reserved", C.c_uint64),
+        ("maxsim_ms", C.c_double), ("topk_ms", C.c_double), ("maxsim_device_ns", C.c_uint64),
+        ("maxsim_device_launches", C.c_uint64),
     ]
 
 

@@ -348,10 +348,11 @@ class Reranker:
     """A table plus one workspace (per-stream scratch): the batched re-rank
     entry point.  One in-flight batch at a time."""
 
-    def __init__(self, store: GpuStore, max_queries: int, max_candidates: int, max_query_tokens: int = 32):
+    def __init__(self, store: GpuStore, max_queries: int, max_candidates: int, max_query_tokens: int = 32,
+                 max_list: int = 0):
         self.store = store
         desc = L.WorkspaceDesc(max_queries=max_queries, max_candidates=max_candidates,
-                               max_query_tokens=max_query_tokens)
+                               max_query_tokens=max_query_tokens, max_list=max_list)
         h = C.c_void_p()
         _check(L.lib().espn_gpu_workspace_create(store.handle, C.byref(desc), C.byref(h)))
         self._h = h
@@ -418,7 +419,7 @@ class Reranker:
     def counters(self) -> dict:
         c = L.Counters()
         _check(L.lib().espn_gpu_get_counters(self._h, C.byref(c)))
-        return {f: int(getattr(c, f)) for f, _ in L.Counters._fields_ if f != "reserved"}
+        return {f: (float(getattr(c, f)) if f.endswith("_ms") else int(getattr(c, f))) for f, _ in L.Counters._fields_}
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -96,6 +96,10 @@ struct MaxSimParams {
   const uint32_t* n_units;     // device: total work units (written by plan_kernel)
   uint32_t bf16;               // table dtype
   uint32_t dbg;                // profiling knobs (ESPN_DEBUG env; 0 in production)
+  // ESPN_RERANK_PROFILE: device-timed kernel duration (globaltimer, min start
+  // over CTAs -> end of the last CTA), accumulated as {sum_ns, launches,
+  // start scratch, CTA-done counter}; graph-replay safe.  NULL = off.
+  unsigned long long* prof;
 };
 
 struct TopKParams {

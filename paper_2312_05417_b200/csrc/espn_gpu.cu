@@ -208,6 +208,7 @@ struct espn_gpu_workspace {
   uint32_t* needed_in = nullptr;  // staged needed_counts (host-offset mode)
   uint32_t* n_units = nullptr;    // planned unit count (device)
   uint32_t max_list = 0;          // longest candidate list the top-k hash is sized for
+  unsigned long long* kprof = nullptr;  // device-timed MaxSim {sum_ns, launches, start, done}
   float* bow = nullptr;
   uint32_t* out_ids = nullptr;
   float* out_scores = nullptr;
@@ -425,6 +426,7 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   al((void**)&w->unit_tab, w->max_units * sizeof(uint4));
   al((void**)&w->needed_in, B * sizeof(uint32_t));
   al((void**)&w->n_units, sizeof(uint32_t));
+  al((void**)&w->kprof, 4 * sizeof(unsigned long long));
   w->max_list = desc->max_list ? desc->max_list : (uint32_t)std::min<size_t>(C, 4096);
   al((void**)&w->bow, C * sizeof(float));
   al((void**)&w->out_ids, B * kMaxK * sizeof(uint32_t));
@@ -441,6 +443,10 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
       if (e == cudaSuccess) e = cudaEventCreate(&ev);
   if (e == cudaSuccess) e = cudaMallocHost(&w->h_err, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(w->err, 0, 4 * sizeof(uint32_t));
+  if (e == cudaSuccess) {
+    const unsigned long long init[4] = {0ull, 0ull, ~0ull, 0ull};
+    e = cudaMemcpy(w->kprof, init, sizeof init, cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     espn_gpu_workspace_destroy(w);
     return fail(ESPN_E_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
@@ -453,7 +459,8 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   if (!w) return ESPN_OK;
   DeviceGuard g(w->table->device);
   cudaFree(w->q32); cudaFree(w->ids); cudaFree(w->cls); cudaFree(w->cand_off);
-  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->needed_in); cudaFree(w->n_units); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
+  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->needed_in); cudaFree(w->n_units);
+  cudaFree(w->kprof); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
   cudaFree(w->out_counts); cudaFree(w->err);
   for (auto& sl : w->slots) {
     if (sl.copied) cudaEventSynchronize(sl.copied);
@@ -521,7 +528,10 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     const char* e = getenv("ESPN_DEBUG");
     return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
   }();
-  const bool profile = (a->flags & ESPN_RERANK_PROFILE) != 0;
+  const bool profile_dev = (a->flags & ESPN_RERANK_PROFILE) != 0;
+  // host CUDA events only outside stream capture (device offsets = graph-capturable
+  // mode); the MaxSim kernel times itself on the device in both modes
+  const bool profile = profile_dev && !dev_off;
   const int pslot = (int)(w->prof_calls % espn_gpu_workspace::kProf);
   if (profile) drain_prof(w, pslot);
 
@@ -601,6 +611,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   mp.n_units = w->n_units;
   mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
   mp.dbg = dbg;
+  mp.prof = (profile_dev && tc) ? w->kprof : nullptr;
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
   cudaError_t e = tc ? launch_tc_rt(t->d, mp, t->num_sms, s) : launch_simt_rt(t->d, mp, t->num_sms, s);
   if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
@@ -781,6 +792,14 @@ int espn_gpu_get_counters(const espn_gpu_workspace* w, espn_counters* out) {
   auto* wm = const_cast<espn_gpu_workspace*>(w);
   for (int i = 0; i < espn_gpu_workspace::kProf; ++i) drain_prof(wm, i);
   *out = w->counters;
+  unsigned long long kp[2] = {0, 0};
+  {
+    DeviceGuard g(w->table->device);
+    ESPN_CUDA_TRY(cudaDeviceSynchronize());
+    ESPN_CUDA_TRY(cudaMemcpy(kp, w->kprof, sizeof kp, cudaMemcpyDeviceToHost));
+  }
+  out->maxsim_device_ns = kp[0];
+  out->maxsim_device_launches = kp[1];
   return ESPN_OK;
 }
 

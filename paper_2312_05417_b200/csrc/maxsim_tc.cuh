@@ -147,6 +147,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
+  if (p.prof && tid == 0) atomicMin(&p.prof[2], (unsigned long long)gtimer());
 
   // ---- one-time setup: zero operand tiles (stale NaN bit patterns would leak
   // into other quarters through the zero rows of A), barriers, TMEM ----------
@@ -550,6 +551,16 @@ maxsim_tc_kernel(const MaxSimParams p) {
   if (warp == L::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc<L::TMEM_COLS>(tmem_base);
+  }
+  if (p.prof && tid == 0) {
+    __threadfence();
+    if (atomicAdd(&p.prof[3], 1ull) == gridDim.x - 1) {  // last CTA out
+      const unsigned long long t0 = atomicAdd(&p.prof[2], 0ull);
+      atomicAdd(&p.prof[0], (unsigned long long)gtimer() - t0);
+      atomicAdd(&p.prof[1], 1ull);
+      p.prof[2] = ~0ull;
+      p.prof[3] = 0;
+    }
   }
   if ((p.dbg & 8u) && blockIdx.x == 0 && tid == 0) {
     const char* nm[7] = {"ld.start", "ld.slot", "ld.ready", "pr.start", "ep.start", "ep.mmadone", "ep.done"};
