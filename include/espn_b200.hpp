@@ -1,0 +1,240 @@
+// espn_b200.hpp -- C++ host API of the B200 re-rank path (the drop-in for
+// stages 3-6 of espn::run_query, proj/include/espn/pipeline.hpp:56-64).
+//
+// It is a thin layer over the C-ABI in espn_gpu.h: argument marshalling,
+// QueryStats accounting and the error mapping of error.hpp:8-42 (status code
+// -> exception class).  No compute happens here.
+//
+// Carrier types.  Built with -DESPN_B200_WITH_REFERENCE_HEADERS and the
+// reference's include directory on the path, this header uses the reference's
+// own espn::QueryEmbedding / CandidateList / PipelineConfig / QueryStats /
+// RankedList / FetchResult / error classes (pipeline.hpp pulls types.hpp,
+// ivf.hpp, store.hpp), so code written against the reference compiles
+// unchanged.  Without it, source-compatible declarations of the same types
+// (same names, members and defaults) are provided below.
+//
+// New seam: the reference has no "candidates in -> ranked
+// out" function; espn::gpu::rerank_candidates / rerank_batch are that seam,
+// and espn::gpu::Store is the HBM tier that replaces StoreHandle for the
+// re-rank path (store.hpp:80-107).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "espn_gpu.h"
+
+#if defined(ESPN_B200_WITH_REFERENCE_HEADERS)
+#include "espn/error.hpp"
+#include "espn/pipeline.hpp"
+#else
+#include <algorithm>
+#include <stdexcept>
+
+namespace espn {
+
+using DocId = std::uint32_t;
+using QueryId = std::uint32_t;
+
+// error.hpp:8-42
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& msg) : std::runtime_error(msg) {}
+};
+struct InvalidInputError : Error { using Error::Error; };
+struct InvalidStateError : Error { using Error::Error; };
+struct InvalidConfigError : Error { using Error::Error; };
+struct FormatError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
+struct DataIntegrityError : Error { using Error::Error; };
+
+// types.hpp:16-55 (t x d / q x d row-major fp32)
+struct EmbeddingMatrix {
+  DocId doc_id = 0;
+  std::uint32_t rows = 0;
+  std::uint32_t cols = 0;
+  std::vector<float> values;
+};
+struct ClsVector {
+  DocId doc_id = 0;
+  std::vector<float> values;
+};
+struct QueryEmbedding {
+  QueryId query_id = 0;
+  std::vector<float> cls;
+  std::uint32_t rows = 0;
+  std::uint32_t cols = 0;
+  std::vector<float> tokens;
+};
+struct ScoredDoc {
+  DocId doc_id = 0;
+  float score = 0.0f;
+};
+struct RankedList {
+  std::vector<ScoredDoc> entries;  // (score desc, doc_id asc), unique ids
+};
+
+// ivf.hpp:40-50
+struct Candidate {
+  DocId doc_id = 0;
+  float cls_score = 0.0f;
+};
+struct CandidateList {
+  std::vector<Candidate> entries;  // (cls_score desc, doc_id asc), deduplicated
+  std::size_t clusters_visited = 0;
+};
+
+// pipeline.hpp:11-29
+struct PipelineConfig {
+  std::uint32_t nprobe = 0;
+  double prefetch_step_pct = 10.0;
+  std::uint32_t rerank_count = 0;
+  std::uint32_t final_k = 10;
+  std::uint32_t prefetch_top_k = 0;
+  std::uint32_t candidate_k = 0;
+  float alpha = 1.0f;
+  bool prefetch_enabled = true;
+  bool partial_rerank_enabled = false;
+
+  std::uint32_t effective_prefetch_top_k() const { return prefetch_top_k ? prefetch_top_k : rerank_count; }
+  std::uint32_t effective_candidate_k() const { return candidate_k ? candidate_k : std::max(rerank_count, final_k); }
+};
+
+// pipeline.hpp:36-54
+struct QueryStats {
+  QueryId query_id = 0;
+  double ann_time = 0.0;
+  double prefetch_time = 0.0;
+  double early_rerank_time = 0.0;
+  double critical_fetch_time = 0.0;
+  double rerank_time = 0.0;
+  double total_time = 0.0;
+  std::uint64_t prefetched_count = 0;
+  std::uint64_t needed_count = 0;
+  std::uint64_t missed_count = 0;
+  double hit_rate = 0.0;
+  std::uint64_t prefetch_bytes = 0;
+  std::uint64_t critical_fetch_bytes = 0;
+  std::uint64_t critical_blocks_read = 0;
+  std::uint64_t needed_payload_bytes = 0;
+};
+
+// pipeline.hpp:66-79
+struct BatchStats {
+  std::size_t n_queries = 0;
+  double mean_latency = 0.0;
+  double p50_latency = 0.0;
+  double p99_latency = 0.0;
+  double wall_time = 0.0;
+  std::uint64_t total_critical_fetch_bytes = 0;
+};
+struct BatchResult {
+  std::vector<RankedList> rankings;
+  std::vector<QueryStats> stats;
+  BatchStats batch;
+};
+
+// store.hpp:61-71
+struct FetchedDoc {
+  ClsVector cls;
+  EmbeddingMatrix bow;
+};
+struct FetchResult {
+  std::vector<FetchedDoc> docs;
+  std::uint64_t bytes_read = 0;
+  std::uint64_t blocks_read = 0;
+  double wall_time = 0.0;
+};
+
+}  // namespace espn
+#endif
+
+namespace espn::gpu {
+
+enum class Dtype : std::uint32_t { f16 = ESPN_DTYPE_F16, bf16 = ESPN_DTYPE_BF16 };
+enum class Kernel : std::uint32_t { automatic = ESPN_KERNEL_AUTO, tcgen05 = ESPN_KERNEL_TCGEN05, simt = ESPN_KERNEL_SIMT };
+
+// Throws the espn:: exception class matching an espn_status (error.hpp:8-42).
+void throw_status(int status);
+
+// Record layout of the reference store (store.hpp:25-34), used only for the
+// QueryStats / FetchResult byte counters.
+struct RecordLayout {
+  std::uint32_t d_cls = 128;
+  std::uint32_t value_width = 2;
+  std::uint32_t alignment = 4096;
+};
+
+// The HBM tier of the embedding table: the re-rank path's StoreHandle.
+// Built from CSR token rows (doc i = rows[row_ptr[i]*d, row_ptr[i+1]*d), 2-byte
+// codes of `dtype`) or from reference EmbeddingMatrix docs (fp32, rounded to
+// dtype).  Move-only; shareable read-only across threads.
+class Store {
+ public:
+  Store(std::span<const std::uint64_t> row_ptr, std::span<const std::uint16_t> rows, std::uint32_t d,
+        Dtype dtype = Dtype::f16, RecordLayout layout = {}, int device = 0);
+  // docs[i].doc_id must equal i (dense ids, store.hpp:20)
+  static Store from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtype = Dtype::f16,
+                              RecordLayout layout = {}, int device = 0);
+  ~Store();
+  Store(Store&&) noexcept;
+  Store& operator=(Store&&) noexcept;
+  Store(const Store&) = delete;
+  Store& operator=(const Store&) = delete;
+
+  espn_gpu_table* handle() const { return table_; }
+  std::uint32_t d() const { return d_; }
+  Dtype dtype() const { return dtype_; }
+  std::uint64_t n_docs() const { return row_ptr_.empty() ? 0 : row_ptr_.size() - 1; }
+  std::uint32_t token_count(DocId id) const;
+  std::uint64_t record_bytes(std::uint32_t token_count) const;
+
+  // StoreHandle::fetch_batch (store.hpp:91-94): request order, duplicates
+  // allowed, unknown ids -> InvalidInputError; values decoded to fp32.
+  FetchResult fetch_batch(std::span<const DocId> doc_ids) const;
+
+ private:
+  espn_gpu_table* table_ = nullptr;
+  std::uint32_t d_ = 0;
+  Dtype dtype_ = Dtype::f16;
+  RecordLayout layout_;
+  int device_ = 0;
+  std::vector<std::uint64_t> row_ptr_;  // host copy for byte accounting
+};
+
+// A reusable batch context (one workspace = per-stream scratch).  Not
+// thread-safe: one in-flight batch per Reranker.
+class Reranker {
+ public:
+  Reranker(const Store& store, std::uint32_t max_queries, std::uint32_t max_candidates,
+           std::uint32_t max_query_tokens = 32);
+  ~Reranker();
+  Reranker(const Reranker&) = delete;
+  Reranker& operator=(const Reranker&) = delete;
+
+  // run_batch (pipeline.hpp:81-85) restricted to stages 3-6: one device pass
+  // for the whole batch, per-query results identical to single-query calls.
+  BatchResult rerank(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
+                     const PipelineConfig& config, Kernel kernel = Kernel::automatic);
+
+  espn_counters counters() const;
+
+ private:
+  const Store* store_;
+  espn_gpu_workspace* ws_ = nullptr;
+};
+
+// The seam: stages 3-6 of run_query for one query (SPEC.md:276 (3)-(6)).
+std::pair<RankedList, QueryStats> rerank_candidates(const QueryEmbedding& query, const CandidateList& candidates,
+                                                    const Store& store, const PipelineConfig& config);
+
+// Batched form (run_batch restricted to stages 3-6).
+BatchResult rerank_batch(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
+                         const Store& store, const PipelineConfig& config);
+
+}  // namespace espn::gpu

@@ -189,6 +189,13 @@ ESPN_API int espn_gpu_gather(espn_gpu_table* table, const uint32_t* ids, uint64_
                     uint16_t* out_rows, uint64_t* out_row_ptr, uint64_t capacity_tokens,
                     void* stream);
 
+/* Host-memory convenience form of espn_gpu_gather (the C++ Store::fetch_batch
+ * uses it): `ids` and the outputs are HOST pointers; out_row_ptr[n+1] receives
+ * the request-order token offsets and out_rows the plain row-major codes
+ * (capacity_tokens rows of d codes).  Synchronous. */
+ESPN_API int espn_gpu_gather_host(espn_gpu_table* table, const uint32_t* ids, uint64_t n,
+                         uint16_t* out_rows, uint64_t* out_row_ptr, uint64_t capacity_tokens);
+
 /* Merge per-shard ranked lists (multi-GPU, doc-id sharding): for each of
  * n_queries queries, `n_lists` ranked lists of up to k entries, merged into
  * the global top-k by (score desc, doc_id asc).  List l's arrays start at

@@ -1,7 +1,7 @@
 """In-tree build of the native library (no JIT cache, so the .so travels with
 the repo snapshot to the GPU box).
 
-    python -m paper_2312_05417_b200.build        # libespn_gpu.so + oracle
+    python -m paper_2312_05417_b200.build        # libespn_gpu.so + libespn_host.so
 
 libespn_gpu.so = csrc/espn_gpu.cu (+ headers) compiled for sm_100a only
 (`-gencode arch=compute_100a,code=sm_100a`: plain -arch=sm_100a would also
@@ -63,15 +63,43 @@ def build_lib(verbose: bool = False, force: bool = False) -> Path:
     return LIB
 
 
-def build_oracle() -> None:
-    """Oracle (test infrastructure) + the reference codec shim when the
-    reference tree is present (this container only)."""
-    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
-    if Path("/root/reference/proj/include/espn/half.hpp").exists():
-        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"], check=True)
+HOST_LIB = LIB_DIR / "libespn_host.so"
+HOST_SRC = CSRC / "host" / "espn_b200.cpp"
+CXX = os.environ.get("CXX", "g++")
+CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-fvisibility=default"]
+
+
+def build_host(force: bool = False) -> Path:
+    """libespn_host.so: the C++ espn::gpu API (include/espn_b200.hpp) over the
+    C-ABI, linked against libespn_gpu.so (rpath $ORIGIN)."""
+    deps = [HOST_SRC, ROOT / "include" / "espn_b200.hpp", ROOT / "include" / "espn_gpu.h", LIB]
+    if not force and HOST_LIB.exists() and all(p.stat().st_mtime <= HOST_LIB.stat().st_mtime for p in deps):
+        return HOST_LIB
+    cmd = [CXX, *CXX_FLAGS, "-shared", "-I", str(ROOT / "include"), "-o", str(HOST_LIB), str(HOST_SRC),
+           "-L", str(LIB_DIR), "-lespn_gpu", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building libespn_host.so")
+    return HOST_LIB
+
+
+def check_reference_headers() -> bool:
+    """Compile the C++ host API against the reference's own headers (source
+    compatibility of the drop-in), where /root/reference exists."""
+    inc = Path("/root/reference/proj/include")
+    if not inc.exists():
+        return False
+    cmd = [CXX, *CXX_FLAGS, "-fsyntax-only", "-DESPN_B200_WITH_REFERENCE_HEADERS", "-I", str(ROOT / "include"),
+           "-I", str(inc), str(HOST_SRC)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("C++ host API does not compile against the reference headers")
+    return True
 
 
 if __name__ == "__main__":
     build_lib(verbose="-v" in sys.argv, force="-f" in sys.argv)
-    build_oracle()
+    build_host(force="-f" in sys.argv)
     print(LIB)

@@ -753,6 +753,43 @@ int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t
   return ESPN_OK;
 }
 
+int espn_gpu_gather_host(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t* out_rows,
+                         uint64_t* out_row_ptr, uint64_t capacity_tokens) {
+  if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
+  if (!out_row_ptr) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  out_row_ptr[0] = 0;
+  if (n == 0) return ESPN_OK;
+  if (!ids) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  DeviceGuard g(t->device);
+  uint32_t* d_ids = nullptr;
+  uint64_t* d_rp = nullptr;
+  uint16_t* d_rows = nullptr;
+  auto cleanup = [&] { cudaFree(d_ids); cudaFree(d_rp); cudaFree(d_rows); };
+  if (cudaMalloc(&d_ids, n * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&d_rp, (n + 1) * sizeof(uint64_t)) != cudaSuccess) {
+    cleanup();
+    return fail(ESPN_E_CUDA, "cudaMalloc failed (gather)");
+  }
+  cudaMemcpy(d_ids, ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  int st = espn_gpu_gather(t, d_ids, n, nullptr, d_rp, 0, nullptr);
+  if (st) { cleanup(); return st; }
+  cudaMemcpy(out_row_ptr, d_rp, (n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+  const uint64_t total = out_row_ptr[n];
+  if (!out_rows) { cleanup(); return ESPN_OK; }
+  if (total > capacity_tokens) { cleanup(); return fail(ESPN_E_INVALID_INPUT, "out_rows capacity too small"); }
+  if (cudaMalloc(&d_rows, std::max<uint64_t>(total * t->d, 1) * sizeof(uint16_t)) != cudaSuccess) {
+    cleanup();
+    return fail(ESPN_E_CUDA, "cudaMalloc failed (gather rows)");
+  }
+  st = espn_gpu_gather(t, d_ids, n, d_rows, d_rp, total, nullptr);
+  if (st == ESPN_OK) {
+    const cudaError_t e = cudaMemcpy(out_rows, d_rows, total * t->d * sizeof(uint16_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = fail(ESPN_E_CUDA, cudaGetErrorString(e));
+  }
+  cleanup();
+  return st;
+}
+
 int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const uint32_t* counts,
                         uint32_t n_lists, uint64_t list_stride, uint32_t n_queries, uint32_t k,
                         uint32_t* out_ids, float* out_scores, uint32_t* out_counts, void* stream_v) {

@@ -1,0 +1,295 @@
+// espn_b200.cpp -- C++ host API (include/espn_b200.hpp) over the C-ABI.
+// Marshalling, byte accounting and exception mapping only; every score is
+// computed by libespn_gpu.so.
+#include "espn_b200.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+namespace espn::gpu {
+namespace {
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void check(int status) {
+  if (status != ESPN_OK) throw_status(status);
+}
+
+std::uint16_t encode(float x, Dtype dt) {
+  if (dt == Dtype::f16) {
+    const _Float16 h = static_cast<_Float16>(x);  // IEEE binary16, round to nearest even
+    std::uint16_t u;
+    std::memcpy(&u, &h, 2);
+    return u;
+  }
+  std::uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return static_cast<std::uint16_t>((u >> 16) | 0x40u);  // quiet NaN
+  return static_cast<std::uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+
+float decode(std::uint16_t c, Dtype dt) {
+  if (dt == Dtype::f16) {
+    _Float16 h;
+    std::memcpy(&h, &c, 2);
+    return static_cast<float>(h);
+  }
+  const std::uint32_t u = static_cast<std::uint32_t>(c) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+double percentile(std::vector<double> v, double p) {
+  if (v.empty()) return 0.0;
+  std::sort(v.begin(), v.end());
+  const double r = p / 100.0 * static_cast<double>(v.size() - 1);
+  const std::size_t lo = static_cast<std::size_t>(r);
+  const std::size_t hi = std::min(lo + 1, v.size() - 1);
+  return v[lo] + (v[hi] - v[lo]) * (r - static_cast<double>(lo));
+}
+
+}  // namespace
+
+void throw_status(int status) {
+  const std::string msg = espn_last_error();
+  switch (status) {
+    case ESPN_E_INVALID_INPUT: throw InvalidInputError(msg);
+    case ESPN_E_INVALID_STATE: throw InvalidStateError(msg);
+    case ESPN_E_INVALID_CONFIG: throw InvalidConfigError(msg);
+    case ESPN_E_FORMAT: throw FormatError(msg);
+    case ESPN_E_IO: throw IoError(msg);
+    case ESPN_E_DATA_INTEGRITY: throw DataIntegrityError(msg);
+    default: throw Error(msg.empty() ? std::string("espn_gpu failure ") + std::to_string(status) : msg);
+  }
+}
+
+// ---------------------------------------------------------------- Store
+Store::Store(std::span<const std::uint64_t> row_ptr, std::span<const std::uint16_t> rows, std::uint32_t d,
+             Dtype dtype, RecordLayout layout, int device)
+    : d_(d), dtype_(dtype), layout_(layout), device_(device), row_ptr_(row_ptr.begin(), row_ptr.end()) {
+  if (row_ptr.size() < 2) throw InvalidInputError("empty table");
+  espn_table_desc desc{};
+  desc.n_docs = row_ptr.size() - 1;
+  desc.d = d;
+  desc.dtype = static_cast<std::uint32_t>(dtype);
+  desc.d_cls = layout.d_cls;
+  desc.value_width = layout.value_width;
+  desc.alignment = layout.alignment;
+  desc.row_ptr = row_ptr.data();
+  desc.rows = rows.data();
+  desc.device = device;
+  if (rows.size() < row_ptr.back() * d) throw InvalidInputError("rows shorter than row_ptr[n_docs] * d");
+  check(espn_gpu_table_open(&desc, &table_));
+}
+
+Store Store::from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtype, RecordLayout layout, int device) {
+  if (docs.empty()) throw InvalidInputError("no documents");
+  const std::uint32_t d = docs[0].cols;
+  std::vector<std::uint64_t> rp(docs.size() + 1, 0);
+  for (std::size_t i = 0; i < docs.size(); ++i) {
+    const auto& m = docs[i];
+    if (m.doc_id != i) throw InvalidInputError("doc ids must be dense [0, n) in order (store.hpp:20)");
+    if (m.cols != d) throw InvalidInputError("inconsistent embedding dims");
+    if (m.rows < 1) throw InvalidInputError("doc with t < 1 (types.hpp:64-68)");
+    if (m.values.size() != static_cast<std::size_t>(m.rows) * m.cols) throw InvalidInputError("values size != rows*cols");
+    rp[i + 1] = rp[i] + m.rows;
+  }
+  std::vector<std::uint16_t> codes(rp.back() * d);
+  for (std::size_t i = 0; i < docs.size(); ++i) {
+    const auto& v = docs[i].values;
+    for (std::size_t j = 0; j < v.size(); ++j) {
+      if (!std::isfinite(v[j])) throw InvalidInputError("non-finite embedding value (types.hpp:64-68)");
+      codes[rp[i] * d + j] = encode(v[j], dtype);
+    }
+  }
+  return Store(rp, codes, d, dtype, layout, device);
+}
+
+Store::~Store() {
+  if (table_) espn_gpu_table_close(table_);
+}
+Store::Store(Store&& o) noexcept
+    : table_(std::exchange(o.table_, nullptr)), d_(o.d_), dtype_(o.dtype_), layout_(o.layout_), device_(o.device_),
+      row_ptr_(std::move(o.row_ptr_)) {}
+Store& Store::operator=(Store&& o) noexcept {
+  if (this != &o) {
+    if (table_) espn_gpu_table_close(table_);
+    table_ = std::exchange(o.table_, nullptr);
+    d_ = o.d_;
+    dtype_ = o.dtype_;
+    layout_ = o.layout_;
+    device_ = o.device_;
+    row_ptr_ = std::move(o.row_ptr_);
+  }
+  return *this;
+}
+
+std::uint32_t Store::token_count(DocId id) const {
+  if (id >= n_docs()) throw InvalidInputError("unknown doc id " + std::to_string(id));
+  return static_cast<std::uint32_t>(row_ptr_[id + 1] - row_ptr_[id]);
+}
+
+std::uint64_t Store::record_bytes(std::uint32_t t) const {
+  return (static_cast<std::uint64_t>(layout_.d_cls) + static_cast<std::uint64_t>(t) * d_) * layout_.value_width;
+}
+
+FetchResult Store::fetch_batch(std::span<const DocId> doc_ids) const {
+  const double t0 = now_s();
+  FetchResult res;
+  const std::uint64_t n = doc_ids.size();
+  std::vector<DocId> bad;
+  for (DocId id : doc_ids)
+    if (id >= n_docs()) bad.push_back(id);
+  if (!bad.empty()) {
+    std::string m = "unknown doc ids:";
+    for (std::size_t i = 0; i < std::min<std::size_t>(bad.size(), 16); ++i) m += " " + std::to_string(bad[i]);
+    throw InvalidInputError(m);  // store.hpp:92-93
+  }
+  if (n == 0) return res;
+  // device buffers through the CUDA runtime the library links
+  std::uint64_t tokens = 0;
+  std::vector<std::uint64_t> out_rp(n + 1, 0);
+  for (std::uint64_t i = 0; i < n; ++i) out_rp[i + 1] = out_rp[i] + token_count(doc_ids[i]);
+  tokens = out_rp[n];
+  std::vector<std::uint16_t> codes(tokens * d_);
+  check(espn_gpu_gather_host(table_, doc_ids.data(), n, codes.data(), out_rp.data(), tokens));
+  res.docs.resize(n);
+  for (std::uint64_t i = 0; i < n; ++i) {
+    auto& doc = res.docs[i].bow;
+    doc.doc_id = doc_ids[i];
+    doc.rows = static_cast<std::uint32_t>(out_rp[i + 1] - out_rp[i]);
+    doc.cols = d_;
+    doc.values.resize(static_cast<std::size_t>(doc.rows) * d_);
+    for (std::size_t j = 0; j < doc.values.size(); ++j) doc.values[j] = decode(codes[out_rp[i] * d_ + j], dtype_);
+    res.docs[i].cls.doc_id = doc_ids[i];
+    const std::uint64_t pb = record_bytes(doc.rows);
+    res.bytes_read += pb;
+    res.blocks_read += (pb + 4095) / 4096;  // block = 4096 outside direct mode (store.hpp:63-65)
+  }
+  res.wall_time = now_s() - t0;
+  return res;
+}
+
+// ---------------------------------------------------------------- Reranker
+Reranker::Reranker(const Store& store, std::uint32_t max_queries, std::uint32_t max_candidates,
+                   std::uint32_t max_query_tokens)
+    : store_(&store) {
+  espn_workspace_desc desc{};
+  desc.max_queries = std::max(max_queries, 1u);
+  desc.max_candidates = std::max(max_candidates, 1u);
+  desc.max_query_tokens = max_query_tokens;
+  check(espn_gpu_workspace_create(store.handle(), &desc, &ws_));
+}
+
+Reranker::~Reranker() {
+  if (ws_) espn_gpu_workspace_destroy(ws_);
+}
+
+espn_counters Reranker::counters() const {
+  espn_counters c{};
+  check(espn_gpu_get_counters(ws_, &c));
+  return c;
+}
+
+BatchResult Reranker::rerank(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
+                             const PipelineConfig& config, Kernel kernel) {
+  if (queries.size() != candidates.size()) throw InvalidInputError("queries and candidate lists differ in length");
+  BatchResult res;
+  const std::uint32_t B = static_cast<std::uint32_t>(queries.size());
+  if (B == 0) return res;
+  const std::uint32_t d = store_->d();
+  const std::uint32_t nq = queries[0].rows;
+  std::vector<float> qt(static_cast<std::size_t>(B) * nq * d);
+  std::vector<std::uint64_t> off(B + 1, 0);
+  for (std::uint32_t b = 0; b < B; ++b) {
+    const auto& q = queries[b];
+    if (q.cols != d) throw InvalidInputError("query dim " + std::to_string(q.cols) + " != table dim " + std::to_string(d));
+    if (q.rows != nq) throw InvalidInputError("all queries of a batch must have the same token count");
+    if (q.tokens.size() != static_cast<std::size_t>(q.rows) * q.cols) throw InvalidInputError("tokens size != rows*cols");
+    std::copy(q.tokens.begin(), q.tokens.end(), qt.begin() + static_cast<std::size_t>(b) * nq * d);
+    off[b + 1] = off[b] + candidates[b].entries.size();
+  }
+  std::vector<std::uint32_t> ids(off[B]);
+  std::vector<float> cls(off[B]);
+  for (std::uint32_t b = 0; b < B; ++b)
+    for (std::size_t j = 0; j < candidates[b].entries.size(); ++j) {
+      ids[off[b] + j] = candidates[b].entries[j].doc_id;
+      cls[off[b] + j] = candidates[b].entries[j].cls_score;
+    }
+  const std::uint32_t k = config.final_k;
+  std::vector<std::uint32_t> out_ids(static_cast<std::size_t>(B) * k), out_n(B);
+  std::vector<float> out_sc(static_cast<std::size_t>(B) * k);
+  espn_rerank_args a{};
+  a.n_queries = B;
+  a.n_query_tokens = nq;
+  a.query_tokens = qt.data();
+  a.cand_ids = ids.data();
+  a.cand_cls = cls.data();
+  a.cand_offsets = off.data();
+  a.rerank_count = config.rerank_count;
+  a.final_k = k;
+  a.alpha = config.alpha;
+  a.flags = config.partial_rerank_enabled ? ESPN_RERANK_PARTIAL : 0u;
+  a.kernel = static_cast<std::uint32_t>(kernel);
+  espn_rerank_out o{};
+  o.ids = out_ids.data();
+  o.scores = out_sc.data();
+  o.counts = out_n.data();
+  const double t0 = now_s();
+  check(espn_gpu_rerank(store_->handle(), ws_, &a, &o, nullptr));
+  const double wall = now_s() - t0;
+  res.rankings.resize(B);
+  res.stats.resize(B);
+  std::vector<double> lat(B, wall);
+  for (std::uint32_t b = 0; b < B; ++b) {
+    auto& rl = res.rankings[b];
+    rl.entries.resize(out_n[b]);
+    for (std::uint32_t i = 0; i < out_n[b]; ++i)
+      rl.entries[i] = ScoredDoc{out_ids[static_cast<std::size_t>(b) * k + i], out_sc[static_cast<std::size_t>(b) * k + i]};
+    // QueryStats (pipeline.hpp:36-54): the HBM tier holds every needed row
+    // before scoring, so nothing is fetched on the critical path.
+    auto& st = res.stats[b];
+    st.query_id = queries[b].query_id;
+    const std::uint64_t n = off[b + 1] - off[b];
+    st.needed_count = std::min<std::uint64_t>(n, config.rerank_count);
+    st.prefetched_count = st.needed_count;
+    st.missed_count = 0;
+    st.hit_rate = st.needed_count ? 1.0 : 0.0;
+    for (std::uint64_t j = 0; j < st.needed_count; ++j)
+      st.needed_payload_bytes += store_->record_bytes(store_->token_count(ids[off[b] + j]));
+    st.rerank_time = wall;
+    st.total_time = wall;
+  }
+  res.batch.n_queries = B;
+  res.batch.mean_latency = wall;
+  res.batch.p50_latency = percentile(lat, 50);
+  res.batch.p99_latency = percentile(lat, 99);
+  res.batch.wall_time = wall;
+  return res;
+}
+
+// ---------------------------------------------------------------- free functions
+BatchResult rerank_batch(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
+                         const Store& store, const PipelineConfig& config) {
+  std::uint64_t c = 0;
+  std::uint32_t nq = 1;
+  for (const auto& cl : candidates) c += cl.entries.size();
+  if (!queries.empty()) nq = std::max<std::uint32_t>(queries[0].rows, 1);
+  Reranker rr(store, static_cast<std::uint32_t>(queries.size()), static_cast<std::uint32_t>(std::max<std::uint64_t>(c, 1)),
+              std::min<std::uint32_t>(nq, 32));
+  return rr.rerank(queries, candidates, config);
+}
+
+std::pair<RankedList, QueryStats> rerank_candidates(const QueryEmbedding& query, const CandidateList& candidates,
+                                                    const Store& store, const PipelineConfig& config) {
+  BatchResult r = rerank_batch(std::span<const QueryEmbedding>(&query, 1),
+                               std::span<const CandidateList>(&candidates, 1), store, config);
+  return {std::move(r.rankings[0]), r.stats[0]};
+}
+
+}  // namespace espn::gpu
