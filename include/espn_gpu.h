@@ -94,7 +94,13 @@ typedef struct {
    * All ids crossing the ABI stay global.  0 or 1 = unsharded. */
   uint32_t shard_count;
   uint32_t shard_index;
-  uint32_t reserved[5];
+  /* Tiered store (SURVEY.md §8 a9, configs[3]): optional HOST array of n_docs
+   * flags; docs with resident[i] != 0 live in HBM, the others in a pinned-host
+   * tier (the overflow tier) and are staged into HBM per batch -- ahead of time
+   * by espn_gpu_prefetch on a side stream, or on the critical path.  NULL =
+   * every doc HBM-resident. */
+  const uint8_t* resident;
+  uint32_t reserved[4];
 } espn_table_desc;
 
 typedef struct {
@@ -105,6 +111,8 @@ typedef struct {
   uint32_t max_tokens;     /* longest doc */
   uint32_t min_tokens;
   uint64_t hbm_bytes;      /* device bytes held by the table */
+  uint64_t host_bytes;     /* pinned-host tier bytes (tiered tables) */
+  uint64_t resident_docs;  /* docs in HBM (n_docs unless tiered) */
 } espn_table_info;
 
 /* Validates (t >= 1 per doc, row_ptr monotone; types.hpp:64-68) and uploads
@@ -121,7 +129,9 @@ typedef struct {
   uint32_t max_query_tokens; /* <= 32 */
   uint32_t max_list;         /* longest candidate list of a query (sizes the top-k duplicate
                                 check when offsets are device-resident); 0 = min(max_candidates, 4096) */
-  uint32_t reserved[4];
+  uint64_t staging_bytes;    /* tiered tables: HBM staging per batch for host-tier rows
+                                (two buffers: one scoring, one prefetching); 0 = 64 MB */
+  uint32_t reserved[2];
 } espn_workspace_desc;
 
 ESPN_API int espn_gpu_workspace_create(espn_gpu_table* table, const espn_workspace_desc* desc,
@@ -135,6 +145,9 @@ ESPN_API int espn_gpu_workspace_destroy(espn_gpu_workspace* ws);
 #define ESPN_RERANK_WRITE_BOW 0x8u    /* also return per-candidate MaxSim (bow) scores */
 #define ESPN_RERANK_PROFILE 0x10u     /* time the MaxSim and top-k kernels with CUDA events on
                                          `stream` (accumulated into espn_counters) */
+#define ESPN_RERANK_PREFETCHED 0x40u  /* tiered table: this batch was staged by the last
+                                         espn_gpu_prefetch of this workspace (same ids/offsets);
+                                         otherwise host-tier rows are staged on the critical path */
 #define ESPN_RERANK_DEVICE_OFFSETS 0x20u /* cand_offsets / needed_counts are DEVICE pointers (needs
                                          DEVICE_IO): the batch is planned on the device, the call has
                                          no host-side loop, no host sync with ASYNC, and is CUDA-graph
@@ -165,16 +178,41 @@ typedef struct {
   uint32_t reserved[3];
 } espn_rerank_args;
 
+/* Per-query fetch accounting of a batch (QueryStats, pipeline.hpp:45-53), for
+ * tiered tables: needed = first min(R, n) candidates; resident = needed rows
+ * already in HBM; prefetched = needed host-tier rows staged by espn_gpu_prefetch
+ * before scoring; missed = needed host-tier rows staged on the critical path;
+ * bytes are table-row bytes moved over PCIe. */
+typedef struct {
+  uint64_t needed;
+  uint64_t resident;
+  uint64_t prefetched;
+  uint64_t missed;
+  uint64_t prefetch_bytes;
+  uint64_t critical_bytes;
+} espn_fetch_stats;
+
 typedef struct {
   uint32_t* ids;        /* B * final_k */
   float* scores;        /* B * final_k */
   uint32_t* counts;     /* B: entries written for each query */
   float* bow_scores;    /* optional (WRITE_BOW): cand_offsets[B] MaxSim scores; entries of
                            candidates beyond R are left untouched */
+  espn_fetch_stats* fetch_stats; /* optional HOST array of B (synchronous calls) */
 } espn_rerank_out;
 
 ESPN_API int espn_gpu_rerank(espn_gpu_table* table, espn_gpu_workspace* ws,
                     const espn_rerank_args* args, espn_rerank_out* out, void* stream);
+
+/* Prefetcher (the paper's prefetch worker):
+ * stages the host-tier rows of the NEXT batch's needed candidates into the
+ * workspace's spare HBM staging buffer on `side_stream`, overlapping the
+ * current batch's scoring.  `next` describes the batch exactly as it will be
+ * passed to espn_gpu_rerank (DEVICE_IO; offsets host or device per its flags);
+ * that call must carry ESPN_RERANK_PREFETCHED and waits on this staging.  A
+ * no-op for untiered tables. */
+ESPN_API int espn_gpu_prefetch(espn_gpu_table* table, espn_gpu_workspace* ws, const espn_rerank_args* next,
+                      void* side_stream);
 
 /* Completes an ASYNC batch on its stream and reports device-side errors
  * (unknown doc id -> DATA_INTEGRITY, non-finite query/cls -> INVALID_INPUT,

@@ -36,6 +36,7 @@ ESPN_RERANK_ASYNC = 0x4
 ESPN_RERANK_WRITE_BOW = 0x8
 ESPN_RERANK_PROFILE = 0x10
 ESPN_RERANK_DEVICE_OFFSETS = 0x20
+ESPN_RERANK_PREFETCHED = 0x40
 
 
 class TableDesc(C.Structure):
@@ -44,7 +45,7 @@ class TableDesc(C.Structure):
         ("d_cls", C.c_uint32), ("value_width", C.c_uint32), ("alignment", C.c_uint32),
         ("flags", C.c_uint32), ("row_ptr", C.c_void_p), ("rows", C.c_void_p),
         ("device", C.c_int32), ("shard_count", C.c_uint32), ("shard_index", C.c_uint32),
-        ("reserved", C.c_uint32 * 5),
+        ("resident", C.c_void_p), ("reserved", C.c_uint32 * 4),
     ]
 
 
@@ -52,14 +53,15 @@ class TableInfo(C.Structure):
     _fields_ = [
         ("n_docs", C.c_uint64), ("n_tokens", C.c_uint64), ("d", C.c_uint32),
         ("dtype", C.c_uint32), ("max_tokens", C.c_uint32), ("min_tokens", C.c_uint32),
-        ("hbm_bytes", C.c_uint64),
+        ("hbm_bytes", C.c_uint64), ("host_bytes", C.c_uint64), ("resident_docs", C.c_uint64),
     ]
 
 
 class WorkspaceDesc(C.Structure):
     _fields_ = [
         ("max_queries", C.c_uint32), ("max_candidates", C.c_uint32),
-        ("max_query_tokens", C.c_uint32), ("max_list", C.c_uint32), ("reserved", C.c_uint32 * 4),
+        ("max_query_tokens", C.c_uint32), ("max_list", C.c_uint32), ("staging_bytes", C.c_uint64),
+        ("reserved", C.c_uint32 * 2),
     ]
 
 
@@ -73,10 +75,15 @@ class RerankArgs(C.Structure):
     ]
 
 
+class FetchStats(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in ("needed", "resident", "prefetched", "missed", "prefetch_bytes",
+                                          "critical_bytes")]
+
+
 class RerankOut(C.Structure):
     _fields_ = [
         ("ids", C.c_void_p), ("scores", C.c_void_p), ("counts", C.c_void_p),
-        ("bow_scores", C.c_void_p),
+        ("bow_scores", C.c_void_p), ("fetch_stats", C.c_void_p),
     ]
 
 
@@ -98,6 +105,7 @@ SIGNATURES = {
     "espn_gpu_workspace_destroy": (C.c_int, [C.c_void_p]),
     "espn_gpu_rerank": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.POINTER(RerankOut), C.c_void_p]),
     "espn_gpu_workspace_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "espn_gpu_prefetch": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.c_void_p]),
     "espn_gpu_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "espn_gpu_gather_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]),
     "espn_gpu_merge_topk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32,

@@ -219,7 +219,7 @@ class GpuStore:
     def __init__(self, row_ptr, rows, d: int, dtype: str = "f16", d_cls: int = 128,
                  value_width: int = 2, alignment: int = 4096, device: int = 0,
                  borrowed_device: bool = False, shard_count: int = 1, shard_index: int = 0,
-                 rows_tiled: bool = False):
+                 rows_tiled: bool = False, resident=None):
         self.d = int(d)
         self.dtype = dtype
         self.d_cls = int(d_cls)
@@ -240,10 +240,16 @@ class GpuStore:
             self._row_ptr_host = row_ptr
             self._keep = (row_ptr, rows)
             rp_p, rows_p, flags = _ptr(row_ptr), _ptr(rows), 0
+        self._resident = None
+        if resident is not None:  # tiered store: HBM for resident docs, pinned host for the rest
+            self._resident = np.ascontiguousarray(np.asarray(resident, dtype=np.uint8))
+            if self._resident.shape[0] != n_docs:
+                raise InvalidInputError("resident mask must have one entry per doc")
         desc = L.TableDesc(n_docs=n_docs, d=self.d, dtype=_DTYPES[dtype], d_cls=self.d_cls,
                            value_width=self.value_width, alignment=self.alignment, flags=flags,
                            row_ptr=rp_p, rows=rows_p, device=self.device, shard_count=int(shard_count),
-                           shard_index=int(shard_index))
+                           shard_index=int(shard_index),
+                           resident=self._resident.ctypes.data if self._resident is not None else None)
         self.shard_count = max(int(shard_count), 1)
         self.shard_index = int(shard_index) if self.shard_count > 1 else 0
         h = C.c_void_p()
@@ -255,6 +261,10 @@ class GpuStore:
         _check(L.lib().espn_gpu_table_info(self._h, C.byref(info)))
         self.n_docs = int(info.n_docs)
         self.n_tokens = int(info.n_tokens)
+        self.hbm_bytes = int(info.hbm_bytes)
+        self.host_bytes = int(info.host_bytes)
+        self.resident_docs = int(info.resident_docs)
+        self.tiered = self._resident is not None
         self.max_tokens = int(info.max_tokens)
         self.min_tokens = int(info.min_tokens)
         self._workspaces = {}
@@ -349,10 +359,10 @@ class Reranker:
     entry point.  One in-flight batch at a time."""
 
     def __init__(self, store: GpuStore, max_queries: int, max_candidates: int, max_query_tokens: int = 32,
-                 max_list: int = 0):
+                 max_list: int = 0, staging_bytes: int = 0):
         self.store = store
         desc = L.WorkspaceDesc(max_queries=max_queries, max_candidates=max_candidates,
-                               max_query_tokens=max_query_tokens, max_list=max_list)
+                               max_query_tokens=max_query_tokens, max_list=max_list, staging_bytes=staging_bytes)
         h = C.c_void_p()
         _check(L.lib().espn_gpu_workspace_create(store.handle, C.byref(desc), C.byref(h)))
         self._h = h
@@ -365,7 +375,8 @@ class Reranker:
 
     def rerank_arrays(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig,
                       kernel: str = "auto", device_io: bool = False, write_bow: bool = False,
-                      out=None, stream=None, sync: bool = True, needed_counts=None):
+                      out=None, stream=None, sync: bool = True, needed_counts=None, prefetched: bool = False,
+                      fetch_stats: bool = False):
         """Batched stages 3-6.  query_tokens (B, q, d) fp32; cand_* CSR over
         queries with cand_offsets (B+1, host uint64).  Host numpy arrays by
         default (copied in and out inside the call); device torch tensors
@@ -399,6 +410,8 @@ class Reranker:
             flags |= L.ESPN_RERANK_WRITE_BOW
         if not sync:
             flags |= L.ESPN_RERANK_ASYNC
+        if prefetched:
+            flags |= L.ESPN_RERANK_PREFETCHED
         args = L.RerankArgs(n_queries=B, n_query_tokens=nq, query_tokens=_ptr(query_tokens),
                             cand_ids=_ptr(cand_ids), cand_cls=_ptr(cand_cls), cand_offsets=offs.ctypes.data,
                             rerank_count=int(config.rerank_count), final_k=k, alpha=float(config.alpha),
@@ -406,12 +419,40 @@ class Reranker:
         if needed_counts is not None:
             needed_counts = np.ascontiguousarray(needed_counts, dtype=np.uint32)
             args.needed_counts = needed_counts.ctypes.data
+        fs = (L.FetchStats * B)() if fetch_stats else None
         o = L.RerankOut(ids=_ptr(out[0]), scores=_ptr(out[1]), counts=_ptr(out[2]),
-                        bow_scores=_ptr(out[3]) if write_bow else None)
+                        bow_scores=_ptr(out[3]) if write_bow else None,
+                        fetch_stats=C.addressof(fs) if fs is not None else None)
         self._keepalive = (query_tokens, cand_ids, cand_cls, offs, out, needed_counts)
         _check(L.lib().espn_gpu_rerank(self.store.handle, self._h, C.byref(args), C.byref(o),
                                        C.c_void_p(stream) if stream else None))
+        if fs is not None:
+            self.last_fetch_stats = [{f: int(getattr(x, f)) for f, _ in L.FetchStats._fields_} for x in fs]
         return out
+
+    def prefetch(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig, stream=None,
+                 needed_counts=None, device_offsets: bool = False):
+        """espn_gpu_prefetch: stage the NEXT batch's host-tier rows on `stream`
+        (a side stream) while the current batch scores; the next
+        rerank_arrays(..., device_io=True, prefetched=True) of the same arrays
+        consumes it.  Device torch tensors; offsets host (numpy) unless
+        device_offsets."""
+        if device_offsets:
+            offs_p, B = _ptr(cand_offsets), int(cand_offsets.numel()) - 1
+            nc_p = _ptr(needed_counts) if needed_counts is not None else None
+        else:
+            offs = np.ascontiguousarray(np.asarray(cand_offsets, dtype=np.uint64))
+            offs_p, B = offs.ctypes.data, offs.shape[0] - 1
+            nc = np.ascontiguousarray(needed_counts, dtype=np.uint32) if needed_counts is not None else None
+            nc_p = nc.ctypes.data if nc is not None else None
+            self._pf_keep = (offs, nc)
+        flags = L.ESPN_RERANK_DEVICE_IO | (L.ESPN_RERANK_DEVICE_OFFSETS if device_offsets else 0)
+        args = L.RerankArgs(n_queries=B, n_query_tokens=int(query_tokens.shape[1]), query_tokens=_ptr(query_tokens),
+                            cand_ids=_ptr(cand_ids), cand_cls=_ptr(cand_cls), cand_offsets=offs_p,
+                            rerank_count=int(config.rerank_count), final_k=int(config.final_k),
+                            alpha=float(config.alpha), flags=flags, needed_counts=nc_p)
+        _check(L.lib().espn_gpu_prefetch(self.store.handle, self._h, C.byref(args),
+                                         C.c_void_p(stream) if stream else None))
 
     def sync(self, stream=None) -> None:
         _check(L.lib().espn_gpu_workspace_sync(self._h, C.c_void_p(stream) if stream else None))
@@ -433,15 +474,24 @@ class Reranker:
             pass
 
 
-def _stats_for(store: GpuStore, ids: np.ndarray, n_needed: int, query_id: int, elapsed: float) -> QueryStats:
-    """QueryStats for an HBM-resident table: every needed row is resident before
-    scoring, so nothing is fetched on the critical path (hit_rate 1.0)."""
+def _stats_for(store: GpuStore, ids: np.ndarray, n_needed: int, query_id: int, elapsed: float,
+               fetch: Optional[dict] = None) -> QueryStats:
+    """QueryStats (pipeline.hpp:36-54) from the device fetch accounting
+    (espn_fetch_stats): needed rows are either HBM-resident, staged ahead by the
+    prefetcher, or staged on the critical path (missed).  hit_rate =
+    |available before scoring| / |needed| (pipeline.hpp:48)."""
     st = QueryStats(query_id=query_id, needed_count=n_needed, rerank_time=elapsed, total_time=elapsed)
     tok = store.token_counts(ids[:n_needed]) if n_needed else np.zeros(0, np.uint64)
     if tok is not None:
         st.needed_payload_bytes = int(store.record_bytes(tok).sum()) if n_needed else 0
-    st.prefetched_count = n_needed
-    st.hit_rate = 1.0 if n_needed else 0.0
+    if fetch is None:
+        fetch = dict(needed=n_needed, resident=n_needed, prefetched=0, missed=0, prefetch_bytes=0, critical_bytes=0)
+    st.prefetched_count = fetch["prefetched"]
+    st.missed_count = fetch["missed"]
+    st.prefetch_bytes = fetch["prefetch_bytes"]
+    st.critical_fetch_bytes = fetch["critical_bytes"]
+    st.critical_blocks_read = (fetch["critical_bytes"] + 4095) // 4096
+    st.hit_rate = (fetch["resident"] + fetch["prefetched"]) / n_needed if n_needed else 0.0
     return st
 
 
@@ -471,7 +521,8 @@ def rerank_batch(queries: Sequence[QueryEmbedding], candidate_lists: Sequence[Ca
     rr = Reranker(store, B, max(int(offs[-1]), 1), max(nq, 1))
     try:
         t0 = time.perf_counter()
-        oid, osc, ocnt, _ = rr.rerank_arrays(qt, ids, cls, offs, config, kernel=kernel)
+        oid, osc, ocnt, _ = rr.rerank_arrays(qt, ids, cls, offs, config, kernel=kernel, fetch_stats=True)
+        fstats = rr.last_fetch_stats
         wall = time.perf_counter() - t0
     finally:
         rr.close()
@@ -481,7 +532,7 @@ def rerank_batch(queries: Sequence[QueryEmbedding], candidate_lists: Sequence[Ca
         res.rankings.append(RankedList([ScoredDoc(int(oid[b, i]), float(osc[b, i])) for i in range(n)]))
         a0, a1 = int(offs[b]), int(offs[b + 1])
         need = min(a1 - a0, int(config.rerank_count))
-        res.stats.append(_stats_for(store, ids[a0:a1], need, queries[b].query_id, wall))
+        res.stats.append(_stats_for(store, ids[a0:a1], need, queries[b].query_id, wall, fstats[b]))
         lat.append(wall)
     lat = np.asarray(lat)
     res.batch = BatchStats(n_queries=B, mean_latency=float(lat.mean()), p50_latency=float(np.percentile(lat, 50)),

@@ -52,7 +52,31 @@ enum : uint32_t {
   ERR_NONFINITE_SCORE = 1u << 4, // aggregate score not finite -> INVALID_INPUT
   ERR_UNIT_TOO_LARGE = 1u << 5,  // internal: slot budget of a work unit exceeded
   ERR_BAD_OFFSETS = 1u << 6,     // cand_offsets not starting at 0 / decreasing -> INVALID_INPUT
-  ERR_CAPACITY = 1u << 7         // batch exceeds workspace capacity -> INVALID_INPUT
+  ERR_CAPACITY = 1u << 7,        // batch exceeds workspace capacity -> INVALID_INPUT
+  ERR_STAGING = 1u << 8          // host-tier rows of a batch exceed the staging buffer -> INVALID_CONFIG
+};
+
+// Staging of host-tier rows for one batch (stage_kernel): one CTA per query,
+// one warp per needed candidate.
+struct StageParams {
+  const uint64_t* row_ptr;
+  const uint64_t* doc_loc;     // per doc: address | tier bit
+  uint64_t n_docs;
+  uint32_t shard_count, shard_index;
+  const uint32_t* cand_ids;
+  const uint64_t* cand_off;    // B + 1
+  const uint32_t* needed_in;   // optional per-query needed override
+  uint32_t rerank_count;
+  uint32_t n_queries;
+  uint64_t max_candidates;     // bound check on (not yet validated) offsets
+  uint32_t row_bytes;          // 2 * d
+  uint32_t prefetch;           // 1: staged ahead (side stream), 0: critical path
+  uint64_t* cand_src;          // out: per candidate, HBM address of its rows
+  uint8_t* stage;              // HBM staging buffer
+  uint64_t stage_cap;
+  unsigned long long* cursor;  // bytes used in stage (zeroed before the launch)
+  unsigned long long* qstats;  // B x 6 (espn_fetch_stats layout)
+  uint32_t* err;
 };
 
 // Device-side batch planning (plan_kernel): per-query needed counts, work
@@ -74,9 +98,20 @@ struct PlanParams {
   uint32_t write_tab;          // 1: tcgen05 (fill unit_tab)
 };
 
+// Absolute address of doc `loc`'s rows: untiered tables keep every row in one
+// HBM buffer; tiered tables carry a per-doc address with the
+// tier in bit 0 (0 = HBM, 1 = pinned host, mapped).
+__device__ __forceinline__ const uint8_t* doc_rows(const uint16_t* rows, const uint64_t* doc_loc, uint64_t loc,
+                                                   uint64_t r0, uint32_t d) {
+  if (doc_loc) return reinterpret_cast<const uint8_t*>(doc_loc[loc] & ~1ull);
+  return reinterpret_cast<const uint8_t*>(rows + r0 * d);
+}
+
 // One batch of (query, candidate list) pairs, resident on the device.
 struct MaxSimParams {
   const uint16_t* rows;        // table token rows, d codes each
+  const uint64_t* doc_loc;     // tiered tables: per-doc row address | tier bit (else NULL)
+  const uint64_t* cand_src;    // tiered tables: per-candidate row address in HBM after staging
   const uint64_t* row_ptr;     // n_docs + 1
   uint64_t n_docs;             // local docs of this shard
   uint32_t shard_count;        // doc-id sharding: id % shard_count == shard_index

@@ -45,9 +45,11 @@ int err_bits_to_status(uint32_t bits) {
   if (bits & ERR_UNIT_TOO_LARGE) m += " internal: work unit slot budget exceeded;";
   if (bits & ERR_BAD_OFFSETS) m += " cand_offsets must start at 0 and be non-decreasing;";
   if (bits & ERR_CAPACITY) m += " batch exceeds workspace capacity;";
+  if (bits & ERR_STAGING) m += " host-tier rows of the batch exceed the staging buffer (raise staging_bytes);";
   g_last_error = m;
   if (bits & ERR_UNKNOWN_DOC) return ESPN_E_DATA_INTEGRITY;
   if (bits & ERR_UNIT_TOO_LARGE) return ESPN_E_INVALID_STATE;
+  if (bits & ERR_STAGING) return ESPN_E_INVALID_CONFIG;
   return ESPN_E_INVALID_INPUT;
 }
 
@@ -192,6 +194,11 @@ struct espn_gpu_table {
   bool owned_rows = false;  // rows owned
   uint64_t* row_ptr = nullptr;
   uint16_t* rows = nullptr;
+  // tiered store (desc->resident): HBM compact rows in `rows`, pinned host tier
+  bool tiered = false;
+  uint64_t* doc_loc = nullptr;   // device: per-doc row address | tier bit
+  uint8_t* host_rows = nullptr;  // pinned, mapped
+  uint64_t hbm_row_bytes = 0, host_row_bytes = 0, resident_docs = 0;
 };
 
 struct espn_gpu_workspace {
@@ -209,6 +216,25 @@ struct espn_gpu_workspace {
   uint32_t* n_units = nullptr;    // planned unit count (device)
   uint32_t max_list = 0;          // longest candidate list the top-k hash is sized for
   unsigned long long* kprof = nullptr;  // device-timed MaxSim {sum_ns, launches, start, done}
+  // tiered tables: two staging slots (one scoring, one being prefetched)
+  struct Stage {
+    uint8_t* buf = nullptr;
+    uint64_t* cand_src = nullptr;
+    unsigned long long* cursor = nullptr;
+    unsigned long long* qstats = nullptr;  // B x 6
+    uint64_t* off = nullptr;               // device copy of the batch offsets (prefetch, host offsets)
+    uint32_t* need = nullptr;
+    uint64_t* off_h = nullptr;             // pinned staging of host offsets
+    uint32_t* need_h = nullptr;
+    cudaEvent_t done = nullptr;            // staging finished
+    cudaEvent_t free_ev = nullptr;         // last MaxSim reading this slot finished
+    bool used = false;
+  } stage[2];
+  uint64_t staging_bytes = 0;
+  int pf_q[2] = {-1, -1};  // FIFO of prefetched slots awaiting their PREFETCHED batch
+  int pf_count = 0;
+  int next_slot = 0;
+  unsigned long long* h_qstats = nullptr;  // pinned B x 6
   float* bow = nullptr;
   uint32_t* out_ids = nullptr;
   float* out_scores = nullptr;
@@ -249,6 +275,100 @@ void drain_prof(espn_gpu_workspace* w, int i) {
   w->counters.topk_ms += b;
   w->counters.profiled_batches += 1;
   p.pending = false;
+}
+}  // namespace
+
+namespace {
+// Splits an open table into an HBM tier (resident docs, compacted) and a
+// pinned-host tier (the rest), both in the tile layout; see espn_table_desc.
+int tier_table(espn_gpu_table* t, const uint8_t* resident, const uint64_t* host_row_ptr) {
+  const uint32_t rowb = t->d * 2;
+  std::vector<uint64_t> rp;
+  if (!host_row_ptr) {
+    rp.resize(t->n_docs + 1);
+    ESPN_CUDA_TRY(cudaMemcpy(rp.data(), t->row_ptr, (t->n_docs + 1) * 8, cudaMemcpyDeviceToHost));
+    host_row_ptr = rp.data();
+  }
+  uint64_t hb = 0, sb = 0, nres = 0;
+  for (uint64_t i = 0; i < t->n_docs; ++i) {
+    const uint64_t bytes = (host_row_ptr[i + 1] - host_row_ptr[i]) * rowb;
+    if (resident[i]) { hb += bytes; ++nres; } else { sb += bytes; }
+  }
+  uint8_t* hbm = nullptr;
+  uint8_t* host = nullptr;
+  uint64_t* dloc = nullptr;
+  auto undo = [&] { cudaFree(hbm); cudaFreeHost(host); cudaFree(dloc); };
+  if (cudaMalloc(&hbm, std::max<uint64_t>(hb, 16)) != cudaSuccess ||
+      cudaHostAlloc(&host, std::max<uint64_t>(sb, 16), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaMalloc(&dloc, t->n_docs * 8) != cudaSuccess) {
+    undo();
+    return fail(ESPN_E_CUDA, "tiered table: allocation failed (HBM or pinned host)");
+  }
+  uint8_t* host_dev = nullptr;
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&host_dev), host, 0) != cudaSuccess) {
+    undo();
+    return fail(ESPN_E_CUDA, "tiered table: host tier not mappable");
+  }
+  std::vector<uint64_t> loc(t->n_docs);
+  uint64_t oh = 0, os = 0;
+  for (uint64_t i = 0; i < t->n_docs; ++i) {
+    const uint64_t bytes = (host_row_ptr[i + 1] - host_row_ptr[i]) * rowb;
+    if (resident[i]) { loc[i] = reinterpret_cast<uint64_t>(hbm + oh); oh += bytes; }
+    else { loc[i] = reinterpret_cast<uint64_t>(host_dev + os) | 1ull; os += bytes; }
+  }
+  cudaError_t e = cudaMemcpy(dloc, loc.data(), t->n_docs * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    relocate_rows_kernel<<<t->num_sms * 8, 256>>>(reinterpret_cast<const uint8_t*>(t->rows), t->row_ptr, dloc,
+                                                   t->n_docs, rowb);
+    e = cudaDeviceSynchronize();
+  }
+  if (e != cudaSuccess) {
+    undo();
+    return fail(ESPN_E_CUDA, std::string("tiered table: relocation failed: ") + cudaGetErrorString(e));
+  }
+  if (t->owned_rows) cudaFree(t->rows);
+  t->rows = reinterpret_cast<uint16_t*>(hbm);
+  t->owned_rows = true;
+  t->host_rows = host;
+  t->doc_loc = dloc;
+  t->tiered = true;
+  t->hbm_row_bytes = hb;
+  t->host_row_bytes = sb;
+  t->resident_docs = nres;
+  return ESPN_OK;
+}
+// Stage the host-tier rows of one batch into workspace slot `slot` on stream s.
+int launch_stage(espn_gpu_table* t, espn_gpu_workspace* w, int slot, const uint64_t* dev_off,
+                 const uint32_t* dev_need, const uint32_t* dev_ids, uint32_t B, uint32_t R, cudaStream_t s,
+                 bool prefetch) {
+  auto& st = w->stage[slot];
+  if (st.used) ESPN_CUDA_TRY(cudaStreamWaitEvent(s, st.free_ev, 0));  // previous reader done
+  ESPN_CUDA_TRY(cudaMemsetAsync(st.cursor, 0, sizeof(unsigned long long), s));
+  ESPN_CUDA_TRY(cudaMemsetAsync(st.qstats, 0, (size_t)B * 6 * sizeof(unsigned long long), s));
+  StageParams sp{};
+  sp.row_ptr = t->row_ptr;
+  sp.doc_loc = t->doc_loc;
+  sp.n_docs = t->n_docs;
+  sp.shard_count = t->shard_count;
+  sp.shard_index = t->shard_index;
+  sp.cand_ids = dev_ids;
+  sp.cand_off = dev_off;
+  sp.needed_in = dev_need;
+  sp.rerank_count = R;
+  sp.n_queries = B;
+  sp.max_candidates = w->max_candidates;
+  sp.row_bytes = t->d * 2;
+  sp.prefetch = prefetch ? 1u : 0u;
+  sp.cand_src = st.cand_src;
+  sp.stage = st.buf;
+  sp.stage_cap = w->staging_bytes;
+  sp.cursor = st.cursor;
+  sp.qstats = st.qstats;
+  sp.err = w->err;
+  stage_kernel<<<B, 256, 0, s>>>(sp);
+  ESPN_CUDA_TRY(cudaGetLastError());
+  ESPN_CUDA_TRY(cudaEventRecord(st.done, s));
+  return ESPN_OK;
 }
 }  // namespace
 
@@ -368,6 +488,15 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
       t->owned_rows = true;
     }
   }
+  if (desc->resident) {
+    const int ts = tier_table(t, desc->resident, borrowed ? nullptr : desc->row_ptr);
+    if (ts) {
+      espn_gpu_table_close(t);
+      return ts;
+    }
+  } else {
+    t->resident_docs = t->n_docs;
+  }
   *out = t;
   return ESPN_OK;
 }
@@ -377,6 +506,8 @@ int espn_gpu_table_close(espn_gpu_table* t) {
   DeviceGuard g(t->device);
   if (t->owned) cudaFree(t->row_ptr);
   if (t->owned_rows) cudaFree(t->rows);
+  cudaFree(t->doc_loc);
+  if (t->host_rows) cudaFreeHost(t->host_rows);
   delete t;
   return ESPN_OK;
 }
@@ -389,7 +520,10 @@ int espn_gpu_table_info(const espn_gpu_table* t, espn_table_info* out) {
   out->dtype = t->dtype;
   out->max_tokens = t->max_t;
   out->min_tokens = t->min_t;
-  out->hbm_bytes = (t->owned ? (t->n_docs + 1) * 8 : 0) + (t->owned_rows ? t->n_tokens * t->d * 2 : 0);
+  out->hbm_bytes = (t->owned ? (t->n_docs + 1) * 8 : 0) +
+                   (t->tiered ? t->hbm_row_bytes + t->n_docs * 8 : (t->owned_rows ? t->n_tokens * t->d * 2 : 0));
+  out->host_bytes = t->host_row_bytes;
+  out->resident_docs = t->resident_docs;
   return ESPN_OK;
 }
 
@@ -427,6 +561,22 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   al((void**)&w->needed_in, B * sizeof(uint32_t));
   al((void**)&w->n_units, sizeof(uint32_t));
   al((void**)&w->kprof, 4 * sizeof(unsigned long long));
+  if (t->tiered) {
+    w->staging_bytes = desc->staging_bytes ? desc->staging_bytes : (64ull << 20);
+    for (auto& st : w->stage) {
+      al((void**)&st.buf, w->staging_bytes);
+      al((void**)&st.cand_src, C * sizeof(uint64_t));
+      al((void**)&st.cursor, sizeof(unsigned long long));
+      al((void**)&st.qstats, B * 6 * sizeof(unsigned long long));
+      al((void**)&st.off, (B + 1) * sizeof(uint64_t));
+      al((void**)&st.need, B * sizeof(uint32_t));
+      if (e == cudaSuccess) e = cudaMallocHost(&st.off_h, (B + 1) * sizeof(uint64_t));
+      if (e == cudaSuccess) e = cudaMallocHost(&st.need_h, (B + 1) * sizeof(uint32_t));
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st.free_ev, cudaEventDisableTiming);
+    }
+  }
+  if (e == cudaSuccess) e = cudaMallocHost(&w->h_qstats, B * 6 * sizeof(unsigned long long));
   w->max_list = desc->max_list ? desc->max_list : (uint32_t)std::min<size_t>(C, 4096);
   al((void**)&w->bow, C * sizeof(float));
   al((void**)&w->out_ids, B * kMaxK * sizeof(uint32_t));
@@ -460,7 +610,16 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   DeviceGuard g(w->table->device);
   cudaFree(w->q32); cudaFree(w->ids); cudaFree(w->cls); cudaFree(w->cand_off);
   cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->needed_in); cudaFree(w->n_units);
-  cudaFree(w->kprof); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
+  cudaFree(w->kprof);
+  for (auto& st : w->stage) {
+    if (st.done) cudaEventSynchronize(st.done);
+    if (st.free_ev) cudaEventSynchronize(st.free_ev);
+    cudaFree(st.buf); cudaFree(st.cand_src); cudaFree(st.cursor); cudaFree(st.qstats); cudaFree(st.off);
+    cudaFree(st.need); cudaFreeHost(st.off_h); cudaFreeHost(st.need_h);
+    if (st.done) cudaEventDestroy(st.done);
+    if (st.free_ev) cudaEventDestroy(st.free_ev);
+  }
+  cudaFreeHost(w->h_qstats); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
   cudaFree(w->out_counts); cudaFree(w->err);
   for (auto& sl : w->slots) {
     if (sl.copied) cudaEventSynchronize(sl.copied);
@@ -589,9 +748,29 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   plan_kernel<<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp);
   ESPN_CUDA_TRY(cudaGetLastError());
 
+  // ---- tiered table: host-tier rows staged into HBM (prefetched or now) ----
+  int slot = -1;
+  if (t->tiered) {
+    if (a->flags & ESPN_RERANK_PREFETCHED) {
+      if (w->pf_count == 0) return fail(ESPN_E_INVALID_STATE, "PREFETCHED batch without a pending espn_gpu_prefetch");
+      slot = w->pf_q[0];
+      w->pf_q[0] = w->pf_q[1];
+      --w->pf_count;
+      ESPN_CUDA_TRY(cudaStreamWaitEvent(s, w->stage[slot].done, 0));
+    } else {
+      if (w->pf_count == 2) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
+      slot = w->next_slot;
+      w->next_slot ^= 1;
+      const int ss = launch_stage(t, w, slot, cand_off, needed_in, ids, B, a->rerank_count, s, false);
+      if (ss) return ss;
+    }
+  }
+
   // ---- K2: MaxSim ----
   MaxSimParams mp{};
   mp.rows = t->rows;
+  mp.doc_loc = t->doc_loc;
+  mp.cand_src = slot >= 0 ? w->stage[slot].cand_src : nullptr;
   mp.row_ptr = t->row_ptr;
   mp.n_docs = t->n_docs;
   mp.shard_count = t->shard_count;
@@ -615,6 +794,10 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
   cudaError_t e = tc ? launch_tc_rt(t->d, mp, t->num_sms, s) : launch_simt_rt(t->d, mp, t->num_sms, s);
   if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
+  if (slot >= 0) {  // the slot may be re-staged once this MaxSim finished
+    ESPN_CUDA_TRY(cudaEventRecord(w->stage[slot].free_ev, s));
+    w->stage[slot].used = true;
+  }
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[1], s));
 
   // ---- K3: aggregate + top-k ----
@@ -691,10 +874,66 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     return ESPN_OK;
   }
   ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  if (o->fetch_stats && slot >= 0)
+    ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_qstats, w->stage[slot].qstats, (size_t)B * 6 * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s));
   ESPN_CUDA_TRY(cudaStreamSynchronize(s));
   ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
   w->async_pending = false;
+  if (o->fetch_stats) {
+    for (uint32_t b = 0; b < B; ++b) {
+      espn_fetch_stats& f = o->fetch_stats[b];
+      if (slot >= 0) {
+        const unsigned long long* q = w->h_qstats + (size_t)b * 6;
+        f = espn_fetch_stats{q[0], q[1], q[2], q[3], q[4], q[5]};
+      } else if (!dev_off) {  // HBM-resident table: every needed row is resident
+        const uint64_t n = a->cand_offsets[b + 1] - a->cand_offsets[b];
+        const uint64_t need = std::min<uint64_t>(n, a->needed_counts ? a->needed_counts[b] : a->rerank_count);
+        f = espn_fetch_stats{need, need, 0, 0, 0, 0};
+      } else {
+        f = espn_fetch_stats{};
+      }
+    }
+  }
   return err_bits_to_status(*w->h_err);
+}
+
+int espn_gpu_prefetch(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a, void* side_stream) {
+  if (!t || !w || !a) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
+  if (!t->tiered) return ESPN_OK;  // everything is HBM-resident
+  if (!(a->flags & ESPN_RERANK_DEVICE_IO)) return fail(ESPN_E_INVALID_INPUT, "prefetch needs DEVICE_IO batch arrays");
+  const uint32_t B = a->n_queries;
+  if (B == 0) return ESPN_OK;
+  if (B > w->max_queries) return fail(ESPN_E_INVALID_INPUT, "n_queries exceeds workspace capacity");
+  if (w->pf_count == 2) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
+  DeviceGuard g(t->device);
+  cudaStream_t s = static_cast<cudaStream_t>(side_stream);
+  const int slot = w->next_slot;
+  w->next_slot ^= 1;
+  auto& st = w->stage[slot];
+  const uint64_t* off = a->cand_offsets;
+  const uint32_t* need = a->needed_counts;
+  if (!(a->flags & ESPN_RERANK_DEVICE_OFFSETS)) {
+    if (a->cand_offsets[0] != 0) return fail(ESPN_E_INVALID_INPUT, "cand_offsets[0] must be 0");
+    for (uint32_t b = 0; b < B; ++b)
+      if (a->cand_offsets[b + 1] < a->cand_offsets[b]) return fail(ESPN_E_INVALID_INPUT, "cand_offsets must be non-decreasing");
+    if (a->cand_offsets[B] > w->max_candidates) return fail(ESPN_E_INVALID_INPUT, "candidates exceed workspace capacity");
+    if (st.used) ESPN_CUDA_TRY(cudaEventSynchronize(st.done));  // pinned staging of this slot is free
+    std::memcpy(st.off_h, a->cand_offsets, (B + 1) * sizeof(uint64_t));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(st.off, st.off_h, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    off = st.off;
+    if (a->needed_counts) {
+      std::memcpy(st.need_h, a->needed_counts, B * sizeof(uint32_t));
+      ESPN_CUDA_TRY(cudaMemcpyAsync(st.need, st.need_h, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      need = st.need;
+    }
+  }
+  const int ss = launch_stage(t, w, slot, off, need, a->cand_ids, B, a->rerank_count, s, true);
+  if (ss) return ss;
+  w->pf_q[w->pf_count++] = slot;
+  w->async_pending = true;  // staging errors surface at the next sync
+  return ESPN_OK;
 }
 
 int espn_gpu_workspace_sync(espn_gpu_workspace* w, void* stream_v) {
@@ -743,7 +982,7 @@ int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t
   if (total > capacity_tokens) return fail(ESPN_E_INVALID_INPUT, "out_rows capacity too small");
   const int cb = t->num_sms * 8;
   switch (t->d) {
-#define ESPN_G(DD) case DD: gather_copy_kernel<DD><<<cb, 256, 0, s>>>(t->rows, t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, out_rows); break;
+#define ESPN_G(DD) case DD: gather_copy_kernel<DD><<<cb, 256, 0, s>>>(t->rows, t->doc_loc, t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, out_rows); break;
     ESPN_G(8) ESPN_G(16) ESPN_G(32) ESPN_G(48) ESPN_G(64) ESPN_G(96) ESPN_G(128) ESPN_G(256)
 #undef ESPN_G
     default: return fail(ESPN_E_INVALID_CONFIG, "gather supports d in {8,16,32,48,64,96,128,256}");
@@ -815,7 +1054,7 @@ int espn_gpu_gather_rows(espn_gpu_table* t, const uint32_t* ids, uint64_t n, con
   cudaStream_t s = static_cast<cudaStream_t>(stream_v);
   const int cb = t->num_sms * 8;
   switch (t->d) {
-#define ESPN_G(DD) case DD: gather_copy_kernel<DD><<<cb, 256, 0, s>>>(t->rows, t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, out_rows); break;
+#define ESPN_G(DD) case DD: gather_copy_kernel<DD><<<cb, 256, 0, s>>>(t->rows, t->doc_loc, t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, out_rows); break;
     ESPN_G(8) ESPN_G(16) ESPN_G(32) ESPN_G(48) ESPN_G(64) ESPN_G(96) ESPN_G(128) ESPN_G(256)
 #undef ESPN_G
     default: return fail(ESPN_E_INVALID_CONFIG, "gather supports d in {8,16,32,48,64,96,128,256}");

@@ -63,7 +63,9 @@ maxsim_simt_kernel(const MaxSimParams p) {
     }
     const uint64_t r0 = __ldg(&p.row_ptr[loc]);
     const uint32_t t = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
-    const uint8_t* doc = reinterpret_cast<const uint8_t*>(p.rows + r0 * D);
+    const uint8_t* doc = p.cand_src ? reinterpret_cast<const uint8_t*>(p.cand_src[c])
+                                    : reinterpret_cast<const uint8_t*>(p.rows + r0 * D);
+    if (!doc) continue;  // not staged (staging overflow, reported by stage_kernel)
     float m = -INFINITY;
     for (uint32_t j = 0; j < t; ++j) {
       float acc = 0.0f;
@@ -532,9 +534,9 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(uint64_t* a, uint64_t n)
 // tile layout (RowLayout) and writes plain row-major rows in request order.
 template <int D>
 __global__ void __launch_bounds__(256)
-gather_copy_kernel(const uint16_t* rows, const uint64_t* row_ptr, uint64_t n_docs, uint32_t shard_count,
-                   uint32_t shard_index, const uint32_t* ids, uint64_t n, const uint64_t* out_row_ptr,
-                   uint16_t* out_rows) {
+gather_copy_kernel(const uint16_t* rows, const uint64_t* doc_loc, const uint64_t* row_ptr, uint64_t n_docs,
+                   uint32_t shard_count, uint32_t shard_index, const uint32_t* ids, uint64_t n,
+                   const uint64_t* out_row_ptr, uint16_t* out_rows) {
   using RL = RowLayout<D>;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -544,7 +546,7 @@ gather_copy_kernel(const uint16_t* rows, const uint64_t* row_ptr, uint64_t n_doc
     const uint64_t r0 = row_ptr[loc];
     const uint32_t t = (uint32_t)(row_ptr[loc + 1] - r0);
     const uint32_t nvec = t * RL::CH;
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(rows + r0 * D);
+    const uint8_t* src = doc_rows(rows, doc_loc, loc, r0, D);
     uint4* dst = reinterpret_cast<uint4*>(out_rows + out_row_ptr[i] * D);
     auto at = [&](uint32_t v) {
       return __ldcs(reinterpret_cast<const uint4*>(src + RL::off(t, v / RL::CH, v % RL::CH)));
@@ -558,6 +560,78 @@ gather_copy_kernel(const uint16_t* rows, const uint64_t* row_ptr, uint64_t n_doc
       __stcs(dst + v + 96, a3);
     }
     for (; v < nvec; v += 32) __stcs(dst + v, at(v));
+  }
+}
+
+// Tiered table open: copy each doc's (tiled) rows from the full device copy to
+// its tier -- HBM compact buffer or mapped pinned-host memory.  Warp per doc.
+__global__ void __launch_bounds__(256)
+relocate_rows_kernel(const uint8_t* src_rows, const uint64_t* row_ptr, const uint64_t* doc_loc, uint64_t n_docs,
+                     uint32_t row_bytes) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n_docs; i += nwarps) {
+    const uint64_t r0 = row_ptr[i];
+    const uint64_t n16 = (row_ptr[i + 1] - r0) * row_bytes / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(src_rows + r0 * row_bytes);
+    uint4* dst = reinterpret_cast<uint4*>(doc_loc[i] & ~1ull);
+    for (uint64_t v = lane; v < n16; v += 32) dst[v] = __ldcs(src + v);
+  }
+}
+
+// Per-batch staging of host-tier rows (tiered tables).  CTA per query, warp per
+// needed candidate: resident docs resolve to their HBM address; host-tier docs
+// are copied (16-byte loads from mapped pinned memory, i.e. PCIe reads) into
+// the staging buffer.  Writes the per-candidate row address the MaxSim kernel
+// reads, and the per-query fetch accounting.
+__global__ void __launch_bounds__(256) stage_kernel(const StageParams s) {
+  const uint32_t b = blockIdx.x;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint64_t c0 = s.cand_off[b], c1 = s.cand_off[b + 1];
+  if (c1 < c0 || c1 > s.max_candidates) return;  // invalid batch: the plan kernel reports it
+  const uint64_t n = c1 - c0;
+  const uint64_t cap = s.needed_in ? (uint64_t)s.needed_in[b] : (uint64_t)s.rerank_count;
+  const uint64_t need = n < cap ? n : cap;
+  unsigned long long resident = 0, staged = 0, bytes_moved = 0;
+  for (uint64_t j = wid; j < need; j += nw) {
+    const uint64_t loc = shard_local(s.cand_ids[c0 + j], s.shard_count, s.shard_index, s.n_docs);
+    if (loc == ~0ull) {  // reported as DATA_INTEGRITY by the MaxSim kernel
+      if (lane == 0) s.cand_src[c0 + j] = 0;
+      continue;
+    }
+    const uint64_t a = s.doc_loc[loc];
+    if (!(a & 1ull)) {
+      if (lane == 0) s.cand_src[c0 + j] = a;
+      ++resident;
+      continue;
+    }
+    const uint64_t bytes = (s.row_ptr[loc + 1] - s.row_ptr[loc]) * s.row_bytes;
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(s.cursor, (unsigned long long)bytes);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (off + bytes > s.stage_cap) {
+      if (lane == 0) { atomicOr(s.err, ERR_STAGING); s.cand_src[c0 + j] = 0; }
+      continue;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(a & ~1ull);
+    uint4* dst = reinterpret_cast<uint4*>(s.stage + off);
+    const uint64_t n16 = bytes / 16;
+    uint64_t v = lane;
+    for (; v + 96 < n16; v += 128) {  // 4 PCIe reads in flight per lane
+      const uint4 x0 = src[v], x1 = src[v + 32], x2 = src[v + 64], x3 = src[v + 96];
+      dst[v] = x0; dst[v + 32] = x1; dst[v + 64] = x2; dst[v + 96] = x3;
+    }
+    for (; v < n16; v += 32) dst[v] = src[v];
+    if (lane == 0) s.cand_src[c0 + j] = reinterpret_cast<uint64_t>(s.stage + off);
+    ++staged;
+    bytes_moved += bytes;
+  }
+  if (lane == 0 && s.qstats) {
+    unsigned long long* q = s.qstats + (size_t)b * 6;
+    if (wid == 0) atomicAdd(&q[0], (unsigned long long)need);
+    atomicAdd(&q[1], resident);
+    atomicAdd(&q[s.prefetch ? 2 : 3], staged);
+    atomicAdd(&q[s.prefetch ? 4 : 5], bytes_moved);
   }
 }
 

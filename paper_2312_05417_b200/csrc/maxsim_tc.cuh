@@ -85,7 +85,7 @@ struct TcLayout {
     uint64_t cfirst;            // candidate index of the unit's first doc
     uint32_t bitmap[MAXW];      // bit g: a doc starts at group g
     uint32_t wprefix[MAXW];     // docs starting before word w
-    uint64_t src[UNITMAX];      // byte offset of the doc in the table rows
+    uint64_t src[UNITMAX];      // address of the doc's rows (table or staging buffer)
     uint32_t t[UNITMAX];
     uint32_t slot[UNITMAX];
     uint8_t gvalid[NG];         // valid (non-pad) columns of group g, 1..8
@@ -224,11 +224,15 @@ maxsim_tc_kernel(const MaxSimParams p) {
         const uint32_t k = r * 32 + lane;
         uint32_t t = 0;
         uint64_t r0 = 0;
+        uint64_t srcaddr = 0;
         if (k < nd) {
           const uint64_t loc = shard_local(idk[r], p.shard_count, p.shard_index, p.n_docs);
           if (loc != ~0ull) {
             r0 = __ldg(&p.row_ptr[loc]);
             t = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
+            srcaddr = p.cand_src ? __ldg(&p.cand_src[cfirst + k])  // tiered: staged / resident address
+                                 : (uint64_t)(p.rows + r0 * D);
+            if (srcaddr == 0) t = 0;  // not staged (staging overflow, reported by stage_kernel)
           } else {
             atomicOr(p.err, ERR_UNKNOWN_DOC);
           }
@@ -242,7 +246,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
         }
         const uint32_t start = carry + incl - pad;
         if (k < nd) {
-          U.src[k] = r0 * (uint64_t)L::ROWB;
+          U.src[k] = srcaddr;
           U.t[k] = t;
           U.slot[k] = start;
           if (t > 0 && start + pad <= (uint32_t)L::MAX_SLOTS) {
@@ -329,7 +333,6 @@ maxsim_tc_kernel(const MaxSimParams p) {
     // arrives on the stage's full barrier with its own expect_tx byte count.
     const uint32_t pw = warp - L::PROD_WARP0;
     const uint64_t policy = l2_policy_evict_first();
-    const uint8_t* rows = reinterpret_cast<const uint8_t*>(p.rows);
     uint32_t gs = 0;  // global stage counter
     for (uint32_t it = 0;; ++it) {
       const uint32_t ug = blockIdx.x + it * gridDim.x;
@@ -364,7 +367,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
           const uint32_t a = max(sk, x0), e = min(sk + t, x1);
           if (e <= a) continue;
           const uint32_t ja = a - sk, n = e - a;
-          const uint8_t* src = rows + U.src[k];
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(U.src[k]);
 #pragma unroll
           for (int pn = 0; pn < L::NP; ++pn)
             bulk_g2s(sbase + pn * L::PANEL_BYTES + (a - x0) * L::PW,

@@ -272,3 +272,84 @@ def test_synth_table_on_device(cuda_ok):
     codes = rows.cpu().numpy().view(np.uint16)
     sub = ((codes & 0x7C00) == 0) & ((codes & 0x3FF) != 0)
     assert not sub.any(), "synthetic table must not contain fp16 subnormals"
+
+
+# ---- tiered store + prefetcher (SURVEY.md §8 a9, configs[3]) -----------------
+def _tiered_case(seed=101):
+    rp, codes, q, ids, cls, off = build_case(6000, 32, 1, 63, B=8, K=600, seed=seed)
+    rng = np.random.default_rng(seed)
+    resident = (rng.random(6000) < 0.2).astype(np.uint8)  # 1/5 in HBM, 4/5 in pinned host
+    return rp, codes, q, ids, cls, off, resident
+
+
+@pytest.mark.parametrize("kernel", ["tcgen05", "simt"])
+def test_tiered_store_matches_resident_and_oracle(oracle, cuda_ok, kernel):
+    rp, codes, q, ids, cls, off, resident = _tiered_case()
+    cfg = api.PipelineConfig(rerank_count=64, final_k=10, alpha=0.5, partial_rerank_enabled=True)
+    full = run_gpu(rp, codes, 32, "f16", q, ids, cls, off, cfg, kernel)
+    store = api.GpuStore(rp, codes, 32, resident=resident)
+    assert store.tiered and store.resident_docs == int(resident.sum()) and store.host_bytes > 0
+    rr = api.Reranker(store, len(off) - 1, int(off[-1]), 32)
+    got = rr.rerank_arrays(q, ids, cls, off, cfg, kernel=kernel, write_bow=True, fetch_stats=True)
+    # identical arithmetic on identical rows: bit-identical scores and order
+    for g, f in zip(got[:3], full[:3]):
+        assert np.array_equal(g, f)
+    need = np.minimum(np.diff(off), 64)
+    for b, fs in enumerate(rr.last_fetch_stats):  # no prefetch: host-tier rows are critical-path misses
+        assert fs["needed"] == need[b] and fs["prefetched"] == 0
+        a0 = int(off[b])
+        res = int(resident[ids[a0:a0 + need[b]]].sum())
+        assert fs["resident"] == res and fs["missed"] == need[b] - res
+        t = (rp[ids[a0:a0 + need[b]] + 1] - rp[ids[a0:a0 + need[b]]])
+        assert fs["critical_bytes"] == int((t * (1 - resident[ids[a0:a0 + need[b]]])).sum()) * 64
+    rr.close(); store.close()
+
+
+def test_prefetch_on_off_identical_and_hit_rate(cuda_ok):
+    # prefetching only moves I/O off the critical path
+    import torch
+    rp, codes, q, ids, cls, off, resident = _tiered_case(seed=202)
+    cfg = api.PipelineConfig(rerank_count=64, final_k=10, partial_rerank_enabled=True)
+    store = api.GpuStore(rp, codes, 32, resident=resident)
+    B, C = len(off) - 1, int(off[-1])
+    rr = api.Reranker(store, B, C, 32)
+    dev = torch.device("cuda")
+    dq, di, dc = (torch.from_numpy(q).to(dev), torch.from_numpy(ids.view(np.int32)).to(dev),
+                  torch.from_numpy(cls).to(dev))
+    side = torch.cuda.Stream()
+    off_ref = rr.rerank_arrays(dq, di, dc, off, cfg, device_io=True, fetch_stats=True)
+    ref = [x.cpu().numpy() for x in off_ref[:3]]
+    ref_stats = rr.last_fetch_stats
+    rr.prefetch(dq, di, dc, off, cfg, stream=side.cuda_stream)
+    got = rr.rerank_arrays(dq, di, dc, off, cfg, device_io=True, prefetched=True, fetch_stats=True)
+    for g, r in zip(got[:3], ref):
+        assert np.array_equal(g.cpu().numpy(), r)
+    for fs, rs in zip(rr.last_fetch_stats, ref_stats):
+        assert fs["missed"] == 0 and fs["critical_bytes"] == 0
+        assert fs["prefetched"] == rs["missed"] and fs["prefetch_bytes"] == rs["critical_bytes"]
+        assert fs["resident"] + fs["prefetched"] == fs["needed"]  # hit rate 1.0
+    # the api mirror's QueryStats carry the same accounting
+    qs = [api.QueryEmbedding(query_id=b, cls=np.zeros(128, np.float32), rows=32, cols=32, tokens=q[b].ravel())
+          for b in range(B)]
+    cl = [api.CandidateList([api.Candidate(int(i), float(c)) for i, c in zip(ids[int(off[b]):int(off[b + 1])],
+                                                                              cls[int(off[b]):int(off[b + 1])])])
+          for b in range(B)]
+    br = api.rerank_batch(qs, cl, store, cfg)
+    for b, st in enumerate(br.stats):
+        assert st.missed_count == ref_stats[b]["missed"]
+        assert abs(st.hit_rate - ref_stats[b]["resident"] / 64) < 1e-12
+    rr.close(); store.close()
+
+
+def test_tiered_gather_and_staging_overflow(oracle, cuda_ok):
+    rp, codes, q, ids, cls, off, resident = _tiered_case(seed=303)
+    store = api.GpuStore(rp, codes, 32, resident=resident)
+    req = np.random.default_rng(3).integers(0, 6000, size=300).astype(np.uint32)
+    res = store.fetch_batch(req)
+    st, orp, orows = oracle.gather(oracle.OracleTable(rp, codes, 32), req)
+    assert st == 0
+    assert np.array_equal(np.concatenate([api.encode(d.bow.values, "f16") for d in res.docs]), orows)
+    rr = api.Reranker(store, len(off) - 1, int(off[-1]), 32, staging_bytes=4096)  # far too small
+    with pytest.raises(api.InvalidConfigError):
+        rr.rerank_arrays(q, ids, cls, off, api.PipelineConfig(rerank_count=600, final_k=10))
+    rr.close(); store.close()
