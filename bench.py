@@ -49,7 +49,12 @@ CONFIGS = {
     "c3": dict(workload="configs[2]: ColBERTv2-shaped synthetic, 8.8M docs, ~70 tok/doc, d128 fp16, batch 256",
                n_docs=8_800_000, d=128, t_min=40, t_max=100, dtype="f16", batch=256, K=1000, R=1000, k=10, nq=32),
     "c5": dict(workload="configs[4]: large-batch stress d32, batch 4096 x 4000 candidates",
-               n_docs=8_800_000, d=32, t_min=1, t_max=63, dtype="f16", batch=4096, K=4000, R=4000, k=10, nq=32),
+               n_docs=8_800_000, d=32, t_min=1, t_max=63, dtype="f16", batch=4096, K=4000, R=4000, k=10, nq=32,
+               n_batches=4),
+    "c4": dict(workload="configs[3]: partial re-rank + prefetcher, C2 table with 1/5 of the docs in HBM and 4/5 "
+                        "in a pinned-host tier, batch 64, top-1000 -> R=64 MaxSim + alpha*cls tail -> top-10",
+               n_docs=8_800_000, d=32, t_min=1, t_max=63, dtype="f16", batch=64, K=1000, R=64, k=10, nq=32,
+               partial=True, resident_frac=0.2),
 }
 SEED = 42
 N_BATCHES = 16          # distinct candidate batches rotated through the timed loop
@@ -143,6 +148,95 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows), "samples_under_load": len(load)}
 
 
+# ------------------------------------------------------------------ tiered arm
+def run_tiered(args, cfg):
+    """configs[3]: HBM tier (resident_frac of the docs) + pinned-host tier, the
+    side-stream prefetcher staging batch n+1's host-tier rows while batch n
+    scores; prefetch on vs off, hit rate and PCIe bytes reported."""
+    import torch
+    from paper_2312_05417_b200 import _lib as L
+    from paper_2312_05417_b200 import api, synth
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    lib = L.lib()
+    N, d = cfg["n_docs"], cfg["d"]
+    t0 = time.time()
+    row_ptr = torch.zeros(N + 1, dtype=torch.int64, device=dev)
+    assert lib.espn_gpu_synth_table(N, d, 0, cfg["t_min"], cfg["t_max"], SEED, 1, 0, row_ptr.data_ptr(), None, None) == 0
+    rows = torch.empty(int(row_ptr[-1]) * d, dtype=torch.int16, device=dev)
+    assert lib.espn_gpu_synth_table(N, d, 0, cfg["t_min"], cfg["t_max"], SEED, 1, 0, row_ptr.data_ptr(),
+                                    rows.data_ptr(), None) == 0
+    # resident set: a seeded hash of the doc id (uniform, independent of the candidates)
+    h = synth.splitmix64(np.arange(N, dtype=np.uint64) ^ np.uint64(0xC4))
+    resident = ((h >> np.uint64(40)).astype(np.float64) / float(1 << 24) < cfg["resident_frac"]).astype(np.uint8)
+    store = api.GpuStore.from_device(row_ptr, rows, d, "f16", rows_tiled=True, resident=resident)
+    del rows
+    torch.cuda.empty_cache()
+    log(f"[tiered] table: {store.resident_docs} of {N} docs in HBM ({store.hbm_bytes / 1e9:.1f} GB), "
+        f"host tier {store.host_bytes / 1e9:.1f} GB pinned, built in {time.time() - t0:.1f}s")
+    B, K, R, k, nq = cfg["batch"], cfg["K"], cfg["R"], cfg["k"], cfg["nq"]
+    n_batches = N_BATCHES
+    batches = make_batches(cfg, n_batches, B)
+    dbs = [dict(q=torch.from_numpy(b["q"]).to(dev), ids=torch.from_numpy(b["ids"].view(np.int32)).to(dev),
+                cls=torch.from_numpy(b["cls"]).to(dev), off=b["off"]) for b in batches]
+    rr = api.Reranker(store, B, B * K, nq, staging_bytes=256 << 20)
+    pcfg = api.PipelineConfig(rerank_count=R, final_k=k, partial_rerank_enabled=cfg.get("partial", False))
+    out = (torch.zeros((B, k), dtype=torch.int32, device=dev), torch.zeros((B, k), dtype=torch.float32, device=dev),
+           torch.zeros(B, dtype=torch.int32, device=dev), None)
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+
+    def run(n_steps, prefetch):
+        if prefetch:
+            db = dbs[0]
+            rr.prefetch(db["q"], db["ids"], db["cls"], db["off"], pcfg, stream=side.cuda_stream)
+        for st in range(n_steps):
+            db = dbs[st % n_batches]
+            if prefetch and st + 1 < n_steps:  # stage batch st+1 while st scores
+                nx = dbs[(st + 1) % n_batches]
+                rr.prefetch(nx["q"], nx["ids"], nx["cls"], nx["off"], pcfg, stream=side.cuda_stream)
+            rr.rerank_arrays(db["q"], db["ids"], db["cls"], db["off"], pcfg, device_io=True, out=out,
+                             stream=main.cuda_stream, sync=False, prefetched=prefetch)
+
+    res_mode = {}
+    for prefetch in (True, False):
+        run(max(args.warmup, 3), prefetch)
+        torch.cuda.synchronize()
+        rr.sync(main.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        run(args.steps, prefetch)
+        e1.record(main)
+        torch.cuda.synchronize()
+        rr.sync(main.cuda_stream)
+        ms = e0.elapsed_time(e1)
+        # fetch accounting of one representative batch in this mode
+        db = dbs[0]
+        if prefetch:
+            rr.prefetch(db["q"], db["ids"], db["cls"], db["off"], pcfg, stream=side.cuda_stream)
+        rr.rerank_arrays(db["q"], db["ids"], db["cls"], db["off"], pcfg, device_io=True, out=out,
+                         stream=main.cuda_stream, prefetched=prefetch, fetch_stats=True)
+        fs = rr.last_fetch_stats
+        need = sum(f["needed"] for f in fs)
+        res_mode["on" if prefetch else "off"] = {
+            "queries_per_s": B * args.steps / (ms / 1e3), "ms_per_step": ms / args.steps,
+            "hit_rate": sum(f["resident"] + f["prefetched"] for f in fs) / max(need, 1),
+            "critical_path_bytes_per_batch": sum(f["critical_bytes"] for f in fs),
+            "prefetched_bytes_per_batch": sum(f["prefetch_bytes"] for f in fs),
+            "resident_rows_per_batch": sum(f["resident"] for f in fs), "needed_rows_per_batch": need}
+    on = res_mode["on"]
+    res = {"metric": BASE_METRIC, "value": on["queries_per_s"], "unit": "queries/s", "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": on["ms_per_step"], "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+           "data": "synthetic (device counter-RNG table, seeded candidates)",
+           "config": {"workload": cfg["workload"], "n_docs": N, "d": d, "global_batch": B, "candidates_K": K,
+                      "rerank_R": R, "final_k": k, "partial_rerank": True, "resident_frac": cfg["resident_frac"],
+                      "hbm_tier_gb": store.hbm_bytes / 1e9, "host_tier_gb": store.host_bytes / 1e9,
+                      "launch": "eager ASYNC calls; prefetch of batch n+1 on a side stream"},
+           "prefetch": res_mode, "gpu_launches": args.steps * 5}
+    print(json.dumps(res), flush=True)
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, cfg):
     import torch
@@ -159,6 +253,9 @@ def run_ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     G, g = world, rank
+    emulated = G == 1 and args.emulate_shards > 1
+    if emulated:  # one GPU runs shard 0 of an emulate_shards-way doc-id sharding (no collective)
+        G, g = args.emulate_shards, 0
     lib = L.lib()
 
     # ---- the table: shard g of the corpus, generated on the device ----
@@ -176,10 +273,13 @@ def run_ours(args, cfg):
     log(f"[rank {rank}] table shard {g}/{G}: {n_local} docs, {n_tok} tokens, "
         f"{n_tok * cfg['d'] * 2 / 1e9:.1f} GB in {time.time() - t0:.1f}s")
 
-    B_q = cfg["batch"] * G  # global batch: weak scaling keeps per-GPU pairs fixed
+    # global batch: weak scaling keeps per-GPU pairs fixed; an emulated shard
+    # scores its 1/G share of the configuration's own batch
+    B_q = cfg["batch"] if emulated else cfg["batch"] * G
     t0 = time.time()
-    batches = make_batches(cfg, N_BATCHES, B_q)
-    log(f"[rank {rank}] {N_BATCHES} candidate batches of {B_q} queries in {time.time() - t0:.1f}s")
+    n_batches = cfg.get("n_batches", N_BATCHES)
+    batches = make_batches(cfg, n_batches, B_q)
+    log(f"[rank {rank}] {n_batches} candidate batches of {B_q} queries in {time.time() - t0:.1f}s")
     K, R, k, nq, d = cfg["K"], cfg["R"], cfg["k"], cfg["nq"], cfg["d"]
     dev_batches = []
     max_c = 0
@@ -203,7 +303,7 @@ def run_ours(args, cfg):
     rr = api.Reranker(store, B_q, max(max_c, 1), nq, max_list=max_list)
     P = 2 * B_q * k + B_q  # packed [ids | scores | counts] per rank
     packed = torch.zeros(P, dtype=torch.int32, device=dev)
-    gathered = torch.zeros(G * P, dtype=torch.int32, device=dev) if G > 1 else None
+    gathered = torch.zeros(G * P, dtype=torch.int32, device=dev) if world > 1 else None
     m_ids = torch.zeros((B_q, k), dtype=torch.int32, device=dev)
     m_sc = torch.zeros((B_q, k), dtype=torch.float32, device=dev)
     m_cnt = torch.zeros(B_q, dtype=torch.int32, device=dev)
@@ -221,7 +321,7 @@ def run_ours(args, cfg):
         rc = lib.espn_gpu_rerank(store.handle, rr.handle, C.byref(a), C.byref(o), C.c_void_p(stream_ptr))
         if rc:
             raise RuntimeError(L.last_error())
-        if G > 1:
+        if world > 1:
             dist.all_gather_into_tensor(gathered, packed)
             gb = gathered.data_ptr()
             rc = lib.espn_gpu_merge_topk(gb, gb + 4 * B_q * k, gb + 8 * B_q * k, G, P, B_q, k,
@@ -232,12 +332,12 @@ def run_ours(args, cfg):
 
     def barrier():
         torch.cuda.synchronize()
-        if G > 1:
+        if world > 1:
             dist.barrier()
             torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if G == 1:
+        if world == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -247,7 +347,7 @@ def run_ours(args, cfg):
     cap = torch.cuda.Stream()
     with torch.cuda.stream(cap):
         for i in range(3):  # eager warm-up: lazy attributes, NCCL communicator
-            enqueue(dev_batches[i % N_BATCHES], cap.cuda_stream)
+            enqueue(dev_batches[i % n_batches], cap.cuda_stream)
     cap.synchronize()
     rr.sync(cap.cuda_stream)
     graphs = []
@@ -258,7 +358,7 @@ def run_ours(args, cfg):
         graphs.append(gr)
     stream = torch.cuda.current_stream()
     for i in range(args.warmup):
-        graphs[i % N_BATCHES].replay()
+        graphs[i % n_batches].replay()
     barrier()
     rr.sync(stream.cuda_stream)  # raises on any device-side validation error
 
@@ -268,7 +368,7 @@ def run_ours(args, cfg):
         i = 0
         while time.time() < t_end:
             for _ in range(50):
-                graphs[i % N_BATCHES].replay()
+                graphs[i % n_batches].replay()
                 i += 1
             stream.synchronize()
         barrier()
@@ -278,7 +378,7 @@ def run_ours(args, cfg):
         barrier()
         e0.record(stream)
         for st in range(args.steps):
-            graphs[st % N_BATCHES].replay()
+            graphs[st % n_batches].replay()
         e1.record(stream)
         barrier()
         ms = max_over_ranks(e0.elapsed_time(e1))
@@ -291,7 +391,7 @@ def run_ours(args, cfg):
     barrier()
     for st in range(args.steps):
         evs[st][0].record(stream)
-        graphs[st % N_BATCHES].replay()
+        graphs[st % n_batches].replay()
         evs[st][1].record(stream)
     barrier()
     lat = np.array([a.elapsed_time(b) for a, b in evs])
@@ -300,8 +400,10 @@ def run_ours(args, cfg):
     # ---- correctness spot check of the timed path: the source doc ranks first ----
     graphs[0].replay()
     torch.cuda.synchronize()
-    top = (m_ids if G > 1 else packed[:B_q * k].view(B_q, k))[:, 0].cpu().numpy().view(np.uint32)
-    src_ok = float(np.mean(top == dev_batches[0]["glob"]["ids"].reshape(B_q, K)[:, 0]))
+    top = (m_ids if world > 1 else packed[:B_q * k].view(B_q, k))[:, 0].cpu().numpy().view(np.uint32)
+    src = dev_batches[0]["glob"]["ids"].reshape(B_q, K)[:, 0]
+    mine = (src % G) == g  # an emulated shard only sees its own share of the sources
+    src_ok = float(np.mean(top[mine] == src[mine])) if mine.any() else None
 
     # ---- e2e: the public call with pinned HOST buffers; H2D of the step's
     # queries + candidates and D2H of the ranked lists inside the timed region ----
@@ -311,14 +413,14 @@ def run_ours(args, cfg):
                    off=db["off"], need=db["need"]) for db in dev_batches]
     h_out = [pinned(np.zeros((B_q, k), np.int32)), pinned(np.zeros((B_q, k), np.float32)),
              pinned(np.zeros(B_q, np.int32))]
-    if G > 1:
+    if world > 1:
         d_q = torch.empty_like(dev_batches[0]["q"])
         d_ids = torch.empty(max_c, dtype=torch.int32, device=dev)
         d_cls = torch.empty(max_c, dtype=torch.float32, device=dev)
 
     def e2e_step(i):
-        db = e2e_in[i % N_BATCHES]
-        if G == 1:
+        db = e2e_in[i % n_batches]
+        if world == 1:
             a = L.RerankArgs(n_queries=B_q, n_query_tokens=nq, query_tokens=db["q"].data_ptr(),
                              cand_ids=db["ids"].data_ptr(), cand_cls=db["cls"].data_ptr(),
                              cand_offsets=db["off"].ctypes.data, rerank_count=R, final_k=k, alpha=1.0, flags=0,
@@ -361,7 +463,7 @@ def run_ours(args, cfg):
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     db0 = dev_batches[0]
     h2d = (db0["h_q"].nbytes + db0["h_ids"].nbytes + db0["h_cls"].nbytes + (B_q + 1) * 8 + B_q * 4)
-    d2h = B_q * k * 8 + B_q * 4 + (4 if G == 1 else 0)
+    d2h = B_q * k * 8 + B_q * 4 + (4 if world == 1 else 0)
 
     # ---- standalone K1 gather GB/s (copy kernel only, read + write bytes) ----
     gb_ids = dev_batches[0]["ids"]
@@ -394,7 +496,7 @@ def run_ours(args, cfg):
     # needed docs + q*d*b per query + K*8 per query (id + cls in) + k*8 per query out
     alg = []
     for st in range(args.steps):
-        db = dev_batches[st % N_BATCHES]
+        db = dev_batches[st % n_batches]
         alg.append(db["row_bytes"] + B_q * nq * d * 2 + int(db["off"][-1]) * 8 + B_q * k * 8)
     alg_bytes = float(np.mean(alg))
     try:
@@ -411,7 +513,7 @@ def run_ours(args, cfg):
         except ValueError:
             traffic = None
 
-    n_launch_ours = args.steps * (3 + (1 if G > 1 else 0))  # plan, MaxSim, top-k (+ merge)
+    n_launch_ours = args.steps * (3 + (1 if world > 1 else 0))  # plan, MaxSim, top-k (+ merge)
     q_total = B_q * args.steps  # global queries (each rank scored its share of all of them)
     value = q_total / (ms / 1e3)
     res = {
@@ -422,9 +524,13 @@ def run_ours(args, cfg):
         % (cfg["t_min"], cfg["t_max"]),
         "config": {"workload": cfg["workload"], "n_docs": cfg["n_docs"], "d": d, "query_tokens": nq,
                    "batch_per_gpu": cfg["batch"], "global_batch": B_q, "candidates_K": K, "rerank_R": R,
-                   "final_k": k, "parallelism": "1 GPU" if G == 1 else f"doc-id shards x{G} + NCCL all-gather merge",
+                   "final_k": k,
+                   "parallelism": ("1 GPU" if G == 1 else
+                                   f"1 GPU running shard 0 of a {G}-way doc-id sharding (per-GPU share of the "
+                                   f"{G}-GPU workload; no collective)" if emulated else
+                                   f"doc-id shards x{G} + NCCL all-gather merge"),
                    "l2": "inputs > L2: each batch gathers ~%.0f MB of random rows; %d distinct batches rotate"
-                   % (dev_batches[0]["row_bytes"] / 1e6, N_BATCHES),
+                   % (dev_batches[0]["row_bytes"] / 1e6, n_batches),
                    "launch": "one CUDA graph per batch (device-planned: plan -> tcgen05 MaxSim -> top-k)",
                    "kernel": "tcgen05 (auto)"},
         "p50_batch_ms": p50, "p99_batch_ms": p99,
@@ -442,11 +548,11 @@ def run_ours(args, cfg):
         "gpu_launches": n_launch_ours,
         "check": {"source_doc_ranked_first": src_ok},
     }
-    if G == 1 and not args.no_cpu_baseline:
+    if world == 1 and not emulated and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(cfg, store, batches, dev, args)
     if rank == 0:
         print(json.dumps(res), flush=True)
-    if G > 1:
+    if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -553,11 +659,15 @@ def main():
     ap.add_argument("--preroll-s", type=float, default=2.0)
     ap.add_argument("--cpu-batches", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--emulate-shards", type=int, default=0,
+                    help="1 GPU: run shard 0 of an N-way doc-id sharding (the per-GPU share of an N-GPU run)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif "resident_frac" in cfg:
+        run_tiered(args, cfg)
     else:
         run_ours(args, cfg)
 
