@@ -148,6 +148,9 @@ ESPN_API int espn_gpu_workspace_destroy(espn_gpu_workspace* ws);
 #define ESPN_RERANK_PREFETCHED 0x40u  /* tiered table: this batch was staged by the last
                                          espn_gpu_prefetch of this workspace (same ids/offsets);
                                          otherwise host-tier rows are staged on the critical path */
+#define ESPN_RERANK_SEPARATE_TOPK 0x80u /* rank in a separate top-k kernel instead of inside the
+                                         tcgen05 MaxSim kernel (the fused path is the default when
+                                         final_k <= 32; results are identical) */
 #define ESPN_RERANK_DEVICE_OFFSETS 0x20u /* cand_offsets / needed_counts are DEVICE pointers (needs
                                          DEVICE_IO): the batch is planned on the device, the call has
                                          no host-side loop, no host sync with ASYNC, and is CUDA-graph
@@ -260,6 +263,12 @@ typedef struct {
   uint64_t maxsim_device_launches;
 } espn_counters;
 ESPN_API int espn_gpu_get_counters(const espn_gpu_workspace* ws, espn_counters* out);
+
+/* Profiling only (no reference counterpart): per-kernel device timeline of
+   the re-rank step, recorded when ESPN_DEBUG has bit 256 set.  out8 = {plan
+   start, plan end, MaxSim start, MaxSim end, top-k start, top-k end, 0, 0} (globaltimer ns; min over CTA starts, max over CTA ends).
+   Synchronises the device; reset != 0 re-arms the recorder. */
+ESPN_API int espn_gpu_debug_timeline(int device, uint64_t* out8, int reset);
 
 /* Synthetic MS-MARCO-shaped table generation on the device (bench/tests):
  * t ~ U{t_min..t_max} per doc and i.i.d. N(0,1) rows L2-normalised per row,

@@ -37,6 +37,7 @@ ESPN_RERANK_WRITE_BOW = 0x8
 ESPN_RERANK_PROFILE = 0x10
 ESPN_RERANK_DEVICE_OFFSETS = 0x20
 ESPN_RERANK_PREFETCHED = 0x40
+ESPN_RERANK_SEPARATE_TOPK = 0x80
 
 
 class TableDesc(C.Structure):
@@ -111,6 +112,7 @@ SIGNATURES = {
     "espn_gpu_merge_topk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32,
                                       C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "espn_gpu_get_counters": (C.c_int, [C.c_void_p, C.POINTER(Counters)]),
+    "espn_gpu_debug_timeline": (C.c_int, [C.c_int, C.c_void_p, C.c_int]),
     "espn_gpu_synth_table": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                        C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "espn_gpu_gather_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),

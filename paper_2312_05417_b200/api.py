@@ -376,7 +376,7 @@ class Reranker:
     def rerank_arrays(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig,
                       kernel: str = "auto", device_io: bool = False, write_bow: bool = False,
                       out=None, stream=None, sync: bool = True, needed_counts=None, prefetched: bool = False,
-                      fetch_stats: bool = False):
+                      fetch_stats: bool = False, separate_topk: bool = False):
         """Batched stages 3-6.  query_tokens (B, q, d) fp32; cand_* CSR over
         queries with cand_offsets (B+1, host uint64).  Host numpy arrays by
         default (copied in and out inside the call); device torch tensors
@@ -412,6 +412,8 @@ class Reranker:
             flags |= L.ESPN_RERANK_ASYNC
         if prefetched:
             flags |= L.ESPN_RERANK_PREFETCHED
+        if separate_topk:
+            flags |= L.ESPN_RERANK_SEPARATE_TOPK
         args = L.RerankArgs(n_queries=B, n_query_tokens=nq, query_tokens=_ptr(query_tokens),
                             cand_ids=_ptr(cand_ids), cand_cls=_ptr(cand_cls), cand_offsets=offs.ctypes.data,
                             rerank_count=int(config.rerank_count), final_k=k, alpha=float(config.alpha),

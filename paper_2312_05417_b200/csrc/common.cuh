@@ -4,6 +4,24 @@
 
 namespace espn_k {
 
+// ESPN_DEBUG bit 256: per-kernel device timeline of the re-rank step (first
+// CTA start, last CTA end, globaltimer ns) -- slot 0 plan, 1 MaxSim, 2 top-k.
+// Read/reset through espn_gpu_debug_timeline (profiling only).
+__device__ unsigned long long g_ktl[8];
+__device__ unsigned long long g_fin[8];  // profiling: summed finalize phase times
+__device__ unsigned long long g_cta_prof[4 * 256];  // per CTA: end, rank-warp end, merges, dedup-warp end
+__device__ __forceinline__ unsigned long long ktl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ktl_begin(uint32_t dbg, int k) {
+  if ((dbg & 256u) && threadIdx.x == 0) atomicMin(&g_ktl[2 * k], ktl_now());
+}
+__device__ __forceinline__ void ktl_end(uint32_t dbg, int k) {
+  if ((dbg & 256u) && threadIdx.x == 0) atomicMax(&g_ktl[2 * k + 1], ktl_now());
+}
+
 // Global doc id -> local row index of this shard, or UINT64_MAX if the id is
 // not stored here (unknown id / wrong shard -> DataIntegrityError).
 __device__ __forceinline__ uint64_t shard_local(uint32_t id, uint32_t count, uint32_t index,
@@ -96,7 +114,43 @@ struct PlanParams {
   uint32_t rerank_count;
   uint32_t unit_docs;          // docs per unit (tcgen05); 1 for SIMT (units = pairs)
   uint32_t write_tab;          // 1: tcgen05 (fill unit_tab)
+  uint32_t tail_units;         // 1: fused top-k with partial re-rank -- also plan the
+                               //    alpha*cls tail [needed, n) as MMA-free units
+  uint32_t* out_counts;        // fused top-k: queries with no unit get count 0 here (else NULL)
+  uint32_t* fused_state;       // fused top-k: advance {epoch, rows per parity} (else NULL)
+  uint32_t dbg;                // profiling knobs (ESPN_DEBUG env; 0 in production)
 };
+
+// Unit-table entry .y: bits 0-7 doc count, bits 8-30 units of the unit's query,
+// bit 31 = alpha*cls tail unit (no MaxSim).
+constexpr uint32_t kUnitTail = 1u << 31;
+constexpr uint32_t kUnitMaxPerQuery = (1u << 23) - 1;
+__host__ __device__ __forceinline__ uint32_t unit_y(uint32_t nd, uint32_t nu, bool tail) {
+  return nd | (nu << 8) | (tail ? kUnitTail : 0u);
+}
+
+// Ranking keys: key = orderable(score) << 32 | ~doc_id, so "larger key first"
+// is exactly rank()'s (score desc, doc_id asc) (scoring.hpp:16-18); key 0 is
+// never produced by a finite score and marks an empty entry.
+__device__ __forceinline__ uint32_t float_order(float f) {
+  const uint32_t u = __float_as_uint(f + 0.0f);  // canonical +0
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float order_float(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+__device__ __forceinline__ uint64_t make_key(float s, uint32_t id) {
+  return ((uint64_t)float_order(s) << 32) | (uint64_t)(~id);
+}
+// Warp-wide max of a 64-bit key: two 32-bit redux.sync steps (high word, then
+// low word among the lanes holding the high maximum).
+__device__ __forceinline__ uint64_t warp_max_key(uint64_t v) {
+  const uint32_t hi = (uint32_t)(v >> 32);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? (uint32_t)v : 0u);
+  return ((uint64_t)mh << 32) | ml;
+}
+constexpr int kFusedMaxK = 32;
 
 // Absolute address of doc `loc`'s rows: untiered tables keep every row in one
 // HBM buffer; tiered tables carry a per-doc address with the
@@ -135,7 +189,26 @@ struct MaxSimParams {
   // over CTAs -> end of the last CTA), accumulated as {sum_ns, launches,
   // start scratch, CTA-done counter}; graph-replay safe.  NULL = off.
   unsigned long long* prof;
+  // Fused aggregate + top-k (combine warp); out_ids == NULL: off,
+  // the separate top-k kernel runs instead.
+  const float* cand_cls;
+  float alpha;
+  uint32_t k;                  // final_k (<= kFusedMaxK)
+  uint32_t* out_ids;           // B * k
+  float* out_scores;           // B * k
+  uint32_t* out_counts;        // B
+  unsigned long long* unit_top;  // per work unit: its best k keys, descending
+  // Duplicate hash, double-buffered by batch parity: a fused batch inserts
+  // into table[parity] and clears the rows table[parity ^ 1] held for the
+  // previous fused batch (the state word pair {epoch, rows used per parity}
+  // is advanced by plan_kernel), so no kernel pays a clear on its critical path.
+  uint32_t* dedup;             // 2 x max_queries x hash_slots ids, 0xFFFFFFFF = empty
+  uint32_t* ff_seen;           // 2 x max_queries: id 0xFFFFFFFF (the empty code) seen
+  const uint32_t* fused_state; // {epoch, queries used by parity 0, by parity 1}
+  uint32_t hash_slots;         // power of two >= 2 x longest scored list (8x: one-probe inserts)
+  uint32_t max_queries;        // parity stride of dedup / ff_seen
 };
+
 
 struct TopKParams {
   const float* bow;            // per candidate MaxSim (valid for the first R of each query)

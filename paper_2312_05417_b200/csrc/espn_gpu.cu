@@ -97,7 +97,7 @@ int tc_unit_docs_rt(uint32_t d, uint32_t max_t) {
 }
 
 template <int D>
-cudaError_t launch_tc(const MaxSimParams& p, int num_sms, cudaStream_t s) {
+cudaError_t launch_tc(const MaxSimParams& p, int num_sms, cudaStream_t s, bool pdl) {
   using L = TcLayout<D>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -106,17 +106,27 @@ cudaError_t launch_tc(const MaxSimParams& p, int num_sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  // persistent: one CTA per SM; the unit count is read on the device
-  maxsim_tc_kernel<D><<<num_sms, L::NTHREADS, L::SMEM_BYTES, s>>>(p);
-  return cudaGetLastError();
+  // persistent: one CTA per SM; the unit count is read on the device.  As a
+  // programmatic dependent of plan_kernel (pdl) its prologue overlaps the plan.
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(num_sms);
+  lc.blockDim = dim3(L::NTHREADS);
+  lc.dynamicSmemBytes = L::SMEM_BYTES;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, maxsim_tc_kernel<D>, p);
 }
 
-cudaError_t launch_tc_rt(uint32_t d, const MaxSimParams& p, int num_sms, cudaStream_t s) {
+cudaError_t launch_tc_rt(uint32_t d, const MaxSimParams& p, int num_sms, cudaStream_t s, bool pdl) {
   switch (d) {
-    case 16: return launch_tc<16>(p, num_sms, s);
-    case 32: return launch_tc<32>(p, num_sms, s);
-    case 64: return launch_tc<64>(p, num_sms, s);
-    case 128: return launch_tc<128>(p, num_sms, s);
+    case 16: return launch_tc<16>(p, num_sms, s, pdl);
+    case 32: return launch_tc<32>(p, num_sms, s, pdl);
+    case 64: return launch_tc<64>(p, num_sms, s, pdl);
+    case 128: return launch_tc<128>(p, num_sms, s, pdl);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -215,6 +225,12 @@ struct espn_gpu_workspace {
   uint32_t* needed_in = nullptr;  // staged needed_counts (host-offset mode)
   uint32_t* n_units = nullptr;    // planned unit count (device)
   uint32_t max_list = 0;          // longest candidate list the top-k hash is sized for
+  // fused top-k (tcgen05 path, final_k <= kFusedMaxK)
+  unsigned long long* unit_top = nullptr;  // max_units x kFusedMaxK keys
+  uint32_t* dedup = nullptr;               // 2 x B x hash_slots (0xFF.. = empty), by batch parity
+  uint32_t* ff_seen = nullptr;             // 2 x B
+  uint32_t* fused_state = nullptr;         // {epoch, rows used by parity 0, parity 1}
+  uint32_t hash_slots = 0;
   unsigned long long* kprof = nullptr;  // device-timed MaxSim {sum_ns, launches, start, done}
   // tiered tables: two staging slots (one scoring, one being prefetched)
   struct Stage {
@@ -555,7 +571,7 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   // work-unit table capacity: every query may end in a partial unit
   {
     const int ud = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
-    w->max_units = ud > 0 ? (C + ud - 1) / ud + B : 0;
+    w->max_units = ud > 0 ? (C + ud - 1) / ud + 2 * B : 0;  // + partial units (needed, tail)
   }
   al((void**)&w->unit_tab, w->max_units * sizeof(uint4));
   al((void**)&w->needed_in, B * sizeof(uint32_t));
@@ -578,6 +594,19 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   }
   if (e == cudaSuccess) e = cudaMallocHost(&w->h_qstats, B * 6 * sizeof(unsigned long long));
   w->max_list = desc->max_list ? desc->max_list : (uint32_t)std::min<size_t>(C, 4096);
+  // fused top-k state; the dedup hash is 8x the declared list (one-probe
+  // inserts), at most 32K slots (lists up to 16K candidates)
+  w->hash_slots = 128;
+  while (w->hash_slots < 8ull * w->max_list && w->hash_slots < (1u << 15)) w->hash_slots <<= 1;
+  if (w->max_units && 2ull * w->max_list <= w->hash_slots) {
+    al((void**)&w->unit_top, w->max_units * kFusedMaxK * sizeof(unsigned long long));
+    al((void**)&w->dedup, 2 * B * (size_t)w->hash_slots * sizeof(uint32_t));
+    al((void**)&w->ff_seen, 2 * B * sizeof(uint32_t));
+    al((void**)&w->fused_state, 4 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(w->ff_seen, 0, 2 * B * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(w->fused_state, 0, 4 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(w->dedup, 0xFF, 2 * B * (size_t)w->hash_slots * sizeof(uint32_t));
+  }
   al((void**)&w->bow, C * sizeof(float));
   al((void**)&w->out_ids, B * kMaxK * sizeof(uint32_t));
   al((void**)&w->out_scores, B * kMaxK * sizeof(float));
@@ -611,6 +640,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   cudaFree(w->q32); cudaFree(w->ids); cudaFree(w->cls); cudaFree(w->cand_off);
   cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->needed_in); cudaFree(w->n_units);
   cudaFree(w->kprof);
+  cudaFree(w->unit_top); cudaFree(w->dedup); cudaFree(w->ff_seen); cudaFree(w->fused_state);
   for (auto& st : w->stage) {
     if (st.done) cudaEventSynchronize(st.done);
     if (st.free_ev) cudaEventSynchronize(st.free_ev);
@@ -691,6 +721,11 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   // host CUDA events only outside stream capture (device offsets = graph-capturable
   // mode); the MaxSim kernel times itself on the device in both modes
   const bool profile = profile_dev && !dev_off;
+  // Fused aggregate + top-k (and duplicate check) inside the tcgen05 MaxSim
+  // kernel when final_k <= 32 and the workspace's dedup hash covers the
+  // lists; ESPN_DEBUG bit 512 / ESPN_RERANK_SEPARATE_TOPK: separate top-k kernel.
+  const bool fused = tc && k <= (uint32_t)kFusedMaxK && w->dedup != nullptr && 2ull * max_list <= w->hash_slots &&
+                     !(a->flags & ESPN_RERANK_SEPARATE_TOPK) && !(dbg & 512u);
   const int pslot = (int)(w->prof_calls % espn_gpu_workspace::kProf);
   if (profile) drain_prof(w, pslot);
 
@@ -745,6 +780,10 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   pp.rerank_count = a->rerank_count;
   pp.unit_docs = tc ? (uint32_t)unit_docs : 1u;
   pp.write_tab = tc ? 1u : 0u;
+  pp.tail_units = (fused && partial) ? 1u : 0u;
+  pp.out_counts = fused ? (dev_io ? o->counts : w->out_counts) : nullptr;
+  pp.fused_state = fused ? w->fused_state : nullptr;
+  pp.dbg = dbg;
   plan_kernel<<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp);
   ESPN_CUDA_TRY(cudaGetLastError());
 
@@ -791,8 +830,23 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
   mp.dbg = dbg;
   mp.prof = (profile_dev && tc) ? w->kprof : nullptr;
+  if (fused) {
+    mp.cand_cls = cls;
+    mp.alpha = a->alpha;
+    mp.k = k;
+    mp.out_ids = dev_io ? o->ids : w->out_ids;
+    mp.out_scores = dev_io ? o->scores : w->out_scores;
+    mp.out_counts = dev_io ? o->counts : w->out_counts;
+    mp.unit_top = w->unit_top;
+    mp.dedup = w->dedup;
+    mp.ff_seen = w->ff_seen;
+    mp.fused_state = w->fused_state;
+    mp.hash_slots = w->hash_slots;
+    mp.max_queries = w->max_queries;
+  }
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
-  cudaError_t e = tc ? launch_tc_rt(t->d, mp, t->num_sms, s) : launch_simt_rt(t->d, mp, t->num_sms, s);
+  cudaError_t e = tc ? launch_tc_rt(t->d, mp, t->num_sms, s, /*pdl=*/slot < 0 && !profile)
+                     : launch_simt_rt(t->d, mp, t->num_sms, s);
   if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
   if (slot >= 0) {  // the slot may be re-staged once this MaxSim finished
     ESPN_CUDA_TRY(cudaEventRecord(w->stage[slot].free_ev, s));
@@ -800,7 +854,23 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[1], s));
 
-  // ---- K3: aggregate + top-k ----
+  if (fused) {
+    // ---- K3': merge of the per-unit top-k lists (programmatic dependent) ----
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((B + kFinalizeWarps - 1) / kFinalizeWarps);
+    lc.blockDim = dim3(kFinalizeWarps * 32);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = (dbg & 0x10000u) ? 1 : 0;  // plain launch: as a programmatic dependent its CTAs
+                                             // crowd onto the first SMs MaxSim frees
+    ESPN_CUDA_TRY(cudaLaunchKernelEx(&lc, finalize_kernel, mp));
+  }
+
+  // ---- K3: aggregate + top-k (unless fused into MaxSim) ----
+  if (!fused) {
   ESPN_CUDA_TRY(ensure_topk_attr());
   TopKParams tp{};
   tp.bow = w->bow;
@@ -849,6 +919,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
       ESPN_CUDA_TRY(cudaGetLastError());
     }
   }
+  }
   if (profile) {
     ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[2], s));
     w->prof[pslot].pending = true;
@@ -868,7 +939,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
   w->counters.batches += 1;
   w->counters.queries += B;
-  w->counters.kernel_launches += 3;
+  w->counters.kernel_launches += 3 + (t->tiered && !(a->flags & ESPN_RERANK_PREFETCHED) ? 1 : 0);
   if (a->flags & ESPN_RERANK_ASYNC) {
     w->async_pending = true;
     return ESPN_OK;
@@ -1060,6 +1131,25 @@ int espn_gpu_gather_rows(espn_gpu_table* t, const uint32_t* ids, uint64_t n, con
     default: return fail(ESPN_E_INVALID_CONFIG, "gather supports d in {8,16,32,48,64,96,128,256}");
   }
   ESPN_CUDA_TRY(cudaGetLastError());
+  return ESPN_OK;
+}
+
+int espn_gpu_debug_timeline(int device, uint64_t* out8, int reset) {
+  DeviceGuard g(device);
+  if (out8) {
+    ESPN_CUDA_TRY(cudaDeviceSynchronize());
+    ESPN_CUDA_TRY(cudaMemcpyFromSymbol(out8, espn_k::g_ktl, 8 * sizeof(uint64_t)));
+    if (reset == 2) ESPN_CUDA_TRY(cudaMemcpyFromSymbol(out8 + 8, espn_k::g_cta_prof, 4 * 256 * sizeof(uint64_t)));
+    if (reset == 3) ESPN_CUDA_TRY(cudaMemcpyFromSymbol(out8 + 8, espn_k::g_fin, 8 * sizeof(uint64_t)));
+  }
+  if (reset) {
+    unsigned long long init[8];
+    for (int i = 0; i < 8; ++i) init[i] = (i & 1) || i >= 6 ? 0ull : ~0ull;
+    ESPN_CUDA_TRY(cudaMemcpyToSymbol(espn_k::g_ktl, init, sizeof init));
+    static unsigned long long zero[4 * 256] = {};
+    ESPN_CUDA_TRY(cudaMemcpyToSymbol(espn_k::g_cta_prof, zero, sizeof zero));
+    ESPN_CUDA_TRY(cudaMemcpyToSymbol(espn_k::g_fin, zero, 8 * sizeof(uint64_t)));
+  }
   return ESPN_OK;
 }
 

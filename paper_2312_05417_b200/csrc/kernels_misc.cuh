@@ -105,9 +105,16 @@ __device__ __forceinline__ uint64_t plan_units(const PlanParams& q, uint32_t b, 
   const uint64_t cap = q.needed_in ? (uint64_t)q.needed_in[b] : (uint64_t)q.rerank_count;
   const uint64_t need = n < cap ? n : cap;
   *need_out = (uint32_t)need;
-  return q.write_tab ? (need + q.unit_docs - 1) / q.unit_docs : need;
+  if (!q.write_tab) return need;
+  uint64_t u = (need + q.unit_docs - 1) / q.unit_docs;
+  if (q.tail_units) u += (n - need + q.unit_docs - 1) / q.unit_docs;
+  return u;
 }
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q) {
+  ktl_begin(q.dbg, 0);
+  // the MaxSim kernel is a programmatic dependent: its prologue (barriers,
+  // TMEM, operand zeroing) overlaps this kernel; it waits before reading the plan
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ uint64_t wsum[kPlanThreads / 32];
   __shared__ uint64_t base_sh;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -148,6 +155,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q) 
   const bool last = b + 1 == q.n_queries;
   bool over = false;
   if (last && (q.cand_off[q.n_queries] > q.max_candidates || excl + u > q.max_units)) over = true;
+  if (u > kUnitMaxPerQuery) over = true;
   // the last CTA has seen every query (prefix loop + its own): its verdict is global
   const bool any_bad = __syncthreads_or(bad);
   if (any_bad && tid == 0) atomicOr(q.err, ERR_BAD_OFFSETS);
@@ -156,19 +164,32 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q) 
     q.needed[b] = need;
     q.unit_off[b] = (uint32_t)excl;
     if (q.write_tab && excl + u <= q.max_units) {
-      const uint64_t c0 = q.cand_off[b];
+      // MaxSim units over [0, need), then (fused partial re-rank) alpha*cls
+      // tail units over [need, n)
+      const uint64_t c0 = q.cand_off[b], n = q.cand_off[b + 1] - c0;
+      const uint64_t um = (need + q.unit_docs - 1) / q.unit_docs;
       for (uint64_t j = 0; j < u; ++j) {
-        const uint64_t c = c0 + j * q.unit_docs;
-        const uint32_t nd = (uint32_t)min((uint64_t)q.unit_docs, (uint64_t)need - j * q.unit_docs);
-        q.unit_tab[excl + j] = make_uint4(b, nd, (uint32_t)c, (uint32_t)(c >> 32));
+        const bool tail = j >= um;
+        const uint64_t first = tail ? need + (j - um) * q.unit_docs : j * q.unit_docs;
+        const uint64_t end = tail ? n : (uint64_t)need;
+        const uint64_t c = c0 + first;
+        const uint32_t nd = (uint32_t)min((uint64_t)q.unit_docs, end - first);
+        q.unit_tab[excl + j] = make_uint4(b, unit_y(nd, (uint32_t)u, tail), (uint32_t)c, (uint32_t)(c >> 32));
       }
     }
+    if (q.out_counts && u == 0) q.out_counts[b] = 0;  // fused top-k: no unit will rank this query
   }
   if (last) {
+    if (q.fused_state) {  // fused top-k: this batch's dedup parity and the rows it uses
+      const uint32_t ep = q.fused_state[0] + 1u;
+      q.fused_state[0] = ep;
+      q.fused_state[1 + (ep & 1u)] = q.n_queries;
+    }
     q.unit_off[q.n_queries] = (uint32_t)(excl + u);
     // read by the MaxSim kernel; an invalid batch gets an empty plan
     *q.n_units = (any_bad || over) ? 0u : (uint32_t)(excl + u);
   }
+  ktl_end(q.dbg, 0);
 }
 
 // ============================================================================
@@ -182,16 +203,6 @@ constexpr int kTopkSort = 4096;      // keys per sort pass (32 KB)
 constexpr int kTopkHash = 8192;      // duplicate-detection hash slots
 constexpr int kMaxK = 1024;
 
-__device__ __forceinline__ uint32_t float_order(float f) {
-  const uint32_t u = __float_as_uint(f + 0.0f);  // canonical +0
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float order_float(uint32_t o) {
-  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
-}
-__device__ __forceinline__ uint64_t make_key(float s, uint32_t id) {
-  return ((uint64_t)float_order(s) << 32) | (uint64_t)(~id);
-}
 
 // Descending bitonic sort of keys[0..n) (n power of two) by the whole block.
 __device__ void bitonic_sort_desc(uint64_t* keys, int n) {
@@ -247,6 +258,7 @@ topk_kernel(const TopKParams p) {
   uint64_t* best = keys + kTopkSort;
   uint32_t* hash = reinterpret_cast<uint32_t*>(best + kMaxK);
   const uint32_t b = blockIdx.x;
+  ktl_begin(p.dbg, 2);
   if (*p.err & (ERR_BAD_OFFSETS | ERR_CAPACITY)) return;  // plan rejected the batch
   const uint64_t c0 = p.cand_off[b];
   const uint64_t n = p.cand_off[b + 1] - c0;
@@ -312,6 +324,7 @@ topk_cta_kernel(const TopKParams p, uint32_t hash_slots) {
   __shared__ int any_pending;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t b = blockIdx.x;
+  ktl_begin(p.dbg, 2);
   if (*p.err & (ERR_BAD_OFFSETS | ERR_CAPACITY)) return;  // plan rejected the batch
   const uint64_t c0 = p.cand_off[b];
   const uint64_t n = p.cand_off[b + 1] - c0;
@@ -443,6 +456,7 @@ topk_cta_kernel(const TopKParams p, uint32_t hash_slots) {
     }
     if (lane == 0) p.out_counts[b] = r;
   }
+  ktl_end(p.dbg, 2);
 }
 
 // K4: merge n_lists ranked lists per query ([list][query][k]) into one top-k.

@@ -73,7 +73,10 @@ struct TcLayout {
   static constexpr int PROD_WARP0 = NEPI + 1;
   static constexpr int LOADER_WARP = PROD_WARP0 + NPROD;
   static constexpr int COMBINE_WARP = LOADER_WARP + 1;
-  static constexpr int NWARPS = COMBINE_WARP + 1;
+  static constexpr int DEDUP_WARP = COMBINE_WARP + 1;  // fused top-k: duplicate check
+  static constexpr int RANK_WARP = DEDUP_WARP + 1;     // fused top-k: keys, unit top-k
+  static constexpr int NWARPS = RANK_WARP + 1;
+  static constexpr int NB = 8;                     // bow ring (combine -> rank) depth, in units
   static constexpr int HALF = NQC / 2;             // columns per epilogue warp per stage
   static constexpr int LW = HALF < 32 ? HALF : 32; // tcgen05.ld width (columns)
   static constexpr int NLD = HALF / LW;            // loads per epilogue warp per stage
@@ -81,7 +84,7 @@ struct TcLayout {
   static constexpr int NTHREADS = NWARPS * 32;
 
   struct Unit {
-    uint32_t b, nd, S, pad_;
+    uint32_t b, nd, S, tail;   // tail: alpha*cls tail unit (no MaxSim)
     uint64_t cfirst;            // candidate index of the unit's first doc
     uint32_t bitmap[MAXW];      // bit g: a doc starts at group g
     uint32_t wprefix[MAXW];     // docs starting before word w
@@ -97,8 +100,10 @@ struct TcLayout {
   static constexpr int OFF_A = OFF_B + NS * STAGE_BYTES;
   static constexpr int OFF_PM = OFF_A + A_BYTES;
   static constexpr int OFF_UNIT = OFF_PM + PM_FLOATS * 4;
-  static constexpr int OFF_BAR = (OFF_UNIT + NU * (int)sizeof(Unit) + 7) / 8 * 8;
-  static constexpr int N_BARS = 2 * NS + 2 * NBUF + 3 * NU;
+  static constexpr int OFF_UK = (OFF_UNIT + NU * (int)sizeof(Unit) + 15) / 16 * 16;  // rank warp: unit keys
+  static constexpr int OFF_RING = OFF_UK + UNITMAX * 8;
+  static constexpr int OFF_BAR = OFF_RING + NB * UNITMAX * 4;
+  static constexpr int N_BARS = 2 * NS + 2 * NBUF + 3 * NU + 2 * NB;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
@@ -119,6 +124,197 @@ __device__ __forceinline__ uint64_t gtimer() {
   do {                                                                           \
     if ((p.dbg & 8u) && blockIdx.x == 0 && (it) < 8) trace[(slot) * 8 + (it)] = gtimer(); \
   } while (0)
+
+// ---- fused top-k helpers (combine warp) --------------------------------------
+// Duplicate rejection of rank() (scoring.hpp:16-18) across all units of a
+// query, by the dedicated dedup warp: the unit's ids go into the query's
+// open-addressing hash in global memory (L2-resident, atomicCAS, 0xFFFFFFFF =
+// empty; that id itself is tracked by ff_seen).  The table is sized 8x the
+// list, so nearly every insert lands on its first probe; a lane's CAS are
+// issued together.  The query's last arrival clears it (fused_merge).
+template <int NK>
+__device__ __forceinline__ void fused_dedup(const MaxSimParams& p, uint32_t par, uint32_t b, uint64_t cfirst,
+                                            uint32_t nd, uint32_t lane) {
+  uint32_t* tab = p.dedup + ((size_t)par * p.max_queries + b) * p.hash_slots;
+  uint32_t* ff = p.ff_seen + (size_t)par * p.max_queries + b;
+  const uint32_t mask = p.hash_slots - 1;
+  uint32_t id[NK], h[NK], pend = 0, dup = 0, full = 0;
+#pragma unroll
+  for (int r = 0; r < NK; ++r) {
+    const uint32_t k = r * 32 + lane;
+    id[r] = k < nd ? __ldg(&p.cand_ids[cfirst + k]) : 0u;
+    h[r] = ((id[r] * 2654435761u) >> 7) & mask;
+    if (k < nd) {
+      if (id[r] == 0xFFFFFFFFu) dup |= atomicExch(ff, 1u);
+      else pend |= 1u << r;
+    }
+  }
+  for (uint32_t probe = 0; pend; ++probe) {
+    uint32_t old[NK];
+#pragma unroll
+    for (int r = 0; r < NK; ++r) old[r] = (pend >> r) & 1u ? atomicCAS(&tab[h[r]], 0xFFFFFFFFu, id[r]) : 0u;
+#pragma unroll
+    for (int r = 0; r < NK; ++r) {
+      if (!((pend >> r) & 1u)) continue;
+      if (old[r] == 0xFFFFFFFFu || old[r] == id[r]) {
+        dup |= old[r] == id[r];
+        pend &= ~(1u << r);
+      } else {
+        h[r] = (h[r] + 1) & mask;
+      }
+    }
+    if (probe >= mask) { full = 1; break; }  // table full: a longer list than the workspace's max_list
+  }
+  if (dup) atomicOr(p.err, ERR_DUPLICATE);
+  if (full) atomicOr(p.err, ERR_CAPACITY);
+}
+
+// The query's last arrival: merge the units' best-k lists (unit_top, each
+// sorted descending, 0 = empty) into the final ranked list, then reset the
+// query's counters.  Keys are unique (duplicate ids are an
+// error), so the final list is "every key whose rank (number of greater keys)
+// is < k".  With all n = nu*k keys staged in shared memory:
+//   * threshold T = max over lists of its k-th key: a key below T has at
+//     least k greater keys, so only keys >= T are candidates (about 2k);
+//   * candidates are compacted in place (ballot prefix), each lane counts
+//     the candidates greater than its own, and writes it at its rank.
+// Longer inputs (n > FMK) fall back to a chunked k-way merge (k rounds of
+// warp max over list heads).
+template <int FMK>
+__device__ __forceinline__ void fused_merge(const MaxSimParams& p, uint32_t b, uint32_t u0, uint32_t nu,
+                                            uint64_t* fm, uint32_t lane) {
+  const uint32_t kk = p.k;
+  const unsigned long long* src = p.unit_top + (size_t)u0 * kk;
+  const uint32_t n = nu * kk;
+  uint32_t cnt = 0;
+  if (n + 8 <= (uint32_t)FMK) {
+    const unsigned long long tf0 = ktl_now();
+    uint64_t th = 0;
+    for (uint32_t i0 = 0; i0 < n; i0 += 256) {  // 8 loads per lane in flight
+      uint64_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t i = i0 + u * 32 + lane;
+        v[u] = i < n ? __ldcg(&src[i]) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t i = i0 + u * 32 + lane;
+        if (i < n) {
+          fm[i] = v[u];
+          if (i % kk == kk - 1 && v[u] > th) th = v[u];
+        }
+      }
+    }
+    th = warp_max_key(th);
+    __syncwarp();
+    const unsigned long long tf1 = ktl_now();
+    uint32_t nc = 0;
+    {  // compact candidates (v >= th, v != 0) to fm[0, nc)
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint64_t v = i < n ? fm[i] : 0ull;
+      const bool c = v != 0 && v >= th;
+      const uint32_t bal = __ballot_sync(0xffffffffu, c);
+      __syncwarp();
+      if (c) fm[nc + __popc(bal & ((1u << lane) - 1u))] = v;
+      nc += __popc(bal);
+      __syncwarp();
+    }
+    for (uint32_t i0 = 0; i0 < nc; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint64_t v = i < nc ? fm[i] : ~0ull;
+      uint32_t rk = 0;
+      for (uint32_t j0 = 0; j0 < nc; j0 += 8) {  // 8 independent broadcast loads per step
+        uint64_t x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = fm[j0 + u];  // fm has >= nc + 8 slots (FMK >= n + 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rk += (j0 + u < nc && x[u] > v) ? 1u : 0u;
+      }
+      if (i < nc && rk < kk) {
+        p.out_ids[(size_t)b * kk + rk] = ~(uint32_t)(v & 0xFFFFFFFFu);
+        p.out_scores[(size_t)b * kk + rk] = order_float((uint32_t)(v >> 32));
+      }
+    }
+    }
+    cnt = min(nc, kk);
+    if ((p.dbg & 256u) && lane == 0) {
+      atomicAdd(&g_fin[0], tf1 - tf0);
+      atomicAdd(&g_fin[1], ktl_now() - tf1);
+      atomicAdd(&g_fin[2], 1ull);
+      atomicAdd(&g_fin[3], nc);
+    }
+  } else {
+    // chunks of up to 63 unit lists plus the running result (list 0); lane l
+    // owns lists l and l+32 and keeps their heads in registers
+    const uint32_t lpc = min(64u, (uint32_t)FMK / kk);
+    uint64_t mine = 0;  // lane r < cnt: the r-th best so far
+    for (uint32_t l0 = 0; l0 < nu; l0 += lpc - 1) {
+      const uint32_t nl = min(lpc - 1, nu - l0) + 1;
+      if (lane < kk) fm[lane] = mine;
+      for (uint32_t i = lane; i < (nl - 1) * kk; i += 32) fm[kk + i] = __ldcg(&src[(size_t)l0 * kk + i]);
+      __syncwarp();
+      uint32_t c0 = 0, c1 = 0;  // cursors of lists lane, lane + 32
+      uint64_t h0 = lane < nl ? fm[lane * kk] : 0ull;
+      uint64_t h1 = lane + 32 < nl ? fm[(lane + 32) * kk] : 0ull;
+      uint32_t c = 0;
+      for (; c < kk; ++c) {
+        const uint64_t lb = h0 > h1 ? h0 : h1;
+        const uint64_t m = warp_max_key(lb);
+        if (m == 0) break;
+        if (lane == c) mine = m;
+        const uint32_t win = __ffs(__ballot_sync(0xffffffffu, lb == m)) - 1;
+        if (lane == win) {
+          if (h0 == m) {
+            ++c0;
+            h0 = c0 < kk ? fm[lane * kk + c0] : 0ull;
+          } else {
+            ++c1;
+            h1 = c1 < kk ? fm[(lane + 32) * kk + c1] : 0ull;
+          }
+        }
+      }
+      if (lane >= c) mine = 0;
+      cnt = c;
+      __syncwarp();
+    }
+    if (lane < cnt) {
+      p.out_ids[(size_t)b * kk + lane] = ~(uint32_t)(mine & 0xFFFFFFFFu);
+      p.out_scores[(size_t)b * kk + lane] = order_float((uint32_t)(mine >> 32));
+    }
+  }
+  if (lane == 0) p.out_counts[b] = cnt;
+  __syncwarp();
+}
+
+// Fused top-k, last step: one warp per query merges its units' best-k lists
+// (fused_merge) into the ranked output.
+// Launched as a programmatic dependent of the MaxSim kernel: its CTAs are
+// resident (waiting) as MaxSim CTAs retire, and the wait releases when the
+// whole MaxSim grid -- every unit list and every dedup insert -- is done.
+constexpr int kFinalizeWarps = 4;
+constexpr int kFinalizeKeys = 640;  // per-warp merge scratch (keys)
+__global__ void __launch_bounds__(kFinalizeWarps * 32) finalize_kernel(const MaxSimParams p) {
+  __shared__ uint64_t fmk[kFinalizeWarps][kFinalizeKeys];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t b = blockIdx.x * kFinalizeWarps + w;
+  ktl_begin(p.dbg, 2);
+  // the plan completed before MaxSim released this grid: its outputs can be
+  // read before the wait
+  uint32_t u0 = 0, nu = 0;
+  if (b < p.n_queries) {
+    u0 = p.unit_off[b];
+    nu = p.unit_off[b + 1] - u0;
+  }
+  const uint32_t rejected = *p.err & (ERR_BAD_OFFSETS | ERR_CAPACITY);
+  const unsigned long long tw0 = ktl_now();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if ((p.dbg & 256u) && lane == 0) { atomicAdd(&g_fin[4], ktl_now() - tw0); atomicAdd(&g_fin[5], tw0); }
+  if (rejected) return;  // plan rejected the batch
+  if (b < p.n_queries && nu > 0) fused_merge<kFinalizeKeys>(p, b, u0, nu, fmk[w], lane);
+  ktl_end(p.dbg, 2);
+}
 
 template <int D>
 __global__ void __launch_bounds__(TcLayout<D>::NTHREADS, 1)
@@ -142,12 +338,15 @@ maxsim_tc_kernel(const MaxSimParams p) {
   uint64_t* ufull_bar = tempty_bar + L::NBUF;      // [NU] loader -> producer, MMA, epilogue
   uint64_t* uempty_bar = ufull_bar + L::NU;        // [NU] combine -> loader
   uint64_t* edone_bar = uempty_bar + L::NU;        // [NU] epilogue (all lanes) -> combine
+  uint64_t* bdone_bar = edone_bar + L::NU;         // [NB] combine -> rank (bow ring entry full)
+  uint64_t* bfree_bar = bdone_bar + L::NB;         // [NB] rank -> combine (bow ring entry free)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
   if (p.prof && tid == 0) atomicMin(&p.prof[2], (unsigned long long)gtimer());
+  ktl_begin(p.dbg, 1);
 
   // ---- one-time setup: zero operand tiles (stale NaN bit patterns would leak
   // into other quarters through the zero rows of A), barriers, TMEM ----------
@@ -175,6 +374,11 @@ maxsim_tc_kernel(const MaxSimParams p) {
       mbar_init(&uempty_bar[i], 1);
       mbar_init(&edone_bar[i], 32 * L::NEPI);
     }
+    for (int i = 0; i < L::NB; ++i) {
+      mbar_init(&bdone_bar[i], 1);
+      mbar_init(&bfree_bar[i], 1);
+    }
+
     mbar_fence_init();
   }
   if (warp == L::MMA_WARP) tmem_alloc<L::TMEM_COLS>(tmem_holder);
@@ -183,10 +387,12 @@ maxsim_tc_kernel(const MaxSimParams p) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const uint64_t t_start = gtimer();
-  // let the dependent top-k grid launch now: its dedup prologue reads only
-  // candidate ids and then waits (griddepcontrol.wait) for this grid to finish
+  // programmatic dependent of plan_kernel: everything above overlapped it
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // let the dependent grid launch now (the plan is complete): the duplicate
+  // check (fused top-k) or the top-k kernel's id-only dedup prologue runs on
+  // the SMs' spare resources concurrently with this kernel
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-
   const uint32_t n_units = *p.n_units;  // planned on the device (plan_kernel)
 
   if (warp == L::LOADER_WARP) {
@@ -198,8 +404,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
       typename L::Unit& U = units[us];
       // Unit table entry (host-planned): query b, doc count, first candidate.
       if (lane == 0) ESPN_TRACE(0, it);
-      const uint4 ue = __ldg(&p.unit_tab[ug]);
-      const uint32_t b = ue.x, nd = ue.y;
+      const uint4 ue = __ldcg(&p.unit_tab[ug]);
+      const uint32_t b = ue.x, nd = ue.y & 0xFFu, tail = ue.y >> 31;
       const uint64_t cfirst = (uint64_t)ue.z | ((uint64_t)ue.w << 32);
       // Issue every independent global load of the unit up front: candidate
       // ids (<= 2 per lane), then the query tile, then the dependent row_ptr.
@@ -207,7 +413,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
 #pragma unroll
       for (int r = 0; r < L::UNITMAX / 32; ++r) {
         const uint32_t k = r * 32 + lane;
-        idk[r] = k < nd ? __ldg(&p.cand_ids[cfirst + k]) : 0u;
+        idk[r] = (k < nd && !tail) ? __ldg(&p.cand_ids[cfirst + k]) : 0u;
       }
       mbar_wait(&uempty_bar[us], ((it / L::NU) & 1) ^ 1);
       if (lane == 0) ESPN_TRACE(1, it);
@@ -225,7 +431,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
         uint32_t t = 0;
         uint64_t r0 = 0;
         uint64_t srcaddr = 0;
-        if (k < nd) {
+        if (k < nd && !tail) {
           const uint64_t loc = shard_local(idk[r], p.shard_count, p.shard_index, p.n_docs);
           if (loc != ~0ull) {
             r0 = __ldg(&p.row_ptr[loc]);
@@ -270,7 +476,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
       // Query tokens -> A slot `us` (rows 96+128*us .. +32), converted to the
       // table dtype; rows >= nq stay zero.  Item e = (row i, 8-value chunk c);
       // batches of 4 items per lane keep all their loads in flight together.
-      {
+      if (!tail) {
         const float* q = p.q32 + (size_t)b * p.nq * D;
         const int abase = 96 + 128 * (int)us;
         constexpr int ITEMS = 32 * L::CH / 32;  // per lane
@@ -322,6 +528,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
         U.cfirst = cfirst;
         U.nd = nd;
         U.S = carry;
+        U.tail = tail;
       }
       fence_proxy_async_smem();  // A tile is read by the tensor core (async proxy)
       __syncwarp();
@@ -527,26 +734,138 @@ maxsim_tc_kernel(const MaxSimParams p) {
     // bow(doc) = sum_i pm[us][i][doc] (max over the doc's tokens, reduced by the
     // epilogue's atomicMax), i ascending (the oracle's summation order); then
     // the slot's keys are reset and the unit slot is released to the loader.
-    // Runs concurrently with the epilogue of the next units.
+    // Runs concurrently with the epilogue of the next units.  Fused top-k: the
+    // sums also go to the rank warp through the shared-memory bow ring.
+    const bool fused = p.out_ids != nullptr;
+    float* ring = reinterpret_cast<float*>(smem + L::OFF_RING);
+    constexpr int NK = L::UNITMAX / 32;  // docs per lane
     for (uint32_t it = 0;; ++it) {
       const uint32_t ug = blockIdx.x + it * gridDim.x;
       if (ug >= n_units) break;
       const uint32_t us = it % L::NU;
       const typename L::Unit& U = units[us];
       mbar_wait(&edone_bar[us], (it / L::NU) & 1);
-      const uint32_t nd = U.nd;
+      const uint32_t nd = U.nd, tail = U.tail;
       const uint64_t j0 = U.cfirst;
       int* pmu = reinterpret_cast<int*>(pm) + us * 32 * L::PM_STRIDE;
-      for (uint32_t k = lane; k < nd; k += 32) {
-        float s = 0.0f;
-        for (uint32_t i = 0; i < p.nq; ++i) s = __fadd_rn(s, key_ord(pmu[i * L::PM_STRIDE + k]));
-        p.bow_out[j0 + k] = s;
+      float bow[NK];
+#pragma unroll
+      for (int r = 0; r < NK; ++r) {
+        const uint32_t k = r * 32 + lane;
+        bow[r] = 0.0f;
+        if (k < nd && !tail) {
+          float s = 0.0f;
+          for (uint32_t i = 0; i < p.nq; ++i) s = __fadd_rn(s, key_ord(pmu[i * L::PM_STRIDE + k]));
+          bow[r] = s;
 #pragma unroll 8
-        for (uint32_t i = 0; i < 32; ++i) pmu[i * L::PM_STRIDE + k] = ord_key(-INFINITY);
+          for (uint32_t i = 0; i < 32; ++i) pmu[i * L::PM_STRIDE + k] = ord_key(-INFINITY);
+        }
       }
       __syncwarp();
-      if (lane == 0) { ESPN_TRACE(6, it); mbar_arrive(&uempty_bar[us]); }
+      if (lane == 0) { ESPN_TRACE(6, it); mbar_arrive(&uempty_bar[us]); }  // slot free
+      if (fused) {
+        const uint32_t j = it % L::NB;
+        mbar_wait(&bfree_bar[j], ((it / L::NB) & 1) ^ 1);
+#pragma unroll
+        for (int r = 0; r < NK; ++r) ring[j * L::UNITMAX + r * 32 + lane] = bow[r];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bdone_bar[j]);
+      }
+#pragma unroll
+      for (int r = 0; r < NK; ++r)
+        if (r * 32 + lane < nd && !tail) p.bow_out[j0 + r * 32 + lane] = bow[r];
     }
+  } else if (warp == L::DEDUP_WARP || warp == L::RANK_WARP) {
+    // ===================== DEDUP / RANK (fused top-k) ===========================
+    // Both read their units straight from the unit table (the plan is
+    // complete), so they never hold a unit slot: their latency (L2 atomics)
+    // does not stall the copy pipeline.  DEDUP inserts the unit's ids into the
+    // query's duplicate hash while the unit is scored.  RANK forms the keys
+    // alpha*cls + bow (aggregate_score, scoring.hpp:12-14, no FMA contraction;
+    // tail units alpha*cls) from the bow ring and writes the unit's best k,
+    // sorted, to unit_top.  finalize_kernel merges each query's unit lists.
+    const bool fused = p.out_ids != nullptr;
+    const bool is_rank = warp == L::RANK_WARP;
+    uint64_t* fm = reinterpret_cast<uint64_t*>(smem + L::OFF_UK);  // rank warp: unit keys
+    const float* ring = reinterpret_cast<const float*>(smem + L::OFF_RING);
+    constexpr int NK = L::UNITMAX / 32;
+    uint32_t par = 0;  // this batch's dedup table (plan_kernel advanced the epoch)
+    if (fused) {
+      par = __ldcg(&p.fused_state[0]) & 1u;
+      if (!is_rank) {
+        // clear this CTA's slice of the rows the previous fused batch used in
+        // the other table (and its ff_seen flags), off the critical path
+        const uint32_t prev_b = __ldcg(&p.fused_state[1 + (par ^ 1u)]);
+        const size_t n4 = (size_t)prev_b * p.hash_slots / 4;
+        uint4* t4 = reinterpret_cast<uint4*>(p.dedup + (size_t)(par ^ 1u) * p.max_queries * p.hash_slots);
+        for (size_t i = (size_t)blockIdx.x * 32 + lane; i < n4; i += (size_t)gridDim.x * 32)
+          t4[i] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        uint32_t* ff = p.ff_seen + (size_t)(par ^ 1u) * p.max_queries;
+        for (uint32_t i = blockIdx.x * 32 + lane; i < prev_b; i += gridDim.x * 32) ff[i] = 0;
+      }
+    }
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t ug = blockIdx.x + it * gridDim.x;
+      if (ug >= n_units) break;
+      if (!fused) break;
+      const uint4 ue = __ldcg(&p.unit_tab[ug]);
+      const uint32_t b = ue.x, nd = ue.y & 0xFFu;
+      const uint64_t j0 = (uint64_t)ue.z | ((uint64_t)ue.w << 32);
+      if (!is_rank) {
+        fused_dedup<NK>(p, par, b, j0, nd, lane);
+        continue;
+      }
+      uint32_t idv[NK];
+      float clv[NK];
+#pragma unroll
+      for (int r = 0; r < NK; ++r) {  // independent of the scoring: load before waiting
+        const uint32_t k = r * 32 + lane;
+        idv[r] = k < nd ? __ldg(&p.cand_ids[j0 + k]) : 0u;
+        clv[r] = k < nd ? __ldg(&p.cand_cls[j0 + k]) : 0.0f;
+      }
+      const uint32_t j = it % L::NB;
+      mbar_wait(&bdone_bar[j], (it / L::NB) & 1);
+      float bow[NK];
+#pragma unroll
+      for (int r = 0; r < NK; ++r) bow[r] = ring[j * L::UNITMAX + r * 32 + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bfree_bar[j]);
+      uint64_t key[NK];
+      uint32_t bad = 0;
+#pragma unroll
+      for (int r = 0; r < NK; ++r) {
+        key[r] = 0;
+        if (r * 32 + lane < nd) {
+          const float sc = __fadd_rn(__fmul_rn(p.alpha, clv[r]), bow[r]);
+          bad |= !isfinite(clv[r]) ? ERR_NONFINITE_CLS : (!isfinite(sc) ? ERR_NONFINITE_SCORE : 0u);
+          key[r] = make_key(sc, idv[r]);
+        }
+      }
+      if (bad) atomicOr(p.err, bad);
+      // unit-local top-k by rank counting: rank(key) = #keys of the unit
+      // greater than it (ids are unique, so ranks are distinct); the keys of
+      // rank < k land sorted in unit_top, empty ranks are 0
+      const uint32_t kk = p.k;
+      unsigned long long* ut = p.unit_top + (size_t)ug * kk;
+#pragma unroll
+      for (int r = 0; r < NK; ++r) fm[r * 32 + lane] = key[r];
+      __syncwarp();
+      uint32_t rk[NK];
+#pragma unroll
+      for (int r = 0; r < NK; ++r) rk[r] = 0;
+      for (uint32_t j = 0; j < nd; ++j) {
+        const uint64_t x = fm[j];
+#pragma unroll
+        for (int r = 0; r < NK; ++r) rk[r] += x > key[r] ? 1u : 0u;
+      }
+#pragma unroll
+      for (int r = 0; r < NK; ++r)
+        if (r * 32 + lane < nd && rk[r] < kk) ut[rk[r]] = key[r];
+      for (uint32_t i = nd + lane; i < kk; i += 32) ut[i] = 0ull;
+      __syncwarp();
+      if (lane == 0) ESPN_TRACE(7, it);
+    }
+    if ((p.dbg & 256u) && lane == 0 && blockIdx.x < 256) g_cta_prof[4 * blockIdx.x + (is_rank ? 1 : 3)] = ktl_now();
   }
 
   tc_fence_before();
@@ -555,6 +874,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
     tc_fence_after();
     tmem_dealloc<L::TMEM_COLS>(tmem_base);
   }
+  ktl_end(p.dbg, 1);
+  if ((p.dbg & 256u) && threadIdx.x == 0 && blockIdx.x < 256) g_cta_prof[4 * blockIdx.x] = ktl_now();
   if (p.prof && tid == 0) {
     __threadfence();
     if (atomicAdd(&p.prof[3], 1ull) == gridDim.x - 1) {  // last CTA out
@@ -566,9 +887,9 @@ maxsim_tc_kernel(const MaxSimParams p) {
     }
   }
   if ((p.dbg & 8u) && blockIdx.x == 0 && tid == 0) {
-    const char* nm[7] = {"ld.start", "ld.slot", "ld.ready", "pr.start", "ep.start", "ep.mmadone", "ep.done"};
+    const char* nm[8] = {"ld.start", "ld.slot", "ld.ready", "pr.start", "ep.start", "ep.mmadone", "ep.done", "cb.topk"};
     printf("CTA0 units=%u end=%.2fus\n", (n_units + gridDim.x - 1) / gridDim.x, (gtimer() - t_start) / 1e3);
-    for (int e = 0; e < 7; ++e) {
+    for (int e = 0; e < 8; ++e) {
       printf("%-11s", nm[e]);
       for (int u = 0; u < 8 && blockIdx.x + u * gridDim.x < n_units; ++u)
         printf(" %8.2f", ((int64_t)(trace[e * 8 + u] - t_start)) / 1e3);

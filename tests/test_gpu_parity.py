@@ -353,3 +353,73 @@ def test_tiered_gather_and_staging_overflow(oracle, cuda_ok):
     with pytest.raises(api.InvalidConfigError):
         rr.rerank_arrays(q, ids, cls, off, api.PipelineConfig(rerank_count=600, final_k=10))
     rr.close(); store.close()
+
+
+# ---- fused top-k (ranking inside the tcgen05 MaxSim kernel) vs the separate
+# top-k kernel: identical ranked lists, counts and error verdicts ----
+def _run_pair(rp, codes, d, q, ids, cls, off, cfg, reps=1):
+    store = api.GpuStore(rp, codes, d)
+    rr = api.Reranker(store, len(off) - 1, max(int(off[-1]), 1), q.shape[1])
+    outs = []
+    for sep in (False, True) * reps:
+        outs.append(rr.rerank_arrays(q, ids, cls, off, cfg, kernel="tcgen05", separate_topk=sep))
+    rr.close()
+    store.close()
+    return outs
+
+
+@pytest.mark.parametrize("k", [1, 10, 16, 32])
+@pytest.mark.parametrize("partial", [False, True])
+def test_fused_topk_matches_separate(oracle, cuda_ok, k, partial):
+    rp, codes, q, ids, cls, off = build_case(20000, 32, 1, 63, B=6, K=1000, seed=71 + k)
+    cfg = api.PipelineConfig(rerank_count=300 if partial else 1000, final_k=k, alpha=0.7,
+                             partial_rerank_enabled=partial)
+    outs = _run_pair(rp, codes, 32, q, ids, cls, off, cfg, reps=2)
+    for o in outs[1:]:  # repeated batches: per-query hash/counters were reset by the last unit
+        assert np.array_equal(outs[0][0], o[0]) and np.array_equal(outs[0][1].view(np.uint32), o[1].view(np.uint32))
+        assert np.array_equal(outs[0][2], o[2])
+    check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
+
+
+def test_fused_topk_ragged_and_empty_queries(oracle, cuda_ok):
+    # empty lists, lists shorter than k, partial tails only (R=0 would be
+    # invalid; R < n with partial), a single-candidate list
+    rp, codes = synth.make_table(3000, 32, 1, 63, seed=81)
+    q, _ = synth.make_queries(rp, codes, 32, 6, seed=82)
+    rng = np.random.default_rng(83)
+    ids_l, cls_l, offs = [], [], [0]
+    for n in [0, 5, 1, 130, 0, 999]:
+        c = rng.permutation(3000)[:n].astype(np.uint32)
+        s = np.sort(rng.random(n).astype(np.float32))[::-1].copy()
+        o = np.lexsort((c, -s))
+        ids_l.append(c[o]); cls_l.append(s[o]); offs.append(offs[-1] + n)
+    ids = np.concatenate(ids_l).astype(np.uint32)
+    cls = np.concatenate(cls_l).astype(np.float32)
+    off = np.asarray(offs, np.uint64)
+    for cfg in (api.PipelineConfig(rerank_count=64, final_k=10, partial_rerank_enabled=True),
+                api.PipelineConfig(rerank_count=1000, final_k=10)):
+        a, b = _run_pair(rp, codes, 32, q, ids, cls, off, cfg)
+        assert np.array_equal(a[2], b[2])
+        for i in range(6):
+            n = int(a[2][i])
+            assert np.array_equal(a[0][i, :n], b[0][i, :n]) and np.array_equal(a[1][i, :n], b[1][i, :n])
+        check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
+
+
+def test_fused_topk_duplicates_across_units_and_tail(cuda_ok):
+    rp, codes, q, ids, cls, off = build_case(5000, 32, 1, 63, B=3, K=1000, seed=91)
+    store = api.GpuStore(rp, codes, 32)
+    rr = api.Reranker(store, 3, 3000, 32)
+    full = api.PipelineConfig(rerank_count=1000, final_k=10)
+    part = api.PipelineConfig(rerank_count=100, final_k=10, partial_rerank_enabled=True)
+    good = rr.rerank_arrays(q, ids, cls, off, full, kernel="tcgen05")
+    cases = [(1003, 1990, full), (5, 900, full), (2050, 2999, part), (10, 500, part)]  # (copy to, copy from)
+    for i, j, cfg in cases:
+        dup = ids.copy(); dup[i] = dup[j]
+        for sep in (False, True):
+            with pytest.raises(api.InvalidInputError):
+                rr.rerank_arrays(q, dup, cls, off, cfg, kernel="tcgen05", separate_topk=sep)
+        # the failed batch left no state behind
+        again = rr.rerank_arrays(q, ids, cls, off, full, kernel="tcgen05")
+        assert np.array_equal(again[0], good[0]) and np.array_equal(again[2], good[2])
+    rr.close(); store.close()
