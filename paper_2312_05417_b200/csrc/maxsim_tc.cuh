@@ -62,6 +62,7 @@ struct TcLayout {
   static constexpr int NG = MAX_SLOTS / 8;         // 8-slot groups
   static constexpr int MAXW = NG / 32;             // bitmap words (one bit per group)
   static constexpr int MAX_STAGES = MAX_SLOTS / STAGE_SLOTS;  // stages of a full unit
+  static constexpr int MAX_OPS = (UNITMAX + MAX_STAGES) * NP;  // docs + stage straddles, per K-panel
   static constexpr int PM_STRIDE = UNITMAX + 1;    // padded: conflict-free emits and combine
   static constexpr int PM_FLOATS = NU * 32 * PM_STRIDE;  // per unit slot: [query token][doc] keys
   static constexpr int NBUF = (512 / NQC) < 4 ? (512 / NQC) : 4;
@@ -75,7 +76,8 @@ struct TcLayout {
   static constexpr int COMBINE_WARP = LOADER_WARP + 1;
   static constexpr int DEDUP_WARP = COMBINE_WARP + 1;  // fused top-k: duplicate check
   static constexpr int RANK_WARP = DEDUP_WARP + 1;     // fused top-k: keys, unit top-k
-  static constexpr int NWARPS = RANK_WARP + 1;
+  static constexpr int QUERY_WARP = RANK_WARP + 1;     // unit query tile -> A operand slot
+  static constexpr int NWARPS = QUERY_WARP + 1;
   static constexpr int NB = 8;                     // bow ring (combine -> rank) depth, in units
   static constexpr int HALF = NQC / 2;             // columns per epilogue warp per stage
   static constexpr int LW = HALF < 32 ? HALF : 32; // tcgen05.ld width (columns)
@@ -88,12 +90,15 @@ struct TcLayout {
     uint64_t cfirst;            // candidate index of the unit's first doc
     uint32_t bitmap[MAXW];      // bit g: a doc starts at group g
     uint32_t wprefix[MAXW];     // docs starting before word w
-    uint64_t src[UNITMAX];      // address of the doc's rows (table or staging buffer)
-    uint32_t t[UNITMAX];
-    uint32_t slot[UNITMAX];
     uint8_t gvalid[NG];         // valid (non-pad) columns of group g, 1..8
-    uint32_t kbeg[MAX_STAGES];  // docs [kbeg, kend) have rows in stage st
-    uint32_t kend[MAX_STAGES];
+    // Bulk-copy plan (loader-built): one op per (doc, stage piece, K-panel)
+    // {src lo, src hi, byte offset in the stage, bytes}, in stage order;
+    // stage st issues ops [op_beg[st], op_beg[st+1]) (last stage: to n_ops),
+    // producer pw the ops of parity pw, expecting stage_tx[st][pw] bytes.
+    uint4 op[MAX_OPS];
+    uint32_t op_beg[MAX_STAGES];
+    uint32_t stage_tx[MAX_STAGES][2];
+    uint32_t n_ops;
   };
   // Byte offsets inside dynamic shared memory (1024-aligned base).
   static constexpr int OFF_B = 0;
@@ -320,7 +325,7 @@ template <int D>
 __global__ void __launch_bounds__(TcLayout<D>::NTHREADS, 1)
 maxsim_tc_kernel(const MaxSimParams p) {
   __shared__ uint64_t trace[8 * 8];
-  __shared__ uint64_t strace[6 * 16];  // per-stage: producer, MMA full, MMA tempty, epilogue
+  __shared__ uint64_t strace[9 * 16];  // per-stage: producer, MMA full, MMA tempty, epilogue
   using L = TcLayout<D>;
   using namespace espn_ptx;
   // swizzled operand atoms need 1024-byte aligned stage bases: align manually
@@ -370,7 +375,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
       mbar_init(&tempty_bar[i], L::NEPI);
     }
     for (int i = 0; i < L::NU; ++i) {
-      mbar_init(&ufull_bar[i], 1);
+      mbar_init(&ufull_bar[i], 2);  // unit loader + query-tile warp
       mbar_init(&uempty_bar[i], 1);
       mbar_init(&edone_bar[i], 32 * L::NEPI);
     }
@@ -407,42 +412,46 @@ maxsim_tc_kernel(const MaxSimParams p) {
       const uint4 ue = __ldcg(&p.unit_tab[ug]);
       const uint32_t b = ue.x, nd = ue.y & 0xFFu, tail = ue.y >> 31;
       const uint64_t cfirst = (uint64_t)ue.z | ((uint64_t)ue.w << 32);
-      // Issue every independent global load of the unit up front: candidate
-      // ids (<= 2 per lane), then the query tile, then the dependent row_ptr.
-      uint32_t idk[L::UNITMAX / 32];
+      // Every global load of the unit is issued before waiting for its slot:
+      // candidate ids (<= 2 per lane), then the dependent row_ptr / staged
+      // addresses, so the slot wait overlaps their latency.
+      constexpr int NK = L::UNITMAX / 32;
+      uint32_t tk[NK];
+      uint64_t srck[NK];
 #pragma unroll
-      for (int r = 0; r < L::UNITMAX / 32; ++r) {
+      for (int r = 0; r < NK; ++r) {
         const uint32_t k = r * 32 + lane;
-        idk[r] = (k < nd && !tail) ? __ldg(&p.cand_ids[cfirst + k]) : 0u;
+        tk[r] = 0;
+        srck[r] = 0;
+        if (k < nd && !tail) {
+          const uint64_t loc = shard_local(__ldg(&p.cand_ids[cfirst + k]), p.shard_count, p.shard_index, p.n_docs);
+          if (loc != ~0ull) {
+            const uint64_t r0 = __ldg(&p.row_ptr[loc]);
+            tk[r] = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
+            srck[r] = p.cand_src ? __ldg(&p.cand_src[cfirst + k])  // tiered: staged / resident address
+                                 : (uint64_t)(p.rows + r0 * D);
+            if (srck[r] == 0) tk[r] = 0;  // not staged (staging overflow, reported by stage_kernel)
+          } else {
+            atomicOr(p.err, ERR_UNKNOWN_DOC);
+          }
+        }
       }
       mbar_wait(&uempty_bar[us], ((it / L::NU) & 1) ^ 1);
       if (lane == 0) ESPN_TRACE(1, it);
       for (int i = lane; i < L::MAXW; i += 32) U.bitmap[i] = 0;
       for (int i = lane; i < L::MAX_STAGES; i += 32) {
-        U.kbeg[i] = 0xFFFFFFFFu;
-        U.kend[i] = 0;
+        U.op_beg[i] = 0xFFFFFFFFu;
+        U.stage_tx[i][0] = 0;
+        U.stage_tx[i][1] = 0;
       }
       __syncwarp();
-      // doc info + slot prefix sum (warp scan) + group plan
-      uint32_t carry = 0;
+      // doc info + slot prefix sum (warp scan) + group plan + copy ops
+      uint32_t carry = 0, ocarry = 0;
 #pragma unroll
-      for (int r = 0; r < L::UNITMAX / 32; ++r) {
+      for (int r = 0; r < NK; ++r) {
         const uint32_t k = r * 32 + lane;
-        uint32_t t = 0;
-        uint64_t r0 = 0;
-        uint64_t srcaddr = 0;
-        if (k < nd && !tail) {
-          const uint64_t loc = shard_local(idk[r], p.shard_count, p.shard_index, p.n_docs);
-          if (loc != ~0ull) {
-            r0 = __ldg(&p.row_ptr[loc]);
-            t = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
-            srcaddr = p.cand_src ? __ldg(&p.cand_src[cfirst + k])  // tiered: staged / resident address
-                                 : (uint64_t)(p.rows + r0 * D);
-            if (srcaddr == 0) t = 0;  // not staged (staging overflow, reported by stage_kernel)
-          } else {
-            atomicOr(p.err, ERR_UNKNOWN_DOC);
-          }
-        }
+        const uint32_t t = tk[r];
+        const uint64_t srcaddr = srck[r];
         const uint32_t pad = (t + 7u) & ~7u;
         uint32_t incl = pad;
 #pragma unroll
@@ -451,28 +460,71 @@ maxsim_tc_kernel(const MaxSimParams p) {
           if (lane >= o) incl += v;
         }
         const uint32_t start = carry + incl - pad;
-        if (k < nd) {
-          U.src[k] = srcaddr;
-          U.t[k] = t;
-          U.slot[k] = start;
-          if (t > 0 && start + pad <= (uint32_t)L::MAX_SLOTS) {
-            atomicOr(&U.bitmap[start >> 8], 1u << ((start >> 3) & 31));
-            const uint32_t g0 = start >> 3, ng = pad >> 3;
-            for (uint32_t g = 0; g + 1 < ng; ++g) U.gvalid[g0 + g] = 8;
-            U.gvalid[g0 + ng - 1] = (uint8_t)(t - 8 * (ng - 1));
-            // stages holding this doc's rows (a doc spans at most a few)
-            for (uint32_t st = start / L::STAGE_SLOTS; st <= (start + t - 1) / L::STAGE_SLOTS; ++st) {
-              atomicMin(&U.kbeg[st], k);
-              atomicMax(&U.kend[st], k + 1);
+        const bool fits = k < nd && t > 0 && start + pad <= (uint32_t)L::MAX_SLOTS;
+        const uint32_t st0 = start / L::STAGE_SLOTS, st1 = fits ? (start + t - 1) / L::STAGE_SLOTS : st0;
+        const uint32_t npc = fits ? (st1 - st0 + 1) * L::NP : 0u;  // copy ops of this doc
+        uint32_t oincl = npc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, oincl, o);
+          if (lane >= o) oincl += v;
+        }
+        if (fits) {
+          atomicOr(&U.bitmap[start >> 8], 1u << ((start >> 3) & 31));
+          const uint32_t g0 = start >> 3, ng = pad >> 3;
+          for (uint32_t g = 0; g + 1 < ng; ++g) U.gvalid[g0 + g] = 8;
+          U.gvalid[g0 + ng - 1] = (uint8_t)(t - 8 * (ng - 1));
+          // one op per stage piece and K-panel: the piece [a, e) of the doc's
+          // slots inside stage st lands at (a - x0) * PW of panel pn
+          uint32_t o = ocarry + oincl - npc;
+          for (uint32_t st = st0; st <= st1; ++st) {
+            const uint32_t x0 = st * L::STAGE_SLOTS;
+            const uint32_t a = max(start, x0), e = min(start + t, x0 + L::STAGE_SLOTS);
+            const uint32_t ja = a - start, nb = (e - a) * (uint32_t)L::PW;
+            atomicMin(&U.op_beg[st], o);
+#pragma unroll
+            for (int pn = 0; pn < L::NP; ++pn, ++o) {
+              const uint64_t src = srcaddr + ((uint64_t)pn * t + ja) * L::PW;
+              U.op[o] = make_uint4((uint32_t)src, (uint32_t)(src >> 32), pn * L::PANEL_BYTES + (a - x0) * L::PW, nb);
+              atomicAdd(&U.stage_tx[st][o & 1u], nb);
             }
           }
         }
         carry += __shfl_sync(0xffffffffu, incl, 31);
+        ocarry += __shfl_sync(0xffffffffu, oincl, 31);
       }
       if (carry > (uint32_t)L::MAX_SLOTS) {
         if (lane == 0) atomicOr(p.err, ERR_UNIT_TOO_LARGE);
         carry = 0;  // skip the unit's MMA work; the call fails on the host
       }
+      __syncwarp();
+      if (lane == 0) {
+        uint32_t acc = 0;
+        for (int i = 0; i < L::MAXW; ++i) {
+          U.wprefix[i] = acc;
+          acc += __popc(U.bitmap[i]);
+        }
+        U.b = b;
+        U.cfirst = cfirst;
+        U.nd = nd;
+        U.S = carry;
+        U.tail = tail;
+        U.n_ops = ocarry;
+      }
+      __syncwarp();
+      if (lane == 0) { ESPN_TRACE(2, it); mbar_arrive(&ufull_bar[us]); }
+    }
+  } else if (warp == L::QUERY_WARP) {
+    // ============================ QUERY TILE ====================================
+    // The unit's query tokens -> A slot `us`, converted to the table dtype,
+    // in parallel with the loader's slot plan (ufull counts both).
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t ug = blockIdx.x + it * gridDim.x;
+      if (ug >= n_units) break;
+      const uint32_t us = it % L::NU;
+      const uint4 ue = __ldcg(&p.unit_tab[ug]);
+      const uint32_t b = ue.x, tail = ue.y >> 31;
+      mbar_wait(&uempty_bar[us], ((it / L::NU) & 1) ^ 1);
       // Query tokens -> A slot `us` (rows 96+128*us .. +32), converted to the
       // table dtype; rows >= nq stay zero.  Item e = (row i, 8-value chunk c);
       // batches of 4 items per lane keep all their loads in flight together.
@@ -517,27 +569,15 @@ maxsim_tc_kernel(const MaxSimParams p) {
           if (bad) atomicOr(p.err, ERR_NONFINITE_QUERY);
         }
       }
-      __syncwarp();
-      if (lane == 0) {
-        uint32_t acc = 0;
-        for (int i = 0; i < L::MAXW; ++i) {
-          U.wprefix[i] = acc;
-          acc += __popc(U.bitmap[i]);
-        }
-        U.b = b;
-        U.cfirst = cfirst;
-        U.nd = nd;
-        U.S = carry;
-        U.tail = tail;
-      }
       fence_proxy_async_smem();  // A tile is read by the tensor core (async proxy)
       __syncwarp();
-      if (lane == 0) { ESPN_TRACE(2, it); mbar_arrive(&ufull_bar[us]); }
+      if (lane == 0) mbar_arrive(&ufull_bar[us]);
     }
   } else if (warp >= L::PROD_WARP0 && warp < L::PROD_WARP0 + L::NPROD) {
     // ====================== BULK-COPY PRODUCERS (NPROD warps) ======================
-    // Producer pw takes docs kbeg + pw*32 + lane, stride 32*NPROD; each warp
-    // arrives on the stage's full barrier with its own expect_tx byte count.
+    // Lane 0 of producer pw issues the stage's copy ops of parity pw (one
+    // cp.async.bulk each, planned by the loader) and arrives on the stage's
+    // full barrier with their byte count.
     const uint32_t pw = warp - L::PROD_WARP0;
     const uint64_t policy = l2_policy_evict_first();
     uint32_t gs = 0;  // global stage counter
@@ -552,34 +592,25 @@ maxsim_tc_kernel(const MaxSimParams p) {
       const uint32_t n_st = (S + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t s = gs % L::NS;
-        const uint32_t x0 = st * L::STAGE_SLOTS, x1 = x0 + L::STAGE_SLOTS;
-        // docs [kbeg, kend) (loader-planned) contribute rows [max(x0,slot), min(x1,slot+t))
-        const uint32_t kcur = U.kbeg[st], kend = U.kend[st];
-        uint32_t bytes = 0;
-        for (uint32_t k = kcur + pw * 32 + lane; k < kend; k += 32 * L::NPROD) {
-          const uint32_t a = max(U.slot[k], x0), e = min(U.slot[k] + U.t[k], x1);
-          bytes += e > a ? (e - a) * (uint32_t)L::ROWB : 0u;
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        // ops [o0, o1) of this stage (loader-planned); this warp issues parity pw
+        const uint32_t o0 = U.op_beg[st], o1 = st + 1 < n_st ? U.op_beg[st + 1] : U.n_ops;
+        uint32_t bytes = U.stage_tx[st][pw];
         mbar_wait(&empty_bar[s], ((gs / L::NS) & 1) ^ 1);
         if (lane == 0 && pw == 0) ESPN_STRACE(0, gs);
         if (p.dbg & 4u) bytes = 0;
-        if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], bytes);
-        __syncwarp();
-        if (p.dbg & 4u) continue;
-        const uint32_t sbase = smem_u32(sB + s * L::STAGE_BYTES);
-        for (uint32_t k = kcur + pw * 32 + lane; k < kend; k += 32 * L::NPROD) {
-          const uint32_t sk = U.slot[k], t = U.t[k];
-          const uint32_t a = max(sk, x0), e = min(sk + t, x1);
-          if (e <= a) continue;
-          const uint32_t ja = a - sk, n = e - a;
-          const uint8_t* src = reinterpret_cast<const uint8_t*>(U.src[k]);
-#pragma unroll
-          for (int pn = 0; pn < L::NP; ++pn)
-            bulk_g2s(sbase + pn * L::PANEL_BYTES + (a - x0) * L::PW,
-                     src + ((size_t)pn * t + ja) * L::PW, n * L::PW, &full_bar[s], policy);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full_bar[s], bytes);
+          if (!(p.dbg & 4u)) {
+            const uint32_t sbase = smem_u32(sB + s * L::STAGE_BYTES);
+            for (uint32_t o = o0 + ((o0 & 1u) ^ pw); o < o1; o += 2) {
+              const uint4 op = U.op[o];
+              bulk_g2s(sbase + op.z, reinterpret_cast<const void*>((uint64_t)op.x | ((uint64_t)op.y << 32)), op.w,
+                       &full_bar[s], policy);
+            }
+          }
         }
+        __syncwarp();
+        if (lane == 0 && pw == 0) ESPN_STRACE(6, gs);
       }
     }
   } else if (warp == L::MMA_WARP) {
@@ -657,21 +688,15 @@ maxsim_tc_kernel(const MaxSimParams p) {
         const uint32_t xw = st * L::STAGE_SLOTS + w * L::NQC + h * L::HALF;
         const int remv = (p.dbg & 1u) ? 0 : (int)S - (int)xw;
         if (remv > 0) {
-          // All TMEM loads of this warp's columns first, then the TMEM buffer
-          // is released and the group maxima are computed with full ILP; only
-          // the short doc-boundary scan over NGH groups is sequential.
+          // TMEM -> registers in NLD chunks of LW columns: chunk c+1 is read
+          // (the SM's TMEM read port, ~64 B/clk, is the epilogue's floor)
+          // while chunk c's group maxima are computed; the buffer is released
+          // after the last chunk landed.  Only the short doc-boundary scan over
+          // NGH groups is sequential.
           const uint32_t nv = remv < L::HALF ? (uint32_t)remv : (uint32_t)L::HALF;
           const uint32_t taddr0 = tmem_base + ((uint32_t)(w * 32) << 16) + buf * L::NQC + h * L::HALF;
           float v[L::NLD][L::LW];
-#pragma unroll
-          for (int c = 0; c < L::NLD; ++c) {
-            if (p.dbg & 16u) {
-#pragma unroll
-              for (int j = 0; j < L::LW; ++j) v[c][j] = (float)j;
-            } else if (c == 0 || (uint32_t)(L::LW * c) < nv) {
-              tmem_ld_32x32b<L::LW>(taddr0 + L::LW * c, v[c]);
-            }
-          }
+          tmem_ld_32x32b<L::LW>(taddr0, v[0]);
           const uint32_t G0 = xw >> 3;  // multiple of NGH
           const uint32_t bw = U.bitmap[G0 >> 5];
           const uint32_t sbits = (bw >> (G0 & 31)) & ((1u << L::NGH) - 1u);
@@ -685,25 +710,39 @@ maxsim_tc_kernel(const MaxSimParams p) {
 #pragma unroll
             for (int q = 0; q < L::NGH; ++q) gvw[0] |= (uint32_t)U.gvalid[G0 + q] << (8 * q);
           }
-          tmem_ld_wait();
-          if (tid == 0) ESPN_STRACE(4, gs);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty_bar[buf]);
-          if (p.dbg & 32u) continue;
-          // group maxima over the valid (non-pad) columns, branch-free
+          constexpr int GPC = L::LW / 8;  // groups per chunk
           float gm[L::NGH];
 #pragma unroll
-          for (int q = 0; q < L::NGH; ++q) {
-            const float* x = &v[(8 * q) / L::LW][(8 * q) % L::LW];
-            const uint32_t nval = (gvw[q / 4] >> (8 * (q % 4))) & 0xFFu;
-            const float x0 = x[0];
-            const float x1 = sel_gt(nval, 1, x[1], x0), x2 = sel_gt(nval, 2, x[2], x0);
-            const float x3 = sel_gt(nval, 3, x[3], x0), x4 = sel_gt(nval, 4, x[4], x0);
-            const float x5 = sel_gt(nval, 5, x[5], x0), x6 = sel_gt(nval, 6, x[6], x0);
-            const float x7 = sel_gt(nval, 7, x[7], x0);
-            gm[q] = fmaxf(fmax3(x0, x1, x2), fmax3(fmax3(x3, x4, x5), x6, x7));
+          for (int c = 0; c < L::NLD; ++c) {
+            tmem_ld_wait();
+            if (c + 1 < L::NLD) {
+              if ((uint32_t)(L::LW * (c + 1)) < nv) tmem_ld_32x32b<L::LW>(taddr0 + L::LW * (c + 1), v[c + 1]);
+            } else {
+              if (tid == 0) ESPN_STRACE(4, gs);
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+              if (tid == 0) ESPN_STRACE(8, gs);
+            }
+            // group maxima over the valid (non-pad) columns of chunk c
+#pragma unroll
+            for (int qq = 0; qq < GPC; ++qq) {
+              const int q = c * GPC + qq;
+              const float* x = &v[c][8 * qq];
+              const uint32_t nval = (gvw[q / 4] >> (8 * (q % 4))) & 0xFFu;  // warp-uniform
+              const float x0 = x[0];
+              if (nval >= 8u) {  // full group (all but a doc's last): no masking
+                gm[q] = fmaxf(fmax3(x0, x[1], x[2]), fmax3(fmax3(x[3], x[4], x[5]), x[6], x[7]));
+              } else {
+                const float x1 = sel_gt(nval, 1, x[1], x0), x2 = sel_gt(nval, 2, x[2], x0);
+                const float x3 = sel_gt(nval, 3, x[3], x0), x4 = sel_gt(nval, 4, x[4], x0);
+                const float x5 = sel_gt(nval, 5, x[5], x0), x6 = sel_gt(nval, 6, x[6], x0);
+                const float x7 = sel_gt(nval, 7, x[7], x0);
+                gm[q] = fmaxf(fmax3(x0, x1, x2), fmax3(fmax3(x3, x4, x5), x6, x7));
+              }
+            }
           }
+          if (tid == 0) { asm volatile("" ::"f"(gm[L::NGH - 1])); ESPN_STRACE(7, gs); }
           float m = -INFINITY;
 #pragma unroll
           for (int q = 0; q < L::NGH; ++q) {
@@ -895,8 +934,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
         printf(" %8.2f", ((int64_t)(trace[e * 8 + u] - t_start)) / 1e3);
       printf("\n");
     }
-    const char* sn[6] = {"P.empty", "M.full", "M.tempty", "E.tfull", "E.ldone", "E.proc"};
-    for (int e = 0; e < 6; ++e) {
+    const char* sn[9] = {"P.empty", "M.full", "M.tempty", "E.tfull", "E.ldone", "E.proc", "P.issued", "E.gm", "E.rel"};
+    for (int e = 0; e < 9; ++e) {
       printf("%-9s", sn[e]);
       for (int g = 0; g < 16; ++g) printf(" %6.2f", ((int64_t)(strace[e * 16 + g] - t_start)) / 1e3);
       printf("\n");
