@@ -411,8 +411,12 @@ def run_ours(args, cfg):
         return torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     e2e_in = [dict(q=pinned(db["h_q"]), ids=pinned(db["h_ids"].view(np.int32)), cls=pinned(db["h_cls"]),
                    off=db["off"], need=db["need"]) for db in dev_batches]
-    h_out = [pinned(np.zeros((B_q, k), np.int32)), pinned(np.zeros((B_q, k), np.float32)),
-             pinned(np.zeros(B_q, np.int32))]
+    # two pinned output sets: a batch's ranked lists land in host memory while
+    # the next batch is already queued (ASYNC calls, at most 2 in flight)
+    h_outs = [[pinned(np.zeros((B_q, k), np.int32)), pinned(np.zeros((B_q, k), np.float32)),
+               pinned(np.zeros(B_q, np.int32))] for _ in range(2)]
+    h_out = h_outs[0]
+    e2e_ev = [torch.cuda.Event() for _ in range(2)]
     if world > 1:
         d_q = torch.empty_like(dev_batches[0]["q"])
         d_ids = torch.empty(max_c, dtype=torch.int32, device=dev)
@@ -421,15 +425,23 @@ def run_ours(args, cfg):
     def e2e_step(i):
         db = e2e_in[i % n_batches]
         if world == 1:
+            # the public call with HOST buffers, ASYNC, pipelined two deep: the
+            # library stages batch i's inputs (H2D on its copy stream) while
+            # batch i-1 is scored; ranked lists are written into pinned host
+            # memory.  Before reusing output set i%2, batch i-2 must be done.
+            e2e_ev[i % 2].synchronize()
+            ho = h_outs[i % 2]
             a = L.RerankArgs(n_queries=B_q, n_query_tokens=nq, query_tokens=db["q"].data_ptr(),
                              cand_ids=db["ids"].data_ptr(), cand_cls=db["cls"].data_ptr(),
-                             cand_offsets=db["off"].ctypes.data, rerank_count=R, final_k=k, alpha=1.0, flags=0,
-                             kernel=L.ESPN_KERNEL_AUTO, needed_counts=db["need"].ctypes.data)
-            o = L.RerankOut(ids=h_out[0].data_ptr(), scores=h_out[1].data_ptr(), counts=h_out[2].data_ptr())
+                             cand_offsets=db["off"].ctypes.data, rerank_count=R, final_k=k, alpha=1.0,
+                             flags=L.ESPN_RERANK_ASYNC, kernel=L.ESPN_KERNEL_AUTO,
+                             needed_counts=db["need"].ctypes.data)
+            o = L.RerankOut(ids=ho[0].data_ptr(), scores=ho[1].data_ptr(), counts=ho[2].data_ptr())
             rc = lib.espn_gpu_rerank(store.handle, rr.handle, C.byref(a), C.byref(o),
                                      C.c_void_p(stream.cuda_stream))
             if rc:
                 raise RuntimeError(L.last_error())
+            e2e_ev[i % 2].record(stream)
         else:
             n = db["ids"].numel()
             d_q.copy_(db["q"], non_blocking=True)
@@ -461,6 +473,12 @@ def run_ours(args, cfg):
         e2e_step(st)
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
+    rr.sync(stream.cuda_stream)  # device-side validation of the e2e batches
+    e2e_ok = None
+    if world == 1:  # the last batch's ranked lists arrived in host memory: source doc first?
+        last = h_outs[(args.steps - 1) % 2][0].numpy()[:, 0].view(np.uint32)
+        src_last = dev_batches[(args.steps - 1) % n_batches]["glob"]["ids"].reshape(B_q, K)[:, 0]
+        e2e_ok = float(np.mean(last == src_last))
     db0 = dev_batches[0]
     h2d = (db0["h_q"].nbytes + db0["h_ids"].nbytes + db0["h_cls"].nbytes + (B_q + 1) * 8 + B_q * 4)
     d2h = B_q * k * 8 + B_q * 4 + (4 if world == 1 else 0)
@@ -546,7 +564,7 @@ def run_ours(args, cfg):
                      "step_frac": alg_bytes / (ms / args.steps / 1e3) / 1e9 / peak},
         "clocks": clocks,
         "gpu_launches": n_launch_ours,
-        "check": {"source_doc_ranked_first": src_ok},
+        "check": {"source_doc_ranked_first": src_ok, "e2e_source_doc_ranked_first": e2e_ok},
     }
     if world == 1 and not emulated and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(cfg, store, batches, dev, args)

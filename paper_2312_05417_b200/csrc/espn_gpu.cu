@@ -214,15 +214,10 @@ struct espn_gpu_table {
 struct espn_gpu_workspace {
   espn_gpu_table* table = nullptr;
   uint32_t max_queries = 0, max_candidates = 0, max_nq = 0;
-  float* q32 = nullptr;
-  uint32_t* ids = nullptr;
-  float* cls = nullptr;
-  uint64_t* cand_off = nullptr;
   uint32_t* unit_off = nullptr;
   uint32_t* needed = nullptr;
   uint4* unit_tab = nullptr;    // tcgen05 work units {b, n_docs, first candidate}
   uint64_t max_units = 0;
-  uint32_t* needed_in = nullptr;  // staged needed_counts (host-offset mode)
   uint32_t* n_units = nullptr;    // planned unit count (device)
   uint32_t max_list = 0;          // longest candidate list the top-k hash is sized for
   // fused top-k (tcgen05 path, final_k <= kFusedMaxK)
@@ -267,6 +262,24 @@ struct espn_gpu_workspace {
     bool used = false;
   } slots[kSlots];
   uint64_t calls = 0;
+  // Host-I/O batches: inputs staged on a copy stream into one of two device
+  // slots, so batch n+1's H2D overlaps batch n's kernels (ASYNC callers).
+  cudaStream_t cs = nullptr;
+  struct IoSlot {
+    float* q32 = nullptr;
+    uint32_t* ids = nullptr;
+    float* cls = nullptr;
+    uint64_t* cand_off = nullptr;
+    uint32_t* needed_in = nullptr;
+    cudaEvent_t in_ready = nullptr;  // H2D done (copy stream)
+    cudaEvent_t done = nullptr;      // last kernel reading the slot done (compute stream)
+    bool used = false;
+  } io[2];
+  uint64_t io_calls = 0;
+  // zero-copy outputs: last output pointers checked for pinned host memory
+  const void* zc_key[3] = {nullptr, nullptr, nullptr};
+  void* zc_dev[3] = {nullptr, nullptr, nullptr};
+  bool zc_ok = false;
   uint32_t* h_err = nullptr;
   bool async_pending = false;  // device err word carries bits of un-synced ASYNC calls
   // PROFILE: event triples around MaxSim / top-k, drained lazily
@@ -562,10 +575,6 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   auto al = [&](void** p, size_t bytes) {
     if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(bytes, 16));
   };
-  al((void**)&w->q32, B * w->max_nq * t->d * sizeof(float));
-  al((void**)&w->ids, C * sizeof(uint32_t));
-  al((void**)&w->cls, C * sizeof(float));
-  al((void**)&w->cand_off, (B + 1) * sizeof(uint64_t));
   al((void**)&w->unit_off, (B + 1) * sizeof(uint32_t));
   al((void**)&w->needed, B * sizeof(uint32_t));
   // work-unit table capacity: every query may end in a partial unit
@@ -574,7 +583,6 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     w->max_units = ud > 0 ? (C + ud - 1) / ud + 2 * B : 0;  // + partial units (needed, tail)
   }
   al((void**)&w->unit_tab, w->max_units * sizeof(uint4));
-  al((void**)&w->needed_in, B * sizeof(uint32_t));
   al((void**)&w->n_units, sizeof(uint32_t));
   al((void**)&w->kprof, 4 * sizeof(unsigned long long));
   if (t->tiered) {
@@ -612,6 +620,16 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   al((void**)&w->out_scores, B * kMaxK * sizeof(float));
   al((void**)&w->out_counts, B * sizeof(uint32_t));
   al((void**)&w->err, 4 * sizeof(uint32_t));
+  for (auto& io : w->io) {
+    al((void**)&io.q32, B * w->max_nq * t->d * sizeof(float));
+    al((void**)&io.ids, C * sizeof(uint32_t));
+    al((void**)&io.cls, C * sizeof(float));
+    al((void**)&io.cand_off, (B + 1) * sizeof(uint64_t));
+    al((void**)&io.needed_in, B * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.in_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.done, cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cs, cudaStreamNonBlocking);
   for (auto& sl : w->slots) {
     if (e == cudaSuccess) e = cudaMallocHost(&sl.cand_off, (B + 1) * sizeof(uint64_t));
     if (e == cudaSuccess) e = cudaMallocHost(&sl.needed, (B + 1) * sizeof(uint32_t));
@@ -637,8 +655,14 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
 int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   if (!w) return ESPN_OK;
   DeviceGuard g(w->table->device);
-  cudaFree(w->q32); cudaFree(w->ids); cudaFree(w->cls); cudaFree(w->cand_off);
-  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->needed_in); cudaFree(w->n_units);
+  for (auto& io : w->io) {
+    if (io.done) cudaEventSynchronize(io.done);
+    cudaFree(io.q32); cudaFree(io.ids); cudaFree(io.cls); cudaFree(io.cand_off); cudaFree(io.needed_in);
+    if (io.in_ready) cudaEventDestroy(io.in_ready);
+    if (io.done) cudaEventDestroy(io.done);
+  }
+  if (w->cs) { cudaStreamSynchronize(w->cs); cudaStreamDestroy(w->cs); }
+  cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->n_units);
   cudaFree(w->kprof);
   cudaFree(w->unit_top); cudaFree(w->dedup); cudaFree(w->ff_seen); cudaFree(w->fused_state);
   for (auto& st : w->stage) {
@@ -735,32 +759,78 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   const float* q32 = a->query_tokens;
   const uint32_t* ids = a->cand_ids;
   const float* cls = a->cand_cls;
-  if (!dev_off) {
-    // stage the small per-batch tables in a pinned slot (ring: an ASYNC caller
-    // may enqueue batch n+1 before batch n's copies ran)
-    auto& sl = w->slots[w->calls % espn_gpu_workspace::kSlots];
-    if (sl.used) ESPN_CUDA_TRY(cudaEventSynchronize(sl.copied));
-    std::memcpy(sl.cand_off, a->cand_offsets, (B + 1) * sizeof(uint64_t));
-    ESPN_CUDA_TRY(cudaMemcpyAsync(w->cand_off, sl.cand_off, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-    if (a->needed_counts) {
-      std::memcpy(sl.needed, a->needed_counts, B * sizeof(uint32_t));
-      ESPN_CUDA_TRY(cudaMemcpyAsync(w->needed_in, sl.needed, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-      needed_in = w->needed_in;
+  // Host-staged inputs go through I/O slot io_slot on the workspace's copy
+  // stream: the slot's previous batch must be done with it, and the compute
+  // stream waits for the H2D -- batch n+1's copies overlap batch n's kernels.
+  int io_slot = -1;
+  if (!dev_off || !dev_io) {
+    io_slot = (int)(w->io_calls++ % 2);
+    auto& io = w->io[io_slot];
+    if (io.used) ESPN_CUDA_TRY(cudaStreamWaitEvent(w->cs, io.done, 0));
+    if (!dev_off) {
+      // the small per-batch tables via a pinned ring slot (an ASYNC caller may
+      // enqueue batch n+1 before batch n's H2D copies ran)
+      auto& sl = w->slots[w->calls % espn_gpu_workspace::kSlots];
+      if (sl.used) ESPN_CUDA_TRY(cudaEventSynchronize(sl.copied));
+      std::memcpy(sl.cand_off, a->cand_offsets, (B + 1) * sizeof(uint64_t));
+      ESPN_CUDA_TRY(cudaMemcpyAsync(io.cand_off, sl.cand_off, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, w->cs));
+      if (a->needed_counts) {
+        std::memcpy(sl.needed, a->needed_counts, B * sizeof(uint32_t));
+        ESPN_CUDA_TRY(cudaMemcpyAsync(io.needed_in, sl.needed, B * sizeof(uint32_t), cudaMemcpyHostToDevice, w->cs));
+        needed_in = io.needed_in;
+      }
+      ESPN_CUDA_TRY(cudaEventRecord(sl.copied, w->cs));
+      sl.used = true;
+      ++w->calls;
+      cand_off = io.cand_off;
     }
-    ESPN_CUDA_TRY(cudaEventRecord(sl.copied, s));
-    sl.used = true;
-    ++w->calls;
-    cand_off = w->cand_off;
+    if (!dev_io) {
+      ESPN_CUDA_TRY(cudaMemcpyAsync(io.q32, q32, (size_t)B * nq * t->d * sizeof(float), cudaMemcpyHostToDevice, w->cs));
+      if (C) {
+        ESPN_CUDA_TRY(cudaMemcpyAsync(io.ids, ids, C * sizeof(uint32_t), cudaMemcpyHostToDevice, w->cs));
+        ESPN_CUDA_TRY(cudaMemcpyAsync(io.cls, cls, C * sizeof(float), cudaMemcpyHostToDevice, w->cs));
+      }
+      q32 = io.q32;
+      ids = io.ids;
+      cls = io.cls;
+    }
+    ESPN_CUDA_TRY(cudaEventRecord(io.in_ready, w->cs));
+    ESPN_CUDA_TRY(cudaStreamWaitEvent(s, io.in_ready, 0));
   }
-  if (!dev_io) {
-    ESPN_CUDA_TRY(cudaMemcpyAsync(w->q32, q32, (size_t)B * nq * t->d * sizeof(float), cudaMemcpyHostToDevice, s));
-    if (C) {
-      ESPN_CUDA_TRY(cudaMemcpyAsync(w->ids, ids, C * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-      ESPN_CUDA_TRY(cudaMemcpyAsync(w->cls, cls, C * sizeof(float), cudaMemcpyHostToDevice, s));
+  // Outputs: device pointers (DEVICE_IO); pinned host buffers are written
+  // directly by the kernels (zero-copy, no D2H); other host buffers get a
+  // D2H from the workspace's output arrays.
+  uint32_t* out_ids_k = w->out_ids;
+  float* out_scores_k = w->out_scores;
+  uint32_t* out_counts_k = w->out_counts;
+  bool out_direct = dev_io;
+  if (dev_io) {
+    out_ids_k = o->ids;
+    out_scores_k = o->scores;
+    out_counts_k = o->counts;
+  } else {
+    const void* key[3] = {o->ids, o->scores, o->counts};
+    if (!(key[0] == w->zc_key[0] && key[1] == w->zc_key[1] && key[2] == w->zc_key[2])) {
+      bool ok = true;
+      for (int i = 0; i < 3; ++i) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, key[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+            !at.devicePointer) {
+          ok = false;
+          cudaGetLastError();  // clear a sticky "invalid value" for unregistered memory
+          break;
+        }
+        w->zc_dev[i] = at.devicePointer;
+      }
+      for (int i = 0; i < 3; ++i) w->zc_key[i] = key[i];
+      w->zc_ok = ok;
     }
-    q32 = w->q32;
-    ids = w->ids;
-    cls = w->cls;
+    if (w->zc_ok) {
+      out_ids_k = static_cast<uint32_t*>(w->zc_dev[0]);
+      out_scores_k = static_cast<float*>(w->zc_dev[1]);
+      out_counts_k = static_cast<uint32_t*>(w->zc_dev[2]);
+      out_direct = true;
+    }
   }
   // the device error word is sticky across un-synced ASYNC batches; it is
   // read and cleared by the synchronising call (or espn_gpu_workspace_sync)
@@ -781,7 +851,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   pp.unit_docs = tc ? (uint32_t)unit_docs : 1u;
   pp.write_tab = tc ? 1u : 0u;
   pp.tail_units = (fused && partial) ? 1u : 0u;
-  pp.out_counts = fused ? (dev_io ? o->counts : w->out_counts) : nullptr;
+  pp.out_counts = fused ? out_counts_k : nullptr;
   pp.fused_state = fused ? w->fused_state : nullptr;
   pp.dbg = dbg;
   plan_kernel<<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp);
@@ -834,9 +904,9 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     mp.cand_cls = cls;
     mp.alpha = a->alpha;
     mp.k = k;
-    mp.out_ids = dev_io ? o->ids : w->out_ids;
-    mp.out_scores = dev_io ? o->scores : w->out_scores;
-    mp.out_counts = dev_io ? o->counts : w->out_counts;
+    mp.out_ids = out_ids_k;
+    mp.out_scores = out_scores_k;
+    mp.out_counts = out_counts_k;
     mp.unit_top = w->unit_top;
     mp.dedup = w->dedup;
     mp.ff_seen = w->ff_seen;
@@ -878,9 +948,9 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   tp.cand_cls = cls;
   tp.cand_off = cand_off;
   tp.needed = w->needed;
-  tp.out_ids = dev_io ? o->ids : w->out_ids;
-  tp.out_scores = dev_io ? o->scores : w->out_scores;
-  tp.out_counts = dev_io ? o->counts : w->out_counts;
+  tp.out_ids = out_ids_k;
+  tp.out_scores = out_scores_k;
+  tp.out_counts = out_counts_k;
   tp.err = w->err;
   tp.n_queries = B;
   tp.rerank_count = a->rerank_count;
@@ -926,7 +996,11 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     ++w->prof_calls;
   }
 
-  if (!dev_io) {
+  if (io_slot >= 0) {  // every kernel reading the I/O slot is enqueued
+    ESPN_CUDA_TRY(cudaEventRecord(w->io[io_slot].done, s));
+    w->io[io_slot].used = true;
+  }
+  if (!out_direct) {
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->ids, w->out_ids, (size_t)B * k * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->scores, w->out_scores, (size_t)B * k * sizeof(float), cudaMemcpyDeviceToHost, s));
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->counts, w->out_counts, (size_t)B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
