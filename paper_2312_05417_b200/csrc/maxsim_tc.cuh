@@ -52,12 +52,12 @@ struct TcLayout {
   static constexpr int STAGE_SLOTS = 4 * NQC;
   static constexpr int PANEL_BYTES = STAGE_SLOTS * PW;  // one K-panel of a stage
   static constexpr int STAGE_BYTES = NP * PANEL_BYTES;
-  // A (query) operand: K-major SWIZZLE_NONE core matrices
+  // A (query) operand: the same K-major swizzled panel layout as the rows
+  // (RowLayout with t = A_ROWS), so the tensor core reads A conflict-free
   static constexpr int CH = D / 8;                 // 16-byte chunks per query row
-  static constexpr int A_SBO = CH * 128;
-  static constexpr int A_LBO = 128;
   static constexpr int A_ROWS = 96 + NU * 128;     // zeros | Q0 | zeros | Q1 | ...
-  static constexpr int A_BYTES = A_ROWS * D * 2;
+  static constexpr int A_PANEL_BYTES = A_ROWS * PW;
+  static constexpr int A_BYTES = NP * A_PANEL_BYTES;
   static constexpr int MAX_SLOTS = UNITMAX * 64;   // slot budget of one unit
   static constexpr int NG = MAX_SLOTS / 8;         // 8-slot groups
   static constexpr int MAXW = NG / 32;             // bitmap words (one bit per group)
@@ -563,7 +563,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
               w4[h] = (uint32_t)h0 | ((uint32_t)h1 << 16);
             }
             const int r = abase + i;
-            *reinterpret_cast<uint4*>(sA + (r >> 3) * L::A_SBO + c * L::A_LBO + (r & 7) * 16) =
+            *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, r, c)) =
                 make_uint4(w4[0], w4[1], w4[2], w4[3]);
           }
           if (bad) atomicOr(p.err, ERR_NONFINITE_QUERY);
@@ -615,7 +615,9 @@ maxsim_tc_kernel(const MaxSimParams p) {
     }
   } else if (warp == L::MMA_WARP) {
     // ============================ MMA ISSUER ==================================
-    if (lane == 0) {
+    // The whole warp walks the schedule (operands warp-uniform, in uniform
+    // registers); one elected lane issues each tcgen05.mma / commit.
+    {
       uint32_t gs = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       for (uint32_t it = 0;; ++it) {
@@ -644,20 +646,20 @@ maxsim_tc_kernel(const MaxSimParams p) {
             if ((p.dbg & 2u) || ((p.dbg & 64u) && w > 0)) break;
             const uint32_t idesc = umma_idesc_f16(128, n_mma, p.bf16);
             const uint32_t a_row0 = 96 + 128 * us - 32 * w;
-            const uint32_t a_addr = a_base + (a_row0 >> 3) * L::A_SBO;
+            const uint32_t a_addr = a_base + a_row0 * L::PW;
             const uint32_t b_addr = b_base + s * L::STAGE_BYTES + w * L::NQC * L::PW;
 #pragma unroll
             for (int ks = 0; ks < L::KSTEPS; ++ks) {
               const uint32_t kb = ks * 32;  // K offset in bytes
-              const uint64_t ad = umma_desc_kmajor(a_addr + ks * 2 * L::A_LBO, L::A_LBO, L::A_SBO);
+              const uint64_t ad = umma_desc_sw(a_addr + (kb / L::PW) * L::A_PANEL_BYTES + (kb % L::PW), 8 * L::PW, L::SWZ);
               const uint64_t bd = umma_desc_sw(b_addr + (kb / L::PW) * L::PANEL_BYTES + (kb % L::PW),
                                                8 * L::PW, L::SWZ);
-              umma_f16(d_tmem, ad, bd, idesc, acc);
+              umma_f16_elect(d_tmem, ad, bd, idesc, acc);
               acc = 1;
             }
           }
-          umma_commit(&empty_bar[s]);
-          umma_commit(&tfull_bar[buf]);
+          umma_commit_elect(&empty_bar[s]);
+          umma_commit_elect(&tfull_bar[buf]);
         }
       }
     }
@@ -729,34 +731,29 @@ maxsim_tc_kernel(const MaxSimParams p) {
             for (int qq = 0; qq < GPC; ++qq) {
               const int q = c * GPC + qq;
               const float* x = &v[c][8 * qq];
-              const uint32_t nval = (gvw[q / 4] >> (8 * (q % 4))) & 0xFFu;  // warp-uniform
+              const uint32_t nval = (gvw[q / 4] >> (8 * (q % 4))) & 0xFFu;
               const float x0 = x[0];
-              if (nval >= 8u) {  // full group (all but a doc's last): no masking
-                gm[q] = fmaxf(fmax3(x0, x[1], x[2]), fmax3(fmax3(x[3], x[4], x[5]), x[6], x[7]));
-              } else {
-                const float x1 = sel_gt(nval, 1, x[1], x0), x2 = sel_gt(nval, 2, x[2], x0);
-                const float x3 = sel_gt(nval, 3, x[3], x0), x4 = sel_gt(nval, 4, x[4], x0);
-                const float x5 = sel_gt(nval, 5, x[5], x0), x6 = sel_gt(nval, 6, x[6], x0);
-                const float x7 = sel_gt(nval, 7, x[7], x0);
-                gm[q] = fmaxf(fmax3(x0, x1, x2), fmax3(fmax3(x3, x4, x5), x6, x7));
-              }
+              const float x1 = sel_gt(nval, 1, x[1], x0), x2 = sel_gt(nval, 2, x[2], x0);
+              const float x3 = sel_gt(nval, 3, x[3], x0), x4 = sel_gt(nval, 4, x[4], x0);
+              const float x5 = sel_gt(nval, 5, x[5], x0), x6 = sel_gt(nval, 6, x[6], x0);
+              const float x7 = sel_gt(nval, 7, x[7], x0);
+              gm[q] = fmaxf(fmax3(x0, x1, x2), fmax3(fmax3(x3, x4, x5), x6, x7));
             }
           }
           if (tid == 0) { asm volatile("" ::"f"(gm[L::NGH - 1])); ESPN_STRACE(7, gs); }
+          // doc-boundary scan, branch-free: a doc's running max is flushed
+          // (predicated shared red.max) when the next doc starts
           float m = -INFINITY;
 #pragma unroll
           for (int q = 0; q < L::NGH; ++q) {
-            if ((uint32_t)(8 * q) < nv) {
-              if (q > 0 && ((sbits >> q) & 1u)) {
-                atomicMax(&my_pm[doc], ord_key(m));
-                ++doc;
-                m = gm[q];
-              } else {
-                m = fmaxf(m, gm[q]);
-              }
-            }
+            const bool valid = (uint32_t)(8 * q) < nv;
+            const bool start = q > 0 && valid && ((sbits >> q) & 1u);
+            red_max_shared_if(start, &my_pm[doc], ord_key(m));
+            doc += start ? 1 : 0;
+            const float g = valid ? gm[q] : -INFINITY;
+            m = start ? g : fmaxf(m, g);
           }
-          atomicMax(&my_pm[doc], ord_key(m));
+          red_max_shared_if(true, &my_pm[doc], ord_key(m));
           if (tid == 0) ESPN_STRACE(5, gs);
         } else {
           tc_fence_before();

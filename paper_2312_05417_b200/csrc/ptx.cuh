@@ -127,6 +127,27 @@ __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint6
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-collective forms: the whole (converged) warp executes them with
+// warp-uniform operands -- kept in uniform registers, no per-lane R2UR moves
+// -- and one elected lane issues the instruction.
+__device__ __forceinline__ void umma_f16_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 // Arrive on `bar` when all previously issued tcgen05.mma of this thread complete.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
@@ -211,6 +232,13 @@ __device__ __forceinline__ float sel_gt(uint32_t n, uint32_t j, float a, float b
   return r;
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+// Predicated shared-memory max reduction (no branch): if (pred) *addr = max(*addr, v).
+__device__ __forceinline__ void red_max_shared_if(bool pred, int* addr, int v) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tsetp.ne.u32 P, %0, 0;\n\t@P red.shared.max.s32 [%1], %2;\n\t}" ::"r"((uint32_t)pred),
+      "r"(smem_u32(addr)), "r"(v)
+      : "memory");
+}
 // Order-preserving float <-> int key (non-NaN): signed int compare == float compare.
 __device__ __forceinline__ int ord_key(float f) {
   const int i = __float_as_int(f);
