@@ -77,7 +77,8 @@ struct TcLayout {
   static constexpr int DEDUP_WARP = COMBINE_WARP + 1;  // fused top-k: duplicate check
   static constexpr int RANK_WARP = DEDUP_WARP + 1;     // fused top-k: keys, unit top-k
   static constexpr int QUERY_WARP = RANK_WARP + 1;     // unit query tile -> A operand slot
-  static constexpr int NWARPS = QUERY_WARP + 1;
+  static constexpr int PATCH_WARP = QUERY_WARP + 1;    // pad slots <- copies of the doc's last row
+  static constexpr int NWARPS = PATCH_WARP + 1;
   static constexpr int NB = 8;                     // bow ring (combine -> rank) depth, in units
   static constexpr int HALF = NQC / 2;             // columns per epilogue warp per stage
   static constexpr int LW = HALF < 32 ? HALF : 32; // tcgen05.ld width (columns)
@@ -90,7 +91,11 @@ struct TcLayout {
     uint64_t cfirst;            // candidate index of the unit's first doc
     uint32_t bitmap[MAXW];      // bit g: a doc starts at group g
     uint32_t wprefix[MAXW];     // docs starting before word w
-    uint8_t gvalid[NG];         // valid (non-pad) columns of group g, 1..8
+    // Pad patches (loader-built): for each doc whose last 8-slot group is
+    // partial, {stage-relative slot of its last row | pad count << 16 |
+    // stage << 20}, in stage order.
+    uint32_t pt[UNITMAX];
+    uint32_t n_pt;
     // Bulk-copy plan (loader-built): one op per (doc, stage piece, K-panel)
     // {src lo, src hi, byte offset in the stage, bytes}, in stage order;
     // stage st issues ops [op_beg[st], op_beg[st+1]) (last stage: to n_ops),
@@ -108,7 +113,7 @@ struct TcLayout {
   static constexpr int OFF_UK = (OFF_UNIT + NU * (int)sizeof(Unit) + 15) / 16 * 16;  // rank warp: unit keys
   static constexpr int OFF_RING = OFF_UK + UNITMAX * 8;
   static constexpr int OFF_BAR = OFF_RING + NB * UNITMAX * 4;
-  static constexpr int N_BARS = 2 * NS + 2 * NBUF + 3 * NU + 2 * NB;
+  static constexpr int N_BARS = 3 * NS + 2 * NBUF + 3 * NU + 2 * NB;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
@@ -345,6 +350,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
   uint64_t* edone_bar = uempty_bar + L::NU;        // [NU] epilogue (all lanes) -> combine
   uint64_t* bdone_bar = edone_bar + L::NU;         // [NB] combine -> rank (bow ring entry full)
   uint64_t* bfree_bar = bdone_bar + L::NB;         // [NB] rank -> combine (bow ring entry free)
+  uint64_t* patched_bar = bfree_bar + L::NB;       // [NS] patch warp -> MMA (stage rows + pads ready)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
   const int tid = threadIdx.x;
@@ -383,6 +389,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
       mbar_init(&bdone_bar[i], 1);
       mbar_init(&bfree_bar[i], 1);
     }
+    for (int i = 0; i < L::NS; ++i) mbar_init(&patched_bar[i], 1);
 
     mbar_fence_init();
   }
@@ -446,7 +453,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
       }
       __syncwarp();
       // doc info + slot prefix sum (warp scan) + group plan + copy ops
-      uint32_t carry = 0, ocarry = 0;
+      uint32_t carry = 0, ocarry = 0, pcarry = 0;
 #pragma unroll
       for (int r = 0; r < NK; ++r) {
         const uint32_t k = r * 32 + lane;
@@ -464,16 +471,21 @@ maxsim_tc_kernel(const MaxSimParams p) {
         const uint32_t st0 = start / L::STAGE_SLOTS, st1 = fits ? (start + t - 1) / L::STAGE_SLOTS : st0;
         const uint32_t npc = fits ? (st1 - st0 + 1) * L::NP : 0u;  // copy ops of this doc
         uint32_t oincl = npc;
+        const uint32_t npt = (fits && pad != t) ? 1u : 0u;  // pad patch of this doc
+        uint32_t pincl = npt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t v = __shfl_up_sync(0xffffffffu, oincl, o);
-          if (lane >= o) oincl += v;
+          const uint32_t vp = __shfl_up_sync(0xffffffffu, pincl, o);
+          if (lane >= o) { oincl += v; pincl += vp; }
         }
         if (fits) {
           atomicOr(&U.bitmap[start >> 8], 1u << ((start >> 3) & 31));
-          const uint32_t g0 = start >> 3, ng = pad >> 3;
-          for (uint32_t g = 0; g + 1 < ng; ++g) U.gvalid[g0 + g] = 8;
-          U.gvalid[g0 + ng - 1] = (uint8_t)(t - 8 * (ng - 1));
+          if (npt) {  // the doc's last row and its pads share one 8-slot group, one stage
+            const uint32_t last = start + t - 1, stl = last / L::STAGE_SLOTS;
+            const uint32_t pi = pcarry + pincl - 1;
+            U.pt[pi] = (last - stl * L::STAGE_SLOTS) | ((pad - t) << 16) | (stl << 20);
+          }
           // one op per stage piece and K-panel: the piece [a, e) of the doc's
           // slots inside stage st lands at (a - x0) * PW of panel pn
           uint32_t o = ocarry + oincl - npc;
@@ -492,6 +504,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
         }
         carry += __shfl_sync(0xffffffffu, incl, 31);
         ocarry += __shfl_sync(0xffffffffu, oincl, 31);
+        pcarry += __shfl_sync(0xffffffffu, pincl, 31);
       }
       if (carry > (uint32_t)L::MAX_SLOTS) {
         if (lane == 0) atomicOr(p.err, ERR_UNIT_TOO_LARGE);
@@ -510,9 +523,62 @@ maxsim_tc_kernel(const MaxSimParams p) {
         U.S = carry;
         U.tail = tail;
         U.n_ops = ocarry;
+        U.n_pt = pcarry;
       }
       __syncwarp();
       if (lane == 0) { ESPN_TRACE(2, it); mbar_arrive(&ufull_bar[us]); }
+    }
+  } else if (warp == L::PATCH_WARP) {
+    // ============================ PAD PATCH =====================================
+    // Once a stage's rows have landed, every doc whose last 8-slot group is
+    // partial gets copies of its last row in its pad slots (re-swizzled for
+    // the slot), so each MMA column of a group is a real row of its doc and
+    // the epilogue's group maxima need no masking.  One lane per doc.
+    uint32_t gs = 0;
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t ug = blockIdx.x + it * gridDim.x;
+      if (ug >= n_units) break;
+      const uint32_t us = it % L::NU;
+      const typename L::Unit& U = units[us];
+      mbar_wait(&ufull_bar[us], (it / L::NU) & 1);
+      const uint32_t S = U.S, npt = U.n_pt;
+      const uint32_t n_st = (S + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
+      uint32_t pc = 0;  // next patch of the unit (patches are in stage order)
+      for (uint32_t st = 0; st < n_st; ++st, ++gs) {
+        const uint32_t s = gs % L::NS;
+        mbar_wait(&full_bar[s], (gs / L::NS) & 1);
+        uint8_t* stage = sB + s * L::STAGE_BYTES;
+        for (;;) {
+          const uint32_t i = pc + lane;
+          const uint32_t e = i < npt ? U.pt[i] : 0xFFFFFFFFu;
+          const bool mine = i < npt && (e >> 20) == st;
+          const uint32_t nmine = __popc(__ballot_sync(0xffffffffu, mine));  // a prefix of the lanes
+          if (mine) {
+            const uint32_t slot = e & 0xFFFFu, npad = (e >> 16) & 0xFu;
+            const uint32_t sws = ((slot * (uint32_t)L::PW) >> 7) & (uint32_t)(L::RL::CPP - 1);
+#pragma unroll
+            for (int pn = 0; pn < L::NP; ++pn) {
+              uint8_t* panel = stage + pn * L::PANEL_BYTES;
+              uint4 c[L::RL::CPP];
+#pragma unroll
+              for (int cc = 0; cc < L::RL::CPP; ++cc)
+                c[cc] = *reinterpret_cast<const uint4*>(panel + slot * L::PW + ((cc ^ sws) << 4));
+              for (uint32_t r = 1; r <= npad; ++r) {
+                const uint32_t ds = slot + r;
+                const uint32_t swd = ((ds * (uint32_t)L::PW) >> 7) & (uint32_t)(L::RL::CPP - 1);
+#pragma unroll
+                for (int cc = 0; cc < L::RL::CPP; ++cc)
+                  *reinterpret_cast<uint4*>(panel + ds * L::PW + ((cc ^ swd) << 4)) = c[cc];
+              }
+            }
+          }
+          pc += nmine;
+          if (nmine < 32) break;
+        }
+        fence_proxy_async_smem();  // patched rows are read by the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&patched_bar[s]);
+      }
     }
   } else if (warp == L::QUERY_WARP) {
     // ============================ QUERY TILE ====================================
@@ -629,7 +695,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
         const uint32_t n_st = (S + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
         for (uint32_t st = 0; st < n_st; ++st, ++gs) {
           const uint32_t s = gs % L::NS, buf = gs % L::NBUF;
-          mbar_wait(&full_bar[s], (gs / L::NS) & 1);
+          mbar_wait(&patched_bar[s], (gs / L::NS) & 1);  // rows landed and pads patched
           ESPN_STRACE(1, gs);
           mbar_wait(&tempty_bar[buf], ((gs / L::NBUF) & 1) ^ 1);
           ESPN_STRACE(2, gs);
@@ -703,15 +769,6 @@ maxsim_tc_kernel(const MaxSimParams p) {
           const uint32_t bw = U.bitmap[G0 >> 5];
           const uint32_t sbits = (bw >> (G0 & 31)) & ((1u << L::NGH) - 1u);
           int doc = (int)(U.wprefix[G0 >> 5] + __popc(bw & ((2u << (G0 & 31)) - 1u))) - 1;
-          uint32_t gvw[(L::NGH + 3) / 4];
-          if constexpr (L::NGH % 4 == 0) {
-#pragma unroll
-            for (int c = 0; c < L::NGH / 4; ++c) gvw[c] = *reinterpret_cast<const uint32_t*>(&U.gvalid[G0 + 4 * c]);
-          } else {  // G0 is only NGH-aligned: byte loads
-            gvw[0] = 0;
-#pragma unroll
-            for (int q = 0; q < L::NGH; ++q) gvw[0] |= (uint32_t)U.gvalid[G0 + q] << (8 * q);
-          }
           constexpr int GPC = L::LW / 8;  // groups per chunk
           float gm[L::NGH];
 #pragma unroll
@@ -731,13 +788,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
             for (int qq = 0; qq < GPC; ++qq) {
               const int q = c * GPC + qq;
               const float* x = &v[c][8 * qq];
-              const uint32_t nval = (gvw[q / 4] >> (8 * (q % 4))) & 0xFFu;
-              const float x0 = x[0];
-              const float x1 = sel_gt(nval, 1, x[1], x0), x2 = sel_gt(nval, 2, x[2], x0);
-              const float x3 = sel_gt(nval, 3, x[3], x0), x4 = sel_gt(nval, 4, x[4], x0);
-              const float x5 = sel_gt(nval, 5, x[5], x0), x6 = sel_gt(nval, 6, x[6], x0);
-              const float x7 = sel_gt(nval, 7, x[7], x0);
-              gm[q] = fmaxf(fmax3(x0, x1, x2), fmax3(fmax3(x3, x4, x5), x6, x7));
+              // pad columns hold copies of the doc's last row (patch warp): no masking
+              gm[q] = fmaxf(fmax3(x[0], x[1], x[2]), fmax3(fmax3(x[3], x[4], x[5]), x[6], x[7]));
             }
           }
           if (tid == 0) { asm volatile("" ::"f"(gm[L::NGH - 1])); ESPN_STRACE(7, gs); }
