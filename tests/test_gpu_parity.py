@@ -423,3 +423,36 @@ def test_fused_topk_duplicates_across_units_and_tail(cuda_ok):
         again = rr.rerank_arrays(q, ids, cls, off, full, kernel="tcgen05")
         assert np.array_equal(again[0], good[0]) and np.array_equal(again[2], good[2])
     rr.close(); store.close()
+
+
+# ---- host-I/O path: inputs staged on the workspace copy stream (double-
+# buffered slots), ASYNC batches in flight, ranked lists written zero-copy
+# into pinned host outputs -- identical to the synchronous pageable path ----
+def test_host_io_async_pipelined_zero_copy(cuda_ok):
+    import torch
+    rp, codes = synth.make_table(20000, 32, 1, 63, seed=101)
+    store = api.GpuStore(rp, codes, 32)
+    B, K = 8, 600
+    cfg = api.PipelineConfig(rerank_count=K, final_k=10)
+    batches = []
+    for j in range(5):
+        q, src = synth.make_queries(rp, codes, 32, B, seed=102 + j)
+        ids, cls, off = synth.make_candidates(20000, B, K, src=src, seed=110 + j)
+        batches.append((q, ids, cls, off))
+    rr = api.Reranker(store, B, B * K, 32)
+    want = [rr.rerank_arrays(q, ids, cls, off, cfg) for q, ids, cls, off in batches]  # pageable, synchronous
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    ins = [(pin(q), pin(ids.view(np.int32)), pin(cls), off) for q, ids, cls, off in batches]
+    outs = [(pin(np.zeros((B, 10), np.int32)), pin(np.zeros((B, 10), np.float32)), pin(np.zeros(B, np.int32)), None)
+            for _ in batches]
+    s = torch.cuda.Stream()
+    for (q, ids, cls, off), o in zip(ins, outs):  # all five queued before any sync
+        rr.rerank_arrays(q, ids, cls, off, cfg, out=o, stream=s.cuda_stream, sync=False)
+    s.synchronize()
+    rr.sync(s.cuda_stream)
+    for w, o in zip(want, outs):
+        assert np.array_equal(w[0].view(np.int32), o[0].numpy())
+        assert np.array_equal(w[1].view(np.uint32), o[1].numpy().view(np.uint32))
+        assert np.array_equal(w[2].view(np.int32), o[2].numpy())
+    rr.close()
+    store.close()
