@@ -12,6 +12,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--dbg", default="0x100")
 ap.add_argument("--reps", type=int, default=8)
 ap.add_argument("--batches", type=int, default=4)
+ap.add_argument("--shards", type=int, default=1)
 args = ap.parse_args()
 os.environ["ESPN_DEBUG"] = args.dbg
 ROOT = Path(__file__).resolve().parent.parent
@@ -24,22 +25,27 @@ from paper_2312_05417_b200 import _lib as L, api
 cfg = bench.CONFIGS[args.config]
 dev = torch.device("cuda", 0)
 lib = L.lib()
-row_ptr = torch.zeros(cfg["n_docs"] + 1, dtype=torch.int64, device=dev)
-assert lib.espn_gpu_synth_table(cfg["n_docs"], cfg["d"], 0, cfg["t_min"], cfg["t_max"], bench.SEED, 1, 0,
+G = args.shards
+n_local = (cfg["n_docs"] + G - 1) // G
+row_ptr = torch.zeros(n_local + 1, dtype=torch.int64, device=dev)
+assert lib.espn_gpu_synth_table(n_local, cfg["d"], 0, cfg["t_min"], cfg["t_max"], bench.SEED, G, 0,
                                 row_ptr.data_ptr(), None, None) == 0
 n_tok = int(row_ptr[-1])
 rows = torch.empty(n_tok * cfg["d"], dtype=torch.int16, device=dev)
-assert lib.espn_gpu_synth_table(cfg["n_docs"], cfg["d"], 0, cfg["t_min"], cfg["t_max"], bench.SEED, 1, 0,
+assert lib.espn_gpu_synth_table(n_local, cfg["d"], 0, cfg["t_min"], cfg["t_max"], bench.SEED, G, 0,
                                 row_ptr.data_ptr(), rows.data_ptr(), None) == 0
-store = api.GpuStore.from_device(row_ptr, rows, cfg["d"], "f16", device=0, rows_tiled=True)
+store = api.GpuStore.from_device(row_ptr, rows, cfg["d"], "f16", shard_count=G, shard_index=0, device=0,
+                                 rows_tiled=True)
+from paper_2312_05417_b200.sharding import split_by_owner
 B, K, R, k, nq = cfg["batch"], cfg["K"], cfg["R"], cfg["k"], cfg["nq"]
 bts = bench.make_batches(cfg, args.batches, B)
 dbs = []
 for bt in bts:
-    dbs.append(dict(q=torch.from_numpy(bt["q"]).to(dev), ids=torch.from_numpy(bt["ids"].view(np.int32)).to(dev),
-                    cls=torch.from_numpy(bt["cls"]).to(dev),
-                    doff=torch.from_numpy(bt["off"].astype(np.int64)).to(dev),
-                    dneed=torch.full((B,), R, dtype=torch.int32, device=dev)))
+    ids, cls, off, need = split_by_owner(bt["ids"], bt["cls"], bt["off"], R, G, 0)
+    dbs.append(dict(q=torch.from_numpy(bt["q"]).to(dev), ids=torch.from_numpy(ids.view(np.int32)).to(dev),
+                    cls=torch.from_numpy(cls).to(dev),
+                    doff=torch.from_numpy(off.astype(np.int64)).to(dev),
+                    dneed=torch.from_numpy(need.astype(np.int32)).to(dev)))
 rr = api.Reranker(store, B, B * K, nq, max_list=K)
 out = torch.zeros(2 * B * k + B, dtype=torch.int32, device=dev)
 base = out.data_ptr()
