@@ -793,19 +793,21 @@ maxsim_tc_kernel(const MaxSimParams p) {
             }
           }
           if (tid == 0) { asm volatile("" ::"f"(gm[L::NGH - 1])); ESPN_STRACE(7, gs); }
-          // doc-boundary scan, branch-free: a doc's running max is flushed
-          // (predicated shared red.max) when the next doc starts
+          if (p.dbg & 32u) continue;  // profiling knob: no scan / flush
+          // doc-boundary scan, branch-free: after every group the running max
+          // of the current doc goes to pm with a shared red.max (unconditional
+          // -- a doc's last write carries its maximum; predicated flushes
+          // compile into divergent branch blocks)
           float m = -INFINITY;
 #pragma unroll
           for (int q = 0; q < L::NGH; ++q) {
             const bool valid = (uint32_t)(8 * q) < nv;
             const bool start = q > 0 && valid && ((sbits >> q) & 1u);
-            red_max_shared_if(start, &my_pm[doc], ord_key(m));
             doc += start ? 1 : 0;
             const float g = valid ? gm[q] : -INFINITY;
             m = start ? g : fmaxf(m, g);
+            red_max_shared(&my_pm[doc], ord_key(m));
           }
-          red_max_shared_if(true, &my_pm[doc], ord_key(m));
           if (tid == 0) ESPN_STRACE(5, gs);
         } else {
           tc_fence_before();

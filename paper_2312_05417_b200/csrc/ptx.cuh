@@ -232,6 +232,9 @@ __device__ __forceinline__ float sel_gt(uint32_t n, uint32_t j, float a, float b
   return r;
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+__device__ __forceinline__ void red_max_shared(int* addr, int v) {
+  asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(smem_u32(addr)), "r"(v) : "memory");
+}
 // Predicated shared-memory max reduction (no branch): if (pred) *addr = max(*addr, v).
 __device__ __forceinline__ void red_max_shared_if(bool pred, int* addr, int v) {
   asm volatile(
