@@ -36,16 +36,23 @@ namespace espn_k {
 
 template <int D>
 struct TcCfg;
-template <> struct TcCfg<16>  { static constexpr int NQC = 128, NS = 6, UNITMAX = 64, NU = 3; };
-template <> struct TcCfg<32>  { static constexpr int NQC = 128, NS = 4, UNITMAX = 64, NU = 3; };
-template <> struct TcCfg<64>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = 3; };
-template <> struct TcCfg<128> { static constexpr int NQC = 32,  NS = 3, UNITMAX = 32, NU = 2; };
+// REPA: replicated-A mode -- A = the query tile four times (no zero rows) and
+// ONE MMA per K-step covers the whole stage (N = 4 x NQC); lane quarter w of
+// the accumulator holds every slot, epilogue warps of quarter w read columns
+// [w NQC, (w+1) NQC).  Same MAC count as the block-diagonal mode, 4x fewer
+// (wider) MMA instructions and a 3x smaller A tile; needs 4 x NQC TMEM
+// columns per buffer, so it is used where NQC is small (d = 128).
+template <> struct TcCfg<16>  { static constexpr int NQC = 128, NS = 6, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
+template <> struct TcCfg<32>  { static constexpr int NQC = 128, NS = 4, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
+template <> struct TcCfg<64>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
+template <> struct TcCfg<128> { static constexpr int NQC = 32,  NS = 3, UNITMAX = 32, NU = 2; static constexpr bool REPA = true; };
 
 template <int D>
 struct TcLayout {
   using C = TcCfg<D>;
   using RL = RowLayout<D>;
   static constexpr int NQC = C::NQC, NS = C::NS, UNITMAX = C::UNITMAX, NU = C::NU;
+  static constexpr bool REPA = C::REPA;
   static constexpr int ROWB = RL::ROWB, PW = RL::PW, NP = RL::NP;
   static constexpr uint32_t SWZ = PW == 128 ? 2u : PW == 64 ? 4u : 6u;  // UMMA layout code
   static constexpr int KSTEPS = D / 16;
@@ -55,7 +62,7 @@ struct TcLayout {
   // A (query) operand: the same K-major swizzled panel layout as the rows
   // (RowLayout with t = A_ROWS), so the tensor core reads A conflict-free
   static constexpr int CH = D / 8;                 // 16-byte chunks per query row
-  static constexpr int A_ROWS = 96 + NU * 128;     // zeros | Q0 | zeros | Q1 | ...
+  static constexpr int A_ROWS = REPA ? NU * 128 : 96 + NU * 128;  // zeros | Q0 | zeros | Q1 | ... (REPA: Q0 x4 | Q1 x4 ...)
   static constexpr int A_PANEL_BYTES = A_ROWS * PW;
   static constexpr int A_BYTES = NP * A_PANEL_BYTES;
   static constexpr int MAX_SLOTS = UNITMAX * 64;   // slot budget of one unit
@@ -65,9 +72,10 @@ struct TcLayout {
   static constexpr int MAX_OPS = (UNITMAX + MAX_STAGES) * NP;  // docs + stage straddles, per K-panel
   static constexpr int PM_STRIDE = UNITMAX + 1;    // padded: conflict-free emits and combine
   static constexpr int PM_FLOATS = NU * 32 * PM_STRIDE;  // per unit slot: [query token][doc] keys
-  static constexpr int NBUF = (512 / NQC) < 4 ? (512 / NQC) : 4;
-  static constexpr uint32_t TMEM_COLS = NBUF * NQC <= 32 ? 32 : NBUF * NQC <= 64 ? 64
-                                      : NBUF * NQC <= 128 ? 128 : NBUF * NQC <= 256 ? 256 : 512;
+  static constexpr int BUFC = REPA ? 4 * NQC : NQC;  // TMEM columns per accumulator buffer
+  static constexpr int NBUF = (512 / BUFC) < 4 ? (512 / BUFC) : 4;
+  static constexpr uint32_t TMEM_COLS = NBUF * BUFC <= 32 ? 32 : NBUF * BUFC <= 64 ? 64
+                                      : NBUF * BUFC <= 128 ? 128 : NBUF * BUFC <= 256 ? 256 : 512;
   static constexpr int NPROD = 2;                  // bulk-copy producer warps
   static constexpr int NEPI = 8;                   // epilogue warps: 4 lane quarters x 2 column halves
   static constexpr int MMA_WARP = NEPI;
@@ -596,7 +604,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
       // batches of 4 items per lane keep all their loads in flight together.
       if (!tail) {
         const float* q = p.q32 + (size_t)b * p.nq * D;
-        const int abase = 96 + 128 * (int)us;
+        const int abase = (L::REPA ? 0 : 96) + 128 * (int)us;
         constexpr int ITEMS = 32 * L::CH / 32;  // per lane
         constexpr int BATCH = ITEMS < 4 ? ITEMS : 4;
 #pragma unroll
@@ -631,6 +639,12 @@ maxsim_tc_kernel(const MaxSimParams p) {
             const int r = abase + i;
             *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, r, c)) =
                 make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            if constexpr (L::REPA) {  // replicas for lane quarters 1..3
+#pragma unroll
+              for (int rq = 1; rq < 4; ++rq)
+                *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, r + 32 * rq, c)) =
+                    make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            }
           }
           if (bad) atomicOr(p.err, ERR_NONFINITE_QUERY);
         }
@@ -700,9 +714,26 @@ maxsim_tc_kernel(const MaxSimParams p) {
           mbar_wait(&tempty_bar[buf], ((gs / L::NBUF) & 1) ^ 1);
           ESPN_STRACE(2, gs);
           tc_fence_after();
-          const uint32_t d_tmem = tmem_base + buf * L::NQC;
+          const uint32_t d_tmem = tmem_base + buf * L::BUFC;
           const uint32_t x0 = st * L::STAGE_SLOTS;
           uint32_t acc = 0;
+          if constexpr (L::REPA) {
+            // one MMA per K-step over the whole stage: N = its slots (<= 4 NQC)
+            const int rem = (int)S - (int)x0;
+            const uint32_t nv = rem < L::STAGE_SLOTS ? (uint32_t)rem : (uint32_t)L::STAGE_SLOTS;
+            const uint32_t idesc = umma_idesc_f16(128, (nv + 15u) & ~15u, p.bf16);
+            const uint32_t a_addr = a_base + 128 * us * L::PW;
+            const uint32_t b_addr = b_base + s * L::STAGE_BYTES;
+            if (!(p.dbg & 2u))
+#pragma unroll
+              for (int ks = 0; ks < L::KSTEPS; ++ks) {
+                const uint32_t kb = ks * 32;
+                const uint64_t ad = umma_desc_sw(a_addr + (kb / L::PW) * L::A_PANEL_BYTES + (kb % L::PW), 8 * L::PW, L::SWZ);
+                const uint64_t bd = umma_desc_sw(b_addr + (kb / L::PW) * L::PANEL_BYTES + (kb % L::PW), 8 * L::PW, L::SWZ);
+                umma_f16_elect(d_tmem, ad, bd, idesc, acc);
+                acc = 1;
+              }
+          } else
 #pragma unroll 1
           for (int w = 0; w < 4; ++w) {
             const int rem = (int)S - (int)(x0 + w * L::NQC);
@@ -762,7 +793,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
           // after the last chunk landed.  Only the short doc-boundary scan over
           // NGH groups is sequential.
           const uint32_t nv = remv < L::HALF ? (uint32_t)remv : (uint32_t)L::HALF;
-          const uint32_t taddr0 = tmem_base + ((uint32_t)(w * 32) << 16) + buf * L::NQC + h * L::HALF;
+          const uint32_t taddr0 = tmem_base + ((uint32_t)(w * 32) << 16) + buf * L::BUFC +
+                                  (L::REPA ? w * L::NQC : 0) + h * L::HALF;
           float v[L::NLD][L::LW];
           tmem_ld_32x32b<L::LW>(taddr0, v[0]);
           const uint32_t G0 = xw >> 3;  // multiple of NGH
