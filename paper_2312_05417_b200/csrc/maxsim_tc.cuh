@@ -45,7 +45,7 @@ struct TcCfg;
 template <> struct TcCfg<16>  { static constexpr int NQC = 128, NS = 6, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
 template <> struct TcCfg<32>  { static constexpr int NQC = 128, NS = 4, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
 template <> struct TcCfg<64>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
-template <> struct TcCfg<128> { static constexpr int NQC = 32,  NS = 3, UNITMAX = 32, NU = 2; static constexpr bool REPA = true; };
+template <> struct TcCfg<128> { static constexpr int NQC = 64,  NS = 2, UNITMAX = 32, NU = 2; static constexpr bool REPA = true; };
 
 template <int D>
 struct TcLayout {
