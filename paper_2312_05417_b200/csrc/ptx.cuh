@@ -36,18 +36,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(0x989680)
       : "memory");
 }
-// Non-blocking: has the phase with this parity completed?
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
 // Arrive and add `bytes` to the barrier's expected transaction count.
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
@@ -70,29 +58,8 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// Arrive (without pending-count increment) once all prior cp.async of this
-// thread have landed in shared memory.
-__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
 
-// ---- cp.async (LDGSTS), 16 bytes, L2 only ----------------------------------
-__device__ __forceinline__ void cp_async_16(uint32_t dst_smem, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_16_hint(uint32_t dst_smem, const void* src, uint64_t policy) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "l"(policy)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-// ---- barriers / fences ------------------------------------------------------
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
+// ---- fences -----------------------------------------------------------------
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -117,16 +84,6 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// D[tmem] (+)= A[smem] . B[smem]^T, kind::f16 (fp16/bf16 in, fp32 accumulate).
-__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 // Warp-collective forms: the whole (converged) warp executes them with
 // warp-uniform operands -- kept in uniform registers, no per-lane R2UR moves
 // -- and one elected lane issues the instruction.
@@ -145,13 +102,6 @@ __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-// Arrive on `bar` when all previously issued tcgen05.mma of this thread complete.
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
       : "memory");
 }
@@ -190,17 +140,6 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE ("interleaved" core
-// matrices of 8 rows x 16 bytes): LBO = byte distance between K-adjacent core
-// matrices, SBO = byte distance between M/N-adjacent 8-row groups.
-__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-  d |= static_cast<uint64_t>(1) << 46;  // descriptor version 1 (sm_100)
-  return d;
-}
 // UMMA shared-memory descriptor, K-major, swizzled (layout code: 2 = 128B,
 // 4 = 64B, 6 = 32B).  SBO = byte distance between 8-row groups (8 x row
 // pitch); LBO is unused for swizzled K-major operands.  K advance inside the
@@ -221,26 +160,9 @@ __host__ __device__ __forceinline__ uint32_t umma_idesc_f16(uint32_t m, uint32_t
   return (1u << 4) | (bf16 << 7) | (bf16 << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
-// ---- numeric helpers ----------------------------------------------------------
-// (n > j) ? a : b as a forced SETP+SELP pair (keeps masked maxima branch-free;
-// plain ternaries on a runtime count get compiled into decision trees).
-__device__ __forceinline__ float sel_gt(uint32_t n, uint32_t j, float a, float b) {
-  float r;
-  asm("{\n\t.reg .pred q;\n\tsetp.gt.u32 q, %1, %2;\n\tselp.f32 %0, %3, %4, q;\n\t}"
-      : "=f"(r)
-      : "r"(n), "r"(j), "f"(a), "f"(b));
-  return r;
-}
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
 __device__ __forceinline__ void red_max_shared(int* addr, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(smem_u32(addr)), "r"(v) : "memory");
-}
-// Predicated shared-memory max reduction (no branch): if (pred) *addr = max(*addr, v).
-__device__ __forceinline__ void red_max_shared_if(bool pred, int* addr, int v) {
-  asm volatile(
-      "{\n\t.reg .pred P;\n\tsetp.ne.u32 P, %0, 0;\n\t@P red.shared.max.s32 [%1], %2;\n\t}" ::"r"((uint32_t)pred),
-      "r"(smem_u32(addr)), "r"(v)
-      : "memory");
 }
 // Order-preserving float <-> int key (non-NaN): signed int compare == float compare.
 __device__ __forceinline__ int ord_key(float f) {
