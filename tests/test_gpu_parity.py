@@ -456,3 +456,49 @@ def test_host_io_async_pipelined_zero_copy(cuda_ok):
         assert np.array_equal(w[2].view(np.int32), o[2].numpy())
     rr.close()
     store.close()
+
+
+# ---- full size (configs[1]): 8.8 M docs, the 18 GB table generated on the
+# device.  Size-independent parity: fused == separate top-k for every query,
+# and for sampled queries all 1000 MaxSim scores equal the CPU oracle computed
+# on the rows gathered back from HBM; the source doc ranks first ----
+def test_full_scale_c2_sampled_parity(oracle, cuda_ok):
+    import sys
+    from pathlib import Path
+    import torch
+    from paper_2312_05417_b200 import _lib as L
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    cfg = bench.CONFIGS["c2"]
+    N, d, B, K = cfg["n_docs"], cfg["d"], cfg["batch"], cfg["K"]
+    lib = L.lib()
+    rp = torch.zeros(N + 1, dtype=torch.int64, device="cuda")
+    assert lib.espn_gpu_synth_table(N, d, 0, cfg["t_min"], cfg["t_max"], bench.SEED, 1, 0, rp.data_ptr(), None, None) == 0
+    rows = torch.empty(int(rp[-1]) * d, dtype=torch.int16, device="cuda")
+    assert lib.espn_gpu_synth_table(N, d, 0, cfg["t_min"], cfg["t_max"], bench.SEED, 1, 0, rp.data_ptr(),
+                                    rows.data_ptr(), None) == 0
+    store = api.GpuStore.from_device(rp, rows, d, "f16", device=0, rows_tiled=True)
+    bt = bench.make_batches(cfg, 1, B)[0]
+    q, ids, cls, off = bt["q"], bt["ids"], bt["cls"], bt["off"]
+    rr = api.Reranker(store, B, B * K, 32)
+    pcfg = api.PipelineConfig(rerank_count=K, final_k=10)
+    gi, gs, gc, gbow = rr.rerank_arrays(q, ids, cls, off, pcfg, write_bow=True)
+    si, ss, sc, _ = rr.rerank_arrays(q, ids, cls, off, pcfg, separate_topk=True)
+    assert np.array_equal(gi, si) and np.array_equal(gs.view(np.uint32), ss.view(np.uint32))
+    assert np.array_equal(gc, sc) and np.all(gc == 10)
+    assert np.array_equal(gi[:, 0], ids.reshape(B, K)[:, 0])  # the perturbed query's source doc
+    for qi in (0, 37):
+        cid = torch.from_numpy(ids[qi * K:(qi + 1) * K].astype(np.int32)).cuda()
+        lrp = torch.zeros(K + 1, dtype=torch.int64, device="cuda")
+        assert lib.espn_gpu_gather(store.handle, cid.data_ptr(), K, None, lrp.data_ptr(), 0, None) == 0
+        lrows = torch.empty(int(lrp[-1]) * d, dtype=torch.int16, device="cuda")
+        assert lib.espn_gpu_gather(store.handle, cid.data_ptr(), K, lrows.data_ptr(), lrp.data_ptr(),
+                                   int(lrp[-1]), None) == 0
+        ot = oracle.OracleTable(lrp.cpu().numpy(), lrows.cpu().numpy().view(np.uint16), d)
+        st, obow = oracle.maxsim_batch(ot, oracle.round_to(q[qi:qi + 1]), np.arange(K, dtype=np.uint32),
+                                       np.array([0, K], np.uint64))
+        assert st == 0
+        e = rel_err(gbow[qi * K:(qi + 1) * K], obow)
+        assert e.max() <= RTOL, f"query {qi}: max rel err {e.max()}"
+    rr.close()
+    store.close()
