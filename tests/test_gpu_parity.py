@@ -93,6 +93,14 @@ def test_c2_shape_many_units(oracle, cuda_ok):
     check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
 
 
+def test_c3_shape_many_units(oracle, cuda_ok):
+    # configs[2] shape law (t ~ U{40..100}, d=128 -> the replicated-A, N=256
+    # MMA mode with two K-panels) at batch 32 on a 100k-doc table
+    rp, codes, q, ids, cls, off = build_case(100000, 128, 40, 100, B=32, K=1000, seed=7)
+    cfg = api.PipelineConfig(rerank_count=1000, final_k=10)
+    check_against_oracle(oracle, rp, codes, 128, "f16", q, ids, cls, off, cfg, "tcgen05")
+
+
 @pytest.mark.parametrize("kernel", ["tcgen05", "simt"])
 def test_partial_rerank_and_alpha(oracle, cuda_ok, kernel):
     rp, codes, q, ids, cls, off = build_case(5000, 32, 1, 63, B=4, K=1000, seed=9)
