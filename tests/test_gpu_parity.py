@@ -510,3 +510,54 @@ def test_full_scale_c2_sampled_parity(oracle, cuda_ok):
         assert e.max() <= RTOL, f"query {qi}: max rel err {e.max()}"
     rr.close()
     store.close()
+
+
+# ---- the graph-capturable mode the bench times: device arrays + device
+# offsets (the batch is planned on the device), captured in a CUDA graph and
+# replayed; identical to the host-offset call ----
+@pytest.mark.parametrize("partial", [False, True])
+def test_device_offsets_graph_replay(cuda_ok, partial):
+    import ctypes as C
+    import torch
+    from paper_2312_05417_b200 import _lib as L
+    rp, codes, q, ids, cls, off = build_case(20000, 32, 1, 63, B=16, K=700, seed=131)
+    R = 200 if partial else 700
+    cfg = api.PipelineConfig(rerank_count=R, final_k=10, alpha=0.9, partial_rerank_enabled=partial)
+    store = api.GpuStore(rp, codes, 32)
+    rr = api.Reranker(store, 16, 16 * 700, 32, max_list=700)
+    want = rr.rerank_arrays(q, ids, cls, off, cfg)
+    dq = torch.from_numpy(q).cuda()
+    did = torch.from_numpy(ids.view(np.int32)).cuda()
+    dcl = torch.from_numpy(cls).cuda()
+    doff = torch.from_numpy(off.astype(np.int64)).cuda()
+    out = torch.zeros(2 * 16 * 10 + 16, dtype=torch.int32, device="cuda")
+    base = out.data_ptr()
+    flags = L.ESPN_RERANK_DEVICE_IO | L.ESPN_RERANK_DEVICE_OFFSETS | L.ESPN_RERANK_ASYNC
+    flags |= L.ESPN_RERANK_PARTIAL if partial else 0
+
+    def enqueue(sp):
+        a = L.RerankArgs(n_queries=16, n_query_tokens=32, query_tokens=dq.data_ptr(), cand_ids=did.data_ptr(),
+                         cand_cls=dcl.data_ptr(), cand_offsets=doff.data_ptr(), rerank_count=R, final_k=10,
+                         alpha=0.9, flags=flags, kernel=L.ESPN_KERNEL_AUTO)
+        o = L.RerankOut(ids=base, scores=base + 4 * 160, counts=base + 8 * 160)
+        assert L.lib().espn_gpu_rerank(store.handle, rr.handle, C.byref(a), C.byref(o), C.c_void_p(sp)) == 0
+
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        enqueue(s.cuda_stream)  # eager first (lazy attributes)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        enqueue(torch.cuda.current_stream().cuda_stream)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        rr.sync()
+        o = out.cpu().numpy()
+        gi, gs, gc = o[:160].reshape(16, 10), o[160:320].view(np.float32).reshape(16, 10), o[320:]
+        assert np.array_equal(gc, want[2].view(np.int32))
+        assert np.array_equal(gi, want[0].view(np.int32))
+        assert np.array_equal(gs.view(np.uint32), want[1].view(np.uint32))
+    rr.close()
+    store.close()
