@@ -12,21 +12,23 @@
 //     document is one contiguous byte range per K-panel that ONE 1-D
 //     cp.async.bulk (TMA engine, UBLKCP) lands directly in the UMMA K-major
 //     SWIZZLE_{32,64,128}B operand layout -- no per-element address math, no
-//     register hop.  Pad slots of a doc's last 8-row group are not copied; the
-//     epilogue masks those columns.
-//   * Warp roles: 0-3 epilogue, 4 MMA issuer (one thread), 5 bulk-copy
-//     producer, 6 unit loader (candidate ids -> row offsets, slot plan, query
-//     tile) running NU-1 units ahead so the dependent id->row_ptr loads are off
-//     the copy path.
+//     register hop.  The pad slots of a doc's last 8-slot group get copies of
+//     its last row (pad-patch warp), so no column ever needs masking.
+//   * Warp roles (TcLayout): 8 epilogue, MMA issuer, 2 bulk-copy producers
+//     (loader-built op lists), unit loader (ids -> row_ptr issued before the
+//     slot wait; slot plan, doc-start bitmap, copy ops, pad patches), combine
+//     (ordered sums), dedup + rank (fused top-k), query tile, pad patch.
 //   * tcgen05.mma (M=128, N<=NQC, K=16) per quarter and K-step.  A is a 128-row
 //     window over [96 zero rows | Q (32 rows) | 96 zero rows ...] whose offset
 //     puts the query tokens on TMEM lanes 32w..32w+31 for quarter w
-//     ("block-diagonal" A), so all four lane quarters -- and all four epilogue
+//     ("block-diagonal" A), so all four lane quarters -- and all epilogue
 //     warps -- get useful work from every MMA into one accumulator buffer.
-//   * Epilogue warp w reads its lanes with tcgen05.ld: thread i holds query
-//     token i's dot products against the quarter's doc tokens along columns,
-//     so max over doc tokens is an in-register running max; per-doc partial
-//     maxima go to SMEM and one thread per doc sums the q maxima in ascending
+//     d = 128 uses the replicated-A mode instead (TcCfg::REPA).
+//   * Epilogue warp (w, h) reads its lanes with tcgen05.ld: thread i holds
+//     query token i's dot products against a 64-slot range along columns, so
+//     the max over doc tokens is a register max tree per 8-slot group and a
+//     branch-free doc-boundary scan; per-doc partial maxima go to SMEM (shared
+//     red.max) and the combine warp sums the q maxima per doc in ascending
 //     query-token order (the oracle's summation order).
 #pragma once
 #include "common.cuh"
