@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "espn_gpu.h"
+#include "espn_store.h"
 
 #if defined(ESPN_B200_WITH_REFERENCE_HEADERS)
 #include "espn/error.hpp"
@@ -161,6 +162,7 @@ enum class Kernel : std::uint32_t { automatic = ESPN_KERNEL_AUTO, tcgen05 = ESPN
 
 // Throws the espn:: exception class matching an espn_status (error.hpp:8-42).
 void throw_status(int status);
+void throw_status(int status, const std::string& message);
 
 // Record layout of the reference store (store.hpp:25-34), used only for the
 // QueryStats / FetchResult byte counters.
@@ -181,6 +183,10 @@ class Store {
   // docs[i].doc_id must equal i (dense ids, store.hpp:20)
   static Store from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtype = Dtype::f16,
                               RecordLayout layout = {}, int device = 0);
+  // open_store (store.hpp:111-112) for the HBM tier: reads a .espn store
+  // (include/espn_store.h, libespn_store.so) and uploads its rows; the
+  // record layout comes from the manifest.
+  static Store open_store(const std::string& base, Dtype dtype = Dtype::f16, int device = 0);
   ~Store();
   Store(Store&&) noexcept;
   Store& operator=(Store&&) noexcept;
@@ -228,6 +234,11 @@ class Reranker {
   const Store* store_;
   espn_gpu_workspace* ws_ = nullptr;
 };
+
+// build_store (store.hpp:48-51) from a CSR of fp32 rows (+ n_docs * d_cls CLS
+// values, or empty for zeros): writes <base>.espn / .manifest / .manifest.json.
+void build_store(const std::string& base, std::span<const std::uint64_t> row_ptr, std::span<const float> rows,
+                 std::uint32_t d, std::span<const float> cls = {}, RecordLayout layout = {});
 
 // The seam: stages 3-6 of run_query for one query (SPEC.md:276 (3)-(6)).
 std::pair<RankedList, QueryStats> rerank_candidates(const QueryEmbedding& query, const CandidateList& candidates,

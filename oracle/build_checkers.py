@@ -29,11 +29,11 @@ def build_cpp_tests() -> Path:
     against the CPU oracle (test infrastructure: links oracle/_build)."""
     out = ROOT / "tests" / "cpp" / "host_api_test"
     src = ROOT / "tests" / "cpp" / "host_api_test.cpp"
-    deps = [src, HOST_LIB, HERE / "espn_oracle.h", HERE / "_build" / "libespn_oracle.so"]
+    deps = [src, HOST_LIB, ROOT / "include" / "espn_b200.hpp", HERE / "espn_oracle.h", HERE / "_build" / "libespn_oracle.so"]
     if out.exists() and all(p.stat().st_mtime <= out.stat().st_mtime for p in deps):
         return out
     cmd = [CXX, "-std=c++20", "-O2", "-Wall", "-I", str(ROOT / "include"), "-I", str(ROOT / "oracle"), "-o", str(out),
-           str(src), "-L", str(LIB_DIR), "-lespn_host", "-lespn_gpu", "-L", str(ROOT / "oracle" / "_build"),
+           str(src), "-L", str(LIB_DIR), "-lespn_host", "-lespn_gpu", "-lespn_store", "-L", str(ROOT / "oracle" / "_build"),
            "-lespn_oracle", f"-Wl,-rpath,{LIB_DIR}", f"-Wl,-rpath,{ROOT / 'oracle' / '_build'}",
            "-Wl,-rpath,$ORIGIN/../../paper_2312_05417_b200/lib", "-Wl,-rpath,$ORIGIN/../../oracle/_build"]
     r = subprocess.run(cmd, capture_output=True, text=True)

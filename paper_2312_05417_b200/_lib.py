@@ -142,3 +142,46 @@ def lib() -> C.CDLL:
 
 def last_error() -> str:
     return (lib().espn_last_error() or b"").decode("utf-8", "replace")
+
+
+# ---- include/espn_store.h: the on-disk .espn store (libespn_store.so, host only) ----
+STORE_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libespn_store.so"
+
+
+class StoreHeader(C.Structure):
+    _fields_ = [("version", C.c_uint32), ("d", C.c_uint32), ("d_cls", C.c_uint32), ("value_width", C.c_uint32),
+                ("alignment", C.c_uint32), ("count", C.c_uint64)]
+
+
+class ManifestRecord(C.Structure):  # store.hpp:13-18
+    _fields_ = [("byte_offset", C.c_uint64), ("byte_length", C.c_uint32), ("token_count", C.c_uint32)]
+
+
+STORE_SIGNATURES = {
+    "espn_store_build": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_store_load_manifest": (C.c_int, [C.c_char_p, C.POINTER(StoreHeader), C.c_void_p]),
+    "espn_store_read_table": (C.c_int, [C.c_char_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_store_last_error": (C.c_char_p, []),
+}
+
+_store_lib = None
+
+
+def store_lib() -> C.CDLL:
+    """Load libespn_store.so (once).  Raises if it is missing."""
+    global _store_lib
+    if _store_lib is None:
+        if not STORE_LIB_PATH.exists():
+            raise RuntimeError(f"{STORE_LIB_PATH} not found: build it with `python -m paper_2312_05417_b200.build`")
+        h = C.CDLL(str(STORE_LIB_PATH))
+        for name, (res, args) in STORE_SIGNATURES.items():
+            f = getattr(h, name)
+            f.restype = res
+            f.argtypes = args
+        _store_lib = h
+    return _store_lib
+
+
+def store_last_error() -> str:
+    return (store_lib().espn_store_last_error() or b"").decode("utf-8", "replace")

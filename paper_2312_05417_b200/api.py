@@ -77,6 +77,69 @@ def _check(rc: int) -> None:
         raise _STATUS.get(rc, Error)(L.last_error())
 
 
+def _check_store(rc: int) -> None:
+    if rc != L.ESPN_OK:
+        raise _STATUS.get(rc, Error)(L.store_last_error())
+
+
+# ---- the on-disk store (store.hpp:37-54, include/espn_store.h) ---------------------
+@dataclass
+class StoreManifest:
+    """store.hpp:20-35 (records as a numpy structured array)."""
+    version: int
+    d: int
+    d_cls: int
+    value_width: int
+    alignment: int
+    records: np.ndarray  # dtype [("byte_offset", u8), ("byte_length", u4), ("token_count", u4)]
+
+    def count(self) -> int:
+        return int(self.records.shape[0])
+
+    def record_bytes(self, token_count):
+        return (self.d_cls + np.asarray(token_count, dtype=np.uint64) * self.d) * self.value_width
+
+
+_RECORD_DT = np.dtype([("byte_offset", "<u8"), ("byte_length", "<u4"), ("token_count", "<u4")])
+
+
+def build_store(base, row_ptr, rows, d: int, d_cls: int = 128, value_width: int = 2, alignment: int = 4096,
+                cls=None) -> StoreManifest:
+    """build_store (store.hpp:48-51): <base>.espn + <base>.manifest + .manifest.json
+    from a CSR of fp32 token rows (and optional n_docs x d_cls CLS vectors)."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+    rows = np.ascontiguousarray(rows, dtype=np.float32)
+    n = int(row_ptr.shape[0]) - 1
+    cls_a = None if cls is None else np.ascontiguousarray(cls, dtype=np.float32)
+    _check_store(L.store_lib().espn_store_build(str(base).encode(), n, int(d), int(d_cls), int(value_width),
+                                                int(alignment), row_ptr.ctypes.data, rows.ctypes.data,
+                                                cls_a.ctypes.data if cls_a is not None else None))
+    return load_manifest(base)
+
+
+def load_manifest(base) -> StoreManifest:
+    """load_manifest (store.hpp:54)."""
+    h = L.StoreHeader()
+    lib = L.store_lib()
+    _check_store(lib.espn_store_load_manifest(str(base).encode(), C.byref(h), None))
+    recs = np.zeros(int(h.count), _RECORD_DT)
+    _check_store(lib.espn_store_load_manifest(str(base).encode(), C.byref(h), recs.ctypes.data if h.count else None))
+    return StoreManifest(int(h.version), int(h.d), int(h.d_cls), int(h.value_width), int(h.alignment), recs)
+
+
+def read_store_table(base, dtype: str = "f16", with_cls: bool = False):
+    """Every document's rows as the GPU table's CSR of 2-byte `dtype` codes
+    (+ fp32 CLS vectors): (row_ptr, codes, cls or None)."""
+    m = load_manifest(base)
+    tok = m.records["token_count"].astype(np.uint64)
+    row_ptr = np.zeros(m.count() + 1, np.uint64)
+    codes = np.empty(max(int(tok.sum()) * m.d, 1), np.uint16)
+    cls = np.empty((m.count(), m.d_cls), np.float32) if with_cls else None
+    _check_store(L.store_lib().espn_store_read_table(str(base).encode(), _DTYPES[dtype], row_ptr.ctypes.data,
+                                                     codes.ctypes.data, cls.ctypes.data if cls is not None else None))
+    return row_ptr, codes[: int(row_ptr[-1]) * m.d], cls
+
+
 # ---- types.hpp / ivf.hpp / pipeline.hpp carriers --------------------------------
 @dataclass
 class EmbeddingMatrix:
@@ -268,6 +331,15 @@ class GpuStore:
         self.max_tokens = int(info.max_tokens)
         self.min_tokens = int(info.min_tokens)
         self._workspaces = {}
+
+    @classmethod
+    def open_store(cls, base, dtype: str = "f16", **kw) -> "GpuStore":
+        """open_store (store.hpp:111-112) for the HBM tier: reads the .espn
+        store (include/espn_store.h) and uploads its rows; d_cls /
+        value_width / alignment come from the manifest."""
+        m = load_manifest(base)
+        row_ptr, codes, _ = read_store_table(base, dtype)
+        return cls(row_ptr, codes, m.d, dtype, d_cls=m.d_cls, value_width=m.value_width, alignment=m.alignment, **kw)
 
     @classmethod
     def from_device(cls, row_ptr, rows, d: int, dtype: str = "f16", **kw) -> "GpuStore":

@@ -72,16 +72,37 @@ CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-fvisibility=def
 def build_host(force: bool = False) -> Path:
     """libespn_host.so: the C++ espn::gpu API (include/espn_b200.hpp) over the
     C-ABI, linked against libespn_gpu.so (rpath $ORIGIN)."""
-    deps = [HOST_SRC, ROOT / "include" / "espn_b200.hpp", ROOT / "include" / "espn_gpu.h", LIB]
+    build_store_lib()
+    deps = [HOST_SRC, ROOT / "include" / "espn_b200.hpp", ROOT / "include" / "espn_gpu.h", LIB, STORE_LIB]
     if not force and HOST_LIB.exists() and all(p.stat().st_mtime <= HOST_LIB.stat().st_mtime for p in deps):
         return HOST_LIB
     cmd = [CXX, *CXX_FLAGS, "-shared", "-I", str(ROOT / "include"), "-o", str(HOST_LIB), str(HOST_SRC),
-           "-L", str(LIB_DIR), "-lespn_gpu", "-Wl,-rpath,$ORIGIN"]
+           "-L", str(LIB_DIR), "-lespn_gpu", "-lespn_store", "-Wl,-rpath,$ORIGIN"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("g++ failed building libespn_host.so")
     return HOST_LIB
+
+
+STORE_SRC = CSRC / "host" / "espn_store.cpp"
+STORE_LIB = LIB_DIR / "libespn_store.so"
+
+
+def build_store_lib(force: bool = False) -> Path:
+    """libespn_store.so: the on-disk .espn store (include/espn_store.h), pure
+    host C++ -- builds and runs without a GPU."""
+    deps = [STORE_SRC, ROOT / "include" / "espn_store.h", ROOT / "include" / "espn_gpu.h"]
+    if not force and STORE_LIB.exists() and all(p.stat().st_mtime <= STORE_LIB.stat().st_mtime for p in deps):
+        return STORE_LIB
+    LIB_DIR.mkdir(exist_ok=True)
+    cmd = [CXX, *CXX_FLAGS, "-shared", "-fvisibility=hidden", "-I", str(ROOT / "include"), "-o", str(STORE_LIB),
+           str(STORE_SRC)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building libespn_store.so")
+    return STORE_LIB
 
 
 def check_reference_headers() -> bool:
@@ -102,4 +123,5 @@ def check_reference_headers() -> bool:
 if __name__ == "__main__":
     build_lib(verbose="-v" in sys.argv, force="-f" in sys.argv)
     build_host(force="-f" in sys.argv)
+    build_store_lib(force="-f" in sys.argv)
     print(LIB)

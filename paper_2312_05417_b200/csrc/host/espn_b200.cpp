@@ -55,8 +55,9 @@ double percentile(std::vector<double> v, double p) {
 
 }  // namespace
 
-void throw_status(int status) {
-  const std::string msg = espn_last_error();
+void throw_status(int status) { throw_status(status, espn_last_error()); }
+
+void throw_status(int status, const std::string& msg) {
   switch (status) {
     case ESPN_E_INVALID_INPUT: throw InvalidInputError(msg);
     case ESPN_E_INVALID_STATE: throw InvalidStateError(msg);
@@ -108,6 +109,34 @@ Store Store::from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtyp
     }
   }
   return Store(rp, codes, d, dtype, layout, device);
+}
+
+Store Store::open_store(const std::string& base, Dtype dtype, int device) {
+  espn_store_header h{};
+  auto check = [](int st) {
+    if (st != ESPN_OK) throw_status(st, espn_store_last_error());
+  };
+  check(espn_store_load_manifest(base.c_str(), &h, nullptr));
+  std::vector<espn_manifest_record> recs(h.count);
+  check(espn_store_load_manifest(base.c_str(), &h, recs.data()));
+  std::uint64_t tokens = 0;
+  for (const auto& r : recs) tokens += r.token_count;
+  std::vector<std::uint64_t> rp(h.count + 1);
+  std::vector<std::uint16_t> codes(std::max<std::uint64_t>(tokens * h.d, 1));
+  check(espn_store_read_table(base.c_str(), static_cast<std::uint32_t>(dtype), rp.data(), codes.data(), nullptr));
+  codes.resize(tokens * h.d);
+  return Store(rp, codes, h.d, dtype, RecordLayout{h.d_cls, h.value_width, h.alignment}, device);
+}
+
+void build_store(const std::string& base, std::span<const std::uint64_t> row_ptr, std::span<const float> rows,
+                 std::uint32_t d, std::span<const float> cls, RecordLayout layout) {
+  if (row_ptr.empty()) throw InvalidInputError("row_ptr must hold n_docs + 1 offsets");
+  const std::uint64_t n = row_ptr.size() - 1;
+  if (rows.size() != row_ptr.back() * d) throw InvalidInputError("rows size != row_ptr[n] * d");
+  if (!cls.empty() && cls.size() != n * layout.d_cls) throw InvalidInputError("cls size != n_docs * d_cls");
+  const int st = espn_store_build(base.c_str(), n, d, layout.d_cls, layout.value_width, layout.alignment,
+                                  row_ptr.data(), rows.data(), cls.empty() ? nullptr : cls.data());
+  if (st != ESPN_OK) throw_status(st, espn_store_last_error());
 }
 
 Store::~Store() {

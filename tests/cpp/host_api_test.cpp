@@ -152,6 +152,32 @@ int main() {
       CHECK(got.values == docs[req[i]].values, "fetch values of doc %u", req[i]);
     }
   }
+  // ---- build_store -> open_store: same rows, same rankings (store.hpp:48-54, 111-112) ----
+  {
+    std::vector<float> rows;
+    for (const auto& m : docs) rows.insert(rows.end(), m.values.begin(), m.values.end());
+    const std::string base = "/tmp/espn_host_api_test_store";
+    espn::gpu::build_store(base, rp, rows, d);
+    espn::gpu::Store disk = espn::gpu::Store::open_store(base);
+    CHECK(disk.n_docs() == n_docs && disk.d() == d, "open_store dims");
+    CHECK(disk.record_bytes(10) == (128 + 10 * d) * 2, "record layout from the manifest");
+    std::vector<espn::DocId> req = {0, 77, 3999};
+    espn::FetchResult fa = disk.fetch_batch(req), fb = store.fetch_batch(req);
+    for (std::size_t i = 0; i < req.size(); ++i) CHECK(fa.docs[i].bow.values == fb.docs[i].bow.values, "store doc %u", req[i]);
+    espn::PipelineConfig cfg;
+    cfg.rerank_count = K;
+    espn::BatchResult ra = espn::gpu::rerank_batch(qs, cl, disk, cfg), rb = espn::gpu::rerank_batch(qs, cl, store, cfg);
+    for (std::uint32_t b = 0; b < B; ++b) {
+      CHECK(ra.rankings[b].entries.size() == rb.rankings[b].entries.size(), "open_store ranking size");
+      for (std::size_t j = 0; j < ra.rankings[b].entries.size() && j < rb.rankings[b].entries.size(); ++j)
+        CHECK(ra.rankings[b].entries[j].doc_id == rb.rankings[b].entries[j].doc_id &&
+                  ra.rankings[b].entries[j].score == rb.rankings[b].entries[j].score,
+              "open_store ranking q%u pos %zu", b, j);
+    }
+    bool thrown = false;
+    try { espn::gpu::Store::open_store("/tmp/espn_no_such_store"); } catch (const espn::Error&) { thrown = true; }
+    CHECK(thrown, "open_store of a missing store must throw");
+  }
   // ---- error mapping (error.hpp:8-42) ----
   {
     espn::PipelineConfig cfg;

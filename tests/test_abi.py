@@ -80,3 +80,35 @@ def test_product_does_not_import_oracle():
         if p.is_file():
             assert "espn_oracle" not in p.read_text(), p
     assert "espn_oracle" not in (ROOT / "paper_2312_05417_b200" / "build.py").read_text()
+
+
+def test_store_library_exports_and_layouts(tmp_path):
+    """include/espn_store.h: libespn_store.so exports exactly the declared
+    symbols and the ctypes mirror matches the header's struct layouts."""
+    from paper_2312_05417_b200 import _lib as L
+    hdr = ROOT / "include" / "espn_store.h"
+    syms = set(re.findall(r"ESPN_API\s+[\w\s\*]+?\b(espn_\w+)\s*\(", hdr.read_text()))
+    assert syms == set(L.STORE_SIGNATURES)
+    lib = L.store_lib()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(L.STORE_LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert set(re.findall(r"\bT (espn_\w+)", out)) == syms
+    for s in syms:
+        assert hasattr(lib, s)
+    structs = {"espn_store_header": L.StoreHeader, "espn_manifest_record": L.ManifestRecord}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{hdr}"', "int main(void){"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0;}")
+    (tmp_path / "p.c").write_text("\n".join(lines))
+    subprocess.run(["gcc", "-std=c99", "-o", str(tmp_path / "p"), str(tmp_path / "p.c")], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(tmp_path / "p")], capture_output=True, text=True,
+                                                         check=True).stdout.split("\n") if l)
+    for cname, py in structs.items():
+        assert int(got[cname]) == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, f"{cname}.{f}"
+    from paper_2312_05417_b200 import api
+    assert C.sizeof(L.ManifestRecord) == api._RECORD_DT.itemsize == 16
