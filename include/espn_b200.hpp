@@ -21,7 +21,11 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <filesystem>
+#include <istream>
+#include <map>
 #include <memory>
+#include <set>
 #include <span>
 #include <string>
 #include <utility>
@@ -152,6 +156,10 @@ struct FetchResult {
   double wall_time = 0.0;
 };
 
+// types.hpp:57-62
+using Qrels = std::map<QueryId, std::set<DocId>>;
+using ResultsByQuery = std::map<QueryId, RankedList>;
+
 }  // namespace espn
 #endif
 
@@ -247,5 +255,17 @@ std::pair<RankedList, QueryStats> rerank_candidates(const QueryEmbedding& query,
 // Batched form (run_batch restricted to stages 3-6).
 BatchResult rerank_batch(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
                          const Store& store, const PipelineConfig& config);
+
+// Quality harness (metrics.hpp:10-20), to
+// check that re-ranking on the GPU preserves retrieval quality.  Same
+// definitions as the reference's espn::mrr_at_k / recall_at_k / load_qrels:
+// averages run over the qrels queries in id order, a query without results
+// (or without relevant docs) contributes 0, k < 1 -> InvalidInputError.
+double mrr_at_k(const ResultsByQuery& results, const Qrels& qrels, int k);
+double recall_at_k(const ResultsByQuery& results, const Qrels& qrels, int k);
+// TREC qrels: `query_id 0 doc_id relevance` per line, relevance > 0 marks a
+// relevant doc; blank lines skipped; anything else -> FormatError.
+Qrels load_qrels(std::istream& in);
+Qrels load_qrels(const std::filesystem::path& path);
 
 }  // namespace espn::gpu

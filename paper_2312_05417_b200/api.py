@@ -25,7 +25,8 @@ import ctypes as C
 import math
 import time
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence, Tuple
+from pathlib import Path
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -621,3 +622,69 @@ def rerank_candidates(query: QueryEmbedding, candidates: CandidateList, store: G
     the missing "candidates in -> ranked out" seam."""
     r = rerank_batch([query], [candidates], store, config, kernel=kernel)
     return r.rankings[0], r.stats[0]
+
+
+# ---- quality harness (metrics.hpp:10-20; SPEC.md:71-88; SURVEY.md §8 f4) -----------
+def _top_ids(ranked, k: int):
+    if isinstance(ranked, RankedList):
+        return [e.doc_id for e in ranked.entries[:k]]
+    return [int(x) for x in list(ranked)[:k]]  # a plain id sequence (e.g. a row of rerank_arrays ids)
+
+
+def mrr_at_k(results: Dict[int, object], qrels: Dict[int, set], k: int) -> float:
+    """Mean over the qrels queries (id order) of 1/rank of the first relevant
+    doc within the top k; a query without results counts 0 (metrics.hpp:10-12)."""
+    if k < 1:
+        raise InvalidInputError("k must be >= 1 (SPEC.md:74)")
+    if not qrels:
+        return 0.0
+    s = 0.0
+    for qid in sorted(qrels):
+        rel = qrels[qid]
+        for r, d in enumerate(_top_ids(results[qid], k) if qid in results else []):
+            if d in rel:
+                s += 1.0 / (r + 1)
+                break
+    return s / len(qrels)
+
+
+def recall_at_k(results: Dict[int, object], qrels: Dict[int, set], k: int) -> float:
+    """Mean over the qrels queries of |relevant in top k| / |relevant| (metrics.hpp:14-15)."""
+    if k < 1:
+        raise InvalidInputError("k must be >= 1 (SPEC.md:82)")
+    if not qrels:
+        return 0.0
+    s = 0.0
+    for qid in sorted(qrels):
+        rel = qrels[qid]
+        if qid in results and rel:
+            s += sum(1 for d in _top_ids(results[qid], k) if d in rel) / len(rel)
+    return s / len(qrels)
+
+
+def load_qrels(src) -> Dict[int, set]:
+    """TREC qrels (metrics.hpp:17-20): `query_id 0 doc_id relevance` per line,
+    relevance > 0 marks a relevant doc, blank lines skipped, else FormatError.
+    `src` is a path or an iterable of lines."""
+    if isinstance(src, (str, Path)):
+        try:
+            with open(src) as f:
+                return load_qrels(f.read().splitlines())
+        except OSError as e:
+            raise IoError(f"cannot open qrels file {src}: {e}") from None
+    q: Dict[int, set] = {}
+    for n, line in enumerate(src, 1):
+        f = line.split()
+        if not f:
+            continue
+        try:
+            if len(f) != 4:
+                raise ValueError
+            qid, _, did, rel = (int(x) for x in f)
+            if not (0 <= qid <= 0xFFFFFFFF and 0 <= did <= 0xFFFFFFFF):
+                raise ValueError
+        except ValueError:
+            raise FormatError(f"qrels line {n}: expected `query_id 0 doc_id relevance`") from None
+        if rel > 0:
+            q.setdefault(qid, set()).add(did)
+    return q

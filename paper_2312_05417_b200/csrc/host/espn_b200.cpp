@@ -7,6 +7,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 
 namespace espn::gpu {
 namespace {
@@ -319,6 +321,65 @@ std::pair<RankedList, QueryStats> rerank_candidates(const QueryEmbedding& query,
   BatchResult r = rerank_batch(std::span<const QueryEmbedding>(&query, 1),
                                std::span<const CandidateList>(&candidates, 1), store, config);
   return {std::move(r.rankings[0]), r.stats[0]};
+}
+
+// ---------------------------------------------------------------- quality harness (metrics.hpp:10-20)
+double mrr_at_k(const ResultsByQuery& results, const Qrels& qrels, int k) {
+  if (k < 1) throw InvalidInputError("k must be >= 1 (SPEC.md:74)");
+  if (qrels.empty()) return 0.0;
+  double sum = 0.0;
+  for (const auto& [qid, rel] : qrels) {
+    auto it = results.find(qid);
+    if (it == results.end()) continue;
+    const auto& e = it->second.entries;
+    const std::size_t n = std::min<std::size_t>(e.size(), static_cast<std::size_t>(k));
+    for (std::size_t r = 0; r < n; ++r)
+      if (rel.count(e[r].doc_id)) {
+        sum += 1.0 / static_cast<double>(r + 1);
+        break;
+      }
+  }
+  return sum / static_cast<double>(qrels.size());
+}
+
+double recall_at_k(const ResultsByQuery& results, const Qrels& qrels, int k) {
+  if (k < 1) throw InvalidInputError("k must be >= 1 (SPEC.md:82)");
+  if (qrels.empty()) return 0.0;
+  double sum = 0.0;
+  for (const auto& [qid, rel] : qrels) {
+    auto it = results.find(qid);
+    if (it == results.end() || rel.empty()) continue;
+    const auto& e = it->second.entries;
+    const std::size_t n = std::min<std::size_t>(e.size(), static_cast<std::size_t>(k));
+    std::size_t hit = 0;
+    for (std::size_t r = 0; r < n; ++r) hit += rel.count(e[r].doc_id);
+    sum += static_cast<double>(hit) / static_cast<double>(rel.size());
+  }
+  return sum / static_cast<double>(qrels.size());
+}
+
+Qrels load_qrels(std::istream& in) {
+  Qrels q;
+  std::string line;
+  std::size_t lineno = 0;
+  while (std::getline(in, line)) {
+    ++lineno;
+    if (line.find_first_not_of(" \t\r") == std::string::npos) continue;
+    std::istringstream ls(line);
+    long long qid, iter, did, relv;
+    std::string extra;
+    if (!(ls >> qid >> iter >> did >> relv) || (ls >> extra) || qid < 0 || did < 0 || qid > 0xFFFFFFFFLL ||
+        did > 0xFFFFFFFFLL)
+      throw FormatError("qrels line " + std::to_string(lineno) + ": expected `query_id 0 doc_id relevance`");
+    if (relv > 0) q[static_cast<QueryId>(qid)].insert(static_cast<DocId>(did));
+  }
+  return q;
+}
+
+Qrels load_qrels(const std::filesystem::path& path) {
+  std::ifstream f(path);
+  if (!f) throw IoError("cannot open qrels file " + path.string());
+  return load_qrels(f);
 }
 
 }  // namespace espn::gpu
