@@ -224,6 +224,7 @@ def run_tiered(args, cfg):
             "critical_path_bytes_per_batch": sum(f["critical_bytes"] for f in fs),
             "prefetched_bytes_per_batch": sum(f["prefetch_bytes"] for f in fs),
             "resident_rows_per_batch": sum(f["resident"] for f in fs), "needed_rows_per_batch": need}
+    model = tiered_bandwidth_model(rr, dbs, pcfg, out, main, side, res_mode, B, n_batches)
     on = res_mode["on"]
     res = {"metric": BASE_METRIC, "value": on["queries_per_s"], "unit": "queries/s", "n_gpus": 1,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": on["ms_per_step"], "higher_is_better": True,
@@ -233,8 +234,63 @@ def run_tiered(args, cfg):
                       "rerank_R": R, "final_k": k, "partial_rerank": True, "resident_frac": cfg["resident_frac"],
                       "hbm_tier_gb": store.hbm_bytes / 1e9, "host_tier_gb": store.host_bytes / 1e9,
                       "launch": "eager ASYNC calls; prefetch of batch n+1 on a side stream"},
-           "prefetch": res_mode, "gpu_launches": args.steps * 5}
+           "prefetch": res_mode, "bandwidth_model": model, "gpu_launches": args.steps * 5}
     print(json.dumps(res), flush=True)
+
+
+def tiered_bandwidth_model(rr, dbs, pcfg, out, main, side, res_mode, B, n_batches):
+    """§8 f3: Eq. 4 re-parameterised for the pinned-host tier.  Measures, in
+    isolation, the PCIe DMA peak, the prefetcher's own transfer rate and the
+    scoring time of an already-staged batch, then predicts the prefetch on /
+    off step times (paper_2312_05417_b200/bandwidth.py) next to the measured ones."""
+    import torch
+    from paper_2312_05417_b200 import bandwidth as bw
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    dbuf = torch.empty(n, dtype=torch.uint8, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dbuf.copy_(h, non_blocking=True)
+    ts = []
+    for _ in range(5):
+        e0.record()
+        dbuf.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    dma_bps = n / min(ts)
+    del h, dbuf
+    pf_s, sc_s = [], []
+    for i in range(2 * n_batches):
+        db = dbs[i % n_batches]
+        torch.cuda.synchronize()
+        e0.record(side)
+        rr.prefetch(db["q"], db["ids"], db["cls"], db["off"], pcfg, stream=side.cuda_stream)
+        e1.record(side)
+        torch.cuda.synchronize()
+        pf_s.append(e0.elapsed_time(e1) / 1e3)
+        e0.record(main)
+        rr.rerank_arrays(db["q"], db["ids"], db["cls"], db["off"], pcfg, device_io=True, out=out,
+                         stream=main.cuda_stream, sync=False, prefetched=True)
+        e1.record(main)
+        torch.cuda.synchronize()
+        rr.sync(main.cuda_stream)
+        sc_s.append(e0.elapsed_time(e1) / 1e3)
+    pf, sc = float(np.median(pf_s[n_batches:])), float(np.median(sc_s[n_batches:]))
+    miss = res_mode["on"]["prefetched_bytes_per_batch"]
+    tier = bw.TierProfile("pinned-host over PCIe (prefetcher rate)", miss / pf, 1)
+    p_on = bw.predict_tiered_step(sc, miss, tier, prefetch=True)
+    p_off = bw.predict_tiered_step(sc, miss, tier, prefetch=False)
+    bpq = miss / B
+    return {"pcie_dma_gbs": dma_bps / 1e9, "prefetch_gbs": miss / pf / 1e9, "prefetch_ms": pf * 1e3,
+            "score_ms": sc * 1e3, "miss_bytes_per_query": bpq,
+            "predicted": {"on_ms_per_step": p_on["step_s"] * 1e3, "off_ms_per_step": p_off["step_s"] * 1e3,
+                          "on_bound": p_on["bound"]},
+            "measured": {"on_ms_per_step": res_mode["on"]["ms_per_step"],
+                         "off_ms_per_step": res_mode["off"]["ms_per_step"]},
+            "batch_threshold": {"at_prefetch_rate": bw.batch_threshold(tier, sc, bpq),
+                                "at_dma_peak": bw.batch_threshold(bw.TierProfile("pcie", dma_bps, 1), sc, bpq),
+                                "note": "Eq. 4 with the budget = scoring time of this batch: the largest batch whose "
+                                        "host-tier misses the tier delivers while one batch scores"}}
 
 
 # ------------------------------------------------------------------ our arm
