@@ -217,6 +217,24 @@ ESPN_API int espn_gpu_rerank(espn_gpu_table* table, espn_gpu_workspace* ws,
 ESPN_API int espn_gpu_prefetch(espn_gpu_table* table, espn_gpu_workspace* ws, const espn_rerank_args* next,
                       void* side_stream);
 
+/* Prefetch hints (run_query stages (1)-(2), SPEC.md:276,
+ * pipeline.hpp:56-64): stages the host-tier rows of an APPROXIMATE id list --
+ * the IVF cursor's snapshot after delta clusters (ivf.hpp:67-68) -- into the
+ * workspace's spare staging buffer on `side_stream`, while the ANN search
+ * finishes.  hint_ids: device array (CSR over n_queries by hint_offsets, host
+ * array unless flags has ESPN_RERANK_DEVICE_OFFSETS); ids of other shards or
+ * unknown ids are ignored (hints are advisory).  A doc hinted by several
+ * queries is staged once.  The next espn_gpu_rerank of this workspace carrying
+ * ESPN_RERANK_PREFETCHED consumes the staging with ANY candidate lists: needed
+ * host-tier rows found staged are hits (espn_fetch_stats.prefetched), the
+ * others are copied on the critical path (missed).  Results are identical to
+ * an unprefetched call.  The hinted rows use at most half of the staging
+ * buffer; the rest is kept for the critical-path misses.  A no-op for
+ * untiered tables. */
+ESPN_API int espn_gpu_prefetch_hints(espn_gpu_table* table, espn_gpu_workspace* ws, uint32_t n_queries,
+                                     const uint32_t* hint_ids, const uint64_t* hint_offsets, uint32_t flags,
+                                     void* side_stream);
+
 /* Completes an ASYNC batch on its stream and reports device-side errors
  * (unknown doc id -> DATA_INTEGRITY, non-finite query/cls -> INVALID_INPUT,
  * duplicate candidate -> INVALID_INPUT). */

@@ -505,6 +505,21 @@ class Reranker:
             self.last_fetch_stats = [{f: int(getattr(x, f)) for f, _ in L.FetchStats._fields_} for x in fs]
         return out
 
+    def prefetch_hints(self, hint_ids, hint_offsets, stream=None, device_offsets: bool = False):
+        """espn_gpu_prefetch_hints: stage the host-tier rows of an approximate
+        id list (the IVF snapshot after delta clusters, CSR over queries) on
+        `stream`; the next rerank_arrays(..., prefetched=True) consumes it with
+        its final candidates.  hint_ids: device tensor (uint32/int32)."""
+        if device_offsets:
+            offs_p, B = _ptr(hint_offsets), int(hint_offsets.numel()) - 1
+            flags = L.ESPN_RERANK_DEVICE_OFFSETS
+        else:
+            offs = np.ascontiguousarray(np.asarray(hint_offsets, dtype=np.uint64))
+            offs_p, B, flags = offs.ctypes.data, offs.shape[0] - 1, 0
+            self._keep_hints = offs
+        _check(L.lib().espn_gpu_prefetch_hints(self.store.handle, self._h, B, _ptr(hint_ids), offs_p, flags,
+                                               C.c_void_p(stream) if stream else None))
+
     def prefetch(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig, stream=None,
                  needed_counts=None, device_offsets: bool = False):
         """espn_gpu_prefetch: stage the NEXT batch's host-tier rows on `stream`

@@ -102,6 +102,28 @@ struct StageParams {
   unsigned long long* cursor;  // bytes used in stage (zeroed before the launch)
   unsigned long long* qstats;  // B x 6 (espn_fetch_stats layout)
   uint32_t* err;
+  const uint64_t* hint_map;    // optional (consumer of espn_gpu_prefetch_hints): per local doc,
+                               // epoch << 32 | staged offset / 16
+  uint32_t hint_epoch;
+};
+
+// Hint staging (espn_gpu_prefetch_hints): CTA per query, warp per hinted doc.
+struct HintParams {
+  const uint64_t* row_ptr;
+  const uint64_t* doc_loc;
+  uint64_t n_docs;
+  uint32_t shard_count, shard_index;
+  const uint32_t* hint_ids;
+  const uint64_t* hint_off;    // n_queries + 1
+  uint64_t max_hints;          // bound check on the (possibly device) offsets
+  uint32_t row_bytes;
+  uint64_t* hint_map;          // per local doc: epoch << 32 | staged offset / 16 (0xffffffff = claimed)
+  uint32_t epoch;
+  uint8_t* stage;
+  uint64_t stage_cap;          // bytes the hints may use
+  unsigned long long* cursor;
+  unsigned long long* qstats;  // B x 6: [4] += bytes this query's warps staged
+  uint32_t* err;
 };
 
 // Device-side batch planning (plan_kernel): per-query needed counts, work

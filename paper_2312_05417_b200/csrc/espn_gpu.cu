@@ -240,7 +240,10 @@ struct espn_gpu_workspace {
     cudaEvent_t done = nullptr;            // staging finished
     cudaEvent_t free_ev = nullptr;         // last MaxSim reading this slot finished
     bool used = false;
+    uint32_t hint_epoch = 0;               // != 0: filled by espn_gpu_prefetch_hints (doc-keyed)
   } stage[2];
+  uint64_t* hint_map = nullptr;            // per local doc: epoch << 32 | staged offset / 16 (lazy)
+  uint32_t hint_epoch = 0;
   uint64_t staging_bytes = 0;
   int pf_q[2] = {-1, -1};  // FIFO of prefetched slots awaiting their PREFETCHED batch
   int pf_count = 0;
@@ -371,9 +374,14 @@ int launch_stage(espn_gpu_table* t, espn_gpu_workspace* w, int slot, const uint6
                  const uint32_t* dev_need, const uint32_t* dev_ids, uint32_t B, uint32_t R, cudaStream_t s,
                  bool prefetch) {
   auto& st = w->stage[slot];
-  if (st.used) ESPN_CUDA_TRY(cudaStreamWaitEvent(s, st.free_ev, 0));  // previous reader done
-  ESPN_CUDA_TRY(cudaMemsetAsync(st.cursor, 0, sizeof(unsigned long long), s));
-  ESPN_CUDA_TRY(cudaMemsetAsync(st.qstats, 0, (size_t)B * 6 * sizeof(unsigned long long), s));
+  // consumer of espn_gpu_prefetch_hints: keep the hinted rows, the cursor and
+  // the prefetch byte counts, append the misses
+  const bool hinted = !prefetch && st.hint_epoch != 0;
+  if (!hinted) {
+    if (st.used) ESPN_CUDA_TRY(cudaStreamWaitEvent(s, st.free_ev, 0));  // previous reader done
+    ESPN_CUDA_TRY(cudaMemsetAsync(st.cursor, 0, sizeof(unsigned long long), s));
+    ESPN_CUDA_TRY(cudaMemsetAsync(st.qstats, 0, (size_t)B * 6 * sizeof(unsigned long long), s));
+  }
   StageParams sp{};
   sp.row_ptr = t->row_ptr;
   sp.doc_loc = t->doc_loc;
@@ -394,6 +402,8 @@ int launch_stage(espn_gpu_table* t, espn_gpu_workspace* w, int slot, const uint6
   sp.cursor = st.cursor;
   sp.qstats = st.qstats;
   sp.err = w->err;
+  sp.hint_map = hinted ? w->hint_map : nullptr;
+  sp.hint_epoch = hinted ? st.hint_epoch : 0u;
   stage_kernel<<<B, 256, 0, s>>>(sp);
   ESPN_CUDA_TRY(cudaGetLastError());
   ESPN_CUDA_TRY(cudaEventRecord(st.done, s));
@@ -670,9 +680,11 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
     if (st.free_ev) cudaEventSynchronize(st.free_ev);
     cudaFree(st.buf); cudaFree(st.cand_src); cudaFree(st.cursor); cudaFree(st.qstats); cudaFree(st.off);
     cudaFree(st.need); cudaFreeHost(st.off_h); cudaFreeHost(st.need_h);
+    st.hint_epoch = 0;
     if (st.done) cudaEventDestroy(st.done);
     if (st.free_ev) cudaEventDestroy(st.free_ev);
   }
+  cudaFree(w->hint_map);
   cudaFreeHost(w->h_qstats); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
   cudaFree(w->out_counts); cudaFree(w->err);
   for (auto& sl : w->slots) {
@@ -859,6 +871,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
 
   // ---- tiered table: host-tier rows staged into HBM (prefetched or now) ----
   int slot = -1;
+  bool hint_consumed = false;
   if (t->tiered) {
     if (a->flags & ESPN_RERANK_PREFETCHED) {
       if (w->pf_count == 0) return fail(ESPN_E_INVALID_STATE, "PREFETCHED batch without a pending espn_gpu_prefetch");
@@ -866,6 +879,12 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
       w->pf_q[0] = w->pf_q[1];
       --w->pf_count;
       ESPN_CUDA_TRY(cudaStreamWaitEvent(s, w->stage[slot].done, 0));
+      if (w->stage[slot].hint_epoch) {  // doc-keyed hints: resolve this batch's needed rows now
+        hint_consumed = true;
+        const int ss = launch_stage(t, w, slot, cand_off, needed_in, ids, B, a->rerank_count, s, false);
+        w->stage[slot].hint_epoch = 0;
+        if (ss) return ss;
+      }
     } else {
       if (w->pf_count == 2) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
       slot = w->next_slot;
@@ -1013,7 +1032,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
   w->counters.batches += 1;
   w->counters.queries += B;
-  w->counters.kernel_launches += 3 + (t->tiered && !(a->flags & ESPN_RERANK_PREFETCHED) ? 1 : 0);
+  w->counters.kernel_launches += 3 + (t->tiered && (!(a->flags & ESPN_RERANK_PREFETCHED) || hint_consumed) ? 1 : 0);
   if (a->flags & ESPN_RERANK_ASYNC) {
     w->async_pending = true;
     return ESPN_OK;
@@ -1074,10 +1093,75 @@ int espn_gpu_prefetch(espn_gpu_table* t, espn_gpu_workspace* w, const espn_reran
       need = st.need;
     }
   }
+  st.hint_epoch = 0;  // positional staging
   const int ss = launch_stage(t, w, slot, off, need, a->cand_ids, B, a->rerank_count, s, true);
   if (ss) return ss;
   w->pf_q[w->pf_count++] = slot;
   w->async_pending = true;  // staging errors surface at the next sync
+  return ESPN_OK;
+}
+
+int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B, const uint32_t* hint_ids,
+                            const uint64_t* hint_offsets, uint32_t flags, void* side_stream) {
+  if (!t || !w) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
+  if (!t->tiered) return ESPN_OK;  // everything is HBM-resident
+  if (B == 0) return ESPN_OK;
+  if (!hint_offsets) return fail(ESPN_E_INVALID_INPUT, "null hint offsets");
+  if (B > w->max_queries) return fail(ESPN_E_INVALID_INPUT, "n_queries exceeds workspace capacity");
+  if (w->pf_count == 2) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
+  DeviceGuard g(t->device);
+  cudaStream_t s = static_cast<cudaStream_t>(side_stream);
+  const int slot = w->next_slot;
+  auto& st = w->stage[slot];
+  const uint64_t* off = hint_offsets;
+  if (!(flags & ESPN_RERANK_DEVICE_OFFSETS)) {
+    if (hint_offsets[0] != 0) return fail(ESPN_E_INVALID_INPUT, "hint_offsets[0] must be 0");
+    for (uint32_t b = 0; b < B; ++b)
+      if (hint_offsets[b + 1] < hint_offsets[b]) return fail(ESPN_E_INVALID_INPUT, "hint_offsets must be non-decreasing");
+    if (hint_offsets[B] > w->max_candidates) return fail(ESPN_E_INVALID_INPUT, "hints exceed workspace capacity");
+    if (hint_offsets[B] && !hint_ids) return fail(ESPN_E_INVALID_INPUT, "null hint ids");
+    if (st.used) ESPN_CUDA_TRY(cudaEventSynchronize(st.done));  // pinned staging of this slot is free
+    std::memcpy(st.off_h, hint_offsets, (B + 1) * sizeof(uint64_t));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(st.off, st.off_h, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    off = st.off;
+  }
+  if (!w->hint_map) {
+    ESPN_CUDA_TRY(cudaMalloc(&w->hint_map, t->n_docs * sizeof(uint64_t)));
+    ESPN_CUDA_TRY(cudaMemsetAsync(w->hint_map, 0, t->n_docs * sizeof(uint64_t), s));
+  }
+  if (++w->hint_epoch == 0) {  // 2^32 hint batches: reset the map so no stale entry can match
+    ESPN_CUDA_TRY(cudaMemsetAsync(w->hint_map, 0, t->n_docs * sizeof(uint64_t), s));
+    w->hint_epoch = 1;
+  }
+  w->next_slot ^= 1;
+  if (st.used) ESPN_CUDA_TRY(cudaStreamWaitEvent(s, st.free_ev, 0));  // previous reader done
+  ESPN_CUDA_TRY(cudaMemsetAsync(st.cursor, 0, sizeof(unsigned long long), s));
+  ESPN_CUDA_TRY(cudaMemsetAsync(st.qstats, 0, (size_t)B * 6 * sizeof(unsigned long long), s));
+  HintParams hp{};
+  hp.row_ptr = t->row_ptr;
+  hp.doc_loc = t->doc_loc;
+  hp.n_docs = t->n_docs;
+  hp.shard_count = t->shard_count;
+  hp.shard_index = t->shard_index;
+  hp.hint_ids = hint_ids;
+  hp.hint_off = off;
+  hp.max_hints = w->max_candidates;
+  hp.row_bytes = t->d * 2;
+  hp.hint_map = w->hint_map;
+  hp.epoch = w->hint_epoch;
+  hp.stage = st.buf;
+  hp.stage_cap = w->staging_bytes / 2;
+  hp.cursor = st.cursor;
+  hp.qstats = st.qstats;
+  hp.err = w->err;
+  hint_stage_kernel<<<B, 256, 0, s>>>(hp);
+  ESPN_CUDA_TRY(cudaGetLastError());
+  ESPN_CUDA_TRY(cudaEventRecord(st.done, s));
+  st.hint_epoch = w->hint_epoch;
+  w->pf_q[w->pf_count++] = slot;
+  w->async_pending = true;
+  w->counters.kernel_launches += 1;
   return ESPN_OK;
 }
 

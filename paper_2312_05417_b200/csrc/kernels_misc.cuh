@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const StageParams s) {
   const uint64_t n = c1 - c0;
   const uint64_t cap = s.needed_in ? (uint64_t)s.needed_in[b] : (uint64_t)s.rerank_count;
   const uint64_t need = n < cap ? n : cap;
-  unsigned long long resident = 0, staged = 0, bytes_moved = 0;
+  unsigned long long resident = 0, staged = 0, bytes_moved = 0, hits = 0;
   for (uint64_t j = wid; j < need; j += nw) {
     const uint64_t loc = shard_local(s.cand_ids[c0 + j], s.shard_count, s.shard_index, s.n_docs);
     if (loc == ~0ull) {  // reported as DATA_INTEGRITY by the MaxSim kernel
@@ -618,6 +618,14 @@ __global__ void __launch_bounds__(256) stage_kernel(const StageParams s) {
       if (lane == 0) s.cand_src[c0 + j] = a;
       ++resident;
       continue;
+    }
+    if (s.hint_map) {  // staged ahead by espn_gpu_prefetch_hints?
+      const uint64_t e = s.hint_map[loc];
+      if ((uint32_t)(e >> 32) == s.hint_epoch && (uint32_t)e != 0xffffffffu) {
+        if (lane == 0) s.cand_src[c0 + j] = reinterpret_cast<uint64_t>(s.stage) + ((e & 0xffffffffull) << 4);
+        ++hits;
+        continue;
+      }
     }
     const uint64_t bytes = (s.row_ptr[loc + 1] - s.row_ptr[loc]) * s.row_bytes;
     unsigned long long off = 0;
@@ -646,7 +654,62 @@ __global__ void __launch_bounds__(256) stage_kernel(const StageParams s) {
     atomicAdd(&q[1], resident);
     atomicAdd(&q[s.prefetch ? 2 : 3], staged);
     atomicAdd(&q[s.prefetch ? 4 : 5], bytes_moved);
+    if (hits) atomicAdd(&q[2], hits);
   }
+}
+
+// Hint staging (espn_gpu_prefetch_hints): the host-tier rows of each query's
+// hinted docs -> staging buffer, one copy per doc per epoch (the first warp to
+// claim the doc's hint-map entry copies it; the others skip).  The consumer
+// (stage_kernel with hint_map) runs after this kernel on another stream,
+// ordered by an event, so plain stores publish the entries.
+__global__ void __launch_bounds__(256) hint_stage_kernel(const HintParams s) {
+  const uint32_t b = blockIdx.x;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint64_t h0 = s.hint_off[b], h1 = s.hint_off[b + 1];
+  if (h1 < h0 || h1 > s.max_hints) {
+    if (threadIdx.x == 0) atomicOr(s.err, ERR_BAD_OFFSETS);
+    return;
+  }
+  unsigned long long bytes_moved = 0;
+  for (uint64_t j = h0 + wid; j < h1; j += nw) {
+    const uint64_t loc = shard_local(s.hint_ids[j], s.shard_count, s.shard_index, s.n_docs);
+    if (loc == ~0ull) continue;  // another shard's doc, or unknown: hints are advisory
+    const uint64_t a = s.doc_loc[loc];
+    if (!(a & 1ull)) continue;   // HBM-resident
+    const uint64_t bytes = (s.row_ptr[loc + 1] - s.row_ptr[loc]) * s.row_bytes;
+    unsigned long long off = ~0ull;
+    if (lane == 0) {
+      const uint64_t e = s.hint_map[loc];
+      if ((uint32_t)(e >> 32) != s.epoch &&
+          atomicCAS(reinterpret_cast<unsigned long long*>(&s.hint_map[loc]), (unsigned long long)e,
+                    ((unsigned long long)s.epoch << 32) | 0xffffffffull) == (unsigned long long)e) {
+        // bounded bump allocation: a failed add is undone, so while any failure
+        // is pending every add fails and successful regions never overlap
+        const unsigned long long cur = atomicAdd(s.cursor, (unsigned long long)bytes);
+        if (cur + bytes <= s.stage_cap) {
+          off = cur;
+        } else {
+          atomicAdd(s.cursor, (unsigned long long)(0ull - bytes));
+          s.hint_map[loc] = 0;  // budget spent: the consumer copies it on the critical path
+        }
+      }
+    }
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (off == ~0ull) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(a & ~1ull);
+    uint4* dst = reinterpret_cast<uint4*>(s.stage + off);
+    const uint64_t n16 = bytes / 16;
+    uint64_t v = lane;
+    for (; v + 96 < n16; v += 128) {  // 4 PCIe reads in flight per lane
+      const uint4 x0 = src[v], x1 = src[v + 32], x2 = src[v + 64], x3 = src[v + 96];
+      dst[v] = x0; dst[v + 32] = x1; dst[v + 64] = x2; dst[v + 96] = x3;
+    }
+    for (; v < n16; v += 32) dst[v] = src[v];
+    if (lane == 0) s.hint_map[loc] = ((uint64_t)s.epoch << 32) | (off >> 4);
+    bytes_moved += bytes;
+  }
+  if (lane == 0 && s.qstats && bytes_moved) atomicAdd(&s.qstats[(size_t)b * 6 + 4], bytes_moved);
 }
 
 // Plain row-major CSR rows -> HBM tile layout (table open).  Warp per doc.
