@@ -97,7 +97,7 @@ maxsim_simt_kernel(const MaxSimParams p) {
 // within the workspace); on error the plan is empty (n_units = 0) so no kernel
 // touches memory through a bad offset.
 // ============================================================================
-constexpr int kPlanThreads = 256;
+constexpr int kPlanThreads = 128;  // 128 x <=80 regs fits beside a resident MaxSim CTA (next batch plans early)
 __device__ __forceinline__ uint64_t plan_units(const PlanParams& q, uint32_t b, uint32_t* need_out, bool* bad) {
   const uint64_t a = q.cand_off[b], e = q.cand_off[b + 1];
   if (e < a) { *bad = true; return 0; }
