@@ -186,15 +186,20 @@ struct RecordLayout {
 // dtype).  Move-only; shareable read-only across threads.
 class Store {
  public:
+  // resident (optional, n_docs flags): docs with resident[i] == 0 live in a
+  // pinned-host tier and are staged into HBM per batch (prefetched through
+  // Reranker::prefetch_hints, or on the critical path).
   Store(std::span<const std::uint64_t> row_ptr, std::span<const std::uint16_t> rows, std::uint32_t d,
-        Dtype dtype = Dtype::f16, RecordLayout layout = {}, int device = 0);
+        Dtype dtype = Dtype::f16, RecordLayout layout = {}, int device = 0,
+        std::span<const std::uint8_t> resident = {});
   // docs[i].doc_id must equal i (dense ids, store.hpp:20)
   static Store from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtype = Dtype::f16,
                               RecordLayout layout = {}, int device = 0);
   // open_store (store.hpp:111-112) for the HBM tier: reads a .espn store
   // (include/espn_store.h, libespn_store.so) and uploads its rows; the
   // record layout comes from the manifest.
-  static Store open_store(const std::string& base, Dtype dtype = Dtype::f16, int device = 0);
+  static Store open_store(const std::string& base, Dtype dtype = Dtype::f16, int device = 0,
+                          std::span<const std::uint8_t> resident = {});
   ~Store();
   Store(Store&&) noexcept;
   Store& operator=(Store&&) noexcept;
@@ -233,8 +238,18 @@ class Reranker {
 
   // run_batch (pipeline.hpp:81-85) restricted to stages 3-6: one device pass
   // for the whole batch, per-query results identical to single-query calls.
+  // prefetched: the batch consumes the staging of the last prefetch_hints
+  // call (tiered stores); QueryStats then carry the device's fetch accounting.
   BatchResult rerank(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
-                     const PipelineConfig& config, Kernel kernel = Kernel::automatic);
+                     const PipelineConfig& config, Kernel kernel = Kernel::automatic, bool prefetched = false);
+
+  // run_query stages (1)-(2) (pipeline.hpp:56-64): stage the host-tier rows of
+  // the cursors' snapshots after delta clusters (SearchCursor::snapshot,
+  // ivf.hpp:67-68; the first top_k entries of each, 0 = all) on side_stream,
+  // while the search finishes.  The next rerank(..., prefetched = true)
+  // resolves its needed rows against them.  No-op for an all-HBM store.
+  void prefetch_hints(std::span<const CandidateList> snapshots, std::uint32_t top_k = 0,
+                      void* side_stream = nullptr);
 
   espn_counters counters() const;
 

@@ -221,8 +221,10 @@ ESPN_API int espn_gpu_prefetch(espn_gpu_table* table, espn_gpu_workspace* ws, co
  * pipeline.hpp:56-64): stages the host-tier rows of an APPROXIMATE id list --
  * the IVF cursor's snapshot after delta clusters (ivf.hpp:67-68) -- into the
  * workspace's spare staging buffer on `side_stream`, while the ANN search
- * finishes.  hint_ids: device array (CSR over n_queries by hint_offsets, host
- * array unless flags has ESPN_RERANK_DEVICE_OFFSETS); ids of other shards or
+ * finishes.  hint_ids: CSR over n_queries by hint_offsets; a device array
+ * when flags has ESPN_RERANK_DEVICE_IO, else a host array (copied through
+ * pinned staging); hint_offsets is a host array unless flags also has
+ * ESPN_RERANK_DEVICE_OFFSETS.  Ids of other shards or
  * unknown ids are ignored (hints are advisory).  A doc hinted by several
  * queries is staged once.  The next espn_gpu_rerank of this workspace carrying
  * ESPN_RERANK_PREFETCHED consumes the staging with ANY candidate lists: needed

@@ -509,14 +509,20 @@ class Reranker:
         """espn_gpu_prefetch_hints: stage the host-tier rows of an approximate
         id list (the IVF snapshot after delta clusters, CSR over queries) on
         `stream`; the next rerank_arrays(..., prefetched=True) consumes it with
-        its final candidates.  hint_ids: device tensor (uint32/int32)."""
+        its final candidates.  hint_ids: device tensor (uint32/int32) or host
+        numpy array."""
+        if isinstance(hint_ids, np.ndarray):  # host ids: copied by the library
+            hint_ids = np.ascontiguousarray(hint_ids, dtype=np.uint32)
+            flags = 0
+        else:
+            flags = L.ESPN_RERANK_DEVICE_IO
         if device_offsets:
             offs_p, B = _ptr(hint_offsets), int(hint_offsets.numel()) - 1
-            flags = L.ESPN_RERANK_DEVICE_OFFSETS
+            flags |= L.ESPN_RERANK_DEVICE_OFFSETS
         else:
             offs = np.ascontiguousarray(np.asarray(hint_offsets, dtype=np.uint64))
-            offs_p, B, flags = offs.ctypes.data, offs.shape[0] - 1, 0
-            self._keep_hints = offs
+            offs_p, B = offs.ctypes.data, offs.shape[0] - 1
+            self._keep_hints = (offs, hint_ids)
         _check(L.lib().espn_gpu_prefetch_hints(self.store.handle, self._h, B, _ptr(hint_ids), offs_p, flags,
                                                C.c_void_p(stream) if stream else None))
 

@@ -241,6 +241,8 @@ struct espn_gpu_workspace {
     cudaEvent_t free_ev = nullptr;         // last MaxSim reading this slot finished
     bool used = false;
     uint32_t hint_epoch = 0;               // != 0: filled by espn_gpu_prefetch_hints (doc-keyed)
+    uint32_t* hint_ids = nullptr;          // device copy of host hint ids (lazy, max_candidates)
+    uint32_t* hint_ids_h = nullptr;        // its pinned staging
   } stage[2];
   uint64_t* hint_map = nullptr;            // per local doc: epoch << 32 | staged offset / 16 (lazy)
   uint32_t hint_epoch = 0;
@@ -680,6 +682,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
     if (st.free_ev) cudaEventSynchronize(st.free_ev);
     cudaFree(st.buf); cudaFree(st.cand_src); cudaFree(st.cursor); cudaFree(st.qstats); cudaFree(st.off);
     cudaFree(st.need); cudaFreeHost(st.off_h); cudaFreeHost(st.need_h);
+    cudaFree(st.hint_ids); cudaFreeHost(st.hint_ids_h);
     st.hint_epoch = 0;
     if (st.done) cudaEventDestroy(st.done);
     if (st.free_ev) cudaEventDestroy(st.free_ev);
@@ -1115,6 +1118,9 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
   const int slot = w->next_slot;
   auto& st = w->stage[slot];
   const uint64_t* off = hint_offsets;
+  const bool dev_ids = (flags & ESPN_RERANK_DEVICE_IO) != 0;
+  if ((flags & ESPN_RERANK_DEVICE_OFFSETS) && !dev_ids)
+    return fail(ESPN_E_INVALID_INPUT, "DEVICE_OFFSETS hints need DEVICE_IO ids");
   if (!(flags & ESPN_RERANK_DEVICE_OFFSETS)) {
     if (hint_offsets[0] != 0) return fail(ESPN_E_INVALID_INPUT, "hint_offsets[0] must be 0");
     for (uint32_t b = 0; b < B; ++b)
@@ -1125,6 +1131,16 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
     std::memcpy(st.off_h, hint_offsets, (B + 1) * sizeof(uint64_t));
     ESPN_CUDA_TRY(cudaMemcpyAsync(st.off, st.off_h, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
     off = st.off;
+    if (!dev_ids && hint_offsets[B]) {  // host ids: through this slot's pinned staging
+      if (!st.hint_ids) {
+        ESPN_CUDA_TRY(cudaMalloc(&st.hint_ids, w->max_candidates * sizeof(uint32_t)));
+        ESPN_CUDA_TRY(cudaMallocHost(&st.hint_ids_h, w->max_candidates * sizeof(uint32_t)));
+      }
+      std::memcpy(st.hint_ids_h, hint_ids, hint_offsets[B] * sizeof(uint32_t));
+      ESPN_CUDA_TRY(cudaMemcpyAsync(st.hint_ids, st.hint_ids_h, hint_offsets[B] * sizeof(uint32_t),
+                                    cudaMemcpyHostToDevice, s));
+      hint_ids = st.hint_ids;
+    }
   }
   if (!w->hint_map) {
     ESPN_CUDA_TRY(cudaMalloc(&w->hint_map, t->n_docs * sizeof(uint64_t)));

@@ -73,7 +73,7 @@ void throw_status(int status, const std::string& msg) {
 
 // ---------------------------------------------------------------- Store
 Store::Store(std::span<const std::uint64_t> row_ptr, std::span<const std::uint16_t> rows, std::uint32_t d,
-             Dtype dtype, RecordLayout layout, int device)
+             Dtype dtype, RecordLayout layout, int device, std::span<const std::uint8_t> resident)
     : d_(d), dtype_(dtype), layout_(layout), device_(device), row_ptr_(row_ptr.begin(), row_ptr.end()) {
   if (row_ptr.size() < 2) throw InvalidInputError("empty table");
   espn_table_desc desc{};
@@ -86,6 +86,10 @@ Store::Store(std::span<const std::uint64_t> row_ptr, std::span<const std::uint16
   desc.row_ptr = row_ptr.data();
   desc.rows = rows.data();
   desc.device = device;
+  if (!resident.empty()) {
+    if (resident.size() != desc.n_docs) throw InvalidInputError("resident mask size != n_docs");
+    desc.resident = resident.data();
+  }
   if (rows.size() < row_ptr.back() * d) throw InvalidInputError("rows shorter than row_ptr[n_docs] * d");
   check(espn_gpu_table_open(&desc, &table_));
 }
@@ -113,7 +117,7 @@ Store Store::from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtyp
   return Store(rp, codes, d, dtype, layout, device);
 }
 
-Store Store::open_store(const std::string& base, Dtype dtype, int device) {
+Store Store::open_store(const std::string& base, Dtype dtype, int device, std::span<const std::uint8_t> resident) {
   espn_store_header h{};
   auto check = [](int st) {
     if (st != ESPN_OK) throw_status(st, espn_store_last_error());
@@ -127,7 +131,7 @@ Store Store::open_store(const std::string& base, Dtype dtype, int device) {
   std::vector<std::uint16_t> codes(std::max<std::uint64_t>(tokens * h.d, 1));
   check(espn_store_read_table(base.c_str(), static_cast<std::uint32_t>(dtype), rp.data(), codes.data(), nullptr));
   codes.resize(tokens * h.d);
-  return Store(rp, codes, h.d, dtype, RecordLayout{h.d_cls, h.value_width, h.alignment}, device);
+  return Store(rp, codes, h.d, dtype, RecordLayout{h.d_cls, h.value_width, h.alignment}, device, resident);
 }
 
 void build_store(const std::string& base, std::span<const std::uint64_t> row_ptr, std::span<const float> rows,
@@ -227,8 +231,22 @@ espn_counters Reranker::counters() const {
   return c;
 }
 
+void Reranker::prefetch_hints(std::span<const CandidateList> snapshots, std::uint32_t top_k, void* side_stream) {
+  const std::uint32_t B = static_cast<std::uint32_t>(snapshots.size());
+  if (B == 0) return;
+  std::vector<std::uint64_t> off(B + 1, 0);
+  for (std::uint32_t b = 0; b < B; ++b) {
+    const std::size_t n = snapshots[b].entries.size();
+    off[b + 1] = off[b] + (top_k ? std::min<std::size_t>(n, top_k) : n);
+  }
+  std::vector<std::uint32_t> ids(off[B]);
+  for (std::uint32_t b = 0; b < B; ++b)
+    for (std::uint64_t j = 0; j < off[b + 1] - off[b]; ++j) ids[off[b] + j] = snapshots[b].entries[j].doc_id;
+  check(espn_gpu_prefetch_hints(store_->handle(), ws_, B, ids.data(), off.data(), 0u, side_stream));
+}
+
 BatchResult Reranker::rerank(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
-                             const PipelineConfig& config, Kernel kernel) {
+                             const PipelineConfig& config, Kernel kernel, bool prefetched) {
   if (queries.size() != candidates.size()) throw InvalidInputError("queries and candidate lists differ in length");
   BatchResult res;
   const std::uint32_t B = static_cast<std::uint32_t>(queries.size());
@@ -265,12 +283,14 @@ BatchResult Reranker::rerank(std::span<const QueryEmbedding> queries, std::span<
   a.rerank_count = config.rerank_count;
   a.final_k = k;
   a.alpha = config.alpha;
-  a.flags = config.partial_rerank_enabled ? ESPN_RERANK_PARTIAL : 0u;
+  a.flags = (config.partial_rerank_enabled ? ESPN_RERANK_PARTIAL : 0u) | (prefetched ? ESPN_RERANK_PREFETCHED : 0u);
   a.kernel = static_cast<std::uint32_t>(kernel);
+  std::vector<espn_fetch_stats> fs(B);
   espn_rerank_out o{};
   o.ids = out_ids.data();
   o.scores = out_sc.data();
   o.counts = out_n.data();
+  o.fetch_stats = fs.data();
   const double t0 = now_s();
   check(espn_gpu_rerank(store_->handle(), ws_, &a, &o, nullptr));
   const double wall = now_s() - t0;
@@ -282,15 +302,19 @@ BatchResult Reranker::rerank(std::span<const QueryEmbedding> queries, std::span<
     rl.entries.resize(out_n[b]);
     for (std::uint32_t i = 0; i < out_n[b]; ++i)
       rl.entries[i] = ScoredDoc{out_ids[static_cast<std::size_t>(b) * k + i], out_sc[static_cast<std::size_t>(b) * k + i]};
-    // QueryStats (pipeline.hpp:36-54): the HBM tier holds every needed row
-    // before scoring, so nothing is fetched on the critical path.
+    // QueryStats (pipeline.hpp:36-54) from the device's fetch accounting: rows
+    // in HBM when scoring starts (resident, or staged by the prefetch) are
+    // hits; host-tier rows copied on the critical path are misses.  An
+    // all-HBM store has hit rate 1.
     auto& st = res.stats[b];
     st.query_id = queries[b].query_id;
     const std::uint64_t n = off[b + 1] - off[b];
     st.needed_count = std::min<std::uint64_t>(n, config.rerank_count);
-    st.prefetched_count = st.needed_count;
-    st.missed_count = 0;
-    st.hit_rate = st.needed_count ? 1.0 : 0.0;
+    st.missed_count = fs[b].missed;
+    st.prefetched_count = st.needed_count - st.missed_count;
+    st.hit_rate = st.needed_count ? static_cast<double>(st.prefetched_count) / st.needed_count : 0.0;
+    st.prefetch_bytes = fs[b].prefetch_bytes;
+    st.critical_fetch_bytes = fs[b].critical_bytes;
     for (std::uint64_t j = 0; j < st.needed_count; ++j)
       st.needed_payload_bytes += store_->record_bytes(store_->token_count(ids[off[b] + j]));
     st.rerank_time = wall;

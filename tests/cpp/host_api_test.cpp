@@ -178,6 +178,42 @@ int main() {
     try { espn::gpu::Store::open_store("/tmp/espn_no_such_store"); } catch (const espn::Error&) { thrown = true; }
     CHECK(thrown, "open_store of a missing store must throw");
   }
+  // ---- tiered store + prefetch hints (run_query stages 1-2): same rankings, exact accounting ----
+  {
+    std::vector<std::uint8_t> resident(n_docs);
+    for (std::uint32_t i = 0; i < n_docs; ++i) resident[i] = (i * 2654435761u >> 7) % 3 == 0;  // ~1/3 in HBM
+    espn::gpu::Store tiered(rp, codes, d, espn::gpu::Dtype::f16, {}, 0, resident);
+    espn::gpu::Reranker rt(tiered, B, B * K, nq);
+    espn::gpu::Reranker rh(store, B, B * K, nq);
+    espn::PipelineConfig cfg;
+    cfg.rerank_count = 200;
+    cfg.partial_rerank_enabled = true;
+    const std::uint32_t P = 120;  // snapshot: the first P entries of each final list
+    rt.prefetch_hints(cl, P);
+    espn::BatchResult on = rt.rerank(qs, cl, cfg, espn::gpu::Kernel::automatic, /*prefetched=*/true);
+    espn::BatchResult off = rt.rerank(qs, cl, cfg);
+    espn::BatchResult hbm = rh.rerank(qs, cl, cfg);
+    std::vector<char> hinted(n_docs, 0);
+    for (const auto& c : cl)
+      for (std::uint32_t j = 0; j < P && j < c.entries.size(); ++j) hinted[c.entries[j].doc_id] = 1;
+    for (std::uint32_t b = 0; b < B; ++b) {
+      const auto &x = on.rankings[b].entries, &y = off.rankings[b].entries, &z = hbm.rankings[b].entries;
+      CHECK(x.size() == z.size() && y.size() == z.size(), "tiered ranking size q%u", b);
+      for (std::size_t j = 0; j < x.size() && j < z.size() && j < y.size(); ++j)
+        CHECK(x[j].doc_id == z[j].doc_id && x[j].score == z[j].score && y[j].doc_id == z[j].doc_id &&
+                  y[j].score == z[j].score, "tiered ranking q%u pos %zu", b, j);
+      std::uint64_t miss = 0, miss_off = 0;
+      for (std::uint32_t j = 0; j < cfg.rerank_count; ++j) {
+        const std::uint32_t id = cl[b].entries[j].doc_id;
+        if (!resident[id]) { ++miss_off; if (!hinted[id]) ++miss; }
+      }
+      CHECK(on.stats[b].missed_count == miss, "q%u missed %llu vs %llu", b,
+            (unsigned long long)on.stats[b].missed_count, (unsigned long long)miss);
+      CHECK(off.stats[b].missed_count == miss_off, "q%u unprefetched missed", b);
+      CHECK(on.stats[b].prefetched_count + on.stats[b].missed_count == on.stats[b].needed_count, "q%u counts", b);
+      CHECK(hbm.stats[b].hit_rate == 1.0, "all-HBM hit rate");
+    }
+  }
   // ---- error mapping (error.hpp:8-42) ----
   {
     espn::PipelineConfig cfg;
