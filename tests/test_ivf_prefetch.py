@@ -212,3 +212,81 @@ def test_hint_budget_overflow_falls_back_to_critical_path(cuda_ok):
     assert sum(f["missed"] for f in on.fetch) > 0
     rr.close()
     store.close()
+
+
+@pytest.mark.gpu
+def test_prefetch_hints_state_errors_and_untiered_noop(cuda_ok):
+    store, rr, q, qc, ix, _ = _tiered_setup(0.0, B=4)
+    hints = np.arange(40, dtype=np.uint32)
+    off = np.array([0, 10, 20, 30, 40], np.uint64)
+    with pytest.raises(api.InvalidInputError):
+        rr.prefetch_hints(hints, np.array([0, 10, 5, 30, 40], np.uint64))
+    rr.prefetch_hints(hints, off)  # host ids
+    rr.prefetch_hints(hints, off)
+    with pytest.raises(api.InvalidStateError):  # both staging slots hold pending prefetches
+        rr.prefetch_hints(hints, off)
+    rr.close()
+    store.close()
+    # an all-HBM store: hints are a no-op and PREFETCHED re-ranks like a plain call
+    from paper_2312_05417_b200 import synth
+    rp, codes = synth.make_table(3000, 32, 1, 63, seed=5)
+    qq, src = synth.make_queries(rp, codes, 32, 4, nq=32, seed=6)
+    ids, cls, coff = synth.make_candidates(3000, 4, 300, src=src, seed=7)
+    hbm = api.GpuStore(rp, codes, 32, "f16")
+    r2 = api.Reranker(hbm, 4, 1200, 32)
+    r2.prefetch_hints(ids, coff)
+    cfg = api.PipelineConfig(rerank_count=300, final_k=10)
+    a = [np.copy(x) for x in r2.rerank_arrays(qq, ids, cls, coff, cfg, prefetched=True)[:3]]
+    b = [np.copy(x) for x in r2.rerank_arrays(qq, ids, cls, coff, cfg)[:3]]
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    r2.close()
+    hbm.close()
+
+
+@pytest.mark.gpu
+def test_prefetch_hints_sharded_ignore_foreign_ids(cuda_ok):
+    """Two doc-id shards (owner = id % 2) of a host-tier table on one GPU: each
+    gets the FULL hint lists, stages only its own docs, and the merged
+    per-shard rankings equal the unsharded ranking."""
+    from paper_2312_05417_b200 import synth
+    from paper_2312_05417_b200.sharding import merge_ranked, split_by_owner
+    G, n, d, B, K, R, k = 2, 6000, 32, 6, 500, 200, 10
+    rp, codes = synth.make_table(n, d, 1, 63, seed=8)
+    q, src = synth.make_queries(rp, codes, d, B, nq=32, seed=9)
+    ids, cls, off = synth.make_candidates(n, B, K, src=src, seed=10)
+    hints = np.concatenate([ids[int(off[b]):int(off[b]) + 150] for b in range(B)])  # a snapshot per query
+    hoff = np.arange(B + 1, dtype=np.uint64) * 150
+    cfg = api.PipelineConfig(rerank_count=R, final_k=k, partial_rerank_enabled=True)
+    full = api.GpuStore(rp, codes, d, "f16")
+    rf = api.Reranker(full, B, B * K, 32)
+    ref_ids, ref_sc, ref_n, _ = [np.copy(x) if x is not None else None for x in rf.rerank_arrays(q, ids, cls, off, cfg)]
+    rf.close()
+    full.close()
+    lens = np.diff(rp.astype(np.int64))
+    per = []
+    for s in range(G):
+        loc = np.arange(s, n, G)
+        lrp = np.zeros(loc.size + 1, np.uint64)
+        lrp[1:] = np.cumsum(lens[loc])
+        lcodes = np.concatenate([codes[int(rp[i]) * d:int(rp[i + 1]) * d] for i in loc])
+        st = api.GpuStore(lrp, lcodes, d, "f16", shard_count=G, shard_index=s,
+                          resident=np.zeros(loc.size, np.uint8))
+        rr = api.Reranker(st, B, B * K, 32)
+        s_ids, s_cls, s_off, s_need = split_by_owner(ids, cls, off, R, G, s)
+        rr.prefetch_hints(hints, hoff)
+        gi, gs, gc, _ = rr.rerank_arrays(q, s_ids, s_cls, s_off, cfg, needed_counts=s_need, prefetched=True,
+                                         fetch_stats=True)
+        hs = set(int(h) for h in hints if h % G == s)
+        for b, f in enumerate(rr.last_fetch_stats):
+            need = s_ids[int(s_off[b]):int(s_off[b]) + int(s_need[b])]
+            assert f["needed"] == need.size
+            assert f["prefetched"] == sum(int(x) in hs for x in need)
+            assert f["missed"] == need.size - f["prefetched"]
+        per.append((np.copy(gi), np.copy(gs), np.copy(gc)))
+        rr.close()
+        st.close()
+    for b in range(B):
+        mi, ms = merge_ranked([p[0][b] for p in per], [p[1][b] for p in per], [p[2][b] for p in per], k)
+        assert np.array_equal(mi, ref_ids[b, :int(ref_n[b])])
+        assert np.array_equal(ms.view(np.uint32), ref_sc[b, :int(ref_n[b])].view(np.uint32))
