@@ -31,6 +31,9 @@
 //     red.max) and the combine warp sums the q maxima per doc in ascending
 //     query-token order (the oracle's summation order).
 #pragma once
+#ifndef ESPN_PLANES
+#define ESPN_PLANES 4
+#endif
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -79,6 +82,7 @@ struct TcLayout {
   static constexpr uint32_t TMEM_COLS = NBUF * BUFC <= 32 ? 32 : NBUF * BUFC <= 64 ? 64
                                       : NBUF * BUFC <= 128 ? 128 : NBUF * BUFC <= 256 ? 256 : 512;
   static constexpr int NPROD = 2;                  // bulk-copy producer warps
+  static constexpr int PLANES = ESPN_PLANES;       // issuing lanes per producer warp
   static constexpr int NEPI = 8;                   // epilogue warps: 4 lane quarters x 2 column halves
   static constexpr int MMA_WARP = NEPI;
   static constexpr int PROD_WARP0 = NEPI + 1;
@@ -680,15 +684,16 @@ maxsim_tc_kernel(const MaxSimParams p) {
         mbar_wait(&empty_bar[s], ((gs / L::NS) & 1) ^ 1);
         if (lane == 0 && pw == 0) ESPN_STRACE(0, gs);
         if (p.dbg & 4u) bytes = 0;
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&full_bar[s], bytes);
-          if (!(p.dbg & 4u)) {
-            const uint32_t sbase = smem_u32(sB + s * L::STAGE_BYTES);
-            for (uint32_t o = o0 + ((o0 & 1u) ^ pw); o < o1; o += 2) {
-              const uint4 op = U.op[o];
-              bulk_g2s(sbase + op.z, reinterpret_cast<const void*>((uint64_t)op.x | ((uint64_t)op.y << 32)), op.w,
-                       &full_bar[s], policy);
-            }
+        if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], bytes);
+        __syncwarp();
+        // PLANES lanes of the warp issue its ops concurrently (the per-thread
+        // issue of a bulk copy, not the TMA engine, bounds one issuing lane)
+        if (!(p.dbg & 4u) && lane < L::PLANES) {
+          const uint32_t sbase = smem_u32(sB + s * L::STAGE_BYTES);
+          for (uint32_t o = o0 + ((o0 & 1u) ^ pw) + 2 * lane; o < o1; o += 2 * L::PLANES) {
+            const uint4 op = U.op[o];
+            bulk_g2s(sbase + op.z, reinterpret_cast<const void*>((uint64_t)op.x | ((uint64_t)op.y << 32)), op.w,
+                     &full_bar[s], policy);
           }
         }
         __syncwarp();
