@@ -2,6 +2,7 @@
 // lifetime, batch orchestration (H2D -> K2 MaxSim -> K3 top-k -> D2H) and the
 // standalone gather / merge / synth entry points.  Pure CUDA runtime; no torch.
 #include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -1207,18 +1208,43 @@ int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t
   if (!ids || !out_row_ptr) return fail(ESPN_E_INVALID_INPUT, "null argument");
   DeviceGuard g(t->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream_v);
-  uint32_t* derr = nullptr;
-  ESPN_CUDA_TRY(cudaMallocAsync(&derr, sizeof(uint32_t), s));
-  ESPN_CUDA_TRY(cudaMemsetAsync(derr, 0, sizeof(uint32_t), s));
+  // per-thread, per-device scratch (error flag + pinned readback + CUB scan
+  // temp), grown on demand: no allocation on the steady-state call path
+  struct GatherScratch {
+    int device = -1;
+    uint32_t* err = nullptr;
+    uint64_t* h = nullptr;  // pinned: {err, total}
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    ~GatherScratch() { if (err) { cudaFree(err); cudaFree(tmp); cudaFreeHost(h); } }
+  };
+  thread_local GatherScratch gs;
+  if (gs.device != t->device) {
+    if (gs.err) { cudaFree(gs.err); cudaFree(gs.tmp); cudaFreeHost(gs.h); }
+    gs = GatherScratch{};
+    ESPN_CUDA_TRY(cudaMalloc(&gs.err, sizeof(uint32_t)));
+    ESPN_CUDA_TRY(cudaMallocHost(&gs.h, 2 * sizeof(uint64_t)));
+    gs.device = t->device;
+  }
+  size_t need = 0;
+  ESPN_CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, need, out_row_ptr + 1, out_row_ptr + 1, (int64_t)n, s));
+  if (need > gs.tmp_bytes) {
+    cudaFree(gs.tmp);
+    gs.tmp = nullptr;
+    gs.tmp_bytes = 0;
+    ESPN_CUDA_TRY(cudaMalloc(&gs.tmp, need));
+    gs.tmp_bytes = need;
+  }
+  ESPN_CUDA_TRY(cudaMemsetAsync(gs.err, 0, sizeof(uint32_t), s));
+  ESPN_CUDA_TRY(cudaMemsetAsync(out_row_ptr, 0, sizeof(uint64_t), s));
   const int blocks = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)t->num_sms * 8);
-  gather_count_kernel<<<blocks, 256, 0, s>>>(t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, derr);
-  scan_u64_kernel<<<1, 1024, 0, s>>>(out_row_ptr, n);
-  uint32_t herr = 0;
-  uint64_t total = 0;
-  ESPN_CUDA_TRY(cudaMemcpyAsync(&herr, derr, sizeof herr, cudaMemcpyDeviceToHost, s));
-  ESPN_CUDA_TRY(cudaMemcpyAsync(&total, out_row_ptr + n, sizeof total, cudaMemcpyDeviceToHost, s));
+  gather_count_kernel<<<blocks, 256, 0, s>>>(t->row_ptr, t->n_docs, t->shard_count, t->shard_index, ids, n, out_row_ptr, gs.err);
+  ESPN_CUDA_TRY(cub::DeviceScan::InclusiveSum(gs.tmp, need, out_row_ptr + 1, out_row_ptr + 1, (int64_t)n, s));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(gs.h, gs.err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(gs.h + 1, out_row_ptr + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   ESPN_CUDA_TRY(cudaStreamSynchronize(s));
-  cudaFreeAsync(derr, s);
+  const uint32_t herr = (uint32_t)(gs.h[0] & 0xffffffffu);
+  const uint64_t total = gs.h[1];
   if (herr) {
     g_last_error = "unknown doc id in gather request (store.hpp:92-93)";
     return ESPN_E_INVALID_INPUT;
