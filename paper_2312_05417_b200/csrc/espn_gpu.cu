@@ -407,7 +407,7 @@ int launch_stage(espn_gpu_table* t, espn_gpu_workspace* w, int slot, const uint6
   sp.err = w->err;
   sp.hint_map = hinted ? w->hint_map : nullptr;
   sp.hint_epoch = hinted ? st.hint_epoch : 0u;
-  stage_kernel<<<B, 256, 0, s>>>(sp);
+  stage_kernel<<<B, kStageThreads, 0, s>>>(sp);
   ESPN_CUDA_TRY(cudaGetLastError());
   ESPN_CUDA_TRY(cudaEventRecord(st.done, s));
   return ESPN_OK;
@@ -1172,7 +1172,7 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
   hp.cursor = st.cursor;
   hp.qstats = st.qstats;
   hp.err = w->err;
-  hint_stage_kernel<<<B, 256, 0, s>>>(hp);
+  hint_stage_kernel<<<B, kStageThreads, 0, s>>>(hp);
   ESPN_CUDA_TRY(cudaGetLastError());
   ESPN_CUDA_TRY(cudaEventRecord(st.done, s));
   st.hint_epoch = w->hint_epoch;

@@ -593,12 +593,20 @@ relocate_rows_kernel(const uint8_t* src_rows, const uint64_t* row_ptr, const uin
   }
 }
 
+// CTA size of the staging kernels: one CTA per query, a warp per candidate --
+// every warp walks its docs one PCIe/HBM round trip at a time, so more warps
+// per query mean more transfers in flight.
+#ifndef ESPN_STAGE_THREADS
+#define ESPN_STAGE_THREADS 1024
+#endif
+constexpr int kStageThreads = ESPN_STAGE_THREADS;
+
 // Per-batch staging of host-tier rows (tiered tables).  CTA per query, warp per
 // needed candidate: resident docs resolve to their HBM address; host-tier docs
 // are copied (16-byte loads from mapped pinned memory, i.e. PCIe reads) into
 // the staging buffer.  Writes the per-candidate row address the MaxSim kernel
 // reads, and the per-query fetch accounting.
-__global__ void __launch_bounds__(256) stage_kernel(const StageParams s) {
+__global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageParams s) {
   const uint32_t b = blockIdx.x;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t c0 = s.cand_off[b], c1 = s.cand_off[b + 1];
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const StageParams s) {
 // claim the doc's hint-map entry copies it; the others skip).  The consumer
 // (stage_kernel with hint_map) runs after this kernel on another stream,
 // ordered by an event, so plain stores publish the entries.
-__global__ void __launch_bounds__(256) hint_stage_kernel(const HintParams s) {
+__global__ void __launch_bounds__(kStageThreads) hint_stage_kernel(const HintParams s) {
   const uint32_t b = blockIdx.x;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t h0 = s.hint_off[b], h1 = s.hint_off[b + 1];
