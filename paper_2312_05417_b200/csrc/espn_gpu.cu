@@ -79,6 +79,8 @@ int check_device(int dev, int* num_sms, bool* tc_ok) {
   return ESPN_OK;
 }
 
+constexpr int kMinUnitDocs = 8;  // shortest work unit (small batches, see espn_gpu_rerank)
+
 template <int D>
 constexpr int tc_unit_docs(uint32_t max_t) {
   using L = TcLayout<D>;
@@ -592,7 +594,8 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   al((void**)&w->needed, B * sizeof(uint32_t));
   // work-unit table capacity: every query may end in a partial unit
   {
-    const int ud = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
+    int ud = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
+    if (ud > kMinUnitDocs) ud = kMinUnitDocs;  // small batches use units down to kMinUnitDocs docs
     w->max_units = ud > 0 ? (C + ud - 1) / ud + 2 * B : 0;  // + partial units (needed, tail)
   }
   al((void**)&w->unit_tab, w->max_units * sizeof(uint4));
@@ -745,7 +748,14 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
 
   // ---- kernel choice (tcgen05 when the dim has a tensor-core tiling) ----
   uint32_t kern = a->kernel;
-  const int unit_docs = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
+  int unit_docs = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
+  if (unit_docs > kMinUnitDocs) {
+    // small batches: shorter work units so that every SM gets one (C1: one
+    // query x 1000 candidates -> 125 units of 8 docs instead of 16 of 64)
+    const uint64_t ub = (uint64_t)a->n_queries * std::max<uint32_t>(a->rerank_count, 1u);
+    const uint64_t per_sm = (ub + t->num_sms - 1) / t->num_sms;
+    unit_docs = (int)std::max<uint64_t>(kMinUnitDocs, std::min<uint64_t>((uint64_t)unit_docs, per_sm));
+  }
   if (kern == ESPN_KERNEL_AUTO) kern = (tc_supported(t->d) && unit_docs > 0) ? ESPN_KERNEL_TCGEN05 : ESPN_KERNEL_SIMT;
   if (kern == ESPN_KERNEL_TCGEN05 && (!t->tc_ok || !tc_supported(t->d) || unit_docs <= 0))
     return fail(ESPN_E_INVALID_CONFIG, "tcgen05 MaxSim needs an sm_100 device, d in {16,32,64,128} and docs <= 4096 tokens");
