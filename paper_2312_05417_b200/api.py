@@ -111,7 +111,13 @@ def build_store(base, row_ptr, rows, d: int, d_cls: int = 128, value_width: int 
     row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
     rows = np.ascontiguousarray(rows, dtype=np.float32)
     n = int(row_ptr.shape[0]) - 1
+    if n < 0 or (n and int(row_ptr[0]) != 0) or np.any(np.diff(row_ptr.astype(np.int64)) < 0):
+        raise InvalidInputError("row_ptr must start at 0 and be non-decreasing")
+    if rows.size < int(row_ptr[-1]) * int(d):
+        raise InvalidInputError("rows hold fewer than row_ptr[n] * d values")
     cls_a = None if cls is None else np.ascontiguousarray(cls, dtype=np.float32)
+    if cls_a is not None and cls_a.size < n * int(d_cls):
+        raise InvalidInputError("cls holds fewer than n_docs * d_cls values")
     _check_store(L.store_lib().espn_store_build(str(base).encode(), n, int(d), int(d_cls), int(value_width),
                                                 int(alignment), row_ptr.ctypes.data, rows.ctypes.data,
                                                 cls_a.ctypes.data if cls_a is not None else None))

@@ -184,3 +184,13 @@ def test_open_store_reranks_like_in_memory_table(tmp_path, cuda_ok):
         s.close()
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+def test_python_wrapper_bounds_checks(tmp_path):
+    rp = np.array([0, 3, 5], np.uint64)
+    with pytest.raises(api.InvalidInputError):
+        api.build_store(tmp_path / "b", rp, np.zeros((4, 8), np.float32), 8)  # 5 rows needed
+    with pytest.raises(api.InvalidInputError):
+        api.build_store(tmp_path / "b", rp, np.zeros((5, 8), np.float32), 8, 16, cls=np.zeros((1, 16), np.float32))
+    with pytest.raises(api.InvalidInputError):
+        api.build_store(tmp_path / "b", np.array([1, 3], np.uint64), np.zeros((3, 8), np.float32), 8)
