@@ -7,8 +7,9 @@ embeddings to the GPU, PAPER §4.2).  Its role here is to emit, per query, the
 snapshot after delta clusters (the prefetch hints fed to
 espn_gpu_prefetch_hints) and the final candidate list (fed to
 espn_gpu_rerank).  Inner products use BLAS, so cls scores may differ from the
-reference's ascending-order dot_f32 in the last bits; the re-rank path takes
-the cls scores it is given, so this does not affect parity of the path.
+reference's ascending-order dot_f32 in the last bits (they are float64 sums
+rounded once to fp32); the re-rank path takes the cls scores it is given, so
+this does not affect parity of the path.
 
   * train_ivf: k-means++ seeding + Lloyd iterations (L2) on a seeded sample
     of at most `sample_per_list` x nlist vectors, then every vector goes to
@@ -111,6 +112,14 @@ def train_ivf(vectors: np.ndarray, nlist: int, max_iters: int = 20, seed: int = 
     return IvfIndex(d, c, off, order.astype(np.uint32), x[order])
 
 
+def _ip(vecs: np.ndarray, q: np.ndarray) -> np.ndarray:
+    """Inner products accumulated in float64 and rounded once to fp32: the
+    same value whatever BLAS blocking or segment split computes it, so the
+    cursor's candidates are reproducible and match an exhaustive oracle
+    computed the same way (SPEC acceptance #2)."""
+    return (vecs.astype(np.float64) @ q.astype(np.float64)).astype(np.float32)
+
+
 def _top(ids: np.ndarray, scores: np.ndarray, k: int):
     o = np.lexsort((ids, -scores))[:k]  # score desc, doc_id asc (ivf.hpp:45-46)
     return ids[o], scores[o]
@@ -150,7 +159,7 @@ class SearchCursor:
         segs = [(int(ix.list_off[c]), int(ix.list_off[c + 1])) for c in self.plan[self.visited:self.visited + n_clusters]]
         self.visited += n_clusters
         ids = np.concatenate([self._ids] + [ix.ids[a:b] for a, b in segs])
-        sc = np.concatenate([self._scores] + [ix.vectors[a:b] @ self.query for a, b in segs]).astype(np.float32)
+        sc = np.concatenate([self._scores] + [_ip(ix.vectors[a:b], self.query) for a, b in segs]).astype(np.float32)
         self._ids, self._scores = _top(ids, sc, self.capacity)
 
     def snapshot(self, top_k: int) -> CandidateList:

@@ -9,8 +9,9 @@ load_qrels (C++: espn::gpu::mrr_at_k ...).
 Synthetic evaluation set (no network for MS MARCO): every query's relevant
 doc is its source doc (queries are perturbed copies of its rows, synth.py);
 the first-stage candidate list places that doc at a geometric rank
-(mean `mean_rank`) and drops it for a fraction `miss` of the queries, like a
-first-stage retriever with imperfect recall.  Real qrels plug in through
+(mean `mean_rank`, default 10: a CLS-only first stage with MRR@10 ~0.2) and
+drops it for a fraction `miss` of the queries, like a first-stage retriever
+with imperfect recall.  Real qrels plug in through
 load_qrels.
 
     python -m paper_2312_05417_b200.quality [--docs 200000 --queries 512 --K 1000]
@@ -27,7 +28,7 @@ from . import api, synth
 
 
 def make_eval_set(n_docs: int = 20000, d: int = 32, n_queries: int = 64, K: int = 1000, t_min: int = 1,
-                  t_max: int = 63, nq: int = 32, dtype: str = "f16", mean_rank: float = 40.0, miss: float = 0.1,
+                  t_max: int = 63, nq: int = 32, dtype: str = "f16", mean_rank: float = 10.0, miss: float = 0.1,
                   seed: int = 5):
     """(row_ptr, codes, q, ids, cls, off, qrels): CSR candidates sorted
     (cls desc, id asc) with the relevant doc at a geometric first-stage rank."""

@@ -137,3 +137,5 @@ def test_rerank_sweep_matches_oracle_and_is_monotone(oracle, cuda_ok):
     mrr = [r["R"][R]["mrr"] for R in Rs]
     assert all(a <= b for a, b in zip(mrr, mrr[1:])), mrr
     assert mrr[-1] > r["first_stage"]["mrr"]
+    # SPEC.md:464 (scaled-down Fig. 6): MRR@10(R=64) / MRR@10(R=1000) expected >= 0.95
+    assert r["mrr_ratio_vs_Rmax"][64] >= 0.95, r["mrr_ratio_vs_Rmax"]
