@@ -48,7 +48,11 @@ struct TcCfg;
 // (wider) MMA instructions and a 3x smaller A tile; needs 4 x NQC TMEM
 // columns per buffer, so it is used where NQC is small (d = 128).
 template <> struct TcCfg<16>  { static constexpr int NQC = 128, NS = 6, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
-template <> struct TcCfg<32>  { static constexpr int NQC = 128, NS = 4, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
+#ifndef ESPN_D32_NQC
+#define ESPN_D32_NQC 128
+#define ESPN_D32_NS 4
+#endif
+template <> struct TcCfg<32>  { static constexpr int NQC = ESPN_D32_NQC, NS = ESPN_D32_NS, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
 template <> struct TcCfg<64>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
 template <> struct TcCfg<128> { static constexpr int NQC = 64,  NS = 2, UNITMAX = 32, NU = 2; static constexpr bool REPA = true; };
 
