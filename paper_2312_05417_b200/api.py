@@ -404,6 +404,10 @@ class GpuStore:
         return Reranker(self, max_queries, max_candidates, max_query_tokens)
 
     def close(self) -> None:
+        rr = getattr(self, "_pipeline_rr", None)  # workspace cached by pipeline.run_query / run_batch_queries
+        if rr is not None:
+            rr.close()
+            self._pipeline_rr = None
         if getattr(self, "_h", None):
             L.lib().espn_gpu_table_close(self._h)
             self._h = None

@@ -217,3 +217,77 @@ def main(argv=None):
 
 if __name__ == "__main__":
     main()
+
+
+# ---- reference-named entry points (pipeline.hpp:56-97) ------------------------------
+@dataclass
+class HitRatePoint:
+    """pipeline.hpp:87-90."""
+    step_pct: float = 0.0
+    mean_hit_rate: float = 0.0
+
+
+def _reranker_for(store: api.GpuStore, B: int, C: int, nq: int) -> api.Reranker:
+    """One cached workspace per store, regrown when a batch needs more."""
+    rr = getattr(store, "_pipeline_rr", None)
+    if rr is None or rr.max_queries < B or rr.max_candidates < C or rr._nq < nq:
+        if rr is not None:
+            rr.close()
+        rr = api.Reranker(store, B, max(C, 1), nq, staging_bytes=256 << 20)
+        rr._nq = nq
+        store._pipeline_rr = rr
+    return rr
+
+
+def run_batch_queries(queries: Sequence[api.QueryEmbedding], index: IvfIndex, store: api.GpuStore,
+                      config: api.PipelineConfig, concurrency: int = 1) -> api.BatchResult:
+    """run_batch (pipeline.hpp:81-85): every query through stages (1)-(6), the
+    batch in ONE device pass (so `concurrency` only bounds nothing here);
+    per-query results identical to run_query."""
+    B = len(queries)
+    res = api.BatchResult()
+    if B == 0:
+        return res
+    nq, d = int(queries[0].rows), int(queries[0].cols)
+    for qe in queries:
+        if qe.cols != store.d or qe.rows != nq:
+            raise api.InvalidInputError("query dims differ from the table / within the batch")
+        if np.asarray(qe.cls).size != index.d_cls:
+            raise api.InvalidInputError("query CLS dimension != index d_cls")
+    q_bow = np.stack([np.asarray(qe.tokens, np.float32).reshape(nq, d) for qe in queries])
+    q_cls = np.stack([np.asarray(qe.cls, np.float32) for qe in queries])
+    rr = _reranker_for(store, B, B * config.effective_candidate_k(), nq)
+    t0 = time.perf_counter()
+    r = run_batch(q_bow, q_cls, index, rr, config, keep_lists=True)
+    wall = time.perf_counter() - t0
+    for b, qe in enumerate(queries):
+        n = int(r.counts[b])
+        res.rankings.append(api.RankedList([api.ScoredDoc(int(i), float(s))
+                                            for i, s in zip(r.ids[b, :n], r.scores[b, :n])]))
+        st = api._stats_for(store, r.finals[b][0], int(r.needed[b]), qe.query_id, r.rerank_s, r.fetch[b])
+        st.ann_time = r.ann_s
+        st.total_time = r.ann_s + r.rerank_s
+        res.stats.append(st)
+    lat = np.full(B, wall)
+    res.batch = api.BatchStats(n_queries=B, mean_latency=float(lat.mean()), p50_latency=float(np.median(lat)),
+                               p99_latency=float(np.percentile(lat, 99)), wall_time=wall,
+                               total_critical_fetch_bytes=int(sum(s.critical_fetch_bytes for s in res.stats)))
+    return res
+
+
+def run_query(query: api.QueryEmbedding, index: IvfIndex, store: api.GpuStore, config: api.PipelineConfig):
+    """run_query (pipeline.hpp:56-64) -> (RankedList, QueryStats)."""
+    r = run_batch_queries([query], index, store, config)
+    return r.rankings[0], r.stats[0]
+
+
+def measure_hit_rate_queries(queries: Sequence[api.QueryEmbedding], index: IvfIndex, store: api.GpuStore,
+                             base: api.PipelineConfig, steps: Sequence[float]) -> List[HitRatePoint]:
+    """measure_hit_rate (pipeline.hpp:92-97): mean hit rate per prefetch step
+    (the reference definition, |snapshot ∩ needed| / |needed|)."""
+    nq, d = int(queries[0].rows), int(queries[0].cols)
+    q_bow = np.stack([np.asarray(qe.tokens, np.float32).reshape(nq, d) for qe in queries])
+    q_cls = np.stack([np.asarray(qe.cls, np.float32) for qe in queries])
+    rr = _reranker_for(store, len(queries), len(queries) * base.effective_candidate_k(), nq)
+    return [HitRatePoint(p["step_pct"], p["mean_hit_rate"])
+            for p in measure_hit_rate(q_bow, q_cls, index, rr, base, steps)]

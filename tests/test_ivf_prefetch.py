@@ -329,3 +329,27 @@ def test_prefetch_hints_sharded_ignore_foreign_ids(cuda_ok):
         mi, ms = merge_ranked([p[0][b] for p in per], [p[1][b] for p in per], [p[2][b] for p in per], k)
         assert np.array_equal(mi, ref_ids[b, :int(ref_n[b])])
         assert np.array_equal(ms.view(np.uint32), ref_sc[b, :int(ref_n[b])].view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_reference_named_pipeline_entry_points(cuda_ok):
+    """run_query / run_batch / measure_hit_rate with the reference's carrier
+    types (pipeline.hpp:56-97): batch == per-query calls, prefetch on == off,
+    QueryStats consistent, step 100 -> hit rate 1.0."""
+    store, rr, q, qc, ix, _ = _tiered_setup(0.2, B=6)
+    rr.close()
+    queries = [api.QueryEmbedding(query_id=100 + b, cls=qc[b], rows=32, cols=32, tokens=q[b].ravel())
+               for b in range(6)]
+    base = dict(nprobe=64, rerank_count=200, final_k=10, candidate_k=1000, partial_rerank_enabled=True)
+    on = pipeline.run_batch_queries(queries, ix, store, api.PipelineConfig(prefetch_step_pct=30.0, **base))
+    off = pipeline.run_batch_queries(queries, ix, store, api.PipelineConfig(prefetch_enabled=False, **base))
+    assert on.rankings == off.rankings
+    for b, qe in enumerate(queries):
+        rl, st = pipeline.run_query(qe, ix, store, api.PipelineConfig(prefetch_step_pct=30.0, **base))
+        assert rl == on.rankings[b]
+        assert st.query_id == qe.query_id and st.needed_count == 200
+        assert st.prefetched_count + st.missed_count <= st.needed_count
+        assert 0.0 <= st.hit_rate <= 1.0
+    pts = pipeline.measure_hit_rate_queries(queries, ix, store, api.PipelineConfig(**base), [5, 100])
+    assert pts[-1].mean_hit_rate == 1.0 and pts[0].mean_hit_rate <= 1.0
+    store.close()
