@@ -89,6 +89,16 @@ constexpr int tc_unit_docs(uint32_t max_t) {
   return (int)std::min<uint32_t>(u, (uint32_t)L::UNITMAX);
 }
 
+int tc_max_tokens_rt(uint32_t d) {  // longest doc one work unit holds (UNITMAX x 64 slots)
+  switch (d) {
+    case 16: return TcLayout<16>::MAX_SLOTS;
+    case 32: return TcLayout<32>::MAX_SLOTS;
+    case 64: return TcLayout<64>::MAX_SLOTS;
+    case 128: return TcLayout<128>::MAX_SLOTS;
+    default: return 0;
+  }
+}
+
 int tc_unit_docs_rt(uint32_t d, uint32_t max_t) {
   switch (d) {
     case 16: return tc_unit_docs<16>(max_t);
@@ -758,7 +768,9 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
   if (kern == ESPN_KERNEL_AUTO) kern = (tc_supported(t->d) && unit_docs > 0) ? ESPN_KERNEL_TCGEN05 : ESPN_KERNEL_SIMT;
   if (kern == ESPN_KERNEL_TCGEN05 && (!t->tc_ok || !tc_supported(t->d) || unit_docs <= 0))
-    return fail(ESPN_E_INVALID_CONFIG, "tcgen05 MaxSim needs an sm_100 device, d in {16,32,64,128} and docs <= 4096 tokens");
+    return fail(ESPN_E_INVALID_CONFIG, "tcgen05 MaxSim needs an sm_100 device, d in {16,32,64,128} and docs of at most " +
+                                           std::to_string(tc_max_tokens_rt(t->d)) + " tokens at d=" + std::to_string(t->d) +
+                                           " (longest doc here: " + std::to_string(t->max_t) + ")");
   if (kern == ESPN_KERNEL_SIMT && !simt_supported(t->d))
     return fail(ESPN_E_INVALID_CONFIG, "CUDA-core MaxSim supports d in {8,16,32,48,64,96,128}");
   const bool tc = kern == ESPN_KERNEL_TCGEN05;

@@ -137,6 +137,46 @@ def test_short_lists_small_nq_long_docs(oracle, cuda_ok):
     check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "simt", bitexact_bow=True)
 
 
+@pytest.mark.parametrize("d", [32, 128])
+def test_max_length_docs(oracle, cuda_ok, d):
+    # the longest doc the tcgen05 tiling takes (t = 4096 tokens, one doc per
+    # work unit) mixed with short ones, plus a batch of one query (small units)
+    rng = np.random.default_rng(51)
+    t = rng.integers(1, 64, 600)
+    tmax = 4096 if d == 32 else 2048  # UNITMAX x 64 slots (TcCfg)
+    t[[3, 77, 400]] = [tmax, tmax - 1, tmax // 2 + 1]
+    rp = np.zeros(601, np.uint64)
+    rp[1:] = np.cumsum(t)
+    x = rng.standard_normal((int(rp[-1]), d)).astype(np.float32)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    codes = synth.flush_subnormals(api.encode(x.ravel(), "f16"), "f16")
+    q, src = synth.make_queries(rp, codes, d, 3, nq=32, seed=52)
+    ids, cls, off = synth.make_candidates(600, 3, 300, src=src, seed=53)
+    for b in range(3):  # make sure the long docs are candidates
+        seg = ids[int(off[b]):int(off[b + 1])]
+        for j, doc in enumerate([3, 77, 400]):
+            if doc not in seg:
+                seg[-1 - j] = doc
+    cfg = api.PipelineConfig(rerank_count=300, final_k=10)
+    check_against_oracle(oracle, rp, codes, d, "f16", q, ids, cls, off, cfg, "tcgen05")
+    q1, ids1, cls1 = q[:1], ids[:300], cls[:300]
+    check_against_oracle(oracle, rp, codes, d, "f16", q1, ids1, cls1, off[:2], cfg, "tcgen05")
+    # one token more than a unit holds: tcgen05 refuses with the limit, AUTO falls back to the CUDA cores
+    t2 = t.copy()
+    t2[5] = tmax + 1
+    rp2 = np.zeros(601, np.uint64)
+    rp2[1:] = np.cumsum(t2)
+    codes2 = np.zeros(int(rp2[-1]) * d, np.uint16)
+    codes2[:codes.size] = codes
+    store = api.GpuStore(rp2, codes2, d)
+    rr = api.Reranker(store, 3, int(off[-1]), 32)
+    with pytest.raises(api.InvalidConfigError, match=str(tmax)):
+        rr.rerank_arrays(q, ids, cls, off, cfg, kernel="tcgen05")
+    rr.rerank_arrays(q, ids, cls, off, cfg)  # auto -> CUDA cores
+    rr.close()
+    store.close()
+
+
 def test_single_token_docs_and_large_k(oracle, cuda_ok):
     rp, codes, q, ids, cls, off = build_case(4000, 32, 1, 1, B=2, K=3000, seed=41)
     cfg = api.PipelineConfig(rerank_count=3000, final_k=100)
