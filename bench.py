@@ -626,7 +626,11 @@ def run_ours(args, cfg):
         except ValueError:
             traffic = None
 
-    n_launch_ours = args.steps * (3 + (1 if world > 1 else 0))  # plan, MaxSim, top-k (+ merge)
+    # our kernels per step, from the library's own launch counter (plan, primer,
+    # MaxSim, finalize; + the NCCL merge kernel when sharded)
+    c0 = lanes[0].rr.counters()
+    per_batch = c0["kernel_launches"] / max(c0["batches"], 1)
+    n_launch_ours = int(round(args.steps * (per_batch + (1 if world > 1 else 0))))
     q_total = B_q * args.steps  # global queries (each rank scored its share of all of them)
     value = q_total / (ms / 1e3)
     # the L2 claim is computed, not asserted: rows touched per rotation of the
