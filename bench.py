@@ -648,7 +648,7 @@ def run_ours(args, cfg):
         l2_note = ("NOT flushed: the %.0f MB table fits in the 126 MB L2, so rows may be L2-resident between steps "
                    "(a latency-bound configuration)" % (table_bytes / 1e6))
     res = {
-        "metric": BASE_METRIC, "value": value, "unit": "queries/s", "n_gpus": G, "steps": args.steps,
+        "metric": BASE_METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f16", "data": "synthetic: seeded counter-RNG unit-norm fp16 token rows "
         "(t~U{%d..%d}); queries = perturbed rows of a source doc; K-1 uniform random candidates + source"
@@ -677,6 +677,10 @@ def run_ours(args, cfg):
                      "step_frac": alg_bytes / (ms / args.steps / 1e3) / 1e9 / peak},
         "clocks": clocks,
         "gpu_launches": n_launch_ours,
+        **({"emulated_shards": {"shards": G, "measured_gpus": 1,
+                                "value_meaning": "queries/s of the %d-GPU job if every shard ran at this shard's "
+                                                 "measured speed (projection; no collective, no other GPU measured)"
+                                                 % G}} if emulated else {}),
         "check": {"source_doc_ranked_first": src_ok, "e2e_source_doc_ranked_first": e2e_ok},
     }
     if world == 1 and not emulated and not args.no_cpu_baseline:
