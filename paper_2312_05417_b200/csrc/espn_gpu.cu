@@ -291,8 +291,13 @@ struct espn_gpu_workspace {
     uint32_t* needed_in = nullptr;
     cudaEvent_t in_ready = nullptr;  // H2D done (copy stream)
     cudaEvent_t done = nullptr;      // last kernel reading the slot done (compute stream)
+    uint8_t* in_h = nullptr;         // pinned staging of pageable host inputs (q32 | ids | cls)
     bool used = false;
   } io[2];
+  // host input pointers last checked for pinned memory (q32, ids, cls)
+  const void* in_key[3] = {nullptr, nullptr, nullptr};
+  bool in_pinned[3] = {false, false, false};
+  uint8_t* out_h = nullptr;  // pinned bounce of pageable host outputs (synchronous calls)
   uint64_t io_calls = 0;
   // zero-copy outputs: last output pointers checked for pinned host memory
   const void* zc_key[3] = {nullptr, nullptr, nullptr};
@@ -627,6 +632,7 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     }
   }
   if (e == cudaSuccess) e = cudaMallocHost(&w->h_qstats, B * 6 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMallocHost(&w->out_h, (size_t)B * kMaxK * 8 + (size_t)B * 4);
   w->max_list = desc->max_list ? desc->max_list : (uint32_t)std::min<size_t>(C, 4096);
   // fused top-k state; the dedup hash is 8x the declared list (one-probe
   // inserts), at most 32K slots (lists up to 16K candidates)
@@ -652,6 +658,8 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     al((void**)&io.cls, C * sizeof(float));
     al((void**)&io.cand_off, (B + 1) * sizeof(uint64_t));
     al((void**)&io.needed_in, B * sizeof(uint32_t));
+    if (e == cudaSuccess)
+      e = cudaMallocHost(&io.in_h, (size_t)B * w->max_nq * t->d * sizeof(float) + C * (sizeof(uint32_t) + sizeof(float)));
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.in_ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.done, cudaEventDisableTiming);
   }
@@ -684,6 +692,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   for (auto& io : w->io) {
     if (io.done) cudaEventSynchronize(io.done);
     cudaFree(io.q32); cudaFree(io.ids); cudaFree(io.cls); cudaFree(io.cand_off); cudaFree(io.needed_in);
+    cudaFreeHost(io.in_h);
     if (io.in_ready) cudaEventDestroy(io.in_ready);
     if (io.done) cudaEventDestroy(io.done);
   }
@@ -702,7 +711,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
     if (st.free_ev) cudaEventDestroy(st.free_ev);
   }
   cudaFree(w->hint_map);
-  cudaFreeHost(w->h_qstats); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
+  cudaFreeHost(w->h_qstats); cudaFreeHost(w->out_h); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
   cudaFree(w->out_counts); cudaFree(w->err);
   for (auto& sl : w->slots) {
     if (sl.copied) cudaEventSynchronize(sl.copied);
@@ -823,10 +832,30 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
       cand_off = io.cand_off;
     }
     if (!dev_io) {
-      ESPN_CUDA_TRY(cudaMemcpyAsync(io.q32, q32, (size_t)B * nq * t->d * sizeof(float), cudaMemcpyHostToDevice, w->cs));
+      // pinned caller buffers are copied directly (truly async); pageable ones
+      // are staged through the slot's pinned buffer first (a pageable
+      // cudaMemcpyAsync is a synchronous driver copy per array)
+      const void* key[3] = {q32, ids, cls};
+      for (int i = 0; i < 3; ++i)
+        if (key[i] != w->in_key[i]) {
+          cudaPointerAttributes at{};
+          w->in_pinned[i] = cudaPointerGetAttributes(&at, key[i]) == cudaSuccess && at.type == cudaMemoryTypeHost;
+          cudaGetLastError();
+          w->in_key[i] = key[i];
+        }
+      const size_t qb = (size_t)B * nq * t->d * sizeof(float), ib = C * sizeof(uint32_t), cb = C * sizeof(float);
+      if (!(w->in_pinned[0] && w->in_pinned[1] && w->in_pinned[2]) && io.used)
+        ESPN_CUDA_TRY(cudaEventSynchronize(io.in_ready));  // the slot's previous H2D has read in_h
+      uint8_t* hq = io.in_h;
+      uint8_t* hi = io.in_h + qb;
+      uint8_t* hc = hi + ib;
+      const void* srcq = w->in_pinned[0] ? (const void*)q32 : (std::memcpy(hq, q32, qb), (const void*)hq);
+      ESPN_CUDA_TRY(cudaMemcpyAsync(io.q32, srcq, qb, cudaMemcpyHostToDevice, w->cs));
       if (C) {
-        ESPN_CUDA_TRY(cudaMemcpyAsync(io.ids, ids, C * sizeof(uint32_t), cudaMemcpyHostToDevice, w->cs));
-        ESPN_CUDA_TRY(cudaMemcpyAsync(io.cls, cls, C * sizeof(float), cudaMemcpyHostToDevice, w->cs));
+        const void* srci = w->in_pinned[1] ? (const void*)ids : (std::memcpy(hi, ids, ib), (const void*)hi);
+        const void* srcc = w->in_pinned[2] ? (const void*)cls : (std::memcpy(hc, cls, cb), (const void*)hc);
+        ESPN_CUDA_TRY(cudaMemcpyAsync(io.ids, srci, ib, cudaMemcpyHostToDevice, w->cs));
+        ESPN_CUDA_TRY(cudaMemcpyAsync(io.cls, srcc, cb, cudaMemcpyHostToDevice, w->cs));
       }
       q32 = io.q32;
       ids = io.ids;
@@ -1045,9 +1074,18 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     ESPN_CUDA_TRY(cudaEventRecord(w->io[io_slot].done, s));
     w->io[io_slot].used = true;
   }
-  if (!out_direct) {
-    ESPN_CUDA_TRY(cudaMemcpyAsync(o->ids, w->out_ids, (size_t)B * k * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    ESPN_CUDA_TRY(cudaMemcpyAsync(o->scores, w->out_scores, (size_t)B * k * sizeof(float), cudaMemcpyDeviceToHost, s));
+  // pageable host outputs of a synchronous call: D2H into the pinned bounce,
+  // copied out after the sync below (ASYNC callers get direct copies)
+  const bool out_bounce = !out_direct && !(a->flags & ESPN_RERANK_ASYNC) && w->out_h;
+  const size_t ob_ids = (size_t)B * k * sizeof(uint32_t), ob_sc = (size_t)B * k * sizeof(float);
+  if (out_bounce) {
+    ESPN_CUDA_TRY(cudaMemcpyAsync(w->out_h, w->out_ids, ob_ids, cudaMemcpyDeviceToHost, s));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(w->out_h + ob_ids, w->out_scores, ob_sc, cudaMemcpyDeviceToHost, s));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(w->out_h + ob_ids + ob_sc, w->out_counts, (size_t)B * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, s));
+  } else if (!out_direct) {
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->ids, w->out_ids, ob_ids, cudaMemcpyDeviceToHost, s));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->scores, w->out_scores, ob_sc, cudaMemcpyDeviceToHost, s));
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->counts, w->out_counts, (size_t)B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   }
   if ((a->flags & ESPN_RERANK_WRITE_BOW) && o->bow_scores) {
@@ -1070,6 +1108,11 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   ESPN_CUDA_TRY(cudaStreamSynchronize(s));
   ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
   w->async_pending = false;
+  if (out_bounce) {
+    std::memcpy(o->ids, w->out_h, ob_ids);
+    std::memcpy(o->scores, w->out_h + ob_ids, ob_sc);
+    std::memcpy(o->counts, w->out_h + ob_ids + ob_sc, (size_t)B * sizeof(uint32_t));
+  }
   if (o->fetch_stats) {
     for (uint32_t b = 0; b < B; ++b) {
       espn_fetch_stats& f = o->fetch_stats[b];
