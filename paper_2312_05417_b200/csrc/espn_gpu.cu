@@ -291,9 +291,12 @@ struct espn_gpu_workspace {
     uint32_t* needed_in = nullptr;
     cudaEvent_t in_ready = nullptr;  // H2D done (copy stream)
     cudaEvent_t done = nullptr;      // last kernel reading the slot done (compute stream)
-    uint8_t* in_h = nullptr;         // pinned staging of pageable host inputs (q32 | ids | cls)
+    uint8_t* in_h = nullptr;         // pinned staging of pageable host inputs (pack layout)
+    uint8_t* dpack = nullptr;        // device pack (synchronous pageable calls)
+    size_t pack_bytes = 0;
     bool used = false;
   } io[2];
+  uint8_t* opack = nullptr;          // device: err | out ids | scores | counts
   // host input pointers last checked for pinned memory (q32, ids, cls)
   const void* in_key[3] = {nullptr, nullptr, nullptr};
   bool in_pinned[3] = {false, false, false};
@@ -648,18 +651,27 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     if (e == cudaSuccess) e = cudaMemset(w->dedup, 0xFF, 2 * B * (size_t)w->hash_slots * sizeof(uint32_t));
   }
   al((void**)&w->bow, C * sizeof(float));
-  al((void**)&w->out_ids, B * kMaxK * sizeof(uint32_t));
-  al((void**)&w->out_scores, B * kMaxK * sizeof(float));
-  al((void**)&w->out_counts, B * sizeof(uint32_t));
-  al((void**)&w->err, 4 * sizeof(uint32_t));
+  // outputs and the error word in ONE allocation: [err 16 B | ids | scores |
+  // counts], so a synchronous call reads everything back with one copy
+  al((void**)&w->opack, 16 + (size_t)B * kMaxK * 8 + (size_t)B * 4);
+  if (e == cudaSuccess) {
+    w->err = reinterpret_cast<uint32_t*>(w->opack);
+    w->out_ids = reinterpret_cast<uint32_t*>(w->opack + 16);
+    w->out_scores = reinterpret_cast<float*>(w->out_ids + (size_t)B * kMaxK);
+    w->out_counts = reinterpret_cast<uint32_t*>(w->out_scores + (size_t)B * kMaxK);
+  }
   for (auto& io : w->io) {
     al((void**)&io.q32, B * w->max_nq * t->d * sizeof(float));
     al((void**)&io.ids, C * sizeof(uint32_t));
     al((void**)&io.cls, C * sizeof(float));
     al((void**)&io.cand_off, (B + 1) * sizeof(uint64_t));
     al((void**)&io.needed_in, B * sizeof(uint32_t));
-    if (e == cudaSuccess)
-      e = cudaMallocHost(&io.in_h, (size_t)B * w->max_nq * t->d * sizeof(float) + C * (sizeof(uint32_t) + sizeof(float)));
+    // packed inputs of synchronous pageable-buffer calls: [offsets | needed |
+    // q32 | ids | cls], 16-byte aligned pieces, one H2D per call
+    io.pack_bytes = ((B + 1) * 8 + 15) / 16 * 16 + (B * 4 + 15) / 16 * 16 +
+                    ((size_t)B * w->max_nq * t->d * 4 + 15) / 16 * 16 + (C * 4 + 15) / 16 * 16 + C * 4;
+    al((void**)&io.dpack, io.pack_bytes);
+    if (e == cudaSuccess) e = cudaMallocHost(&io.in_h, io.pack_bytes);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.in_ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.done, cudaEventDisableTiming);
   }
@@ -692,7 +704,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   for (auto& io : w->io) {
     if (io.done) cudaEventSynchronize(io.done);
     cudaFree(io.q32); cudaFree(io.ids); cudaFree(io.cls); cudaFree(io.cand_off); cudaFree(io.needed_in);
-    cudaFreeHost(io.in_h);
+    cudaFreeHost(io.in_h); cudaFree(io.dpack);
     if (io.in_ready) cudaEventDestroy(io.in_ready);
     if (io.done) cudaEventDestroy(io.done);
   }
@@ -711,8 +723,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
     if (st.free_ev) cudaEventDestroy(st.free_ev);
   }
   cudaFree(w->hint_map);
-  cudaFreeHost(w->h_qstats); cudaFreeHost(w->out_h); cudaFree(w->bow); cudaFree(w->out_ids); cudaFree(w->out_scores);
-  cudaFree(w->out_counts); cudaFree(w->err);
+  cudaFreeHost(w->h_qstats); cudaFreeHost(w->out_h); cudaFree(w->bow); cudaFree(w->opack);
   for (auto& sl : w->slots) {
     if (sl.copied) cudaEventSynchronize(sl.copied);
     cudaFreeHost(sl.cand_off); cudaFreeHost(sl.needed);
@@ -810,7 +821,42 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   // stream: the slot's previous batch must be done with it, and the compute
   // stream waits for the H2D -- batch n+1's copies overlap batch n's kernels.
   int io_slot = -1;
-  if (!dev_off || !dev_io) {
+  const bool sync_call = !(a->flags & ESPN_RERANK_ASYNC);
+  if (!dev_io) {  // which caller buffers are pinned (cached per pointer)
+    const void* key[3] = {q32, ids, cls};
+    for (int i = 0; i < 3; ++i)
+      if (key[i] != w->in_key[i]) {
+        cudaPointerAttributes at{};
+        w->in_pinned[i] = cudaPointerGetAttributes(&at, key[i]) == cudaSuccess && at.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        w->in_key[i] = key[i];
+      }
+  }
+  const bool all_pinned = !dev_io && w->in_pinned[0] && (C == 0 || (w->in_pinned[1] && w->in_pinned[2]));
+  if (sync_call && !dev_io && !dev_off && !all_pinned) {
+    // synchronous call with pageable buffers: pack every input into the I/O
+    // slot's pinned buffer and move it with ONE copy on the compute stream
+    io_slot = (int)(w->io_calls++ % 2);
+    auto& io = w->io[io_slot];
+    if (io.used) ESPN_CUDA_TRY(cudaEventSynchronize(io.done));  // an earlier ASYNC batch is done with it
+    auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+    const size_t qb = (size_t)B * nq * t->d * sizeof(float), ib = C * sizeof(uint32_t), cb = C * sizeof(float);
+    const size_t o_need = a16((B + 1) * 8), o_q = o_need + a16(B * 4), o_ids = o_q + a16(qb),
+                 o_cls = o_ids + a16(ib), total = o_cls + cb;
+    std::memcpy(io.in_h, a->cand_offsets, (B + 1) * sizeof(uint64_t));
+    if (a->needed_counts) std::memcpy(io.in_h + o_need, a->needed_counts, B * sizeof(uint32_t));
+    std::memcpy(io.in_h + o_q, q32, qb);
+    if (C) {
+      std::memcpy(io.in_h + o_ids, ids, ib);
+      std::memcpy(io.in_h + o_cls, cls, cb);
+    }
+    ESPN_CUDA_TRY(cudaMemcpyAsync(io.dpack, io.in_h, total, cudaMemcpyHostToDevice, s));
+    cand_off = reinterpret_cast<const uint64_t*>(io.dpack);
+    if (a->needed_counts) needed_in = reinterpret_cast<const uint32_t*>(io.dpack + o_need);
+    q32 = reinterpret_cast<const float*>(io.dpack + o_q);
+    ids = reinterpret_cast<const uint32_t*>(io.dpack + o_ids);
+    cls = reinterpret_cast<const float*>(io.dpack + o_cls);
+  } else if (!dev_off || !dev_io) {
     io_slot = (int)(w->io_calls++ % 2);
     auto& io = w->io[io_slot];
     if (io.used) ESPN_CUDA_TRY(cudaStreamWaitEvent(w->cs, io.done, 0));
@@ -835,14 +881,6 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
       // pinned caller buffers are copied directly (truly async); pageable ones
       // are staged through the slot's pinned buffer first (a pageable
       // cudaMemcpyAsync is a synchronous driver copy per array)
-      const void* key[3] = {q32, ids, cls};
-      for (int i = 0; i < 3; ++i)
-        if (key[i] != w->in_key[i]) {
-          cudaPointerAttributes at{};
-          w->in_pinned[i] = cudaPointerGetAttributes(&at, key[i]) == cudaSuccess && at.type == cudaMemoryTypeHost;
-          cudaGetLastError();
-          w->in_key[i] = key[i];
-        }
       const size_t qb = (size_t)B * nq * t->d * sizeof(float), ib = C * sizeof(uint32_t), cb = C * sizeof(float);
       if (!(w->in_pinned[0] && w->in_pinned[1] && w->in_pinned[2]) && io.used)
         ESPN_CUDA_TRY(cudaEventSynchronize(io.in_ready));  // the slot's previous H2D has read in_h
@@ -871,6 +909,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   float* out_scores_k = w->out_scores;
   uint32_t* out_counts_k = w->out_counts;
   bool out_direct = dev_io;
+  bool out_bounce = false;  // synchronous pageable outputs: compact [err | ids | scores | counts], one D2H
   if (dev_io) {
     out_ids_k = o->ids;
     out_scores_k = o->scores;
@@ -897,6 +936,11 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
       out_scores_k = static_cast<float*>(w->zc_dev[1]);
       out_counts_k = static_cast<uint32_t*>(w->zc_dev[2]);
       out_direct = true;
+    } else if (sync_call && w->out_h) {
+      out_bounce = true;
+      out_ids_k = w->out_ids;  // == opack + 16
+      out_scores_k = reinterpret_cast<float*>(w->out_ids + (size_t)B * k);
+      out_counts_k = reinterpret_cast<uint32_t*>(out_scores_k + (size_t)B * k);
     }
   }
   // the device error word is sticky across un-synced ASYNC batches; it is
@@ -1074,14 +1118,12 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     ESPN_CUDA_TRY(cudaEventRecord(w->io[io_slot].done, s));
     w->io[io_slot].used = true;
   }
-  // pageable host outputs of a synchronous call: D2H into the pinned bounce,
-  // copied out after the sync below (ASYNC callers get direct copies)
-  const bool out_bounce = !out_direct && !(a->flags & ESPN_RERANK_ASYNC) && w->out_h;
+  // pageable host outputs of a synchronous call: the compact output pack
+  // (error word included) comes back with ONE copy into the pinned bounce and
+  // is copied out after the sync below (ASYNC callers get direct copies)
   const size_t ob_ids = (size_t)B * k * sizeof(uint32_t), ob_sc = (size_t)B * k * sizeof(float);
   if (out_bounce) {
-    ESPN_CUDA_TRY(cudaMemcpyAsync(w->out_h, w->out_ids, ob_ids, cudaMemcpyDeviceToHost, s));
-    ESPN_CUDA_TRY(cudaMemcpyAsync(w->out_h + ob_ids, w->out_scores, ob_sc, cudaMemcpyDeviceToHost, s));
-    ESPN_CUDA_TRY(cudaMemcpyAsync(w->out_h + ob_ids + ob_sc, w->out_counts, (size_t)B * sizeof(uint32_t),
+    ESPN_CUDA_TRY(cudaMemcpyAsync(w->out_h, w->opack, 16 + ob_ids + ob_sc + (size_t)B * sizeof(uint32_t),
                                   cudaMemcpyDeviceToHost, s));
   } else if (!out_direct) {
     ESPN_CUDA_TRY(cudaMemcpyAsync(o->ids, w->out_ids, ob_ids, cudaMemcpyDeviceToHost, s));
@@ -1101,18 +1143,19 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     w->async_pending = true;
     return ESPN_OK;
   }
-  ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  if (!out_bounce) ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   if (o->fetch_stats && slot >= 0)
     ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_qstats, w->stage[slot].qstats, (size_t)B * 6 * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
   ESPN_CUDA_TRY(cudaStreamSynchronize(s));
-  ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
-  w->async_pending = false;
   if (out_bounce) {
-    std::memcpy(o->ids, w->out_h, ob_ids);
-    std::memcpy(o->scores, w->out_h + ob_ids, ob_sc);
-    std::memcpy(o->counts, w->out_h + ob_ids + ob_sc, (size_t)B * sizeof(uint32_t));
+    std::memcpy(w->h_err, w->out_h, sizeof(uint32_t));
+    std::memcpy(o->ids, w->out_h + 16, ob_ids);
+    std::memcpy(o->scores, w->out_h + 16 + ob_ids, ob_sc);
+    std::memcpy(o->counts, w->out_h + 16 + ob_ids + ob_sc, (size_t)B * sizeof(uint32_t));
   }
+  if (*w->h_err) ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
+  w->async_pending = false;
   if (o->fetch_stats) {
     for (uint32_t b = 0; b < B; ++b) {
       espn_fetch_stats& f = o->fetch_stats[b];
