@@ -297,6 +297,12 @@ struct espn_gpu_workspace {
     bool used = false;
   } io[2];
   uint8_t* opack = nullptr;          // device: err | out ids | scores | counts
+  // synchronous pageable-buffer calls of a repeating shape replay one CUDA
+  // graph (H2D pack -> plan -> MaxSim -> finalize -> D2H pack) on the caller's stream
+  cudaStream_t gs = nullptr;         // capture stream
+  cudaGraphExec_t sg_exec = nullptr;
+  uint64_t sg_key[5] = {0, 0, 0, 0, 0};
+  uint64_t sg_seen[5] = {0, 0, 0, 0, 0};  // last shape run eagerly (captured on its second call)
   // host input pointers last checked for pinned memory (q32, ids, cls)
   const void* in_key[3] = {nullptr, nullptr, nullptr};
   bool in_pinned[3] = {false, false, false};
@@ -676,6 +682,7 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.done, cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->gs, cudaStreamNonBlocking);
   for (auto& sl : w->slots) {
     if (e == cudaSuccess) e = cudaMallocHost(&sl.cand_off, (B + 1) * sizeof(uint64_t));
     if (e == cudaSuccess) e = cudaMallocHost(&sl.needed, (B + 1) * sizeof(uint32_t));
@@ -709,6 +716,8 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
     if (io.done) cudaEventDestroy(io.done);
   }
   if (w->cs) { cudaStreamSynchronize(w->cs); cudaStreamDestroy(w->cs); }
+  if (w->sg_exec) cudaGraphExecDestroy(w->sg_exec);
+  if (w->gs) cudaStreamDestroy(w->gs);
   cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->n_units);
   cudaFree(w->kprof);
   cudaFree(w->unit_top); cudaFree(w->dedup); cudaFree(w->ff_seen); cudaFree(w->fused_state);
@@ -811,6 +820,48 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   const int pslot = (int)(w->prof_calls % espn_gpu_workspace::kProf);
   if (profile) drain_prof(w, pslot);
 
+  const bool sync_call = !(a->flags & ESPN_RERANK_ASYNC);
+  // Outputs: device pointers (DEVICE_IO); pinned host buffers are written
+  // directly by the kernels (zero-copy, no D2H); other host buffers get a
+  // D2H from the workspace's output arrays.
+  uint32_t* out_ids_k = w->out_ids;
+  float* out_scores_k = w->out_scores;
+  uint32_t* out_counts_k = w->out_counts;
+  bool out_direct = dev_io;
+  bool out_bounce = false;  // synchronous pageable outputs: compact [err | ids | scores | counts], one D2H
+  if (dev_io) {
+    out_ids_k = o->ids;
+    out_scores_k = o->scores;
+    out_counts_k = o->counts;
+  } else {
+    const void* key[3] = {o->ids, o->scores, o->counts};
+    if (!(key[0] == w->zc_key[0] && key[1] == w->zc_key[1] && key[2] == w->zc_key[2])) {
+      bool ok = true;
+      for (int i = 0; i < 3; ++i) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, key[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+            !at.devicePointer) {
+          ok = false;
+          cudaGetLastError();  // clear a sticky "invalid value" for unregistered memory
+          break;
+        }
+        w->zc_dev[i] = at.devicePointer;
+      }
+      for (int i = 0; i < 3; ++i) w->zc_key[i] = key[i];
+      w->zc_ok = ok;
+    }
+    if (w->zc_ok) {
+      out_ids_k = static_cast<uint32_t*>(w->zc_dev[0]);
+      out_scores_k = static_cast<float*>(w->zc_dev[1]);
+      out_counts_k = static_cast<uint32_t*>(w->zc_dev[2]);
+      out_direct = true;
+    } else if (sync_call && w->out_h) {
+      out_bounce = true;
+      out_ids_k = w->out_ids;  // == opack + 16
+      out_scores_k = reinterpret_cast<float*>(w->out_ids + (size_t)B * k);
+      out_counts_k = reinterpret_cast<uint32_t*>(out_scores_k + (size_t)B * k);
+    }
+  }
   // ---- inputs -> device ----
   const uint64_t* cand_off = a->cand_offsets;
   const uint32_t* needed_in = a->needed_counts;
@@ -821,7 +872,6 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   // stream: the slot's previous batch must be done with it, and the compute
   // stream waits for the H2D -- batch n+1's copies overlap batch n's kernels.
   int io_slot = -1;
-  const bool sync_call = !(a->flags & ESPN_RERANK_ASYNC);
   if (!dev_io) {  // which caller buffers are pinned (cached per pointer)
     const void* key[3] = {q32, ids, cls};
     for (int i = 0; i < 3; ++i)
@@ -833,12 +883,27 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
       }
   }
   const bool all_pinned = !dev_io && w->in_pinned[0] && (C == 0 || (w->in_pinned[1] && w->in_pinned[2]));
-  if (sync_call && !dev_io && !dev_off && !all_pinned) {
+  const bool packed = sync_call && !dev_io && !dev_off && !all_pinned;
+  // per-shape CUDA graph of the packed synchronous path (everything the graph
+  // bakes in is in the key; the data it reads lives in fixed pinned/device buffers)
+  const bool graph_ok = packed && out_bounce && !t->tiered && !profile_dev && !o->bow_scores && !w->async_pending &&
+                        !(a->flags & (ESPN_RERANK_WRITE_BOW | ESPN_RERANK_PREFETCHED)) && !(dbg & 0x40000u);
+  uint32_t alpha_bits;
+  std::memcpy(&alpha_bits, &a->alpha, 4);
+  const uint64_t gkey[5] = {(uint64_t)B | ((uint64_t)nq << 32), C, (uint64_t)k | ((uint64_t)a->rerank_count << 32),
+                            (uint64_t)alpha_bits | ((uint64_t)a->flags << 32),
+                            (uint64_t)kern | ((uint64_t)fused << 8) | ((uint64_t)(a->needed_counts != nullptr) << 9) |
+                                ((uint64_t)(uint32_t)unit_docs << 16) | ((uint64_t)(o->fetch_stats != nullptr) << 48)};
+  const bool replay = graph_ok && w->sg_exec && std::equal(gkey, gkey + 5, w->sg_key);
+  const bool capture = graph_ok && !replay && std::equal(gkey, gkey + 5, w->sg_seen);
+  if (graph_ok && !replay && !capture) std::copy(gkey, gkey + 5, w->sg_seen);
+  cudaStream_t user_s = s;
+  if (packed) {
     // synchronous call with pageable buffers: pack every input into the I/O
     // slot's pinned buffer and move it with ONE copy on the compute stream
-    io_slot = (int)(w->io_calls++ % 2);
+    io_slot = graph_ok ? 0 : (int)(w->io_calls++ % 2);  // a graph always uses slot 0
     auto& io = w->io[io_slot];
-    if (io.used) ESPN_CUDA_TRY(cudaEventSynchronize(io.done));  // an earlier ASYNC batch is done with it
+    if (io.used) ESPN_CUDA_TRY(cudaEventSynchronize(io.done));  // an earlier batch is done with it
     auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
     const size_t qb = (size_t)B * nq * t->d * sizeof(float), ib = C * sizeof(uint32_t), cb = C * sizeof(float);
     const size_t o_need = a16((B + 1) * 8), o_q = o_need + a16(B * 4), o_ids = o_q + a16(qb),
@@ -849,6 +914,35 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     if (C) {
       std::memcpy(io.in_h + o_ids, ids, ib);
       std::memcpy(io.in_h + o_cls, cls, cb);
+    }
+    if (replay) {
+      ESPN_CUDA_TRY(cudaGraphLaunch(w->sg_exec, s));
+      ESPN_CUDA_TRY(cudaEventRecord(io.done, s));
+      io.used = true;
+      ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+      const size_t ob_ids = (size_t)B * k * sizeof(uint32_t), ob_sc = (size_t)B * k * sizeof(float);
+      std::memcpy(w->h_err, w->out_h, sizeof(uint32_t));
+      std::memcpy(o->ids, w->out_h + 16, ob_ids);
+      std::memcpy(o->scores, w->out_h + 16 + ob_ids, ob_sc);
+      std::memcpy(o->counts, w->out_h + 16 + ob_ids + ob_sc, (size_t)B * sizeof(uint32_t));
+      if (*w->h_err) {
+        ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
+        ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+      }
+      if (o->fetch_stats)
+        for (uint32_t b = 0; b < B; ++b) {  // HBM-resident table: every needed row is resident
+          const uint64_t n = a->cand_offsets[b + 1] - a->cand_offsets[b];
+          const uint64_t need = std::min<uint64_t>(n, a->needed_counts ? a->needed_counts[b] : a->rerank_count);
+          o->fetch_stats[b] = espn_fetch_stats{need, need, 0, 0, 0, 0};
+        }
+      w->counters.batches += 1;
+      w->counters.queries += B;
+      w->counters.kernel_launches += 3;
+      return err_bits_to_status(*w->h_err);
+    }
+    if (capture) {
+      ESPN_CUDA_TRY(cudaStreamBeginCapture(w->gs, cudaStreamCaptureModeRelaxed));
+      s = w->gs;
     }
     ESPN_CUDA_TRY(cudaMemcpyAsync(io.dpack, io.in_h, total, cudaMemcpyHostToDevice, s));
     cand_off = reinterpret_cast<const uint64_t*>(io.dpack);
@@ -901,47 +995,6 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     }
     ESPN_CUDA_TRY(cudaEventRecord(io.in_ready, w->cs));
     ESPN_CUDA_TRY(cudaStreamWaitEvent(s, io.in_ready, 0));
-  }
-  // Outputs: device pointers (DEVICE_IO); pinned host buffers are written
-  // directly by the kernels (zero-copy, no D2H); other host buffers get a
-  // D2H from the workspace's output arrays.
-  uint32_t* out_ids_k = w->out_ids;
-  float* out_scores_k = w->out_scores;
-  uint32_t* out_counts_k = w->out_counts;
-  bool out_direct = dev_io;
-  bool out_bounce = false;  // synchronous pageable outputs: compact [err | ids | scores | counts], one D2H
-  if (dev_io) {
-    out_ids_k = o->ids;
-    out_scores_k = o->scores;
-    out_counts_k = o->counts;
-  } else {
-    const void* key[3] = {o->ids, o->scores, o->counts};
-    if (!(key[0] == w->zc_key[0] && key[1] == w->zc_key[1] && key[2] == w->zc_key[2])) {
-      bool ok = true;
-      for (int i = 0; i < 3; ++i) {
-        cudaPointerAttributes at{};
-        if (cudaPointerGetAttributes(&at, key[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
-            !at.devicePointer) {
-          ok = false;
-          cudaGetLastError();  // clear a sticky "invalid value" for unregistered memory
-          break;
-        }
-        w->zc_dev[i] = at.devicePointer;
-      }
-      for (int i = 0; i < 3; ++i) w->zc_key[i] = key[i];
-      w->zc_ok = ok;
-    }
-    if (w->zc_ok) {
-      out_ids_k = static_cast<uint32_t*>(w->zc_dev[0]);
-      out_scores_k = static_cast<float*>(w->zc_dev[1]);
-      out_counts_k = static_cast<uint32_t*>(w->zc_dev[2]);
-      out_direct = true;
-    } else if (sync_call && w->out_h) {
-      out_bounce = true;
-      out_ids_k = w->out_ids;  // == opack + 16
-      out_scores_k = reinterpret_cast<float*>(w->out_ids + (size_t)B * k);
-      out_counts_k = reinterpret_cast<uint32_t*>(out_scores_k + (size_t)B * k);
-    }
   }
   // the device error word is sticky across un-synced ASYNC batches; it is
   // read and cleared by the synchronising call (or espn_gpu_workspace_sync)
@@ -1114,7 +1167,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     ++w->prof_calls;
   }
 
-  if (io_slot >= 0) {  // every kernel reading the I/O slot is enqueued
+  if (io_slot >= 0 && !capture) {  // every kernel reading the I/O slot is enqueued
     ESPN_CUDA_TRY(cudaEventRecord(w->io[io_slot].done, s));
     w->io[io_slot].used = true;
   }
@@ -1142,6 +1195,24 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   if (a->flags & ESPN_RERANK_ASYNC) {
     w->async_pending = true;
     return ESPN_OK;
+  }
+  if (capture) {  // the graph now holds this call's work: instantiate, then run it on the caller's stream
+    cudaGraph_t graph = nullptr;
+    ESPN_CUDA_TRY(cudaStreamEndCapture(w->gs, &graph));
+    if (w->sg_exec) {
+      cudaGraphExecDestroy(w->sg_exec);
+      w->sg_exec = nullptr;
+    }
+    const cudaError_t ge = cudaGraphInstantiate(&w->sg_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ge != cudaSuccess) return fail(ESPN_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ge));
+    std::copy(gkey, gkey + 5, w->sg_key);
+    s = user_s;
+    ESPN_CUDA_TRY(cudaGraphLaunch(w->sg_exec, s));
+    // (an event recorded during capture is only a capture dependency: record
+    // the slot's completion on the caller's stream, after the graph)
+    ESPN_CUDA_TRY(cudaEventRecord(w->io[io_slot].done, s));
+    w->io[io_slot].used = true;
   }
   if (!out_bounce) ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   if (o->fetch_stats && slot >= 0)

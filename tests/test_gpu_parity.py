@@ -601,3 +601,29 @@ def test_device_offsets_graph_replay(cuda_ok, partial):
         assert np.array_equal(gs.view(np.uint32), want[1].view(np.uint32))
     rr.close()
     store.close()
+
+
+def test_sync_graph_replay_fresh_data_and_errors(oracle, cuda_ok):
+    """Synchronous pageable-buffer calls of a repeating shape run as a replayed
+    CUDA graph from the second call on: every call must see its own inputs,
+    interleaved shapes must re-capture, and device-side errors must surface."""
+    rp, codes = synth.make_table(6000, 32, 1, 63, seed=81)
+    store = api.GpuStore(rp, codes, 32)
+    rr = api.Reranker(store, 8, 8 * 400, 32)
+    cfg = api.PipelineConfig(rerank_count=400, final_k=10)
+    for i in range(6):
+        B = 4 if i % 3 else 3  # shapes 3, 4, 4, 3, 4, 4: captures, replays and re-captures
+        q, src = synth.make_queries(rp, codes, 32, B, nq=32, seed=90 + i)
+        ids, cls, off = synth.make_candidates(6000, B, 400, src=src, seed=100 + i)
+        check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
+        gi, gs, gc, _ = rr.rerank_arrays(q, ids, cls, off, cfg)
+        assert np.array_equal(gi[:, 0], src.astype(np.uint32)), i
+    bad = ids.copy()
+    bad[5] = bad[9]  # duplicate candidate -> InvalidInputError from the device check
+    for _ in range(3):
+        with pytest.raises(api.InvalidInputError):
+            rr.rerank_arrays(q, bad, cls, off, cfg)
+        gi, _, _, _ = rr.rerank_arrays(q, ids, cls, off, cfg)  # and the next call is clean
+        assert np.array_equal(gi[:, 0], src.astype(np.uint32))
+    rr.close()
+    store.close()
