@@ -204,6 +204,11 @@ typedef struct {
   espn_fetch_stats* fetch_stats; /* optional HOST array of B (synchronous calls) */
 } espn_rerank_out;
 
+/* Synchronous calls with pageable host buffers move their inputs with one
+ * packed copy and their results with one; when the same shape (B, C, q, k, R,
+ * alpha, flags) repeats on a workspace, the call replays a CUDA graph of its
+ * device work captured on the second such call (results are identical; the
+ * graph runs on `stream`). */
 ESPN_API int espn_gpu_rerank(espn_gpu_table* table, espn_gpu_workspace* ws,
                     const espn_rerank_args* args, espn_rerank_out* out, void* stream);
 

@@ -10,7 +10,7 @@ namespace espn_k {
 //   1 no epilogue work   2 no MMAs   4 no row copies   8 CTA-0 role trace
 //   32 no doc-boundary scan   64 quarter-0 MMAs only   128 top-k: no dedup
 //   256 device timeline (below)   512 separate top-k kernel
-//   0x10000 finalize as a programmatic dependent of MaxSim
+//   0x10000 finalize as a programmatic dependent of MaxSim   0x40000 no graph for synchronous host calls
 // ESPN_DEBUG bit 256: per-kernel device timeline of the re-rank step (first
 // CTA start, last CTA end, globaltimer ns) -- slot 0 plan, 1 MaxSim, 2 top-k.
 // Read/reset through espn_gpu_debug_timeline (profiling only).
