@@ -303,6 +303,7 @@ struct espn_gpu_workspace {
   cudaGraphExec_t sg_exec = nullptr;
   uint64_t sg_key[5] = {0, 0, 0, 0, 0};
   uint64_t sg_seen[5] = {0, 0, 0, 0, 0};  // last shape run eagerly (captured on its second call)
+  bool capturing = false;            // a capture left open by an error return
   // host input pointers last checked for pinned memory (q32, ids, cls)
   const void* in_key[3] = {nullptr, nullptr, nullptr};
   bool in_pinned[3] = {false, false, false};
@@ -898,6 +899,13 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   const bool capture = graph_ok && !replay && std::equal(gkey, gkey + 5, w->sg_seen);
   if (graph_ok && !replay && !capture) std::copy(gkey, gkey + 5, w->sg_seen);
   cudaStream_t user_s = s;
+  if (w->capturing) {  // an earlier call failed inside its capture: close it, drop the graph
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(w->gs, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    w->capturing = false;
+  }
   if (packed) {
     // synchronous call with pageable buffers: pack every input into the I/O
     // slot's pinned buffer and move it with ONE copy on the compute stream
@@ -942,6 +950,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     }
     if (capture) {
       ESPN_CUDA_TRY(cudaStreamBeginCapture(w->gs, cudaStreamCaptureModeRelaxed));
+      w->capturing = true;
       s = w->gs;
     }
     ESPN_CUDA_TRY(cudaMemcpyAsync(io.dpack, io.in_h, total, cudaMemcpyHostToDevice, s));
@@ -1198,6 +1207,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
   if (capture) {  // the graph now holds this call's work: instantiate, then run it on the caller's stream
     cudaGraph_t graph = nullptr;
+    w->capturing = false;
     ESPN_CUDA_TRY(cudaStreamEndCapture(w->gs, &graph));
     if (w->sg_exec) {
       cudaGraphExecDestroy(w->sg_exec);
