@@ -185,10 +185,12 @@ def maxsim_batch(t: OracleTable, q, cand_ids, cand_off, nthreads=None):
     q = np.ascontiguousarray(q, np.float32)
     ids = np.ascontiguousarray(cand_ids, np.uint32)
     off = np.ascontiguousarray(cand_off, np.uint64)
-    out = np.full(ids.size, np.nan, np.float32)
-    st = lib().eo_maxsim_batch(C.byref(t.s), _p(q), q.shape[0], q.shape[1], _p(ids), _p(off), _p(out),
+    # never NULL: the C batch runner tells a MaxSim job from a re-rank job by a
+    # non-NULL output pointer, so an all-empty batch still needs one
+    out = np.full(max(ids.size, 1), np.nan, np.float32)
+    st = lib().eo_maxsim_batch(C.byref(t.s), _p(q), q.shape[0], q.shape[1], _p(ids), _p(off), out.ctypes.data,
                                nthreads or os.cpu_count() or 1)
-    return st, out
+    return st, out[:ids.size]
 
 
 def ref_half():
