@@ -357,7 +357,8 @@ def run_ours(args, cfg):
             row_bytes=row_bytes, n_pairs=int(need.sum()), h_ids=ids, h_cls=cls, h_q=bt["q"], glob=bt))
     max_list = max(int(np.diff(db["off"]).max()) for db in dev_batches)
     P = 2 * B_q * k + B_q  # packed [ids | scores | counts] per rank
-    flags = L.ESPN_RERANK_DEVICE_IO | L.ESPN_RERANK_DEVICE_OFFSETS | L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_PROFILE
+    QP = {"auto": 0, "split": L.ESPN_RERANK_QUERY_SPLIT, "rounded": L.ESPN_RERANK_QUERY_ROUNDED}[args.query_precision]
+    flags = L.ESPN_RERANK_DEVICE_IO | L.ESPN_RERANK_DEVICE_OFFSETS | L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_PROFILE | QP
 
     class Lane:
         """One batch in flight: its own workspace, stream, output buffers, NCCL
@@ -540,7 +541,7 @@ def run_ours(args, cfg):
         j = (i // NL) % 2
         e2e_ev[i % NL][j].synchronize()
         ln.enqueue(dev_batches[i % n_batches], ln.stream.cuda_stream,
-                   flags=L.ESPN_RERANK_ASYNC if world == 1 else L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_DEVICE_IO,
+                   flags=(L.ESPN_RERANK_ASYNC if world == 1 else L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_DEVICE_IO) | QP,
                    host=(e2e_in[i % n_batches] if world == 1 else _dev_inputs(i), h_outs[i % NL][j]))
         e2e_ev[i % NL][j].record(ln.stream)
 
@@ -663,7 +664,12 @@ def run_ours(args, cfg):
                    "l2": l2_note,
                    "launch": "one CUDA graph per batch (device-planned: plan -> tcgen05 MaxSim with fused ranking -> "
                              "finalize merge); %d batches in flight on separate streams/workspaces" % NL,
-                   "kernel": "tcgen05 (auto)"},
+                   "kernel": "tcgen05 (auto)",
+                   "query_precision": {"auto": "fp32 query as hi + lo in the table dtype (two MMAs per K-step)"
+                                               if not (d == 128 and cfg["dtype"] == "f16") else
+                                               "fp32 query rounded to f16 (d=128 default)",
+                                       "split": "fp32 query as hi + lo in the table dtype (two MMAs per K-step)",
+                                       "rounded": "fp32 query rounded to the table dtype"}[args.query_precision]},
         "p50_batch_ms": p50, "p99_batch_ms": p99,
         "gather_hbm_gbs": gather_gbs,
         "e2e": {"value": q_total / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
@@ -716,7 +722,7 @@ def cpu_baseline(cfg, store, batches, dev, args):
     rows = torch.empty(tot * cfg["d"], dtype=torch.int16, device=dev)
     assert lib.espn_gpu_gather(store.handle, d_ids.data_ptr(), uniq.size, rows.data_ptr(), rp.data_ptr(), tot, None) == 0
     t = oracle_py.OracleTable(rp.cpu().numpy().astype(np.uint64), rows.cpu().numpy().view(np.uint16), cfg["d"])
-    qr = oracle_py.round_to(q)
+    qr = np.ascontiguousarray(q, np.float32)  # the reference's fp32 query (types.hpp:33-44)
     ncores = os.cpu_count() or 1
     # the sample is re-ranked repeatedly until >= cpu_seconds of CPU work (a
     # stable figure), all host threads; then one thread for a third of that
@@ -773,7 +779,7 @@ def run_reference(args, cfg):
     ncores = os.cpu_count() or 1
     prepared = []
     for b in batches:
-        prepared.append((oracle_py.round_to(b["q"]), np.searchsorted(uniq, b["ids"]).astype(np.uint32), b["cls"], b["off"]))
+        prepared.append((np.ascontiguousarray(b["q"], np.float32), np.searchsorted(uniq, b["ids"]).astype(np.uint32), b["cls"], b["off"]))
 
     def step(i):
         q, ids, cls, off = prepared[i % n_b]
@@ -817,6 +823,7 @@ def main():
                     help="CPU-baseline sample length (all host threads; one thread runs a third of it)")
     ap.add_argument("--inflight", type=int, default=3,
                     help="batches in flight (one stream + workspace each); the latency percentiles use one")
+    ap.add_argument("--query-precision", default="auto", choices=["auto", "split", "rounded"])
     ap.add_argument("--emulate-shards", type=int, default=0,
                     help="1 GPU: run shard 0 of an N-way doc-id sharding (the per-GPU share of an N-GPU run)")
     args = ap.parse_args()

@@ -151,6 +151,13 @@ ESPN_API int espn_gpu_workspace_destroy(espn_gpu_workspace* ws);
 #define ESPN_RERANK_SEPARATE_TOPK 0x80u /* rank in a separate top-k kernel instead of inside the
                                          tcgen05 MaxSim kernel (the fused path is the default when
                                          final_k <= 32; results are identical) */
+#define ESPN_RERANK_QUERY_ROUNDED 0x100u /* legacy precision: the fp32 query is rounded to the table dtype
+                                         before MaxSim (one MMA per K-step).  Default: the fp32 query is
+                                         honoured (types.hpp:33-44) -- CUDA-core path exactly, tcgen05 path
+                                         as q = hi + lo in the table dtype (two MMAs per K-step; 22 / 16
+                                         significant bits for f16 / bf16), except f16 tables at d = 128,
+                                         which round unless ESPN_RERANK_QUERY_SPLIT */
+#define ESPN_RERANK_QUERY_SPLIT 0x200u  /* tcgen05: force the hi + lo query for every dim and dtype */
 #define ESPN_RERANK_DEVICE_OFFSETS 0x20u /* cand_offsets / needed_counts are DEVICE pointers (needs
                                          DEVICE_IO): the batch is planned on the device, the call has
                                          no host-side loop, no host sync with ASYNC, and is CUDA-graph

@@ -5,7 +5,7 @@
  * Follows, function by function:
  *   codecs        proj/include/espn/half.hpp:11-76 (IEEE semantics; the reference's
  *                 subnormal defects are documented in SURVEY.md §8(a3) and pinned
- *                 by tests/test_oracle_golden.py)
+ *                 by tests/test_oracle.py against tests/golden/half_ref_codec.npz)
  *   dot/maxsim    proj/include/espn/scoring.hpp:7-10, 20-21
  *   aggregate     scoring.hpp:12-14
  *   rank          scoring.hpp:16-18; types.hpp:51-55

@@ -12,8 +12,9 @@
  * keep -ffp-contract=off so a*b+c is never fused.
  *
  * Parity pinning: the fp16 codec is checked against the reference's own
- * half.hpp compiled in oracle/_ref (all 65,536 codes; see oracle/build.sh and
- * tests/golden/), and scoring/rank/aggregate against SPEC.md's known-answer
+ * half.hpp compiled in oracle/_ref (all 65,536 codes; recipe `make -C oracle ref`,
+ * fixture tests/golden/half_ref_codec.npz made by tests/golden/make_golden.py,
+ * checked in tests/test_oracle.py), and scoring/rank/aggregate against SPEC.md's known-answer
  * examples.
  */
 #ifndef ESPN_ORACLE_H

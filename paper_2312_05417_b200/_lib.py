@@ -38,6 +38,8 @@ ESPN_RERANK_PROFILE = 0x10
 ESPN_RERANK_DEVICE_OFFSETS = 0x20
 ESPN_RERANK_PREFETCHED = 0x40
 ESPN_RERANK_SEPARATE_TOPK = 0x80
+ESPN_RERANK_QUERY_ROUNDED = 0x100
+ESPN_RERANK_QUERY_SPLIT = 0x200
 
 
 class TableDesc(C.Structure):

@@ -276,6 +276,7 @@ def _ptr(a) -> Optional[int]:
 
 
 _DTYPES = {"f16": L.ESPN_DTYPE_F16, "fp16": L.ESPN_DTYPE_F16, "bf16": L.ESPN_DTYPE_BF16}
+_QPREC = {"auto": 0, "split": L.ESPN_RERANK_QUERY_SPLIT, "rounded": L.ESPN_RERANK_QUERY_ROUNDED}
 _KERNELS = {"auto": L.ESPN_KERNEL_AUTO, "tcgen05": L.ESPN_KERNEL_TCGEN05, "simt": L.ESPN_KERNEL_SIMT}
 
 
@@ -459,11 +460,14 @@ class Reranker:
     def rerank_arrays(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig,
                       kernel: str = "auto", device_io: bool = False, write_bow: bool = False,
                       out=None, stream=None, sync: bool = True, needed_counts=None, prefetched: bool = False,
-                      fetch_stats: bool = False, separate_topk: bool = False):
+                      fetch_stats: bool = False, separate_topk: bool = False, query_precision: str = "auto"):
         """Batched stages 3-6.  query_tokens (B, q, d) fp32; cand_* CSR over
         queries with cand_offsets (B+1, host uint64).  Host numpy arrays by
         default (copied in and out inside the call); device torch tensors
-        with device_io=True.  Returns (ids[B,k], scores[B,k], counts[B], bow)."""
+        with device_io=True.  Returns (ids[B,k], scores[B,k], counts[B], bow).
+        query_precision: "auto" (the fp32 query as given; tcgen05 as hi + lo,
+        espn_gpu.h ESPN_RERANK_QUERY_*), "split" (hi + lo everywhere) or
+        "rounded" (query rounded to the table dtype first)."""
         offs = np.ascontiguousarray(np.asarray(cand_offsets, dtype=np.uint64))
         B = offs.shape[0] - 1
         k = int(config.final_k)
@@ -478,9 +482,25 @@ class Reranker:
                        torch.empty((int(offs[-1]),), dtype=torch.float32, device=dev) if write_bow else None)
         else:
             query_tokens = np.ascontiguousarray(query_tokens, dtype=np.float32)
-            cand_ids = np.ascontiguousarray(cand_ids, dtype=np.uint32)
-            cand_cls = np.ascontiguousarray(cand_cls, dtype=np.float32)
-            nq = int(query_tokens.shape[1]) if query_tokens.ndim == 3 else int(query_tokens.shape[0] // max(B, 1) // self.store.d)
+            cand_ids = np.ascontiguousarray(cand_ids, dtype=np.uint32).ravel()
+            cand_cls = np.ascontiguousarray(cand_cls, dtype=np.float32).ravel()
+            # the C side trusts these sizes (it copies B*q*d and C entries)
+            if B < 0 or (B and int(offs[0]) != 0) or np.any(np.diff(offs.astype(np.int64)) < 0):
+                raise InvalidInputError("cand_offsets must start at 0 and be non-decreasing")
+            n_c = int(offs[-1]) if B else 0
+            if cand_ids.size < n_c or cand_cls.size < n_c:
+                raise InvalidInputError(f"cand_ids / cand_cls hold {cand_ids.size} / {cand_cls.size} entries, "
+                                        f"cand_offsets needs {n_c}")
+            if B == 0:
+                nq = int(query_tokens.shape[1]) if query_tokens.ndim == 3 and query_tokens.shape[1] else 1
+            elif query_tokens.ndim == 3:
+                if query_tokens.shape[0] != B or query_tokens.shape[2] != self.store.d:
+                    raise InvalidInputError(f"query_tokens shape {query_tokens.shape} != (B={B}, q, d={self.store.d})")
+                nq = int(query_tokens.shape[1])
+            else:
+                if query_tokens.size == 0 or query_tokens.size % (B * self.store.d):
+                    raise InvalidInputError("query_tokens must hold B * q * d values")
+                nq = int(query_tokens.size // B // self.store.d)
             if out is None:
                 out = (np.zeros((B, k), np.uint32), np.zeros((B, k), np.float32), np.zeros(B, np.uint32),
                        np.full(int(offs[-1]), np.nan, np.float32) if write_bow else None)
@@ -497,6 +517,7 @@ class Reranker:
             flags |= L.ESPN_RERANK_PREFETCHED
         if separate_topk:
             flags |= L.ESPN_RERANK_SEPARATE_TOPK
+        flags |= _QPREC[query_precision]
         args = L.RerankArgs(n_queries=B, n_query_tokens=nq, query_tokens=_ptr(query_tokens),
                             cand_ids=_ptr(cand_ids), cand_cls=_ptr(cand_cls), cand_offsets=offs.ctypes.data,
                             rerank_count=int(config.rerank_count), final_k=k, alpha=float(config.alpha),

@@ -213,6 +213,7 @@ struct MaxSimParams {
   uint32_t unit_docs;          // docs per work unit (<= kUnitMax)
   const uint32_t* n_units;     // device: total work units (written by plan_kernel)
   uint32_t bf16;               // table dtype
+  uint32_t qround;             // SIMT: round the query to the table dtype first (ESPN_RERANK_QUERY_ROUNDED)
   uint32_t dbg;                // profiling knobs (ESPN_DEBUG env; 0 in production)
   // ESPN_RERANK_PROFILE: device-timed kernel duration (globaltimer, min start
   // over CTAs -> end of the last CTA), accumulated as {sum_ns, launches,

@@ -5,6 +5,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -109,15 +110,27 @@ int tc_unit_docs_rt(uint32_t d, uint32_t max_t) {
   }
 }
 
-template <int D>
+// cudaFuncSetAttribute is per DEVICE: one process may drive several GPUs
+// through the C-ABI, so each (kernel, device) pair is configured once.
+template <typename K>
+cudaError_t smem_attr_once(K* kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+template <int D, bool SPLIT>
 cudaError_t launch_tc(const MaxSimParams& p, int num_sms, cudaStream_t s, bool pdl) {
-  using L = TcLayout<D>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(maxsim_tc_kernel<D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_BYTES);
+  using L = TcLayout<D, SPLIT>;
+  static std::atomic<uint64_t> attr_set{0};
+  {
+    cudaError_t e = smem_attr_once(maxsim_tc_kernel<D, SPLIT>, L::SMEM_BYTES, attr_set);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   // persistent: one CTA per SM; the unit count is read on the device.  As a
   // programmatic dependent of plan_kernel (pdl) its prologue overlaps the plan.
@@ -131,17 +144,28 @@ cudaError_t launch_tc(const MaxSimParams& p, int num_sms, cudaStream_t s, bool p
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&lc, maxsim_tc_kernel<D>, p);
+  return cudaLaunchKernelEx(&lc, maxsim_tc_kernel<D, SPLIT>, p);
 }
 
-cudaError_t launch_tc_rt(uint32_t d, const MaxSimParams& p, int num_sms, cudaStream_t s, bool pdl) {
-  switch (d) {
-    case 16: return launch_tc<16>(p, num_sms, s, pdl);
-    case 32: return launch_tc<32>(p, num_sms, s, pdl);
-    case 64: return launch_tc<64>(p, num_sms, s, pdl);
-    case 128: return launch_tc<128>(p, num_sms, s, pdl);
+cudaError_t launch_tc_rt(uint32_t d, bool split, const MaxSimParams& p, int num_sms, cudaStream_t s, bool pdl) {
+  switch (d * 2 + (split ? 1 : 0)) {
+    case 32: return launch_tc<16, false>(p, num_sms, s, pdl);
+    case 33: return launch_tc<16, true>(p, num_sms, s, pdl);
+    case 64: return launch_tc<32, false>(p, num_sms, s, pdl);
+    case 65: return launch_tc<32, true>(p, num_sms, s, pdl);
+    case 128: return launch_tc<64, false>(p, num_sms, s, pdl);
+    case 129: return launch_tc<64, true>(p, num_sms, s, pdl);
+    case 256: return launch_tc<128, false>(p, num_sms, s, pdl);
+    case 257: return launch_tc<128, true>(p, num_sms, s, pdl);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// Query precision of the tcgen05 path (ESPN_RERANK_QUERY_* in espn_gpu.h).
+bool tc_query_split(uint32_t d, uint32_t dtype, uint32_t flags) {
+  if (flags & ESPN_RERANK_QUERY_ROUNDED) return false;
+  if (flags & ESPN_RERANK_QUERY_SPLIT) return true;
+  return !(d == 128 && dtype == ESPN_DTYPE_F16);
 }
 
 template <int D>
@@ -173,16 +197,12 @@ size_t topk_smem_bytes() {
 }
 
 cudaError_t ensure_topk_attr() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)topk_smem_bytes());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)topk_smem_bytes());
-  if (e != cudaSuccess) return e;
-  done = true;
-  return cudaSuccess;
+  static std::atomic<uint64_t> d1{0}, d2{0}, d3{0}, d4{0};
+  cudaError_t e = smem_attr_once(topk_kernel, (int)topk_smem_bytes(), d1);
+  if (e == cudaSuccess) e = smem_attr_once(merge_topk_kernel, (int)topk_smem_bytes(), d2);
+  if (e == cudaSuccess) e = smem_attr_once(topk_cta_kernel<16>, 8192 * 8 + 8 * 32 * 8, d3);
+  if (e == cudaSuccess) e = smem_attr_once(topk_cta_kernel<32>, 8192 * 8 + 8 * 32 * 8, d4);
+  return e;
 }
 
 bool layout_tiled(uint32_t d) { return d == 16 || d == 32 || d == 64 || d == 128; }
@@ -341,6 +361,20 @@ void drain_prof(espn_gpu_workspace* w, int i) {
 }  // namespace
 
 namespace {
+// Staging slots of a tiered workspace: pf_q lists the slots holding a
+// prefetch not yet consumed by its PREFETCHED batch; any other staging must
+// use the other slot, or it would overwrite that prefetch.
+int peek_free_slot(const espn_gpu_workspace* w) {
+  if (w->pf_count >= 2) return -1;
+  int s = w->next_slot;
+  if (w->pf_count == 1 && w->pf_q[0] == s) s ^= 1;
+  return s;
+}
+int take_free_slot(espn_gpu_workspace* w) {
+  const int s = peek_free_slot(w);
+  if (s >= 0) w->next_slot = s ^ 1;
+  return s;
+}
 // Splits an open table into an HBM tier (resident docs, compacted) and a
 // pinned-host tier (the rest), both in the tile layout; see espn_table_desc.
 int tier_table(espn_gpu_table* t, const uint8_t* resident, const uint64_t* host_row_ptr) {
@@ -642,7 +676,8 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     }
   }
   if (e == cudaSuccess) e = cudaMallocHost(&w->h_qstats, B * 6 * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMallocHost(&w->out_h, (size_t)B * kMaxK * 8 + (size_t)B * 4);
+  // same size as opack ([err 16 B | ids | scores | counts]): the bounce receives the whole pack
+  if (e == cudaSuccess) e = cudaMallocHost(&w->out_h, 16 + (size_t)B * kMaxK * 8 + (size_t)B * 4);
   w->max_list = desc->max_list ? desc->max_list : (uint32_t)std::min<size_t>(C, 4096);
   // fused top-k state; the dedup hash is 8x the declared list (one-probe
   // inserts), at most 32K slots (lists up to 16K candidates)
@@ -818,6 +853,10 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   // lists; ESPN_DEBUG bit 512 / ESPN_RERANK_SEPARATE_TOPK: separate top-k kernel.
   const bool fused = tc && k <= (uint32_t)kFusedMaxK && w->dedup != nullptr && 2ull * max_list <= w->hash_slots &&
                      !(a->flags & ESPN_RERANK_SEPARATE_TOPK) && !(dbg & 512u);
+  // dedup hash of the separate top-k kernel, sized by the longest scored list
+  // (part of the graph key: a captured launch bakes it in)
+  uint32_t topk_hs = 64;
+  while (topk_hs < 2 * max_list) topk_hs <<= 1;
   const int pslot = (int)(w->prof_calls % espn_gpu_workspace::kProf);
   if (profile) drain_prof(w, pslot);
 
@@ -894,7 +933,8 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   const uint64_t gkey[5] = {(uint64_t)B | ((uint64_t)nq << 32), C, (uint64_t)k | ((uint64_t)a->rerank_count << 32),
                             (uint64_t)alpha_bits | ((uint64_t)a->flags << 32),
                             (uint64_t)kern | ((uint64_t)fused << 8) | ((uint64_t)(a->needed_counts != nullptr) << 9) |
-                                ((uint64_t)(uint32_t)unit_docs << 16) | ((uint64_t)(o->fetch_stats != nullptr) << 48)};
+                                ((uint64_t)(uint32_t)unit_docs << 16) | ((uint64_t)__builtin_ctz(topk_hs) << 32) |
+                                ((uint64_t)(o->fetch_stats != nullptr) << 48)};
   const bool replay = graph_ok && w->sg_exec && std::equal(gkey, gkey + 5, w->sg_key);
   const bool capture = graph_ok && !replay && std::equal(gkey, gkey + 5, w->sg_seen);
   if (graph_ok && !replay && !capture) std::copy(gkey, gkey + 5, w->sg_seen);
@@ -1047,9 +1087,8 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
         if (ss) return ss;
       }
     } else {
-      if (w->pf_count == 2) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
-      slot = w->next_slot;
-      w->next_slot ^= 1;
+      slot = take_free_slot(w);
+      if (slot < 0) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
       const int ss = launch_stage(t, w, slot, cand_off, needed_in, ids, B, a->rerank_count, s, false);
       if (ss) return ss;
     }
@@ -1078,6 +1117,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   mp.unit_docs = (uint32_t)std::max(unit_docs, 1);
   mp.n_units = w->n_units;
   mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
+  mp.qround = (a->flags & ESPN_RERANK_QUERY_ROUNDED) ? 1u : 0u;
   mp.dbg = dbg;
   mp.prof = (profile_dev && tc) ? w->kprof : nullptr;
   if (fused) {
@@ -1095,7 +1135,8 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     mp.max_queries = w->max_queries;
   }
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
-  cudaError_t e = tc ? launch_tc_rt(t->d, mp, t->num_sms, s, /*pdl=*/slot < 0 && !profile)
+  cudaError_t e = tc ? launch_tc_rt(t->d, tc_query_split(t->d, t->dtype, a->flags), mp, t->num_sms, s,
+                                    /*pdl=*/slot < 0 && !profile)
                      : launch_simt_rt(t->d, mp, t->num_sms, s);
   if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
   if (slot >= 0) {  // the slot may be re-staged once this MaxSim finished
@@ -1142,16 +1183,9 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     // CTA-per-query fast path when final_k <= 32 and the dedup hash fits;
     // launched as a programmatic dependent of MaxSim (its id-only dedup
     // prologue overlaps the MaxSim tail)
-    uint32_t hs = 64;
-    while (hs < 2 * max_list) hs <<= 1;
+    const uint32_t hs = topk_hs;
     if (k <= 32 && hs <= 8192) {
       const size_t smem = (size_t)hs * 8 + 8 * 32 * 8;
-      static bool attr = false;
-      if (!attr) {
-        ESPN_CUDA_TRY(cudaFuncSetAttribute(topk_cta_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8 + 8 * 32 * 8));
-        ESPN_CUDA_TRY(cudaFuncSetAttribute(topk_cta_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8 + 8 * 32 * 8));
-        attr = true;
-      }
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3(B);
       lc.blockDim = dim3(kTopkCtaThreads);
@@ -1266,8 +1300,7 @@ int espn_gpu_prefetch(espn_gpu_table* t, espn_gpu_workspace* w, const espn_reran
   if (w->pf_count == 2) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
   DeviceGuard g(t->device);
   cudaStream_t s = static_cast<cudaStream_t>(side_stream);
-  const int slot = w->next_slot;
-  w->next_slot ^= 1;
+  const int slot = take_free_slot(w);
   auto& st = w->stage[slot];
   const uint64_t* off = a->cand_offsets;
   const uint32_t* need = a->needed_counts;
@@ -1305,7 +1338,7 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
   if (w->pf_count == 2) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
   DeviceGuard g(t->device);
   cudaStream_t s = static_cast<cudaStream_t>(side_stream);
-  const int slot = w->next_slot;
+  const int slot = peek_free_slot(w);
   auto& st = w->stage[slot];
   const uint64_t* off = hint_offsets;
   const bool dev_ids = (flags & ESPN_RERANK_DEVICE_IO) != 0;
@@ -1340,7 +1373,7 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
     ESPN_CUDA_TRY(cudaMemsetAsync(w->hint_map, 0, t->n_docs * sizeof(uint64_t), s));
     w->hint_epoch = 1;
   }
-  w->next_slot ^= 1;
+  w->next_slot = slot ^ 1;
   if (st.used) ESPN_CUDA_TRY(cudaStreamWaitEvent(s, st.free_ev, 0));  // previous reader done
   ESPN_CUDA_TRY(cudaMemsetAsync(st.cursor, 0, sizeof(unsigned long long), s));
   ESPN_CUDA_TRY(cudaMemsetAsync(st.qstats, 0, (size_t)B * 6 * sizeof(unsigned long long), s));

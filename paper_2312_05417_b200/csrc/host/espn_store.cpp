@@ -94,7 +94,24 @@ int load_manifest(const char* base, espn_store_header* h, std::vector<espn_manif
     return fail(ESPN_E_FORMAT, "unsupported manifest header (version / d / value_width / alignment): " + mp);
   }
   if (recs) {
-    recs->resize(count);
+    // the untrusted count must match the file size before anything is sized by it
+    if (std::fseek(f, 0, SEEK_END) != 0) {
+      std::fclose(f);
+      return fail(ESPN_E_IO, "cannot seek " + mp);
+    }
+    const long fsz = std::ftell(f);
+    if (fsz < 0 || (uint64_t)fsz < kHeaderBytes || count != ((uint64_t)fsz - kHeaderBytes) / sizeof(espn_manifest_record) ||
+        ((uint64_t)fsz - kHeaderBytes) % sizeof(espn_manifest_record) != 0) {
+      std::fclose(f);
+      return fail(ESPN_E_FORMAT, "manifest record count does not match its file size: " + mp);
+    }
+    std::fseek(f, (long)kHeaderBytes, SEEK_SET);
+    try {
+      recs->resize(count);
+    } catch (const std::exception&) {
+      std::fclose(f);
+      return fail(ESPN_E_FORMAT, "manifest record count too large: " + mp);
+    }
     if (count && std::fread(recs->data(), sizeof(espn_manifest_record), count, f) != count) {
       std::fclose(f);
       return fail(ESPN_E_FORMAT, "manifest truncated: " + mp);

@@ -15,10 +15,10 @@ namespace espn_k {
 
 // ============================================================================
 // CUDA-core MaxSim.  One warp per (query, candidate) pair range; lane i owns
-// query token i (kept in registers, already rounded to the table dtype), doc
+// query token i (kept in registers as fp32), doc
 // rows are read once with broadcast 16-byte loads.  Products and sums use
-// __fmul_rn/__fadd_rn in ascending index order, so with identical decoded
-// inputs the result equals the oracle bit for bit.
+// __fmul_rn/__fadd_rn in ascending index order on the fp32 query, so the
+// result equals the oracle (fed the same fp32 query) bit for bit.
 // ============================================================================
 template <int D>
 __global__ void __launch_bounds__(256)
@@ -49,7 +49,10 @@ maxsim_simt_kernel(const MaxSimParams p) {
       bool bad = false;
 #pragma unroll
       for (int k = 0; k < D; ++k) {
-        const float x = espn_ptx::code_to_f32(espn_ptx::f32_to_code(__ldg(&qs[k]), p.bf16), p.bf16);
+        // the reference multiplies the fp32 query as given (types.hpp:33-44);
+        // qround (ESPN_RERANK_QUERY_ROUNDED) first rounds it to the table dtype
+        const float x0 = __ldg(&qs[k]);
+        const float x = p.qround ? espn_ptx::code_to_f32(espn_ptx::f32_to_code(x0, p.bf16), p.bf16) : x0;
         bad |= !isfinite(x);
         q[k] = x;
       }

@@ -39,26 +39,34 @@
 
 namespace espn_k {
 
-template <int D>
+template <int D, bool SPLIT>
 struct TcCfg;
+// SPLIT: the fp32 query is carried as q = hi + lo, both in the table dtype
+// (hi = round(q), lo = round(q - hi)), and every K-step issues two MMAs into
+// the same accumulator.  The products then carry the query at 22 (f16) / 16
+// (bf16) significant bits instead of 11 / 8 -- the reference multiplies the
+// fp32 query (types.hpp:33-44, scoring.hpp:7-10), and a bf16-rounded query
+// alone is off by up to ~3.5e-3 relative.  The A tile doubles (lo slots after
+// the hi slots), so the larger dims run fewer unit slots.
 // REPA: replicated-A mode -- A = the query tile four times (no zero rows) and
 // ONE MMA per K-step covers the whole stage (N = 4 x NQC); lane quarter w of
 // the accumulator holds every slot, epilogue warps of quarter w read columns
 // [w NQC, (w+1) NQC).  Same MAC count as the block-diagonal mode, 4x fewer
 // (wider) MMA instructions and a 3x smaller A tile; needs 4 x NQC TMEM
 // columns per buffer, so it is used where NQC is small (d = 128).
-template <> struct TcCfg<16>  { static constexpr int NQC = 128, NS = 6, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
+template <bool S> struct TcCfg<16, S>  { static constexpr int NQC = 128, NS = 6, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
 #ifndef ESPN_D32_NQC
 #define ESPN_D32_NQC 128
 #define ESPN_D32_NS 4
 #endif
-template <> struct TcCfg<32>  { static constexpr int NQC = ESPN_D32_NQC, NS = ESPN_D32_NS, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
-template <> struct TcCfg<64>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
-template <> struct TcCfg<128> { static constexpr int NQC = 64,  NS = 2, UNITMAX = 32, NU = 2; static constexpr bool REPA = true; };
+template <bool S> struct TcCfg<32, S>  { static constexpr int NQC = ESPN_D32_NQC, NS = ESPN_D32_NS, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
+template <bool S> struct TcCfg<64, S>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = S ? 2 : 3; static constexpr bool REPA = false; };
+template <bool S> struct TcCfg<128, S> { static constexpr int NQC = 64,  NS = 2, UNITMAX = 32, NU = S ? 1 : 2; static constexpr bool REPA = true; };
 
-template <int D>
+template <int D, bool SPLIT_ = false>
 struct TcLayout {
-  using C = TcCfg<D>;
+  using C = TcCfg<D, SPLIT_>;
+  static constexpr bool SPLIT = SPLIT_;
   using RL = RowLayout<D>;
   static constexpr int NQC = C::NQC, NS = C::NS, UNITMAX = C::UNITMAX, NU = C::NU;
   static constexpr bool REPA = C::REPA;
@@ -71,7 +79,8 @@ struct TcLayout {
   // A (query) operand: the same K-major swizzled panel layout as the rows
   // (RowLayout with t = A_ROWS), so the tensor core reads A conflict-free
   static constexpr int CH = D / 8;                 // 16-byte chunks per query row
-  static constexpr int A_ROWS = REPA ? NU * 128 : 96 + NU * 128;  // zeros | Q0 | zeros | Q1 | ... (REPA: Q0 x4 | Q1 x4 ...)
+  static constexpr int LO_ROWS = NU * 128;         // SPLIT: lo slots start LO_ROWS rows after the hi slots
+  static constexpr int A_ROWS = (REPA ? 0 : 96) + (SPLIT ? 2 : 1) * NU * 128;  // zeros | Q0 | zeros | Q1 | ... (REPA: Q0 x4 | Q1 x4 ...)
   static constexpr int A_PANEL_BYTES = A_ROWS * PW;
   static constexpr int A_BYTES = NP * A_PANEL_BYTES;
   static constexpr int MAX_SLOTS = UNITMAX * 64;   // slot budget of one unit
@@ -344,12 +353,12 @@ __global__ void __launch_bounds__(kFinalizeWarps * 32) finalize_kernel(const Max
   ktl_end(p.dbg, 2);
 }
 
-template <int D>
-__global__ void __launch_bounds__(TcLayout<D>::NTHREADS, 1)
+template <int D, bool SPLIT>
+__global__ void __launch_bounds__(TcLayout<D, SPLIT>::NTHREADS, 1)
 maxsim_tc_kernel(const MaxSimParams p) {
   __shared__ uint64_t trace[8 * 8];
   __shared__ uint64_t strace[9 * 16];  // per-stage: producer, MMA full, MMA tempty, epilogue
-  using L = TcLayout<D>;
+  using L = TcLayout<D, SPLIT>;
   using namespace espn_ptx;
   // swizzled operand atoms need 1024-byte aligned stage bases: align manually
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
@@ -639,21 +648,30 @@ maxsim_tc_kernel(const MaxSimParams p) {
             const int i = e / L::CH, c = e % L::CH;
             const float f[8] = {x[u][0].x, x[u][0].y, x[u][0].z, x[u][0].w,
                                 x[u][1].x, x[u][1].y, x[u][1].z, x[u][1].w};
-            uint32_t w4[4];
+            uint32_t w4[4], l4[4];
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
               const uint16_t h0 = f32_to_code(f[2 * h], p.bf16), h1 = f32_to_code(f[2 * h + 1], p.bf16);
-              bad |= !isfinite(code_to_f32(h0, p.bf16)) || !isfinite(code_to_f32(h1, p.bf16));
+              const float r0 = code_to_f32(h0, p.bf16), r1 = code_to_f32(h1, p.bf16);
+              bad |= !isfinite(r0) || !isfinite(r1);
               w4[h] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+              if constexpr (L::SPLIT) {  // residuals (exact in fp32), rounded to the dtype
+                const uint16_t l0 = f32_to_code(__fsub_rn(f[2 * h], r0), p.bf16);
+                const uint16_t l1 = f32_to_code(__fsub_rn(f[2 * h + 1], r1), p.bf16);
+                l4[h] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+              }
             }
             const int r = abase + i;
-            *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, r, c)) =
-                make_uint4(w4[0], w4[1], w4[2], w4[3]);
-            if constexpr (L::REPA) {  // replicas for lane quarters 1..3
 #pragma unroll
-              for (int rq = 1; rq < 4; ++rq)
-                *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, r + 32 * rq, c)) =
-                    make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            for (int part = 0; part < (L::SPLIT ? 2 : 1); ++part) {
+              const uint4 val = part ? make_uint4(l4[0], l4[1], l4[2], l4[3]) : make_uint4(w4[0], w4[1], w4[2], w4[3]);
+              const int rr = r + part * L::LO_ROWS;
+              *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, rr, c)) = val;
+              if constexpr (L::REPA) {  // replicas for lane quarters 1..3
+#pragma unroll
+                for (int rq = 1; rq < 4; ++rq)
+                  *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, rr + 32 * rq, c)) = val;
+              }
             }
           }
           if (bad) atomicOr(p.err, ERR_NONFINITE_QUERY);
@@ -739,10 +757,14 @@ maxsim_tc_kernel(const MaxSimParams p) {
 #pragma unroll
               for (int ks = 0; ks < L::KSTEPS; ++ks) {
                 const uint32_t kb = ks * 32;
-                const uint64_t ad = umma_desc_sw(a_addr + (kb / L::PW) * L::A_PANEL_BYTES + (kb % L::PW), 8 * L::PW, L::SWZ);
                 const uint64_t bd = umma_desc_sw(b_addr + (kb / L::PW) * L::PANEL_BYTES + (kb % L::PW), 8 * L::PW, L::SWZ);
-                umma_f16_elect(d_tmem, ad, bd, idesc, acc);
-                acc = 1;
+#pragma unroll
+                for (int part = 0; part < (L::SPLIT ? 2 : 1); ++part) {
+                  const uint64_t ad = umma_desc_sw(a_addr + part * L::LO_ROWS * L::PW + (kb / L::PW) * L::A_PANEL_BYTES +
+                                                       (kb % L::PW), 8 * L::PW, L::SWZ);
+                  umma_f16_elect(d_tmem, ad, bd, idesc, acc);
+                  acc = 1;
+                }
               }
           } else
 #pragma unroll 1
@@ -759,11 +781,15 @@ maxsim_tc_kernel(const MaxSimParams p) {
 #pragma unroll
             for (int ks = 0; ks < L::KSTEPS; ++ks) {
               const uint32_t kb = ks * 32;  // K offset in bytes
-              const uint64_t ad = umma_desc_sw(a_addr + (kb / L::PW) * L::A_PANEL_BYTES + (kb % L::PW), 8 * L::PW, L::SWZ);
               const uint64_t bd = umma_desc_sw(b_addr + (kb / L::PW) * L::PANEL_BYTES + (kb % L::PW),
                                                8 * L::PW, L::SWZ);
-              umma_f16_elect(d_tmem, ad, bd, idesc, acc);
-              acc = 1;
+#pragma unroll
+              for (int part = 0; part < (L::SPLIT ? 2 : 1); ++part) {  // hi, then lo (SPLIT)
+                const uint64_t ad = umma_desc_sw(a_addr + part * L::LO_ROWS * L::PW + (kb / L::PW) * L::A_PANEL_BYTES +
+                                                     (kb % L::PW), 8 * L::PW, L::SWZ);
+                umma_f16_elect(d_tmem, ad, bd, idesc, acc);
+                acc = 1;
+              }
             }
           }
           umma_commit_elect(&empty_bar[s]);

@@ -51,19 +51,21 @@ def test_random_shapes_against_oracle(oracle, cuda_ok, d, dtype):
         R = int(rng.integers(1, kmax + 2)) if partial else int(rng.choice([k, max(k, kmax // 2), kmax + 5]))
         alpha = float(rng.choice([1.0, 0.5, 2.0]))
         cfg = api.PipelineConfig(rerank_count=R, final_k=k, alpha=alpha, partial_rerank_enabled=partial)
-        qr = oracle.round_to(q, odt)
+        qp = str(rng.choice(["auto", "auto", "split", "rounded"]))
+        # the reference's fp32 query, unrounded (the legacy "rounded" mode: the dtype-rounded one)
+        qr = oracle.round_to(q, odt) if qp == "rounded" else np.ascontiguousarray(q, np.float32)
         if not partial and R < k:  # R < final_k needs partial re-ranking: both sides reject
             st, *_ = oracle.rerank_batch(ot, qr, ids, cls, off, R, k, alpha, partial)
             assert st != 0
             with pytest.raises(api.InvalidInputError):
-                rr.rerank_arrays(q, ids, cls, off, cfg)
+                rr.rerank_arrays(q, ids, cls, off, cfg, query_precision=qp)
             continue
         st, obow = oracle.maxsim_batch(ot, qr, ids, off)
         assert st == 0
         st, oi, os_, on = oracle.rerank_batch(ot, qr, ids, cls, off, R, k, alpha, partial)
         assert st == 0
         for rep in range(3):  # eager, captured, replayed
-            gi, gs, gc, _ = [np.copy(x) if x is not None else None for x in rr.rerank_arrays(q, ids, cls, off, cfg)]
+            gi, gs, gc, _ = [np.copy(x) if x is not None else None for x in rr.rerank_arrays(q, ids, cls, off, cfg, query_precision=qp)]
             for b in range(B):
                 a0, a1 = int(off[b]), int(off[b + 1])
                 need = min(a1 - a0, R)
@@ -71,6 +73,6 @@ def test_random_shapes_against_oracle(oracle, cuda_ok, d, dtype):
                 assert int(gc[b]) == int(on[b]), (case, rep, b)
                 n = int(on[b])
                 assert_topk_equivalent(gi[b, :n], gs[b, :n], oi[b, :n], os_[b, :n], ids[a0:a1], full,
-                                       ctx=f"d={d} case {case} rep {rep} query {b}")
+                                       ctx=f"d={d} {qp} case {case} rep {rep} query {b}")
     rr.close()
     store.close()

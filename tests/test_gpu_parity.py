@@ -23,19 +23,22 @@ def build_case(n_docs, d, t_min, t_max, B, K, nq=32, dtype="f16", seed=1):
     return rp, codes, q, ids, cls, off
 
 
-def run_gpu(rp, codes, d, dtype, q, ids, cls, off, cfg, kernel):
+def run_gpu(rp, codes, d, dtype, q, ids, cls, off, cfg, kernel, query_precision="auto"):
     store = api.GpuStore(rp, codes, d, dtype=dtype)
     rr = api.Reranker(store, len(off) - 1, max(int(off[-1]), 1), q.shape[1])
-    out = rr.rerank_arrays(q, ids, cls, off, cfg, kernel=kernel, write_bow=True)
+    out = rr.rerank_arrays(q, ids, cls, off, cfg, kernel=kernel, write_bow=True, query_precision=query_precision)
     rr.close()
     store.close()
     return out
 
 
-def check_against_oracle(oracle, rp, codes, d, dtype, q, ids, cls, off, cfg, kernel, bitexact_bow=False):
+def check_against_oracle(oracle, rp, codes, d, dtype, q, ids, cls, off, cfg, kernel, bitexact_bow=False,
+                         query_precision="auto", rtol=RTOL):
     ot = oracle.OracleTable(rp, codes, d, dtype=_dt(dtype))
-    qr = oracle.round_to(q, _dt(dtype))  # the oracle consumes the same rounded query
-    gi, gs, gc, gbow = run_gpu(rp, codes, d, dtype, q, ids, cls, off, cfg, kernel)
+    # the reference multiplies the fp32 query as given (types.hpp:33-44); only the
+    # legacy "rounded" mode is compared against the oracle fed the dtype-rounded query
+    qr = oracle.round_to(q, _dt(dtype)) if query_precision == "rounded" else np.ascontiguousarray(q, np.float32)
+    gi, gs, gc, gbow = run_gpu(rp, codes, d, dtype, q, ids, cls, off, cfg, kernel, query_precision)
     st, obow = oracle.maxsim_batch(ot, qr, ids, off)
     assert st == 0
     st, oi, os_, on = oracle.rerank_batch(ot, qr, ids, cls, off, cfg.rerank_count, cfg.final_k, cfg.alpha,
@@ -51,7 +54,7 @@ def check_against_oracle(oracle, rp, codes, d, dtype, q, ids, cls, off, cfg, ker
             assert np.array_equal(g.view(np.uint32), o.view(np.uint32)), f"query {b}: SIMT bow not bit-exact"
         elif need:
             e = rel_err(g, o)
-            assert e.max() <= RTOL, f"query {b}: max rel err {e.max()} at {int(e.argmax())}"
+            assert e.max() <= rtol, f"query {b}: max rel err {e.max()} at {int(e.argmax())}"
         full = oracle_full_scores(obow[a0:a1], cls[a0:a1], cfg.alpha, need, cfg.partial_rerank_enabled)
         assert int(gc[b]) == int(on[b])
         n = int(on[b])
@@ -91,6 +94,40 @@ def test_c2_shape_many_units(oracle, cuda_ok):
     rp, codes, q, ids, cls, off = build_case(200000, 32, 1, 63, B=64, K=1000, seed=5)
     cfg = api.PipelineConfig(rerank_count=1000, final_k=10)
     check_against_oracle(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, "tcgen05")
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_fp32_query_parity_c2_shape(oracle, cuda_ok, dtype):
+    # the reference's query is fp32 (types.hpp:33-44) and the
+    # C-ABI takes fp32; the oracle here gets the UNROUNDED query.  The default
+    # tcgen05 path carries it as hi + lo (two MMAs per K-step): well inside
+    # 1e-3 for both dtypes (a bf16-rounded query alone is off by ~3e-3).
+    rp, codes, q, ids, cls, off = build_case(200000, 32, 1, 63, B=64, K=1000, dtype=dtype, seed=55)
+    cfg = api.PipelineConfig(rerank_count=1000, final_k=10)
+    gbow, obow = check_against_oracle(oracle, rp, codes, 32, dtype, q, ids, cls, off, cfg, "tcgen05", rtol=1e-4)
+    assert rel_err(gbow, obow).max() <= 1e-4
+
+
+@pytest.mark.parametrize("d,dtype", [(16, "bf16"), (64, "bf16"), (128, "bf16"), (128, "f16"), (32, "f16")])
+def test_fp32_query_parity_dims(oracle, cuda_ok, d, dtype):
+    # every dim against the unrounded-query oracle; forced split for f16 d=128
+    t_max = 100 if d == 128 else 63
+    rp, codes, q, ids, cls, off = build_case(4000, d, 1, t_max, B=5, K=400, dtype=dtype, seed=60 + d)
+    cfg = api.PipelineConfig(rerank_count=400, final_k=10)
+    check_against_oracle(oracle, rp, codes, d, dtype, q, ids, cls, off, cfg, "tcgen05")
+    gbow, obow = check_against_oracle(oracle, rp, codes, d, dtype, q, ids, cls, off, cfg, "tcgen05",
+                                      query_precision="split", rtol=1e-4)
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_rounded_query_mode_matches_rounded_oracle(oracle, cuda_ok, dtype):
+    # ESPN_RERANK_QUERY_ROUNDED: the legacy precision, equal to the oracle fed
+    # the dtype-rounded query (SIMT bit-exact)
+    rp, codes, q, ids, cls, off = build_case(3000, 32, 1, 63, B=3, K=300, dtype=dtype, seed=71)
+    cfg = api.PipelineConfig(rerank_count=300, final_k=10)
+    check_against_oracle(oracle, rp, codes, 32, dtype, q, ids, cls, off, cfg, "tcgen05", query_precision="rounded")
+    check_against_oracle(oracle, rp, codes, 32, dtype, q, ids, cls, off, cfg, "simt", query_precision="rounded",
+                         bitexact_bow=True)
 
 
 def test_c3_shape_many_units(oracle, cuda_ok):
@@ -286,7 +323,7 @@ def test_api_mirror_rerank_candidates(oracle, cuda_ok):
     cl = api.CandidateList([api.Candidate(int(i), float(c)) for i, c in zip(ids, cls)])
     ranked, stats = api.rerank_candidates(qe, cl, store, api.PipelineConfig(rerank_count=200, final_k=10))
     ot = oracle.OracleTable(rp, codes, 32)
-    st, oi, os_, ostats = oracle.rerank_query(ot, oracle.round_to(q[0]), ids, cls, 200, 10)
+    st, oi, os_, ostats = oracle.rerank_query(ot, np.ascontiguousarray(q[0], np.float32), ids, cls, 200, 10)
     assert st == 0
     assert [e.doc_id for e in ranked.entries] == list(oi)
     assert stats.needed_count == 200 and stats.query_id == 3
@@ -386,6 +423,58 @@ def test_prefetch_on_off_identical_and_hit_rate(cuda_ok):
     for b, st in enumerate(br.stats):
         assert st.missed_count == ref_stats[b]["missed"]
         assert abs(st.hit_rate - ref_stats[b]["resident"] / 64) < 1e-12
+    rr.close(); store.close()
+
+
+def test_prefetch_survives_interleaved_plain_batches(cuda_ok):
+    # prefetch(A), plain(X), plain(Y), prefetched(A) -- the plain
+    # batches must not restage A's pending staging slot
+    import torch
+    rp, codes, q, ids, cls, off, resident = _tiered_case(seed=212)
+    cfg = api.PipelineConfig(rerank_count=64, final_k=10, partial_rerank_enabled=True)
+    store = api.GpuStore(rp, codes, 32, resident=resident)
+    B, C = len(off) - 1, int(off[-1])
+    rr = api.Reranker(store, B, C, 32)
+    dev = torch.device("cuda")
+    dq, di, dc = (torch.from_numpy(q).to(dev), torch.from_numpy(ids.view(np.int32)).to(dev),
+                  torch.from_numpy(cls).to(dev))
+    rng = np.random.default_rng(5)
+    perm = [rng.permutation(B) for _ in range(2)]
+    other = [(dq[p].contiguous(), torch.from_numpy(np.concatenate([ids[int(off[b]):int(off[b + 1])] for b in p])
+                                                   .view(np.int32)).to(dev),
+              torch.from_numpy(np.concatenate([cls[int(off[b]):int(off[b + 1])] for b in p])).to(dev),
+              np.concatenate([[0], np.cumsum(np.diff(off)[p])]).astype(np.uint64)) for p in perm]
+    ref = [x.cpu().numpy() for x in rr.rerank_arrays(dq, di, dc, off, cfg, device_io=True)[:3]]
+    side = torch.cuda.Stream()
+    rr.prefetch(dq, di, dc, off, cfg, stream=side.cuda_stream)
+    for oq, oi, oc, oo in other:
+        rr.rerank_arrays(oq, oi, oc, oo, cfg, device_io=True)
+    got = rr.rerank_arrays(dq, di, dc, off, cfg, device_io=True, prefetched=True, fetch_stats=True)
+    for g, r in zip(got[:3], ref):
+        assert np.array_equal(g.cpu().numpy(), r)
+    assert all(fs["missed"] == 0 for fs in rr.last_fetch_stats)
+    rr.close(); store.close()
+
+
+def test_sync_graph_key_tracks_list_lengths(cuda_ok):
+    # the separate top-k's dedup hash is sized by the longest list;
+    # a replayed graph of the same (B, C) with a longer list must still reject
+    # duplicates
+    rp, codes = synth.make_table(4000, 48, 1, 20, seed=17)  # d=48: CUDA-core path, separate top-k
+    q, _ = synth.make_queries(rp, codes, 48, 4, seed=18)
+    cfg = api.PipelineConfig(rerank_count=2000, final_k=10)
+    store = api.GpuStore(rp, codes, 48)
+    rr = api.Reranker(store, 4, 2000, 32)
+    rng = np.random.default_rng(19)
+    even = np.arange(5) * 500
+    for _ in range(3):  # eager, capture, replay of the balanced shape
+        ids = rng.permutation(4000)[:2000].astype(np.uint32)
+        rr.rerank_arrays(q, ids, rng.random(2000, dtype=np.float32), even.astype(np.uint64), cfg)
+    skew = np.array([0, 1700, 1800, 1900, 2000], np.uint64)  # same B and C, one long list
+    ids = rng.permutation(4000)[:2000].astype(np.uint32)
+    ids[1600] = ids[3]  # duplicate inside the long list
+    with pytest.raises(api.InvalidInputError):
+        rr.rerank_arrays(q, ids, rng.random(2000, dtype=np.float32), skew, cfg)
     rr.close(); store.close()
 
 
@@ -543,7 +632,7 @@ def test_full_scale_c2_sampled_parity(oracle, cuda_ok):
         assert lib.espn_gpu_gather(store.handle, cid.data_ptr(), K, lrows.data_ptr(), lrp.data_ptr(),
                                    int(lrp[-1]), None) == 0
         ot = oracle.OracleTable(lrp.cpu().numpy(), lrows.cpu().numpy().view(np.uint16), d)
-        st, obow = oracle.maxsim_batch(ot, oracle.round_to(q[qi:qi + 1]), np.arange(K, dtype=np.uint32),
+        st, obow = oracle.maxsim_batch(ot, np.ascontiguousarray(q[qi:qi + 1]), np.arange(K, dtype=np.uint32),
                                        np.array([0, K], np.uint64))
         assert st == 0
         e = rel_err(gbow[qi * K:(qi + 1) * K], obow)

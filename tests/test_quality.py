@@ -127,7 +127,7 @@ def test_rerank_sweep_matches_oracle_and_is_monotone(oracle, cuda_ok):
     store.close()
     import oracle_py
     ot = oracle.OracleTable(rp, codes, 32, dtype=oracle_py.F16)
-    qr = oracle.round_to(q, oracle_py.F16)
+    qr = np.ascontiguousarray(q, np.float32)  # the reference's fp32 query
     for R in Rs:
         st, oi, _, on = oracle.rerank_batch(ot, qr, ids, cls, off, R, 10, 1.0, True)
         assert st == 0
