@@ -1,6 +1,6 @@
 # K1 standalone gather (espn_gpu_gather, StoreHandle::fetch_batch restated)
 # on the C2 table: 64 x 1000 random doc ids per call (one batch's candidates).
-#   python scratch/gather_bench.py [--reps 20]
+#   python tools/gather_bench.py [--reps 20]
 # Algorithmic bytes per call = gathered tokens x 64 B read + the same written.
 import argparse
 import json

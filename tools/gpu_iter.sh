@@ -1,4 +1,4 @@
-# usage: bash scratch/gpu_iter.sh [tests] [bench] [ncu] [ncufull]   (outputs in gpurun_out/)
+# usage: bash tools/gpu_iter.sh [tests] [bench] [ncu] [ncufull]   (outputs in gpurun_out/)
 set -x
 for a in "$@"; do case $a in
 tests) timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -15 gpurun_out/pytest_gpu.log;;

@@ -1,6 +1,6 @@
 # Measurement behind ESPN_KERNEL_AUTO: tcgen05 vs CUDA-core (SIMT) MaxSim per dim,
 # C2-shaped batch (64 queries x 1000 candidates, t~U{1..63}) on a 2M-doc table.
-#   python scratch/kernel_choice.py
+#   python tools/kernel_choice.py
 import json, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))

@@ -1,6 +1,6 @@
 """Kernel timing harness (dev tool): C2-shaped batch through the C-ABI with
 ESPN_RERANK_PROFILE; prints mean MaxSim / top-k kernel ms.  Usage:
-  ESPN_DEBUG=<bits> python scratch/ktime.py [config] [n]"""
+  ESPN_DEBUG=<bits> python tools/ktime.py [config] [n]"""
 import ctypes as C, os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))

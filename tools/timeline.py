@@ -1,6 +1,6 @@
 # Profiling experiment (not product): per-kernel device timeline of the C2
 # step under CUDA-graph replay and eager ASYNC calls (ESPN_DEBUG bit 256).
-#   python scratch/timeline.py [--config c2] [--dbg 0x100]
+#   python tools/timeline.py [--config c2] [--dbg 0x100]
 import argparse
 import ctypes as C
 import os

@@ -1,6 +1,6 @@
 # Profiling experiment: CTA-0 role trace (ESPN_DEBUG bit 8) of MaxSim launches
 # in the bench's steady state -- 3 lanes (streams + workspaces) in flight, C2.
-#   ESPN_DEBUG=8 python scratch/timeline_lanes.py
+#   ESPN_DEBUG=8 python tools/timeline_lanes.py
 import os
 import sys
 from pathlib import Path
