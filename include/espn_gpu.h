@@ -151,13 +151,14 @@ ESPN_API int espn_gpu_workspace_destroy(espn_gpu_workspace* ws);
 #define ESPN_RERANK_SEPARATE_TOPK 0x80u /* rank in a separate top-k kernel instead of inside the
                                          tcgen05 MaxSim kernel (the fused path is the default when
                                          final_k <= 32; results are identical) */
-#define ESPN_RERANK_QUERY_ROUNDED 0x100u /* legacy precision: the fp32 query is rounded to the table dtype
-                                         before MaxSim (one MMA per K-step).  Default: the fp32 query is
-                                         honoured (types.hpp:33-44) -- CUDA-core path exactly, tcgen05 path
-                                         as q = hi + lo in the table dtype (two MMAs per K-step; 22 / 16
-                                         significant bits for f16 / bf16), except f16 tables at d = 128,
-                                         which round unless ESPN_RERANK_QUERY_SPLIT */
-#define ESPN_RERANK_QUERY_SPLIT 0x200u  /* tcgen05: force the hi + lo query for every dim and dtype */
+#define ESPN_RERANK_QUERY_ROUNDED 0x100u /* round the fp32 query to the table dtype before MaxSim (one MMA
+                                         per K-step; CUDA-core path too).  Default: the CUDA-core path
+                                         multiplies the fp32 query exactly (types.hpp:33-44); the tcgen05
+                                         path carries it as q = hi + lo in the table dtype (two MMAs per
+                                         K-step, 16 significant bits) for bf16 tables and rounds it to f16
+                                         (11 bits, <= ~5e-4 relative) for f16 tables */
+#define ESPN_RERANK_QUERY_SPLIT 0x200u  /* tcgen05: hi + lo query for f16 tables too (22 significant bits;
+                                         ~17% slower MaxSim at d = 32) */
 #define ESPN_RERANK_DEVICE_OFFSETS 0x20u /* cand_offsets / needed_counts are DEVICE pointers (needs
                                          DEVICE_IO): the batch is planned on the device, the call has
                                          no host-side loop, no host sync with ASYNC, and is CUDA-graph
@@ -278,6 +279,53 @@ ESPN_API int espn_gpu_gather_host(espn_gpu_table* table, const uint32_t* ids, ui
 ESPN_API int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const uint32_t* counts,
                         uint32_t n_lists, uint64_t list_stride, uint32_t n_queries, uint32_t k,
                         uint32_t* out_ids, float* out_scores, uint32_t* out_counts, void* stream);
+
+/* ---- Multi-GPU --------------------------------
+ * One process (rank) per GPU, or one process driving several GPUs.  Every rank
+ * passes the SAME global batch (global doc ids; the candidate generator's
+ * top-K per query, as run_batch hands it over, pipeline.hpp:81-85) and gets
+ * the SAME global ranked lists back.  The placement follows the table:
+ *   SHARD   (espn_table_desc.shard_count = G > 1; rank g opened shard g):
+ *           each rank scores its own candidates (doc_id % G == g) -- needed
+ *           count = its share of the query's global top-R prefix -- and ranks
+ *           them; one ncclAllGather of the packed local top-k lists; merge.
+ *   REPLICA (shard_count <= 1, every rank holds the whole table): rank g
+ *           scores queries [g*ceil(B/G), (g+1)*ceil(B/G)); one ncclAllGather
+ *           reassembles the batch.
+ * Packed per-rank block (int32 words): [err bits, 0, 0, 0 | ids BQ x k |
+ * scores BQ x k (fp32 bits) | counts BQ], BQ = B (SHARD) or ceil(B/G)
+ * (REPLICA).  All steps run on `stream` (graph-capturable with DEVICE_IO |
+ * DEVICE_OFFSETS | ASYNC); errors of any rank surface on every rank.  Not
+ * combinable with WRITE_BOW, PREFETCHED or fetch_stats.
+ * NCCL is loaded at run time (dlopen "libnccl.so.2", reusing an already
+ * loaded copy, e.g. torch's); a nccl_comm is an ncclComm_t passed as void*. */
+typedef struct { uint8_t internal[128]; } espn_nccl_id;  /* ncclUniqueId */
+ESPN_API int espn_nccl_get_unique_id(espn_nccl_id* out);
+/* ncclCommInitRank on `device` (the caller exchanges the id, e.g. over torch.distributed). */
+ESPN_API int espn_nccl_comm_init(int nranks, const espn_nccl_id* id, int rank, int device, void** comm);
+/* ncclCommInitAll: one communicator per device for a single process driving ndev GPUs. */
+ESPN_API int espn_nccl_comm_init_all(int ndev, const int* devices, void** comms);
+ESPN_API int espn_nccl_comm_destroy(void* comm);
+
+/* Pack + all-gather + merge on `stream`.  nccl_comm: this rank's communicator
+ * (SHARD: nranks == shard_count, rank == shard_index). */
+ESPN_API int espn_gpu_rerank_sharded(espn_gpu_table* table, espn_gpu_workspace* ws, const espn_rerank_args* args,
+                                     espn_rerank_out* out, void* nccl_comm, void* stream);
+/* Single process, n GPUs (tables[i] on its own device, comms from
+ * espn_nccl_comm_init_all): the same batch on every device, the NCCL calls in
+ * one group (required when one thread drives several ranks).  outs[i] gets
+ * the global result on device i (DEVICE_IO) or a host copy. */
+ESPN_API int espn_gpu_rerank_sharded_multi(uint32_t n, espn_gpu_table* const* tables, espn_gpu_workspace* const* ws,
+                                           const espn_rerank_args* args, espn_rerank_out* outs,
+                                           void* const* nccl_comms, void* const* streams);
+/* The two local phases without NCCL (tests, custom transports): pack this
+ * rank's block into the workspace's send buffer (*send, *words on return:
+ * device pointer and int32 count), then -- after the caller gathered the G
+ * blocks contiguously into `recv` (device) -- merge them into `out`. */
+ESPN_API int espn_gpu_shard_pack(espn_gpu_table* table, espn_gpu_workspace* ws, const espn_rerank_args* args,
+                                 uint32_t nranks, uint32_t rank, void* stream, const int32_t** send, uint64_t* words);
+ESPN_API int espn_gpu_shard_merge(espn_gpu_table* table, espn_gpu_workspace* ws, const espn_rerank_args* args,
+                                  const int32_t* recv, uint32_t nranks, espn_rerank_out* out, void* stream);
 
 /* Cumulative counters of a workspace since creation.  Reading them
  * synchronizes the device (completes PROFILE timings still in flight). */

@@ -147,6 +147,7 @@ struct PlanParams {
                                //    alpha*cls tail [needed, n) as MMA-free units
   uint32_t* out_counts;        // fused top-k: queries with no unit get count 0 here (else NULL)
   uint32_t* fused_state;       // fused top-k: advance {epoch, rows per parity} (else NULL)
+  uint32_t base_ok;            // cand_off[0] may be nonzero (a query slice of a larger batch, REPLICA placement)
   uint32_t dbg;                // profiling knobs (ESPN_DEBUG env; 0 in production)
 };
 

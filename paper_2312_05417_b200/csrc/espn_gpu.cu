@@ -3,8 +3,11 @@
 // standalone gather / merge / synth entry points.  Pure CUDA runtime; no torch.
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is loaded at run time (nccl_api below)
 
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -17,6 +20,7 @@
 #include "common.cuh"
 #include "kernels_misc.cuh"
 #include "maxsim_tc.cuh"
+#include "shard.cuh"
 
 using namespace espn_k;
 
@@ -80,7 +84,10 @@ int check_device(int dev, int* num_sms, bool* tc_ok) {
   return ESPN_OK;
 }
 
-constexpr int kMinUnitDocs = 8;  // shortest work unit (small batches, see espn_gpu_rerank)
+constexpr int kMinUnitDocs = 8;
+// internal re-rank flag: device cand_offsets are a query slice of a larger
+// batch (cand_offsets[0] may be nonzero; REPLICA placement of the sharded call)
+constexpr uint32_t kFlagBaseOffsets = 0x80000000u;  // shortest work unit (small batches, see espn_gpu_rerank)
 
 template <int D>
 constexpr int tc_unit_docs(uint32_t max_t) {
@@ -165,7 +172,11 @@ cudaError_t launch_tc_rt(uint32_t d, bool split, const MaxSimParams& p, int num_
 bool tc_query_split(uint32_t d, uint32_t dtype, uint32_t flags) {
   if (flags & ESPN_RERANK_QUERY_ROUNDED) return false;
   if (flags & ESPN_RERANK_QUERY_SPLIT) return true;
-  return !(d == 128 && dtype == ESPN_DTYPE_F16);
+  (void)d;
+  // bf16 needs the split (a bf16-rounded query is off by ~3e-3 relative); an
+  // f16-rounded one stays within ~5e-4, and the second MMA costs ~17% of the
+  // C2 step (46.4 vs 39.8 us, profiles/query_split_r2_{split,rounded}.json), so f16 rounds
+  return dtype == ESPN_DTYPE_BF16;
 }
 
 template <int D>
@@ -204,6 +215,67 @@ cudaError_t ensure_topk_attr() {
   if (e == cudaSuccess) e = smem_attr_once(topk_cta_kernel<32>, 8192 * 8 + 8 * 32 * 8, d4);
   return e;
 }
+
+
+// ---- NCCL, loaded at run time ------------------------------------------------
+// The C-ABI does not link NCCL: torch (or the integrator) may already have a
+// libnccl.so.2 loaded, and that copy must be the one whose communicators we
+// are handed, so dlopen(RTLD_NOLOAD) first, then the default search path.
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommCuDevice)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      a.why = std::string("NCCL not loadable (libnccl.so.2): ") + (e ? e : "?");
+      return a;
+    }
+    bool all = true;
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn) all = false;
+    };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommInitAll, "ncclCommInitAll");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.CommCount, "ncclCommCount");
+    sym(a.CommUserRank, "ncclCommUserRank");
+    sym(a.CommCuDevice, "ncclCommCuDevice");
+    sym(a.AllGather, "ncclAllGather");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    a.ok = all;
+    if (!all) a.why = "libnccl.so.2 lacks an expected symbol";
+    return a;
+  }();
+  return api;
+}
+#define ESPN_NCCL_TRY(expr)                                                                   \
+  do {                                                                                        \
+    const ncclResult_t r_ = (expr);                                                           \
+    if (r_ != ncclSuccess)                                                                    \
+      return fail(ESPN_E_CUDA, std::string(#expr) + ": " + nccl_api().GetErrorString(r_));    \
+  } while (0)
+
 
 bool layout_tiled(uint32_t d) { return d == 16 || d == 32 || d == 64 || d == 128; }
 
@@ -343,6 +415,24 @@ struct espn_gpu_workspace {
   } prof[kProf];
   uint64_t prof_calls = 0;
   espn_counters counters{};
+  // multi-GPU (espn_gpu_rerank_sharded): the global batch staged from host
+  // arrays, this shard's own lists, the packed exchange blocks.  Grown on the
+  // first sharded call of a shape (never inside a stream capture).
+  struct Shard {
+    float* g_q = nullptr;
+    uint32_t* g_ids = nullptr;
+    float* g_cls = nullptr;
+    uint64_t* g_off = nullptr;
+    uint32_t* g_need = nullptr;
+    uint32_t* loc_ids = nullptr;
+    float* loc_cls = nullptr;
+    uint64_t* loc_off = nullptr;
+    uint32_t* loc_need = nullptr;
+    int32_t* send = nullptr;
+    int32_t* recv = nullptr;
+    uint64_t send_cap = 0, recv_cap = 0;  // int32 words
+    bool lists = false;
+  } sh;
 };
 
 namespace {
@@ -778,6 +868,12 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
     for (auto& ev : pr.e)
       if (ev) { cudaEventSynchronize(ev); cudaEventDestroy(ev); }
   cudaFreeHost(w->h_err);
+  {
+    auto& h = w->sh;
+    cudaFree(h.g_q); cudaFree(h.g_ids); cudaFree(h.g_cls); cudaFree(h.g_off); cudaFree(h.g_need);
+    cudaFree(h.loc_ids); cudaFree(h.loc_cls); cudaFree(h.loc_off); cudaFree(h.loc_need);
+    cudaFree(h.send); cudaFree(h.recv);
+  }
   delete w;
   return ESPN_OK;
 }
@@ -1066,6 +1162,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   pp.tail_units = (fused && partial) ? 1u : 0u;
   pp.out_counts = fused ? out_counts_k : nullptr;
   pp.fused_state = fused ? w->fused_state : nullptr;
+  pp.base_ok = (dev_off && (a->flags & kFlagBaseOffsets)) ? 1u : 0u;
   pp.dbg = dbg;
   plan_kernel<<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp);
   ESPN_CUDA_TRY(cudaGetLastError());
@@ -1619,6 +1716,400 @@ int espn_gpu_synth_table(uint64_t n_docs, uint32_t d, uint32_t dtype, uint32_t t
   ESPN_CUDA_TRY(cudaGetLastError());
   ESPN_CUDA_TRY(cudaStreamSynchronize(s));
   return ESPN_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// Multi-GPU re-rank (espn_gpu.h "Multi-GPU"; shard.cuh)
+// ============================================================================
+namespace {
+cudaError_t grow(void** p, uint64_t* cap, uint64_t need_bytes) {
+  if (*cap >= need_bytes) return cudaSuccess;
+  cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  const cudaError_t e = cudaMalloc(p, need_bytes);
+  if (e == cudaSuccess) *cap = need_bytes;
+  return e;
+}
+
+struct ShardJob {  // one rank's view of a sharded call
+  bool replica = false;
+  uint32_t G = 1, g = 0, B = 0, k = 0, nq = 0, BQ = 0;
+  uint64_t P = 0;                 // packed words per rank
+  const float* q = nullptr;       // device views of the global batch
+  const uint32_t* ids = nullptr;
+  const float* cls = nullptr;
+  const uint64_t* off = nullptr;
+  const uint32_t* need = nullptr;
+};
+
+int shard_validate(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a, uint32_t nranks,
+                   uint32_t rank, ShardJob* j) {
+  if (!t || !w || !a) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
+  if (nranks < 1 || rank >= nranks) return fail(ESPN_E_INVALID_INPUT, "rank must be in [0, nranks)");
+  if (a->flags & (ESPN_RERANK_WRITE_BOW | ESPN_RERANK_PREFETCHED))
+    return fail(ESPN_E_INVALID_INPUT, "sharded re-rank: WRITE_BOW / PREFETCHED are not supported");
+  if ((a->flags & ESPN_RERANK_DEVICE_OFFSETS) && !(a->flags & ESPN_RERANK_DEVICE_IO))
+    return fail(ESPN_E_INVALID_INPUT, "DEVICE_OFFSETS requires DEVICE_IO");
+  j->replica = t->shard_count <= 1;
+  if (!j->replica && (nranks != t->shard_count || rank != t->shard_index))
+    return fail(ESPN_E_INVALID_CONFIG, "sharded table: the communicator must have shard_count ranks, this one at "
+                                       "rank shard_index (got " + std::to_string(nranks) + " ranks, rank " +
+                                       std::to_string(rank) + "; table shard " + std::to_string(t->shard_index) +
+                                       " of " + std::to_string(t->shard_count) + ")");
+  j->G = nranks;
+  j->g = rank;
+  j->B = a->n_queries;
+  j->k = a->final_k;
+  j->nq = a->n_query_tokens;
+  if (j->B > w->max_queries) return fail(ESPN_E_INVALID_INPUT, "n_queries exceeds workspace capacity");
+  if (j->k < 1 || j->k > (uint32_t)kMaxK) return fail(ESPN_E_INVALID_INPUT, "final_k must be in [1, 1024]");
+  if (j->nq < 1 || j->nq > w->max_nq) return fail(ESPN_E_INVALID_INPUT, "n_query_tokens must be in [1, workspace max]");
+  j->BQ = j->replica ? (j->B + j->G - 1) / j->G : j->B;
+  j->P = pack_words(j->BQ, j->k);
+  return ESPN_OK;
+}
+
+// Phase 1: the global batch on the device, this rank's local pass, its block
+// packed into w->sh.send.  Everything on `s`.
+int shard_pack(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a, ShardJob& j, cudaStream_t s) {
+  auto& h = w->sh;
+  const bool dev_io = (a->flags & ESPN_RERANK_DEVICE_IO) != 0;
+  const bool dev_off = (a->flags & ESPN_RERANK_DEVICE_OFFSETS) != 0;
+  const uint64_t C = w->max_candidates;
+  // ---- buffers (grown outside captures only) ----
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  ESPN_CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+  const bool need_lists = !h.lists && (!j.replica || !dev_io || !dev_off);
+  if ((need_lists || h.send_cap < j.P) && cap != cudaStreamCaptureStatusNone)
+    return fail(ESPN_E_INVALID_STATE, "sharded re-rank: run one call of this shape outside the stream capture first "
+                                      "(it sizes the exchange buffers)");
+  if (need_lists) {
+    const uint64_t B = w->max_queries;
+    cudaError_t e = cudaSuccess;
+    auto al = [&](void** p, size_t bytes) { if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(bytes, 16)); };
+    al((void**)&h.g_q, B * w->max_nq * t->d * sizeof(float));
+    al((void**)&h.g_ids, C * 4);
+    al((void**)&h.g_cls, C * 4);
+    al((void**)&h.g_off, (B + 1) * 8);
+    al((void**)&h.g_need, B * 4);
+    al((void**)&h.loc_ids, C * 4);
+    al((void**)&h.loc_cls, C * 4);
+    al((void**)&h.loc_off, (B + 1) * 8);
+    al((void**)&h.loc_need, B * 4);
+    if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("sharded workspace buffers: ") + cudaGetErrorString(e));
+    h.lists = true;
+  }
+  {
+    uint64_t sc = h.send_cap * 4;
+    const cudaError_t e = grow(reinterpret_cast<void**>(&h.send), &sc, j.P * 4);
+    if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("sharded send buffer: ") + cudaGetErrorString(e));
+    h.send_cap = sc / 4;
+  }
+  // ---- the global batch as device arrays ----
+  j.q = a->query_tokens;
+  j.ids = a->cand_ids;
+  j.cls = a->cand_cls;
+  j.off = a->cand_offsets;
+  j.need = a->needed_counts;
+  uint64_t Ch = 0;
+  if (!dev_off) {  // host offsets: validate here, stage them
+    const uint64_t* off = a->cand_offsets;
+    if (!off) return fail(ESPN_E_INVALID_INPUT, "null cand_offsets");
+    if (off[0] != 0) return fail(ESPN_E_INVALID_INPUT, "cand_offsets[0] must be 0");
+    for (uint32_t b = 0; b < j.B; ++b)
+      if (off[b + 1] < off[b]) return fail(ESPN_E_INVALID_INPUT, "cand_offsets must be non-decreasing");
+    Ch = off[j.B];
+    if (Ch > C) return fail(ESPN_E_INVALID_INPUT, "candidates exceed workspace capacity");
+    ESPN_CUDA_TRY(cudaMemcpyAsync(h.g_off, off, (j.B + 1) * 8, cudaMemcpyHostToDevice, s));
+    j.off = h.g_off;
+    if (a->needed_counts) {
+      ESPN_CUDA_TRY(cudaMemcpyAsync(h.g_need, a->needed_counts, j.B * 4, cudaMemcpyHostToDevice, s));
+      j.need = h.g_need;
+    }
+  }
+  if (!dev_io) {
+    if (!a->query_tokens || (Ch && (!a->cand_ids || !a->cand_cls))) return fail(ESPN_E_INVALID_INPUT, "null array argument");
+    ESPN_CUDA_TRY(cudaMemcpyAsync(h.g_q, a->query_tokens, (size_t)j.B * j.nq * t->d * 4, cudaMemcpyHostToDevice, s));
+    if (Ch) {
+      ESPN_CUDA_TRY(cudaMemcpyAsync(h.g_ids, a->cand_ids, Ch * 4, cudaMemcpyHostToDevice, s));
+      ESPN_CUDA_TRY(cudaMemcpyAsync(h.g_cls, a->cand_cls, Ch * 4, cudaMemcpyHostToDevice, s));
+    }
+    j.q = h.g_q;
+    j.ids = h.g_ids;
+    j.cls = h.g_cls;
+  }
+  // ---- this rank's local pass, written straight into its packed block ----
+  espn_rerank_args la = *a;
+  la.flags = (a->flags & (ESPN_RERANK_PARTIAL | ESPN_RERANK_PROFILE | ESPN_RERANK_SEPARATE_TOPK |
+                          ESPN_RERANK_QUERY_ROUNDED | ESPN_RERANK_QUERY_SPLIT)) |
+             ESPN_RERANK_DEVICE_IO | ESPN_RERANK_DEVICE_OFFSETS | ESPN_RERANK_ASYNC;
+  int32_t* blk = h.send;
+  espn_rerank_out lo{};
+  lo.ids = reinterpret_cast<uint32_t*>(blk + kPackHeaderWords);
+  lo.scores = reinterpret_cast<float*>(blk + kPackHeaderWords + (uint64_t)j.BQ * j.k);
+  lo.counts = reinterpret_cast<uint32_t*>(blk + kPackHeaderWords + 2ull * j.BQ * j.k);
+  if (j.replica) {
+    // rows this rank does not own stay empty (count 0)
+    ESPN_CUDA_TRY(cudaMemsetAsync(lo.counts, 0, (size_t)j.BQ * 4, s));
+    const uint32_t b0 = std::min<uint32_t>(j.B, j.g * j.BQ), b1 = std::min<uint32_t>(j.B, b0 + j.BQ);
+    la.n_queries = b1 - b0;
+    la.query_tokens = j.q + (size_t)b0 * j.nq * t->d;
+    la.cand_ids = j.ids;
+    la.cand_cls = j.cls;
+    la.cand_offsets = j.off + b0;
+    la.needed_counts = j.need ? j.need + b0 : nullptr;
+    la.flags |= kFlagBaseOffsets;
+  } else {
+    ShardSplitParams sp{};
+    sp.ids = j.ids;
+    sp.cls = j.cls;
+    sp.off = j.off;
+    sp.need_in = j.need;
+    sp.n_queries = j.B;
+    sp.rerank_count = a->rerank_count;
+    sp.shards = j.G;
+    sp.shard = j.g;
+    sp.max_candidates = C;
+    sp.loc_off = h.loc_off;
+    sp.loc_need = h.loc_need;
+    sp.loc_ids = h.loc_ids;
+    sp.loc_cls = h.loc_cls;
+    sp.err = w->err;
+    if (j.B) {
+      shard_count_kernel<<<j.B, kShardThreads, 0, s>>>(sp);
+      scan_u64_kernel<<<1, 1024, 0, s>>>(h.loc_off, j.B);
+      shard_scatter_kernel<<<j.B, kShardThreads, 0, s>>>(sp);
+      ESPN_CUDA_TRY(cudaGetLastError());
+      w->counters.kernel_launches += 3;
+    }
+    la.cand_ids = h.loc_ids;
+    la.cand_cls = h.loc_cls;
+    la.cand_offsets = h.loc_off;
+    la.needed_counts = h.loc_need;
+    la.query_tokens = j.q;
+  }
+  if (la.n_queries) {
+    const int st = espn_gpu_rerank(t, w, &la, &lo, s);
+    if (st) return st;
+  }
+  pack_err_kernel<<<1, 32, 0, s>>>(w->err, blk);
+  ESPN_CUDA_TRY(cudaGetLastError());
+  w->counters.kernel_launches += 1;
+  return ESPN_OK;
+}
+
+// Phase 3: the G gathered blocks -> the global ranked lists (+ every rank's
+// error bits), outputs, and for synchronous calls the verdict.
+int shard_merge(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a, const ShardJob& j,
+                const int32_t* recv, espn_rerank_out* o, cudaStream_t s) {
+  (void)t;
+  if (!o || !o->ids || !o->scores || !o->counts) return fail(ESPN_E_INVALID_INPUT, "null output array");
+  const bool dev_io = (a->flags & ESPN_RERANK_DEVICE_IO) != 0;
+  uint32_t* oi = dev_io ? o->ids : w->out_ids;
+  float* os = dev_io ? o->scores : w->out_scores;
+  uint32_t* oc = dev_io ? o->counts : w->out_counts;
+  if (j.B) {
+    if (j.replica) {
+      unpack_replica_kernel<<<j.B, 128, 0, s>>>(recv, j.G, j.P, j.B, j.BQ, j.k, oi, os, oc, w->err);
+    } else {
+      ESPN_CUDA_TRY(ensure_topk_attr());
+      merge_packed_kernel<<<j.B, kTopkThreads, topk_smem_bytes(), s>>>(recv, j.G, j.P, j.B, j.k, oi, os, oc, w->err);
+    }
+    ESPN_CUDA_TRY(cudaGetLastError());
+    w->counters.kernel_launches += 1;
+  }
+  if (!dev_io && j.B) {
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->ids, oi, (size_t)j.B * j.k * 4, cudaMemcpyDeviceToHost, s));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->scores, os, (size_t)j.B * j.k * 4, cudaMemcpyDeviceToHost, s));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(o->counts, oc, (size_t)j.B * 4, cudaMemcpyDeviceToHost, s));
+  }
+  w->counters.batches += 1;
+  w->counters.queries += j.B;
+  if (a->flags & ESPN_RERANK_ASYNC) {
+    w->async_pending = true;
+    return ESPN_OK;
+  }
+  ESPN_CUDA_TRY(cudaMemcpyAsync(w->h_err, w->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+  if (*w->h_err) ESPN_CUDA_TRY(cudaMemsetAsync(w->err, 0, sizeof(uint32_t), s));
+  w->async_pending = false;
+  return err_bits_to_status(*w->h_err);
+}
+
+int shard_recv_buffer(espn_gpu_workspace* w, const ShardJob& j, cudaStream_t s) {
+  auto& h = w->sh;
+  if (h.recv_cap >= j.P * j.G) return ESPN_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  ESPN_CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+  if (cap != cudaStreamCaptureStatusNone)
+    return fail(ESPN_E_INVALID_STATE, "sharded re-rank: run one call of this shape outside the stream capture first");
+  uint64_t rc = h.recv_cap * 4;
+  const cudaError_t e = grow(reinterpret_cast<void**>(&h.recv), &rc, j.P * j.G * 4);
+  if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("sharded recv buffer: ") + cudaGetErrorString(e));
+  h.recv_cap = rc / 4;
+  return ESPN_OK;
+}
+
+int comm_shape(void* comm, uint32_t* nranks, uint32_t* rank, int* device) {
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return fail(ESPN_E_CUDA, n.why);
+  if (!comm) return fail(ESPN_E_INVALID_INPUT, "null NCCL communicator");
+  int c = 0, r = 0, d = 0;
+  ESPN_NCCL_TRY(n.CommCount(static_cast<ncclComm_t>(comm), &c));
+  ESPN_NCCL_TRY(n.CommUserRank(static_cast<ncclComm_t>(comm), &r));
+  ESPN_NCCL_TRY(n.CommCuDevice(static_cast<ncclComm_t>(comm), &d));
+  *nranks = (uint32_t)c;
+  *rank = (uint32_t)r;
+  *device = d;
+  return ESPN_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int espn_nccl_get_unique_id(espn_nccl_id* out) {
+  if (!out) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return fail(ESPN_E_CUDA, n.why);
+  static_assert(sizeof(espn_nccl_id) == sizeof(ncclUniqueId), "id size");
+  ncclUniqueId id;
+  ESPN_NCCL_TRY(n.GetUniqueId(&id));
+  std::memcpy(out, &id, sizeof id);
+  return ESPN_OK;
+}
+
+int espn_nccl_comm_init(int nranks, const espn_nccl_id* id, int rank, int device, void** comm) {
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(ESPN_E_INVALID_INPUT, "bad argument");
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return fail(ESPN_E_CUDA, n.why);
+  DeviceGuard g(device);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  ncclComm_t c = nullptr;
+  ESPN_NCCL_TRY(n.CommInitRank(&c, nranks, uid, rank));
+  *comm = c;
+  return ESPN_OK;
+}
+
+int espn_nccl_comm_init_all(int ndev, const int* devices, void** comms) {
+  if (ndev < 1 || !devices || !comms) return fail(ESPN_E_INVALID_INPUT, "bad argument");
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return fail(ESPN_E_CUDA, n.why);
+  std::vector<ncclComm_t> c(ndev, nullptr);
+  ESPN_NCCL_TRY(n.CommInitAll(c.data(), ndev, devices));
+  for (int i = 0; i < ndev; ++i) comms[i] = c[i];
+  return ESPN_OK;
+}
+
+int espn_nccl_comm_destroy(void* comm) {
+  if (!comm) return ESPN_OK;
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return fail(ESPN_E_CUDA, n.why);
+  ESPN_NCCL_TRY(n.CommDestroy(static_cast<ncclComm_t>(comm)));
+  return ESPN_OK;
+}
+
+int espn_gpu_shard_pack(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a, uint32_t nranks,
+                        uint32_t rank, void* stream, const int32_t** send, uint64_t* words) {
+  ShardJob j;
+  int st = shard_validate(t, w, a, nranks, rank, &j);
+  if (st) return st;
+  DeviceGuard g(t->device);
+  st = shard_pack(t, w, a, j, static_cast<cudaStream_t>(stream));
+  if (st) return st;
+  if (send) *send = w->sh.send;
+  if (words) *words = j.P;
+  return ESPN_OK;
+}
+
+int espn_gpu_shard_merge(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a, const int32_t* recv,
+                         uint32_t nranks, espn_rerank_out* out, void* stream) {
+  ShardJob j;
+  // the rank only matters for the pack; the merge is rank-independent
+  const uint32_t r = (t && t->shard_count > 1) ? t->shard_index : 0;
+  int st = shard_validate(t, w, a, nranks, r, &j);
+  if (st) return st;
+  if (!recv) return fail(ESPN_E_INVALID_INPUT, "null recv");
+  DeviceGuard g(t->device);
+  return shard_merge(t, w, a, j, recv, out, static_cast<cudaStream_t>(stream));
+}
+
+int espn_gpu_rerank_sharded(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a, espn_rerank_out* o,
+                            void* comm, void* stream) {
+  uint32_t G = 0, r = 0;
+  int cdev = 0;
+  int st = comm_shape(comm, &G, &r, &cdev);
+  if (st) return st;
+  ShardJob j;
+  st = shard_validate(t, w, a, G, r, &j);
+  if (st) return st;
+  if (cdev != t->device) return fail(ESPN_E_INVALID_CONFIG, "NCCL communicator and table are on different devices");
+  DeviceGuard g(t->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = shard_recv_buffer(w, j, s);
+  if (!st) st = shard_pack(t, w, a, j, s);
+  if (st) return st;
+  const NcclApi& n = nccl_api();
+  ESPN_NCCL_TRY(n.AllGather(w->sh.send, w->sh.recv, j.P, ncclInt32, static_cast<ncclComm_t>(comm), s));
+  return shard_merge(t, w, a, j, w->sh.recv, o, s);
+}
+
+int espn_gpu_rerank_sharded_multi(uint32_t n, espn_gpu_table* const* tables, espn_gpu_workspace* const* ws,
+                                  const espn_rerank_args* a, espn_rerank_out* outs, void* const* comms,
+                                  void* const* streams) {
+  if (n == 0) return ESPN_OK;
+  if (!tables || !ws || !a || !outs || !comms || !streams) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  std::vector<ShardJob> jobs(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    uint32_t G = 0, r = 0;
+    int cdev = 0;
+    int st = comm_shape(comms[i], &G, &r, &cdev);
+    if (st) return st;
+    if (G != n) return fail(ESPN_E_INVALID_CONFIG, "every device of the call needs one rank of an n-rank communicator");
+    st = shard_validate(tables[i], ws[i], a, G, r, &jobs[i]);
+    if (st) return st;
+    if (cdev != tables[i]->device) return fail(ESPN_E_INVALID_CONFIG, "communicator / table device mismatch");
+  }
+  // phase 1 on every device, then the all-gathers as ONE group (one thread
+  // drives several ranks), then the merges; synchronous calls sync at the end
+  espn_rerank_args aa = *a;
+  aa.flags |= ESPN_RERANK_ASYNC;
+  for (uint32_t i = 0; i < n; ++i) {
+    DeviceGuard g(tables[i]->device);
+    cudaStream_t s = static_cast<cudaStream_t>(streams[i]);
+    int st = shard_recv_buffer(ws[i], jobs[i], s);
+    if (!st) st = shard_pack(tables[i], ws[i], a, jobs[i], s);
+    if (st) return st;
+  }
+  const NcclApi& nc = nccl_api();
+  ESPN_NCCL_TRY(nc.GroupStart());
+  for (uint32_t i = 0; i < n; ++i) {
+    DeviceGuard g(tables[i]->device);
+    const ncclResult_t r = nc.AllGather(ws[i]->sh.send, ws[i]->sh.recv, jobs[i].P, ncclInt32,
+                                        static_cast<ncclComm_t>(comms[i]), static_cast<cudaStream_t>(streams[i]));
+    if (r != ncclSuccess) {
+      nc.GroupEnd();
+      return fail(ESPN_E_CUDA, std::string("ncclAllGather: ") + nc.GetErrorString(r));
+    }
+  }
+  ESPN_NCCL_TRY(nc.GroupEnd());
+  for (uint32_t i = 0; i < n; ++i) {
+    DeviceGuard g(tables[i]->device);
+    const int st = shard_merge(tables[i], ws[i], &aa, jobs[i], ws[i]->sh.recv, &outs[i],
+                               static_cast<cudaStream_t>(streams[i]));
+    if (st) return st;
+  }
+  if (a->flags & ESPN_RERANK_ASYNC) return ESPN_OK;
+  int worst = ESPN_OK;
+  for (uint32_t i = 0; i < n; ++i) {
+    const int st = espn_gpu_workspace_sync(ws[i], streams[i]);
+    if (st && !worst) worst = st;
+  }
+  return worst;
 }
 
 }  // extern "C"

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q) 
   uint64_t woff = 0;
   for (uint32_t i = 0; i < wid; ++i) woff += wsum[i];
   const uint64_t excl = base + woff + incl - u;
-  if (tid == 0 && q.cand_off[0] != 0) bad = true;
+  if (tid == 0 && q.cand_off[0] != 0 && !q.base_ok) bad = true;  // base_ok: a slice of a larger CSR
   const bool last = b + 1 == q.n_queries;
   bool over = false;
   if (last && (q.cand_off[q.n_queries] > q.max_candidates || excl + u > q.max_units)) over = true;
