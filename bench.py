@@ -293,6 +293,325 @@ def tiered_bandwidth_model(rr, dbs, pcfg, out, main, side, res_mode, B, n_batche
                                         "host-tier misses the tier delivers while one batch scores"}}
 
 
+
+# ------------------------------------------------------------------ ranks
+def init_ranks():
+    """One process per GPU (torchrun env).  torch.distributed is the control
+    plane only (barriers, max over ranks, the NCCL unique-id broadcast); the
+    data-path collective is the library's own NCCL communicator.  Ranks that
+    share a GPU (fewer GPUs than ranks: a harness check on a 1-GPU box) use
+    gloo, since NCCL refuses two ranks on one device."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = max(torch.cuda.device_count(), 1)
+    shared = world > ndev
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    if world > 1:
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    return world, rank, local, dev, shared
+
+
+def rank_sync(world, dev):
+    import torch
+    import torch.distributed as dist
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        if dist.get_backend() == "nccl":
+            t = t.to(dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return barrier, max_over_ranks
+
+
+# ------------------------------------------------------------------ multi-GPU arm
+def run_sharded(args, cfg, placement):
+    """N GPUs through the library's multi-GPU call (espn_gpu_rerank_sharded):
+    every rank gets the SAME global batch of configs' stated size; SHARD = the
+    table is doc-id sharded (owner = id % N), each rank scores its own
+    candidates and one ncclAllGather of the packed local top-k + merge gives
+    every rank the global lists; REPLICA-SPLIT = every rank holds the whole
+    table and scores 1/N of the queries.  Total work is fixed -> "strong"."""
+    import torch
+    import torch.distributed as dist
+    from paper_2312_05417_b200 import _lib as L
+    from paper_2312_05417_b200 import api, sharding
+
+    world, rank, local, dev, shared = init_ranks()
+    G, g = world, rank
+    lib = L.lib()
+    barrier, max_over_ranks = rank_sync(world, dev)
+    shard = placement == "shard"
+    exchange = args.exchange if args.exchange != "auto" else ("gloo" if shared else "nccl")
+    if exchange == "nccl" and shared:
+        raise SystemExit("NCCL needs one GPU per rank; use --exchange gloo for a shared-GPU harness check")
+    # ---- the table: shard g (SHARD) or the whole table (REPLICA-SPLIT) ----
+    TG, Tg = (G, g) if shard else (1, 0)
+    n_local = (cfg["n_docs"] - Tg + TG - 1) // TG
+    t0 = time.time()
+    row_ptr = torch.zeros(n_local + 1, dtype=torch.int64, device=dev)
+    assert lib.espn_gpu_synth_table(n_local, cfg["d"], 0, cfg["t_min"], cfg["t_max"], SEED, TG, Tg,
+                                    row_ptr.data_ptr(), None, None) == 0, L.last_error()
+    n_tok = int(row_ptr[-1])
+    rows = torch.empty(n_tok * cfg["d"], dtype=torch.int16, device=dev)
+    assert lib.espn_gpu_synth_table(n_local, cfg["d"], 0, cfg["t_min"], cfg["t_max"], SEED, TG, Tg,
+                                    row_ptr.data_ptr(), rows.data_ptr(), None) == 0, L.last_error()
+    store = api.GpuStore.from_device(row_ptr, rows, cfg["d"], "f16", shard_count=TG, shard_index=Tg,
+                                     device=dev.index, rows_tiled=True)
+    log(f"[rank {rank}] {placement}: table {Tg}/{TG}: {n_local} docs, {n_tok * cfg['d'] * 2 / 1e9:.1f} GB "
+        f"in {time.time() - t0:.1f}s")
+    B, K, R, k, nq, d = cfg["batch"], cfg["K"], cfg["R"], cfg["k"], cfg["nq"], cfg["d"]
+    n_batches = cfg.get("n_batches", N_BATCHES)
+    batches = make_batches(cfg, n_batches, B)  # the same global batches on every rank
+    bq = -(-B // G)
+    b0, b1 = min(B, g * bq), min(B, g * bq + bq)
+    dev_batches = []
+    for bt in batches:
+        ids, off = bt["ids"], bt["off"]
+        # this rank's MaxSim rows (roofline accounting): own needed docs
+        if shard:
+            s_ids, _, s_off, s_need = sharding.split_by_owner(ids, bt["cls"], off, R, G, g)
+            pos = np.arange(s_ids.size) - np.repeat(s_off[:-1].astype(np.int64), np.diff(s_off.astype(np.int64)))
+            mine = s_ids[pos < np.repeat(s_need.astype(np.int64), np.diff(s_off.astype(np.int64)))]
+            loc = torch.from_numpy((mine // G).astype(np.int64)).to(dev)
+        else:
+            sel = np.concatenate([ids[int(off[b]):int(off[b]) + min(R, int(off[b + 1] - off[b]))]
+                                  for b in range(b0, b1)]) if b1 > b0 else np.zeros(0, np.uint32)
+            loc = torch.from_numpy(sel.astype(np.int64)).to(dev)
+        row_bytes = int((row_ptr[loc + 1] - row_ptr[loc]).sum()) * d * 2 if loc.numel() else 0
+        dev_batches.append(dict(q=torch.from_numpy(bt["q"]).to(dev), ids=torch.from_numpy(ids.view(np.int32)).to(dev),
+                                cls=torch.from_numpy(bt["cls"]).to(dev), doff=torch.from_numpy(off.astype(np.int64)).to(dev),
+                                off=off, row_bytes=row_bytes, n_local_q=(B if shard else b1 - b0), glob=bt))
+    QP = {"auto": 0, "split": L.ESPN_RERANK_QUERY_SPLIT, "rounded": L.ESPN_RERANK_QUERY_ROUNDED}[args.query_precision]
+    flags = (L.ESPN_RERANK_DEVICE_IO | L.ESPN_RERANK_DEVICE_OFFSETS | L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_PROFILE
+             | QP)
+
+    def new_comm():
+        uid = [api.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        return api.NcclComm(G, uid[0], g, dev.index)
+
+    class Lane:
+        def __init__(self):
+            self.rr = api.Reranker(store, B, B * K, nq, max_list=K)
+            self.out = (torch.zeros((B, k), dtype=torch.int32, device=dev),
+                        torch.zeros((B, k), dtype=torch.float32, device=dev), torch.zeros(B, dtype=torch.int32, device=dev))
+            self.comm = new_comm() if exchange == "nccl" else None
+            self.stream = torch.cuda.Stream()
+            self.graphs = []
+
+        def args(self, db, fl, host=None):
+            if host is None:
+                return L.RerankArgs(n_queries=B, n_query_tokens=nq, query_tokens=db["q"].data_ptr(),
+                                    cand_ids=db["ids"].data_ptr(), cand_cls=db["cls"].data_ptr(),
+                                    cand_offsets=db["doff"].data_ptr(), rerank_count=R, final_k=k, alpha=1.0,
+                                    flags=fl, kernel=L.ESPN_KERNEL_AUTO)
+            return L.RerankArgs(n_queries=B, n_query_tokens=nq, query_tokens=host["q"].data_ptr(),
+                                cand_ids=host["ids"].data_ptr(), cand_cls=host["cls"].data_ptr(),
+                                cand_offsets=host["off"].ctypes.data, rerank_count=R, final_k=k, alpha=1.0,
+                                flags=fl, kernel=L.ESPN_KERNEL_AUTO)
+
+        def enqueue(self, db, sp, fl=flags, host=None, hout=None):
+            a = self.args(db, fl, host)
+            outs = hout if hout is not None else self.out
+            o = L.RerankOut(ids=outs[0].data_ptr(), scores=outs[1].data_ptr(), counts=outs[2].data_ptr())
+            if exchange == "nccl":
+                rc = lib.espn_gpu_rerank_sharded(store.handle, self.rr.handle, C.byref(a), C.byref(o),
+                                                 self.comm.handle, C.c_void_p(sp))
+                if rc:
+                    raise RuntimeError(L.last_error())
+                return
+            # gloo harness exchange (ranks share a GPU): pack -> host all-gather -> merge
+            send, words = C.c_void_p(), C.c_uint64()
+            rc = lib.espn_gpu_shard_pack(store.handle, self.rr.handle, C.byref(a), G, g, C.c_void_p(sp),
+                                         C.byref(send), C.byref(words))
+            if rc:
+                raise RuntimeError(L.last_error())
+            blk = torch.empty(int(words.value), dtype=torch.int32)
+            torch.cuda.synchronize()
+            C.CDLL("libcudart.so.12").cudaMemcpy(C.c_void_p(blk.data_ptr()), send, C.c_size_t(4 * blk.numel()), 2)
+            parts = [torch.empty_like(blk) for _ in range(G)]
+            dist.all_gather(parts, blk)
+            recv = torch.cat(parts).to(dev)
+            rc = lib.espn_gpu_shard_merge(store.handle, self.rr.handle, C.byref(a), recv.data_ptr(), G, C.byref(o),
+                                          C.c_void_p(sp))
+            torch.cuda.synchronize()
+            if rc:
+                raise RuntimeError(L.last_error())
+
+    lanes = [Lane() for _ in range(max(1, args.inflight if exchange == "nccl" else 1))]
+    NL = len(lanes)
+    stream = torch.cuda.current_stream()
+    for ln in lanes:
+        for i in range(3):  # eager: sizes the exchange buffers, NCCL warm-up
+            ln.enqueue(dev_batches[i % n_batches], ln.stream.cuda_stream)
+        ln.stream.synchronize()
+        ln.rr.sync(ln.stream.cuda_stream)
+        if exchange == "nccl":
+            for db in dev_batches:
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=ln.stream):
+                    ln.enqueue(db, torch.cuda.current_stream().cuda_stream)
+                ln.graphs.append(gr)
+
+    def replay(st):
+        ln = lanes[st % NL]
+        if ln.graphs:
+            with torch.cuda.stream(ln.stream):
+                ln.graphs[st % n_batches].replay()
+        else:
+            ln.enqueue(dev_batches[st % n_batches], ln.stream.cuda_stream)
+
+    for i in range(args.warmup):
+        replay(i)
+    barrier()
+    for ln in lanes:
+        ln.rr.sync(ln.stream.cuda_stream)
+
+    def counters():
+        cs = [ln.rr.counters() for ln in lanes]
+        return {key: sum(c[key] for c in cs) for key in ("maxsim_device_ns", "maxsim_device_launches")}
+
+    with ClockSampler(dev.index) as clk:
+        c0 = counters()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for ln in lanes:
+            ln.stream.wait_event(e0)
+        for st in range(args.steps):
+            replay(st)
+        for ln in lanes:
+            stream.wait_event(ln.stream.record_event())
+        e1.record(stream)
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        c1 = counters()
+    clocks = clk.summary()
+    for ln in lanes:
+        ln.rr.sync(ln.stream.cuda_stream)
+    # per-batch latency (one batch at a time)
+    ln0 = lanes[0]
+    lat = []
+    for st in range(min(args.steps, 64)):
+        barrier()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(ln0.stream)
+        if ln0.graphs:
+            with torch.cuda.stream(ln0.stream):
+                ln0.graphs[st % n_batches].replay()
+        else:
+            ln0.enqueue(dev_batches[st % n_batches], ln0.stream.cuda_stream)
+        b_.record(ln0.stream)
+        b_.synchronize()
+        lat.append(a_.elapsed_time(b_))
+    p50 = max_over_ranks(float(np.percentile(lat, 50)))
+    p99 = max_over_ranks(float(np.percentile(lat, 99)))
+    # check: the global lists on every rank put each query's source doc first
+    barrier()
+    if ln0.graphs:
+        with torch.cuda.stream(ln0.stream):
+            ln0.graphs[0].replay()
+    else:
+        ln0.enqueue(dev_batches[0], ln0.stream.cuda_stream)
+    torch.cuda.synchronize()
+    top = ln0.out[0][:, 0].cpu().numpy().view(np.uint32)
+    src = dev_batches[0]["glob"]["ids"].reshape(B, K)[:, 0]
+    src_ok = float(np.mean(top == src))
+    # e2e: host arrays in (pinned), global lists out (pinned), same call
+    def pinned(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    e2e_in = [dict(q=pinned(db["glob"]["q"]), ids=pinned(db["glob"]["ids"].view(np.int32)),
+                   cls=pinned(db["glob"]["cls"]), off=db["off"]) for db in dev_batches]
+    h_out = [[pinned(np.zeros((B, k), np.int32)), pinned(np.zeros((B, k), np.float32)), pinned(np.zeros(B, np.int32))]
+             for _ in range(NL)]
+    fl_e2e = L.ESPN_RERANK_ASYNC | QP
+    for i in range(max(args.warmup, 3)):
+        lanes[i % NL].enqueue(None, lanes[i % NL].stream.cuda_stream, fl_e2e, e2e_in[i % n_batches], h_out[i % NL])
+    barrier()
+    t0 = time.perf_counter()
+    for st in range(args.steps):
+        ln = lanes[st % NL]
+        ln.stream.synchronize()  # this lane's pinned outputs are free again
+        ln.enqueue(None, ln.stream.cuda_stream, fl_e2e, e2e_in[st % n_batches], h_out[st % NL])
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    for ln in lanes:
+        ln.rr.sync(ln.stream.cuda_stream)
+    last = h_out[(args.steps - 1) % NL][0].numpy()[:, 0].view(np.uint32)
+    src_last = dev_batches[(args.steps - 1) % n_batches]["glob"]["ids"].reshape(B, K)[:, 0]
+    e2e_ok = float(np.mean(last == src_last))
+    db0 = dev_batches[0]
+    h2d = db0["glob"]["q"].nbytes + db0["glob"]["ids"].nbytes + db0["glob"]["cls"].nbytes + (B + 1) * 8
+    d2h = B * k * 8 + B * 4 + 4
+    n_prof = c1["maxsim_device_launches"] - c0["maxsim_device_launches"]
+    maxsim_ms = (c1["maxsim_device_ns"] - c0["maxsim_device_ns"]) / max(n_prof, 1) / 1e6
+    alg = [db["row_bytes"] + db["n_local_q"] * nq * d * 2 + int(db["off"][-1]) * 8 + B * k * 8
+           for db in (dev_batches[st % n_batches] for st in range(args.steps))]
+    alg_bytes = float(np.mean(alg))
+    try:
+        peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except (OSError, KeyError, ValueError):
+        peak, peak_src = 6650.0, "B200_PROFILING.md fallback 6.65 TB/s (MEASURED_PEAKS.json absent)"
+    achieved = alg_bytes / (maxsim_ms / 1e3) / 1e9 if maxsim_ms > 0 else None
+    cnt = lanes[0].rr.counters()
+    n_launch = int(round(args.steps * cnt["kernel_launches"] / max(cnt["batches"], 1)))
+    value = B * args.steps / (ms / 1e3)
+    res = {"metric": BASE_METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f16",
+           "data": "synthetic: seeded counter-RNG unit-norm fp16 token rows (t~U{%d..%d}); queries = perturbed rows "
+                   "of a source doc; K-1 uniform random candidates + source" % (cfg["t_min"], cfg["t_max"]),
+           "config": {"workload": cfg["workload"], "n_docs": cfg["n_docs"], "d": d, "query_tokens": nq,
+                      "global_batch": B, "candidates_K": K, "rerank_R": R, "final_k": k, "placement": placement,
+                      "parallelism": (f"doc-id shards x{G} (owner = id % {G}), per-shard top-k, one ncclAllGather of "
+                                      f"the packed lists + merge (espn_gpu_rerank_sharded)" if shard else
+                                      f"{G} replicas, each scoring {bq} of the {B} queries, one ncclAllGather "
+                                      f"(espn_gpu_rerank_sharded)")
+                                     + ("" if exchange == "nccl" else
+                                        " [exchange over gloo/host: ranks share a GPU -- harness check, not a "
+                                        "performance number]"),
+                      "launch": "one CUDA graph per batch (split -> plan -> tcgen05 MaxSim -> finalize -> "
+                                "ncclAllGather -> merge); %d batches in flight" % NL if lanes[0].graphs else "eager",
+                      "l2": "inputs > L2: each rank gathers ~%.0f MB of random rows per batch"
+                            % (dev_batches[0]["row_bytes"] / 1e6)},
+           "p50_batch_ms": p50, "p99_batch_ms": p99,
+           "e2e": {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(d2h)},
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": (achieved / peak) if achieved else None, "traffic": None,
+                        "kernel": f"maxsim_tc_kernel<{d}>", "kernel_ms": maxsim_ms,
+                        "kernel_timing": "device globaltimer, first CTA start -> last CTA end, per launch (rank 0)",
+                        "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                        "step_frac": alg_bytes / (ms / args.steps / 1e3) / 1e9 / peak},
+           "clocks": clocks, "gpu_launches": n_launch,
+           "check": {"source_doc_ranked_first": src_ok, "e2e_source_doc_ranked_first": e2e_ok}}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    for ln in lanes:
+        if ln.comm is not None:
+            ln.comm.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, cfg):
     import torch
@@ -301,15 +620,12 @@ def run_ours(args, cfg):
     from paper_2312_05417_b200 import api
     from paper_2312_05417_b200.sharding import split_by_owner
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    G, g = world, rank
-    emulated = G == 1 and args.emulate_shards > 1
+    world, rank, local, dev, shared = init_ranks()
+    # N > 1 here = independent replicas (placement "replica"): every rank holds
+    # the whole table and serves its own stream of batch-`batch` queries; no
+    # collective on the data path (the table fits one B200)
+    G, g = 1, 0
+    emulated = world == 1 and args.emulate_shards > 1
     if emulated:  # one GPU runs shard 0 of an emulate_shards-way doc-id sharding (no collective)
         G, g = args.emulate_shards, 0
     lib = L.lib()
@@ -329,12 +645,12 @@ def run_ours(args, cfg):
     log(f"[rank {rank}] table shard {g}/{G}: {n_local} docs, {n_tok} tokens, "
         f"{n_tok * cfg['d'] * 2 / 1e9:.1f} GB in {time.time() - t0:.1f}s")
 
-    # global batch: weak scaling keeps per-GPU pairs fixed; an emulated shard
-    # scores its 1/G share of the configuration's own batch
-    B_q = cfg["batch"] if emulated else cfg["batch"] * G
+    # per-rank batch = the configuration's batch (replicas: each rank its own
+    # queries, seeded by rank); an emulated shard scores its 1/G share of it
+    B_q = cfg["batch"]
     t0 = time.time()
     n_batches = cfg.get("n_batches", N_BATCHES)
-    batches = make_batches(cfg, n_batches, B_q)
+    batches = make_batches(cfg, n_batches, B_q, seed=SEED + 1000 * rank)
     log(f"[rank {rank}] {n_batches} candidate batches of {B_q} queries in {time.time() - t0:.1f}s")
     K, R, k, nq, d = cfg["K"], cfg["R"], cfg["k"], cfg["nq"], cfg["d"]
     dev_batches = []
@@ -356,7 +672,7 @@ def run_ours(args, cfg):
             dneed=torch.from_numpy(need.astype(np.int32)).to(dev),
             row_bytes=row_bytes, n_pairs=int(need.sum()), h_ids=ids, h_cls=cls, h_q=bt["q"], glob=bt))
     max_list = max(int(np.diff(db["off"]).max()) for db in dev_batches)
-    P = 2 * B_q * k + B_q  # packed [ids | scores | counts] per rank
+    P = 2 * B_q * k + B_q  # packed [ids | scores | counts]
     QP = {"auto": 0, "split": L.ESPN_RERANK_QUERY_SPLIT, "rounded": L.ESPN_RERANK_QUERY_ROUNDED}[args.query_precision]
     flags = L.ESPN_RERANK_DEVICE_IO | L.ESPN_RERANK_DEVICE_OFFSETS | L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_PROFILE | QP
 
@@ -369,19 +685,13 @@ def run_ours(args, cfg):
         def __init__(self):
             self.rr = api.Reranker(store, B_q, max(max_c, 1), nq, max_list=max_list)
             self.packed = torch.zeros(P, dtype=torch.int32, device=dev)
-            self.gathered = torch.zeros(G * P, dtype=torch.int32, device=dev) if world > 1 else None
-            self.m_ids = torch.zeros((B_q, k), dtype=torch.int32, device=dev)
-            self.m_sc = torch.zeros((B_q, k), dtype=torch.float32, device=dev)
-            self.m_cnt = torch.zeros(B_q, dtype=torch.int32, device=dev)
-            self.pg = dist.new_group(backend="nccl") if world > 1 else None
             self.stream = torch.cuda.Stream()
             self.graphs = []
 
         def enqueue(self, db, stream_ptr, flags=flags, host=None):
             """One step on `stream_ptr`: device-planned re-rank (plan -> tcgen05
-            MaxSim with fused ranking -> finalize merge) and, sharded, the
-            all-gather + merge.  host = (q, ids, cls) pinned tensors + host
-            offsets for the public host-buffer call (e2e)."""
+            MaxSim with fused ranking -> finalize merge).  host = (q, ids, cls)
+            pinned tensors + host offsets for the public host-buffer call (e2e)."""
             base = self.packed.data_ptr()
             if host is None:
                 a = L.RerankArgs(n_queries=B_q, n_query_tokens=nq, query_tokens=db["q"].data_ptr(),
@@ -395,38 +705,12 @@ def run_ours(args, cfg):
                                  cand_ids=hq["ids"].data_ptr(), cand_cls=hq["cls"].data_ptr(),
                                  cand_offsets=hq["off"].ctypes.data, rerank_count=R, final_k=k, alpha=1.0,
                                  flags=flags, kernel=L.ESPN_KERNEL_AUTO, needed_counts=hq["need"].ctypes.data)
-                o = (L.RerankOut(ids=hout[0].data_ptr(), scores=hout[1].data_ptr(), counts=hout[2].data_ptr())
-                     if world == 1 else L.RerankOut(ids=base, scores=base + 4 * B_q * k, counts=base + 8 * B_q * k))
+                o = L.RerankOut(ids=hout[0].data_ptr(), scores=hout[1].data_ptr(), counts=hout[2].data_ptr())
             rc = lib.espn_gpu_rerank(store.handle, self.rr.handle, C.byref(a), C.byref(o), C.c_void_p(stream_ptr))
             if rc:
                 raise RuntimeError(L.last_error())
-            if world > 1:
-                with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr)):
-                    dist.all_gather_into_tensor(self.gathered, self.packed, group=self.pg)
-                gb = self.gathered.data_ptr()
-                rc = lib.espn_gpu_merge_topk(gb, gb + 4 * B_q * k, gb + 8 * B_q * k, G, P, B_q, k,
-                                             self.m_ids.data_ptr(), self.m_sc.data_ptr(), self.m_cnt.data_ptr(),
-                                             C.c_void_p(stream_ptr))
-                if rc:
-                    raise RuntimeError(L.last_error())
-                if host is not None:
-                    with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr)):
-                        host[1][0].copy_(self.m_ids, non_blocking=True)
-                        host[1][1].copy_(self.m_sc, non_blocking=True)
-                        host[1][2].copy_(self.m_cnt, non_blocking=True)
 
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-            torch.cuda.synchronize()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    barrier, max_over_ranks = rank_sync(world, dev)
 
     lanes = [Lane() for _ in range(max(1, args.inflight))]
     NL = len(lanes)
@@ -435,7 +719,7 @@ def run_ours(args, cfg):
     # ---- one CUDA graph per (lane, input batch): a step is a single graph launch ----
     for ln in lanes:
         with torch.cuda.stream(ln.stream):
-            for i in range(3):  # eager warm-up: lazy attributes, NCCL communicator
+            for i in range(3):  # eager warm-up: lazy attributes
                 ln.enqueue(dev_batches[i % n_batches], ln.stream.cuda_stream)
         ln.stream.synchronize()
         ln.rr.sync(ln.stream.cuda_stream)
@@ -469,7 +753,7 @@ def run_ours(args, cfg):
         return {key: sum(c[key] for c in cs) for key in ("maxsim_device_ns", "maxsim_device_launches")}
 
     # ---- clocks: sample during a sustained pre-roll and the timed region ----
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev.index) as clk:
         t_end = time.time() + args.preroll_s
         i = 0
         while time.time() < t_end:
@@ -512,7 +796,7 @@ def run_ours(args, cfg):
     with torch.cuda.stream(ln0.stream):
         ln0.graphs[0].replay()
     torch.cuda.synchronize()
-    top = (ln0.m_ids if world > 1 else ln0.packed[:B_q * k].view(B_q, k))[:, 0].cpu().numpy().view(np.uint32)
+    top = ln0.packed[:B_q * k].view(B_q, k)[:, 0].cpu().numpy().view(np.uint32)
     src = dev_batches[0]["glob"]["ids"].reshape(B_q, K)[:, 0]
     mine = (src % G) == g  # an emulated shard only sees its own share of the sources
     src_ok = float(np.mean(top[mine] == src[mine])) if mine.any() else None
@@ -528,9 +812,6 @@ def run_ours(args, cfg):
     h_outs = [[[pinned(np.zeros((B_q, k), np.int32)), pinned(np.zeros((B_q, k), np.float32)),
                 pinned(np.zeros(B_q, np.int32))] for _ in range(2)] for _ in range(NL)]
     e2e_ev = [[torch.cuda.Event() for _ in range(2)] for _ in range(NL)]
-    if world > 1:  # sharded: host arrays are split per shard; the library takes device copies
-        for hq, db in zip(e2e_in, dev_batches):
-            hq["ids"], hq["cls"] = pinned(db["h_ids"].view(np.int32)), pinned(db["h_cls"])
 
     def e2e_step(i):
         # the public call with HOST buffers, ASYNC: the library stages batch
@@ -540,24 +821,9 @@ def run_ours(args, cfg):
         ln = lanes[i % NL]
         j = (i // NL) % 2
         e2e_ev[i % NL][j].synchronize()
-        ln.enqueue(dev_batches[i % n_batches], ln.stream.cuda_stream,
-                   flags=(L.ESPN_RERANK_ASYNC if world == 1 else L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_DEVICE_IO) | QP,
-                   host=(e2e_in[i % n_batches] if world == 1 else _dev_inputs(i), h_outs[i % NL][j]))
+        ln.enqueue(dev_batches[i % n_batches], ln.stream.cuda_stream, flags=L.ESPN_RERANK_ASYNC | QP,
+                   host=(e2e_in[i % n_batches], h_outs[i % NL][j]))
         e2e_ev[i % NL][j].record(ln.stream)
-
-    if world > 1:
-        d_in = [dict(q=torch.empty_like(dev_batches[0]["q"]), ids=torch.empty(max_c, dtype=torch.int32, device=dev),
-                     cls=torch.empty(max_c, dtype=torch.float32, device=dev)) for _ in range(NL)]
-
-    def _dev_inputs(i):
-        """Sharded e2e: H2D of this rank's share into device buffers on the lane's stream."""
-        ln, hq, dq = lanes[i % NL], e2e_in[i % n_batches], d_in[i % NL]
-        n = hq["ids"].numel()
-        with torch.cuda.stream(ln.stream):
-            dq["q"].copy_(hq["q"], non_blocking=True)
-            dq["ids"][:n].copy_(hq["ids"], non_blocking=True)
-            dq["cls"][:n].copy_(hq["cls"], non_blocking=True)
-        return dict(q=dq["q"], ids=dq["ids"], cls=dq["cls"], off=hq["off"], need=hq["need"])
 
     for i in range(max(args.warmup, 3)):
         e2e_step(i)
@@ -577,7 +843,7 @@ def run_ours(args, cfg):
     e2e_ok = float(np.mean(last[mine_l] == src_last[mine_l])) if mine_l.any() else None
     db0 = dev_batches[0]
     h2d = (db0["h_q"].nbytes + db0["h_ids"].nbytes + db0["h_cls"].nbytes + (B_q + 1) * 8 + B_q * 4)
-    d2h = B_q * k * 8 + B_q * 4 + (4 if world == 1 else 0)
+    d2h = B_q * k * 8 + B_q * 4 + 4
 
     # ---- standalone K1 gather GB/s (copy kernel only, read + write bytes) ----
     gb_ids = dev_batches[0]["ids"]
@@ -627,12 +893,12 @@ def run_ours(args, cfg):
         except ValueError:
             traffic = None
 
-    # our kernels per step, from the library's own launch counter (plan, primer,
-    # MaxSim, finalize; + the NCCL merge kernel when sharded)
+    # our kernels per step, from the library's own launch counter (plan,
+    # MaxSim, finalize)
     c0 = lanes[0].rr.counters()
     per_batch = c0["kernel_launches"] / max(c0["batches"], 1)
-    n_launch_ours = int(round(args.steps * (per_batch + (1 if world > 1 else 0))))
-    q_total = B_q * args.steps  # global queries (each rank scored its share of all of them)
+    n_launch_ours = int(round(args.steps * per_batch))
+    q_total = B_q * args.steps * world  # every replica served its own B_q-query batches
     value = q_total / (ms / 1e3)
     # the L2 claim is computed, not asserted: rows touched per rotation of the
     # batches vs the 126 MB L2, and the table size
@@ -655,12 +921,15 @@ def run_ours(args, cfg):
         "(t~U{%d..%d}); queries = perturbed rows of a source doc; K-1 uniform random candidates + source"
         % (cfg["t_min"], cfg["t_max"]),
         "config": {"workload": cfg["workload"], "n_docs": cfg["n_docs"], "d": d, "query_tokens": nq,
-                   "batch_per_gpu": cfg["batch"], "global_batch": B_q, "candidates_K": K, "rerank_R": R,
-                   "final_k": k,
-                   "parallelism": ("1 GPU" if G == 1 else
+                   "batch_per_gpu": cfg["batch"], "global_batch": B_q * world, "candidates_K": K, "rerank_R": R,
+                   "final_k": k, "placement": "replica" if world > 1 else "single",
+                   "parallelism": ("1 GPU" if world == 1 and G == 1 else
                                    f"1 GPU running shard 0 of a {G}-way doc-id sharding (per-GPU share of the "
                                    f"{G}-GPU workload; no collective)" if emulated else
-                                   f"doc-id shards x{G} + NCCL all-gather merge"),
+                                   f"{world} independent replicas of the whole table, each serving its own "
+                                   f"batch-{B_q} stream (no collective on the data path)"
+                                   + (" [ranks share GPUs: harness check, not a performance number]"
+                                      if shared else "")),
                    "l2": l2_note,
                    "launch": "one CUDA graph per batch (device-planned: plan -> tcgen05 MaxSim with fused ranking -> "
                              "finalize merge); %d batches in flight on separate streams/workspaces" % NL,
@@ -824,15 +1093,40 @@ def main():
     ap.add_argument("--inflight", type=int, default=3,
                     help="batches in flight (one stream + workspace each); the latency percentiles use one")
     ap.add_argument("--query-precision", default="auto", choices=["auto", "split", "rounded"])
+    ap.add_argument("--placement", default="auto", choices=["auto", "replica", "replica-split", "shard"],
+                    help="N>1: replica = independent replicas (weak scaling, no collective); shard / replica-split = "
+                         "the stated global batch through espn_gpu_rerank_sharded (strong scaling); auto: shard for "
+                         "c3/c5, replica otherwise")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "gloo"],
+                    help="sharded data exchange: nccl (one GPU per rank) or gloo through host memory (ranks sharing "
+                         "a GPU, harness check only)")
     ap.add_argument("--emulate-shards", type=int, default=0,
                     help="1 GPU: run shard 0 of an N-way doc-id sharding (the per-GPU share of an N-GPU run)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: become N ranks (one per GPU) under torchrun
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                                   f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]])
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and args.impl != "reference":
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} ranks")
+    placement = args.placement
+    if placement == "auto":  # tables that fit one B200 run as replicas; configs[2]/[4] are doc-id sharded
+        placement = "shard" if args.config in ("c3", "c5") else "replica"
     if args.impl == "reference":
         run_reference(args, cfg)
     elif "resident_frac" in cfg:
         run_tiered(args, cfg)
+    elif world > 1 and placement in ("shard", "replica-split"):
+        run_sharded(args, cfg, placement)
     else:
         run_ours(args, cfg)
 

@@ -120,6 +120,18 @@ SIGNATURES = {
     "espn_gpu_synth_table": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                        C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "espn_gpu_gather_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_nccl_get_unique_id": (C.c_int, [C.c_void_p]),
+    "espn_nccl_comm_init": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "espn_nccl_comm_init_all": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
+    "espn_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
+    "espn_gpu_rerank_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.POINTER(RerankOut),
+                                          C.c_void_p, C.c_void_p]),
+    "espn_gpu_rerank_sharded_multi": (C.c_int, [C.c_uint32, C.c_void_p, C.c_void_p, C.POINTER(RerankArgs),
+                                                C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_gpu_shard_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.c_uint32, C.c_uint32,
+                                      C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
+    "espn_gpu_shard_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.c_void_p, C.c_uint32,
+                                       C.POINTER(RerankOut), C.c_void_p]),
     "espn_last_error": (C.c_char_p, []),
     "espn_abi_version": (C.c_int, []),
 }

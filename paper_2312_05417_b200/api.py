@@ -536,6 +536,86 @@ class Reranker:
             self.last_fetch_stats = [{f: int(getattr(x, f)) for f, _ in L.FetchStats._fields_} for x in fs]
         return out
 
+    # ---- multi-GPU (espn_gpu.h "Multi-GPU") -------------------------
+    def _sharded_args(self, query_tokens, cand_ids, cand_cls, cand_offsets, config, device_io, device_offsets,
+                      sync, needed_counts, query_precision, out):
+        if device_offsets:
+            offs_p, B = _ptr(cand_offsets), int(cand_offsets.numel()) - 1
+            nc_p = _ptr(needed_counts) if needed_counts is not None else None
+            keep = ()
+        else:
+            offs = np.ascontiguousarray(np.asarray(cand_offsets, dtype=np.uint64))
+            offs_p, B = offs.ctypes.data, offs.shape[0] - 1
+            nc = np.ascontiguousarray(needed_counts, dtype=np.uint32) if needed_counts is not None else None
+            nc_p = nc.ctypes.data if nc is not None else None
+            keep = (offs, nc)
+        k = int(config.final_k)
+        if not device_io:
+            query_tokens = np.ascontiguousarray(query_tokens, dtype=np.float32)
+            cand_ids = np.ascontiguousarray(cand_ids, dtype=np.uint32).ravel()
+            cand_cls = np.ascontiguousarray(cand_cls, dtype=np.float32).ravel()
+            if query_tokens.ndim != 3 or query_tokens.shape[0] != B or query_tokens.shape[2] != self.store.d:
+                raise InvalidInputError(f"query_tokens must be (B={B}, q, d={self.store.d})")
+            if B and (cand_ids.size < int(keep[0][-1]) or cand_cls.size < int(keep[0][-1])):
+                raise InvalidInputError("cand_ids / cand_cls shorter than cand_offsets[B]")
+            if out is None:
+                out = (np.zeros((B, k), np.uint32), np.zeros((B, k), np.float32), np.zeros(B, np.uint32))
+        elif out is None:
+            import torch
+            dev = query_tokens.device
+            out = (torch.empty((B, k), dtype=torch.int32, device=dev), torch.empty((B, k), dtype=torch.float32, device=dev),
+                   torch.empty((B,), dtype=torch.int32, device=dev))
+        flags = _QPREC[query_precision]
+        if config.partial_rerank_enabled:
+            flags |= L.ESPN_RERANK_PARTIAL
+        if device_io:
+            flags |= L.ESPN_RERANK_DEVICE_IO
+        if device_offsets:
+            flags |= L.ESPN_RERANK_DEVICE_OFFSETS
+        if not sync:
+            flags |= L.ESPN_RERANK_ASYNC
+        args = L.RerankArgs(n_queries=B, n_query_tokens=int(query_tokens.shape[1]), query_tokens=_ptr(query_tokens),
+                            cand_ids=_ptr(cand_ids), cand_cls=_ptr(cand_cls), cand_offsets=offs_p,
+                            rerank_count=int(config.rerank_count), final_k=k, alpha=float(config.alpha),
+                            flags=flags, kernel=L.ESPN_KERNEL_AUTO, needed_counts=nc_p)
+        o = L.RerankOut(ids=_ptr(out[0]), scores=_ptr(out[1]), counts=_ptr(out[2]))
+        self._keep_sh = (query_tokens, cand_ids, cand_cls, keep, out)
+        return args, o, out
+
+    def rerank_sharded(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig, comm: "NcclComm",
+                       device_io: bool = False, device_offsets: bool = False, out=None, stream=None, sync: bool = True,
+                       needed_counts=None, query_precision: str = "auto"):
+        """espn_gpu_rerank_sharded: every rank passes the SAME global batch
+        (global doc ids) and gets the global ranked lists back; the table's
+        placement (doc-id shard or full replica) decides the split.  Returns
+        (ids[B,k], scores[B,k], counts[B])."""
+        args, o, out = self._sharded_args(query_tokens, cand_ids, cand_cls, cand_offsets, config, device_io,
+                                          device_offsets, sync, needed_counts, query_precision, out)
+        _check(L.lib().espn_gpu_rerank_sharded(self.store.handle, self._h, C.byref(args), C.byref(o), comm.handle,
+                                               C.c_void_p(stream) if stream else None))
+        return out
+
+    def shard_pack(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig, nranks: int,
+                   rank: int, device_io: bool = True, stream=None, query_precision: str = "auto"):
+        """Phase 1 without NCCL: this rank's packed block (device pointer, int32
+        words) in the workspace's send buffer."""
+        args, o, _ = self._sharded_args(query_tokens, cand_ids, cand_cls, cand_offsets, config, device_io, False,
+                                        True, None, query_precision, None)
+        ptr, words = C.c_void_p(), C.c_uint64()
+        _check(L.lib().espn_gpu_shard_pack(self.store.handle, self._h, C.byref(args), int(nranks), int(rank),
+                                           C.c_void_p(stream) if stream else None, C.byref(ptr), C.byref(words)))
+        return int(ptr.value or 0), int(words.value)
+
+    def shard_merge(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig, recv, nranks: int,
+                    device_io: bool = True, out=None, stream=None, query_precision: str = "auto"):
+        """Phase 3 without NCCL: merge nranks gathered blocks (device tensor
+        `recv`) into the global ranked lists."""
+        args, o, out = self._sharded_args(query_tokens, cand_ids, cand_cls, cand_offsets, config, device_io, False,
+                                          True, None, query_precision, out)
+        _check(L.lib().espn_gpu_shard_merge(self.store.handle, self._h, C.byref(args), _ptr(recv), int(nranks),
+                                            C.byref(o), C.c_void_p(stream) if stream else None))
+        return out
+
     def prefetch_hints(self, hint_ids, hint_offsets, stream=None, device_offsets: bool = False):
         """espn_gpu_prefetch_hints: stage the host-tier rows of an approximate
         id list (the IVF snapshot after delta clusters, CSR over queries) on
@@ -599,6 +679,47 @@ class Reranker:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (the bytes every rank passes to NcclComm)."""
+    buf = (C.c_uint8 * 128)()
+    _check(L.lib().espn_nccl_get_unique_id(C.addressof(buf)))
+    return bytes(buf)
+
+
+class NcclComm:
+    """An NCCL communicator created by the library (ncclCommInitRank on
+    `device`); hand the same `uid` (nccl_unique_id() on one rank, broadcast)
+    to every rank."""
+
+    def __init__(self, nranks: int, uid: bytes, rank: int, device: int = 0, handle=None):
+        if handle is not None:
+            self._h = C.c_void_p(handle)
+            return
+        if len(uid) != 128:
+            raise InvalidInputError("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(L.lib().espn_nccl_comm_init(int(nranks), C.addressof(buf), int(rank), int(device), C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def init_all(cls, devices) -> List["NcclComm"]:
+        """ncclCommInitAll: one communicator per device of this process."""
+        devs = (C.c_int * len(devices))(*[int(x) for x in devices])
+        hs = (C.c_void_p * len(devices))()
+        _check(L.lib().espn_nccl_comm_init_all(len(devices), C.addressof(devs), C.addressof(hs)))
+        return [cls(0, b"", 0, handle=hs[i]) for i in range(len(devices))]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            L.lib().espn_nccl_comm_destroy(self._h)
+            self._h = None
 
 
 def _stats_for(store: GpuStore, ids: np.ndarray, n_needed: int, query_id: int, elapsed: float,
