@@ -640,7 +640,7 @@ def run_ours(args, cfg):
     rows = torch.empty(n_tok * cfg["d"], dtype=torch.int16, device=dev)
     assert lib.espn_gpu_synth_table(n_local, cfg["d"], 0, cfg["t_min"], cfg["t_max"], SEED, G, g,
                                     row_ptr.data_ptr(), rows.data_ptr(), None) == 0, L.last_error()
-    store = api.GpuStore.from_device(row_ptr, rows, cfg["d"], "f16", shard_count=G, shard_index=g, device=local,
+    store = api.GpuStore.from_device(row_ptr, rows, cfg["d"], "f16", shard_count=G, shard_index=g, device=dev.index,
                                      rows_tiled=True)
     log(f"[rank {rank}] table shard {g}/{G}: {n_local} docs, {n_tok} tokens, "
         f"{n_tok * cfg['d'] * 2 / 1e9:.1f} GB in {time.time() - t0:.1f}s")

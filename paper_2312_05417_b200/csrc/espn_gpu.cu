@@ -208,8 +208,9 @@ size_t topk_smem_bytes() {
 }
 
 cudaError_t ensure_topk_attr() {
-  static std::atomic<uint64_t> d1{0}, d2{0}, d3{0}, d4{0};
+  static std::atomic<uint64_t> d1{0}, d2{0}, d3{0}, d4{0}, d5{0};
   cudaError_t e = smem_attr_once(topk_kernel, (int)topk_smem_bytes(), d1);
+  if (e == cudaSuccess) e = smem_attr_once(merge_packed_kernel, (int)topk_smem_bytes(), d5);
   if (e == cudaSuccess) e = smem_attr_once(merge_topk_kernel, (int)topk_smem_bytes(), d2);
   if (e == cudaSuccess) e = smem_attr_once(topk_cta_kernel<16>, 8192 * 8 + 8 * 32 * 8, d3);
   if (e == cudaSuccess) e = smem_attr_once(topk_cta_kernel<32>, 8192 * 8 + 8 * 32 * 8, d4);
