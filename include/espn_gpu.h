@@ -280,6 +280,24 @@ ESPN_API int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const
                         uint32_t n_lists, uint64_t list_stride, uint32_t n_queries, uint32_t k,
                         uint32_t* out_ids, float* out_scores, uint32_t* out_counts, void* stream);
 
+/* ---- Persistent re-rank server ---------------------------------
+ * A long-lived tcgen05 MaxSim kernel (one CTA per SM) fed by a device-side
+ * batch queue: a served espn_gpu_rerank enqueues only the plan kernel (which
+ * submits the planned batch to the queue) and a one-thread wait kernel; the
+ * server's CTAs outlive batches, so one batch's start-up (CTA launch, prologue,
+ * first unit's dependent loads) overlaps the previous batch's tail.  Served
+ * batches: untiered table, tcgen05, fused top-k (final_k <= 32), the query
+ * precision the server was started with (flags: ESPN_RERANK_QUERY_*).  While
+ * the server runs, a non-servable tcgen05 batch on this table fails with
+ * INVALID_STATE (it could not get an SM).  The server exits by itself after
+ * idle_us without work (0 = 50 ms) -- a device-wide synchronisation in the
+ * process (cudaDeviceSynchronize, cudaFree) waits at most that long -- and is
+ * relaunched by the next served call made outside a stream capture.  Results
+ * are identical to unserved calls.  espn_gpu_table_close stops it. */
+ESPN_API int espn_gpu_server_start(espn_gpu_table* table, uint32_t flags, uint32_t idle_us);
+ESPN_API int espn_gpu_server_stop(espn_gpu_table* table);
+ESPN_API int espn_gpu_server_running(const espn_gpu_table* table);
+
 /* ---- Multi-GPU --------------------------------
  * One process (rank) per GPU, or one process driving several GPUs.  Every rank
  * passes the SAME global batch (global doc ids; the candidate generator's

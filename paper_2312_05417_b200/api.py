@@ -401,6 +401,21 @@ class GpuStore:
         res.wall_time = time.perf_counter() - t0
         return res
 
+    # ---- persistent re-rank server (espn_gpu.h) ----
+    def server_start(self, query_precision: str = "auto", idle_us: int = 0) -> None:
+        """Launch the persistent MaxSim server: fused tcgen05 batches of this
+        table are then submitted to it (plan + wait kernels per batch, no
+        per-batch MaxSim launch).  It exits after idle_us without work (0 =
+        50 ms) and is relaunched by the next served call."""
+        _check(L.lib().espn_gpu_server_start(self._h, _QPREC[query_precision], int(idle_us)))
+
+    def server_stop(self) -> None:
+        _check(L.lib().espn_gpu_server_stop(self._h))
+
+    @property
+    def server_running(self) -> bool:
+        return bool(L.lib().espn_gpu_server_running(self._h))
+
     def workspace(self, max_queries: int, max_candidates: int, max_query_tokens: int = 32) -> "Reranker":
         return Reranker(self, max_queries, max_candidates, max_query_tokens)
 

@@ -78,7 +78,8 @@ enum : uint32_t {
   ERR_UNIT_TOO_LARGE = 1u << 5,  // internal: slot budget of a work unit exceeded
   ERR_BAD_OFFSETS = 1u << 6,     // cand_offsets not starting at 0 / decreasing -> INVALID_INPUT
   ERR_CAPACITY = 1u << 7,        // batch exceeds workspace capacity -> INVALID_INPUT
-  ERR_STAGING = 1u << 8          // host-tier rows of a batch exceed the staging buffer -> INVALID_CONFIG
+  ERR_STAGING = 1u << 8,         // host-tier rows of a batch exceed the staging buffer -> INVALID_CONFIG
+  ERR_SERVER = 1u << 9           // persistent server: the batch did not complete in time -> INVALID_STATE
 };
 
 // Staging of host-tier rows for one batch (stage_kernel): one CTA per query,
@@ -191,6 +192,7 @@ __device__ __forceinline__ const uint8_t* doc_rows(const uint16_t* rows, const u
   return reinterpret_cast<const uint8_t*>(rows + r0 * d);
 }
 
+struct ServerQueue;
 // One batch of (query, candidate list) pairs, resident on the device.
 struct MaxSimParams {
   const uint16_t* rows;        // table token rows, d codes each
@@ -238,7 +240,69 @@ struct MaxSimParams {
   const uint32_t* fused_state; // {epoch, queries used by parity 0, by parity 1}
   uint32_t hash_slots;         // power of two >= 2 x longest scored list (8x: one-probe inserts)
   uint32_t max_queries;        // parity stride of dedup / ff_seen
+  // Persistent re-rank server: the kernel launch carries only
+  // `server`; each batch's parameters arrive through the server's queue.
+  // done_flag: the workspace's completion flag (set by the server once the
+  // batch's ranked lists are written, consumed by server_wait_kernel).
+  struct ServerQueue* server;
+  uint32_t* done_flag;
 };
+
+// ---- persistent re-rank server: the batch queue in device memory ----------------
+// plan_kernel (the submitter, on the caller's stream) takes seq = tail++,
+// waits for the slot of seq - kServerSlots to be done, writes the batch's
+// MaxSimParams into slot seq % kServerSlots and publishes ready = seq + 1.
+// Every warp of the persistent MaxSim kernel walks seq 0, 1, 2, ...; the
+// rank + dedup warps of all CTAs count the batch done (done_count), the dedup
+// warps merge the queries' unit lists (merge_count), the last one sets the
+// workspace's done_flag and the slot's done = seq + 1.
+constexpr int kServerSlots = 8;
+struct ServerSlot {
+  MaxSimParams p;
+  uint32_t ready;        // seq + 1: published
+  uint32_t done;         // seq + 1: ranked lists written, slot reusable
+  uint32_t done_count;   // rank + dedup warps finished (target 2 x grid)
+  uint32_t merge_count;  // dedup warps finished merging (target grid)
+};
+// state = kServerStopped | next sequence number.  A submitter takes seq =
+// state++ only while not stopped (CAS); a server warp waiting at seq T for a
+// batch that is not there stops the server -- on a host request or after
+// idle_ns without work -- with CAS(state: T -> T | stopped).  Every warp of
+// every CTA then sees "stopped at T" and exits at the same point, and no
+// batch can be taken after it.  An idle server exits by itself so a device-
+// wide synchronisation (cudaFree, cudaDeviceSynchronize) in the process is
+// delayed by at most idle_ns instead of deadlocking; the library relaunches
+// it on the next served batch.
+constexpr unsigned long long kServerStopped = 1ull << 63;
+struct ServerQueue {
+  unsigned long long state;  // kServerStopped | next sequence number
+  uint32_t stop_req;         // host: stop once the queue is drained
+  uint32_t exited;           // CTAs that left the persistent loop
+  unsigned long long idle_ns;
+  uint32_t* alive_host;      // mapped pinned word: 1 while the kernel runs (last CTA out clears it)
+  uint32_t pad[2];
+  ServerSlot slot[kServerSlots];
+};
+// plan_kernel's submission to a running server (server == NULL: none)
+struct ServerSubmit {
+  ServerQueue* server;
+  uint32_t* plan_done;      // per workspace: plan CTAs finished (reset by the submitter)
+  MaxSimParams msp;         // the batch's parameters
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 
 struct TopKParams {

@@ -52,10 +52,12 @@ int err_bits_to_status(uint32_t bits) {
   if (bits & ERR_BAD_OFFSETS) m += " cand_offsets must start at 0 and be non-decreasing;";
   if (bits & ERR_CAPACITY) m += " batch exceeds workspace capacity;";
   if (bits & ERR_STAGING) m += " host-tier rows of the batch exceed the staging buffer (raise staging_bytes);";
+  if (bits & ERR_SERVER) m += " the persistent re-rank server did not complete the batch (stopped or stalled);";
   g_last_error = m;
   if (bits & ERR_UNKNOWN_DOC) return ESPN_E_DATA_INTEGRITY;
   if (bits & ERR_UNIT_TOO_LARGE) return ESPN_E_INVALID_STATE;
   if (bits & ERR_STAGING) return ESPN_E_INVALID_CONFIG;
+  if (bits & ERR_SERVER) return ESPN_E_INVALID_STATE;
   return ESPN_E_INVALID_INPUT;
 }
 
@@ -315,6 +317,14 @@ struct espn_gpu_table {
   uint64_t* doc_loc = nullptr;   // device: per-doc row address | tier bit
   uint8_t* host_rows = nullptr;  // pinned, mapped
   uint64_t hbm_row_bytes = 0, host_row_bytes = 0, resident_docs = 0;
+  // persistent re-rank server (espn_gpu_server_start)
+  ServerQueue* server = nullptr;      // device queue (NULL: no server)
+  cudaStream_t server_stream = nullptr;
+  uint32_t* server_alive_h = nullptr;  // mapped pinned: 1 while the kernel runs
+  bool server_split = false;
+  uint32_t server_dbg = 0;
+  uint64_t server_idle_ns = 0;
+  uint64_t server_launches = 0;
 };
 
 struct espn_gpu_workspace {
@@ -416,6 +426,8 @@ struct espn_gpu_workspace {
   } prof[kProf];
   uint64_t prof_calls = 0;
   espn_counters counters{};
+  uint32_t* done_flag = nullptr;  // persistent server: batch done (server -> server_wait_kernel)
+  uint32_t* plan_done = nullptr;  // persistent server: plan CTAs finished (plan_kernel's submitter)
   // multi-GPU (espn_gpu_rerank_sharded): the global batch staged from host
   // arrays, this shard's own lists, the packed exchange blocks.  Grown on the
   // first sharded call of a shape (never inside a stream capture).
@@ -566,6 +578,144 @@ int launch_stage(espn_gpu_table* t, espn_gpu_workspace* w, int slot, const uint6
 }
 }  // namespace
 
+
+namespace {
+constexpr unsigned long long kServerWaitNs = 30ull * 1000 * 1000 * 1000;  // a batch that takes > 30 s fails
+
+// (Re)launch the persistent MaxSim kernel of table t on its server stream:
+// the previous launch (if any) has exited; the queue is reset and fully
+// written before the kernel starts and before this returns, so work the
+// caller enqueues afterwards sees the fresh queue.
+int server_launch(espn_gpu_table* t) {
+  ESPN_CUDA_TRY(cudaStreamSynchronize(t->server_stream));  // the old kernel is gone
+  ServerQueue init{};
+  init.idle_ns = t->server_idle_ns;
+  init.alive_host = nullptr;
+  uint32_t* alive_dev = nullptr;
+  ESPN_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&alive_dev), t->server_alive_h, 0));
+  init.alive_host = alive_dev;
+  ESPN_CUDA_TRY(cudaMemsetAsync(t->server, 0, sizeof(ServerQueue), t->server_stream));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(t->server, &init, offsetof(ServerQueue, slot), cudaMemcpyHostToDevice, t->server_stream));
+  ESPN_CUDA_TRY(cudaStreamSynchronize(t->server_stream));
+  *reinterpret_cast<volatile uint32_t*>(t->server_alive_h) = 1u;
+  MaxSimParams p{};
+  p.server = t->server;
+  p.dbg = t->server_dbg;
+  const cudaError_t e = launch_tc_rt(t->d, t->server_split, p, t->num_sms, t->server_stream, false);
+  if (e != cudaSuccess) {
+    *reinterpret_cast<volatile uint32_t*>(t->server_alive_h) = 0u;
+    return fail(ESPN_E_CUDA, std::string("server launch: ") + cudaGetErrorString(e));
+  }
+  ++t->server_launches;
+  return ESPN_OK;
+}
+
+// Before a served batch: relaunch a server that exited idle.  Not inside a
+// stream capture (the relaunch synchronises).
+int server_ensure(espn_gpu_table* t) {
+  if (*reinterpret_cast<volatile uint32_t*>(t->server_alive_h)) return ESPN_OK;
+  return server_launch(t);
+}
+}  // namespace
+
+extern "C" {
+
+int espn_gpu_server_start(espn_gpu_table* t, uint32_t flags, uint32_t idle_us) {
+  if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
+  DeviceGuard g(t->device);
+  if (t->server) return server_ensure(t);
+  if (!t->tc_ok || !tc_supported(t->d))
+    return fail(ESPN_E_INVALID_CONFIG, "the persistent server runs the tcgen05 MaxSim: needs sm_100 and d in {16,32,64,128}");
+  if (t->tiered) return fail(ESPN_E_INVALID_CONFIG, "the persistent server serves HBM-resident (untiered) tables");
+  const bool split = tc_query_split(t->d, t->dtype, flags);
+  // the per-batch plan and wait kernels must fit on an SM beside a server CTA
+  {
+    int smem_sm = 0, reserved = 0, regs_sm = 0;
+    ESPN_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, t->device));
+    ESPN_CUDA_TRY(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, t->device));
+    ESPN_CUDA_TRY(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, t->device));
+    cudaFuncAttributes fp{}, fw{};
+    ESPN_CUDA_TRY(cudaFuncGetAttributes(&fp, plan_kernel));
+    ESPN_CUDA_TRY(cudaFuncGetAttributes(&fw, server_wait_kernel));
+    int tc_smem = 0, tc_threads = 0, tc_regs = 0;
+    switch (t->d * 2 + (split ? 1 : 0)) {
+#define ESPN_SZ(DD, SS)                                                                    \
+  case DD * 2 + SS: {                                                                      \
+    cudaFuncAttributes fa{};                                                               \
+    ESPN_CUDA_TRY(cudaFuncGetAttributes(&fa, maxsim_tc_kernel<DD, (bool)SS>));             \
+    tc_smem = TcLayout<DD, (bool)SS>::SMEM_BYTES + (int)fa.sharedSizeBytes;                \
+    tc_threads = TcLayout<DD, (bool)SS>::NTHREADS;                                         \
+    tc_regs = fa.numRegs;                                                                  \
+  } break;
+      ESPN_SZ(16, 0) ESPN_SZ(16, 1) ESPN_SZ(32, 0) ESPN_SZ(32, 1) ESPN_SZ(64, 0) ESPN_SZ(64, 1) ESPN_SZ(128, 0)
+      ESPN_SZ(128, 1)
+#undef ESPN_SZ
+    }
+    const int need_smem = tc_smem + reserved + (int)fp.sharedSizeBytes + reserved;
+    const int need_regs = tc_regs * tc_threads + fp.numRegs * kPlanThreads + fw.numRegs * 32;
+    if (need_smem > smem_sm || need_regs > regs_sm)
+      return fail(ESPN_E_INVALID_CONFIG, "persistent server: the plan kernel would not fit beside a server CTA (smem " +
+                                             std::to_string(need_smem) + "/" + std::to_string(smem_sm) + ", regs " +
+                                             std::to_string(need_regs) + "/" + std::to_string(regs_sm) + ")");
+  }
+  ServerQueue* q = nullptr;
+  uint32_t* alive = nullptr;
+  cudaStream_t st = nullptr;
+  if (cudaMalloc(&q, sizeof(ServerQueue)) != cudaSuccess ||
+      cudaHostAlloc(&alive, sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaFree(q);
+    cudaFreeHost(alive);
+    if (st) cudaStreamDestroy(st);
+    return fail(ESPN_E_CUDA, "persistent server: allocation failed");
+  }
+  *alive = 0;
+  t->server = q;
+  t->server_alive_h = alive;
+  t->server_stream = st;
+  t->server_split = split;
+  t->server_idle_ns = (uint64_t)(idle_us ? idle_us : 50000u) * 1000ull;
+  static const uint32_t dbg = [] {
+    const char* e = getenv("ESPN_DEBUG");
+    return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
+  }();
+  t->server_dbg = dbg;
+  const int rc = server_launch(t);
+  if (rc) {
+    const std::string why = g_last_error;
+    espn_gpu_server_stop(t);
+    return fail(rc, why);
+  }
+  return ESPN_OK;
+}
+
+int espn_gpu_server_stop(espn_gpu_table* t) {
+  if (!t || !t->server) return ESPN_OK;
+  DeviceGuard g(t->device);
+  // ask the kernel to stop once the queue is drained, then wait for it
+  cudaStream_t cs = nullptr;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess) {
+    static const uint32_t one = 1u;
+    cudaMemcpyAsync(&t->server->stop_req, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
+    cudaStreamSynchronize(cs);
+    cudaStreamDestroy(cs);
+  }
+  cudaStreamSynchronize(t->server_stream);
+  cudaStreamDestroy(t->server_stream);
+  cudaFree(t->server);
+  cudaFreeHost(t->server_alive_h);
+  t->server = nullptr;
+  t->server_stream = nullptr;
+  t->server_alive_h = nullptr;
+  return ESPN_OK;
+}
+
+int espn_gpu_server_running(const espn_gpu_table* t) {
+  return (t && t->server && *reinterpret_cast<volatile uint32_t*>(t->server_alive_h)) ? 1 : 0;
+}
+
+}  // extern "C"
+
 extern "C" {
 
 const char* espn_last_error(void) { return g_last_error.c_str(); }
@@ -697,6 +847,7 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
 
 int espn_gpu_table_close(espn_gpu_table* t) {
   if (!t) return ESPN_OK;
+  espn_gpu_server_stop(t);
   DeviceGuard g(t->device);
   if (t->owned) cudaFree(t->row_ptr);
   if (t->owned_rows) cudaFree(t->rows);
@@ -751,6 +902,10 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   al((void**)&w->unit_tab, w->max_units * sizeof(uint4));
   al((void**)&w->n_units, sizeof(uint32_t));
   al((void**)&w->kprof, 4 * sizeof(unsigned long long));
+  al((void**)&w->done_flag, sizeof(uint32_t));
+  al((void**)&w->plan_done, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(w->done_flag, 0, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(w->plan_done, 0, sizeof(uint32_t));
   if (t->tiered) {
     w->staging_bytes = desc->staging_bytes ? desc->staging_bytes : (64ull << 20);
     for (auto& st : w->stage) {
@@ -847,6 +1002,8 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   if (w->gs) cudaStreamDestroy(w->gs);
   cudaFree(w->unit_off); cudaFree(w->needed); cudaFree(w->unit_tab); cudaFree(w->n_units);
   cudaFree(w->kprof);
+  cudaFree(w->done_flag);
+  cudaFree(w->plan_done);
   cudaFree(w->unit_top); cudaFree(w->dedup); cudaFree(w->ff_seen); cudaFree(w->fused_state);
   for (auto& st : w->stage) {
     if (st.done) cudaEventSynchronize(st.done);
@@ -950,6 +1107,17 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   // lists; ESPN_DEBUG bit 512 / ESPN_RERANK_SEPARATE_TOPK: separate top-k kernel.
   const bool fused = tc && k <= (uint32_t)kFusedMaxK && w->dedup != nullptr && 2ull * max_list <= w->hash_slots &&
                      !(a->flags & ESPN_RERANK_SEPARATE_TOPK) && !(dbg & 512u);
+  // ---- persistent server (espn_gpu_server_start): the batch is submitted to
+  // the running MaxSim kernel by the plan and awaited by a one-thread kernel ----
+  const bool qsplit = tc && tc_query_split(t->d, t->dtype, a->flags);
+  const bool served = t->server != nullptr && tc && fused && !t->tiered && qsplit == t->server_split;
+  if (t->server && tc && !served)
+    return fail(ESPN_E_INVALID_STATE, "a persistent re-rank server runs on this table: only fused tcgen05 batches "
+                                      "(final_k <= 32, the server's query precision) can be served; stop it first");
+  if (served) {
+    const int ss = server_ensure(t);
+    if (ss) return ss;
+  }
   // dedup hash of the separate top-k kernel, sized by the longest scored list
   // (part of the graph key: a captured launch bakes it in)
   uint32_t topk_hs = 64;
@@ -1031,6 +1199,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
                             (uint64_t)alpha_bits | ((uint64_t)a->flags << 32),
                             (uint64_t)kern | ((uint64_t)fused << 8) | ((uint64_t)(a->needed_counts != nullptr) << 9) |
                                 ((uint64_t)(uint32_t)unit_docs << 16) | ((uint64_t)__builtin_ctz(topk_hs) << 32) |
+                                ((uint64_t)served << 40) |
                                 ((uint64_t)(o->fetch_stats != nullptr) << 48)};
   const bool replay = graph_ok && w->sg_exec && std::equal(gkey, gkey + 5, w->sg_key);
   const bool capture = graph_ok && !replay && std::equal(gkey, gkey + 5, w->sg_seen);
@@ -1082,7 +1251,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
         }
       w->counters.batches += 1;
       w->counters.queries += B;
-      w->counters.kernel_launches += 3;
+      w->counters.kernel_launches += served ? 2 : 3;
       return err_bits_to_status(*w->h_err);
     }
     if (capture) {
@@ -1145,6 +1314,47 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   // the device error word is sticky across un-synced ASYNC batches; it is
   // read and cleared by the synchronising call (or espn_gpu_workspace_sync)
 
+  // ---- MaxSim parameters (also the server's batch descriptor) ----
+  MaxSimParams mp{};
+  mp.rows = t->rows;
+  mp.doc_loc = t->doc_loc;
+  mp.cand_src = nullptr;  // tiered: set once the staging slot is known
+  mp.row_ptr = t->row_ptr;
+  mp.n_docs = t->n_docs;
+  mp.shard_count = t->shard_count;
+  mp.shard_index = t->shard_index;
+  mp.q32 = q32;
+  mp.cand_ids = ids;
+  mp.cand_off = cand_off;
+  mp.unit_off = w->unit_off;
+  mp.unit_tab = w->unit_tab;
+  mp.needed = w->needed;
+  mp.bow_out = w->bow;
+  mp.err = w->err;
+  mp.n_queries = B;
+  mp.nq = nq;
+  mp.rerank_count = a->rerank_count;
+  mp.unit_docs = (uint32_t)std::max(unit_docs, 1);
+  mp.n_units = w->n_units;
+  mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
+  mp.qround = (a->flags & ESPN_RERANK_QUERY_ROUNDED) ? 1u : 0u;
+  mp.dbg = dbg;
+  mp.prof = (profile_dev && tc && !served) ? w->kprof : nullptr;
+  mp.done_flag = w->done_flag;
+  if (fused) {
+    mp.cand_cls = cls;
+    mp.alpha = a->alpha;
+    mp.k = k;
+    mp.out_ids = out_ids_k;
+    mp.out_scores = out_scores_k;
+    mp.out_counts = out_counts_k;
+    mp.unit_top = w->unit_top;
+    mp.dedup = w->dedup;
+    mp.ff_seen = w->ff_seen;
+    mp.fused_state = w->fused_state;
+    mp.hash_slots = w->hash_slots;
+    mp.max_queries = w->max_queries;
+  }
   // ---- K0: batch plan on the device ----
   PlanParams pp{};
   pp.cand_off = cand_off;
@@ -1165,7 +1375,13 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   pp.fused_state = fused ? w->fused_state : nullptr;
   pp.base_ok = (dev_off && (a->flags & kFlagBaseOffsets)) ? 1u : 0u;
   pp.dbg = dbg;
-  plan_kernel<<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp);
+  ServerSubmit sb{};
+  if (served) {
+    sb.server = t->server;
+    sb.plan_done = w->plan_done;
+    sb.msp = mp;
+  }
+  plan_kernel<<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp, sb);
   ESPN_CUDA_TRY(cudaGetLastError());
 
   // ---- tiered table: host-tier rows staged into HBM (prefetched or now) ----
@@ -1192,50 +1408,11 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     }
   }
 
-  // ---- K2: MaxSim ----
-  MaxSimParams mp{};
-  mp.rows = t->rows;
-  mp.doc_loc = t->doc_loc;
   mp.cand_src = slot >= 0 ? w->stage[slot].cand_src : nullptr;
-  mp.row_ptr = t->row_ptr;
-  mp.n_docs = t->n_docs;
-  mp.shard_count = t->shard_count;
-  mp.shard_index = t->shard_index;
-  mp.q32 = q32;
-  mp.cand_ids = ids;
-  mp.cand_off = cand_off;
-  mp.unit_off = w->unit_off;
-  mp.unit_tab = w->unit_tab;
-  mp.needed = w->needed;
-  mp.bow_out = w->bow;
-  mp.err = w->err;
-  mp.n_queries = B;
-  mp.nq = nq;
-  mp.rerank_count = a->rerank_count;
-  mp.unit_docs = (uint32_t)std::max(unit_docs, 1);
-  mp.n_units = w->n_units;
-  mp.bf16 = t->dtype == ESPN_DTYPE_BF16;
-  mp.qround = (a->flags & ESPN_RERANK_QUERY_ROUNDED) ? 1u : 0u;
-  mp.dbg = dbg;
-  mp.prof = (profile_dev && tc) ? w->kprof : nullptr;
-  if (fused) {
-    mp.cand_cls = cls;
-    mp.alpha = a->alpha;
-    mp.k = k;
-    mp.out_ids = out_ids_k;
-    mp.out_scores = out_scores_k;
-    mp.out_counts = out_counts_k;
-    mp.unit_top = w->unit_top;
-    mp.dedup = w->dedup;
-    mp.ff_seen = w->ff_seen;
-    mp.fused_state = w->fused_state;
-    mp.hash_slots = w->hash_slots;
-    mp.max_queries = w->max_queries;
-  }
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
-  cudaError_t e = tc ? launch_tc_rt(t->d, tc_query_split(t->d, t->dtype, a->flags), mp, t->num_sms, s,
-                                    /*pdl=*/slot < 0 && !profile)
-                     : launch_simt_rt(t->d, mp, t->num_sms, s);
+  cudaError_t e = served ? (server_wait_kernel<<<1, 32, 0, s>>>(w->done_flag, w->err, kServerWaitNs), cudaGetLastError())
+                  : tc   ? launch_tc_rt(t->d, qsplit, mp, t->num_sms, s, /*pdl=*/slot < 0 && !profile)
+                         : launch_simt_rt(t->d, mp, t->num_sms, s);
   if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
   if (slot >= 0) {  // the slot may be re-staged once this MaxSim finished
     ESPN_CUDA_TRY(cudaEventRecord(w->stage[slot].free_ev, s));
@@ -1243,7 +1420,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[1], s));
 
-  if (fused) {
+  if (fused && !served) {  // (served: the server's dedup warps merged the lists)
     // ---- K3': merge of the per-unit top-k lists (programmatic dependent) ----
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3((B + kFinalizeWarps - 1) / kFinalizeWarps);
@@ -1332,7 +1509,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
   w->counters.batches += 1;
   w->counters.queries += B;
-  w->counters.kernel_launches += 3 + (t->tiered && (!(a->flags & ESPN_RERANK_PREFETCHED) || hint_consumed) ? 1 : 0);
+  w->counters.kernel_launches += (served ? 2 : 3) + (t->tiered && (!(a->flags & ESPN_RERANK_PREFETCHED) || hint_consumed) ? 1 : 0);
   if (a->flags & ESPN_RERANK_ASYNC) {
     w->async_pending = true;
     return ESPN_OK;

@@ -113,7 +113,36 @@ __device__ __forceinline__ uint64_t plan_units(const PlanParams& q, uint32_t b, 
   if (q.tail_units) u += (n - need + q.unit_docs - 1) / q.unit_docs;
   return u;
 }
-__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q) {
+// Submission of the planned batch to a running persistent server (last plan
+// CTA to finish, one thread): sequence number, wait for the slot's previous
+// batch, descriptor copy, release-publish.
+__device__ __noinline__ void server_submit(const ServerSubmit& sb) {
+  ServerQueue* Q = sb.server;
+  unsigned long long seq;
+  for (;;) {  // take the next sequence number unless the server stopped
+    const unsigned long long st = ld_acquire_u64(&Q->state);
+    if (st & kServerStopped) {  // no server to take it: fail the batch, release the waiter
+      atomicOr(sb.msp.err, ERR_SERVER);
+      __threadfence();
+      st_release_u32(sb.msp.done_flag, 1u);
+      return;
+    }
+    if (atomicCAS(&Q->state, st, st + 1ull) == st) {
+      seq = st;
+      break;
+    }
+  }
+  ServerSlot* sl = &Q->slot[seq % kServerSlots];
+  const uint32_t want = seq >= (unsigned long long)kServerSlots ? (uint32_t)(seq - kServerSlots + 1) : 0u;
+  while (ld_acquire_u32(&sl->done) != want) __nanosleep(128);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(&sb.msp);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(&sl->p);
+  for (int i = 0; i < (int)(sizeof(MaxSimParams) / 4); ++i) __stcg(dst + i, src[i]);
+  __threadfence();
+  st_release_u32(&sl->ready, (uint32_t)seq + 1u);
+}
+
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q, const ServerSubmit sb) {
   ktl_begin(q.dbg, 0);
   // the MaxSim kernel is a programmatic dependent: its prologue (barriers,
   // TMEM, operand zeroing) overlaps this kernel; it waits before reading the plan
@@ -192,7 +221,36 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q) 
     // read by the MaxSim kernel; an invalid batch gets an empty plan
     *q.n_units = (any_bad || over) ? 0u : (uint32_t)(excl + u);
   }
+  if (sb.server) {  // persistent server: the last plan CTA to finish publishes the batch
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(sb.plan_done, 1u) == gridDim.x - 1) {
+        *sb.plan_done = 0;
+        __threadfence();
+        server_submit(sb);
+      }
+    }
+  }
   ktl_end(q.dbg, 0);
+}
+
+// The caller's stream waits for its batch (persistent server): one thread
+// polls the workspace's done flag and consumes it.  A batch that does not
+// complete within timeout_ns (server stopped or stalled) raises ERR_SERVER
+// instead of hanging the stream.
+__global__ void server_wait_kernel(uint32_t* flag, uint32_t* err, unsigned long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = ktl_now();
+  while (ld_acquire_u32(flag) == 0u) {
+    __nanosleep(256);
+    if (ktl_now() - t0 > timeout_ns) {
+      atomicOr(err, ERR_SERVER);
+      return;
+    }
+  }
+  *flag = 0u;
+  __threadfence();
 }
 
 // ============================================================================

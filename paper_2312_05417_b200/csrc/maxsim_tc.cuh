@@ -142,7 +142,9 @@ struct TcLayout {
   static constexpr int OFF_BAR = OFF_RING + NB * UNITMAX * 4;
   static constexpr int N_BARS = 3 * NS + 2 * NBUF + 3 * NU + 2 * NB;
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
-  static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
+  static constexpr int MERGE_KEYS = 640;           // persistent server: the dedup warp's merge scratch
+  static constexpr int OFF_FM = (OFF_TMEM + 16 + 15) / 16 * 16;
+  static constexpr int SMEM_BYTES = OFF_FM + MERGE_KEYS * 8 + 1024;  // + alignment slack
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(STAGE_BYTES % 1024 == 0 && A_BYTES % 16 == 0, "alignment");
 };
@@ -152,16 +154,6 @@ __device__ __forceinline__ uint64_t gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// ESPN_DEBUG bit 8: CTA 0 records a per-unit timeline of its roles and prints it.
-#define ESPN_STRACE(slot, g)                                                     \
-  do {                                                                           \
-    if ((p.dbg & 8u) && blockIdx.x == 0 && (g) < 16) strace[(slot) * 16 + (g)] = gtimer(); \
-  } while (0)
-#define ESPN_TRACE(slot, it)                                                     \
-  do {                                                                           \
-    if ((p.dbg & 8u) && blockIdx.x == 0 && (it) < 8) trace[(slot) * 8 + (it)] = gtimer(); \
-  } while (0)
-
 // ---- fused top-k helpers (combine warp) --------------------------------------
 // Duplicate rejection of rank() (scoring.hpp:16-18) across all units of a
 // query, by the dedicated dedup warp: the unit's ids go into the query's
@@ -179,7 +171,7 @@ __device__ __forceinline__ void fused_dedup(const MaxSimParams& p, uint32_t par,
 #pragma unroll
   for (int r = 0; r < NK; ++r) {
     const uint32_t k = r * 32 + lane;
-    id[r] = k < nd ? __ldg(&p.cand_ids[cfirst + k]) : 0u;
+    id[r] = k < nd ? __ldcg(&p.cand_ids[cfirst + k]) : 0u;
     h[r] = ((id[r] * 2654435761u) >> 7) & mask;
     if (k < nd) {
       if (id[r] == 0xFFFFFFFFu) dup |= atomicExch(ff, 1u);
@@ -353,102 +345,72 @@ __global__ void __launch_bounds__(kFinalizeWarps * 32) finalize_kernel(const Max
   ktl_end(p.dbg, 2);
 }
 
+// Shared-memory views and barrier set of one MaxSim CTA.
 template <int D, bool SPLIT>
-__global__ void __launch_bounds__(TcLayout<D, SPLIT>::NTHREADS, 1)
-maxsim_tc_kernel(const MaxSimParams p) {
-  __shared__ uint64_t trace[8 * 8];
-  __shared__ uint64_t strace[9 * 16];  // per-stage: producer, MMA full, MMA tempty, epilogue
+struct TcSmem {
+  uint8_t* sB;
+  uint8_t* sA;
+  float* pm;
+  typename TcLayout<D, SPLIT>::Unit* units;
+  uint8_t* smem;
+  uint64_t* full_bar;     // [NS]  producer (expect_tx) -> MMA
+  uint64_t* empty_bar;    // [NS]  MMA commit -> producer
+  uint64_t* tfull_bar;    // [NBUF] MMA commit -> epilogue
+  uint64_t* tempty_bar;   // [NBUF] epilogue -> MMA
+  uint64_t* ufull_bar;    // [NU] loader + query warp -> producer, MMA, epilogue, patch
+  uint64_t* uempty_bar;   // [NU] combine -> loader / query warp
+  uint64_t* edone_bar;    // [NU] epilogue (all lanes) -> combine
+  uint64_t* bdone_bar;    // [NB] combine -> rank (bow ring entry full)
+  uint64_t* bfree_bar;    // [NB] rank -> combine (bow ring entry free)
+  uint64_t* patched_bar;  // [NS] patch warp -> MMA (stage rows + pads ready)
+  uint32_t tmem_base;
+};
+
+// Pipeline position of one warp role, carried across the batches of a
+// persistent launch: gu = unit iterations done (unit slot us = gu % NU and the
+// slot barriers' phase), gs = stages done (stage / TMEM buffer and phases),
+// rot = the round-robin origin (the next batch's unit 0 goes to CTA rot,
+// so units spread over the CTAs across batches, not only within one).
+struct TcRoleState {
+  uint32_t gu = 0, gs = 0, rot = 0;
+};
+
+// One batch through every warp role of the CTA (the body of the MaxSim
+// kernel; a persistent launch runs it once per queued batch).  `slot` != NULL:
+// persistent mode -- the rank and dedup warps report the batch done and the
+// dedup warps merge the queries' unit lists (instead of finalize_kernel).
+template <int D, bool SPLIT>
+__device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, SPLIT>& S, TcRoleState& rs,
+                                         ServerSlot* slot, uint32_t seq) {
   using L = TcLayout<D, SPLIT>;
   using namespace espn_ptx;
-  // swizzled operand atoms need 1024-byte aligned stage bases: align manually
-  extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
-  uint8_t* smem = tc_smem_raw + ((1024u - (smem_u32(tc_smem_raw) & 1023u)) & 1023u);
-  uint8_t* sB = smem + L::OFF_B;
-  uint8_t* sA = smem + L::OFF_A;
-  float* pm = reinterpret_cast<float*>(smem + L::OFF_PM);
-  typename L::Unit* units = reinterpret_cast<typename L::Unit*>(smem + L::OFF_UNIT);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* full_bar = bars;                       // [NS]  producer (expect_tx) -> MMA
-  uint64_t* empty_bar = bars + L::NS;              // [NS]  MMA commit -> producer
-  uint64_t* tfull_bar = bars + 2 * L::NS;          // [NBUF] MMA commit -> epilogue
-  uint64_t* tempty_bar = tfull_bar + L::NBUF;      // [NBUF] epilogue -> MMA
-  uint64_t* ufull_bar = tempty_bar + L::NBUF;      // [NU] loader -> producer, MMA, epilogue
-  uint64_t* uempty_bar = ufull_bar + L::NU;        // [NU] combine -> loader
-  uint64_t* edone_bar = uempty_bar + L::NU;        // [NU] epilogue (all lanes) -> combine
-  uint64_t* bdone_bar = edone_bar + L::NU;         // [NB] combine -> rank (bow ring entry full)
-  uint64_t* bfree_bar = bdone_bar + L::NB;         // [NB] rank -> combine (bow ring entry free)
-  uint64_t* patched_bar = bfree_bar + L::NB;       // [NS] patch warp -> MMA (stage rows + pads ready)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
-
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
-  if (p.prof && tid == 0) atomicMin(&p.prof[2], (unsigned long long)gtimer());
-  ktl_begin(p.dbg, 1);
-
-  // ---- one-time setup: zero operand tiles (stale NaN bit patterns would leak
-  // into other quarters through the zero rows of A), barriers, TMEM ----------
-  {
-    uint4* z = reinterpret_cast<uint4*>(smem);
-    const int n16 = (L::OFF_PM) / 16;
-    for (int i = tid; i < n16; i += L::NTHREADS) z[i] = make_uint4(0, 0, 0, 0);
-  }
-  {
-    int* pmk = reinterpret_cast<int*>(smem + L::OFF_PM);
-    for (int i = tid; i < L::PM_FLOATS; i += L::NTHREADS) pmk[i] = ord_key(-INFINITY);
-  }
-  fence_proxy_async_smem();
-  if (tid == 0) {
-    for (int i = 0; i < L::NS; ++i) {
-      mbar_init(&full_bar[i], L::NPROD);
-      mbar_init(&empty_bar[i], 1);
-    }
-    for (int i = 0; i < L::NBUF; ++i) {
-      mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], L::NEPI);
-    }
-    for (int i = 0; i < L::NU; ++i) {
-      mbar_init(&ufull_bar[i], 2);  // unit loader + query-tile warp
-      mbar_init(&uempty_bar[i], 1);
-      mbar_init(&edone_bar[i], 32 * L::NEPI);
-    }
-    for (int i = 0; i < L::NB; ++i) {
-      mbar_init(&bdone_bar[i], 1);
-      mbar_init(&bfree_bar[i], 1);
-    }
-    for (int i = 0; i < L::NS; ++i) mbar_init(&patched_bar[i], 1);
-
-    mbar_fence_init();
-  }
-  if (warp == L::MMA_WARP) tmem_alloc<L::TMEM_COLS>(tmem_holder);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-  const uint64_t t_start = gtimer();
-  // programmatic dependent of plan_kernel: everything above overlapped it
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  // let the dependent grid launch now (the plan is complete): the duplicate
-  // check (fused top-k) or the top-k kernel's id-only dedup prologue runs on
-  // the SMs' spare resources concurrently with this kernel
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const uint32_t n_units = *p.n_units;  // planned on the device (plan_kernel)
+  const uint32_t G = gridDim.x;
+  const uint32_t n_units = slot ? __ldcg(p.n_units) : *p.n_units;  // planned on the device (plan_kernel)
+  const uint32_t first = (blockIdx.x + G - rs.rot) % G;
+  const uint32_t cnt = n_units > first ? (n_units - first + G - 1) / G : 0u;  // this CTA's units
+  const uint32_t gu0 = rs.gu;
+  rs.gu += cnt;
+  rs.rot = (uint32_t)(((uint64_t)rs.rot + n_units) % G);
+  typename L::Unit* units = S.units;
+  uint8_t* smem = S.smem;
 
   if (warp == L::LOADER_WARP) {
     // ============================ UNIT LOADER ===================================
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t ug = blockIdx.x + it * gridDim.x;
-      if (ug >= n_units) break;
-      const uint32_t us = it % L::NU;
+    for (uint32_t it = 0; it < cnt; ++it) {
+      const uint32_t ug = first + it * G, gi = gu0 + it;
+      const uint32_t us = gi % L::NU;
       typename L::Unit& U = units[us];
-      // Unit table entry (host-planned): query b, doc count, first candidate.
-      if (lane == 0) ESPN_TRACE(0, it);
+      // Unit table entry (device-planned): query b, doc count, first candidate.
       const uint4 ue = __ldcg(&p.unit_tab[ug]);
       const uint32_t b = ue.x, nd = ue.y & 0xFFu, tail = ue.y >> 31;
       const uint64_t cfirst = (uint64_t)ue.z | ((uint64_t)ue.w << 32);
       // Every global load of the unit is issued before waiting for its slot:
       // candidate ids (<= 2 per lane), then the dependent row_ptr / staged
-      // addresses, so the slot wait overlaps their latency.
+      // addresses, so the slot wait overlaps their latency.  Per-batch inputs
+      // use L2-coherent loads: a persistent CTA outlives the batch's buffers.
       constexpr int NK = L::UNITMAX / 32;
       uint32_t tk[NK];
       uint64_t srck[NK];
@@ -458,11 +420,11 @@ maxsim_tc_kernel(const MaxSimParams p) {
         tk[r] = 0;
         srck[r] = 0;
         if (k < nd && !tail) {
-          const uint64_t loc = shard_local(__ldg(&p.cand_ids[cfirst + k]), p.shard_count, p.shard_index, p.n_docs);
+          const uint64_t loc = shard_local(__ldcg(&p.cand_ids[cfirst + k]), p.shard_count, p.shard_index, p.n_docs);
           if (loc != ~0ull) {
             const uint64_t r0 = __ldg(&p.row_ptr[loc]);
             tk[r] = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
-            srck[r] = p.cand_src ? __ldg(&p.cand_src[cfirst + k])  // tiered: staged / resident address
+            srck[r] = p.cand_src ? __ldcg(&p.cand_src[cfirst + k])  // tiered: staged / resident address
                                  : (uint64_t)(p.rows + r0 * D);
             if (srck[r] == 0) tk[r] = 0;  // not staged (staging overflow, reported by stage_kernel)
           } else {
@@ -470,8 +432,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
           }
         }
       }
-      mbar_wait(&uempty_bar[us], ((it / L::NU) & 1) ^ 1);
-      if (lane == 0) ESPN_TRACE(1, it);
+      mbar_wait(&S.uempty_bar[us], ((gi / L::NU) & 1) ^ 1);
       for (int i = lane; i < L::MAXW; i += 32) U.bitmap[i] = 0;
       for (int i = lane; i < L::MAX_STAGES; i += 32) {
         U.op_beg[i] = 0xFFFFFFFFu;
@@ -553,7 +514,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
         U.n_pt = pcarry;
       }
       __syncwarp();
-      if (lane == 0) { ESPN_TRACE(2, it); mbar_arrive(&ufull_bar[us]); }
+      if (lane == 0) mbar_arrive(&S.ufull_bar[us]);
     }
   } else if (warp == L::PATCH_WARP) {
     // ============================ PAD PATCH =====================================
@@ -561,37 +522,35 @@ maxsim_tc_kernel(const MaxSimParams p) {
     // partial gets copies of its last row in its pad slots (re-swizzled for
     // the slot), so each MMA column of a group is a real row of its doc and
     // the epilogue's group maxima need no masking.  One lane per doc.
-    uint32_t gs = 0;
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t ug = blockIdx.x + it * gridDim.x;
-      if (ug >= n_units) break;
-      const uint32_t us = it % L::NU;
+    uint32_t& gs = rs.gs;
+    for (uint32_t it = 0; it < cnt; ++it) {
+      const uint32_t gi = gu0 + it, us = gi % L::NU;
       const typename L::Unit& U = units[us];
-      mbar_wait(&ufull_bar[us], (it / L::NU) & 1);
-      const uint32_t S = U.S, npt = U.n_pt;
-      const uint32_t n_st = (S + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
+      mbar_wait(&S.ufull_bar[us], (gi / L::NU) & 1);
+      const uint32_t Sl = U.S, npt = U.n_pt;
+      const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       uint32_t pc = 0;  // next patch of the unit (patches are in stage order)
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t s = gs % L::NS;
-        mbar_wait(&full_bar[s], (gs / L::NS) & 1);
-        uint8_t* stage = sB + s * L::STAGE_BYTES;
+        mbar_wait(&S.full_bar[s], (gs / L::NS) & 1);
+        uint8_t* stage = S.sB + s * L::STAGE_BYTES;
         for (;;) {
           const uint32_t i = pc + lane;
           const uint32_t e = i < npt ? U.pt[i] : 0xFFFFFFFFu;
           const bool mine = i < npt && (e >> 20) == st;
           const uint32_t nmine = __popc(__ballot_sync(0xffffffffu, mine));  // a prefix of the lanes
           if (mine) {
-            const uint32_t slot = e & 0xFFFFu, npad = (e >> 16) & 0xFu;
-            const uint32_t sws = ((slot * (uint32_t)L::PW) >> 7) & (uint32_t)(L::RL::CPP - 1);
+            const uint32_t sl = e & 0xFFFFu, npad = (e >> 16) & 0xFu;
+            const uint32_t sws = ((sl * (uint32_t)L::PW) >> 7) & (uint32_t)(L::RL::CPP - 1);
 #pragma unroll
             for (int pn = 0; pn < L::NP; ++pn) {
               uint8_t* panel = stage + pn * L::PANEL_BYTES;
               uint4 c[L::RL::CPP];
 #pragma unroll
               for (int cc = 0; cc < L::RL::CPP; ++cc)
-                c[cc] = *reinterpret_cast<const uint4*>(panel + slot * L::PW + ((cc ^ sws) << 4));
+                c[cc] = *reinterpret_cast<const uint4*>(panel + sl * L::PW + ((cc ^ sws) << 4));
               for (uint32_t r = 1; r <= npad; ++r) {
-                const uint32_t ds = slot + r;
+                const uint32_t ds = sl + r;
                 const uint32_t swd = ((ds * (uint32_t)L::PW) >> 7) & (uint32_t)(L::RL::CPP - 1);
 #pragma unroll
                 for (int cc = 0; cc < L::RL::CPP; ++cc)
@@ -604,20 +563,18 @@ maxsim_tc_kernel(const MaxSimParams p) {
         }
         fence_proxy_async_smem();  // patched rows are read by the tensor core
         __syncwarp();
-        if (lane == 0) mbar_arrive(&patched_bar[s]);
+        if (lane == 0) mbar_arrive(&S.patched_bar[s]);
       }
     }
   } else if (warp == L::QUERY_WARP) {
     // ============================ QUERY TILE ====================================
-    // The unit's query tokens -> A slot `us`, converted to the table dtype,
-    // in parallel with the loader's slot plan (ufull counts both).
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t ug = blockIdx.x + it * gridDim.x;
-      if (ug >= n_units) break;
-      const uint32_t us = it % L::NU;
+    // The unit's query tokens -> A slot `us` (hi, and lo when SPLIT), in the
+    // table dtype, in parallel with the loader's slot plan (ufull counts both).
+    for (uint32_t it = 0; it < cnt; ++it) {
+      const uint32_t ug = first + it * G, gi = gu0 + it, us = gi % L::NU;
       const uint4 ue = __ldcg(&p.unit_tab[ug]);
       const uint32_t b = ue.x, tail = ue.y >> 31;
-      mbar_wait(&uempty_bar[us], ((it / L::NU) & 1) ^ 1);
+      mbar_wait(&S.uempty_bar[us], ((gi / L::NU) & 1) ^ 1);
       // Query tokens -> A slot `us` (rows 96+128*us .. +32), converted to the
       // table dtype; rows >= nq stay zero.  Item e = (row i, 8-value chunk c);
       // batches of 4 items per lane keep all their loads in flight together.
@@ -635,8 +592,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
             const int i = e / L::CH, c = e % L::CH;
             if ((uint32_t)i < p.nq) {
               const float4* src = reinterpret_cast<const float4*>(q + i * D + c * 8);
-              x[u][0] = __ldg(src);
-              x[u][1] = __ldg(src + 1);
+              x[u][0] = __ldcg(src);
+              x[u][1] = __ldcg(src + 1);
             } else {
               x[u][0] = x[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
@@ -666,11 +623,11 @@ maxsim_tc_kernel(const MaxSimParams p) {
             for (int part = 0; part < (L::SPLIT ? 2 : 1); ++part) {
               const uint4 val = part ? make_uint4(l4[0], l4[1], l4[2], l4[3]) : make_uint4(w4[0], w4[1], w4[2], w4[3]);
               const int rr = r + part * L::LO_ROWS;
-              *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, rr, c)) = val;
+              *reinterpret_cast<uint4*>(S.sA + L::RL::off(L::A_ROWS, rr, c)) = val;
               if constexpr (L::REPA) {  // replicas for lane quarters 1..3
 #pragma unroll
                 for (int rq = 1; rq < 4; ++rq)
-                  *reinterpret_cast<uint4*>(sA + L::RL::off(L::A_ROWS, rr + 32 * rq, c)) = val;
+                  *reinterpret_cast<uint4*>(S.sA + L::RL::off(L::A_ROWS, rr + 32 * rq, c)) = val;
               }
             }
           }
@@ -679,97 +636,85 @@ maxsim_tc_kernel(const MaxSimParams p) {
       }
       fence_proxy_async_smem();  // A tile is read by the tensor core (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ufull_bar[us]);
+      if (lane == 0) mbar_arrive(&S.ufull_bar[us]);
     }
   } else if (warp >= L::PROD_WARP0 && warp < L::PROD_WARP0 + L::NPROD) {
     // ====================== BULK-COPY PRODUCERS (NPROD warps) ======================
-    // Lane 0 of producer pw issues the stage's copy ops of parity pw (one
-    // cp.async.bulk each, planned by the loader) and arrives on the stage's
-    // full barrier with their byte count.
+    // PLANES lanes of producer pw issue the stage's copy ops of parity pw (one
+    // cp.async.bulk each, planned by the loader); lane 0 arms the stage's full
+    // barrier with their byte count.
     const uint32_t pw = warp - L::PROD_WARP0;
     const uint64_t policy = l2_policy_evict_first();
-    uint32_t gs = 0;  // global stage counter
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t ug = blockIdx.x + it * gridDim.x;
-      if (ug >= n_units) break;
-      const uint32_t us = it % L::NU;
+    uint32_t& gs = rs.gs;
+    for (uint32_t it = 0; it < cnt; ++it) {
+      const uint32_t gi = gu0 + it, us = gi % L::NU;
       const typename L::Unit& U = units[us];
-      mbar_wait(&ufull_bar[us], (it / L::NU) & 1);
-      if (lane == 0 && pw == 0) ESPN_TRACE(3, it);
-      const uint32_t S = U.S;
-      const uint32_t n_st = (S + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
+      mbar_wait(&S.ufull_bar[us], (gi / L::NU) & 1);
+      const uint32_t Sl = U.S;
+      const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t s = gs % L::NS;
         // ops [o0, o1) of this stage (loader-planned); this warp issues parity pw
         const uint32_t o0 = U.op_beg[st], o1 = st + 1 < n_st ? U.op_beg[st + 1] : U.n_ops;
         uint32_t bytes = U.stage_tx[st][pw];
-        mbar_wait(&empty_bar[s], ((gs / L::NS) & 1) ^ 1);
-        if (lane == 0 && pw == 0) ESPN_STRACE(0, gs);
+        mbar_wait(&S.empty_bar[s], ((gs / L::NS) & 1) ^ 1);
         if (p.dbg & 4u) bytes = 0;
-        if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], bytes);
+        if (lane == 0) mbar_arrive_expect_tx(&S.full_bar[s], bytes);
         __syncwarp();
-        // PLANES lanes of the warp issue its ops concurrently (the per-thread
-        // issue of a bulk copy, not the TMA engine, bounds one issuing lane)
         if (!(p.dbg & 4u) && lane < L::PLANES) {
-          const uint32_t sbase = smem_u32(sB + s * L::STAGE_BYTES);
+          const uint32_t sbase = smem_u32(S.sB + s * L::STAGE_BYTES);
           for (uint32_t o = o0 + ((o0 & 1u) ^ pw) + 2 * lane; o < o1; o += 2 * L::PLANES) {
             const uint4 op = U.op[o];
             bulk_g2s(sbase + op.z, reinterpret_cast<const void*>((uint64_t)op.x | ((uint64_t)op.y << 32)), op.w,
-                     &full_bar[s], policy);
+                     &S.full_bar[s], policy);
           }
         }
         __syncwarp();
-        if (lane == 0 && pw == 0) ESPN_STRACE(6, gs);
       }
     }
   } else if (warp == L::MMA_WARP) {
     // ============================ MMA ISSUER ==================================
     // The whole warp walks the schedule (operands warp-uniform, in uniform
     // registers); one elected lane issues each tcgen05.mma / commit.
-    {
-      uint32_t gs = 0;
-      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-      for (uint32_t it = 0;; ++it) {
-        const uint32_t ug = blockIdx.x + it * gridDim.x;
-        if (ug >= n_units) break;
-        const uint32_t us = it % L::NU;
-        mbar_wait(&ufull_bar[us], (it / L::NU) & 1);
-        const uint32_t S = units[us].S;
-        const uint32_t n_st = (S + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
-        for (uint32_t st = 0; st < n_st; ++st, ++gs) {
-          const uint32_t s = gs % L::NS, buf = gs % L::NBUF;
-          mbar_wait(&patched_bar[s], (gs / L::NS) & 1);  // rows landed and pads patched
-          ESPN_STRACE(1, gs);
-          mbar_wait(&tempty_bar[buf], ((gs / L::NBUF) & 1) ^ 1);
-          ESPN_STRACE(2, gs);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem_base + buf * L::BUFC;
-          const uint32_t x0 = st * L::STAGE_SLOTS;
-          uint32_t acc = 0;
-          if constexpr (L::REPA) {
-            // one MMA per K-step over the whole stage: N = its slots (<= 4 NQC)
-            const int rem = (int)S - (int)x0;
-            const uint32_t nv = rem < L::STAGE_SLOTS ? (uint32_t)rem : (uint32_t)L::STAGE_SLOTS;
-            const uint32_t idesc = umma_idesc_f16(128, (nv + 15u) & ~15u, p.bf16);
-            const uint32_t a_addr = a_base + 128 * us * L::PW;
-            const uint32_t b_addr = b_base + s * L::STAGE_BYTES;
-            if (!(p.dbg & 2u))
+    uint32_t& gs = rs.gs;
+    const uint32_t a_base = smem_u32(S.sA), b_base = smem_u32(S.sB);
+    for (uint32_t it = 0; it < cnt; ++it) {
+      const uint32_t gi = gu0 + it, us = gi % L::NU;
+      mbar_wait(&S.ufull_bar[us], (gi / L::NU) & 1);
+      const uint32_t Sl = units[us].S;
+      const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
+      for (uint32_t st = 0; st < n_st; ++st, ++gs) {
+        const uint32_t s = gs % L::NS, buf = gs % L::NBUF;
+        mbar_wait(&S.patched_bar[s], (gs / L::NS) & 1);  // rows landed and pads patched
+        mbar_wait(&S.tempty_bar[buf], ((gs / L::NBUF) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = S.tmem_base + buf * L::BUFC;
+        const uint32_t x0 = st * L::STAGE_SLOTS;
+        uint32_t acc = 0;
+        if constexpr (L::REPA) {
+          // one MMA per K-step over the whole stage: N = its slots (<= 4 NQC)
+          const int rem = (int)Sl - (int)x0;
+          const uint32_t nv = rem < L::STAGE_SLOTS ? (uint32_t)rem : (uint32_t)L::STAGE_SLOTS;
+          const uint32_t idesc = umma_idesc_f16(128, (nv + 15u) & ~15u, p.bf16);
+          const uint32_t a_addr = a_base + 128 * us * L::PW;
+          const uint32_t b_addr = b_base + s * L::STAGE_BYTES;
+          if (!(p.dbg & 2u))
 #pragma unroll
-              for (int ks = 0; ks < L::KSTEPS; ++ks) {
-                const uint32_t kb = ks * 32;
-                const uint64_t bd = umma_desc_sw(b_addr + (kb / L::PW) * L::PANEL_BYTES + (kb % L::PW), 8 * L::PW, L::SWZ);
+            for (int ks = 0; ks < L::KSTEPS; ++ks) {
+              const uint32_t kb = ks * 32;
+              const uint64_t bd = umma_desc_sw(b_addr + (kb / L::PW) * L::PANEL_BYTES + (kb % L::PW), 8 * L::PW, L::SWZ);
 #pragma unroll
-                for (int part = 0; part < (L::SPLIT ? 2 : 1); ++part) {
-                  const uint64_t ad = umma_desc_sw(a_addr + part * L::LO_ROWS * L::PW + (kb / L::PW) * L::A_PANEL_BYTES +
-                                                       (kb % L::PW), 8 * L::PW, L::SWZ);
-                  umma_f16_elect(d_tmem, ad, bd, idesc, acc);
-                  acc = 1;
-                }
+              for (int part = 0; part < (L::SPLIT ? 2 : 1); ++part) {
+                const uint64_t ad = umma_desc_sw(a_addr + part * L::LO_ROWS * L::PW + (kb / L::PW) * L::A_PANEL_BYTES +
+                                                     (kb % L::PW), 8 * L::PW, L::SWZ);
+                umma_f16_elect(d_tmem, ad, bd, idesc, acc);
+                acc = 1;
               }
-          } else
+            }
+        } else
 #pragma unroll 1
           for (int w = 0; w < 4; ++w) {
-            const int rem = (int)S - (int)(x0 + w * L::NQC);
+            const int rem = (int)Sl - (int)(x0 + w * L::NQC);
             if (rem <= 0) break;
             const uint32_t nv = rem < L::NQC ? (uint32_t)rem : (uint32_t)L::NQC;
             const uint32_t n_mma = (nv + 15u) & ~15u;
@@ -792,9 +737,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
               }
             }
           }
-          umma_commit_elect(&empty_bar[s]);
-          umma_commit_elect(&tfull_bar[buf]);
-        }
+        umma_commit_elect(&S.empty_bar[s]);
+        umma_commit_elect(&S.tfull_bar[buf]);
       }
     }
     __syncwarp();
@@ -805,32 +749,28 @@ maxsim_tc_kernel(const MaxSimParams p) {
     // halves of a quarter may both flush a doc straddling the split, so
     // flushes are shared-memory atomicMax (a few per stage).
     const int w = warp & 3, h = warp >> 2;
-    uint32_t gs = 0;
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t ug = blockIdx.x + it * gridDim.x;
-      if (ug >= n_units) break;
-      const uint32_t us = it % L::NU;
+    uint32_t& gs = rs.gs;
+    for (uint32_t it = 0; it < cnt; ++it) {
+      const uint32_t gi = gu0 + it, us = gi % L::NU;
       const typename L::Unit& U = units[us];
-      mbar_wait(&ufull_bar[us], (it / L::NU) & 1);
-      if (tid == 0) ESPN_TRACE(4, it);
-      const uint32_t S = U.S;
-      int* my_pm = reinterpret_cast<int*>(pm) + (us * 32 + lane) * L::PM_STRIDE;
-      const uint32_t n_st = (S + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
+      mbar_wait(&S.ufull_bar[us], (gi / L::NU) & 1);
+      const uint32_t Sl = U.S;
+      int* my_pm = reinterpret_cast<int*>(S.pm) + (us * 32 + lane) * L::PM_STRIDE;
+      const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t buf = gs % L::NBUF;
-        mbar_wait(&tfull_bar[buf], (gs / L::NBUF) & 1);
-        if (tid == 0) ESPN_STRACE(3, gs);
+        mbar_wait(&S.tfull_bar[buf], (gs / L::NBUF) & 1);
         tc_fence_after();
         const uint32_t xw = st * L::STAGE_SLOTS + w * L::NQC + h * L::HALF;
-        const int remv = (p.dbg & 1u) ? 0 : (int)S - (int)xw;
+        const int remv = (p.dbg & 1u) ? 0 : (int)Sl - (int)xw;
         if (remv > 0) {
           // TMEM -> registers in NLD chunks of LW columns: chunk c+1 is read
-          // (the SM's TMEM read port, ~64 B/clk, is the epilogue's floor)
-          // while chunk c's group maxima are computed; the buffer is released
-          // after the last chunk landed.  Only the short doc-boundary scan over
-          // NGH groups is sequential.
+          // (the SM's TMEM read port is the epilogue's floor) while chunk c's
+          // group maxima are computed; the buffer is released after the last
+          // chunk landed.  Only the short doc-boundary scan over NGH groups is
+          // sequential.
           const uint32_t nv = remv < L::HALF ? (uint32_t)remv : (uint32_t)L::HALF;
-          const uint32_t taddr0 = tmem_base + ((uint32_t)(w * 32) << 16) + buf * L::BUFC +
+          const uint32_t taddr0 = S.tmem_base + ((uint32_t)(w * 32) << 16) + buf * L::BUFC +
                                   (L::REPA ? w * L::NQC : 0) + h * L::HALF;
           float v[L::NLD][L::LW];
           tmem_ld_32x32b<L::LW>(taddr0, v[0]);
@@ -846,11 +786,9 @@ maxsim_tc_kernel(const MaxSimParams p) {
             if (c + 1 < L::NLD) {
               if ((uint32_t)(L::LW * (c + 1)) < nv) tmem_ld_32x32b<L::LW>(taddr0 + L::LW * (c + 1), v[c + 1]);
             } else {
-              if (tid == 0) ESPN_STRACE(4, gs);
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&tempty_bar[buf]);
-              if (tid == 0) ESPN_STRACE(8, gs);
+              if (lane == 0) mbar_arrive(&S.tempty_bar[buf]);
             }
             // group maxima over the valid (non-pad) columns of chunk c
 #pragma unroll
@@ -861,7 +799,6 @@ maxsim_tc_kernel(const MaxSimParams p) {
               gm[q] = fmaxf(fmax3(x[0], x[1], x[2]), fmax3(fmax3(x[3], x[4], x[5]), x[6], x[7]));
             }
           }
-          if (tid == 0) { asm volatile("" ::"f"(gm[L::NGH - 1])); ESPN_STRACE(7, gs); }
           if (p.dbg & 32u) continue;  // profiling knob: no scan / flush
           // doc-boundary scan, branch-free: after every group the running max
           // of the current doc goes to pm with a shared red.max (unconditional
@@ -877,16 +814,14 @@ maxsim_tc_kernel(const MaxSimParams p) {
             m = start ? g : fmaxf(m, g);
             red_max_shared(&my_pm[doc], ord_key(m));
           }
-          if (tid == 0) ESPN_STRACE(5, gs);
         } else {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+          if (lane == 0) mbar_arrive(&S.tempty_bar[buf]);
         }
       }
       // all lanes' flushes of this unit are done: hand the slot to the combiner
-      if (tid == 0) ESPN_TRACE(5, it);
-      mbar_arrive(&edone_bar[us]);
+      mbar_arrive(&S.edone_bar[us]);
     }
   } else if (warp == L::COMBINE_WARP) {
     // ============================ COMBINE ========================================
@@ -898,37 +833,35 @@ maxsim_tc_kernel(const MaxSimParams p) {
     const bool fused = p.out_ids != nullptr;
     float* ring = reinterpret_cast<float*>(smem + L::OFF_RING);
     constexpr int NK = L::UNITMAX / 32;  // docs per lane
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t ug = blockIdx.x + it * gridDim.x;
-      if (ug >= n_units) break;
-      const uint32_t us = it % L::NU;
+    for (uint32_t it = 0; it < cnt; ++it) {
+      const uint32_t gi = gu0 + it, us = gi % L::NU;
       const typename L::Unit& U = units[us];
-      mbar_wait(&edone_bar[us], (it / L::NU) & 1);
+      mbar_wait(&S.edone_bar[us], (gi / L::NU) & 1);
       const uint32_t nd = U.nd, tail = U.tail;
       const uint64_t j0 = U.cfirst;
-      int* pmu = reinterpret_cast<int*>(pm) + us * 32 * L::PM_STRIDE;
+      int* pmu = reinterpret_cast<int*>(S.pm) + us * 32 * L::PM_STRIDE;
       float bow[NK];
 #pragma unroll
       for (int r = 0; r < NK; ++r) {
         const uint32_t k = r * 32 + lane;
         bow[r] = 0.0f;
         if (k < nd && !tail) {
-          float s = 0.0f;
-          for (uint32_t i = 0; i < p.nq; ++i) s = __fadd_rn(s, key_ord(pmu[i * L::PM_STRIDE + k]));
-          bow[r] = s;
+          float sacc = 0.0f;
+          for (uint32_t i = 0; i < p.nq; ++i) sacc = __fadd_rn(sacc, key_ord(pmu[i * L::PM_STRIDE + k]));
+          bow[r] = sacc;
 #pragma unroll 8
           for (uint32_t i = 0; i < 32; ++i) pmu[i * L::PM_STRIDE + k] = ord_key(-INFINITY);
         }
       }
       __syncwarp();
-      if (lane == 0) { ESPN_TRACE(6, it); mbar_arrive(&uempty_bar[us]); }  // slot free
+      if (lane == 0) mbar_arrive(&S.uempty_bar[us]);  // slot free
       if (fused) {
-        const uint32_t j = it % L::NB;
-        mbar_wait(&bfree_bar[j], ((it / L::NB) & 1) ^ 1);
+        const uint32_t j = gi % L::NB;
+        mbar_wait(&S.bfree_bar[j], ((gi / L::NB) & 1) ^ 1);
 #pragma unroll
         for (int r = 0; r < NK; ++r) ring[j * L::UNITMAX + r * 32 + lane] = bow[r];
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bdone_bar[j]);
+        if (lane == 0) mbar_arrive(&S.bdone_bar[j]);
       }
 #pragma unroll
       for (int r = 0; r < NK; ++r)
@@ -942,7 +875,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
     // query's duplicate hash while the unit is scored.  RANK forms the keys
     // alpha*cls + bow (aggregate_score, scoring.hpp:12-14, no FMA contraction;
     // tail units alpha*cls) from the bow ring and writes the unit's best k,
-    // sorted, to unit_top.  finalize_kernel merges each query's unit lists.
+    // sorted, to unit_top.  finalize_kernel (or, persistent, the dedup warps)
+    // merges each query's unit lists.
     const bool fused = p.out_ids != nullptr;
     const bool is_rank = warp == L::RANK_WARP;
     uint64_t* fm = reinterpret_cast<uint64_t*>(smem + L::OFF_UK);  // rank warp: unit keys
@@ -957,16 +891,14 @@ maxsim_tc_kernel(const MaxSimParams p) {
         const uint32_t prev_b = __ldcg(&p.fused_state[1 + (par ^ 1u)]);
         const size_t n4 = (size_t)prev_b * p.hash_slots / 4;
         uint4* t4 = reinterpret_cast<uint4*>(p.dedup + (size_t)(par ^ 1u) * p.max_queries * p.hash_slots);
-        for (size_t i = (size_t)blockIdx.x * 32 + lane; i < n4; i += (size_t)gridDim.x * 32)
+        for (size_t i = (size_t)blockIdx.x * 32 + lane; i < n4; i += (size_t)G * 32)
           t4[i] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
         uint32_t* ff = p.ff_seen + (size_t)(par ^ 1u) * p.max_queries;
-        for (uint32_t i = blockIdx.x * 32 + lane; i < prev_b; i += gridDim.x * 32) ff[i] = 0;
+        for (uint32_t i = blockIdx.x * 32 + lane; i < prev_b; i += G * 32) ff[i] = 0;
       }
     }
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t ug = blockIdx.x + it * gridDim.x;
-      if (ug >= n_units) break;
-      if (!fused) break;
+    for (uint32_t it = 0; it < cnt && fused; ++it) {
+      const uint32_t ug = first + it * G, gi = gu0 + it;
       const uint4 ue = __ldcg(&p.unit_tab[ug]);
       const uint32_t b = ue.x, nd = ue.y & 0xFFu;
       const uint64_t j0 = (uint64_t)ue.z | ((uint64_t)ue.w << 32);
@@ -979,16 +911,16 @@ maxsim_tc_kernel(const MaxSimParams p) {
 #pragma unroll
       for (int r = 0; r < NK; ++r) {  // independent of the scoring: load before waiting
         const uint32_t k = r * 32 + lane;
-        idv[r] = k < nd ? __ldg(&p.cand_ids[j0 + k]) : 0u;
-        clv[r] = k < nd ? __ldg(&p.cand_cls[j0 + k]) : 0.0f;
+        idv[r] = k < nd ? __ldcg(&p.cand_ids[j0 + k]) : 0u;
+        clv[r] = k < nd ? __ldcg(&p.cand_cls[j0 + k]) : 0.0f;
       }
-      const uint32_t j = it % L::NB;
-      mbar_wait(&bdone_bar[j], (it / L::NB) & 1);
+      const uint32_t j = gi % L::NB;
+      mbar_wait(&S.bdone_bar[j], (gi / L::NB) & 1);
       float bow[NK];
 #pragma unroll
       for (int r = 0; r < NK; ++r) bow[r] = ring[j * L::UNITMAX + r * 32 + lane];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bfree_bar[j]);
+      if (lane == 0) mbar_arrive(&S.bfree_bar[j]);
       uint64_t key[NK];
       uint32_t bad = 0;
 #pragma unroll
@@ -1012,8 +944,8 @@ maxsim_tc_kernel(const MaxSimParams p) {
       uint32_t rk[NK];
 #pragma unroll
       for (int r = 0; r < NK; ++r) rk[r] = 0;
-      for (uint32_t j = 0; j < nd; ++j) {
-        const uint64_t x = fm[j];
+      for (uint32_t jj = 0; jj < nd; ++jj) {
+        const uint64_t x = fm[jj];
 #pragma unroll
         for (int r = 0; r < NK; ++r) rk[r] += x > key[r] ? 1u : 0u;
       }
@@ -1022,16 +954,164 @@ maxsim_tc_kernel(const MaxSimParams p) {
         if (r * 32 + lane < nd && rk[r] < kk) ut[rk[r]] = key[r];
       for (uint32_t i = nd + lane; i < kk; i += 32) ut[i] = 0ull;
       __syncwarp();
-      if (lane == 0) ESPN_TRACE(7, it);
     }
-    if ((p.dbg & 256u) && lane == 0 && blockIdx.x < 256) g_cta_prof[4 * blockIdx.x + (is_rank ? 1 : 3)] = ktl_now();
+    if (slot) {
+      // ---- persistent server: batch completion + the merge of finalize_kernel ----
+      __threadfence();  // this warp's unit_top / hash / error writes
+      __syncwarp();
+      if (lane == 0) atomicAdd(&slot->done_count, 1u);
+      if (!is_rank) {
+        if (lane == 0)
+          while (ld_acquire_u32(&slot->done_count) < 2u * G) __nanosleep(64);
+        __syncwarp();
+        __threadfence();
+        const uint32_t rejected = __ldcg(p.err) & (ERR_BAD_OFFSETS | ERR_CAPACITY);
+        if (fused && !rejected) {
+          uint64_t* mfm = reinterpret_cast<uint64_t*>(smem + L::OFF_FM);
+          for (uint32_t b = blockIdx.x; b < p.n_queries; b += G) {
+            const uint32_t u0 = __ldcg(&p.unit_off[b]), nu = __ldcg(&p.unit_off[b + 1]) - u0;
+            if (nu > 0) fused_merge<L::MERGE_KEYS>(p, b, u0, nu, mfm, lane);
+          }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0 && atomicAdd(&slot->merge_count, 1u) == G - 1) {
+          slot->done_count = 0;
+          slot->merge_count = 0;
+          __threadfence();
+          st_release_u32(p.done_flag, 1u);
+          st_release_u32(&slot->done, seq + 1u);
+        }
+      }
+    }
+  }
+}
+
+template <int D, bool SPLIT>
+__global__ void __launch_bounds__(TcLayout<D, SPLIT>::NTHREADS, 1)
+maxsim_tc_kernel(const MaxSimParams p) {
+  using L = TcLayout<D, SPLIT>;
+  using namespace espn_ptx;
+  // swizzled operand atoms need 1024-byte aligned stage bases: align manually
+  extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
+  uint8_t* smem = tc_smem_raw + ((1024u - (smem_u32(tc_smem_raw) & 1023u)) & 1023u);
+  TcSmem<D, SPLIT> S;
+  S.smem = smem;
+  S.sB = smem + L::OFF_B;
+  S.sA = smem + L::OFF_A;
+  S.pm = reinterpret_cast<float*>(smem + L::OFF_PM);
+  S.units = reinterpret_cast<typename L::Unit*>(smem + L::OFF_UNIT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  S.full_bar = bars;
+  S.empty_bar = bars + L::NS;
+  S.tfull_bar = bars + 2 * L::NS;
+  S.tempty_bar = S.tfull_bar + L::NBUF;
+  S.ufull_bar = S.tempty_bar + L::NBUF;
+  S.uempty_bar = S.ufull_bar + L::NU;
+  S.edone_bar = S.uempty_bar + L::NU;
+  S.bdone_bar = S.edone_bar + L::NU;
+  S.bfree_bar = S.bdone_bar + L::NB;
+  S.patched_bar = S.bfree_bar + L::NB;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  if (p.prof && tid == 0) atomicMin(&p.prof[2], (unsigned long long)gtimer());
+  ktl_begin(p.dbg, 1);
+
+  // ---- one-time setup: zero operand tiles (stale NaN bit patterns would leak
+  // into other quarters through the zero rows of A), barriers, TMEM ----------
+  {
+    uint4* z = reinterpret_cast<uint4*>(smem);
+    const int n16 = (L::OFF_PM) / 16;
+    for (int i = tid; i < n16; i += L::NTHREADS) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  {
+    int* pmk = reinterpret_cast<int*>(smem + L::OFF_PM);
+    for (int i = tid; i < L::PM_FLOATS; i += L::NTHREADS) pmk[i] = ord_key(-INFINITY);
+  }
+  fence_proxy_async_smem();
+  if (tid == 0) {
+    for (int i = 0; i < L::NS; ++i) {
+      mbar_init(&S.full_bar[i], L::NPROD);
+      mbar_init(&S.empty_bar[i], 1);
+    }
+    for (int i = 0; i < L::NBUF; ++i) {
+      mbar_init(&S.tfull_bar[i], 1);
+      mbar_init(&S.tempty_bar[i], L::NEPI);
+    }
+    for (int i = 0; i < L::NU; ++i) {
+      mbar_init(&S.ufull_bar[i], 2);  // unit loader + query-tile warp
+      mbar_init(&S.uempty_bar[i], 1);
+      mbar_init(&S.edone_bar[i], 32 * L::NEPI);
+    }
+    for (int i = 0; i < L::NB; ++i) {
+      mbar_init(&S.bdone_bar[i], 1);
+      mbar_init(&S.bfree_bar[i], 1);
+    }
+    for (int i = 0; i < L::NS; ++i) mbar_init(&S.patched_bar[i], 1);
+    mbar_fence_init();
+  }
+  if (warp == L::MMA_WARP) tmem_alloc<L::TMEM_COLS>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  S.tmem_base = *tmem_holder;
+  TcRoleState rs;
+
+  if (!p.server) {
+    // programmatic dependent of plan_kernel: everything above overlapped it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // let the dependent grid launch now (the plan is complete): the finalize
+    // merge or the top-k kernel's id-only dedup prologue runs on the SMs'
+    // spare resources concurrently with this kernel
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    tc_batch<D, SPLIT>(p, S, rs, nullptr, 0u);
+  } else {
+    // ---- persistent re-rank server: every warp walks the queue in order ----
+    ServerQueue* Q = p.server;
+    const unsigned long long idle_ns = Q->idle_ns;
+    for (uint32_t seq = 0;; ++seq) {
+      ServerSlot* sl = &Q->slot[seq % kServerSlots];
+      uint32_t stop = 0;
+      if (lane == 0) {
+        const unsigned long long t_wait = gtimer();
+        for (;;) {
+          if (ld_acquire_u32(&sl->ready) == seq + 1u) break;
+          const unsigned long long st = ld_acquire_u64(&Q->state);
+          if (st == (kServerStopped | seq)) { stop = 1; break; }  // stopped here by another warp
+          if ((st & ~kServerStopped) == seq &&                    // nothing taken beyond what we wait for
+              (ld_acquire_u32(&Q->stop_req) || gtimer() - t_wait > idle_ns) &&
+              atomicCAS(&Q->state, (unsigned long long)seq, kServerStopped | seq) == seq) {
+            stop = 1;
+            break;
+          }
+          __nanosleep(200);
+        }
+      }
+      if (__shfl_sync(0xffffffffu, stop, 0)) break;
+      // the batch descriptor, L2-coherent (the slot is rewritten every kServerSlots batches)
+      MaxSimParams P;
+      {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(&sl->p);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&P);
+#pragma unroll 8
+        for (int i = 0; i < (int)(sizeof(MaxSimParams) / 4); ++i) dst[i] = __ldcg(src + i);
+      }
+      tc_batch<D, SPLIT>(P, S, rs, sl, seq);
+    }
   }
 
   tc_fence_before();
   __syncthreads();
   if (warp == L::MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc<L::TMEM_COLS>(tmem_base);
+    tmem_dealloc<L::TMEM_COLS>(S.tmem_base);
+  }
+  if (p.server && tid == 0 && atomicAdd(&p.server->exited, 1u) == gridDim.x - 1) {
+    __threadfence_system();
+    *reinterpret_cast<volatile uint32_t*>(p.server->alive_host) = 0u;  // the host may relaunch
   }
   ktl_end(p.dbg, 1);
   if ((p.dbg & 256u) && threadIdx.x == 0 && blockIdx.x < 256) g_cta_prof[4 * blockIdx.x] = ktl_now();
@@ -1043,22 +1123,6 @@ maxsim_tc_kernel(const MaxSimParams p) {
       atomicAdd(&p.prof[1], 1ull);
       p.prof[2] = ~0ull;
       p.prof[3] = 0;
-    }
-  }
-  if ((p.dbg & 8u) && blockIdx.x == 0 && tid == 0) {
-    const char* nm[8] = {"ld.start", "ld.slot", "ld.ready", "pr.start", "ep.start", "ep.mmadone", "ep.done", "cb.topk"};
-    printf("CTA0 units=%u end=%.2fus\n", (n_units + gridDim.x - 1) / gridDim.x, (gtimer() - t_start) / 1e3);
-    for (int e = 0; e < 8; ++e) {
-      printf("%-11s", nm[e]);
-      for (int u = 0; u < 8 && blockIdx.x + u * gridDim.x < n_units; ++u)
-        printf(" %8.2f", ((int64_t)(trace[e * 8 + u] - t_start)) / 1e3);
-      printf("\n");
-    }
-    const char* sn[9] = {"P.empty", "M.full", "M.tempty", "E.tfull", "E.ldone", "E.proc", "P.issued", "E.gm", "E.rel"};
-    for (int e = 0; e < 9; ++e) {
-      printf("%-9s", sn[e]);
-      for (int g = 0; g < 16; ++g) printf(" %6.2f", ((int64_t)(strace[e * 16 + g] - t_start)) / 1e3);
-      printf("\n");
     }
   }
 }
