@@ -297,6 +297,9 @@ ESPN_API int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const
 ESPN_API int espn_gpu_server_start(espn_gpu_table* table, uint32_t flags, uint32_t idle_us);
 ESPN_API int espn_gpu_server_stop(espn_gpu_table* table);
 ESPN_API int espn_gpu_server_running(const espn_gpu_table* table);
+/* Diagnostics: {state, stop_req, exited CTAs, idle_ns, slot0 ready, slot0 done,
+   slot0 done|merge counts, alive | launches << 8}. */
+ESPN_API int espn_gpu_server_debug(const espn_gpu_table* table, uint64_t* out8);
 
 /* ---- Multi-GPU --------------------------------
  * One process (rank) per GPU, or one process driving several GPUs.  Every rank

@@ -710,6 +710,26 @@ int espn_gpu_server_stop(espn_gpu_table* t) {
   return ESPN_OK;
 }
 
+int espn_gpu_server_debug(const espn_gpu_table* t, uint64_t* out8) {
+  if (!t || !t->server || !out8) return fail(ESPN_E_INVALID_INPUT, "no server");
+  DeviceGuard g(t->device);
+  cudaStream_t cs = nullptr;
+  ESPN_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  ServerQueue h;
+  ESPN_CUDA_TRY(cudaMemcpyAsync(&h, t->server, sizeof h, cudaMemcpyDeviceToHost, cs));
+  ESPN_CUDA_TRY(cudaStreamSynchronize(cs));
+  cudaStreamDestroy(cs);
+  out8[0] = h.state;
+  out8[1] = h.stop_req;
+  out8[2] = h.exited;
+  out8[3] = h.idle_ns;
+  out8[4] = h.slot[0].ready;
+  out8[5] = h.slot[0].done;
+  out8[6] = (uint64_t)h.slot[0].done_count | ((uint64_t)h.slot[0].merge_count << 32);
+  out8[7] = *reinterpret_cast<volatile uint32_t*>(t->server_alive_h) | (t->server_launches << 8);
+  return ESPN_OK;
+}
+
 int espn_gpu_server_running(const espn_gpu_table* t) {
   return (t && t->server && *reinterpret_cast<volatile uint32_t*>(t->server_alive_h)) ? 1 : 0;
 }
@@ -1858,7 +1878,8 @@ int espn_gpu_get_counters(const espn_gpu_workspace* w, espn_counters* out) {
   unsigned long long kp[2] = {0, 0};
   {
     DeviceGuard g(w->table->device);
-    ESPN_CUDA_TRY(cudaDeviceSynchronize());
+    // (not while a persistent server runs: a device-wide sync would wait for it)
+    if (!espn_gpu_server_running(w->table)) ESPN_CUDA_TRY(cudaDeviceSynchronize());
     ESPN_CUDA_TRY(cudaMemcpy(kp, w->kprof, sizeof kp, cudaMemcpyDeviceToHost));
   }
   out->maxsim_device_ns = kp[0];
