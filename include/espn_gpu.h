@@ -296,6 +296,11 @@ ESPN_API int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const
  * are identical to unserved calls.  espn_gpu_table_close stops it. */
 ESPN_API int espn_gpu_server_start(espn_gpu_table* table, uint32_t flags, uint32_t idle_us);
 ESPN_API int espn_gpu_server_stop(espn_gpu_table* table);
+/* Stop the kernel (once drained) but keep the table attached: calls stay in
+ * served mode (captures record plan + wait), the next eager served call or
+ * espn_gpu_server_start relaunches it.  CUDA-graph replays of served batches
+ * need a running server (otherwise they fail with INVALID_STATE). */
+ESPN_API int espn_gpu_server_pause(espn_gpu_table* table);
 ESPN_API int espn_gpu_server_running(const espn_gpu_table* table);
 /* Diagnostics: {state, stop_req, exited CTAs, idle_ns, slot0 ready, slot0 done,
    slot0 done|merge counts, alive | launches << 8}. */

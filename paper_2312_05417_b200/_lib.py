@@ -122,6 +122,7 @@ SIGNATURES = {
     "espn_gpu_gather_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "espn_gpu_server_start": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32]),
     "espn_gpu_server_stop": (C.c_int, [C.c_void_p]),
+    "espn_gpu_server_pause": (C.c_int, [C.c_void_p]),
     "espn_gpu_server_running": (C.c_int, [C.c_void_p]),
     "espn_gpu_server_debug": (C.c_int, [C.c_void_p, C.c_void_p]),
     "espn_nccl_get_unique_id": (C.c_int, [C.c_void_p]),

@@ -412,6 +412,11 @@ class GpuStore:
     def server_stop(self) -> None:
         _check(L.lib().espn_gpu_server_stop(self._h))
 
+    def server_pause(self) -> None:
+        """Stop the kernel but stay in served mode (capture graphs now;
+        server_start relaunches it before replaying them)."""
+        _check(L.lib().espn_gpu_server_pause(self._h))
+
     @property
     def server_running(self) -> bool:
         return bool(L.lib().espn_gpu_server_running(self._h))

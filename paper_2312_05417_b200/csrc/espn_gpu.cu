@@ -139,6 +139,9 @@ cudaError_t launch_tc(const MaxSimParams& p, int num_sms, cudaStream_t s, bool p
   static std::atomic<uint64_t> attr_set{0};
   {
     cudaError_t e = smem_attr_once(maxsim_tc_kernel<D, SPLIT>, L::SMEM_BYTES, attr_set);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(maxsim_tc_kernel<D, SPLIT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
   }
   // persistent: one CTA per SM; the unit count is read on the device.  As a
@@ -610,11 +613,39 @@ int server_launch(espn_gpu_table* t) {
   return ESPN_OK;
 }
 
-// Before a served batch: relaunch a server that exited idle.  Not inside a
-// stream capture (the relaunch synchronises).
-int server_ensure(espn_gpu_table* t) {
+// Before a served batch: relaunch a server that exited (idle or paused).
+// Inside a stream capture nothing is launched: the captured plan submits to
+// whatever server runs when the graph is replayed (none: ERR_SERVER).
+int server_ensure(espn_gpu_table* t, cudaStream_t s) {
   if (*reinterpret_cast<volatile uint32_t*>(t->server_alive_h)) return ESPN_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  ESPN_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return ESPN_OK;
   return server_launch(t);
+}
+
+// The SM's shared-memory carveout is fixed while CTAs are resident: a CTA
+// whose kernel prefers another split cannot join an SM the server occupies.
+// The per-batch kernels therefore ask for the server's (maximum) carveout.
+cudaError_t server_carveouts() {
+  cudaError_t e = cudaFuncSetAttribute(plan_kernel<16>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(server_wait_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  return e;
+}
+
+// Stop the kernel once the queue is drained (the table stays attached).
+void server_halt(espn_gpu_table* t) {
+  cudaStream_t cs = nullptr;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess) {
+    static const uint32_t one = 1u;
+    cudaMemcpyAsync(&t->server->stop_req, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
+    cudaStreamSynchronize(cs);
+    cudaStreamDestroy(cs);
+  }
+  cudaStreamSynchronize(t->server_stream);
 }
 }  // namespace
 
@@ -623,7 +654,7 @@ extern "C" {
 int espn_gpu_server_start(espn_gpu_table* t, uint32_t flags, uint32_t idle_us) {
   if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
   DeviceGuard g(t->device);
-  if (t->server) return server_ensure(t);
+  if (t->server) return server_ensure(t, nullptr);
   if (!t->tc_ok || !tc_supported(t->d))
     return fail(ESPN_E_INVALID_CONFIG, "the persistent server runs the tcgen05 MaxSim: needs sm_100 and d in {16,32,64,128}");
   if (t->tiered) return fail(ESPN_E_INVALID_CONFIG, "the persistent server serves HBM-resident (untiered) tables");
@@ -635,7 +666,7 @@ int espn_gpu_server_start(espn_gpu_table* t, uint32_t flags, uint32_t idle_us) {
     ESPN_CUDA_TRY(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, t->device));
     ESPN_CUDA_TRY(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, t->device));
     cudaFuncAttributes fp{}, fw{};
-    ESPN_CUDA_TRY(cudaFuncGetAttributes(&fp, plan_kernel));
+    ESPN_CUDA_TRY(cudaFuncGetAttributes(&fp, plan_kernel<16>));
     ESPN_CUDA_TRY(cudaFuncGetAttributes(&fw, server_wait_kernel));
     int tc_smem = 0, tc_threads = 0, tc_regs = 0;
     switch (t->d * 2 + (split ? 1 : 0)) {
@@ -652,12 +683,18 @@ int espn_gpu_server_start(espn_gpu_table* t, uint32_t flags, uint32_t idle_us) {
 #undef ESPN_SZ
     }
     const int need_smem = tc_smem + reserved + (int)fp.sharedSizeBytes + reserved;
-    const int need_regs = tc_regs * tc_threads + fp.numRegs * kPlanThreads + fw.numRegs * 32;
-    if (need_smem > smem_sm || need_regs > regs_sm)
+    // registers come from the SM's 4 sub-partitions (16K each); a CTA's warps
+    // are spread over all four, so the busiest sub-partition (ceil(17/4) = 5
+    // server warps) must still hold a plan (or wait) warp
+    auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
+    const int tc_warps = tc_threads / 32;
+    const int need_regs = ((tc_warps + 3) / 4) * warp_regs(tc_regs) + std::max(warp_regs(fp.numRegs), warp_regs(fw.numRegs));
+    if (need_smem > smem_sm || need_regs > regs_sm / 4)
       return fail(ESPN_E_INVALID_CONFIG, "persistent server: the plan kernel would not fit beside a server CTA (smem " +
                                              std::to_string(need_smem) + "/" + std::to_string(smem_sm) + ", regs " +
-                                             std::to_string(need_regs) + "/" + std::to_string(regs_sm) + ")");
+                                             std::to_string(need_regs) + "/" + std::to_string(regs_sm / 4) + " per sub-partition)");
   }
+  ESPN_CUDA_TRY(server_carveouts());
   ServerQueue* q = nullptr;
   uint32_t* alive = nullptr;
   cudaStream_t st = nullptr;
@@ -689,18 +726,17 @@ int espn_gpu_server_start(espn_gpu_table* t, uint32_t flags, uint32_t idle_us) {
   return ESPN_OK;
 }
 
+int espn_gpu_server_pause(espn_gpu_table* t) {
+  if (!t || !t->server) return ESPN_OK;
+  DeviceGuard g(t->device);
+  server_halt(t);
+  return ESPN_OK;
+}
+
 int espn_gpu_server_stop(espn_gpu_table* t) {
   if (!t || !t->server) return ESPN_OK;
   DeviceGuard g(t->device);
-  // ask the kernel to stop once the queue is drained, then wait for it
-  cudaStream_t cs = nullptr;
-  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess) {
-    static const uint32_t one = 1u;
-    cudaMemcpyAsync(&t->server->stop_req, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
-    cudaStreamSynchronize(cs);
-    cudaStreamDestroy(cs);
-  }
-  cudaStreamSynchronize(t->server_stream);
+  server_halt(t);  // the kernel stops once the queue is drained
   cudaStreamDestroy(t->server_stream);
   cudaFree(t->server);
   cudaFreeHost(t->server_alive_h);
@@ -1135,7 +1171,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     return fail(ESPN_E_INVALID_STATE, "a persistent re-rank server runs on this table: only fused tcgen05 batches "
                                       "(final_k <= 32, the server's query precision) can be served; stop it first");
   if (served) {
-    const int ss = server_ensure(t);
+    const int ss = server_ensure(t, s);
     if (ss) return ss;
   }
   // dedup hash of the separate top-k kernel, sized by the longest scored list
@@ -1401,7 +1437,10 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     sb.plan_done = w->plan_done;
     sb.msp = mp;
   }
-  plan_kernel<<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp, sb);
+  if (served)
+    plan_kernel<16><<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp, sb);
+  else
+    plan_kernel<1><<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp, sb);
   ESPN_CUDA_TRY(cudaGetLastError());
 
   // ---- tiered table: host-tier rows staged into HBM (prefetched or now) ----
@@ -1547,6 +1586,10 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     if (ge != cudaSuccess) return fail(ESPN_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ge));
     std::copy(gkey, gkey + 5, w->sg_key);
     s = user_s;
+    if (served) {  // instantiation may have waited for an idle server to exit
+      const int ss = server_ensure(t, s);
+      if (ss) return ss;
+    }
     ESPN_CUDA_TRY(cudaGraphLaunch(w->sg_exec, s));
     // (an event recorded during capture is only a capture dependency: record
     // the slot's completion on the caller's stream, after the graph)

@@ -142,7 +142,12 @@ __device__ __noinline__ void server_submit(const ServerSubmit& sb) {
   st_release_u32(&sl->ready, (uint32_t)seq + 1u);
 }
 
-__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanParams q, const ServerSubmit sb) {
+// MINB = 16 caps the plan at 32 registers: a served batch's plan CTA must fit
+// beside a persistent MaxSim CTA, whose 17 warps x 96 registers leave only
+// 1024 registers free on the SM sub-partition holding 5 of them (each of the 4
+// sub-partitions has 16K registers; a CTA's warps are spread over all four).
+template <int MINB>
+__global__ void __launch_bounds__(kPlanThreads, MINB) plan_kernel(const PlanParams q, const ServerSubmit sb) {
   ktl_begin(q.dbg, 0);
   // the MaxSim kernel is a programmatic dependent: its prologue (barriers,
   // TMEM, operand zeroing) overlaps this kernel; it waits before reading the plan

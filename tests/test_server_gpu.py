@@ -78,6 +78,9 @@ def test_many_batches_three_workspaces_graphs(cuda_ok):
     ref = [x for x in api.Reranker(store, B, Cn, 32).rerank_arrays(q, ids, cls, off, cfg)[:3]]
     store.server_start()
     flags = L.ESPN_RERANK_DEVICE_IO | L.ESPN_RERANK_DEVICE_OFFSETS | L.ESPN_RERANK_ASYNC
+    # (while the server runs, allocations and device-wide syncs in the process
+    # wait for it to go idle: graphs are captured with the server paused and
+    # nothing but the replays runs while it serves)
 
     def enqueue(rr, out, sp):
         a = L.RerankArgs(n_queries=B, n_query_tokens=32, query_tokens=dq.data_ptr(), cand_ids=di.data_ptr(),
@@ -91,21 +94,27 @@ def test_many_batches_three_workspaces_graphs(cuda_ok):
     graphs = []
     for rr, out, s in lanes:
         with torch.cuda.stream(s):
-            enqueue(rr, out, s.cuda_stream)
+            enqueue(rr, out, s.cuda_stream)  # eager, served
         s.synchronize()
+        rr.sync(s.cuda_stream)
+    store.server_pause()
+    for rr, out, s in lanes:
+        out.zero_()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             enqueue(rr, out, torch.cuda.current_stream().cuda_stream)
         graphs.append(g)
+    torch.cuda.synchronize()
+    store.server_start()  # relaunch before the replays
     for i in range(60):
         rr, out, s = lanes[i % 3]
         with torch.cuda.stream(s):
-            out.zero_()
             graphs[i % 3].replay()
     for rr, out, s in lanes:
         s.synchronize()
         rr.sync(s.cuda_stream)
-        h = out.cpu().numpy()
+    hs = [out.cpu().numpy() for _, out, _ in lanes]
+    for h in hs:
         assert np.array_equal(h[:B * 10].view(np.uint32).reshape(B, 10), ref[0])
         assert np.array_equal(h[B * 10:2 * B * 10].view(np.float32).reshape(B, 10), ref[1])
     store.server_stop()

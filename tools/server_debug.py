@@ -21,12 +21,21 @@ store.server_start(idle_us=int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 dbg(store, "after start")
 time.sleep(0.01)
 dbg(store, "after 10ms")
+import torch
+mode = sys.argv[2] if len(sys.argv) > 2 else "host"
+dq, di, dc = torch.from_numpy(q).cuda(), torch.from_numpy(ids.view(np.int32)).cuda(), torch.from_numpy(cls).cuda()
+st = torch.cuda.Stream()
 for i in range(3):
     try:
-        got = rr.rerank_arrays(q, ids, cls, off, cfg)
-        print("call", i, "ok", np.array_equal(got[0], ref[0]), flush=True)
+        t0 = time.perf_counter()
+        if mode == "host":
+            got = rr.rerank_arrays(q, ids, cls, off, cfg)
+        else:
+            got = rr.rerank_arrays(dq, di, dc, off, cfg, device_io=True, stream=st.cuda_stream)
+            got = [x.cpu().numpy() for x in got[:3]]
+        print("call", i, "ok", np.array_equal(got[0].view(np.uint32), ref[0]), "%.1f ms" % ((time.perf_counter() - t0) * 1e3), flush=True)
     except Exception as e:
-        print("call", i, "error", e, flush=True)
+        print("call", i, "error", e, "%.1f ms" % ((time.perf_counter() - t0) * 1e3), flush=True)
     dbg(store, f"after call {i}")
 time.sleep(0.2)
 dbg(store, "after 200ms")
