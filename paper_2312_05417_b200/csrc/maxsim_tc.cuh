@@ -144,7 +144,13 @@ struct TcLayout {
   static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
   static constexpr int MERGE_KEYS = 640;           // persistent server: the dedup warp's merge scratch
   static constexpr int OFF_FM = (OFF_TMEM + 16 + 15) / 16 * 16;
-  static constexpr int SMEM_BYTES = OFF_FM + MERGE_KEYS * 8 + 1024;  // + alignment slack
+  // persistent server: the CTA's batch gate -- a 4-deep ring of batch
+  // descriptors copied from the global queue by the loader warp, and
+  // {published count, stop marker, per-ring-slot finished-warp counts}
+  static constexpr int DESC_RING = 4;
+  static constexpr int OFF_DESC = OFF_FM + MERGE_KEYS * 8;
+  static constexpr int OFF_GATE = OFF_DESC + DESC_RING * (int)sizeof(MaxSimParams);
+  static constexpr int SMEM_BYTES = OFF_GATE + 32 + 1024;  // + alignment slack
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(STAGE_BYTES % 1024 == 0 && A_BYTES % 16 == 0, "alignment");
 };
@@ -961,12 +967,13 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       __syncwarp();
       if (lane == 0) atomicAdd(&slot->done_count, 1u);
       if (!is_rank) {
-        if (lane == 0)
-          while (ld_acquire_u32(&slot->done_count) < 2u * G) __nanosleep(64);
+        const bool merges = fused && blockIdx.x < p.n_queries;  // this CTA merges queries blockIdx.x + i*G
+        if (merges && lane == 0)
+          while (ld_acquire_u32(&slot->done_count) < 2u * G) __nanosleep(256);
         __syncwarp();
         __threadfence();
-        const uint32_t rejected = __ldcg(p.err) & (ERR_BAD_OFFSETS | ERR_CAPACITY);
-        if (fused && !rejected) {
+        const uint32_t rejected = merges ? __ldcg(p.err) & (ERR_BAD_OFFSETS | ERR_CAPACITY) : 1u;
+        if (merges && !rejected) {
           uint64_t* mfm = reinterpret_cast<uint64_t*>(smem + L::OFF_FM);
           for (uint32_t b = blockIdx.x; b < p.n_queries; b += G) {
             const uint32_t u0 = __ldcg(&p.unit_off[b]), nu = __ldcg(&p.unit_off[b + 1]) - u0;
@@ -1030,6 +1037,7 @@ maxsim_tc_kernel(const MaxSimParams p) {
   {
     int* pmk = reinterpret_cast<int*>(smem + L::OFF_PM);
     for (int i = tid; i < L::PM_FLOATS; i += L::NTHREADS) pmk[i] = ord_key(-INFINITY);
+    if (tid < 8) reinterpret_cast<uint32_t*>(smem + L::OFF_GATE)[tid] = 0u;
   }
   fence_proxy_async_smem();
   if (tid == 0) {
@@ -1070,36 +1078,62 @@ maxsim_tc_kernel(const MaxSimParams p) {
     tc_batch<D, SPLIT>(p, S, rs, nullptr, 0u);
   } else {
     // ---- persistent re-rank server: every warp walks the queue in order ----
+    // Only the loader warp's lane 0 polls the global queue (one poller per
+    // CTA keeps the queue's cache line cool); it copies each batch descriptor
+    // into the CTA's shared ring and opens the gate; the other warps wait on
+    // the gate in shared memory and read the descriptor from the ring.
     ServerQueue* Q = p.server;
     const unsigned long long idle_ns = Q->idle_ns;
+    MaxSimParams* ring = reinterpret_cast<MaxSimParams*>(smem + L::OFF_DESC);
+    volatile uint32_t* gate = reinterpret_cast<volatile uint32_t*>(smem + L::OFF_GATE);
+    constexpr int NW = (int)(sizeof(MaxSimParams) / 4);
     for (uint32_t seq = 0;; ++seq) {
       ServerSlot* sl = &Q->slot[seq % kServerSlots];
+      const uint32_t rslot = seq % L::DESC_RING;
       uint32_t stop = 0;
-      if (lane == 0) {
-        const unsigned long long t_wait = gtimer();
-        for (;;) {
-          if (ld_acquire_u32(&sl->ready) == seq + 1u) break;
-          const unsigned long long st = ld_acquire_u64(&Q->state);
-          if (st == (kServerStopped | seq)) { stop = 1; break; }  // stopped here by another warp
-          if ((st & ~kServerStopped) == seq &&                    // nothing taken beyond what we wait for
-              (ld_acquire_u32(&Q->stop_req) || gtimer() - t_wait > idle_ns) &&
-              atomicCAS(&Q->state, (unsigned long long)seq, kServerStopped | seq) == seq) {
-            stop = 1;
-            break;
+      if (warp == L::LOADER_WARP) {
+        if (lane == 0) {
+          const unsigned long long t_wait = gtimer();
+          for (;;) {
+            if (ld_acquire_u32(&sl->ready) == seq + 1u) break;
+            const unsigned long long st = ld_acquire_u64(&Q->state);
+            if (st == (kServerStopped | seq)) { stop = 1; break; }  // stopped here by another CTA
+            if ((st & ~kServerStopped) == seq &&                    // nothing taken beyond what we wait for
+                (ld_acquire_u32(&Q->stop_req) || gtimer() - t_wait > idle_ns) &&
+                atomicCAS(&Q->state, (unsigned long long)seq, kServerStopped | seq) == seq) {
+              stop = 1;
+              break;
+            }
+            __nanosleep(400);
           }
-          __nanosleep(200);
+          // the ring slot is free once every warp finished the batch RING before
+          if (!stop && seq >= (uint32_t)L::DESC_RING)
+            while (gate[2 + rslot] < (uint32_t)L::NWARPS * (seq / L::DESC_RING)) __nanosleep(32);
+        }
+        stop = __shfl_sync(0xffffffffu, stop, 0);
+        if (!stop) {
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(&sl->p);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(&ring[rslot]);
+          for (int i = lane; i < NW; i += 32) dst[i] = __ldcg(src + i);
+          __threadfence_block();
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (stop) gate[1] = seq + 1u;
+          else gate[0] = seq + 1u;
+        }
+      } else if (lane == 0) {
+        for (;;) {
+          if (gate[0] > seq) break;
+          if (gate[1] == seq + 1u) { stop = 1; break; }
+          __nanosleep(32);
         }
       }
       if (__shfl_sync(0xffffffffu, stop, 0)) break;
-      // the batch descriptor, L2-coherent (the slot is rewritten every kServerSlots batches)
-      MaxSimParams P;
-      {
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(&sl->p);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(&P);
-#pragma unroll 8
-        for (int i = 0; i < (int)(sizeof(MaxSimParams) / 4); ++i) dst[i] = __ldcg(src + i);
-      }
-      tc_batch<D, SPLIT>(P, S, rs, sl, seq);
+      __threadfence_block();
+      tc_batch<D, SPLIT>(ring[rslot], S, rs, sl, seq);
+      __syncwarp();
+      if (lane == 0) atomicAdd(const_cast<uint32_t*>(&gate[2 + rslot]), 1u);  // done with the ring slot
     }
   }
 
