@@ -30,8 +30,11 @@ def _lists(rng, n_docs, B, kmax, src):
             np.asarray(offs, np.uint64))
 
 
-@pytest.mark.parametrize("d,dtype", [(32, "f16"), (16, "bf16"), (64, "f16"), (128, "bf16")])
-def test_random_shapes_against_oracle(oracle, cuda_ok, d, dtype):
+@pytest.mark.parametrize("d,dtype,served", [(32, "f16", False), (16, "bf16", False), (64, "f16", False),
+                                            (128, "bf16", False), (32, "f16", True), (64, "bf16", True)])
+def test_random_shapes_against_oracle(oracle, cuda_ok, d, dtype, served):
+    # served: the same cases through the persistent re-rank server (fused
+    # top-k only: k <= 32, the server's query precision)
     import oracle_py
     odt = oracle_py.F16 if dtype == "f16" else oracle_py.BF16
     rng = np.random.default_rng(1000 + d)
@@ -40,18 +43,20 @@ def test_random_shapes_against_oracle(oracle, cuda_ok, d, dtype):
     store = api.GpuStore(rp, codes, d, dtype=dtype)
     rr = api.Reranker(store, 17, 17 * 900, 32)
     ot = oracle.OracleTable(rp, codes, d, dtype=odt)
+    if served:
+        store.server_start()
     for case in range(int(os.environ.get("ESPN_FUZZ_CASES", "8"))):
         B = int(rng.choice([1, 2, 5, 17]))
         kmax = int(rng.choice([1, 30, 300, 900]))
         nq = int(rng.choice([1, 7, 32]))
         q, src = synth.make_queries(rp, codes, d, B, nq=nq, dtype=dtype, seed=case + 10 * d)
         ids, cls, off = _lists(rng, n_docs, B, kmax, src)
-        k = int(rng.choice([1, 10, 32, 100]))
+        k = int(rng.choice([1, 10, 32] if served else [1, 10, 32, 100]))
         partial = bool(rng.random() < 0.5)
         R = int(rng.integers(1, kmax + 2)) if partial else int(rng.choice([k, max(k, kmax // 2), kmax + 5]))
         alpha = float(rng.choice([1.0, 0.5, 2.0]))
         cfg = api.PipelineConfig(rerank_count=R, final_k=k, alpha=alpha, partial_rerank_enabled=partial)
-        qp = str(rng.choice(["auto", "auto", "split", "rounded"]))
+        qp = "auto" if served else str(rng.choice(["auto", "auto", "split", "rounded"]))
         # the reference's fp32 query, unrounded (the legacy "rounded" mode: the dtype-rounded one)
         qr = oracle.round_to(q, odt) if qp == "rounded" else np.ascontiguousarray(q, np.float32)
         if not partial and R < k:  # R < final_k needs partial re-ranking: both sides reject
@@ -74,5 +79,7 @@ def test_random_shapes_against_oracle(oracle, cuda_ok, d, dtype):
                 n = int(on[b])
                 assert_topk_equivalent(gi[b, :n], gs[b, :n], oi[b, :n], os_[b, :n], ids[a0:a1], full,
                                        ctx=f"d={d} {qp} case {case} rep {rep} query {b}")
+    if served:
+        store.server_stop()
     rr.close()
     store.close()
