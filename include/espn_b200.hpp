@@ -25,6 +25,7 @@
 #include <istream>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <set>
 #include <span>
 #include <string>
@@ -217,7 +218,19 @@ class Store {
   // allowed, unknown ids -> InvalidInputError; values decoded to fp32.
   FetchResult fetch_batch(std::span<const DocId> doc_ids) const;
 
+  // Per-record I/O of the reference store (store.hpp:61-65): payload bytes
+  // and ceil(bytes / 4096) blocks of doc `id`'s record (buffered reads).
+  std::pair<std::uint64_t, std::uint64_t> record_io(DocId id) const;
+
+  // The calling thread's cached workspace, at least this large (the free
+  // rerank_batch / rerank_candidates reuse it instead of allocating one per
+  // call; one per thread, so concurrent callers never share scratch).
+  class Reranker& thread_reranker(std::uint32_t max_queries, std::uint32_t max_candidates,
+                                  std::uint32_t max_query_tokens) const;
+
  private:
+  struct WorkspaceCache;
+  std::unique_ptr<WorkspaceCache> cache_;
   espn_gpu_table* table_ = nullptr;
   std::uint32_t d_ = 0;
   Dtype dtype_ = Dtype::f16;
@@ -239,9 +252,19 @@ class Reranker {
   // run_batch (pipeline.hpp:81-85) restricted to stages 3-6: one device pass
   // for the whole batch, per-query results identical to single-query calls.
   // prefetched: the batch consumes the staging of the last prefetch_hints
-  // call (tiered stores); QueryStats then carry the device's fetch accounting.
+  // call (tiered stores).  QueryStats follow the reference exactly
+  // (pipeline.hpp:45-53, the oracle's eo_rerank_query): prefetched = the
+  // query's snapshot ids given to prefetch_hints (none when !prefetched),
+  // hits = needed ∩ prefetched, per-record byte / block counters.  The tier
+  // view (rows resident in HBM vs staged over PCIe) is last_fetch_stats().
   BatchResult rerank(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
                      const PipelineConfig& config, Kernel kernel = Kernel::automatic, bool prefetched = false);
+
+  // Device fetch accounting of the last rerank, per query (espn_fetch_stats).
+  const std::vector<espn_fetch_stats>& last_fetch_stats() const { return last_fs_; }
+  std::uint32_t max_queries() const { return max_queries_; }
+  std::uint32_t max_candidates() const { return max_candidates_; }
+  std::uint32_t max_query_tokens() const { return max_nq_; }
 
   // run_query stages (1)-(2) (pipeline.hpp:56-64): stage the host-tier rows of
   // the cursors' snapshots after delta clusters (SearchCursor::snapshot,
@@ -256,7 +279,17 @@ class Reranker {
  private:
   const Store* store_;
   espn_gpu_workspace* ws_ = nullptr;
+  std::uint32_t max_queries_ = 0, max_candidates_ = 0, max_nq_ = 0;
+  std::vector<std::uint32_t> hint_ids_;   // last prefetch_hints snapshot (CSR)
+  std::vector<std::uint64_t> hint_off_;
+  std::vector<espn_fetch_stats> last_fs_;
 };
+
+// QueryStats of one query exactly as the reference computes them
+// (pipeline.hpp:45-53): needed = the first n_needed candidates, prefetched =
+// the ids the prefetcher fetched; record sizes from the store's manifest layout.
+QueryStats query_stats(const Store& store, QueryId query_id, std::span<const DocId> candidates, std::uint64_t n_needed,
+                       std::span<const DocId> prefetched);
 
 // build_store (store.hpp:48-51) from a CSR of fp32 rows (+ n_docs * d_cls CLS
 // values, or empty for zeros): writes <base>.espn / .manifest / .manifest.json.

@@ -255,6 +255,14 @@ ESPN_API int espn_gpu_prefetch_hints(espn_gpu_table* table, espn_gpu_workspace* 
  * duplicate candidate -> INVALID_INPUT). */
 ESPN_API int espn_gpu_workspace_sync(espn_gpu_workspace* ws, void* stream);
 
+/* Per-candidate fetch status of the workspace's last completed batch (the
+ * record-level accounting behind QueryStats, pipeline.hpp:45-53): for each of
+ * the first n candidates of the batch, 0 = the row was in HBM, 1 = staged by
+ * the prefetcher before scoring (hit), 2 = staged on the critical path
+ * (missed), 3 = not staged (staging overflow / unknown id).  Only the needed
+ * candidates (first min(R, n_b) of each query) are defined.  HOST array. */
+ESPN_API int espn_gpu_workspace_cand_status(espn_gpu_workspace* ws, uint8_t* out, uint64_t n);
+
 /* Gather (StoreHandle::fetch_batch, store.hpp:91-94): copies the token rows of
  * `ids` (request order, duplicates allowed) into out_rows as CSR with
  * out_row_ptr[n+1] (token offsets).  ids/out_* are device pointers.

@@ -108,6 +108,7 @@ SIGNATURES = {
     "espn_gpu_workspace_destroy": (C.c_int, [C.c_void_p]),
     "espn_gpu_rerank": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.POINTER(RerankOut), C.c_void_p]),
     "espn_gpu_workspace_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "espn_gpu_workspace_cand_status": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "espn_gpu_prefetch": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.c_void_p]),
     "espn_gpu_prefetch_hints": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
                                           C.c_void_p]),

@@ -742,24 +742,43 @@ class NcclComm:
             self._h = None
 
 
+def record_io(store: GpuStore, token_counts) -> Tuple[np.ndarray, np.ndarray]:
+    """Per-record (bytes, blocks) of the reference store (store.hpp:61-65,
+    SPEC.md "Block accounting"): buffered reads move the exact payload
+    record_bytes = (d_cls + t*d) * value_width and touch ceil(bytes / 4096)
+    blocks."""
+    rec = store.record_bytes(np.asarray(token_counts, np.uint64)).astype(np.uint64)
+    return rec, (rec + np.uint64(4095)) // np.uint64(4096)
+
+
 def _stats_for(store: GpuStore, ids: np.ndarray, n_needed: int, query_id: int, elapsed: float,
-               fetch: Optional[dict] = None) -> QueryStats:
-    """QueryStats (pipeline.hpp:36-54) from the device fetch accounting
-    (espn_fetch_stats): needed rows are either HBM-resident, staged ahead by the
-    prefetcher, or staged on the critical path (missed).  hit_rate =
-    |available before scoring| / |needed| (pipeline.hpp:48)."""
-    st = QueryStats(query_id=query_id, needed_count=n_needed, rerank_time=elapsed, total_time=elapsed)
-    tok = store.token_counts(ids[:n_needed]) if n_needed else np.zeros(0, np.uint64)
-    if tok is not None:
-        st.needed_payload_bytes = int(store.record_bytes(tok).sum()) if n_needed else 0
-    if fetch is None:
-        fetch = dict(needed=n_needed, resident=n_needed, prefetched=0, missed=0, prefetch_bytes=0, critical_bytes=0)
-    st.prefetched_count = fetch["prefetched"]
-    st.missed_count = fetch["missed"]
-    st.prefetch_bytes = fetch["prefetch_bytes"]
-    st.critical_fetch_bytes = fetch["critical_bytes"]
-    st.critical_blocks_read = (fetch["critical_bytes"] + 4095) // 4096
-    st.hit_rate = (fetch["resident"] + fetch["prefetched"]) / n_needed if n_needed else 0.0
+               prefetched_ids=None) -> QueryStats:
+    """QueryStats (pipeline.hpp:36-54) exactly as the reference defines them
+    for one query -- the same set arithmetic as the oracle's eo_rerank_query:
+    needed = first n_needed final candidates; prefetched = the ids the
+    prefetcher fetched (the query's snapshot hints; none without prefetch);
+    hits = needed ∩ prefetched; missed = needed minus prefetched; byte and block
+    counters per record over prefetched / missed / needed docs.  The tier view
+    (rows resident in HBM vs staged over PCIe) is the separate device
+    accounting, Reranker.last_fetch_stats."""
+    ids = np.asarray(ids, np.uint32)
+    needed = ids[:n_needed]
+    pf = np.unique(np.asarray(prefetched_ids if prefetched_ids is not None else np.zeros(0), np.uint32))
+    st = QueryStats(query_id=query_id, needed_count=int(n_needed), rerank_time=elapsed, total_time=elapsed)
+    st.prefetched_count = int(np.asarray(prefetched_ids).size) if prefetched_ids is not None else 0
+    hit = np.isin(needed, pf) if pf.size else np.zeros(needed.size, bool)
+    st.missed_count = int(n_needed - hit.sum())
+    st.hit_rate = float(hit.sum()) / n_needed if n_needed else 0.0
+    tok_n = store.token_counts(needed)
+    if tok_n is not None:
+        rec, blk = record_io(store, tok_n)
+        st.needed_payload_bytes = int(rec.sum())
+        st.critical_fetch_bytes = int(rec[~hit].sum())
+        st.critical_blocks_read = int(blk[~hit].sum())
+    if prefetched_ids is not None and np.asarray(prefetched_ids).size:
+        tok_p = store.token_counts(np.asarray(prefetched_ids, np.uint32))
+        if tok_p is not None:
+            st.prefetch_bytes = int(record_io(store, tok_p)[0].sum())
     return st
 
 
@@ -800,7 +819,7 @@ def rerank_batch(queries: Sequence[QueryEmbedding], candidate_lists: Sequence[Ca
         res.rankings.append(RankedList([ScoredDoc(int(oid[b, i]), float(osc[b, i])) for i in range(n)]))
         a0, a1 = int(offs[b]), int(offs[b + 1])
         need = min(a1 - a0, int(config.rerank_count))
-        res.stats.append(_stats_for(store, ids[a0:a1], need, queries[b].query_id, wall, fstats[b]))
+        res.stats.append(_stats_for(store, ids[a0:a1], need, queries[b].query_id, wall))
         lat.append(wall)
     lat = np.asarray(lat)
     res.batch = BatchStats(n_queries=B, mean_latency=float(lat.mean()), p50_latency=float(np.percentile(lat, 50)),

@@ -106,6 +106,8 @@ struct StageParams {
   const uint64_t* hint_map;    // optional (consumer of espn_gpu_prefetch_hints): per local doc,
                                // epoch << 32 | staged offset / 16
   uint32_t hint_epoch;
+  uint8_t* cand_status;        // out, per needed candidate: 0 HBM-resident, 1 staged by the prefetcher,
+                               // 2 staged on the critical path, 3 not staged (overflow / unknown id)
 };
 
 // Hint staging (espn_gpu_prefetch_hints): CTA per query, warp per hinted doc.

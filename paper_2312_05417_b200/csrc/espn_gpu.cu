@@ -350,6 +350,7 @@ struct espn_gpu_workspace {
   struct Stage {
     uint8_t* buf = nullptr;
     uint64_t* cand_src = nullptr;
+    uint8_t* cand_status = nullptr;        // per needed candidate (StageParams::cand_status)
     unsigned long long* cursor = nullptr;
     unsigned long long* qstats = nullptr;  // B x 6
     uint64_t* off = nullptr;               // device copy of the batch offsets (prefetch, host offsets)
@@ -369,6 +370,7 @@ struct espn_gpu_workspace {
   int pf_q[2] = {-1, -1};  // FIFO of prefetched slots awaiting their PREFETCHED batch
   int pf_count = 0;
   int next_slot = 0;
+  int last_slot = -1;  // staging slot of the last re-ranked batch (espn_gpu_workspace_cand_status)
   unsigned long long* h_qstats = nullptr;  // pinned B x 6
   float* bow = nullptr;
   uint32_t* out_ids = nullptr;
@@ -574,6 +576,7 @@ int launch_stage(espn_gpu_table* t, espn_gpu_workspace* w, int slot, const uint6
   sp.err = w->err;
   sp.hint_map = hinted ? w->hint_map : nullptr;
   sp.hint_epoch = hinted ? st.hint_epoch : 0u;
+  sp.cand_status = st.cand_status;
   stage_kernel<<<B, kStageThreads, 0, s>>>(sp);
   ESPN_CUDA_TRY(cudaGetLastError());
   ESPN_CUDA_TRY(cudaEventRecord(st.done, s));
@@ -967,6 +970,7 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     for (auto& st : w->stage) {
       al((void**)&st.buf, w->staging_bytes);
       al((void**)&st.cand_src, C * sizeof(uint64_t));
+      al((void**)&st.cand_status, C);
       al((void**)&st.cursor, sizeof(unsigned long long));
       al((void**)&st.qstats, B * 6 * sizeof(unsigned long long));
       al((void**)&st.off, (B + 1) * sizeof(uint64_t));
@@ -1064,7 +1068,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   for (auto& st : w->stage) {
     if (st.done) cudaEventSynchronize(st.done);
     if (st.free_ev) cudaEventSynchronize(st.free_ev);
-    cudaFree(st.buf); cudaFree(st.cand_src); cudaFree(st.cursor); cudaFree(st.qstats); cudaFree(st.off);
+    cudaFree(st.buf); cudaFree(st.cand_src); cudaFree(st.cand_status); cudaFree(st.cursor); cudaFree(st.qstats); cudaFree(st.off);
     cudaFree(st.need); cudaFreeHost(st.off_h); cudaFreeHost(st.need_h);
     cudaFree(st.hint_ids); cudaFreeHost(st.hint_ids_h);
     st.hint_epoch = 0;
@@ -1468,6 +1472,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
 
   mp.cand_src = slot >= 0 ? w->stage[slot].cand_src : nullptr;
+  w->last_slot = slot;
   if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
   cudaError_t e = served ? (server_wait_kernel<<<1, 32, 0, s>>>(w->done_flag, w->err, kServerWaitNs), cudaGetLastError())
                   : tc   ? launch_tc_rt(t->d, qsplit, mp, t->num_sms, s, /*pdl=*/slot < 0 && !profile)
@@ -1739,6 +1744,22 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
   w->pf_q[w->pf_count++] = slot;
   w->async_pending = true;
   w->counters.kernel_launches += 1;
+  return ESPN_OK;
+}
+
+int espn_gpu_workspace_cand_status(espn_gpu_workspace* w, uint8_t* out, uint64_t n) {
+  if (!w || (n && !out)) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (n > w->max_candidates) return fail(ESPN_E_INVALID_INPUT, "n exceeds the workspace's candidates");
+  if (!w->table->tiered || w->last_slot < 0) {  // every row was in HBM
+    std::memset(out, 0, n);
+    return ESPN_OK;
+  }
+  DeviceGuard g(w->table->device);
+  cudaStream_t cs = nullptr;
+  ESPN_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  ESPN_CUDA_TRY(cudaMemcpyAsync(out, w->stage[w->last_slot].cand_status, n, cudaMemcpyDeviceToHost, cs));
+  ESPN_CUDA_TRY(cudaStreamSynchronize(cs));
+  cudaStreamDestroy(cs);
   return ESPN_OK;
 }
 

@@ -9,6 +9,9 @@
 #include <cstring>
 #include <fstream>
 #include <sstream>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
 
 namespace espn::gpu {
 namespace {
@@ -72,9 +75,64 @@ void throw_status(int status, const std::string& msg) {
 }
 
 // ---------------------------------------------------------------- Store
+struct Store::WorkspaceCache {
+  std::mutex mu;
+  std::unordered_map<std::thread::id, std::unique_ptr<Reranker>> by_thread;
+};
+
+Reranker& Store::thread_reranker(std::uint32_t max_queries, std::uint32_t max_candidates,
+                                 std::uint32_t max_query_tokens) const {
+  std::lock_guard<std::mutex> lk(cache_->mu);
+  auto& slot = cache_->by_thread[std::this_thread::get_id()];
+  if (!slot || slot->max_queries() < max_queries || slot->max_candidates() < max_candidates ||
+      slot->max_query_tokens() < max_query_tokens) {
+    // grow geometrically so a slowly growing workload does not reallocate every call
+    std::uint32_t q = max_queries, c = max_candidates, t = max_query_tokens;
+    if (slot) {
+      q = std::max(q, slot->max_queries());
+      c = std::max(c, slot->max_candidates());
+      t = std::max(t, slot->max_query_tokens());
+    }
+    slot.reset();
+    slot = std::make_unique<Reranker>(*this, q, c, std::min<std::uint32_t>(t, 32));
+  }
+  return *slot;
+}
+
+std::pair<std::uint64_t, std::uint64_t> Store::record_io(DocId id) const {
+  const std::uint64_t b = record_bytes(token_count(id));
+  return {b, (b + 4095) / 4096};
+}
+
+QueryStats query_stats(const Store& store, QueryId query_id, std::span<const DocId> candidates, std::uint64_t n_needed,
+                       std::span<const DocId> prefetched) {
+  QueryStats st;
+  st.query_id = query_id;
+  st.needed_count = n_needed;
+  st.prefetched_count = prefetched.size();
+  std::unordered_set<DocId> pf(prefetched.begin(), prefetched.end());
+  for (DocId id : prefetched) st.prefetch_bytes += store.record_io(id).first;
+  std::uint64_t hits = 0;
+  for (std::uint64_t j = 0; j < n_needed; ++j) {
+    const DocId id = candidates[j];
+    const auto [bytes, blocks] = store.record_io(id);
+    st.needed_payload_bytes += bytes;
+    if (pf.count(id)) {
+      ++hits;
+    } else {
+      st.critical_fetch_bytes += bytes;
+      st.critical_blocks_read += blocks;
+    }
+  }
+  st.missed_count = n_needed - hits;
+  st.hit_rate = n_needed ? static_cast<double>(hits) / static_cast<double>(n_needed) : 0.0;
+  return st;
+}
+
 Store::Store(std::span<const std::uint64_t> row_ptr, std::span<const std::uint16_t> rows, std::uint32_t d,
              Dtype dtype, RecordLayout layout, int device, std::span<const std::uint8_t> resident)
-    : d_(d), dtype_(dtype), layout_(layout), device_(device), row_ptr_(row_ptr.begin(), row_ptr.end()) {
+    : cache_(std::make_unique<WorkspaceCache>()), d_(d), dtype_(dtype), layout_(layout), device_(device),
+      row_ptr_(row_ptr.begin(), row_ptr.end()) {
   if (row_ptr.size() < 2) throw InvalidInputError("empty table");
   espn_table_desc desc{};
   desc.n_docs = row_ptr.size() - 1;
@@ -146,13 +204,18 @@ void build_store(const std::string& base, std::span<const std::uint64_t> row_ptr
 }
 
 Store::~Store() {
+  cache_.reset();  // workspaces first: they belong to the table
   if (table_) espn_gpu_table_close(table_);
 }
 Store::Store(Store&& o) noexcept
-    : table_(std::exchange(o.table_, nullptr)), d_(o.d_), dtype_(o.dtype_), layout_(o.layout_), device_(o.device_),
-      row_ptr_(std::move(o.row_ptr_)) {}
+    : cache_(std::make_unique<WorkspaceCache>()), table_(std::exchange(o.table_, nullptr)), d_(o.d_),
+      dtype_(o.dtype_), layout_(o.layout_), device_(o.device_), row_ptr_(std::move(o.row_ptr_)) {
+  o.cache_.reset();  // its workspaces point at the moved-from object
+}
 Store& Store::operator=(Store&& o) noexcept {
   if (this != &o) {
+    cache_ = std::make_unique<WorkspaceCache>();
+    o.cache_.reset();
     if (table_) espn_gpu_table_close(table_);
     table_ = std::exchange(o.table_, nullptr);
     d_ = o.d_;
@@ -218,6 +281,9 @@ Reranker::Reranker(const Store& store, std::uint32_t max_queries, std::uint32_t 
   desc.max_queries = std::max(max_queries, 1u);
   desc.max_candidates = std::max(max_candidates, 1u);
   desc.max_query_tokens = max_query_tokens;
+  max_queries_ = desc.max_queries;
+  max_candidates_ = desc.max_candidates;
+  max_nq_ = max_query_tokens;
   check(espn_gpu_workspace_create(store.handle(), &desc, &ws_));
 }
 
@@ -243,6 +309,8 @@ void Reranker::prefetch_hints(std::span<const CandidateList> snapshots, std::uin
   for (std::uint32_t b = 0; b < B; ++b)
     for (std::uint64_t j = 0; j < off[b + 1] - off[b]; ++j) ids[off[b] + j] = snapshots[b].entries[j].doc_id;
   check(espn_gpu_prefetch_hints(store_->handle(), ws_, B, ids.data(), off.data(), 0u, side_stream));
+  hint_ids_ = std::move(ids);  // the prefetched ids of the next prefetched rerank (QueryStats)
+  hint_off_ = std::move(off);
 }
 
 BatchResult Reranker::rerank(std::span<const QueryEmbedding> queries, std::span<const CandidateList> candidates,
@@ -302,29 +370,25 @@ BatchResult Reranker::rerank(std::span<const QueryEmbedding> queries, std::span<
     rl.entries.resize(out_n[b]);
     for (std::uint32_t i = 0; i < out_n[b]; ++i)
       rl.entries[i] = ScoredDoc{out_ids[static_cast<std::size_t>(b) * k + i], out_sc[static_cast<std::size_t>(b) * k + i]};
-    // QueryStats (pipeline.hpp:36-54) from the device's fetch accounting: rows
-    // in HBM when scoring starts (resident, or staged by the prefetch) are
-    // hits; host-tier rows copied on the critical path are misses.  An
-    // all-HBM store has hit rate 1.
-    auto& st = res.stats[b];
-    st.query_id = queries[b].query_id;
+    // QueryStats (pipeline.hpp:36-54) as the reference defines them: the
+    // prefetched ids are the query's snapshot hints (prefetched batches only)
     const std::uint64_t n = off[b + 1] - off[b];
-    st.needed_count = std::min<std::uint64_t>(n, config.rerank_count);
-    st.missed_count = fs[b].missed;
-    st.prefetched_count = st.needed_count - st.missed_count;
-    st.hit_rate = st.needed_count ? static_cast<double>(st.prefetched_count) / st.needed_count : 0.0;
-    st.prefetch_bytes = fs[b].prefetch_bytes;
-    st.critical_fetch_bytes = fs[b].critical_bytes;
-    for (std::uint64_t j = 0; j < st.needed_count; ++j)
-      st.needed_payload_bytes += store_->record_bytes(store_->token_count(ids[off[b] + j]));
+    std::span<const DocId> pf;
+    if (prefetched && b + 1 < hint_off_.size())
+      pf = std::span<const DocId>(hint_ids_.data() + hint_off_[b], hint_off_[b + 1] - hint_off_[b]);
+    auto& st = res.stats[b];
+    st = query_stats(*store_, queries[b].query_id, std::span<const DocId>(ids.data() + off[b], n),
+                     std::min<std::uint64_t>(n, config.rerank_count), pf);
     st.rerank_time = wall;
     st.total_time = wall;
   }
+  last_fs_ = std::move(fs);
   res.batch.n_queries = B;
   res.batch.mean_latency = wall;
   res.batch.p50_latency = percentile(lat, 50);
   res.batch.p99_latency = percentile(lat, 99);
   res.batch.wall_time = wall;
+  for (const auto& st : res.stats) res.batch.total_critical_fetch_bytes += st.critical_fetch_bytes;
   return res;
 }
 
@@ -335,8 +399,9 @@ BatchResult rerank_batch(std::span<const QueryEmbedding> queries, std::span<cons
   std::uint32_t nq = 1;
   for (const auto& cl : candidates) c += cl.entries.size();
   if (!queries.empty()) nq = std::max<std::uint32_t>(queries[0].rows, 1);
-  Reranker rr(store, static_cast<std::uint32_t>(queries.size()), static_cast<std::uint32_t>(std::max<std::uint64_t>(c, 1)),
-              std::min<std::uint32_t>(nq, 32));
+  Reranker& rr = store.thread_reranker(static_cast<std::uint32_t>(queries.size()),
+                                       static_cast<std::uint32_t>(std::max<std::uint64_t>(c, 1)),
+                                       std::min<std::uint32_t>(nq, 32));
   return rr.rerank(queries, candidates, config);
 }
 

@@ -684,19 +684,22 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageParams 
   for (uint64_t j = wid; j < need; j += nw) {
     const uint64_t loc = shard_local(s.cand_ids[c0 + j], s.shard_count, s.shard_index, s.n_docs);
     if (loc == ~0ull) {  // reported as DATA_INTEGRITY by the MaxSim kernel
-      if (lane == 0) s.cand_src[c0 + j] = 0;
+      if (lane == 0) { s.cand_src[c0 + j] = 0; if (s.cand_status) s.cand_status[c0 + j] = 3; }
       continue;
     }
     const uint64_t a = s.doc_loc[loc];
     if (!(a & 1ull)) {
-      if (lane == 0) s.cand_src[c0 + j] = a;
+      if (lane == 0) { s.cand_src[c0 + j] = a; if (s.cand_status) s.cand_status[c0 + j] = 0; }
       ++resident;
       continue;
     }
     if (s.hint_map) {  // staged ahead by espn_gpu_prefetch_hints?
       const uint64_t e = s.hint_map[loc];
       if ((uint32_t)(e >> 32) == s.hint_epoch && (uint32_t)e != 0xffffffffu) {
-        if (lane == 0) s.cand_src[c0 + j] = reinterpret_cast<uint64_t>(s.stage) + ((e & 0xffffffffull) << 4);
+        if (lane == 0) {
+          s.cand_src[c0 + j] = reinterpret_cast<uint64_t>(s.stage) + ((e & 0xffffffffull) << 4);
+          if (s.cand_status) s.cand_status[c0 + j] = 1;
+        }
         ++hits;
         continue;
       }
@@ -706,7 +709,11 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageParams 
     if (lane == 0) off = atomicAdd(s.cursor, (unsigned long long)bytes);
     off = __shfl_sync(0xffffffffu, off, 0);
     if (off + bytes > s.stage_cap) {
-      if (lane == 0) { atomicOr(s.err, ERR_STAGING); s.cand_src[c0 + j] = 0; }
+      if (lane == 0) {
+        atomicOr(s.err, ERR_STAGING);
+        s.cand_src[c0 + j] = 0;
+        if (s.cand_status) s.cand_status[c0 + j] = 3;
+      }
       continue;
     }
     const uint4* src = reinterpret_cast<const uint4*>(a & ~1ull);
@@ -718,7 +725,10 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageParams 
       dst[v] = x0; dst[v + 32] = x1; dst[v + 64] = x2; dst[v + 96] = x3;
     }
     for (; v < n16; v += 32) dst[v] = src[v];
-    if (lane == 0) s.cand_src[c0 + j] = reinterpret_cast<uint64_t>(s.stage + off);
+    if (lane == 0) {
+      s.cand_src[c0 + j] = reinterpret_cast<uint64_t>(s.stage + off);
+      if (s.cand_status) s.cand_status[c0 + j] = s.prefetch ? 1 : 2;
+    }
     ++staged;
     bytes_moved += bytes;
   }

@@ -264,7 +264,8 @@ def run_batch_queries(queries: Sequence[api.QueryEmbedding], index: IvfIndex, st
         n = int(r.counts[b])
         res.rankings.append(api.RankedList([api.ScoredDoc(int(i), float(s))
                                             for i, s in zip(r.ids[b, :n], r.scores[b, :n])]))
-        st = api._stats_for(store, r.finals[b][0], int(r.needed[b]), qe.query_id, r.rerank_s, r.fetch[b])
+        st = api._stats_for(store, r.finals[b][0], int(r.needed[b]), qe.query_id, r.rerank_s,
+                            r.hints[b] if r.hints is not None else None)
         st.ann_time = r.ann_s
         st.total_time = r.ann_s + r.rerank_s
         res.stats.append(st)

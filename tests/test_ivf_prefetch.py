@@ -344,12 +344,32 @@ def test_reference_named_pipeline_entry_points(cuda_ok):
     on = pipeline.run_batch_queries(queries, ix, store, api.PipelineConfig(prefetch_step_pct=30.0, **base))
     off = pipeline.run_batch_queries(queries, ix, store, api.PipelineConfig(prefetch_enabled=False, **base))
     assert on.rankings == off.rankings
+    # QueryStats field for field with the oracle's eo_rerank_query on the same
+    # final candidates, prefetched = the same snapshot (pipeline.hpp:45-53);
+    # the cursors are deterministic, so the snapshot / final lists are rebuilt here
+    import oracle_py
+    from paper_2312_05417_b200 import synth
+    rp, codes = synth.make_table(20000, 32, 1, 63, seed=21)
+    ot = oracle_py.OracleTable(rp, codes, 32)
+    cfg_on = api.PipelineConfig(prefetch_step_pct=30.0, **base)
     for b, qe in enumerate(queries):
-        rl, st = pipeline.run_query(qe, ix, store, api.PipelineConfig(prefetch_step_pct=30.0, **base))
+        rl, st = pipeline.run_query(qe, ix, store, cfg_on)
         assert rl == on.rankings[b]
-        assert st.query_id == qe.query_id and st.needed_count == 200
-        assert st.prefetched_count + st.missed_count <= st.needed_count
-        assert 0.0 <= st.hit_rate <= 1.0
+        cur = ivf.SearchCursor(ix, qc[b], cfg_on.nprobe, cfg_on.effective_candidate_k())
+        cur.advance(cfg_on.delta())
+        snap = cur.snapshot_arrays(cfg_on.effective_prefetch_top_k())[0]
+        cur.advance(cfg_on.nprobe - cfg_on.delta())
+        fid, fcls = cur.finish_arrays(cfg_on.effective_candidate_k())
+        for got in (st, on.stats[b]):
+            ost_ = oracle_py.rerank_query(ot, q[b], fid, fcls, 200, 10, 1.0, True, True, snap)
+            assert ost_[0] == 0
+            o = ost_[3]
+            assert got.query_id == qe.query_id
+            for f in ("prefetched_count", "needed_count", "missed_count", "hit_rate", "prefetch_bytes",
+                      "critical_fetch_bytes", "critical_blocks_read", "needed_payload_bytes"):
+                assert getattr(got, f) == getattr(o, f), (b, f, getattr(got, f), getattr(o, f))
+        st_off = off.stats[b]  # no prefetch: every needed doc is fetched on the critical path
+        assert st_off.prefetched_count == 0 and st_off.missed_count == st_off.needed_count == 200
     pts = pipeline.measure_hit_rate_queries(queries, ix, store, api.PipelineConfig(**base), [5, 100])
     assert pts[-1].mean_hit_rate == 1.0 and pts[0].mean_hit_rate <= 1.0
     store.close()
