@@ -207,3 +207,28 @@ def store_lib() -> C.CDLL:
 
 def store_last_error() -> str:
     return (store_lib().espn_store_last_error() or b"").decode("utf-8", "replace")
+
+
+# ---- include/espn_host.h: the C++ host layer (libespn_host.so) ------------------------
+HOST_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libespn_host.so"
+HOST_SIGNATURES = {
+    "espn_host_run_batches": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+                                        C.c_void_p, C.c_uint32, C.POINTER(C.c_double)]),
+}
+_host_lib = None
+
+
+def host_lib() -> C.CDLL:
+    """Load libespn_host.so (once; it links libespn_gpu.so).  Raises if missing."""
+    global _host_lib
+    if _host_lib is None:
+        lib()  # the GPU library first (same copy the host layer links, via rpath $ORIGIN)
+        if not HOST_LIB_PATH.exists():
+            raise RuntimeError(f"{HOST_LIB_PATH} not found: build it with `python -m paper_2312_05417_b200.build`")
+        h = C.CDLL(str(HOST_LIB_PATH))
+        for name, (res, args) in HOST_SIGNATURES.items():
+            f = getattr(h, name)
+            f.restype = res
+            f.argtypes = args
+        _host_lib = h
+    return _host_lib

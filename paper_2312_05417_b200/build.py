@@ -64,6 +64,8 @@ def build_lib(verbose: bool = False, force: bool = False) -> Path:
 
 
 HOST_LIB = LIB_DIR / "libespn_host.so"
+CUDA_INC = "/usr/local/cuda/include"
+CUDA_LIB = "/usr/local/cuda/lib64"
 HOST_SRC = CSRC / "host" / "espn_b200.cpp"
 CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-fvisibility=default"]
@@ -73,11 +75,13 @@ def build_host(force: bool = False) -> Path:
     """libespn_host.so: the C++ espn::gpu API (include/espn_b200.hpp) over the
     C-ABI, linked against libespn_gpu.so (rpath $ORIGIN)."""
     build_store_lib()
-    deps = [HOST_SRC, ROOT / "include" / "espn_b200.hpp", ROOT / "include" / "espn_gpu.h", LIB, STORE_LIB]
+    deps = [HOST_SRC, ROOT / "include" / "espn_b200.hpp", ROOT / "include" / "espn_gpu.h",
+            ROOT / "include" / "espn_host.h", LIB, STORE_LIB]
     if not force and HOST_LIB.exists() and all(p.stat().st_mtime <= HOST_LIB.stat().st_mtime for p in deps):
         return HOST_LIB
-    cmd = [CXX, *CXX_FLAGS, "-shared", "-I", str(ROOT / "include"), "-o", str(HOST_LIB), str(HOST_SRC),
-           "-L", str(LIB_DIR), "-lespn_gpu", "-lespn_store", "-Wl,-rpath,$ORIGIN"]
+    cmd = [CXX, *CXX_FLAGS, "-shared", "-I", str(ROOT / "include"), "-I", CUDA_INC, "-o", str(HOST_LIB),
+           str(HOST_SRC), "-L", str(LIB_DIR), "-lespn_gpu", "-lespn_store", "-L", CUDA_LIB, "-lcudart",
+           "-Wl,-rpath,$ORIGIN"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -112,7 +116,7 @@ def check_reference_headers() -> bool:
     if not inc.exists():
         return False
     cmd = [CXX, *CXX_FLAGS, "-fsyntax-only", "-DESPN_B200_WITH_REFERENCE_HEADERS", "-I", str(ROOT / "include"),
-           "-I", str(inc), str(HOST_SRC)]
+           "-I", CUDA_INC, "-I", str(inc), str(HOST_SRC)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -413,14 +413,37 @@ struct espn_gpu_workspace {
   uint64_t sg_seen[5] = {0, 0, 0, 0, 0};  // last shape run eagerly (captured on its second call)
   bool capturing = false;            // a capture left open by an error return
   // host input pointers last checked for pinned memory (q32, ids, cls)
-  const void* in_key[3] = {nullptr, nullptr, nullptr};
-  bool in_pinned[3] = {false, false, false};
+  bool in_pinned[3] = {false, false, false};  // this call's q32 / ids / cls
   uint8_t* out_h = nullptr;  // pinned bounce of pageable host outputs (synchronous calls)
   uint64_t io_calls = 0;
   // zero-copy outputs: last output pointers checked for pinned host memory
-  const void* zc_key[3] = {nullptr, nullptr, nullptr};
   void* zc_dev[3] = {nullptr, nullptr, nullptr};
-  bool zc_ok = false;
+  // Host pointers seen by this workspace -> pinned? (and the device alias of
+  // mapped pinned memory): callers rotate a few buffer sets, so a small cache
+  // keeps cudaPointerGetAttributes off the per-call path.
+  struct PtrCache {
+    static constexpr int N = 64;
+    const void* key[N] = {};
+    void* dev[N] = {};
+    bool pinned[N] = {};
+    int next = 0;
+    bool lookup(const void* p, void** devptr) {
+      for (int i = 0; i < N; ++i)
+        if (key[i] == p && p) {
+          *devptr = dev[i];
+          return pinned[i];
+        }
+      cudaPointerAttributes at{};
+      const bool pin = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+      cudaGetLastError();  // clear a sticky "invalid value" for unregistered memory
+      key[next] = p;
+      pinned[next] = pin;
+      dev[next] = pin ? at.devicePointer : nullptr;
+      next = (next + 1) % N;
+      *devptr = pin ? at.devicePointer : nullptr;
+      return pin;
+    }
+  } ptrs;
   uint32_t* h_err = nullptr;
   bool async_pending = false;  // device err word carries bits of un-synced ASYNC calls
   // PROFILE: event triples around MaxSim / top-k, drained lazily
@@ -1200,22 +1223,9 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     out_counts_k = o->counts;
   } else {
     const void* key[3] = {o->ids, o->scores, o->counts};
-    if (!(key[0] == w->zc_key[0] && key[1] == w->zc_key[1] && key[2] == w->zc_key[2])) {
-      bool ok = true;
-      for (int i = 0; i < 3; ++i) {
-        cudaPointerAttributes at{};
-        if (cudaPointerGetAttributes(&at, key[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
-            !at.devicePointer) {
-          ok = false;
-          cudaGetLastError();  // clear a sticky "invalid value" for unregistered memory
-          break;
-        }
-        w->zc_dev[i] = at.devicePointer;
-      }
-      for (int i = 0; i < 3; ++i) w->zc_key[i] = key[i];
-      w->zc_ok = ok;
-    }
-    if (w->zc_ok) {
+    bool zc_ok = true;
+    for (int i = 0; i < 3; ++i) zc_ok = w->ptrs.lookup(key[i], &w->zc_dev[i]) && w->zc_dev[i] && zc_ok;
+    if (zc_ok) {
       out_ids_k = static_cast<uint32_t*>(w->zc_dev[0]);
       out_scores_k = static_cast<float*>(w->zc_dev[1]);
       out_counts_k = static_cast<uint32_t*>(w->zc_dev[2]);
@@ -1239,13 +1249,8 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   int io_slot = -1;
   if (!dev_io) {  // which caller buffers are pinned (cached per pointer)
     const void* key[3] = {q32, ids, cls};
-    for (int i = 0; i < 3; ++i)
-      if (key[i] != w->in_key[i]) {
-        cudaPointerAttributes at{};
-        w->in_pinned[i] = cudaPointerGetAttributes(&at, key[i]) == cudaSuccess && at.type == cudaMemoryTypeHost;
-        cudaGetLastError();
-        w->in_key[i] = key[i];
-      }
+    void* dummy = nullptr;
+    for (int i = 0; i < 3; ++i) w->in_pinned[i] = w->ptrs.lookup(key[i], &dummy);
   }
   const bool all_pinned = !dev_io && w->in_pinned[0] && (C == 0 || (w->in_pinned[1] && w->in_pinned[2]));
   const bool packed = sync_call && !dev_io && !dev_off && !all_pinned;

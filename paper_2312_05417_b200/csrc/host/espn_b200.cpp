@@ -472,3 +472,56 @@ Qrels load_qrels(const std::filesystem::path& path) {
 }
 
 }  // namespace espn::gpu
+
+// ---------------------------------------------------------------- serving loop (include/espn_host.h)
+#include <cuda_runtime_api.h>
+#include <deque>
+
+#include "espn_host.h"
+
+extern "C" int espn_host_run_batches(espn_gpu_table* table, espn_gpu_workspace* const* ws, void* const* streams,
+                                     uint32_t lanes, uint32_t depth, const espn_rerank_args* batches,
+                                     espn_rerank_out* outs, uint32_t n, double* seconds) {
+  if (!table || !ws || !streams || !batches || !outs || lanes == 0) return ESPN_E_INVALID_INPUT;
+  depth = std::max(depth, 1u);
+  std::vector<std::deque<cudaEvent_t>> inflight(lanes);
+  std::vector<cudaEvent_t> pool;
+  auto get_event = [&]() -> cudaEvent_t {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+  };
+  int status = ESPN_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint32_t i = 0; i < n && status == ESPN_OK; ++i) {
+    const uint32_t l = i % lanes;
+    auto& q = inflight[l];
+    if (q.size() >= depth) {  // the lane's oldest batch must finish before its buffers are reused
+      cudaEventSynchronize(q.front());
+      pool.push_back(q.front());
+      q.pop_front();
+    }
+    espn_rerank_args a = batches[i];
+    a.flags |= ESPN_RERANK_ASYNC;
+    status = espn_gpu_rerank(table, ws[l], &a, &outs[i], streams[l]);
+    if (status == ESPN_OK) {
+      cudaEvent_t e = get_event();
+      cudaEventRecord(e, static_cast<cudaStream_t>(streams[l]));
+      q.push_back(e);
+    }
+  }
+  for (uint32_t l = 0; l < lanes; ++l) {
+    const int st = espn_gpu_workspace_sync(ws[l], streams[l]);  // completes the lane, reports device errors
+    if (status == ESPN_OK) status = st;
+  }
+  if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  for (auto& q : inflight)
+    for (cudaEvent_t e : q) cudaEventDestroy(e);
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  return status;
+}
