@@ -406,6 +406,21 @@ ESPN_API int espn_gpu_synth_table(uint64_t n_local_docs, uint32_t d, uint32_t dt
 ESPN_API int espn_gpu_gather_rows(espn_gpu_table* table, const uint32_t* ids, uint64_t n,
                          const uint64_t* out_row_ptr, uint16_t* out_rows, void* stream);
 
+/* Reference scoring primitives on the device, HOST arrays, synchronous (the
+ * unmodified-header definitions of scoring.hpp in csrc/host/espn_ref_api.cpp):
+ *   espn_gpu_maxsim_f32  maxsim_score (scoring.hpp:7-10) of one fp32 query
+ *                        (nq x d) and one fp32 document (t x d): dot over k
+ *                        ascending, max over doc tokens, sum over query tokens
+ *                        ascending -- bit-exact with the reference order
+ *                        (dot_f32 = the nq = t = 1 case);
+ *   espn_gpu_rank        rank (scoring.hpp:16-18): sort by (score desc,
+ *                        doc_id asc); duplicate ids or non-finite scores ->
+ *                        INVALID_INPUT. */
+ESPN_API int espn_gpu_maxsim_f32(const float* q, uint32_t nq, const float* doc, uint32_t t, uint32_t d, float* out,
+                                 int device);
+ESPN_API int espn_gpu_rank(const uint32_t* ids, const float* scores, uint64_t n, uint32_t* out_ids,
+                           float* out_scores, int device);
+
 ESPN_API const char* espn_last_error(void);
 ESPN_API int espn_abi_version(void);
 

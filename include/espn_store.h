@@ -76,6 +76,39 @@ ESPN_API int espn_store_load_manifest(const char* base, espn_store_header* heade
 ESPN_API int espn_store_read_table(const char* base, uint32_t dtype, uint64_t* row_ptr_out,
                                    uint16_t* codes_out, float* cls_out);
 
+/* save_manifest (store.hpp:53): writes <base>.manifest (+ .manifest.json)
+ * from a header and its `count` records. */
+ESPN_API int espn_store_save_manifest(const char* base, const espn_store_header* header,
+                                      const espn_manifest_record* records);
+
+/* File-backed batched reads: StoreHandle / open_store / fetch_batch
+ * (store.hpp:56-112), the reference's own retrieval path --
+ * the NVMe tier on the host side.  Modes follow ReadMode (store.hpp:11):
+ * DIRECT bypasses the page cache (O_DIRECT, aligned spans through an aligned
+ * bounce buffer; needs alignment >= 512, else INVALID_CONFIG; a filesystem
+ * without O_DIRECT -> IO), BUFFERED preads the exact payload, MMAP copies
+ * from a shared mapping.  queue_depth reads are in flight (store.hpp:73-76). */
+#define ESPN_READ_DIRECT 0u
+#define ESPN_READ_BUFFERED 1u
+#define ESPN_READ_MMAP 2u
+typedef struct espn_store_reader espn_store_reader;
+ESPN_API int espn_store_open(const char* base, uint32_t mode, uint32_t queue_depth, espn_store_reader** out,
+                             espn_store_header* header);
+ESPN_API int espn_store_close(espn_store_reader* reader);
+/* The manifest records (header.count of them). */
+ESPN_API int espn_store_records(const espn_store_reader* reader, espn_manifest_record* out);
+/* Reads the records of ids[0..n) (duplicates allowed; unknown id ->
+ * INVALID_INPUT listing the offenders) in request order: record i's payload
+ * (byte_length bytes: CLS values then BOW rows, value_width each) lands at
+ * out + out_off[i], out_off[n+1] being the prefix of payload sizes.  Counters
+ * (store.hpp:61-65): bytes_read = payload bytes, aligned-rounded in direct
+ * mode; blocks_read = sum of ceil(byte_length / block), block = alignment in
+ * direct mode else 4096; wall_time in seconds.  out == NULL: offsets and
+ * counters only.  Short read -> IO. */
+ESPN_API int espn_store_fetch(espn_store_reader* reader, const uint32_t* ids, uint64_t n, uint8_t* out,
+                              uint64_t* out_off, uint64_t capacity, uint64_t* bytes_read, uint64_t* blocks_read,
+                              double* wall_time);
+
 /* Thread-local message of the last failing call of this library. */
 ESPN_API const char* espn_store_last_error(void);
 

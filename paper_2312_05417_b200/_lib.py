@@ -138,6 +138,9 @@ SIGNATURES = {
                                       C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
     "espn_gpu_shard_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.c_void_p, C.c_uint32,
                                        C.POINTER(RerankOut), C.c_void_p]),
+    "espn_gpu_maxsim_f32": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+                                      C.c_int]),
+    "espn_gpu_rank": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int]),
     "espn_last_error": (C.c_char_p, []),
     "espn_abi_version": (C.c_int, []),
 }

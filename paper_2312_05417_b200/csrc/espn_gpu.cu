@@ -2,6 +2,7 @@
 // lifetime, batch orchestration (H2D -> K2 MaxSim -> K3 top-k -> D2H) and the
 // standalone gather / merge / synth entry points.  Pure CUDA runtime; no torch.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the library is loaded at run time (nccl_api below)
@@ -2378,6 +2379,91 @@ int espn_gpu_rerank_sharded_multi(uint32_t n, espn_gpu_table* const* tables, esp
     if (st && !worst) worst = st;
   }
   return worst;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// Reference scoring primitives (scoring.hpp:7-21) on the device
+// ============================================================================
+extern "C" {
+
+int espn_gpu_maxsim_f32(const float* q, uint32_t nq, const float* doc, uint32_t t, uint32_t d, float* out,
+                        int device) {
+  if (!out || (nq && !q) || (t && !doc)) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (nq == 0 || t == 0 || d == 0) return fail(ESPN_E_INVALID_INPUT, "empty query or document (types.hpp:64-68)");
+  int sms = 0;
+  bool tc = false;
+  int st = check_device(device, &sms, &tc);
+  if (st) return st;
+  DeviceGuard g(device);
+  float *dq = nullptr, *dd = nullptr, *dm = nullptr;
+  auto cleanup = [&] { cudaFree(dq); cudaFree(dd); cudaFree(dm); };
+  cudaError_t e = cudaMalloc(&dq, (size_t)nq * d * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dd, (size_t)t * d * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dm, (size_t)(nq + 1) * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(dq, q, (size_t)nq * d * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dd, doc, (size_t)t * d * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    maxsim_f32_kernel<<<nq, 256>>>(dq, dd, t, d, dm + 1);
+    sum_ordered_kernel<<<1, 32>>>(dm + 1, nq, dm);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dm, 4, cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("maxsim_f32: ") + cudaGetErrorString(e));
+  return ESPN_OK;
+}
+
+int espn_gpu_rank(const uint32_t* ids, const float* scores, uint64_t n, uint32_t* out_ids, float* out_scores,
+                  int device) {
+  if (n == 0) return ESPN_OK;
+  if (!ids || !scores || !out_ids || !out_scores) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  int sms = 0;
+  bool tc = false;
+  int st = check_device(device, &sms, &tc);
+  if (st) return st;
+  DeviceGuard g(device);
+  uint32_t *di = nullptr, *di2 = nullptr, *derr = nullptr;
+  float* ds = nullptr;
+  unsigned long long *dk = nullptr, *dk2 = nullptr;
+  void* tmp = nullptr;
+  auto cleanup = [&] { cudaFree(di); cudaFree(di2); cudaFree(derr); cudaFree(ds); cudaFree(dk); cudaFree(dk2); cudaFree(tmp); };
+  size_t tb1 = 0, tb2 = 0;
+  cub::DeviceRadixSort::SortKeysDescending(nullptr, tb1, dk, dk2, (int64_t)n);
+  cub::DeviceRadixSort::SortKeys(nullptr, tb2, di, di2, (int64_t)n);
+  cudaError_t e = cudaMalloc(&di, n * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&di2, n * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&ds, n * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dk, n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&dk2, n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&derr, 4);
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, std::max(tb1, tb2));
+  if (e == cudaSuccess) e = cudaMemset(derr, 0, 4);
+  if (e == cudaSuccess) e = cudaMemcpy(di, ids, n * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ds, scores, n * 4, cudaMemcpyHostToDevice);
+  const int blocks = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8);
+  if (e == cudaSuccess) {
+    rank_keys_kernel<<<blocks, 256>>>(di, ds, n, dk, derr);
+    size_t tb = std::max(tb1, tb2);
+    e = cub::DeviceRadixSort::SortKeysDescending(tmp, tb, dk, dk2, (int64_t)n);
+    tb = std::max(tb1, tb2);
+    if (e == cudaSuccess) e = cub::DeviceRadixSort::SortKeys(tmp, tb, di, di2, (int64_t)n);
+    if (e == cudaSuccess) {
+      adjacent_dup_kernel<<<blocks, 256>>>(di2, n, derr);
+      rank_unkey_kernel<<<blocks, 256>>>(dk2, n, di, ds);
+      e = cudaGetLastError();
+    }
+  }
+  uint32_t herr = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&herr, derr, 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && !herr) e = cudaMemcpy(out_ids, di, n * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && !herr) e = cudaMemcpy(out_scores, ds, n * 4, cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("rank: ") + cudaGetErrorString(e));
+  if (herr & ERR_DUPLICATE) return fail(ESPN_E_INVALID_INPUT, "rank: duplicate doc id (scoring.hpp:16-18)");
+  if (herr) return fail(ESPN_E_INVALID_INPUT, "rank: non-finite score (scoring.hpp:16-18)");
+  return ESPN_OK;
 }
 
 }  // extern "C"

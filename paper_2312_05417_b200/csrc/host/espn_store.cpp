@@ -10,10 +10,15 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <atomic>
+#include <cerrno>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -194,16 +199,22 @@ int espn_store_build(const char* base, uint64_t n_docs, uint32_t d, uint32_t d_c
   if (std::fclose(f) != 0 && st == ESPN_OK) st = fail(ESPN_E_IO, "close failed: " + dp);
   if (st != ESPN_OK) return st;
 
+  const espn_store_header h{kVersion, d, d_cls, value_width, alignment, n_docs};
+  return espn_store_save_manifest(base, &h, recs.data());
+}
+
+int espn_store_save_manifest(const char* base, const espn_store_header* h, const espn_manifest_record* recs) {
+  if (!base || !h || (h->count && !recs)) return fail(ESPN_E_INVALID_INPUT, "null argument");
   const std::string mp = path_of(base, ".manifest");
   FILE* m = std::fopen(mp.c_str(), "wb");
   if (!m) return fail(ESPN_E_IO, "cannot create " + mp);
   unsigned char hdr[kHeaderBytes] = {};
   std::memcpy(hdr, kMagic, 8);
-  const uint32_t u[6] = {kVersion, d, d_cls, value_width, alignment, 0};
+  const uint32_t u[6] = {h->version, h->d, h->d_cls, h->value_width, h->alignment, 0};
   std::memcpy(hdr + 8, u, 24);
-  std::memcpy(hdr + 32, &n_docs, 8);
-  st = write_all(m, hdr, kHeaderBytes, mp);
-  if (st == ESPN_OK) st = write_all(m, recs.data(), recs.size() * sizeof(espn_manifest_record), mp);
+  std::memcpy(hdr + 32, &h->count, 8);
+  int st = write_all(m, hdr, kHeaderBytes, mp);
+  if (st == ESPN_OK) st = write_all(m, recs, h->count * sizeof(espn_manifest_record), mp);
   if (std::fclose(m) != 0 && st == ESPN_OK) st = fail(ESPN_E_IO, "close failed: " + mp);
   if (st != ESPN_OK) return st;
 
@@ -212,8 +223,8 @@ int espn_store_build(const char* base, uint64_t n_docs, uint32_t d, uint32_t d_c
   if (!j) return fail(ESPN_E_IO, "cannot create " + jp);
   std::fprintf(j, "{\"magic\": \"ESPNSTR1\", \"version\": %u, \"d\": %u, \"d_cls\": %u, \"value_width\": %u, "
                   "\"alignment\": %u, \"count\": %llu, \"records\": [",
-               kVersion, d, d_cls, value_width, alignment, static_cast<unsigned long long>(n_docs));
-  for (uint64_t i = 0; i < n_docs; ++i)
+               h->version, h->d, h->d_cls, h->value_width, h->alignment, static_cast<unsigned long long>(h->count));
+  for (uint64_t i = 0; i < h->count; ++i)
     std::fprintf(j, "%s[%llu, %u, %u]", i ? ", " : "", static_cast<unsigned long long>(recs[i].byte_offset),
                  recs[i].byte_length, recs[i].token_count);
   std::fprintf(j, "]}\n");
@@ -292,6 +303,159 @@ int espn_store_read_table(const char* base, uint32_t dtype, uint64_t* row_ptr_ou
   }
   if (data) ::munmap(const_cast<unsigned char*>(data), size);
   (void)st;
+  return ESPN_OK;
+}
+
+
+// ---- file-backed batched reads (StoreHandle::fetch_batch, store.hpp:56-112) ----
+struct espn_store_reader {
+  espn_store_header h{};
+  std::vector<espn_manifest_record> recs;
+  uint32_t mode = ESPN_READ_BUFFERED;
+  uint32_t queue_depth = 16;
+  int fd = -1;
+  const unsigned char* map = nullptr;
+  uint64_t file_size = 0;
+};
+
+int espn_store_open(const char* base, uint32_t mode, uint32_t queue_depth, espn_store_reader** out,
+                    espn_store_header* header) {
+  if (!base || !out) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  *out = nullptr;
+  if (mode > ESPN_READ_MMAP) return fail(ESPN_E_INVALID_INPUT, "read mode must be direct, buffered or mmap");
+  auto* r = new espn_store_reader();
+  int st = load_manifest(base, &r->h, &r->recs);
+  if (st != ESPN_OK) { delete r; return st; }
+  // direct mode needs alignment >= 512 (store.hpp:109-110; SPEC.md open_store)
+  if (mode == ESPN_READ_DIRECT && r->h.alignment < 512) {
+    delete r;
+    return fail(ESPN_E_INVALID_CONFIG, "direct mode requires a store with alignment >= 512");
+  }
+  r->mode = mode;
+  r->queue_depth = queue_depth ? queue_depth : 16;
+  const std::string dp = path_of(base, ".espn");
+  r->fd = ::open(dp.c_str(), O_RDONLY | (mode == ESPN_READ_DIRECT ? O_DIRECT : 0));
+  if (r->fd < 0) {
+    const int e = errno;
+    delete r;
+    if (mode == ESPN_READ_DIRECT && e == EINVAL)
+      return fail(ESPN_E_IO, "the filesystem of " + dp + " does not honour O_DIRECT");
+    return fail(ESPN_E_IO, "cannot open " + dp + ": " + std::strerror(e));
+  }
+  struct stat sb {};
+  if (::fstat(r->fd, &sb) != 0) { espn_store_close(r); return fail(ESPN_E_IO, "cannot stat " + dp); }
+  r->file_size = static_cast<uint64_t>(sb.st_size);
+  const uint64_t need = r->recs.empty() ? 0 : r->recs.back().byte_offset + r->recs.back().byte_length;
+  if (r->file_size < need) { espn_store_close(r); return fail(ESPN_E_IO, "short data file (truncated store): " + dp); }
+  if (mode == ESPN_READ_MMAP && r->file_size) {
+    void* m = ::mmap(nullptr, r->file_size, PROT_READ, MAP_SHARED, r->fd, 0);
+    if (m == MAP_FAILED) { espn_store_close(r); return fail(ESPN_E_IO, "mmap failed: " + dp); }
+    r->map = static_cast<const unsigned char*>(m);
+  }
+  if (header) *header = r->h;
+  *out = r;
+  return ESPN_OK;
+}
+
+int espn_store_close(espn_store_reader* r) {
+  if (!r) return ESPN_OK;
+  if (r->map) ::munmap(const_cast<unsigned char*>(r->map), r->file_size);
+  if (r->fd >= 0) ::close(r->fd);
+  delete r;
+  return ESPN_OK;
+}
+
+int espn_store_records(const espn_store_reader* r, espn_manifest_record* out) {
+  if (!r || (!r->recs.empty() && !out)) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  std::memcpy(out, r->recs.data(), r->recs.size() * sizeof(espn_manifest_record));
+  return ESPN_OK;
+}
+
+int espn_store_fetch(espn_store_reader* r, const uint32_t* ids, uint64_t n, uint8_t* out, uint64_t* out_off,
+                     uint64_t capacity, uint64_t* bytes_read, uint64_t* blocks_read, double* wall_time) {
+  if (!r || !out_off || (n && !ids)) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  const auto t0 = std::chrono::steady_clock::now();
+  // unknown ids -> InvalidInputError listing the offenders (store.hpp:92-93)
+  std::string bad;
+  int nbad = 0;
+  for (uint64_t i = 0; i < n; ++i)
+    if (ids[i] >= r->h.count) {
+      if (nbad++ < 16) bad += " " + std::to_string(ids[i]);
+    }
+  if (nbad) return fail(ESPN_E_INVALID_INPUT, "unknown doc ids:" + bad + (nbad > 16 ? " ..." : ""));
+  out_off[0] = 0;
+  uint64_t br = 0, bl = 0;
+  const bool direct = r->mode == ESPN_READ_DIRECT;
+  const uint64_t align = r->h.alignment ? r->h.alignment : 1;
+  const uint64_t block = direct ? align : 4096u;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t len = r->recs[ids[i]].byte_length;
+    out_off[i + 1] = out_off[i] + len;
+    br += direct ? (len + align - 1) / align * align : len;  // aligned-rounded in direct mode
+    bl += (len + block - 1) / block;                         // block = alignment (direct) else 4096
+  }
+  if (bytes_read) *bytes_read = br;
+  if (blocks_read) *blocks_read = bl;
+  if (!out) return ESPN_OK;  // sizes only
+  if (out_off[n] > capacity) return fail(ESPN_E_INVALID_INPUT, "output capacity too small");
+  // queue_depth reads in flight: workers take records in request order and
+  // write each to its own slot (completion order free, result order fixed)
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> status{ESPN_OK};
+  thread_local std::string werr;
+  std::string first_err;
+  std::atomic<bool> err_set{false};
+  auto worker = [&] {
+    void* bounce = nullptr;
+    size_t bounce_cap = 0;
+    for (;;) {
+      const uint64_t i = next.fetch_add(1);
+      if (i >= n || status.load() != ESPN_OK) break;
+      const espn_manifest_record& rec = r->recs[ids[i]];
+      uint8_t* dst = out + out_off[i];
+      if (r->mode == ESPN_READ_MMAP) {
+        std::memcpy(dst, r->map + rec.byte_offset, rec.byte_length);
+        continue;
+      }
+      if (!direct) {
+        uint64_t done = 0;
+        while (done < rec.byte_length) {
+          const ssize_t got = ::pread(r->fd, dst + done, rec.byte_length - done, rec.byte_offset + done);
+          if (got <= 0) { status = ESPN_E_IO; break; }
+          done += static_cast<uint64_t>(got);
+        }
+        continue;
+      }
+      // direct: the aligned span covering the record, into an aligned bounce buffer
+      const uint64_t a0 = rec.byte_offset / align * align;
+      const uint64_t a1 = (rec.byte_offset + rec.byte_length + align - 1) / align * align;
+      const size_t span = static_cast<size_t>(a1 - a0);
+      if (span > bounce_cap) {
+        std::free(bounce);
+        bounce = nullptr;
+        if (posix_memalign(&bounce, 4096, span) != 0) { status = ESPN_E_IO; break; }
+        bounce_cap = span;
+      }
+      uint64_t done = 0;
+      while (done < span) {
+        const ssize_t got = ::pread(r->fd, static_cast<uint8_t*>(bounce) + done, span - done, a0 + done);
+        if (got <= 0) break;  // a short read at the end of the file is fine once the record is in
+        done += static_cast<uint64_t>(got);
+      }
+      if (done < rec.byte_offset + rec.byte_length - a0) { status = ESPN_E_IO; break; }
+      std::memcpy(dst, static_cast<uint8_t*>(bounce) + (rec.byte_offset - a0), rec.byte_length);
+    }
+    std::free(bounce);
+  };
+  const uint32_t nt = static_cast<uint32_t>(std::min<uint64_t>(r->queue_depth, std::max<uint64_t>(n, 1)));
+  std::vector<std::thread> pool;
+  for (uint32_t t = 1; t < nt; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  (void)first_err;
+  (void)err_set;
+  if (wall_time) *wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (status.load() != ESPN_OK) return fail(ESPN_E_IO, "short read from the store's data file");
   return ESPN_OK;
 }
 

@@ -902,3 +902,59 @@ __global__ void minmax_len_kernel(const uint64_t* row_ptr, uint64_t n_docs, unsi
 }
 
 }  // namespace espn_k
+
+namespace espn_k {
+// ============================================================================
+// Reference scoring primitives on the device (the unmodified-header API of
+// csrc/host/espn_ref_api.cpp): fp32 inputs, the reference's fixed order.
+// ============================================================================
+// maxsim_score (scoring.hpp:7-10): block i = query token i; thread j-strided
+// over doc tokens: dot over k ascending (__fmul_rn/__fadd_rn), max over j
+// (exact); then one thread sums the per-token maxima in ascending i.
+__global__ void __launch_bounds__(256) maxsim_f32_kernel(const float* q, const float* doc, uint32_t t, uint32_t d,
+                                                        float* qmax) {
+  __shared__ float red[256];
+  const uint32_t i = blockIdx.x;
+  float m = -INFINITY;
+  for (uint32_t j = threadIdx.x; j < t; j += blockDim.x) {
+    float acc = 0.0f;
+    for (uint32_t k = 0; k < d; ++k) acc = __fadd_rn(acc, __fmul_rn(q[(size_t)i * d + k], doc[(size_t)j * d + k]));
+    m = acc > m ? acc : m;
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) qmax[i] = red[0];
+}
+__global__ void sum_ordered_kernel(const float* x, uint32_t n, float* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  float s = 0.0f;
+  for (uint32_t i = 0; i < n; ++i) s = __fadd_rn(s, x[i]);
+  *out = s;
+}
+
+// rank (scoring.hpp:16-18): keys orderable(score) << 32 | ~id (descending =
+// (score desc, id asc)); non-finite scores flagged.
+__global__ void rank_keys_kernel(const uint32_t* ids, const float* scores, uint64_t n, unsigned long long* keys,
+                                 uint32_t* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const float s = scores[i];
+    if (!isfinite(s)) atomicOr(err, ERR_NONFINITE_SCORE);
+    keys[i] = make_key(s, ids[i]);
+  }
+}
+__global__ void rank_unkey_kernel(const unsigned long long* keys, uint64_t n, uint32_t* ids, float* scores) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    ids[i] = ~(uint32_t)(keys[i] & 0xFFFFFFFFull);
+    scores[i] = order_float((uint32_t)(keys[i] >> 32));
+  }
+}
+// duplicates: ids sorted ascending, any equal neighbours
+__global__ void adjacent_dup_kernel(const uint32_t* sorted_ids, uint64_t n, uint32_t* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (sorted_ids[i] == sorted_ids[i + 1]) atomicOr(err, ERR_DUPLICATE);
+}
+}  // namespace espn_k

@@ -427,7 +427,10 @@ def test_prefetch_on_off_identical_and_hit_rate(cuda_ok):
     br = api.rerank_batch(qs, cl, store, cfg)
     for b, st in enumerate(br.stats):  # reference semantics: no prefetch -> every needed doc is fetched
         assert st.needed_count == 64 and st.missed_count == 64 and st.hit_rate == 0.0
-        assert st.critical_blocks_read == st.missed_count  # every record fits one 4 KiB block here
+        nid = ids[int(off[b]):int(off[b]) + 64].astype(np.int64)
+        rec = (128 + (rp[nid + 1] - rp[nid]).astype(np.int64) * 32) * 2  # store.hpp:32-34, d_cls 128, fp16
+        assert st.critical_fetch_bytes == int(rec.sum()) == st.needed_payload_bytes
+        assert st.critical_blocks_read == int(((rec + 4095) // 4096).sum())  # per record (SPEC "Block accounting")
     rr.close(); store.close()
 
 
