@@ -8,7 +8,7 @@
  * re-ranker" (kind "port": the reference ships headers only).
  *
  * Every function cites the reference contract it restates (paths relative to
- * the upstream tree: proj/include/espn/*.hpp and SPEC.md).  Build flags must
+ * the upstream tree: proj/include/espn/<name>.hpp and SPEC.md).  Build flags must
  * keep -ffp-contract=off so a*b+c is never fused.
  *
  * Parity pinning: the fp16 codec is checked against the reference's own

@@ -109,6 +109,34 @@ def build_store_lib(force: bool = False) -> Path:
     return STORE_LIB
 
 
+REFAPI_SRC = CSRC / "host" / "espn_ref_api.cpp"
+REFAPI_LIB = LIB_DIR / "libespn_refapi.so"
+REF_INC = Path("/root/reference/proj/include")
+
+
+def build_refapi(force: bool = False) -> Path | None:
+    """lib/libespn_refapi.so: the reference's declarations (its UNMODIFIED
+    headers) defined over the B200 path -- espn_ref_api.cpp plus the C++ host
+    layer compiled with the reference's carrier types.  Built where the
+    reference headers exist (this container); the .so ships with the tree."""
+    if not REF_INC.exists():
+        return REFAPI_LIB if REFAPI_LIB.exists() else None
+    build_store_lib()
+    deps = [REFAPI_SRC, HOST_SRC, ROOT / "include" / "espn_b200.hpp", ROOT / "include" / "espn_gpu.h",
+            ROOT / "include" / "espn_store.h", ROOT / "include" / "espn_host.h", LIB, STORE_LIB]
+    if not force and REFAPI_LIB.exists() and all(p.stat().st_mtime <= REFAPI_LIB.stat().st_mtime for p in deps):
+        return REFAPI_LIB
+    cmd = [CXX, *CXX_FLAGS, "-ffp-contract=off", "-shared", "-DESPN_B200_WITH_REFERENCE_HEADERS",
+           "-I", str(ROOT / "include"), "-I", str(REF_INC), "-I", CUDA_INC, "-o", str(REFAPI_LIB), str(REFAPI_SRC),
+           str(HOST_SRC), "-L", str(LIB_DIR), "-lespn_gpu", "-lespn_store", "-L", CUDA_LIB, "-lcudart",
+           "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building libespn_refapi.so against the reference headers")
+    return REFAPI_LIB
+
+
 def check_reference_headers() -> bool:
     """Compile the C++ host API against the reference's own headers (source
     compatibility of the drop-in), where /root/reference exists."""
@@ -128,4 +156,5 @@ if __name__ == "__main__":
     build_lib(verbose="-v" in sys.argv, force="-f" in sys.argv)
     build_host(force="-f" in sys.argv)
     build_store_lib(force="-f" in sys.argv)
+    build_refapi(force="-f" in sys.argv)
     print(LIB)
