@@ -68,6 +68,13 @@ typedef struct espn_gpu_workspace espn_gpu_workspace;
                                            plain row-major and the library tiles them at open (a
                                            borrowed plain table gets a library-owned tiled copy) */
 
+#define ESPN_TABLE_STREAMED 0x4u       /* rows == NULL: the table is allocated from row_ptr (and the resident
+                                           mask) -- the HBM tier holds only the resident docs, the pinned-host
+                                           tier the rest -- and filled by espn_gpu_table_load_rows in doc order,
+                                           so neither the whole table nor its HBM-sized staging ever exists on
+                                           the host or the device (a table larger than free HBM opens); calls
+                                           that read rows fail with INVALID_STATE until every doc is loaded */
+
 /* The embedding table (store.hpp:13-35).  The HBM tier holds BOW rows only as
  * CSR: doc i's t_i token rows live at rows[row_ptr[i]*d .. row_ptr[i+1]*d),
  * 2-byte codes of `dtype`.  Callers pass plain row-major rows; in HBM the
@@ -119,6 +126,12 @@ typedef struct {
  * the table to HBM (or adopts device pointers when DEVICE_BORROWED). */
 ESPN_API int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out);
 ESPN_API int espn_gpu_table_close(espn_gpu_table* table);
+/* ESPN_TABLE_STREAMED tables: loads docs [doc_begin, doc_begin + n) (the
+ * next docs in order) from plain row-major HOST codes (the docs' rows back
+ * to back, row_ptr order) into their tiers, tiled on the way (HBM docs through
+ * a bounded pinned/device bounce, host-tier docs tiled directly into the
+ * pinned tier).  Synchronous. */
+ESPN_API int espn_gpu_table_load_rows(espn_gpu_table* table, uint64_t doc_begin, uint64_t n, const uint16_t* rows);
 ESPN_API int espn_gpu_table_info(const espn_gpu_table* table, espn_table_info* out);
 
 /* Per-stream scratch sized for at most max_queries queries and

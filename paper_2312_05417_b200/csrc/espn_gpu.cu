@@ -321,6 +321,12 @@ struct espn_gpu_table {
   uint64_t* doc_loc = nullptr;   // device: per-doc row address | tier bit
   uint8_t* host_rows = nullptr;  // pinned, mapped
   uint64_t hbm_row_bytes = 0, host_row_bytes = 0, resident_docs = 0;
+  // ESPN_TABLE_STREAMED: filled in doc order by espn_gpu_table_load_rows
+  bool streamed = false;
+  uint64_t loaded_docs = 0;
+  std::vector<uint64_t> h_row_ptr;  // host copies used while filling
+  std::vector<uint64_t> h_loc;      // tiered: per-doc address | tier bit
+  uint8_t* host_dev = nullptr;      // device alias of host_rows
   // persistent re-rank server (espn_gpu_server_start)
   ServerQueue* server = nullptr;      // device queue (NULL: no server)
   cudaStream_t server_stream = nullptr;
@@ -493,6 +499,156 @@ void drain_prof(espn_gpu_workspace* w, int i) {
 }  // namespace
 
 namespace {
+// Calls that read rows need every doc of a streamed table loaded.
+int require_loaded(const espn_gpu_table* t) {
+  if (t && t->streamed && t->loaded_docs != t->n_docs)
+    return fail(ESPN_E_INVALID_STATE, "streamed table: " + std::to_string(t->n_docs - t->loaded_docs) +
+                                          " docs not loaded yet (espn_gpu_table_load_rows)");
+  return ESPN_OK;
+}
+// ---- ESPN_TABLE_STREAMED: allocation from row_ptr, fill in doc order ----
+int open_streamed(espn_gpu_table* t, const espn_table_desc* desc) {
+  const uint64_t* rp = desc->row_ptr;
+  const uint64_t n = desc->n_docs;
+  if (rp[0] != 0) return fail(ESPN_E_INVALID_INPUT, "row_ptr[0] must be 0");
+  uint32_t mn = UINT32_MAX, mx = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (rp[i + 1] <= rp[i]) return fail(ESPN_E_INVALID_INPUT, "doc " + std::to_string(i) + " has t < 1 (types.hpp:64-68)");
+    const uint64_t len = rp[i + 1] - rp[i];
+    mn = (uint32_t)std::min<uint64_t>(mn, len);
+    mx = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(mx, len), UINT32_MAX);
+  }
+  t->min_t = mn;
+  t->max_t = mx;
+  t->n_tokens = rp[n];
+  t->streamed = true;
+  t->h_row_ptr.assign(rp, rp + n + 1);
+  ESPN_CUDA_TRY(cudaMalloc(&t->row_ptr, (n + 1) * sizeof(uint64_t)));
+  t->owned = true;
+  ESPN_CUDA_TRY(cudaMemcpy(t->row_ptr, rp, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  const uint64_t rowb = (uint64_t)t->d * 2;
+  if (!desc->resident) {  // all in HBM, exactly the table's bytes
+    ESPN_CUDA_TRY(cudaMalloc(&t->rows, std::max<uint64_t>(t->n_tokens * rowb, 16)));
+    t->owned_rows = true;
+    t->resident_docs = n;
+    return ESPN_OK;
+  }
+  uint64_t hb = 0, sb = 0, nres = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t bytes = (rp[i + 1] - rp[i]) * rowb;
+    if (desc->resident[i]) { hb += bytes; ++nres; } else { sb += bytes; }
+  }
+  uint8_t* hbm = nullptr;
+  ESPN_CUDA_TRY(cudaMalloc(&hbm, std::max<uint64_t>(hb, 16)));
+  t->rows = reinterpret_cast<uint16_t*>(hbm);
+  t->owned_rows = true;
+  ESPN_CUDA_TRY(cudaHostAlloc(&t->host_rows, std::max<uint64_t>(sb, 16), cudaHostAllocMapped | cudaHostAllocPortable));
+  ESPN_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&t->host_dev), t->host_rows, 0));
+  ESPN_CUDA_TRY(cudaMalloc(&t->doc_loc, n * 8));
+  t->h_loc.resize(n);
+  uint64_t oh = 0, os = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t bytes = (rp[i + 1] - rp[i]) * rowb;
+    if (desc->resident[i]) { t->h_loc[i] = reinterpret_cast<uint64_t>(hbm + oh); oh += bytes; }
+    else { t->h_loc[i] = reinterpret_cast<uint64_t>(t->host_dev + os) | 1ull; os += bytes; }
+  }
+  ESPN_CUDA_TRY(cudaMemcpy(t->doc_loc, t->h_loc.data(), n * 8, cudaMemcpyHostToDevice));
+  t->tiered = true;
+  t->hbm_row_bytes = hb;
+  t->host_row_bytes = sb;
+  t->resident_docs = nres;
+  return ESPN_OK;
+}
+
+template <int D>
+void tile_doc_host(const uint8_t* src, uint32_t t, uint8_t* dst) {
+  using RL = RowLayout<D>;
+  for (uint32_t j = 0; j < t; ++j)
+    for (uint32_t c = 0; c < (uint32_t)RL::CH; ++c) std::memcpy(dst + RL::off(t, j, c), src + ((uint64_t)j * RL::CH + c) * 16, 16);
+}
+void tile_doc_host_rt(uint32_t d, const uint8_t* src, uint32_t t, uint8_t* dst) {
+  switch (d) {
+    case 16: tile_doc_host<16>(src, t, dst); break;
+    case 32: tile_doc_host<32>(src, t, dst); break;
+    case 64: tile_doc_host<64>(src, t, dst); break;
+    case 128: tile_doc_host<128>(src, t, dst); break;
+    default: std::memcpy(dst, src, (uint64_t)t * d * 2); break;  // plain-row dims
+  }
+}
+
+int load_streamed(espn_gpu_table* t, uint64_t b0, uint64_t n, const uint16_t* rows) {
+  const uint64_t rowb = (uint64_t)t->d * 2;
+  const uint64_t* rp = t->h_row_ptr.data();
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(rows);
+  // HBM docs go through a bounded bounce: pinned chunk -> device chunk -> tile kernel
+  constexpr uint64_t kChunk = 64ull << 20;
+  uint8_t* h_chunk = nullptr;
+  uint8_t* d_chunk = nullptr;
+  TileJob* h_jobs = nullptr;
+  TileJob* d_jobs = nullptr;
+  const uint64_t max_jobs = std::max<uint64_t>(kChunk / rowb, 1);
+  auto cleanup = [&] { cudaFreeHost(h_chunk); cudaFree(d_chunk); cudaFreeHost(h_jobs); cudaFree(d_jobs); };
+  bool have_hbm = false;
+  for (uint64_t i = b0; i < b0 + n && !have_hbm; ++i) have_hbm = !t->tiered || !(t->h_loc[i] & 1ull);
+  if (have_hbm) {
+    if (cudaHostAlloc(&h_chunk, kChunk, cudaHostAllocDefault) != cudaSuccess || cudaMalloc(&d_chunk, kChunk) != cudaSuccess ||
+        cudaHostAlloc(&h_jobs, max_jobs * sizeof(TileJob), cudaHostAllocDefault) != cudaSuccess ||
+        cudaMalloc(&d_jobs, max_jobs * sizeof(TileJob)) != cudaSuccess) {
+      cleanup();
+      return fail(ESPN_E_CUDA, "streamed load: bounce allocation failed");
+    }
+  }
+  uint64_t used = 0, nj = 0;
+  auto flush = [&]() -> cudaError_t {
+    if (!nj) return cudaSuccess;
+    cudaError_t e = cudaMemcpy(d_chunk, h_chunk, used, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_jobs, h_jobs, nj * sizeof(TileJob), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      const int blocks = (int)std::min<uint64_t>((nj + 7) / 8, (uint64_t)t->num_sms * 8);
+      switch (t->d) {
+        case 16: tile_jobs_kernel<16><<<blocks, 256>>>(d_chunk, d_jobs, (uint32_t)nj); break;
+        case 32: tile_jobs_kernel<32><<<blocks, 256>>>(d_chunk, d_jobs, (uint32_t)nj); break;
+        case 64: tile_jobs_kernel<64><<<blocks, 256>>>(d_chunk, d_jobs, (uint32_t)nj); break;
+        case 128: tile_jobs_kernel<128><<<blocks, 256>>>(d_chunk, d_jobs, (uint32_t)nj); break;
+        default:
+          for (uint64_t j = 0; j < nj && e == cudaSuccess; ++j)
+            e = cudaMemcpy(reinterpret_cast<void*>(h_jobs[j].dst), d_chunk + h_jobs[j].src, (uint64_t)h_jobs[j].t * rowb,
+                           cudaMemcpyDeviceToDevice);
+          break;
+      }
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    used = 0;
+    nj = 0;
+    return e;
+  };
+  for (uint64_t i = b0; i < b0 + n; ++i) {
+    const uint32_t tt = (uint32_t)(rp[i + 1] - rp[i]);
+    const uint64_t bytes = (uint64_t)tt * rowb;
+    const uint8_t* s = src + (rp[i] - rp[b0]) * rowb;
+    const bool host_tier = t->tiered && (t->h_loc[i] & 1ull);
+    if (host_tier) {  // tile straight into the pinned tier
+      const uint64_t a = (t->h_loc[i] & ~1ull) - reinterpret_cast<uint64_t>(t->host_dev);
+      tile_doc_host_rt(t->d, s, tt, t->host_rows + a);
+      continue;
+    }
+    if (bytes > kChunk) { cleanup(); return fail(ESPN_E_INVALID_INPUT, "a document larger than the 64 MB bounce"); }
+    if (used + bytes > kChunk || nj == max_jobs) {
+      const cudaError_t e = flush();
+      if (e != cudaSuccess) { cleanup(); return fail(ESPN_E_CUDA, std::string("streamed load: ") + cudaGetErrorString(e)); }
+    }
+    std::memcpy(h_chunk + used, s, bytes);
+    const uint64_t dst = t->tiered ? t->h_loc[i] : reinterpret_cast<uint64_t>(t->rows) + rp[i] * rowb;
+    h_jobs[nj++] = TileJob{used, dst, tt, 0};
+    used += bytes;
+  }
+  const cudaError_t e = flush();
+  cleanup();
+  if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("streamed load: ") + cudaGetErrorString(e));
+  return ESPN_OK;
+}
+
 // Staging slots of a tiered workspace: pf_q lists the slots holding a
 // prefetch not yet consumed by its PREFETCHED batch; any other staging must
 // use the other slot, or it would overwrite that prefetch.
@@ -815,7 +971,10 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
   if (desc->alignment != 1 && desc->alignment != 512 && desc->alignment != 4096)
     return fail(ESPN_E_INVALID_INPUT, "alignment must be 1, 512 or 4096 (store.hpp:28)");
   if (desc->n_docs == 0) return fail(ESPN_E_INVALID_INPUT, "empty table");
-  if (!desc->row_ptr || !desc->rows) return fail(ESPN_E_INVALID_INPUT, "null row_ptr/rows");
+  const bool streamed = (desc->flags & ESPN_TABLE_STREAMED) != 0;
+  if (!desc->row_ptr || (!desc->rows && !streamed)) return fail(ESPN_E_INVALID_INPUT, "null row_ptr/rows");
+  if (streamed && (desc->flags & ESPN_TABLE_DEVICE_BORROWED))
+    return fail(ESPN_E_INVALID_INPUT, "a streamed table takes a HOST row_ptr");
   int sms = 0;
   bool tc = false;
   int st = check_device(desc->device, &sms, &tc);
@@ -835,6 +994,15 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
   t->shard_index = desc->shard_count > 1 ? desc->shard_index : 0;
   if (t->shard_index >= t->shard_count) { delete t; return fail(ESPN_E_INVALID_INPUT, "shard_index >= shard_count"); }
   const bool borrowed = (desc->flags & ESPN_TABLE_DEVICE_BORROWED) != 0;
+  if (streamed) {
+    const int ss = open_streamed(t, desc);
+    if (ss) {
+      espn_gpu_table_close(t);
+      return ss;
+    }
+    *out = t;
+    return ESPN_OK;
+  }
   if (!borrowed) {
     // host tables: validate (types.hpp:64-68: t >= 1), then upload
     const uint64_t* rp = desc->row_ptr;
@@ -937,6 +1105,24 @@ int espn_gpu_table_close(espn_gpu_table* t) {
   cudaFree(t->doc_loc);
   if (t->host_rows) cudaFreeHost(t->host_rows);
   delete t;
+  return ESPN_OK;
+}
+
+int espn_gpu_table_load_rows(espn_gpu_table* t, uint64_t doc_begin, uint64_t n, const uint16_t* rows) {
+  if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
+  if (!t->streamed) return fail(ESPN_E_INVALID_STATE, "not a streamed table (ESPN_TABLE_STREAMED)");
+  if (doc_begin != t->loaded_docs) return fail(ESPN_E_INVALID_INPUT, "streamed docs must be loaded in order");
+  if (n == 0) return ESPN_OK;
+  if (doc_begin + n > t->n_docs) return fail(ESPN_E_INVALID_INPUT, "doc range beyond the table");
+  if (!rows) return fail(ESPN_E_INVALID_INPUT, "null rows");
+  DeviceGuard g(t->device);
+  const int st = load_streamed(t, doc_begin, n, rows);
+  if (st) return st;
+  t->loaded_docs += n;
+  if (t->loaded_docs == t->n_docs) {  // complete: drop the fill-time host copies
+    std::vector<uint64_t>().swap(t->h_loc);
+    std::vector<uint64_t>().swap(t->h_row_ptr);
+  }
   return ESPN_OK;
 }
 
@@ -1124,6 +1310,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
                     espn_rerank_out* o, void* stream_v) {
   if (!t || !w || !a || !o) return fail(ESPN_E_INVALID_INPUT, "null argument");
   if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
+  if (const int ls = require_loaded(t)) return ls;
   cudaStream_t s = static_cast<cudaStream_t>(stream_v);
   const uint32_t B = a->n_queries, nq = a->n_query_tokens, k = a->final_k;
   // ---- host-side validation (pipeline.hpp:31-32) ----
@@ -1641,6 +1828,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
 int espn_gpu_prefetch(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_args* a, void* side_stream) {
   if (!t || !w || !a) return fail(ESPN_E_INVALID_INPUT, "null argument");
   if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
+  if (const int ls = require_loaded(t)) return ls;
   if (!t->tiered) return ESPN_OK;  // everything is HBM-resident
   if (!(a->flags & ESPN_RERANK_DEVICE_IO)) return fail(ESPN_E_INVALID_INPUT, "prefetch needs DEVICE_IO batch arrays");
   const uint32_t B = a->n_queries;
@@ -1680,6 +1868,7 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
                             const uint64_t* hint_offsets, uint32_t flags, void* side_stream) {
   if (!t || !w) return fail(ESPN_E_INVALID_INPUT, "null argument");
   if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
+  if (const int ls = require_loaded(t)) return ls;
   if (!t->tiered) return ESPN_OK;  // everything is HBM-resident
   if (B == 0) return ESPN_OK;
   if (!hint_offsets) return fail(ESPN_E_INVALID_INPUT, "null hint offsets");
@@ -1783,6 +1972,7 @@ int espn_gpu_workspace_sync(espn_gpu_workspace* w, void* stream_v) {
 int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t* out_rows,
                     uint64_t* out_row_ptr, uint64_t capacity_tokens, void* stream_v) {
   if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
+  if (const int ls = require_loaded(t)) return ls;
   if (n == 0) {
     if (out_row_ptr) {
       uint64_t z = 0;
@@ -1906,6 +2096,7 @@ int espn_gpu_merge_topk(const uint32_t* ids, const float* scores, const uint32_t
 int espn_gpu_gather_rows(espn_gpu_table* t, const uint32_t* ids, uint64_t n, const uint64_t* out_row_ptr,
                          uint16_t* out_rows, void* stream_v) {
   if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
+  if (const int ls = require_loaded(t)) return ls;
   if (n == 0) return ESPN_OK;
   if (!ids || !out_row_ptr || !out_rows) return fail(ESPN_E_INVALID_INPUT, "null argument");
   DeviceGuard g(t->device);

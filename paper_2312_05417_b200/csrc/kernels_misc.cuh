@@ -958,3 +958,27 @@ __global__ void adjacent_dup_kernel(const uint32_t* sorted_ids, uint64_t n, uint
     if (sorted_ids[i] == sorted_ids[i + 1]) atomicOr(err, ERR_DUPLICATE);
 }
 }  // namespace espn_k
+
+namespace espn_k {
+// Streamed table fill (espn_gpu_table_load_rows): warp per doc, plain rows
+// from a bounce chunk -> the doc's tile-layout destination in HBM.
+struct TileJob {
+  uint64_t src;  // byte offset of the doc's plain rows in the chunk
+  uint64_t dst;  // destination address
+  uint32_t t;    // tokens
+  uint32_t pad;
+};
+template <int D>
+__global__ void __launch_bounds__(256) tile_jobs_kernel(const uint8_t* chunk, const TileJob* jobs, uint32_t n) {
+  using RL = RowLayout<D>;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
+    const TileJob j = jobs[i];
+    const uint4* src = reinterpret_cast<const uint4*>(chunk + j.src);
+    uint8_t* dst = reinterpret_cast<uint8_t*>(j.dst);
+    for (uint32_t v = lane; v < j.t * RL::CH; v += 32)
+      *reinterpret_cast<uint4*>(dst + RL::off(j.t, v / RL::CH, v % RL::CH)) = src[v];
+  }
+}
+}  // namespace espn_k
