@@ -196,11 +196,18 @@ class Store {
   // docs[i].doc_id must equal i (dense ids, store.hpp:20)
   static Store from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtype = Dtype::f16,
                               RecordLayout layout = {}, int device = 0);
-  // open_store (store.hpp:111-112) for the HBM tier: reads a .espn store
-  // (include/espn_store.h, libespn_store.so) and uploads its rows; the
-  // record layout comes from the manifest.
+  // open_store (store.hpp:111-112) for the GPU table, streamed from a .espn
+  // store (include/espn_store.h): allocated from the manifest -- only the
+  // resident docs in HBM when `resident` is given -- and filled in chunks of
+  // chunk_bytes, so the store is never read whole; the record layout comes
+  // from the manifest.
   static Store open_store(const std::string& base, Dtype dtype = Dtype::f16, int device = 0,
-                          std::span<const std::uint8_t> resident = {});
+                          std::span<const std::uint8_t> resident = {}, std::uint64_t chunk_bytes = 64ull << 20);
+  // ESPN_TABLE_STREAMED: an empty table allocated from row_ptr (+ resident),
+  // filled in doc order by load_rows (plain 2-byte codes of the next docs).
+  static Store streamed(std::span<const std::uint64_t> row_ptr, std::uint32_t d, Dtype dtype = Dtype::f16,
+                        RecordLayout layout = {}, int device = 0, std::span<const std::uint8_t> resident = {});
+  void load_rows(std::uint64_t doc_begin, std::uint64_t n_docs, std::span<const std::uint16_t> codes);
   ~Store();
   Store(Store&&) noexcept;
   Store& operator=(Store&&) noexcept;
@@ -230,6 +237,9 @@ class Store {
 
  private:
   struct WorkspaceCache;
+  struct StreamedTag {};
+  Store(StreamedTag, std::span<const std::uint64_t> row_ptr, std::uint32_t d, Dtype dtype, RecordLayout layout,
+        int device, std::span<const std::uint8_t> resident);
   std::unique_ptr<WorkspaceCache> cache_;
   espn_gpu_table* table_ = nullptr;
   std::uint32_t d_ = 0;

@@ -109,6 +109,14 @@ ESPN_API int espn_store_fetch(espn_store_reader* reader, const uint32_t* ids, ui
                               uint64_t* out_off, uint64_t capacity, uint64_t* bytes_read, uint64_t* blocks_read,
                               double* wall_time);
 
+/* The BOW rows of docs [doc_begin, doc_begin + n) in the GPU table's code
+ * format (fp16: width-2 stores copied bit-exactly; else round to nearest
+ * even): row_ptr_out[n + 1] local token offsets, codes_out the rows (NULL:
+ * offsets only).  Feeds espn_gpu_table_load_rows chunk by chunk, so a store
+ * opens without ever being read whole. */
+ESPN_API int espn_store_read_rows(espn_store_reader* reader, uint64_t doc_begin, uint64_t n, uint32_t dtype,
+                                  uint64_t* row_ptr_out, uint16_t* codes_out);
+
 /* Thread-local message of the last failing call of this library. */
 ESPN_API const char* espn_store_last_error(void);
 

@@ -40,6 +40,8 @@ ESPN_RERANK_PREFETCHED = 0x40
 ESPN_RERANK_SEPARATE_TOPK = 0x80
 ESPN_RERANK_QUERY_ROUNDED = 0x100
 ESPN_RERANK_QUERY_SPLIT = 0x200
+ESPN_TABLE_STREAMED = 0x4
+ESPN_READ_DIRECT, ESPN_READ_BUFFERED, ESPN_READ_MMAP = 0, 1, 2
 
 
 class TableDesc(C.Structure):
@@ -103,6 +105,7 @@ class Counters(C.Structure):
 SIGNATURES = {
     "espn_gpu_table_open": (C.c_int, [C.POINTER(TableDesc), C.POINTER(C.c_void_p)]),
     "espn_gpu_table_close": (C.c_int, [C.c_void_p]),
+    "espn_gpu_table_load_rows": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]),
     "espn_gpu_table_info": (C.c_int, [C.c_void_p, C.POINTER(TableInfo)]),
     "espn_gpu_workspace_create": (C.c_int, [C.c_void_p, C.POINTER(WorkspaceDesc), C.POINTER(C.c_void_p)]),
     "espn_gpu_workspace_destroy": (C.c_int, [C.c_void_p]),
@@ -187,6 +190,13 @@ STORE_SIGNATURES = {
                                    C.c_void_p, C.c_void_p, C.c_void_p]),
     "espn_store_load_manifest": (C.c_int, [C.c_char_p, C.POINTER(StoreHeader), C.c_void_p]),
     "espn_store_read_table": (C.c_int, [C.c_char_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "espn_store_save_manifest": (C.c_int, [C.c_char_p, C.POINTER(StoreHeader), C.c_void_p]),
+    "espn_store_open": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p), C.POINTER(StoreHeader)]),
+    "espn_store_close": (C.c_int, [C.c_void_p]),
+    "espn_store_records": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "espn_store_fetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
+                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
+    "espn_store_read_rows": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]),
     "espn_store_last_error": (C.c_char_p, []),
 }
 

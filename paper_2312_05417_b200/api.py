@@ -290,7 +290,7 @@ class GpuStore:
     def __init__(self, row_ptr, rows, d: int, dtype: str = "f16", d_cls: int = 128,
                  value_width: int = 2, alignment: int = 4096, device: int = 0,
                  borrowed_device: bool = False, shard_count: int = 1, shard_index: int = 0,
-                 rows_tiled: bool = False, resident=None):
+                 rows_tiled: bool = False, resident=None, streamed: bool = False):
         self.d = int(d)
         self.dtype = dtype
         self.d_cls = int(d_cls)
@@ -304,6 +304,12 @@ class GpuStore:
             rp_p, rows_p, flags = _ptr(row_ptr), _ptr(rows), L.ESPN_TABLE_DEVICE_BORROWED
             if rows_tiled:
                 flags |= L.ESPN_TABLE_ROWS_TILED
+        elif streamed:  # ESPN_TABLE_STREAMED: allocated from row_ptr, filled by load_rows
+            row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+            n_docs = int(row_ptr.shape[0]) - 1
+            self._row_ptr_host = row_ptr
+            self._keep = (row_ptr,)
+            rp_p, rows_p, flags = _ptr(row_ptr), None, L.ESPN_TABLE_STREAMED
         else:
             row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
             rows = np.ascontiguousarray(rows, dtype=np.uint16)
@@ -341,13 +347,48 @@ class GpuStore:
         self._workspaces = {}
 
     @classmethod
-    def open_store(cls, base, dtype: str = "f16", **kw) -> "GpuStore":
-        """open_store (store.hpp:111-112) for the HBM tier: reads the .espn
-        store (include/espn_store.h) and uploads its rows; d_cls /
-        value_width / alignment come from the manifest."""
+    def open_store(cls, base, dtype: str = "f16", mode: str = "buffered", chunk_bytes: int = 64 << 20,
+                   **kw) -> "GpuStore":
+        """open_store (store.hpp:111-112) for the GPU table, STREAMED from the
+        .espn file (include/espn_store.h): the table is allocated from the
+        manifest (only resident docs in HBM when `resident` is given, the rest
+        in the pinned-host tier) and filled chunk by chunk (chunk_bytes of
+        rows at a time), so the store is never read whole into memory.
+        d_cls / value_width / alignment come from the manifest."""
         m = load_manifest(base)
-        row_ptr, codes, _ = read_store_table(base, dtype)
-        return cls(row_ptr, codes, m.d, dtype, d_cls=m.d_cls, value_width=m.value_width, alignment=m.alignment, **kw)
+        tok = m.records["token_count"].astype(np.uint64)
+        row_ptr = np.zeros(m.count() + 1, np.uint64)
+        row_ptr[1:] = np.cumsum(tok)
+        store = cls(row_ptr, None, m.d, dtype, d_cls=m.d_cls, value_width=m.value_width, alignment=m.alignment,
+                    streamed=True, **kw)
+        slib = L.store_lib()
+        reader = C.c_void_p()
+        h = L.StoreHeader()
+        _check_store(slib.espn_store_open(str(base).encode(), {"direct": L.ESPN_READ_DIRECT, "buffered":
+                                          L.ESPN_READ_BUFFERED, "mmap": L.ESPN_READ_MMAP}[mode], 16,
+                                          C.byref(reader), C.byref(h)))
+        try:
+            i, n = 0, m.count()
+            row_bytes = m.d * 2
+            while i < n:
+                j = int(np.searchsorted(row_ptr, row_ptr[i] + max(chunk_bytes // row_bytes, 1), side="right")) - 1
+                j = min(max(j, i + 1), n)
+                rp_l = np.zeros(j - i + 1, np.uint64)
+                codes = np.empty(max(int(row_ptr[j] - row_ptr[i]) * m.d, 1), np.uint16)
+                _check_store(slib.espn_store_read_rows(reader, i, j - i, _DTYPES[dtype], rp_l.ctypes.data,
+                                                       codes.ctypes.data))
+                store.load_rows(i, codes)
+                i = j
+        finally:
+            slib.espn_store_close(reader)
+        return store
+
+    def load_rows(self, doc_begin: int, codes) -> None:
+        """espn_gpu_table_load_rows: the next docs' plain 2-byte codes (streamed tables)."""
+        codes = np.ascontiguousarray(codes, dtype=np.uint16)
+        rp = self._row_ptr_host
+        n = int(np.searchsorted(rp, rp[doc_begin] + codes.size // self.d, side="right")) - 1 - doc_begin
+        _check(L.lib().espn_gpu_table_load_rows(self._h, int(doc_begin), int(n), codes.ctypes.data))
 
     @classmethod
     def from_device(cls, row_ptr, rows, d: int, dtype: str = "f16", **kw) -> "GpuStore":

@@ -175,21 +175,68 @@ Store Store::from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtyp
   return Store(rp, codes, d, dtype, layout, device);
 }
 
-Store Store::open_store(const std::string& base, Dtype dtype, int device, std::span<const std::uint8_t> resident) {
-  espn_store_header h{};
-  auto check = [](int st) {
+Store::Store(StreamedTag, std::span<const std::uint64_t> row_ptr, std::uint32_t d, Dtype dtype, RecordLayout layout,
+             int device, std::span<const std::uint8_t> resident)
+    : cache_(std::make_unique<WorkspaceCache>()), d_(d), dtype_(dtype), layout_(layout), device_(device),
+      row_ptr_(row_ptr.begin(), row_ptr.end()) {
+  if (row_ptr.size() < 2) throw InvalidInputError("empty table");
+  espn_table_desc desc{};
+  desc.n_docs = row_ptr.size() - 1;
+  desc.d = d;
+  desc.dtype = static_cast<std::uint32_t>(dtype);
+  desc.d_cls = layout.d_cls;
+  desc.value_width = layout.value_width;
+  desc.alignment = layout.alignment;
+  desc.flags = ESPN_TABLE_STREAMED;
+  desc.row_ptr = row_ptr.data();
+  desc.rows = nullptr;
+  desc.device = device;
+  if (!resident.empty()) {
+    if (resident.size() != desc.n_docs) throw InvalidInputError("resident mask size != n_docs");
+    desc.resident = resident.data();
+  }
+  check(espn_gpu_table_open(&desc, &table_));
+}
+
+Store Store::streamed(std::span<const std::uint64_t> row_ptr, std::uint32_t d, Dtype dtype, RecordLayout layout,
+                      int device, std::span<const std::uint8_t> resident) {
+  return Store(StreamedTag{}, row_ptr, d, dtype, layout, device, resident);
+}
+
+void Store::load_rows(std::uint64_t doc_begin, std::uint64_t n_docs, std::span<const std::uint16_t> codes) {
+  if (doc_begin + n_docs > this->n_docs()) throw InvalidInputError("load_rows: doc range beyond the table");
+  if (codes.size() < (row_ptr_[doc_begin + n_docs] - row_ptr_[doc_begin]) * d_)
+    throw InvalidInputError("load_rows: codes shorter than the docs' rows");
+  check(espn_gpu_table_load_rows(table_, doc_begin, n_docs, codes.data()));
+}
+
+Store Store::open_store(const std::string& base, Dtype dtype, int device, std::span<const std::uint8_t> resident,
+                        std::uint64_t chunk_bytes) {
+  auto check_store = [](int st) {
     if (st != ESPN_OK) throw_status(st, espn_store_last_error());
   };
-  check(espn_store_load_manifest(base.c_str(), &h, nullptr));
+  espn_store_reader* rd = nullptr;
+  espn_store_header h{};
+  check_store(espn_store_open(base.c_str(), ESPN_READ_BUFFERED, 16, &rd, &h));
+  std::unique_ptr<espn_store_reader, int (*)(espn_store_reader*)> guard(rd, espn_store_close);
   std::vector<espn_manifest_record> recs(h.count);
-  check(espn_store_load_manifest(base.c_str(), &h, recs.data()));
-  std::uint64_t tokens = 0;
-  for (const auto& r : recs) tokens += r.token_count;
-  std::vector<std::uint64_t> rp(h.count + 1);
-  std::vector<std::uint16_t> codes(std::max<std::uint64_t>(tokens * h.d, 1));
-  check(espn_store_read_table(base.c_str(), static_cast<std::uint32_t>(dtype), rp.data(), codes.data(), nullptr));
-  codes.resize(tokens * h.d);
-  return Store(rp, codes, h.d, dtype, RecordLayout{h.d_cls, h.value_width, h.alignment}, device, resident);
+  check_store(espn_store_records(rd, recs.data()));
+  std::vector<std::uint64_t> rp(h.count + 1, 0);
+  for (std::uint64_t i = 0; i < h.count; ++i) rp[i + 1] = rp[i] + recs[i].token_count;
+  Store s = streamed(rp, h.d, dtype, RecordLayout{h.d_cls, h.value_width, h.alignment}, device, resident);
+  const std::uint64_t max_tok = std::max<std::uint64_t>(chunk_bytes / (2ull * h.d), 1);
+  std::vector<std::uint16_t> codes;
+  std::vector<std::uint64_t> lrp;
+  for (std::uint64_t i = 0; i < h.count;) {
+    std::uint64_t j = i + 1;
+    while (j < h.count && rp[j + 1] - rp[i] <= max_tok) ++j;
+    codes.resize((rp[j] - rp[i]) * h.d);
+    lrp.resize(j - i + 1);
+    check_store(espn_store_read_rows(rd, i, j - i, static_cast<std::uint32_t>(dtype), lrp.data(), codes.data()));
+    s.load_rows(i, j - i, codes);
+    i = j;
+  }
+  return s;
 }
 
 void build_store(const std::string& base, std::span<const std::uint64_t> row_ptr, std::span<const float> rows,

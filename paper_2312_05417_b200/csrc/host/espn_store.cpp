@@ -459,4 +459,46 @@ int espn_store_fetch(espn_store_reader* r, const uint32_t* ids, uint64_t n, uint
   return ESPN_OK;
 }
 
+
+int espn_store_read_rows(espn_store_reader* r, uint64_t doc_begin, uint64_t n, uint32_t dtype, uint64_t* row_ptr_out,
+                         uint16_t* codes_out) {
+  if (!r || !row_ptr_out) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (dtype != ESPN_DTYPE_F16 && dtype != ESPN_DTYPE_BF16) return fail(ESPN_E_INVALID_INPUT, "dtype must be f16 or bf16");
+  if (doc_begin + n > r->h.count) return fail(ESPN_E_INVALID_INPUT, "doc range beyond the store");
+  row_ptr_out[0] = 0;
+  for (uint64_t i = 0; i < n; ++i) row_ptr_out[i + 1] = row_ptr_out[i] + r->recs[doc_begin + i].token_count;
+  if (!codes_out || n == 0) return ESPN_OK;
+  std::vector<uint32_t> ids(n);
+  for (uint64_t i = 0; i < n; ++i) ids[i] = static_cast<uint32_t>(doc_begin + i);
+  std::vector<uint64_t> off(n + 1);
+  uint64_t br = 0, bl = 0;
+  int st = espn_store_fetch(r, ids.data(), n, nullptr, off.data(), 0, &br, &bl, nullptr);
+  if (st != ESPN_OK) return st;
+  std::vector<uint8_t> buf(std::max<uint64_t>(off[n], 1));
+  st = espn_store_fetch(r, ids.data(), n, buf.data(), off.data(), buf.size(), &br, &bl, nullptr);
+  if (st != ESPN_OK) return st;
+  const uint32_t w = r->h.value_width, d = r->h.d;
+  for (uint64_t i = 0; i < n; ++i) {
+    const unsigned char* b = buf.data() + off[i] + uint64_t(r->h.d_cls) * w;
+    uint16_t* out = codes_out + row_ptr_out[i] * d;
+    const uint64_t nv = (row_ptr_out[i + 1] - row_ptr_out[i]) * d;
+    if (w == 2 && dtype == ESPN_DTYPE_F16) {
+      std::memcpy(out, b, nv * 2);  // the store's own fp16 codes, bit-exact
+      continue;
+    }
+    for (uint64_t j = 0; j < nv; ++j) {
+      float x;
+      if (w == 2) {
+        uint16_t c;
+        std::memcpy(&c, b + 2 * j, 2);
+        x = f16_to_f32(c);
+      } else {
+        std::memcpy(&x, b + 4 * j, 4);
+      }
+      out[j] = dtype == ESPN_DTYPE_F16 ? f32_to_f16(x) : f32_to_bf16(x);
+    }
+  }
+  return ESPN_OK;
+}
+
 }  // extern "C"
