@@ -740,7 +740,7 @@ def run_ours(args, cfg):
                 pinned(np.zeros(B_q, np.int32))] for _ in range(2)] for _ in range(NL)]
     e2e_ev = [[torch.cuda.Event() for _ in range(2)] for _ in range(NL)]
 
-    serve = args.server == "on" and not emulated
+    serve = (args.server == "on" or (args.server == "auto" and cfg["batch"] >= 16)) and not emulated
     if serve:
         store.server_start(query_precision=args.query_precision, idle_us=2_000_000)
 
@@ -1161,8 +1161,9 @@ def main():
     ap.add_argument("--inflight", type=int, default=3,
                     help="batches in flight (one stream + workspace each); the latency percentiles use one")
     ap.add_argument("--query-precision", default="auto", choices=["auto", "split", "rounded"])
-    ap.add_argument("--server", default="on", choices=["on", "off"],
-                    help="serve the timed batches with the persistent MaxSim server (DESIGN.md §3)")
+    ap.add_argument("--server", default="auto", choices=["auto", "on", "off"],
+                    help="serve the timed batches with the persistent MaxSim server (DESIGN.md §3); auto: on for "
+                         "batches of >= 16 queries (small batches do not amortise its per-batch gate and merge)")
     ap.add_argument("--placement", default="auto", choices=["auto", "replica", "replica-split", "shard"],
                     help="N>1: replica = independent replicas (weak scaling, no collective); shard / replica-split = "
                          "the stated global batch through espn_gpu_rerank_sharded (strong scaling); auto: shard for "

@@ -1,0 +1,8 @@
+# round-2 re-entry check: full GPU suite, smoke, default bench, reference arm
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_h.log 2>&1; echo pytest=$?
+tail -15 gpurun_out/pytest_h.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_h.log 2>&1; echo smoke=$?; tail -3 gpurun_out/smoke_h.log
+timeout 600 python bench.py > gpurun_out/bench_h.json 2> gpurun_out/bench_h.err; echo bench=$?
+tail -3 gpurun_out/bench_h.err; cat gpurun_out/bench_h.json
+timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_h_ref.json 2> gpurun_out/bench_h_ref.err; echo ref=$?; cat gpurun_out/bench_h_ref.json
