@@ -676,6 +676,7 @@ def run_ours(args, cfg):
     QP = {"auto": 0, "split": L.ESPN_RERANK_QUERY_SPLIT, "rounded": L.ESPN_RERANK_QUERY_ROUNDED}[args.query_precision]
     flags = L.ESPN_RERANK_DEVICE_IO | L.ESPN_RERANK_DEVICE_OFFSETS | L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_PROFILE | QP
 
+    KERN = {"auto": L.ESPN_KERNEL_AUTO, "tcgen05": L.ESPN_KERNEL_TCGEN05, "small": L.ESPN_KERNEL_SMALL}[args.kernel]
     class Lane:
         """One batch in flight: its own workspace, stream, output buffers, NCCL
         group (sharded) and one CUDA graph per input batch.  `inflight` lanes
@@ -697,14 +698,14 @@ def run_ours(args, cfg):
                 a = L.RerankArgs(n_queries=B_q, n_query_tokens=nq, query_tokens=db["q"].data_ptr(),
                                  cand_ids=db["ids"].data_ptr(), cand_cls=db["cls"].data_ptr(),
                                  cand_offsets=db["doff"].data_ptr(), rerank_count=R, final_k=k, alpha=1.0,
-                                 flags=flags, kernel=L.ESPN_KERNEL_AUTO, needed_counts=db["dneed"].data_ptr())
+                                 flags=flags, kernel=KERN, needed_counts=db["dneed"].data_ptr())
                 o = L.RerankOut(ids=base, scores=base + 4 * B_q * k, counts=base + 8 * B_q * k)
             else:
                 hq, hout = host
                 a = L.RerankArgs(n_queries=B_q, n_query_tokens=nq, query_tokens=hq["q"].data_ptr(),
                                  cand_ids=hq["ids"].data_ptr(), cand_cls=hq["cls"].data_ptr(),
                                  cand_offsets=hq["off"].ctypes.data, rerank_count=R, final_k=k, alpha=1.0,
-                                 flags=flags, kernel=L.ESPN_KERNEL_AUTO, needed_counts=hq["need"].ctypes.data)
+                                 flags=flags, kernel=KERN, needed_counts=hq["need"].ctypes.data)
                 o = L.RerankOut(ids=hout[0].data_ptr(), scores=hout[1].data_ptr(), counts=hout[2].data_ptr())
             rc = lib.espn_gpu_rerank(store.handle, self.rr.handle, C.byref(a), C.byref(o), C.c_void_p(stream_ptr))
             if rc:
@@ -751,6 +752,14 @@ def run_ours(args, cfg):
                 ln.enqueue(dev_batches[i % n_batches], ln.stream.cuda_stream)
         ln.stream.synchronize()
         ln.rr.sync(ln.stream.cuda_stream)
+    # which path the library took (espn_counters: 1 launch per batch = the
+    # single-launch small-batch kernel, 3 = plan -> MaxSim -> finalize, 2 = served)
+    cw = lanes[0].rr.counters()
+    per_batch = int(round(cw["kernel_launches"] / max(cw["batches"], 1)))
+    small_path = per_batch == 1 and not serve
+    kern_name = f"rerank_small_kernel<{d}>" if small_path else f"maxsim_tc_kernel<{d}>"
+    kern_label = ("single-launch small-batch kernel (CUDA cores, fp32 query, bit-exact; %s)" % args.kernel
+                  if small_path else "tcgen05 (%s)" % args.kernel)
     if serve:  # graph capture synchronises the device: capture with the server paused
         store.server_pause()
     for ln in lanes:
@@ -852,7 +861,7 @@ def run_ours(args, cfg):
             A[i] = L.RerankArgs(n_queries=B_q, n_query_tokens=nq, query_tokens=hq["q"].data_ptr(),
                                 cand_ids=hq["ids"].data_ptr(), cand_cls=hq["cls"].data_ptr(),
                                 cand_offsets=hq["off"].ctypes.data, rerank_count=R, final_k=k, alpha=1.0,
-                                flags=L.ESPN_RERANK_ASYNC | QP, kernel=L.ESPN_KERNEL_AUTO,
+                                flags=L.ESPN_RERANK_ASYNC | QP, kernel=KERN,
                                 needed_counts=hq["need"].ctypes.data)
             ho = h_outs[i % NL][(i // NL) % 2]
             O[i] = L.RerankOut(ids=ho[0].data_ptr(), scores=ho[1].data_ptr(), counts=ho[2].data_ptr())
@@ -956,7 +965,7 @@ def run_ours(args, cfg):
     # kernel, plus the ONE persistent MaxSim launch (server); else plan,
     # MaxSim, finalize per step (the library's launch counter agrees:
     # espn_counters.kernel_launches counts 2 per served and 3 per plain batch)
-    n_launch_ours = args.steps * 2 + 1 if serve else args.steps * 3
+    n_launch_ours = args.steps * 2 + 1 if serve else args.steps * per_batch
     q_total = B_q * args.steps * world  # every replica served its own B_q-query batches
     value = q_total / (ms / 1e3)
     # the L2 claim is computed, not asserted: rows touched per rotation of the
@@ -993,9 +1002,12 @@ def run_ours(args, cfg):
                    "launch": ("persistent tcgen05 MaxSim server (one launch) fed by a device batch queue; a step = one "
                               "CUDA graph (plan + submit -> wait); %d batches in flight on separate streams/workspaces"
                               % NL if serve else
+                              ("one CUDA graph per batch (ONE kernel: validation, CUDA-core MaxSim, aggregate, "
+                               "per-CTA top-k, last-CTA merge + duplicate check); %d batches in flight on separate "
+                               "streams/workspaces" % NL) if small_path else
                               "one CUDA graph per batch (device-planned: plan -> tcgen05 MaxSim with fused ranking -> "
                               "finalize merge); %d batches in flight on separate streams/workspaces" % NL),
-                   "kernel": "tcgen05 (auto)",
+                   "kernel": kern_label,
                    "query_precision": {"auto": "fp32 query as hi + lo in the table dtype (two MMAs per K-step)"
                                                if not (d == 128 and cfg["dtype"] == "f16") else
                                                "fp32 query rounded to f16 (d=128 default)",
@@ -1007,7 +1019,7 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": f"maxsim_tc_kernel<{d}>", "kernel_ms": maxsim_ms,
+                     "kernel": kern_name, "kernel_ms": maxsim_ms,
                      "kernel_timing": ("persistent server: one MaxSim launch serves every batch of the timed region; "
                                        "per-batch service time = timed region / batches" if serve else
                                        "device globaltimer, first CTA start -> last CTA end, per launch, "
@@ -1152,6 +1164,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "small"],
+                    help="espn_kernel of the re-rank calls (auto: the library's choice -- the single-launch "
+                         "small-batch kernel for <= 4096 scored pairs, else tcgen05)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--preroll-s", type=float, default=2.0)
     ap.add_argument("--cpu-batches", type=int, default=8)

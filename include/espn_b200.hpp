@@ -167,7 +167,8 @@ using ResultsByQuery = std::map<QueryId, RankedList>;
 namespace espn::gpu {
 
 enum class Dtype : std::uint32_t { f16 = ESPN_DTYPE_F16, bf16 = ESPN_DTYPE_BF16 };
-enum class Kernel : std::uint32_t { automatic = ESPN_KERNEL_AUTO, tcgen05 = ESPN_KERNEL_TCGEN05, simt = ESPN_KERNEL_SIMT };
+enum class Kernel : std::uint32_t { automatic = ESPN_KERNEL_AUTO, tcgen05 = ESPN_KERNEL_TCGEN05, simt = ESPN_KERNEL_SIMT,
+                                        small = ESPN_KERNEL_SMALL };
 
 // Throws the espn:: exception class matching an espn_status (error.hpp:8-42).
 void throw_status(int status);

@@ -51,11 +51,16 @@ typedef enum {
 typedef enum { ESPN_DTYPE_F16 = 0, ESPN_DTYPE_BF16 = 1 } espn_dtype;
 
 /* MaxSim implementation selector (north_star: tcgen05 path plus a CUDA-core
- * path for tiny dims, chosen by measurement). */
+ * path for tiny dims, chosen by measurement).  SMALL: the whole re-rank of a
+ * small batch (<= 16 queries, scored lists <= 2048, final_k <= 32, table in
+ * HBM) in ONE launch on the CUDA cores -- bit-exact with the fp32-query
+ * reference; AUTO picks it for batches of at most 4096 scored pairs (the
+ * latency-bound configs[0] shape) unless a persistent server runs. */
 typedef enum {
   ESPN_KERNEL_AUTO = 0,
   ESPN_KERNEL_TCGEN05 = 1,
-  ESPN_KERNEL_SIMT = 2
+  ESPN_KERNEL_SIMT = 2,
+  ESPN_KERNEL_SMALL = 3
 } espn_kernel;
 
 typedef struct espn_gpu_table espn_gpu_table;
@@ -221,7 +226,7 @@ typedef struct {
   float* scores;        /* B * final_k */
   uint32_t* counts;     /* B: entries written for each query */
   float* bow_scores;    /* optional (WRITE_BOW): cand_offsets[B] MaxSim scores; entries of
-                           candidates beyond R are left untouched */
+                           candidates beyond the needed prefix (R) are 0 */
   espn_fetch_stats* fetch_stats; /* optional HOST array of B (synchronous calls) */
 } espn_rerank_out;
 

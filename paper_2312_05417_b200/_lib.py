@@ -26,6 +26,7 @@ ESPN_DTYPE_BF16 = 1
 ESPN_KERNEL_AUTO = 0
 ESPN_KERNEL_TCGEN05 = 1
 ESPN_KERNEL_SIMT = 2
+ESPN_KERNEL_SMALL = 3
 
 ESPN_TABLE_DEVICE_BORROWED = 0x1
 ESPN_TABLE_ROWS_TILED = 0x2

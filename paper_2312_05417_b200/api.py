@@ -277,7 +277,8 @@ def _ptr(a) -> Optional[int]:
 
 _DTYPES = {"f16": L.ESPN_DTYPE_F16, "fp16": L.ESPN_DTYPE_F16, "bf16": L.ESPN_DTYPE_BF16}
 _QPREC = {"auto": 0, "split": L.ESPN_RERANK_QUERY_SPLIT, "rounded": L.ESPN_RERANK_QUERY_ROUNDED}
-_KERNELS = {"auto": L.ESPN_KERNEL_AUTO, "tcgen05": L.ESPN_KERNEL_TCGEN05, "simt": L.ESPN_KERNEL_SIMT}
+_KERNELS = {"auto": L.ESPN_KERNEL_AUTO, "tcgen05": L.ESPN_KERNEL_TCGEN05, "simt": L.ESPN_KERNEL_SIMT,
+            "small": L.ESPN_KERNEL_SMALL}
 
 
 class GpuStore:

@@ -22,6 +22,7 @@
 #include "kernels_misc.cuh"
 #include "maxsim_tc.cuh"
 #include "shard.cuh"
+#include "small.cuh"
 
 using namespace espn_k;
 
@@ -352,6 +353,8 @@ struct espn_gpu_workspace {
   uint32_t* ff_seen = nullptr;             // 2 x B
   uint32_t* fused_state = nullptr;         // {epoch, rows used by parity 0, parity 1}
   uint32_t hash_slots = 0;
+  uint32_t* small_arrive = nullptr;        // single-launch small batches: per-query arrival counters
+  unsigned long long* small_top = nullptr; // ... and per-CTA best-k lists (kSmallMaxCtas x kFusedMaxK)
   unsigned long long* kprof = nullptr;  // device-timed MaxSim {sum_ns, launches, start, done}
   // tiered tables: two staging slots (one scoring, one being prefetched)
   struct Stage {
@@ -1208,6 +1211,11 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     if (e == cudaSuccess) e = cudaMemset(w->fused_state, 0, 4 * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(w->dedup, 0xFF, 2 * B * (size_t)w->hash_slots * sizeof(uint32_t));
   }
+  // single-launch small batches (ESPN_KERNEL_SMALL): arrival counters (zero
+  // between batches; each query's last CTA resets its own) and per-CTA lists
+  al((void**)&w->small_arrive, kSmallMaxB * sizeof(uint32_t));
+  al((void**)&w->small_top, (size_t)kSmallMaxCtas * kFusedMaxK * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(w->small_arrive, 0, kSmallMaxB * sizeof(uint32_t));
   al((void**)&w->bow, C * sizeof(float));
   // outputs and the error word in ONE allocation: [err 16 B | ids | scores |
   // counts], so a synchronous call reads everything back with one copy
@@ -1275,6 +1283,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   cudaFree(w->done_flag);
   cudaFree(w->plan_done);
   cudaFree(w->unit_top); cudaFree(w->dedup); cudaFree(w->ff_seen); cudaFree(w->fused_state);
+  cudaFree(w->small_arrive); cudaFree(w->small_top);
   for (auto& st : w->stage) {
     if (st.done) cudaEventSynchronize(st.done);
     if (st.free_ev) cudaEventSynchronize(st.free_ev);
@@ -1356,6 +1365,17 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     const uint64_t per_sm = (ub + t->num_sms - 1) / t->num_sms;
     unit_docs = (int)std::max<uint64_t>(kMinUnitDocs, std::min<uint64_t>((uint64_t)unit_docs, per_sm));
   }
+  // single-launch small batches (K5, small.cuh): a few queries, short lists,
+  // fused-size k, table in HBM; AUTO takes it for <= 4096 scored pairs
+  const bool small_ok = k <= (uint32_t)kFusedMaxK && !t->tiered && simt_supported(t->d) && B <= (uint32_t)kSmallMaxB &&
+                        max_list <= (uint64_t)kSmallMaxList && !(a->flags & ESPN_RERANK_PREFETCHED);
+  if (kern == ESPN_KERNEL_AUTO && small_ok && !t->server && (uint64_t)B * max_list <= 4096) kern = ESPN_KERNEL_SMALL;
+  if (kern == ESPN_KERNEL_SMALL && !small_ok)
+    return fail(ESPN_E_INVALID_CONFIG, "single-launch small batches need n_queries <= 16, scored lists <= 2048, "
+                                       "final_k <= 32, an HBM-resident table and d in {8,16,32,48,64,96,128}");
+  const bool small = kern == ESPN_KERNEL_SMALL;
+  const uint32_t small_P = small ? small_ctas_per_query(max_list, B) : 0u;
+  if (small) unit_docs = (int)small_P;  // (graph key: the grid shape)
   if (kern == ESPN_KERNEL_AUTO) kern = (tc_supported(t->d) && unit_docs > 0) ? ESPN_KERNEL_TCGEN05 : ESPN_KERNEL_SIMT;
   if (kern == ESPN_KERNEL_TCGEN05 && (!t->tc_ok || !tc_supported(t->d) || unit_docs <= 0))
     return fail(ESPN_E_INVALID_CONFIG, "tcgen05 MaxSim needs an sm_100 device, d in {16,32,64,128} and docs of at most " +
@@ -1504,7 +1524,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
         }
       w->counters.batches += 1;
       w->counters.queries += B;
-      w->counters.kernel_launches += served ? 2 : 3;
+      w->counters.kernel_launches += small ? 1 : served ? 2 : 3;
       return err_bits_to_status(*w->h_err);
     }
     if (capture) {
@@ -1567,6 +1587,10 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   // the device error word is sticky across un-synced ASYNC batches; it is
   // read and cleared by the synchronising call (or espn_gpu_workspace_sync)
 
+  // bow scores are defined for the needed prefix of each list only: the rest
+  // of the returned array reads as 0 (not as the previous batch's values)
+  if ((a->flags & ESPN_RERANK_WRITE_BOW) && o->bow_scores && C)
+    ESPN_CUDA_TRY(cudaMemsetAsync(w->bow, 0, C * sizeof(float), s));
   // ---- MaxSim parameters (also the server's batch descriptor) ----
   MaxSimParams mp{};
   mp.rows = t->rows;
@@ -1608,133 +1632,157 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     mp.hash_slots = w->hash_slots;
     mp.max_queries = w->max_queries;
   }
-  // ---- K0: batch plan on the device ----
-  PlanParams pp{};
-  pp.cand_off = cand_off;
-  pp.needed_in = needed_in;
-  pp.needed = w->needed;
-  pp.unit_off = w->unit_off;
-  pp.unit_tab = w->unit_tab;
-  pp.n_units = w->n_units;
-  pp.err = w->err;
-  pp.max_candidates = w->max_candidates;
-  pp.max_units = tc ? w->max_units : ~0ull;
-  pp.n_queries = B;
-  pp.rerank_count = a->rerank_count;
-  pp.unit_docs = tc ? (uint32_t)unit_docs : 1u;
-  pp.write_tab = tc ? 1u : 0u;
-  pp.tail_units = (fused && partial) ? 1u : 0u;
-  pp.out_counts = fused ? out_counts_k : nullptr;
-  pp.fused_state = fused ? w->fused_state : nullptr;
-  pp.base_ok = (dev_off && (a->flags & kFlagBaseOffsets)) ? 1u : 0u;
-  pp.dbg = dbg;
-  ServerSubmit sb{};
-  if (served) {
-    sb.server = t->server;
-    sb.plan_done = w->plan_done;
-    sb.msp = mp;
-  }
-  if (served)
-    plan_kernel<16><<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp, sb);
-  else
-    plan_kernel<1><<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp, sb);
-  ESPN_CUDA_TRY(cudaGetLastError());
-
-  // ---- tiered table: host-tier rows staged into HBM (prefetched or now) ----
   int slot = -1;
   bool hint_consumed = false;
-  if (t->tiered) {
-    if (a->flags & ESPN_RERANK_PREFETCHED) {
-      if (w->pf_count == 0) return fail(ESPN_E_INVALID_STATE, "PREFETCHED batch without a pending espn_gpu_prefetch");
-      slot = w->pf_q[0];
-      w->pf_q[0] = w->pf_q[1];
-      --w->pf_count;
-      ESPN_CUDA_TRY(cudaStreamWaitEvent(s, w->stage[slot].done, 0));
-      if (w->stage[slot].hint_epoch) {  // doc-keyed hints: resolve this batch's needed rows now
-        hint_consumed = true;
+  if (small) {
+    // ---- K5: the whole batch in one launch ----
+    SmallParams sp{};
+    sp.m = mp;
+    sp.m.cand_cls = cls;
+    sp.m.alpha = a->alpha;
+    sp.m.k = k;
+    sp.m.out_ids = out_ids_k;
+    sp.m.out_scores = out_scores_k;
+    sp.m.out_counts = out_counts_k;
+    sp.m.unit_top = w->small_top;
+    sp.m.prof = profile_dev ? w->kprof : nullptr;
+    sp.needed_in = needed_in;
+    sp.max_candidates = w->max_candidates;
+    sp.partial = partial ? 1u : 0u;
+    sp.P = small_P;
+    sp.base_ok = (dev_off && (a->flags & kFlagBaseOffsets)) ? 1u : 0u;
+    sp.arrive = w->small_arrive;
+    if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
+    const cudaError_t se = launch_small_rt(t->d, sp, B, s);
+    if (se != cudaSuccess) return fail(ESPN_E_CUDA, std::string("small-batch launch: ") + cudaGetErrorString(se));
+    if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[1], s));
+  } else {
+    // ---- K0: batch plan on the device ----
+    PlanParams pp{};
+    pp.cand_off = cand_off;
+    pp.needed_in = needed_in;
+    pp.needed = w->needed;
+    pp.unit_off = w->unit_off;
+    pp.unit_tab = w->unit_tab;
+    pp.n_units = w->n_units;
+    pp.err = w->err;
+    pp.max_candidates = w->max_candidates;
+    pp.max_units = tc ? w->max_units : ~0ull;
+    pp.n_queries = B;
+    pp.rerank_count = a->rerank_count;
+    pp.unit_docs = tc ? (uint32_t)unit_docs : 1u;
+    pp.write_tab = tc ? 1u : 0u;
+    pp.tail_units = (fused && partial) ? 1u : 0u;
+    pp.out_counts = fused ? out_counts_k : nullptr;
+    pp.fused_state = fused ? w->fused_state : nullptr;
+    pp.base_ok = (dev_off && (a->flags & kFlagBaseOffsets)) ? 1u : 0u;
+    pp.dbg = dbg;
+    ServerSubmit sb{};
+    if (served) {
+      sb.server = t->server;
+      sb.plan_done = w->plan_done;
+      sb.msp = mp;
+    }
+    if (served)
+      plan_kernel<16><<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp, sb);
+    else
+      plan_kernel<1><<<(B + kPlanThreads - 1) / kPlanThreads, kPlanThreads, 0, s>>>(pp, sb);
+    ESPN_CUDA_TRY(cudaGetLastError());
+
+    // ---- tiered table: host-tier rows staged into HBM (prefetched or now) ----
+    if (t->tiered) {
+      if (a->flags & ESPN_RERANK_PREFETCHED) {
+        if (w->pf_count == 0) return fail(ESPN_E_INVALID_STATE, "PREFETCHED batch without a pending espn_gpu_prefetch");
+        slot = w->pf_q[0];
+        w->pf_q[0] = w->pf_q[1];
+        --w->pf_count;
+        ESPN_CUDA_TRY(cudaStreamWaitEvent(s, w->stage[slot].done, 0));
+        if (w->stage[slot].hint_epoch) {  // doc-keyed hints: resolve this batch's needed rows now
+          hint_consumed = true;
+          const int ss = launch_stage(t, w, slot, cand_off, needed_in, ids, B, a->rerank_count, s, false);
+          w->stage[slot].hint_epoch = 0;
+          if (ss) return ss;
+        }
+      } else {
+        slot = take_free_slot(w);
+        if (slot < 0) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
         const int ss = launch_stage(t, w, slot, cand_off, needed_in, ids, B, a->rerank_count, s, false);
-        w->stage[slot].hint_epoch = 0;
         if (ss) return ss;
       }
-    } else {
-      slot = take_free_slot(w);
-      if (slot < 0) return fail(ESPN_E_INVALID_STATE, "both staging slots hold pending prefetches");
-      const int ss = launch_stage(t, w, slot, cand_off, needed_in, ids, B, a->rerank_count, s, false);
-      if (ss) return ss;
     }
-  }
 
-  mp.cand_src = slot >= 0 ? w->stage[slot].cand_src : nullptr;
-  w->last_slot = slot;
-  if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
-  cudaError_t e = served ? (server_wait_kernel<<<1, 32, 0, s>>>(w->done_flag, w->err, kServerWaitNs), cudaGetLastError())
-                  : tc   ? launch_tc_rt(t->d, qsplit, mp, t->num_sms, s, /*pdl=*/slot < 0 && !profile)
-                         : launch_simt_rt(t->d, mp, t->num_sms, s);
-  if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
-  if (slot >= 0) {  // the slot may be re-staged once this MaxSim finished
-    ESPN_CUDA_TRY(cudaEventRecord(w->stage[slot].free_ev, s));
-    w->stage[slot].used = true;
-  }
-  if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[1], s));
+    mp.cand_src = slot >= 0 ? w->stage[slot].cand_src : nullptr;
+    w->last_slot = slot;
+    if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
+    cudaError_t e = served ? (server_wait_kernel<<<1, 32, 0, s>>>(w->done_flag, w->err, kServerWaitNs), cudaGetLastError())
+                    : tc   ? launch_tc_rt(t->d, qsplit, mp, t->num_sms, s, /*pdl=*/slot < 0 && !profile)
+                           : launch_simt_rt(t->d, mp, t->num_sms, s);
+    if (e != cudaSuccess) return fail(ESPN_E_CUDA, std::string("MaxSim launch: ") + cudaGetErrorString(e));
+    if (slot >= 0) {  // the slot may be re-staged once this MaxSim finished
+      ESPN_CUDA_TRY(cudaEventRecord(w->stage[slot].free_ev, s));
+      w->stage[slot].used = true;
+    }
+    if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[1], s));
 
-  if (fused && !served) {  // (served: the server's dedup warps merged the lists)
-    // ---- K3': merge of the per-unit top-k lists (programmatic dependent) ----
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3((B + kFinalizeWarps - 1) / kFinalizeWarps);
-    lc.blockDim = dim3(kFinalizeWarps * 32);
-    lc.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = at;
-    lc.numAttrs = (dbg & 0x10000u) ? 1 : 0;  // plain launch: as a programmatic dependent its CTAs
-                                             // crowd onto the first SMs MaxSim frees
-    ESPN_CUDA_TRY(cudaLaunchKernelEx(&lc, finalize_kernel, mp));
-  }
-
-  // ---- K3: aggregate + top-k (unless fused into MaxSim) ----
-  if (!fused) {
-  ESPN_CUDA_TRY(ensure_topk_attr());
-  TopKParams tp{};
-  tp.bow = w->bow;
-  tp.cand_ids = ids;
-  tp.cand_cls = cls;
-  tp.cand_off = cand_off;
-  tp.needed = w->needed;
-  tp.out_ids = out_ids_k;
-  tp.out_scores = out_scores_k;
-  tp.out_counts = out_counts_k;
-  tp.err = w->err;
-  tp.n_queries = B;
-  tp.rerank_count = a->rerank_count;
-  tp.k = k;
-  tp.partial = partial ? 1u : 0u;
-  tp.alpha = a->alpha;
-  tp.dbg = dbg;
-  {
-    // CTA-per-query fast path when final_k <= 32 and the dedup hash fits;
-    // launched as a programmatic dependent of MaxSim (its id-only dedup
-    // prologue overlaps the MaxSim tail)
-    const uint32_t hs = topk_hs;
-    if (k <= 32 && hs <= 8192) {
-      const size_t smem = (size_t)hs * 8 + 8 * 32 * 8;
+    if (fused && !served) {  // (served: the server's dedup warps merged the lists)
+      // ---- K3': merge of the per-unit top-k lists (programmatic dependent) ----
       cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3(B);
-      lc.blockDim = dim3(kTopkCtaThreads);
-      lc.dynamicSmemBytes = smem;
+      lc.gridDim = dim3((B + kFinalizeWarps - 1) / kFinalizeWarps);
+      lc.blockDim = dim3(kFinalizeWarps * 32);
       lc.stream = s;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[0].val.programmaticStreamSerializationAllowed = 1;
       lc.attrs = at;
-      lc.numAttrs = 1;
-      ESPN_CUDA_TRY(k <= 16 ? cudaLaunchKernelEx(&lc, topk_cta_kernel<16>, tp, hs)
-                            : cudaLaunchKernelEx(&lc, topk_cta_kernel<32>, tp, hs));
-    } else {
-      topk_kernel<<<B, kTopkThreads, topk_smem_bytes(), s>>>(tp);
-      ESPN_CUDA_TRY(cudaGetLastError());
+      lc.numAttrs = (dbg & 0x10000u) ? 1 : 0;  // plain launch: as a programmatic dependent its CTAs
+                                               // crowd onto the first SMs MaxSim frees
+      ESPN_CUDA_TRY(cudaLaunchKernelEx(&lc, finalize_kernel, mp));
     }
-  }
+
+    // ---- K3: aggregate + top-k (unless fused into MaxSim) ----
+    if (!fused) {
+    ESPN_CUDA_TRY(ensure_topk_attr());
+    TopKParams tp{};
+    tp.bow = w->bow;
+    tp.cand_ids = ids;
+    tp.cand_cls = cls;
+    tp.cand_off = cand_off;
+    tp.needed = w->needed;
+    tp.out_ids = out_ids_k;
+    tp.out_scores = out_scores_k;
+    tp.out_counts = out_counts_k;
+    tp.err = w->err;
+    tp.n_queries = B;
+    tp.rerank_count = a->rerank_count;
+    tp.k = k;
+    tp.partial = partial ? 1u : 0u;
+    tp.alpha = a->alpha;
+    tp.dbg = dbg;
+    {
+      // CTA-per-query fast path when final_k <= 32 and the dedup hash fits;
+      // launched as a programmatic dependent of MaxSim (its id-only dedup
+      // prologue overlaps the MaxSim tail)
+      const uint32_t hs = topk_hs;
+      if (k <= 32 && hs <= 8192) {
+        const size_t smem = (size_t)hs * 8 + 8 * 32 * 8;
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(B);
+        lc.blockDim = dim3(kTopkCtaThreads);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        ESPN_CUDA_TRY(k <= 16 ? cudaLaunchKernelEx(&lc, topk_cta_kernel<16>, tp, hs)
+                              : cudaLaunchKernelEx(&lc, topk_cta_kernel<32>, tp, hs));
+      } else {
+        topk_kernel<<<B, kTopkThreads, topk_smem_bytes(), s>>>(tp);
+        ESPN_CUDA_TRY(cudaGetLastError());
+      }
+    }
+    }
   }
   if (profile) {
     ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[2], s));
@@ -1766,7 +1814,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   }
   w->counters.batches += 1;
   w->counters.queries += B;
-  w->counters.kernel_launches += (served ? 2 : 3) + (t->tiered && (!(a->flags & ESPN_RERANK_PREFETCHED) || hint_consumed) ? 1 : 0);
+  w->counters.kernel_launches += small ? 1 : (served ? 2 : 3) + (t->tiered && (!(a->flags & ESPN_RERANK_PREFETCHED) || hint_consumed) ? 1 : 0);
   if (a->flags & ESPN_RERANK_ASYNC) {
     w->async_pending = true;
     return ESPN_OK;

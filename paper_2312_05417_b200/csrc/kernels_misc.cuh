@@ -409,33 +409,19 @@ topk_cta_kernel(const TopKParams p, uint32_t hash_slots) {
         if (j < n_scored) pend |= 1u << u;
         hpos[u] = ((idv[u] * 2654435761u) >> 7) & (hash_slots - 1);
       }
-      __syncthreads();  // table initialised / previous batch settled
-      for (;;) {
-        uint32_t wrote = 0;
+      if (j0 == 0) __syncthreads();  // table initialised
+      // one shared 64-bit CAS per probe: {id, position} claims an empty slot;
+      // a slot holding the same id is a duplicate
+      while (pend) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (pend & (1u << u)) {
-            const uint64_t e = hash[hpos[u]];
-            if (e == EMPTY) {
-              hash[hpos[u]] = ((uint64_t)idv[u] << 32) | (uint32_t)(j0 + u * kTopkCtaThreads + tid);
-              wrote |= 1u << u;
-            } else if ((uint32_t)(e >> 32) == idv[u]) {
-              dup = 1;
-              pend &= ~(1u << u);
-            } else {
-              hpos[u] = (hpos[u] + 1) & (hash_slots - 1);
-            }
-          }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (wrote & (1u << u)) {
             const uint64_t mine = ((uint64_t)idv[u] << 32) | (uint32_t)(j0 + u * kTopkCtaThreads + tid);
-            const uint64_t e = hash[hpos[u]];
-            if (e == mine) {
+            const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long*>(&hash[hpos[u]]),
+                                           (unsigned long long)EMPTY, (unsigned long long)mine);
+            if (old == EMPTY) {
               pend &= ~(1u << u);
-            } else if ((uint32_t)(e >> 32) == idv[u]) {
+            } else if ((uint32_t)(old >> 32) == idv[u]) {
               dup = 1;
               pend &= ~(1u << u);
             } else {
@@ -443,7 +429,6 @@ topk_cta_kernel(const TopKParams p, uint32_t hash_slots) {
             }
           }
         }
-        if (!__syncthreads_or(pend != 0)) break;
       }
     }
     if (dup) atomicOr(p.err, ERR_DUPLICATE);

@@ -2,13 +2,14 @@
 // d=32 fp16, 32 query tokens, top-1000 -> top-10), host buffers, synchronous
 // espn_gpu_rerank calls -- what a C++ serving loop sees per query, without the
 // Python layer the bench's e2e figure includes.
-//   g++ -O2 -std=c++17 -I include scratch/c1_latency.cpp -L paper_2312_05417_b200/lib -lespn_gpu \
+//   g++ -O2 -std=c++17 -I include tools/c1_latency.cpp -L paper_2312_05417_b200/lib -lespn_gpu \
 //       -L /usr/local/cuda/lib64 -lcudart -Wl,-rpath,$PWD/paper_2312_05417_b200/lib -o /tmp/c1_latency
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 #include <vector>
 
@@ -23,7 +24,9 @@
     }                                                                      \
   } while (0)
 
-int main() {
+// argv[1]: espn_kernel (0 auto, 1 tcgen05, 2 simt, 3 small)
+int main(int argc, char** argv) {
+  const uint32_t kern = argc > 1 ? (uint32_t)atoi(argv[1]) : ESPN_KERNEL_AUTO;
   const uint64_t N = 100000;
   const uint32_t d = 32, nq = 32, K = 1000, k = 10, reps = 3000;
   uint64_t* rp = nullptr;
@@ -85,7 +88,7 @@ int main() {
     a.rerank_count = K;
     a.final_k = k;
     a.alpha = 1.0f;
-    a.kernel = ESPN_KERNEL_AUTO;
+    a.kernel = kern;
     espn_rerank_out o{};
     o.ids = out_ids;
     o.scores = out_sc;
@@ -98,9 +101,9 @@ int main() {
   std::sort(lat.begin(), lat.end());
   double sum = 0;
   for (double x : lat) sum += x;
-  std::printf("{\"config\": \"configs[0] batch 1, host buffers, synchronous C-ABI calls\", \"calls\": %zu, "
+  std::printf("{\"config\": \"configs[0] batch 1, host buffers, synchronous C-ABI calls\", \"kernel\": %u, \"calls\": %zu, "
               "\"mean_us\": %.2f, \"p50_us\": %.2f, \"p99_us\": %.2f, \"queries_per_s\": %.0f}\n",
-              lat.size(), sum / lat.size(), lat[lat.size() / 2], lat[lat.size() * 99 / 100], lat.size() / (sum * 1e-6));
+              kern, lat.size(), sum / lat.size(), lat[lat.size() / 2], lat[lat.size() * 99 / 100], lat.size() / (sum * 1e-6));
   espn_gpu_workspace_destroy(w);
   espn_gpu_table_close(t);
   cudaFree(rows);
