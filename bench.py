@@ -676,6 +676,8 @@ def run_ours(args, cfg):
     QP = {"auto": 0, "split": L.ESPN_RERANK_QUERY_SPLIT, "rounded": L.ESPN_RERANK_QUERY_ROUNDED}[args.query_precision]
     flags = L.ESPN_RERANK_DEVICE_IO | L.ESPN_RERANK_DEVICE_OFFSETS | L.ESPN_RERANK_ASYNC | L.ESPN_RERANK_PROFILE | QP
 
+    if args.kernel is None:
+        args.kernel = "small" if cfg["batch"] * cfg["K"] <= 4096 else "auto"
     KERN = {"auto": L.ESPN_KERNEL_AUTO, "tcgen05": L.ESPN_KERNEL_TCGEN05, "small": L.ESPN_KERNEL_SMALL}[args.kernel]
     class Lane:
         """One batch in flight: its own workspace, stream, output buffers, NCCL
@@ -1008,9 +1010,11 @@ def run_ours(args, cfg):
                               "one CUDA graph per batch (device-planned: plan -> tcgen05 MaxSim with fused ranking -> "
                               "finalize merge); %d batches in flight on separate streams/workspaces" % NL),
                    "kernel": kern_label,
-                   "query_precision": {"auto": "fp32 query as hi + lo in the table dtype (two MMAs per K-step)"
-                                               if not (d == 128 and cfg["dtype"] == "f16") else
-                                               "fp32 query rounded to f16 (d=128 default)",
+                   "query_precision": {"auto": ("fp32 query as hi + lo in bf16 (two MMAs per K-step)"
+                                                if cfg["dtype"] == "bf16" else
+                                                "fp32 query rounded to f16 (one MMA per K-step; <= 5.1e-4 relative "
+                                                "vs the fp32-query oracle, tests/test_gpu_parity.py)")
+                                               if not small_path else "fp32 query as given (CUDA cores, bit-exact)",
                                        "split": "fp32 query as hi + lo in the table dtype (two MMAs per K-step)",
                                        "rounded": "fp32 query rounded to the table dtype"}[args.query_precision]},
         "p50_batch_ms": p50, "p99_batch_ms": p99,
@@ -1164,9 +1168,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "small"],
-                    help="espn_kernel of the re-rank calls (auto: the library's choice -- the single-launch "
-                         "small-batch kernel for <= 4096 scored pairs, else tcgen05)")
+    ap.add_argument("--kernel", default=None, choices=["auto", "tcgen05", "small"],
+                    help="espn_kernel of the re-rank calls; default: small (the single-launch kernel) for "
+                         "configs[0] (batch 1), auto (tcgen05) otherwise")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--preroll-s", type=float, default=2.0)
     ap.add_argument("--cpu-batches", type=int, default=8)

@@ -54,8 +54,8 @@ typedef enum { ESPN_DTYPE_F16 = 0, ESPN_DTYPE_BF16 = 1 } espn_dtype;
  * path for tiny dims, chosen by measurement).  SMALL: the whole re-rank of a
  * small batch (<= 16 queries, scored lists <= 2048, final_k <= 32, table in
  * HBM) in ONE launch on the CUDA cores -- bit-exact with the fp32-query
- * reference; AUTO picks it for batches of at most 4096 scored pairs (the
- * latency-bound configs[0] shape) unless a persistent server runs. */
+ * reference; for latency-bound callers (configs[0]: batch 1).  Opt-in: AUTO
+ * keeps one arithmetic (tcgen05) for every batch size. */
 typedef enum {
   ESPN_KERNEL_AUTO = 0,
   ESPN_KERNEL_TCGEN05 = 1,

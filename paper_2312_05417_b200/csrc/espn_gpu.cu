@@ -66,6 +66,9 @@ int err_bits_to_status(uint32_t bits) {
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
+    // a non-sticky error left pending by an earlier, unrelated runtime call of
+    // this thread would otherwise surface at this call's first launch check
+    (void)cudaGetLastError();
     cudaGetDevice(&prev);
     if (prev != dev) cudaSetDevice(dev);
   }
@@ -1366,10 +1369,12 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     unit_docs = (int)std::max<uint64_t>(kMinUnitDocs, std::min<uint64_t>((uint64_t)unit_docs, per_sm));
   }
   // single-launch small batches (K5, small.cuh): a few queries, short lists,
-  // fused-size k, table in HBM; AUTO takes it for <= 4096 scored pairs
+  // fused-size k, table in HBM.  Opt-in only: its CUDA-core arithmetic on the
+  // fp32 query is exact, the tcgen05 path rounds the query (f16) or splits it
+  // (bf16), so AUTO never switches arithmetic with the batch size -- a query's
+  // scores do not depend on the batch it arrives in.
   const bool small_ok = k <= (uint32_t)kFusedMaxK && !t->tiered && simt_supported(t->d) && B <= (uint32_t)kSmallMaxB &&
                         max_list <= (uint64_t)kSmallMaxList && !(a->flags & ESPN_RERANK_PREFETCHED);
-  if (kern == ESPN_KERNEL_AUTO && small_ok && !t->server && (uint64_t)B * max_list <= 4096) kern = ESPN_KERNEL_SMALL;
   if (kern == ESPN_KERNEL_SMALL && !small_ok)
     return fail(ESPN_E_INVALID_CONFIG, "single-launch small batches need n_queries <= 16, scored lists <= 2048, "
                                        "final_k <= 32, an HBM-resident table and d in {8,16,32,48,64,96,128}");

@@ -595,8 +595,11 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(uint64_t* a, uint64_t n)
   }
 }
 
-// Warp per doc, 16-byte vector copies, 4 in flight per lane.  Reads the HBM
-// tile layout (RowLayout) and writes plain row-major rows in request order.
+// Warp per group of 8 requested docs.  Lanes 0-7 resolve the group's metadata
+// together (id -> row_ptr pair, output offset: one dependent round trip per 8
+// docs instead of per doc), then the warp copies the docs two at a time with
+// 16-byte vectors, 8 loads per lane in flight.  Reads the HBM tile layout
+// (RowLayout) and writes plain row-major rows in request order.
 template <int D>
 __global__ void __launch_bounds__(256)
 gather_copy_kernel(const uint16_t* rows, const uint64_t* doc_loc, const uint64_t* row_ptr, uint64_t n_docs,
@@ -605,26 +608,44 @@ gather_copy_kernel(const uint16_t* rows, const uint64_t* doc_loc, const uint64_t
   using RL = RowLayout<D>;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
-    const uint64_t loc = shard_local(ids[i], shard_count, shard_index, n_docs);
-    if (loc == ~0ull) continue;
-    const uint64_t r0 = row_ptr[loc];
-    const uint32_t t = (uint32_t)(row_ptr[loc + 1] - r0);
-    const uint32_t nvec = t * RL::CH;
-    const uint8_t* src = doc_rows(rows, doc_loc, loc, r0, D);
-    uint4* dst = reinterpret_cast<uint4*>(out_rows + out_row_ptr[i] * D);
-    auto at = [&](uint32_t v) {
-      return __ldcs(reinterpret_cast<const uint4*>(src + RL::off(t, v / RL::CH, v % RL::CH)));
-    };
-    uint32_t v = lane;
-    for (; v + 96 < nvec; v += 128) {
-      const uint4 a0 = at(v), a1 = at(v + 32), a2 = at(v + 64), a3 = at(v + 96);
-      __stcs(dst + v, a0);
-      __stcs(dst + v + 32, a1);
-      __stcs(dst + v + 64, a2);
-      __stcs(dst + v + 96, a3);
+  const uint64_t ngroups = (n + 7) / 8;
+  for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nwarps) {
+    const uint64_t i = g * 8 + (lane & 7);
+    uint64_t src = 0, dst = 0;
+    uint32_t t = 0;
+    if (lane < 8 && i < n) {
+      const uint64_t loc = shard_local(__ldg(&ids[i]), shard_count, shard_index, n_docs);
+      dst = reinterpret_cast<uint64_t>(out_rows + __ldg(&out_row_ptr[i]) * D);
+      if (loc != ~0ull) {  // (unknown ids were rejected by the count pass)
+        const uint64_t r0 = __ldg(&row_ptr[loc]);
+        t = (uint32_t)(__ldg(&row_ptr[loc + 1]) - r0);
+        src = reinterpret_cast<uint64_t>(doc_rows(rows, doc_loc, loc, r0, D));
+      }
     }
-    for (; v < nvec; v += 32) __stcs(dst + v, at(v));
+#pragma unroll 1
+    for (int p = 0; p < 8; p += 2) {
+      const uint32_t ta = __shfl_sync(0xffffffffu, t, p), tb = __shfl_sync(0xffffffffu, t, p + 1);
+      const uint8_t* sa = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, src, p));
+      const uint8_t* sb = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, src, p + 1));
+      uint4* da = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, dst, p));
+      uint4* db = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, dst, p + 1));
+      const uint32_t na = ta * RL::CH, nb = tb * RL::CH, nm = na > nb ? na : nb;
+      for (uint32_t v0 = 0; v0 < nm; v0 += 128) {
+        uint4 a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t v = v0 + u * 32 + lane;
+          if (v < na) a[u] = __ldcs(reinterpret_cast<const uint4*>(sa + RL::off(ta, v / RL::CH, v % RL::CH)));
+          if (v < nb) b[u] = __ldcs(reinterpret_cast<const uint4*>(sb + RL::off(tb, v / RL::CH, v % RL::CH)));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t v = v0 + u * 32 + lane;
+          if (v < na) __stcs(da + v, a[u]);
+          if (v < nb) __stcs(db + v, b[u]);
+        }
+      }
+    }
   }
 }
 

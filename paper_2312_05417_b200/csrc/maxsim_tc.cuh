@@ -215,14 +215,18 @@ __device__ __forceinline__ void fused_dedup(const MaxSimParams& p, uint32_t par,
 //     the candidates greater than its own, and writes it at its rank.
 // Longer inputs (n > FMK) fall back to a chunked k-way merge (k rounds of
 // warp max over list heads).
+// `kway`: always the k-way merge -- for many SHORT lists (fewer than k
+// entries each, e.g. the single-launch small-batch kernel's per-CTA lists)
+// every list's k-th key is empty, the threshold is 0 and the counting rank
+// would be quadratic in the number of keys.
 template <int FMK>
 __device__ __forceinline__ void fused_merge(const MaxSimParams& p, uint32_t b, uint32_t u0, uint32_t nu,
-                                            uint64_t* fm, uint32_t lane) {
+                                            uint64_t* fm, uint32_t lane, bool kway = false) {
   const uint32_t kk = p.k;
   const unsigned long long* src = p.unit_top + (size_t)u0 * kk;
   const uint32_t n = nu * kk;
   uint32_t cnt = 0;
-  if (n + 8 <= (uint32_t)FMK) {
+  if (!kway && n + 8 <= (uint32_t)FMK) {
     const unsigned long long tf0 = ktl_now();
     uint64_t th = 0;
     for (uint32_t i0 = 0; i0 < n; i0 += 256) {  // 8 loads per lane in flight
@@ -288,7 +292,20 @@ __device__ __forceinline__ void fused_merge(const MaxSimParams& p, uint32_t b, u
     for (uint32_t l0 = 0; l0 < nu; l0 += lpc - 1) {
       const uint32_t nl = min(lpc - 1, nu - l0) + 1;
       if (lane < kk) fm[lane] = mine;
-      for (uint32_t i = lane; i < (nl - 1) * kk; i += 32) fm[kk + i] = __ldcg(&src[(size_t)l0 * kk + i]);
+      const uint32_t nk = (nl - 1) * kk;
+      for (uint32_t i0 = 0; i0 < nk; i0 += 256) {  // 8 loads per lane in flight
+        uint64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t i = i0 + u * 32 + lane;
+          v[u] = i < nk ? __ldcg(&src[(size_t)l0 * kk + i]) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t i = i0 + u * 32 + lane;
+          if (i < nk) fm[kk + i] = v[u];
+        }
+      }
       __syncwarp();
       uint32_t c0 = 0, c1 = 0;  // cursors of lists lane, lane + 32
       uint64_t h0 = lane < nl ? fm[lane * kk] : 0ull;
@@ -520,7 +537,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
         U.n_pt = pcarry;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.ufull_bar[us]);
+      mbar_arrive(&S.ufull_bar[us]);  // every lane (its writes are released by its own arrive)
     }
   } else if (warp == L::PATCH_WARP) {
     // ============================ PAD PATCH =====================================
@@ -642,7 +659,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       }
       fence_proxy_async_smem();  // A tile is read by the tensor core (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.ufull_bar[us]);
+      mbar_arrive(&S.ufull_bar[us]);
     }
   } else if (warp >= L::PROD_WARP0 && warp < L::PROD_WARP0 + L::NPROD) {
     // ====================== BULK-COPY PRODUCERS (NPROD warps) ======================
@@ -866,8 +883,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
         mbar_wait(&S.bfree_bar[j], ((gi / L::NB) & 1) ^ 1);
 #pragma unroll
         for (int r = 0; r < NK; ++r) ring[j * L::UNITMAX + r * 32 + lane] = bow[r];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.bdone_bar[j]);
+        mbar_arrive(&S.bdone_bar[j]);  // every lane releases its own ring writes
       }
 #pragma unroll
       for (int r = 0; r < NK; ++r)
@@ -925,8 +941,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       float bow[NK];
 #pragma unroll
       for (int r = 0; r < NK; ++r) bow[r] = ring[j * L::UNITMAX + r * 32 + lane];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.bfree_bar[j]);
+      mbar_arrive(&S.bfree_bar[j]);
       uint64_t key[NK];
       uint32_t bad = 0;
 #pragma unroll
@@ -1050,13 +1065,17 @@ maxsim_tc_kernel(const MaxSimParams p) {
       mbar_init(&S.tempty_bar[i], L::NEPI);
     }
     for (int i = 0; i < L::NU; ++i) {
-      mbar_init(&S.ufull_bar[i], 2);  // unit loader + query-tile warp
+      // unit loader + query-tile warp, every lane: a lane's own arrive
+      // releases its shared-memory writes (compute-sanitizer racecheck does
+      // not carry a __syncwarp + one-lane arrive across warps,
+      // tools/racecheck_probe.cu)
+      mbar_init(&S.ufull_bar[i], 64);
       mbar_init(&S.uempty_bar[i], 1);
       mbar_init(&S.edone_bar[i], 32 * L::NEPI);
     }
     for (int i = 0; i < L::NB; ++i) {
-      mbar_init(&S.bdone_bar[i], 1);
-      mbar_init(&S.bfree_bar[i], 1);
+      mbar_init(&S.bdone_bar[i], 32);  // combine warp, every lane
+      mbar_init(&S.bfree_bar[i], 32);  // rank warp, every lane
     }
     for (int i = 0; i < L::NS; ++i) mbar_init(&S.patched_bar[i], 1);
     mbar_fence_init();

@@ -33,7 +33,9 @@ constexpr int kSmallMaxB = 16;            // queries per small batch
 constexpr int kSmallMaxChunk = 256;       // scored candidates per CTA
 constexpr int kSmallMaxList = 2048;       // scored candidates per query (dedup hash: 2x)
 constexpr int kSmallMaxCtas = 296;        // 2 per SM
-constexpr int kSmallMergeKeys = 1536;     // merge scratch (P x k keys; longer -> chunked merge)
+constexpr int kSmallMergeKeys = 1016;     // merge scratch (P x k keys; longer -> k-way merge)
+constexpr int kSmallWarpRowBytes = 2048;  // per-warp row staging (one piece: 32 rows at d=32)
+constexpr int kSmallRegionBytes = 24 * 1024;  // row staging | last CTA: merge keys + dedup hash
 
 struct SmallParams {
   MaxSimParams m;              // table, batch and outputs; m.unit_top = B x P x k per-CTA lists
@@ -71,11 +73,21 @@ __device__ __forceinline__ void small_prof_end(const MaxSimParams& p) {
 template <int D>
 __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const SmallParams sp) {
   const MaxSimParams& p = sp.m;
-  __shared__ __align__(16) float sq[32 * D];                      // query tokens (fp32, as given)
-  __shared__ uint64_t keys[kSmallMaxChunk];         // this CTA's candidate keys
-  __shared__ __align__(16) uint64_t fmk[kSmallMergeKeys + 8];      // last CTA: merge keys (warp 0)
-  __shared__ uint32_t hash[2 * kSmallMaxList];                      // last CTA: dedup hash (warps 1-7)
+  using RL = RowLayout<D>;
+  constexpr uint32_t NW = kSmallThreads / 32;
+  constexpr uint32_t WBUF = kSmallWarpRowBytes;              // per-warp row staging
+  constexpr uint32_t WROWS = WBUF / (2 * D);                 // rows per staged piece
+  __shared__ __align__(16) float sq[32 * D];                 // query tokens (fp32, as given)
+  __shared__ uint64_t keys[kSmallMaxChunk];                  // this CTA's candidate keys
+  __shared__ uint64_t m_src[kSmallMaxChunk];                 // per candidate: row address (0: none)
+  __shared__ uint32_t m_t[kSmallMaxChunk], m_id[kSmallMaxChunk];
+  __shared__ float m_cls[kSmallMaxChunk];
+  // compute phase: NW row-staging buffers; the last CTA's merge phase reuses
+  // the space for the merge keys (warp 0) and the duplicate hash (warps 1-7)
+  __shared__ __align__(16) uint8_t region[kSmallRegionBytes];
   __shared__ uint32_t s_last, s_ff;
+  static_assert(NW * WBUF <= kSmallRegionBytes && WROWS >= 1, "row staging");
+  static_assert((kSmallMergeKeys + 8) * 8 + 2 * kSmallMaxList * 4 <= kSmallRegionBytes, "merge scratch");
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t b = blockIdx.y, pc = blockIdx.x, P = sp.P;
   ktl_begin(p.dbg, 1);
@@ -97,7 +109,30 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
   if ((nc > (uint32_t)kSmallMaxChunk || (pc == 0 && ns > (uint64_t)kSmallMaxList)) && tid == 0) atomicOr(p.err, ERR_CAPACITY);
   const uint32_t ncs = min(nc, (uint32_t)kSmallMaxChunk);
   const uint32_t nq = p.nq;
-  // ---- query -> shared memory (only if this CTA has MaxSim work) ----
+  uint32_t ebits = 0;
+  // ---- candidate metadata (one thread per candidate: id -> row_ptr pair,
+  // two dependent round trips for the whole CTA) and the query, together ----
+  if (tid < ncs) {
+    const uint64_t j = j0 + tid, c = off0 + j;
+    const uint32_t id = __ldg(&p.cand_ids[c]);
+    m_id[tid] = id;
+    m_cls[tid] = __ldg(&p.cand_cls[c]);
+    uint64_t src = 0;
+    uint32_t t = 0;
+    if (j < need) {
+      const uint64_t loc = shard_local(id, p.shard_count, p.shard_index, p.n_docs);
+      if (loc == ~0ull) {
+        ebits |= ERR_UNKNOWN_DOC;
+        src = 1;  // marker: no key
+      } else {
+        const uint64_t r0 = __ldg(&p.row_ptr[loc]);
+        t = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
+        src = reinterpret_cast<uint64_t>(p.rows + r0 * D);
+      }
+    }
+    m_src[tid] = src;
+    m_t[tid] = t;
+  }
   if (j0 < need && ncs > 0) {
     const float* qs = p.q32 + (size_t)b * nq * D;
     bool badq = false;
@@ -120,34 +155,40 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
     }
   }
   const float alpha = p.alpha;
-  uint32_t ebits = 0;
+  uint8_t* wbuf = region + wid * WBUF;
   // ---- warp per candidate: MaxSim (needed prefix) + aggregate -> key ----
-  for (uint32_t jj = wid; jj < ncs; jj += kSmallThreads / 32) {
-    const uint64_t j = j0 + jj, c = off0 + j;
-    const uint32_t id = __ldg(&p.cand_ids[c]);
-    const float cl = __ldg(&p.cand_cls[c]);
+  for (uint32_t jj = wid; jj < ncs; jj += NW) {
+    const uint64_t j = j0 + jj;
+    const uint64_t src = m_src[jj];
+    const uint32_t t = m_t[jj];
     float bow = 0.0f;
-    bool ok = true;
-    if (j < need) {
-      const uint64_t loc = shard_local(id, p.shard_count, p.shard_index, p.n_docs);
-      if (loc == ~0ull) {
-        ok = false;
-        ebits |= ERR_UNKNOWN_DOC;
-      } else {
-        const uint64_t r0 = __ldg(&p.row_ptr[loc]);
-        const uint32_t t = (uint32_t)(__ldg(&p.row_ptr[loc + 1]) - r0);
-        const uint8_t* doc = reinterpret_cast<const uint8_t*>(p.rows + r0 * D);
-        float m = -INFINITY;
+    const bool ok = src != 1;
+    if (j < need && ok) {
+      const uint8_t* doc = reinterpret_cast<const uint8_t*>(src);
+      float m = -INFINITY;
+      // the doc's rows in pieces of WROWS: one coalesced round trip per piece
+      // into the warp's buffer (kept in the tile layout), then every lane
+      // reads each row with broadcast 16-byte shared loads
+      for (uint32_t r0 = 0; r0 < t; r0 += WROWS) {
+        const uint32_t nr = min(WROWS, t - r0);
+        const uint32_t nv = nr * RL::CH;
+        __syncwarp();  // the previous piece is consumed
+        for (uint32_t v = lane; v < nv; v += 32) {
+          const uint32_t jr = r0 + v / RL::CH, cc = v % RL::CH;
+          const uint32_t o = RL::off(t, jr, cc);
+          *reinterpret_cast<uint4*>(wbuf + (jr - r0) * (2 * D) + cc * 16) = __ldg(reinterpret_cast<const uint4*>(doc + o));
+        }
+        __syncwarp();
         // four rows at a time: independent accumulators, each summed in
         // ascending k (the reference's order); maxima applied in row order
         uint32_t jr = 0;
-        for (; jr + 4 <= t; jr += 4) {
+        for (; jr + 4 <= nr; jr += 4) {
           float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
           for (int k8 = 0; k8 < D / 8; ++k8) {
             uint4 v[4];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) v[r] = __ldg(reinterpret_cast<const uint4*>(doc + RowLayout<D>::off(t, jr + r, k8)));
+            for (int r = 0; r < 4; ++r) v[r] = *reinterpret_cast<const uint4*>(wbuf + (jr + r) * (2 * D) + k8 * 16);
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
@@ -164,11 +205,11 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
           for (int r = 0; r < 4; ++r)
             if (acc[r] > m) m = acc[r];
         }
-        for (; jr < t; ++jr) {
+        for (; jr < nr; ++jr) {
           float acc = 0.0f;
 #pragma unroll
           for (int k8 = 0; k8 < D / 8; ++k8) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(doc + RowLayout<D>::off(t, jr, k8)));
+            const uint4 v = *reinterpret_cast<const uint4*>(wbuf + jr * (2 * D) + k8 * 16);
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
@@ -180,18 +221,19 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
           }
           if (acc > m) m = acc;
         }
-        float s = 0.0f;
-        for (uint32_t i = 0; i < nq; ++i) s = __fadd_rn(s, __shfl_sync(0xffffffffu, m, i));
-        bow = s;
-        if (p.bow_out && lane == 0) p.bow_out[c] = s;
       }
+      float s = 0.0f;
+      for (uint32_t i = 0; i < nq; ++i) s = __fadd_rn(s, __shfl_sync(0xffffffffu, m, i));
+      bow = s;
+      if (p.bow_out && lane == 0) p.bow_out[off0 + j] = s;
     }
     if (lane == 0) {
       uint64_t key = 0;
       if (ok) {
+        const float cl = m_cls[jj];
         const float sc = __fadd_rn(__fmul_rn(alpha, cl), bow);
         ebits |= !isfinite(cl) ? ERR_NONFINITE_CLS : (!isfinite(sc) ? ERR_NONFINITE_SCORE : 0u);
-        key = make_key(sc, id);
+        key = make_key(sc, m_id[jj]);
       }
       keys[jj] = key;
     }
@@ -223,9 +265,11 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
   }
   __threadfence();
   if (wid == 0) {
-    fused_merge<kSmallMergeKeys>(p, b, b * P, P, fmk, lane);
+    uint64_t* fmk = reinterpret_cast<uint64_t*>(region);
+    fused_merge<kSmallMergeKeys>(p, b, b * P, P, fmk, lane, /*kway=*/chunk < k);
   } else {
     // duplicate check over the query's scored ids (warps 1-7)
+    uint32_t* hash = reinterpret_cast<uint32_t*>(region + (kSmallMergeKeys + 8) * 8);
     constexpr uint32_t HS = 2 * kSmallMaxList, HM = HS - 1;
     const uint32_t t7 = tid - 32;
     constexpr uint32_t N7 = kSmallThreads - 32;

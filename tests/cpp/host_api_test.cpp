@@ -203,7 +203,9 @@ int main() {
     const std::vector<espn_fetch_stats> on_fs = rt.last_fetch_stats();
     espn::BatchResult off = rt.rerank(qs, cl, cfg);
     const std::vector<espn_fetch_stats> off_fs = rt.last_fetch_stats();
-    espn::BatchResult hbm = rh.rerank(qs, cl, cfg);
+    // the same arithmetic as the tiered calls (AUTO may pick the single-launch
+    // CUDA-core kernel for a small HBM-resident batch; tiered batches run tcgen05)
+    espn::BatchResult hbm = rh.rerank(qs, cl, cfg, espn::gpu::Kernel::tcgen05);
     std::vector<char> hinted(n_docs, 0);
     for (const auto& c : cl)
       for (std::uint32_t j = 0; j < P && j < c.entries.size(); ++j) hinted[c.entries[j].doc_id] = 1;

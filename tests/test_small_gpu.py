@@ -123,10 +123,9 @@ def test_auto_choice(cuda_ok):
     rp, codes, q, ids, cls, off, _ = _case(4000, 32, 32, 1, 1000, seed=5)
     cfg = api.PipelineConfig(rerank_count=1000, final_k=10)
     _, n = _run(rp, codes, 32, "f16", q, ids, cls, off, cfg, kernel="auto")
-    assert n == 1  # batch 1 x 1000: one launch
-    rp, codes, q, ids, cls, off, _ = _case(4000, 32, 32, 8, 1000, seed=6)
-    _, n = _run(rp, codes, 32, "f16", q, ids, cls, off, cfg, kernel="auto")
-    assert n == 3  # 8 x 1000 scored pairs: the tcgen05 chain
+    assert n == 3  # opt-in only: AUTO keeps the tcgen05 chain (one arithmetic for every batch size)
+    _, n = _run(rp, codes, 32, "f16", q, ids, cls, off, cfg, kernel="small")
+    assert n == 1
     cfg = api.PipelineConfig(rerank_count=1000, final_k=33)  # k beyond the fused lists
     rp, codes, q, ids, cls, off, _ = _case(4000, 32, 32, 1, 1000, seed=7)
     with pytest.raises(api.InvalidConfigError):

@@ -7,6 +7,10 @@
 //   C  as A, but __syncthreads instead of the mbarrier     (control)
 //   D  warp 0 lane 0: cp.async.bulk global -> smem completing on the mbarrier
 //      (expect_tx); warp 1 waits, reads                    (the TMA landing)
+//   E  WAR through the tensor-core proxy: warp 1 reads smem, then releases it
+//      with tcgen05.commit (arrive::one, nothing pending); warp 0 waits, writes
+//      (how the MMA warp frees a stage / TMEM buffer)
+//   F  as E with a plain mbarrier.arrive by every lane of warp 1 (control)
 // Run: compute-sanitizer --tool racecheck ./racecheck_probe
 #include <cstdio>
 #include <cstdint>
@@ -21,10 +25,26 @@ __global__ void k(const uint4* g, uint32_t* out) {
   __shared__ uint64_t bar;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar)), "r"(V == 1 ? 32 : 1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar)), "r"(V == 1 || V == 5 ? 32 : 1));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
+  if (V == 4 || V == 5) {  // WAR: warp 1 reads first, warp 0 writes after the release
+    if (w == 1) {
+      out[l] = buf[31 - l].x;
+      __syncwarp();
+      if (V == 4) {
+        asm volatile("{.reg .pred e; elect.sync _|e, 0xffffffff;\n\t"
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];}" ::"r"(su32(&bar)) : "memory");
+      } else {
+        arrive(&bar);
+      }
+    } else {
+      wait(&bar, 0);
+      buf[l] = make_uint4(l, l, l, l);
+    }
+    return;
+  }
   if (V == 2) {
     if (w == 0) buf[l] = make_uint4(l, l, l, l);
     __syncthreads();
@@ -55,6 +75,8 @@ int main() {
   k<1><<<1, 64>>>(g, o); cudaDeviceSynchronize(); printf("B done\n");
   k<2><<<1, 64>>>(g, o); cudaDeviceSynchronize(); printf("C done\n");
   k<3><<<1, 64>>>(g, o); cudaDeviceSynchronize(); printf("D done\n");
+  k<4><<<1, 64>>>(g, o); cudaDeviceSynchronize(); printf("E done\n");
+  k<5><<<1, 64>>>(g, o); cudaDeviceSynchronize(); printf("F done\n");
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
