@@ -356,8 +356,10 @@ struct espn_gpu_workspace {
   uint32_t* ff_seen = nullptr;             // 2 x B
   uint32_t* fused_state = nullptr;         // {epoch, rows used by parity 0, parity 1}
   uint32_t hash_slots = 0;
-  uint32_t* small_arrive = nullptr;        // single-launch small batches: per-query arrival counters
-  unsigned long long* small_top = nullptr; // ... and per-CTA best-k lists (kSmallMaxCtas x kFusedMaxK)
+  uint32_t* small_arrive = nullptr;        // single-launch small batches: per-query arrival counters,
+  unsigned long long* small_top = nullptr; // per-CTA best-k lists (kSmallMaxCtas x kFusedMaxK),
+  uint32_t* small_hash = nullptr;          // per-query duplicate hashes (kSmallMaxB x kSmallHashSlots)
+  uint32_t* small_ff = nullptr;            // and their empty-code flags
   unsigned long long* kprof = nullptr;  // device-timed MaxSim {sum_ns, launches, start, done}
   // tiered tables: two staging slots (one scoring, one being prefetched)
   struct Stage {
@@ -1218,7 +1220,11 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   // between batches; each query's last CTA resets its own) and per-CTA lists
   al((void**)&w->small_arrive, kSmallMaxB * sizeof(uint32_t));
   al((void**)&w->small_top, (size_t)kSmallMaxCtas * kFusedMaxK * sizeof(unsigned long long));
+  al((void**)&w->small_hash, (size_t)kSmallMaxB * kSmallHashSlots * sizeof(uint32_t));
+  al((void**)&w->small_ff, kSmallMaxB * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(w->small_arrive, 0, kSmallMaxB * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(w->small_ff, 0, kSmallMaxB * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(w->small_hash, 0xFF, (size_t)kSmallMaxB * kSmallHashSlots * sizeof(uint32_t));
   al((void**)&w->bow, C * sizeof(float));
   // outputs and the error word in ONE allocation: [err 16 B | ids | scores |
   // counts], so a synchronous call reads everything back with one copy
@@ -1255,7 +1261,9 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
     for (auto& ev : pr.e)
       if (e == cudaSuccess) e = cudaEventCreate(&ev);
   if (e == cudaSuccess) e = cudaMallocHost(&w->h_err, sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemset(w->err, 0, 4 * sizeof(uint32_t));
+  // the whole output pack starts defined: a synchronous call copies it back in
+  // one piece, including the slots beyond a query's count (unspecified, 0 here)
+  if (e == cudaSuccess) e = cudaMemset(w->opack, 0, 16 + (size_t)B * kMaxK * 8 + (size_t)B * 4);
   if (e == cudaSuccess) {
     const unsigned long long init[4] = {0ull, 0ull, ~0ull, 0ull};
     e = cudaMemcpy(w->kprof, init, sizeof init, cudaMemcpyHostToDevice);
@@ -1286,7 +1294,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
   cudaFree(w->done_flag);
   cudaFree(w->plan_done);
   cudaFree(w->unit_top); cudaFree(w->dedup); cudaFree(w->ff_seen); cudaFree(w->fused_state);
-  cudaFree(w->small_arrive); cudaFree(w->small_top);
+  cudaFree(w->small_arrive); cudaFree(w->small_top); cudaFree(w->small_hash); cudaFree(w->small_ff);
   for (auto& st : w->stage) {
     if (st.done) cudaEventSynchronize(st.done);
     if (st.free_ev) cudaEventSynchronize(st.free_ev);
@@ -1657,6 +1665,8 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     sp.P = small_P;
     sp.base_ok = (dev_off && (a->flags & kFlagBaseOffsets)) ? 1u : 0u;
     sp.arrive = w->small_arrive;
+    sp.hash = w->small_hash;
+    sp.ff_seen = w->small_ff;
     if (profile) ESPN_CUDA_TRY(cudaEventRecord(w->prof[pslot].e[0], s));
     const cudaError_t se = launch_small_rt(t->d, sp, B, s);
     if (se != cudaSuccess) return fail(ESPN_E_CUDA, std::string("small-batch launch: ") + cudaGetErrorString(se));

@@ -34,6 +34,12 @@
 #ifndef ESPN_PLANES
 #define ESPN_PLANES 4
 #endif
+// 1: every lane of the loader / query / combine / rank warps arrives on the
+// unit and bow-ring barriers (each lane's arrive releases its own writes);
+// 0: __syncwarp + one arriving lane (A/B measurement knob)
+#ifndef ESPN_ARRIVE_ALL
+#define ESPN_ARRIVE_ALL 1
+#endif
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -537,7 +543,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
         U.n_pt = pcarry;
       }
       __syncwarp();
-      mbar_arrive(&S.ufull_bar[us]);  // every lane (its writes are released by its own arrive)
+      if (ESPN_ARRIVE_ALL || lane == 0) mbar_arrive(&S.ufull_bar[us]);  // every lane releases its own writes
     }
   } else if (warp == L::PATCH_WARP) {
     // ============================ PAD PATCH =====================================
@@ -659,7 +665,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       }
       fence_proxy_async_smem();  // A tile is read by the tensor core (async proxy)
       __syncwarp();
-      mbar_arrive(&S.ufull_bar[us]);
+      if (ESPN_ARRIVE_ALL || lane == 0) mbar_arrive(&S.ufull_bar[us]);
     }
   } else if (warp >= L::PROD_WARP0 && warp < L::PROD_WARP0 + L::NPROD) {
     // ====================== BULK-COPY PRODUCERS (NPROD warps) ======================
@@ -877,13 +883,14 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.uempty_bar[us]);  // slot free
+      if (ESPN_ARRIVE_ALL || lane == 0) mbar_arrive(&S.uempty_bar[us]);  // slot free
       if (fused) {
         const uint32_t j = gi % L::NB;
         mbar_wait(&S.bfree_bar[j], ((gi / L::NB) & 1) ^ 1);
 #pragma unroll
         for (int r = 0; r < NK; ++r) ring[j * L::UNITMAX + r * 32 + lane] = bow[r];
-        mbar_arrive(&S.bdone_bar[j]);  // every lane releases its own ring writes
+        __syncwarp();
+        if (ESPN_ARRIVE_ALL || lane == 0) mbar_arrive(&S.bdone_bar[j]);  // every lane releases its own ring writes
       }
 #pragma unroll
       for (int r = 0; r < NK; ++r)
@@ -941,7 +948,8 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       float bow[NK];
 #pragma unroll
       for (int r = 0; r < NK; ++r) bow[r] = ring[j * L::UNITMAX + r * 32 + lane];
-      mbar_arrive(&S.bfree_bar[j]);
+      __syncwarp();
+      if (ESPN_ARRIVE_ALL || lane == 0) mbar_arrive(&S.bfree_bar[j]);
       uint64_t key[NK];
       uint32_t bad = 0;
 #pragma unroll
@@ -1069,13 +1077,13 @@ maxsim_tc_kernel(const MaxSimParams p) {
       // releases its shared-memory writes (compute-sanitizer racecheck does
       // not carry a __syncwarp + one-lane arrive across warps,
       // tools/racecheck_probe.cu)
-      mbar_init(&S.ufull_bar[i], 64);
-      mbar_init(&S.uempty_bar[i], 1);
+      mbar_init(&S.ufull_bar[i], ESPN_ARRIVE_ALL ? 64 : 2);
+      mbar_init(&S.uempty_bar[i], ESPN_ARRIVE_ALL ? 32 : 1);  // combine warp
       mbar_init(&S.edone_bar[i], 32 * L::NEPI);
     }
     for (int i = 0; i < L::NB; ++i) {
-      mbar_init(&S.bdone_bar[i], 32);  // combine warp, every lane
-      mbar_init(&S.bfree_bar[i], 32);  // rank warp, every lane
+      mbar_init(&S.bdone_bar[i], ESPN_ARRIVE_ALL ? 32 : 1);  // combine warp, every lane
+      mbar_init(&S.bfree_bar[i], ESPN_ARRIVE_ALL ? 32 : 1);  // rank warp, every lane
     }
     for (int i = 0; i < L::NS; ++i) mbar_init(&S.patched_bar[i], 1);
     mbar_fence_init();

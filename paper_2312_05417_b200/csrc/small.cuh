@@ -9,33 +9,45 @@
 //   * grid (P, B): CTA (p, b) scores chunk p of query b's scored list -- the
 //     needed prefix min(R, n) (or needed_counts[b]); with partial re-rank the
 //     tail [needed, n) as alpha*cls (SPEC.md:276 (5));
-//   * MaxSim on the CUDA cores, warp per document, lane = query token, fp32
-//     query, __fmul_rn/__fadd_rn in the reference's order (scoring.hpp:7-10,
-//     20-21): bit-exact with the oracle, like maxsim_simt_kernel; rows are read
-//     from the tile layout (RowLayout::off) with broadcast 16-byte loads;
+//   * candidate metadata (id -> row_ptr pair) one thread per candidate, so the
+//     CTA pays two dependent round trips, not two per document; the same
+//     threads insert the ids into the query's duplicate hash in L2 (rank()'s
+//     duplicate rejection, scoring.hpp:16-18) and check the answers later;
+//   * MaxSim on the CUDA cores, two warps per document (each half of its
+//     rows), lane = query token, fp32 query, __fmul_rn/__fadd_rn in the
+//     reference's order (scoring.hpp:7-10, 20-21); rows staged per warp in
+//     shared memory with one coalesced round trip per piece.  Bit-exact with
+//     the oracle: the max over rows is order-free (a +-0 tie cannot change
+//     the sum, which starts at +0), the sum over query tokens is sequential;
 //   * aggregate alpha*cls + bow without contraction (scoring.hpp:12-14) and
 //     the CTA's best k by rank counting, written sorted to a per-CTA list;
-//   * the query's last CTA to arrive (atomic counter, reset by itself) merges
-//     the P lists (fused_merge, the finalize merge) in warp 0 while warps 1-7
-//     run rank()'s duplicate check (scoring.hpp:16-18) over the query's scored
-//     ids in a shared-memory hash.
+//   * the query's last CTA to arrive (atomic counter) merges the P lists in
+//     shared memory -- warps k-way merge 32 lists each, warp 0 merges their
+//     results -- writes the ranked list and resets the query's hash/counter.
 // Errors are the same bits as the three-kernel path (offsets, capacity,
 // unknown id, non-finite query / cls / score, duplicates).
 #pragma once
 #include "common.cuh"
 #include "ptx.cuh"
-#include "maxsim_tc.cuh"  // fused_merge
+#include "maxsim_tc.cuh"  // fused_merge (long lists fallback)
 
 namespace espn_k {
 
-constexpr int kSmallThreads = 256;        // 8 warps
+constexpr int kSmallThreads = 512;        // 16 warps: 8 documents in flight, two warps each
+constexpr int kSmallDocsPerRound = kSmallThreads / 64;
+// d >= 96 keeps the fp32 query row (d registers per lane) without spilling at
+// 256 threads (4 documents per round)
+template <int D>
+constexpr int small_threads() { return D >= 96 ? 256 : kSmallThreads; }
 constexpr int kSmallMaxB = 16;            // queries per small batch
 constexpr int kSmallMaxChunk = 256;       // scored candidates per CTA
-constexpr int kSmallMaxList = 2048;       // scored candidates per query (dedup hash: 2x)
+constexpr int kSmallMaxList = 2048;       // scored candidates per query
+constexpr int kSmallHashSlots = 4096;     // per-query duplicate hash (2x the longest list)
 constexpr int kSmallMaxCtas = 296;        // 2 per SM
-constexpr int kSmallMergeKeys = 1016;     // merge scratch (P x k keys; longer -> k-way merge)
-constexpr int kSmallWarpRowBytes = 2048;  // per-warp row staging (one piece: 32 rows at d=32)
-constexpr int kSmallRegionBytes = 24 * 1024;  // row staging | last CTA: merge keys + dedup hash
+constexpr int kSmallWarpRowBytes = 1024;  // per-warp row staging (16 rows at d=32)
+constexpr int kSmallRegionBytes = 16 * 1024;  // row staging | last CTA: the lists + level-1 merges
+constexpr int kSmallLevel1Keys = 16 * kFusedMaxK;                       // <= 16 level-1 lists of k
+constexpr int kSmallListKeys = kSmallRegionBytes / 8 - kSmallLevel1Keys;  // P x k keys merged in smem
 
 struct SmallParams {
   MaxSimParams m;              // table, batch and outputs; m.unit_top = B x P x k per-CTA lists
@@ -45,11 +57,13 @@ struct SmallParams {
   uint32_t P;                  // CTAs per query
   uint32_t base_ok;            // cand_off[0] may be nonzero (query slice of a larger CSR)
   uint32_t* arrive;            // B arrival counters, zero between batches
+  uint32_t* hash;              // B x kSmallHashSlots ids, 0xFFFFFFFF = empty between batches
+  uint32_t* ff_seen;           // B: id 0xFFFFFFFF (the empty code) seen, 0 between batches
 };
 
 // Host-side sizing (espn_gpu.cu): CTAs per query for the longest scored list.
 inline uint32_t small_ctas_per_query(uint64_t max_scored, uint32_t B) {
-  uint64_t P = (max_scored + 7) / 8;  // one document per warp
+  uint64_t P = (max_scored + kSmallDocsPerRound - 1) / kSmallDocsPerRound;  // one round of documents
   const uint64_t cap = B ? (uint64_t)kSmallMaxCtas / B : 1;
   if (P > cap) P = cap;
   return P < 1 ? 1u : (uint32_t)P;
@@ -70,28 +84,58 @@ __device__ __forceinline__ void small_prof_end(const MaxSimParams& p) {
   }
 }
 
+// One warp merges nl <= 32 descending lists of k keys (0 = empty) at
+// lists[l * k], lane l owning list l: k rounds of warp max over the heads.
+// Writes k keys (0-filled) to out; returns the number of non-empty keys.
+__device__ __forceinline__ uint32_t small_kway(const uint64_t* lists, uint32_t nl, uint32_t k, uint64_t* out,
+                                               uint32_t lane) {
+  uint32_t cur = 0;
+  uint64_t head = lane < nl ? lists[lane * k] : 0ull;
+  uint32_t r = 0;
+  for (; r < k; ++r) {
+    const uint64_t m = warp_max_key(head);
+    if (m == 0) break;
+    const uint32_t win = __ffs(__ballot_sync(0xffffffffu, head == m)) - 1;
+    if (lane == win) {
+      ++cur;
+      head = cur < k ? lists[lane * k + cur] : 0ull;
+    }
+    if (lane == 0) out[r] = m;
+  }
+  for (uint32_t i = r + lane; i < k; i += 32) out[i] = 0ull;
+  return r;
+}
+
 template <int D>
-__global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const SmallParams sp) {
+__global__ void __launch_bounds__(small_threads<D>()) rerank_small_kernel(const SmallParams sp) {
   const MaxSimParams& p = sp.m;
   using RL = RowLayout<D>;
-  constexpr uint32_t NW = kSmallThreads / 32;
+  constexpr uint32_t NT = small_threads<D>();
+  constexpr uint32_t NW = NT / 32;
+  constexpr uint32_t NDR = NT / 64;                          // documents per round
   constexpr uint32_t WBUF = kSmallWarpRowBytes;              // per-warp row staging
   constexpr uint32_t WROWS = WBUF / (2 * D);                 // rows per staged piece
+  constexpr uint32_t HM = kSmallHashSlots - 1;
   __shared__ __align__(16) float sq[32 * D];                 // query tokens (fp32, as given)
   __shared__ uint64_t keys[kSmallMaxChunk];                  // this CTA's candidate keys
-  __shared__ uint64_t m_src[kSmallMaxChunk];                 // per candidate: row address (0: none)
+  __shared__ uint64_t m_src[kSmallMaxChunk];                 // per candidate: row address (1: unknown id)
   __shared__ uint32_t m_t[kSmallMaxChunk], m_id[kSmallMaxChunk];
   __shared__ float m_cls[kSmallMaxChunk];
+  __shared__ float halfmax[NDR][32];                         // second half's row maxima per document
   // compute phase: NW row-staging buffers; the last CTA's merge phase reuses
-  // the space for the merge keys (warp 0) and the duplicate hash (warps 1-7)
+  // the space for the P lists and the level-1 merges
   __shared__ __align__(16) uint8_t region[kSmallRegionBytes];
-  __shared__ uint32_t s_last, s_ff;
+  __shared__ uint32_t s_last;
   static_assert(NW * WBUF <= kSmallRegionBytes && WROWS >= 1, "row staging");
-  static_assert((kSmallMergeKeys + 8) * 8 + 2 * kSmallMaxList * 4 <= kSmallRegionBytes, "merge scratch");
+  static_assert(NT >= kSmallMaxChunk, "one thread per candidate");
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t b = blockIdx.y, pc = blockIdx.x, P = sp.P;
   ktl_begin(p.dbg, 1);
   if (p.prof && tid == 0) atomicMin(&p.prof[2], ktl_now());
+  // ESPN_DEBUG bit 8: per-CTA phase stamps (start, inputs ready, scored, done)
+  const uint32_t cta = blockIdx.y * gridDim.x + blockIdx.x;
+  const bool trace = (p.dbg & 8u) && tid == 0 && cta < 256;
+  if (trace) g_cta_prof[4 * cta] = ktl_now();
   // ---- this query's list (validated before any dependent read) ----
   uint64_t off0 = p.cand_off[b], off1 = p.cand_off[b + 1];
   const bool bad_off = off1 < off0 || (b == 0 && off0 != 0 && !sp.base_ok);
@@ -106,21 +150,35 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
   const uint64_t j0 = min(ns, (uint64_t)pc * chunk), j1 = min(ns, j0 + chunk);
   const uint32_t nc = (uint32_t)(j1 - j0);
   // host sizing guards both (device offsets: a list longer than the workspace's declared max_list)
-  if ((nc > (uint32_t)kSmallMaxChunk || (pc == 0 && ns > (uint64_t)kSmallMaxList)) && tid == 0) atomicOr(p.err, ERR_CAPACITY);
+  const bool too_long = ns > (uint64_t)kSmallMaxList;
+  if ((nc > (uint32_t)kSmallMaxChunk || (pc == 0 && too_long)) && tid == 0) atomicOr(p.err, ERR_CAPACITY);
   const uint32_t ncs = min(nc, (uint32_t)kSmallMaxChunk);
   const uint32_t nq = p.nq;
   uint32_t ebits = 0;
-  // ---- candidate metadata (one thread per candidate: id -> row_ptr pair,
-  // two dependent round trips for the whole CTA) and the query, together ----
+  // ---- candidate metadata, one thread per candidate (two dependent round
+  // trips for the whole CTA), and its duplicate-hash insert: the CAS answer
+  // is only looked at after scoring, so its latency hides behind it ----
+  uint32_t* qhash = sp.hash + (size_t)b * kSmallHashSlots;
+  uint32_t my_id = 0, h = 0, cas_old = 0;
+  bool pend = false;
   if (tid < ncs) {
     const uint64_t j = j0 + tid, c = off0 + j;
-    const uint32_t id = __ldg(&p.cand_ids[c]);
-    m_id[tid] = id;
+    my_id = __ldg(&p.cand_ids[c]);
+    m_id[tid] = my_id;
     m_cls[tid] = __ldg(&p.cand_cls[c]);
+    if (!too_long) {
+      if (my_id == 0xFFFFFFFFu) {
+        if (atomicExch(&sp.ff_seen[b], 1u)) ebits |= ERR_DUPLICATE;
+      } else {
+        h = ((my_id * 2654435761u) >> 7) & HM;
+        cas_old = atomicCAS(&qhash[h], 0xFFFFFFFFu, my_id);
+        pend = true;
+      }
+    }
     uint64_t src = 0;
     uint32_t t = 0;
     if (j < need) {
-      const uint64_t loc = shard_local(id, p.shard_count, p.shard_index, p.n_docs);
+      const uint64_t loc = shard_local(my_id, p.shard_count, p.shard_index, p.n_docs);
       if (loc == ~0ull) {
         ebits |= ERR_UNKNOWN_DOC;
         src = 1;  // marker: no key
@@ -136,7 +194,7 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
   if (j0 < need && ncs > 0) {
     const float* qs = p.q32 + (size_t)b * nq * D;
     bool badq = false;
-    for (uint32_t i = tid; i < nq * D; i += kSmallThreads) {
+    for (uint32_t i = tid; i < nq * D; i += NT) {
       const float x0 = __ldg(&qs[i]);
       const float x = p.qround ? espn_ptx::code_to_f32(espn_ptx::f32_to_code(x0, p.bf16), p.bf16) : x0;
       badq |= !isfinite(x);
@@ -145,6 +203,7 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
     if (badq) atomicOr(p.err, ERR_NONFINITE_QUERY);
   }
   __syncthreads();
+  if (trace) g_cta_prof[4 * cta + 1] = ktl_now();
   float q[D];  // lane i: query token i (lanes >= nq mirror token 0; their maxima are not summed)
   {
     const float* qr = sq + (lane < nq ? lane : 0u) * D;
@@ -156,31 +215,36 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
   }
   const float alpha = p.alpha;
   uint8_t* wbuf = region + wid * WBUF;
-  // ---- warp per candidate: MaxSim (needed prefix) + aggregate -> key ----
-  for (uint32_t jj = wid; jj < ncs; jj += NW) {
+  const uint32_t slot = wid >> 1, half = wid & 1;  // document slot of the round, row half
+  // ---- rounds of NDR documents, two warps each: MaxSim (needed prefix) +
+  // aggregate -> key ----
+  for (uint32_t d0 = 0; d0 < ncs; d0 += NDR) {  // uniform across the CTA
+    const uint32_t jj = d0 + slot;
     const uint64_t j = j0 + jj;
-    const uint64_t src = m_src[jj];
-    const uint32_t t = m_t[jj];
-    float bow = 0.0f;
-    const bool ok = src != 1;
-    if (j < need && ok) {
+    const bool mine = jj < ncs;
+    const uint64_t src = mine ? m_src[jj] : 0ull;
+    const uint32_t t = mine ? m_t[jj] : 0u;
+    const bool scored = mine && j < need && src != 1;
+    float m = -INFINITY;
+    if (scored) {
       const uint8_t* doc = reinterpret_cast<const uint8_t*>(src);
-      float m = -INFINITY;
-      // the doc's rows in pieces of WROWS: one coalesced round trip per piece
-      // into the warp's buffer (kept in the tile layout), then every lane
-      // reads each row with broadcast 16-byte shared loads
-      for (uint32_t r0 = 0; r0 < t; r0 += WROWS) {
-        const uint32_t nr = min(WROWS, t - r0);
+      const uint32_t th = (t + 1) / 2;
+      const uint32_t ra = half ? th : 0u, rb = half ? t : th;  // this warp's rows [ra, rb)
+      // rows in pieces of WROWS: one coalesced round trip per piece into the
+      // warp's buffer (plain rows), then every lane reads each row with
+      // broadcast 16-byte shared loads
+      for (uint32_t r0 = ra; r0 < rb; r0 += WROWS) {
+        const uint32_t nr = min(WROWS, rb - r0);
         const uint32_t nv = nr * RL::CH;
         __syncwarp();  // the previous piece is consumed
         for (uint32_t v = lane; v < nv; v += 32) {
           const uint32_t jr = r0 + v / RL::CH, cc = v % RL::CH;
-          const uint32_t o = RL::off(t, jr, cc);
-          *reinterpret_cast<uint4*>(wbuf + (jr - r0) * (2 * D) + cc * 16) = __ldg(reinterpret_cast<const uint4*>(doc + o));
+          *reinterpret_cast<uint4*>(wbuf + (jr - r0) * (2 * D) + cc * 16) =
+              __ldg(reinterpret_cast<const uint4*>(doc + RL::off(t, jr, cc)));
         }
         __syncwarp();
         // four rows at a time: independent accumulators, each summed in
-        // ascending k (the reference's order); maxima applied in row order
+        // ascending k (the reference's order)
         uint32_t jr = 0;
         for (; jr + 4 <= nr; jr += 4) {
           float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -193,11 +257,11 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
             for (int r = 0; r < 4; ++r) {
               const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
 #pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const float d0 = espn_ptx::code_to_f32((uint16_t)(w[h] & 0xFFFFu), p.bf16);
-                const float d1 = espn_ptx::code_to_f32((uint16_t)(w[h] >> 16), p.bf16);
-                acc[r] = __fadd_rn(acc[r], __fmul_rn(q[k8 * 8 + 2 * h], d0));
-                acc[r] = __fadd_rn(acc[r], __fmul_rn(q[k8 * 8 + 2 * h + 1], d1));
+              for (int hh = 0; hh < 4; ++hh) {
+                const float x0 = espn_ptx::code_to_f32((uint16_t)(w[hh] & 0xFFFFu), p.bf16);
+                const float x1 = espn_ptx::code_to_f32((uint16_t)(w[hh] >> 16), p.bf16);
+                acc[r] = __fadd_rn(acc[r], __fmul_rn(q[k8 * 8 + 2 * hh], x0));
+                acc[r] = __fadd_rn(acc[r], __fmul_rn(q[k8 * 8 + 2 * hh + 1], x1));
               }
             }
           }
@@ -212,34 +276,51 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
             const uint4 v = *reinterpret_cast<const uint4*>(wbuf + jr * (2 * D) + k8 * 16);
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const float d0 = espn_ptx::code_to_f32((uint16_t)(w[h] & 0xFFFFu), p.bf16);
-              const float d1 = espn_ptx::code_to_f32((uint16_t)(w[h] >> 16), p.bf16);
-              acc = __fadd_rn(acc, __fmul_rn(q[k8 * 8 + 2 * h], d0));
-              acc = __fadd_rn(acc, __fmul_rn(q[k8 * 8 + 2 * h + 1], d1));
+            for (int hh = 0; hh < 4; ++hh) {
+              const float x0 = espn_ptx::code_to_f32((uint16_t)(w[hh] & 0xFFFFu), p.bf16);
+              const float x1 = espn_ptx::code_to_f32((uint16_t)(w[hh] >> 16), p.bf16);
+              acc = __fadd_rn(acc, __fmul_rn(q[k8 * 8 + 2 * hh], x0));
+              acc = __fadd_rn(acc, __fmul_rn(q[k8 * 8 + 2 * hh + 1], x1));
             }
           }
           if (acc > m) m = acc;
         }
       }
-      float s = 0.0f;
-      for (uint32_t i = 0; i < nq; ++i) s = __fadd_rn(s, __shfl_sync(0xffffffffu, m, i));
-      bow = s;
-      if (p.bow_out && lane == 0) p.bow_out[off0 + j] = s;
     }
-    if (lane == 0) {
-      uint64_t key = 0;
-      if (ok) {
-        const float cl = m_cls[jj];
-        const float sc = __fadd_rn(__fmul_rn(alpha, cl), bow);
-        ebits |= !isfinite(cl) ? ERR_NONFINITE_CLS : (!isfinite(sc) ? ERR_NONFINITE_SCORE : 0u);
-        key = make_key(sc, m_id[jj]);
+    if (half) halfmax[slot][lane] = m;
+    __syncthreads();
+    if (!half && mine) {
+      float bow = 0.0f;
+      if (scored) {
+        const float m2 = halfmax[slot][lane];
+        if (m2 > m) m = m2;
+        float s = 0.0f;
+        for (uint32_t i = 0; i < nq; ++i) s = __fadd_rn(s, __shfl_sync(0xffffffffu, m, i));
+        bow = s;
+        if (p.bow_out && lane == 0) p.bow_out[off0 + j] = s;
       }
-      keys[jj] = key;
+      if (lane == 0) {
+        uint64_t key = 0;
+        if (src != 1) {
+          const float cl = m_cls[jj];
+          const float sc = __fadd_rn(__fmul_rn(alpha, cl), bow);
+          ebits |= !isfinite(cl) ? ERR_NONFINITE_CLS : (!isfinite(sc) ? ERR_NONFINITE_SCORE : 0u);
+          key = make_key(sc, m_id[jj]);
+        }
+        keys[jj] = key;
+      }
     }
+    __syncthreads();  // halfmax / staging buffers reused by the next round
+  }
+  // ---- duplicate hash: the early CAS answers, further probes on collision ----
+  while (pend) {
+    if (cas_old == 0xFFFFFFFFu) break;
+    if (cas_old == my_id) { ebits |= ERR_DUPLICATE; break; }
+    h = (h + 1) & HM;
+    cas_old = atomicCAS(&qhash[h], 0xFFFFFFFFu, my_id);
   }
   if (ebits) atomicOr(p.err, ebits);
-  __syncthreads();
+  if (trace) g_cta_prof[4 * cta + 2] = ktl_now();
   // ---- the CTA's best k, sorted: key i goes to position rank(i) ----
   const uint32_t k = p.k;
   unsigned long long* mylist = p.unit_top + ((size_t)b * P + pc) * k;
@@ -252,57 +333,64 @@ __global__ void __launch_bounds__(kSmallThreads) rerank_small_kernel(const Small
     if (v != 0 && rk < k) __stcg(&mylist[rk], (unsigned long long)v);
     nz = (uint32_t)__syncthreads_count(v != 0);
   }
-  for (uint32_t r = min(nz, k) + tid; r < k; r += kSmallThreads) __stcg(&mylist[r], 0ull);
+  for (uint32_t r = min(nz, k) + tid; r < k; r += NT) __stcg(&mylist[r], 0ull);
   // ---- arrival; the query's last CTA finishes it ----
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(&sp.arrive[b], 1u) == P - 1 ? 1u : 0u;
   __syncthreads();
   if (!s_last) {
+    if (trace) g_cta_prof[4 * cta + 3] = ktl_now();
     ktl_end(p.dbg, 1);
     small_prof_end(p);
     return;
   }
   __threadfence();
-  if (wid == 0) {
-    uint64_t* fmk = reinterpret_cast<uint64_t*>(region);
-    fused_merge<kSmallMergeKeys>(p, b, b * P, P, fmk, lane, /*kway=*/chunk < k);
-  } else {
-    // duplicate check over the query's scored ids (warps 1-7)
-    uint32_t* hash = reinterpret_cast<uint32_t*>(region + (kSmallMergeKeys + 8) * 8);
-    constexpr uint32_t HS = 2 * kSmallMaxList, HM = HS - 1;
-    const uint32_t t7 = tid - 32;
-    constexpr uint32_t N7 = kSmallThreads - 32;
-    for (uint32_t i = t7; i < HS; i += N7) hash[i] = 0xFFFFFFFFu;
-    if (t7 == 0) s_ff = 0;
-    asm volatile("bar.sync 1, %0;" ::"n"(N7) : "memory");
-    uint32_t dup = 0;
-    const uint64_t nd = min(ns, (uint64_t)kSmallMaxList);
-    for (uint64_t j = t7; j < nd; j += N7) {
-      const uint32_t id = __ldg(&p.cand_ids[off0 + j]);
-      if (id == 0xFFFFFFFFu) {
-        dup |= atomicExch(&s_ff, 1u);
-        continue;
+  const unsigned long long* lists = p.unit_top + (size_t)b * P * k;
+  const uint32_t nkeys = P * k;
+  if (nkeys <= (uint32_t)kSmallListKeys && P <= 32u * NW) {
+    // the P lists -> shared memory in one round trip; warps k-way merge 32
+    // lists each (level 1), warp 0 merges their results
+    uint64_t* L0 = reinterpret_cast<uint64_t*>(region);
+    uint64_t* L1 = L0 + kSmallListKeys;
+    for (uint32_t i = tid; i < nkeys; i += NT) L0[i] = __ldcg(&lists[i]);
+    __syncthreads();
+    const uint32_t n1 = (P + 31) / 32;
+    if (wid < n1) small_kway(L0 + (size_t)wid * 32 * k, min(32u, P - wid * 32), k, L1 + wid * k, lane);
+    __syncthreads();
+    if (wid == 0) {
+      uint64_t* fin = L0;  // level 0 is consumed
+      const uint32_t cnt = small_kway(L1, n1, k, fin, lane);
+      __syncwarp();
+      for (uint32_t r = lane; r < cnt; r += 32) {
+        const uint64_t v = fin[r];
+        p.out_ids[(size_t)b * k + r] = ~(uint32_t)(v & 0xFFFFFFFFu);
+        p.out_scores[(size_t)b * k + r] = order_float((uint32_t)(v >> 32));
       }
-      uint32_t h = ((id * 2654435761u) >> 7) & HM;
-      for (;;) {
-        const uint32_t old = atomicCAS(&hash[h], 0xFFFFFFFFu, id);
-        if (old == 0xFFFFFFFFu) break;
-        if (old == id) { dup = 1; break; }
-        h = (h + 1) & HM;
-      }
+      if (lane == 0) p.out_counts[b] = cnt;
     }
-    if (dup) atomicOr(p.err, ERR_DUPLICATE);
+  } else if (wid == 0) {  // long: the chunked k-way merge straight from the lists
+    fused_merge<kSmallListKeys>(p, b, b * P, P, reinterpret_cast<uint64_t*>(region), lane, /*kway=*/true);
   }
-  if (tid == 0) sp.arrive[b] = 0u;  // every CTA of the query has arrived
+  // the batch is done for this query: reset its hash, empty-code flag and counter
+  {
+    uint4* h4 = reinterpret_cast<uint4*>(qhash);
+    for (uint32_t i = tid; i < kSmallHashSlots / 4; i += NT)
+      h4[i] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  }
+  if (tid == 0) {
+    sp.ff_seen[b] = 0u;
+    sp.arrive[b] = 0u;  // every CTA of the query has arrived
+  }
   ktl_end(p.dbg, 1);
-  __syncthreads();  // (the profile's end stamp after the merge and the dedup)
+  __syncthreads();  // (the profile's end stamp after the merge)
+  if (trace) g_cta_prof[4 * cta + 3] = ktl_now() | (1ull << 63);  // the merging CTA
   small_prof_end(p);
 }
 
 template <int D>
 cudaError_t launch_small(const SmallParams& sp, uint32_t B, cudaStream_t s) {
-  rerank_small_kernel<D><<<dim3(sp.P, B), kSmallThreads, 0, s>>>(sp);
+  rerank_small_kernel<D><<<dim3(sp.P, B), small_threads<D>(), 0, s>>>(sp);
   return cudaGetLastError();
 }
 inline cudaError_t launch_small_rt(uint32_t d, const SmallParams& sp, uint32_t B, cudaStream_t s) {
