@@ -80,6 +80,12 @@ typedef struct espn_gpu_workspace espn_gpu_workspace;
                                            the host or the device (a table larger than free HBM opens); calls
                                            that read rows fail with INVALID_STATE until every doc is loaded */
 
+#define ESPN_TABLE_DISK_TIER 0x8u      /* with STREAMED + resident: the non-resident docs stay in the store
+                                           file (the NVMe tier, PAPER.md's premise) -- no pinned or HBM copy is
+                                           made; a batch that needs them must be staged by espn_gpu_prefetch_rows
+                                           (rows the caller read from the file, espn_store_fetch) and re-ranked
+                                           with ESPN_RERANK_PREFETCHED, else INVALID_STATE; gathers fail */
+
 /* The embedding table (store.hpp:13-35).  The HBM tier holds BOW rows only as
  * CSR: doc i's t_i token rows live at rows[row_ptr[i]*d .. row_ptr[i+1]*d),
  * 2-byte codes of `dtype`.  Callers pass plain row-major rows; in HBM the
@@ -267,6 +273,21 @@ ESPN_API int espn_gpu_prefetch(espn_gpu_table* table, espn_gpu_workspace* ws, co
 ESPN_API int espn_gpu_prefetch_hints(espn_gpu_table* table, espn_gpu_workspace* ws, uint32_t n_queries,
                                      const uint32_t* hint_ids, const uint64_t* hint_offsets, uint32_t flags,
                                      void* side_stream);
+
+/* The disk-tier prefetcher (ESPN_TABLE_DISK_TIER; PAPER.md's SSD tier): the
+ * caller read the records of some docs from the store file (espn_store_fetch,
+ * O_DIRECT, queue_depth reads in flight) and hands their BOW rows over --
+ * plain row-major table codes, doc ids[j]'s t rows at byte row_byte_off[j]
+ * (16-byte aligned) of `rows` (a HOST buffer of rows_bytes; pinned makes the
+ * upload asynchronous).  ids: HOST CSR over n_queries by id_offsets (per-query
+ * byte accounting).  The rows are uploaded on side_stream, tiled into a free
+ * staging slot and keyed by doc exactly like espn_gpu_prefetch_hints; the next
+ * espn_gpu_rerank carrying ESPN_RERANK_PREFETCHED finds them (hits).  HBM-
+ * resident docs, other shards' and unknown ids are skipped.  Works for any
+ * streamed tiered table (host-tier docs may be handed over too). */
+ESPN_API int espn_gpu_prefetch_rows(espn_gpu_table* table, espn_gpu_workspace* ws, uint32_t n_queries,
+                                    const uint32_t* ids, const uint64_t* id_offsets, const void* rows,
+                                    const uint64_t* row_byte_off, uint64_t rows_bytes, void* side_stream);
 
 /* Completes an ASYNC batch on its stream and reports device-side errors
  * (unknown doc id -> DATA_INTEGRITY, non-finite query/cls -> INVALID_INPUT,

@@ -42,6 +42,7 @@ ESPN_RERANK_SEPARATE_TOPK = 0x80
 ESPN_RERANK_QUERY_ROUNDED = 0x100
 ESPN_RERANK_QUERY_SPLIT = 0x200
 ESPN_TABLE_STREAMED = 0x4
+ESPN_TABLE_DISK_TIER = 0x8
 ESPN_READ_DIRECT, ESPN_READ_BUFFERED, ESPN_READ_MMAP = 0, 1, 2
 
 
@@ -116,6 +117,8 @@ SIGNATURES = {
     "espn_gpu_prefetch": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(RerankArgs), C.c_void_p]),
     "espn_gpu_prefetch_hints": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
                                           C.c_void_p]),
+    "espn_gpu_prefetch_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_uint64, C.c_void_p]),
     "espn_gpu_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "espn_gpu_gather_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]),
     "espn_gpu_merge_topk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32,

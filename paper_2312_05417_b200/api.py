@@ -147,6 +147,60 @@ def read_store_table(base, dtype: str = "f16", with_cls: bool = False):
     return row_ptr, codes[: int(row_ptr[-1]) * m.d], cls
 
 
+class StoreReader:
+    """The reference's file-backed StoreHandle (store.hpp:56-112) over
+    libespn_store: ReadMode direct (O_DIRECT) / buffered / mmap with
+    queue_depth reads in flight -- the host side of the disk tier."""
+
+    _MODES = {"direct": 0, "buffered": 1, "mmap": 2}
+
+    def __init__(self, base, mode: str = "direct", queue_depth: int = 16):
+        self._lib = L.store_lib()
+        self._h = C.c_void_p()
+        self.header = L.StoreHeader()
+        _check_store(self._lib.espn_store_open(str(base).encode(), self._MODES[mode], int(queue_depth),
+                                               C.byref(self._h), C.byref(self.header)))
+        self.d_cls, self.value_width = int(self.header.d_cls), int(self.header.value_width)
+
+    def fetch(self, ids, out=None):
+        """Records of ids in request order -> (payload bytes, offsets[n+1],
+        {bytes_read, blocks_read, wall_time}) (store.hpp:61-65, 91-94).
+        `out`: optional preallocated uint8 buffer (numpy, or a pinned torch
+        tensor) large enough for the payloads."""
+        ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint32))
+        n = ids.shape[0]
+        off = np.zeros(n + 1, np.uint64)
+        br, bl, wt = C.c_uint64(), C.c_uint64(), C.c_double()
+        _check_store(self._lib.espn_store_fetch(self._h, ids.ctypes.data, n, None, off.ctypes.data, 0,
+                                                C.byref(br), C.byref(bl), C.byref(wt)))
+        need = int(off[-1])
+        if out is None:
+            out = np.empty(max(need, 1), np.uint8)
+        cap = int(out.nbytes) if isinstance(out, np.ndarray) else int(out.numel())
+        if cap < need:
+            raise InvalidInputError("fetch buffer too small")
+        ptr = out.ctypes.data if isinstance(out, np.ndarray) else int(out.data_ptr())
+        _check_store(self._lib.espn_store_fetch(self._h, ids.ctypes.data, n, ptr, off.ctypes.data, cap,
+                                                C.byref(br), C.byref(bl), C.byref(wt)))
+        return out, off, {"bytes_read": br.value, "blocks_read": bl.value, "wall_time": wt.value}
+
+    def row_offsets(self, off):
+        """Byte offsets of each fetched record's BOW rows inside the payload
+        buffer (the CLS vector comes first: d_cls x value_width bytes)."""
+        return np.asarray(off[:-1], np.uint64) + np.uint64(self.d_cls * self.value_width)
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.espn_store_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # ---- types.hpp / ivf.hpp / pipeline.hpp carriers --------------------------------
 @dataclass
 class EmbeddingMatrix:
@@ -291,7 +345,7 @@ class GpuStore:
     def __init__(self, row_ptr, rows, d: int, dtype: str = "f16", d_cls: int = 128,
                  value_width: int = 2, alignment: int = 4096, device: int = 0,
                  borrowed_device: bool = False, shard_count: int = 1, shard_index: int = 0,
-                 rows_tiled: bool = False, resident=None, streamed: bool = False):
+                 rows_tiled: bool = False, resident=None, streamed: bool = False, disk_tier: bool = False):
         self.d = int(d)
         self.dtype = dtype
         self.d_cls = int(d_cls)
@@ -311,6 +365,8 @@ class GpuStore:
             self._row_ptr_host = row_ptr
             self._keep = (row_ptr,)
             rp_p, rows_p, flags = _ptr(row_ptr), None, L.ESPN_TABLE_STREAMED
+            if disk_tier:  # non-resident docs stay in the store file (espn_gpu_prefetch_rows)
+                flags |= L.ESPN_TABLE_DISK_TIER
         else:
             row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint64)
             rows = np.ascontiguousarray(rows, dtype=np.uint16)
@@ -698,6 +754,25 @@ class Reranker:
             self._keep_hints = (offs, hint_ids)
         _check(L.lib().espn_gpu_prefetch_hints(self.store.handle, self._h, B, _ptr(hint_ids), offs_p, flags,
                                                C.c_void_p(stream) if stream else None))
+
+    def prefetch_rows(self, ids, id_offsets, rows, row_byte_off, stream=None):
+        """espn_gpu_prefetch_rows: stage rows the caller read from the store
+        file (the disk tier) -- doc ids[j]'s plain codes at byte row_byte_off[j]
+        of the host buffer `rows` (numpy uint8, or a pinned torch tensor) --
+        keyed by doc; the next rerank_arrays(..., prefetched=True) finds them."""
+        ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint32))
+        offs = np.ascontiguousarray(np.asarray(id_offsets, dtype=np.uint64))
+        boff = np.ascontiguousarray(np.asarray(row_byte_off, dtype=np.uint64))
+        if boff.shape[0] < ids.shape[0]:
+            raise InvalidInputError("one row offset per id")
+        if isinstance(rows, np.ndarray):
+            rows_p, nbytes = rows.ctypes.data, int(rows.nbytes)
+        else:  # torch tensor (pinned host memory: asynchronous upload)
+            rows_p, nbytes = int(rows.data_ptr()), int(rows.numel() * rows.element_size())
+        self._keep_rows = (ids, offs, boff, rows)
+        _check(L.lib().espn_gpu_prefetch_rows(self.store.handle, self._h, offs.shape[0] - 1, ids.ctypes.data,
+                                              offs.ctypes.data, rows_p, boff.ctypes.data, nbytes,
+                                              C.c_void_p(stream) if stream else None))
 
     def prefetch(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig, stream=None,
                  needed_counts=None, device_offsets: bool = False):

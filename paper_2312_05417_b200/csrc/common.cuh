@@ -79,8 +79,13 @@ enum : uint32_t {
   ERR_BAD_OFFSETS = 1u << 6,     // cand_offsets not starting at 0 / decreasing -> INVALID_INPUT
   ERR_CAPACITY = 1u << 7,        // batch exceeds workspace capacity -> INVALID_INPUT
   ERR_STAGING = 1u << 8,         // host-tier rows of a batch exceed the staging buffer -> INVALID_CONFIG
-  ERR_SERVER = 1u << 9           // persistent server: the batch did not complete in time -> INVALID_STATE
+  ERR_SERVER = 1u << 9,          // persistent server: the batch did not complete in time -> INVALID_STATE
+  ERR_NOT_PREFETCHED = 1u << 10  // disk tier: a needed doc was not staged by espn_gpu_prefetch_rows -> INVALID_STATE
 };
+
+// doc_loc tier bits (tiered tables): bit 0 = not in HBM; bit 1 = on the disk
+// tier (ESPN_TABLE_DISK_TIER: no in-memory copy, the word holds no address)
+constexpr uint64_t kLocHost = 1ull, kLocDisk = 2ull;
 
 // Staging of host-tier rows for one batch (stage_kernel): one CTA per query,
 // one warp per needed candidate.
@@ -127,7 +132,23 @@ struct HintParams {
   unsigned long long* cursor;
   unsigned long long* qstats;  // B x 6: [4] += bytes this query's warps staged
   uint32_t* err;
+  // espn_gpu_prefetch_rows: the rows come from the caller (plain row-major
+  // codes in device memory, hint j's doc at ext_src + ext_off[j]) and are
+  // tiled into the staging slot; NULL: copy the doc's host-tier rows
+  const uint8_t* ext_src;
+  const uint64_t* ext_off;
+  uint32_t d;
 };
+
+// Byte offset of 16-byte chunk c of row j inside a doc of t rows in the HBM
+// tile layout -- RowLayout<D>::off for a run-time d.
+__device__ __forceinline__ uint32_t tile_off_rt(uint32_t d, uint32_t t, uint32_t j, uint32_t c) {
+  if (d != 16 && d != 32 && d != 64 && d != 128) return j * 2 * d + c * 16;
+  const uint32_t pw = 2 * d < 128 ? 2 * d : 128, cpp = pw / 16;
+  const uint32_t p = c / cpp, cc = c % cpp;
+  const uint32_t sw = ((j * pw) >> 7) & (cpp - 1);
+  return (p * t + j) * pw + ((cc ^ sw) << 4);
+}
 
 // Device-side batch planning (plan_kernel): per-query needed counts, work
 // units of the MaxSim kernel, all from device-resident candidate offsets, so

@@ -55,11 +55,14 @@ int err_bits_to_status(uint32_t bits) {
   if (bits & ERR_CAPACITY) m += " batch exceeds workspace capacity;";
   if (bits & ERR_STAGING) m += " host-tier rows of the batch exceed the staging buffer (raise staging_bytes);";
   if (bits & ERR_SERVER) m += " the persistent re-rank server did not complete the batch (stopped or stalled);";
+  if (bits & ERR_NOT_PREFETCHED)
+    m += " a needed doc of the disk tier was not staged by espn_gpu_prefetch_rows before this PREFETCHED batch;";
   g_last_error = m;
   if (bits & ERR_UNKNOWN_DOC) return ESPN_E_DATA_INTEGRITY;
   if (bits & ERR_UNIT_TOO_LARGE) return ESPN_E_INVALID_STATE;
   if (bits & ERR_STAGING) return ESPN_E_INVALID_CONFIG;
   if (bits & ERR_SERVER) return ESPN_E_INVALID_STATE;
+  if (bits & ERR_NOT_PREFETCHED) return ESPN_E_INVALID_STATE;
   return ESPN_E_INVALID_INPUT;
 }
 
@@ -327,6 +330,7 @@ struct espn_gpu_table {
   uint64_t hbm_row_bytes = 0, host_row_bytes = 0, resident_docs = 0;
   // ESPN_TABLE_STREAMED: filled in doc order by espn_gpu_table_load_rows
   bool streamed = false;
+  bool disk_tier = false;  // ESPN_TABLE_DISK_TIER: non-resident docs have no in-memory copy
   uint64_t loaded_docs = 0;
   std::vector<uint64_t> h_row_ptr;  // host copies used while filling
   std::vector<uint64_t> h_loc;      // tiered: per-doc address | tier bit
@@ -378,6 +382,10 @@ struct espn_gpu_workspace {
     uint32_t hint_epoch = 0;               // != 0: filled by espn_gpu_prefetch_hints (doc-keyed)
     uint32_t* hint_ids = nullptr;          // device copy of host hint ids (lazy, max_candidates)
     uint32_t* hint_ids_h = nullptr;        // its pinned staging
+    uint8_t* ext_buf = nullptr;            // espn_gpu_prefetch_rows: the caller's rows on the device (lazy)
+    uint64_t ext_cap = 0;
+    uint64_t* ext_off = nullptr;           // per hint: byte offset of its rows in ext_buf (lazy)
+    uint64_t* ext_off_h = nullptr;         // its pinned staging
   } stage[2];
   uint64_t* hint_map = nullptr;            // per local doc: epoch << 32 | staged offset / 16 (lazy)
   uint32_t hint_epoch = 0;
@@ -507,6 +515,8 @@ void drain_prof(espn_gpu_workspace* w, int i) {
 }  // namespace
 
 namespace {
+const char* const kDiskGather =
+    "gather of a disk-tier table: its non-resident docs exist only in the store file (espn_store_fetch)";
 // Calls that read rows need every doc of a streamed table loaded.
 int require_loaded(const espn_gpu_table* t) {
   if (t && t->streamed && t->loaded_docs != t->n_docs)
@@ -541,10 +551,11 @@ int open_streamed(espn_gpu_table* t, const espn_table_desc* desc) {
     t->resident_docs = n;
     return ESPN_OK;
   }
+  t->disk_tier = (desc->flags & ESPN_TABLE_DISK_TIER) != 0;
   uint64_t hb = 0, sb = 0, nres = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const uint64_t bytes = (rp[i + 1] - rp[i]) * rowb;
-    if (desc->resident[i]) { hb += bytes; ++nres; } else { sb += bytes; }
+    if (desc->resident[i]) { hb += bytes; ++nres; } else if (!t->disk_tier) { sb += bytes; }
   }
   uint8_t* hbm = nullptr;
   ESPN_CUDA_TRY(cudaMalloc(&hbm, std::max<uint64_t>(hb, 16)));
@@ -558,7 +569,8 @@ int open_streamed(espn_gpu_table* t, const espn_table_desc* desc) {
   for (uint64_t i = 0; i < n; ++i) {
     const uint64_t bytes = (rp[i + 1] - rp[i]) * rowb;
     if (desc->resident[i]) { t->h_loc[i] = reinterpret_cast<uint64_t>(hbm + oh); oh += bytes; }
-    else { t->h_loc[i] = reinterpret_cast<uint64_t>(t->host_dev + os) | 1ull; os += bytes; }
+    else if (t->disk_tier) { t->h_loc[i] = kLocHost | kLocDisk; }  // no address: staged only by prefetch_rows
+    else { t->h_loc[i] = reinterpret_cast<uint64_t>(t->host_dev + os) | kLocHost; os += bytes; }
   }
   ESPN_CUDA_TRY(cudaMemcpy(t->doc_loc, t->h_loc.data(), n * 8, cudaMemcpyHostToDevice));
   t->tiered = true;
@@ -635,6 +647,7 @@ int load_streamed(espn_gpu_table* t, uint64_t b0, uint64_t n, const uint16_t* ro
     const uint32_t tt = (uint32_t)(rp[i + 1] - rp[i]);
     const uint64_t bytes = (uint64_t)tt * rowb;
     const uint8_t* s = src + (rp[i] - rp[b0]) * rowb;
+    if (t->tiered && (t->h_loc[i] & kLocDisk)) continue;  // disk tier: stays in the file
     const bool host_tier = t->tiered && (t->h_loc[i] & 1ull);
     if (host_tier) {  // tile straight into the pinned tier
       const uint64_t a = (t->h_loc[i] & ~1ull) - reinterpret_cast<uint64_t>(t->host_dev);
@@ -983,6 +996,8 @@ int espn_gpu_table_open(const espn_table_desc* desc, espn_gpu_table** out) {
   if (!desc->row_ptr || (!desc->rows && !streamed)) return fail(ESPN_E_INVALID_INPUT, "null row_ptr/rows");
   if (streamed && (desc->flags & ESPN_TABLE_DEVICE_BORROWED))
     return fail(ESPN_E_INVALID_INPUT, "a streamed table takes a HOST row_ptr");
+  if ((desc->flags & ESPN_TABLE_DISK_TIER) && !(streamed && desc->resident))
+    return fail(ESPN_E_INVALID_INPUT, "ESPN_TABLE_DISK_TIER needs ESPN_TABLE_STREAMED and a resident mask");
   int sms = 0;
   bool tc = false;
   int st = check_device(desc->device, &sms, &tc);
@@ -1129,7 +1144,7 @@ int espn_gpu_table_load_rows(espn_gpu_table* t, uint64_t doc_begin, uint64_t n, 
   t->loaded_docs += n;
   if (t->loaded_docs == t->n_docs) {  // complete: drop the fill-time host copies
     std::vector<uint64_t>().swap(t->h_loc);
-    std::vector<uint64_t>().swap(t->h_row_ptr);
+    if (!t->disk_tier) std::vector<uint64_t>().swap(t->h_row_ptr);  // (disk tier: espn_gpu_prefetch_rows checks)
   }
   return ESPN_OK;
 }
@@ -1301,6 +1316,7 @@ int espn_gpu_workspace_destroy(espn_gpu_workspace* w) {
     cudaFree(st.buf); cudaFree(st.cand_src); cudaFree(st.cand_status); cudaFree(st.cursor); cudaFree(st.qstats); cudaFree(st.off);
     cudaFree(st.need); cudaFreeHost(st.off_h); cudaFreeHost(st.need_h);
     cudaFree(st.hint_ids); cudaFreeHost(st.hint_ids_h);
+    cudaFree(st.ext_buf); cudaFree(st.ext_off); cudaFreeHost(st.ext_off_h);
     st.hint_epoch = 0;
     if (st.done) cudaEventDestroy(st.done);
     if (st.free_ev) cudaEventDestroy(st.free_ev);
@@ -1927,8 +1943,14 @@ int espn_gpu_prefetch(espn_gpu_table* t, espn_gpu_workspace* w, const espn_reran
   return ESPN_OK;
 }
 
-int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B, const uint32_t* hint_ids,
-                            const uint64_t* hint_offsets, uint32_t flags, void* side_stream) {
+namespace {
+// Doc-keyed staging of one hint batch into a free staging slot (the body of
+// espn_gpu_prefetch_hints and espn_gpu_prefetch_rows).  ext_rows != NULL:
+// the rows come from the caller (plain codes, hint j's doc at byte
+// ext_off[j] of ext_rows, ext_bytes in all) instead of the host tier.
+int prefetch_hint_impl(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B, const uint32_t* hint_ids,
+                       const uint64_t* hint_offsets, uint32_t flags, void* side_stream, const void* ext_rows,
+                       const uint64_t* ext_off, uint64_t ext_bytes) {
   if (!t || !w) return fail(ESPN_E_INVALID_INPUT, "null argument");
   if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
   if (const int ls = require_loaded(t)) return ls;
@@ -1979,6 +2001,27 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
   ESPN_CUDA_TRY(cudaMemsetAsync(st.cursor, 0, sizeof(unsigned long long), s));
   ESPN_CUDA_TRY(cudaMemsetAsync(st.qstats, 0, (size_t)B * 6 * sizeof(unsigned long long), s));
   HintParams hp{};
+  if (ext_rows) {  // the caller's rows and their offsets -> this slot's device buffers
+    const uint64_t nh = hint_offsets[B];
+    if (!st.ext_off) {
+      ESPN_CUDA_TRY(cudaMalloc(&st.ext_off, w->max_candidates * sizeof(uint64_t)));
+      ESPN_CUDA_TRY(cudaMallocHost(&st.ext_off_h, w->max_candidates * sizeof(uint64_t)));
+    }
+    if (st.ext_cap < ext_bytes) {
+      ESPN_CUDA_TRY(cudaStreamSynchronize(s));
+      cudaFree(st.ext_buf);
+      st.ext_buf = nullptr;
+      st.ext_cap = 0;
+      ESPN_CUDA_TRY(cudaMalloc(&st.ext_buf, ext_bytes));
+      st.ext_cap = ext_bytes;
+    }
+    std::memcpy(st.ext_off_h, ext_off, nh * sizeof(uint64_t));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(st.ext_off, st.ext_off_h, nh * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    ESPN_CUDA_TRY(cudaMemcpyAsync(st.ext_buf, ext_rows, ext_bytes, cudaMemcpyHostToDevice, s));
+    hp.ext_src = st.ext_buf;
+    hp.ext_off = st.ext_off;
+  }
+  hp.d = t->d;
   hp.row_ptr = t->row_ptr;
   hp.doc_loc = t->doc_loc;
   hp.n_docs = t->n_docs;
@@ -2003,6 +2046,49 @@ int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B
   w->async_pending = true;
   w->counters.kernel_launches += 1;
   return ESPN_OK;
+}
+}  // namespace
+
+int espn_gpu_prefetch_hints(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B, const uint32_t* hint_ids,
+                            const uint64_t* hint_offsets, uint32_t flags, void* side_stream) {
+  return prefetch_hint_impl(t, w, B, hint_ids, hint_offsets, flags, side_stream, nullptr, nullptr, 0);
+}
+
+int espn_gpu_prefetch_rows(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B, const uint32_t* ids,
+                           const uint64_t* id_offsets, const void* rows, const uint64_t* row_byte_off,
+                           uint64_t rows_bytes, void* side_stream) {
+  if (!t || !w) return fail(ESPN_E_INVALID_INPUT, "null argument");
+  if (w->table != t) return fail(ESPN_E_INVALID_STATE, "workspace belongs to another table");
+  if (const int ls = require_loaded(t)) return ls;
+  if (!t->tiered) return ESPN_OK;  // everything is HBM-resident
+  if (B == 0) return ESPN_OK;
+  if (!id_offsets) return fail(ESPN_E_INVALID_INPUT, "null id offsets");
+  if (t->h_row_ptr.empty()) return fail(ESPN_E_INVALID_STATE, "espn_gpu_prefetch_rows needs a streamed tiered table");
+  if (B > w->max_queries) return fail(ESPN_E_INVALID_INPUT, "n_queries exceeds workspace capacity");
+  if (id_offsets[0] != 0) return fail(ESPN_E_INVALID_INPUT, "id_offsets[0] must be 0");
+  for (uint32_t b = 0; b < B; ++b)
+    if (id_offsets[b + 1] < id_offsets[b]) return fail(ESPN_E_INVALID_INPUT, "id_offsets must be non-decreasing");
+  const uint64_t nh = id_offsets[B];
+  if (nh > w->max_candidates) return fail(ESPN_E_INVALID_INPUT, "ids exceed workspace capacity");
+  if (nh == 0) return prefetch_hint_impl(t, w, B, ids, id_offsets, 0, side_stream, nullptr, nullptr, 0);
+  if (!ids || !rows || !row_byte_off) return fail(ESPN_E_INVALID_INPUT, "null ids / rows / row offsets");
+  // every doc's rows must lie inside the buffer, 16-byte aligned (the copy
+  // reads whole 16-byte chunks); unknown ids and other shards' ids are
+  // ignored like hints
+  const uint64_t rowb = (uint64_t)t->d * 2;
+  for (uint64_t j = 0; j < nh; ++j) {
+    if (row_byte_off[j] % 16) return fail(ESPN_E_INVALID_INPUT, "row_byte_off must be 16-byte aligned");
+    const uint32_t id = ids[j];
+    uint64_t loc = id;
+    if (t->shard_count > 1) {
+      if (id % t->shard_count != t->shard_index) continue;
+      loc = id / t->shard_count;
+    }
+    if (loc >= t->n_docs) continue;
+    const uint64_t bytes = (t->h_row_ptr.size() > loc + 1 ? t->h_row_ptr[loc + 1] - t->h_row_ptr[loc] : 0) * rowb;
+    if (row_byte_off[j] + bytes > rows_bytes) return fail(ESPN_E_INVALID_INPUT, "a doc's rows run past rows_bytes");
+  }
+  return prefetch_hint_impl(t, w, B, ids, id_offsets, 0, side_stream, rows, row_byte_off, rows_bytes);
 }
 
 int espn_gpu_workspace_cand_status(espn_gpu_workspace* w, uint8_t* out, uint64_t n) {
@@ -2036,6 +2122,7 @@ int espn_gpu_gather(espn_gpu_table* t, const uint32_t* ids, uint64_t n, uint16_t
                     uint64_t* out_row_ptr, uint64_t capacity_tokens, void* stream_v) {
   if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
   if (const int ls = require_loaded(t)) return ls;
+  if (t->disk_tier) return fail(ESPN_E_INVALID_STATE, kDiskGather);
   if (n == 0) {
     if (out_row_ptr) {
       uint64_t z = 0;
@@ -2160,6 +2247,7 @@ int espn_gpu_gather_rows(espn_gpu_table* t, const uint32_t* ids, uint64_t n, con
                          uint16_t* out_rows, void* stream_v) {
   if (!t) return fail(ESPN_E_INVALID_INPUT, "null table");
   if (const int ls = require_loaded(t)) return ls;
+  if (t->disk_tier) return fail(ESPN_E_INVALID_STATE, kDiskGather);
   if (n == 0) return ESPN_OK;
   if (!ids || !out_row_ptr || !out_rows) return fail(ESPN_E_INVALID_INPUT, "null argument");
   DeviceGuard g(t->device);

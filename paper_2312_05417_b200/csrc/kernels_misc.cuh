@@ -710,6 +710,14 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageParams 
         continue;
       }
     }
+    if (a & kLocDisk) {  // disk tier, not staged by espn_gpu_prefetch_rows: cannot be copied from memory
+      if (lane == 0) {
+        atomicOr(s.err, ERR_NOT_PREFETCHED);
+        s.cand_src[c0 + j] = 0;
+        if (s.cand_status) s.cand_status[c0 + j] = 3;
+      }
+      continue;
+    }
     const uint64_t bytes = (s.row_ptr[loc + 1] - s.row_ptr[loc]) * s.row_bytes;
     unsigned long long off = 0;
     if (lane == 0) off = atomicAdd(s.cursor, (unsigned long long)bytes);
@@ -766,7 +774,8 @@ __global__ void __launch_bounds__(kStageThreads) hint_stage_kernel(const HintPar
     const uint64_t loc = shard_local(s.hint_ids[j], s.shard_count, s.shard_index, s.n_docs);
     if (loc == ~0ull) continue;  // another shard's doc, or unknown: hints are advisory
     const uint64_t a = s.doc_loc[loc];
-    if (!(a & 1ull)) continue;   // HBM-resident
+    if (!(a & kLocHost)) continue;                  // HBM-resident
+    if ((a & kLocDisk) && !s.ext_src) continue;     // disk tier: only espn_gpu_prefetch_rows stages it
     const uint64_t bytes = (s.row_ptr[loc + 1] - s.row_ptr[loc]) * s.row_bytes;
     unsigned long long off = ~0ull;
     if (lane == 0) {
@@ -787,15 +796,25 @@ __global__ void __launch_bounds__(kStageThreads) hint_stage_kernel(const HintPar
     }
     off = __shfl_sync(0xffffffffu, off, 0);
     if (off == ~0ull) continue;
-    const uint4* src = reinterpret_cast<const uint4*>(a & ~1ull);
-    uint4* dst = reinterpret_cast<uint4*>(s.stage + off);
     const uint64_t n16 = bytes / 16;
-    uint64_t v = lane;
-    for (; v + 96 < n16; v += 128) {  // 4 PCIe reads in flight per lane
-      const uint4 x0 = src[v], x1 = src[v + 32], x2 = src[v + 64], x3 = src[v + 96];
-      dst[v] = x0; dst[v + 32] = x1; dst[v + 64] = x2; dst[v + 96] = x3;
+    if (s.ext_src) {  // caller rows (plain) -> tile layout in the staging slot
+      const uint4* src = reinterpret_cast<const uint4*>(s.ext_src + s.ext_off[j]);
+      uint8_t* dst = s.stage + off;
+      const uint32_t t = (uint32_t)(s.row_ptr[loc + 1] - s.row_ptr[loc]), ch = s.d / 8;
+      for (uint64_t v = lane; v < n16; v += 32) {
+        const uint32_t jr = (uint32_t)(v / ch), cc = (uint32_t)(v % ch);
+        *reinterpret_cast<uint4*>(dst + tile_off_rt(s.d, t, jr, cc)) = src[v];
+      }
+    } else {
+      const uint4* src = reinterpret_cast<const uint4*>(a & ~kLocHost);
+      uint4* dst = reinterpret_cast<uint4*>(s.stage + off);
+      uint64_t v = lane;
+      for (; v + 96 < n16; v += 128) {  // 4 PCIe reads in flight per lane
+        const uint4 x0 = src[v], x1 = src[v + 32], x2 = src[v + 64], x3 = src[v + 96];
+        dst[v] = x0; dst[v + 32] = x1; dst[v + 64] = x2; dst[v + 96] = x3;
+      }
+      for (; v < n16; v += 32) dst[v] = src[v];
     }
-    for (; v < n16; v += 32) dst[v] = src[v];
     if (lane == 0) s.hint_map[loc] = ((uint64_t)s.epoch << 32) | (off >> 4);
     bytes_moved += bytes;
   }
