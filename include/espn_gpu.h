@@ -284,7 +284,9 @@ ESPN_API int espn_gpu_prefetch_hints(espn_gpu_table* table, espn_gpu_workspace* 
  * staging slot and keyed by doc exactly like espn_gpu_prefetch_hints; the next
  * espn_gpu_rerank carrying ESPN_RERANK_PREFETCHED finds them (hits).  HBM-
  * resident docs, other shards' and unknown ids are skipped.  Works for any
- * streamed tiered table (host-tier docs may be handed over too). */
+ * streamed tiered table (host-tier docs may be handed over too).  The rows
+ * handed over must fit the workspace's staging slot (staging_bytes, all of
+ * it -- host-tier hints use half), else INVALID_CONFIG. */
 ESPN_API int espn_gpu_prefetch_rows(espn_gpu_table* table, espn_gpu_workspace* ws, uint32_t n_queries,
                                     const uint32_t* ids, const uint64_t* id_offsets, const void* rows,
                                     const uint64_t* row_byte_off, uint64_t rows_bytes, void* side_stream);

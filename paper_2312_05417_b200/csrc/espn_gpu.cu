@@ -2034,7 +2034,9 @@ int prefetch_hint_impl(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B, con
   hp.hint_map = w->hint_map;
   hp.epoch = w->hint_epoch;
   hp.stage = st.buf;
-  hp.stage_cap = w->staging_bytes / 2;
+  // host-tier hints keep half of the slot for the critical-path misses; rows
+  // handed over by the caller may fill it (a disk-tier doc has no fallback)
+  hp.stage_cap = ext_rows ? w->staging_bytes : w->staging_bytes / 2;
   hp.cursor = st.cursor;
   hp.qstats = st.qstats;
   hp.err = w->err;
@@ -2076,6 +2078,7 @@ int espn_gpu_prefetch_rows(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B,
   // reads whole 16-byte chunks); unknown ids and other shards' ids are
   // ignored like hints
   const uint64_t rowb = (uint64_t)t->d * 2;
+  uint64_t total = 0;
   for (uint64_t j = 0; j < nh; ++j) {
     if (row_byte_off[j] % 16) return fail(ESPN_E_INVALID_INPUT, "row_byte_off must be 16-byte aligned");
     const uint32_t id = ids[j];
@@ -2087,7 +2090,11 @@ int espn_gpu_prefetch_rows(espn_gpu_table* t, espn_gpu_workspace* w, uint32_t B,
     if (loc >= t->n_docs) continue;
     const uint64_t bytes = (t->h_row_ptr.size() > loc + 1 ? t->h_row_ptr[loc + 1] - t->h_row_ptr[loc] : 0) * rowb;
     if (row_byte_off[j] + bytes > rows_bytes) return fail(ESPN_E_INVALID_INPUT, "a doc's rows run past rows_bytes");
+    total += bytes;
   }
+  if (total > w->staging_bytes)
+    return fail(ESPN_E_INVALID_CONFIG, "the handed-over rows (" + std::to_string(total) + " B) exceed the workspace's "
+                                       "staging slot (" + std::to_string(w->staging_bytes) + " B): raise staging_bytes");
   return prefetch_hint_impl(t, w, B, ids, id_offsets, 0, side_stream, rows, row_byte_off, rows_bytes);
 }
 

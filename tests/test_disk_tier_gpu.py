@@ -104,4 +104,12 @@ def test_prefetch_rows_input_checks(tmp_path, cuda_ok):
         rr.prefetch_rows(ids, np.array([0, 3], np.uint64), np.zeros(1 << 16, np.uint8), np.array([0, 8, 16], np.uint64))
     with pytest.raises(api.InvalidInputError):  # decreasing offsets
         rr.prefetch_rows(ids, np.array([0, 2, 1], np.uint64), np.zeros(1 << 16, np.uint8), np.zeros(3, np.uint64))
-    rr.close(); disk.close()
+    rr.close()
+    small = api.Reranker(disk, 2, 400, 32, staging_bytes=4096)  # rows larger than the staging slot
+    nd = disk.n_docs
+    many = np.arange(nd, dtype=np.uint32)[:200]
+    tok = disk.token_counts(many).astype(np.uint64)
+    boff = np.concatenate([[0], np.cumsum(tok * 64)[:-1]]).astype(np.uint64)
+    with pytest.raises(api.InvalidConfigError):
+        small.prefetch_rows(many, np.array([0, 200, 200], np.uint64), np.zeros(int(tok.sum()) * 64, np.uint8), boff)
+    small.close(); disk.close()

@@ -42,7 +42,8 @@ t_build = time.time() - t0
 resident = (np.random.default_rng(1).random(N) < 0.2).astype(np.uint8)
 disk = api.GpuStore.open_store(base, resident=resident, disk_tier=True)
 reader = api.StoreReader(base, mode="direct", queue_depth=QD)
-rr = api.Reranker(disk, B, B * K, 32)
+# a batch's misses (~51 K docs x ~2.2 KB) must fit one staging slot
+rr = api.Reranker(disk, B, B * K, 32, staging_bytes=256 << 20)
 cfg = api.PipelineConfig(rerank_count=R, final_k=k)
 
 batches = []
