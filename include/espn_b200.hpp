@@ -202,12 +202,17 @@ class Store {
   // resident docs in HBM when `resident` is given -- and filled in chunks of
   // chunk_bytes, so the store is never read whole; the record layout comes
   // from the manifest.
+  // disk_tier (with `resident`): the non-resident docs stay ONLY in the file
+  // (ESPN_TABLE_DISK_TIER, the paper's SSD tier); batches that need them are
+  // staged by Reranker::prefetch_from_file and re-ranked with prefetched = true.
   static Store open_store(const std::string& base, Dtype dtype = Dtype::f16, int device = 0,
-                          std::span<const std::uint8_t> resident = {}, std::uint64_t chunk_bytes = 64ull << 20);
+                          std::span<const std::uint8_t> resident = {}, std::uint64_t chunk_bytes = 64ull << 20,
+                          bool disk_tier = false);
   // ESPN_TABLE_STREAMED: an empty table allocated from row_ptr (+ resident),
   // filled in doc order by load_rows (plain 2-byte codes of the next docs).
   static Store streamed(std::span<const std::uint64_t> row_ptr, std::uint32_t d, Dtype dtype = Dtype::f16,
-                        RecordLayout layout = {}, int device = 0, std::span<const std::uint8_t> resident = {});
+                        RecordLayout layout = {}, int device = 0, std::span<const std::uint8_t> resident = {},
+                        bool disk_tier = false);
   void load_rows(std::uint64_t doc_begin, std::uint64_t n_docs, std::span<const std::uint16_t> codes);
   ~Store();
   Store(Store&&) noexcept;
@@ -218,6 +223,7 @@ class Store {
   espn_gpu_table* handle() const { return table_; }
   std::uint32_t d() const { return d_; }
   Dtype dtype() const { return dtype_; }
+  const RecordLayout& layout() const { return layout_; }
   std::uint64_t n_docs() const { return row_ptr_.empty() ? 0 : row_ptr_.size() - 1; }
   std::uint32_t token_count(DocId id) const;
   std::uint64_t record_bytes(std::uint32_t token_count) const;
@@ -236,11 +242,14 @@ class Store {
   class Reranker& thread_reranker(std::uint32_t max_queries, std::uint32_t max_candidates,
                                   std::uint32_t max_query_tokens) const;
 
+  // Tier of doc `id` (tiered stores): true = HBM-resident.
+  bool resident(DocId id) const { return resident_.empty() || resident_[id] != 0; }
+
  private:
   struct WorkspaceCache;
   struct StreamedTag {};
   Store(StreamedTag, std::span<const std::uint64_t> row_ptr, std::uint32_t d, Dtype dtype, RecordLayout layout,
-        int device, std::span<const std::uint8_t> resident);
+        int device, std::span<const std::uint8_t> resident, bool disk_tier);
   std::unique_ptr<WorkspaceCache> cache_;
   espn_gpu_table* table_ = nullptr;
   std::uint32_t d_ = 0;
@@ -248,6 +257,7 @@ class Store {
   RecordLayout layout_;
   int device_ = 0;
   std::vector<std::uint64_t> row_ptr_;  // host copy for byte accounting
+  std::vector<std::uint8_t> resident_;  // tiered stores: the residency mask
 };
 
 // A reusable batch context (one workspace = per-stream scratch).  Not
@@ -255,7 +265,7 @@ class Store {
 class Reranker {
  public:
   Reranker(const Store& store, std::uint32_t max_queries, std::uint32_t max_candidates,
-           std::uint32_t max_query_tokens = 32);
+           std::uint32_t max_query_tokens = 32, std::uint64_t staging_bytes = 0);
   ~Reranker();
   Reranker(const Reranker&) = delete;
   Reranker& operator=(const Reranker&) = delete;
@@ -285,6 +295,17 @@ class Reranker {
   void prefetch_hints(std::span<const CandidateList> snapshots, std::uint32_t top_k = 0,
                       void* side_stream = nullptr);
 
+  // The disk tier's prefetcher (ESPN_TABLE_DISK_TIER stores): reads the
+  // records of each list's first `top_k` entries (0 = all) that are not in
+  // HBM from the store file through `reader` (espn_store_fetch: O_DIRECT /
+  // buffered / mmap, queue_depth reads in flight -- the reference's own
+  // StoreHandle::fetch_batch) into a pinned buffer and stages their rows
+  // (espn_gpu_prefetch_rows) on side_stream.  Pass the final lists with
+  // top_k = rerank_count so every needed doc is staged; the next
+  // rerank(..., prefetched = true) finds them.  Returns the bytes read.
+  std::uint64_t prefetch_from_file(std::span<const CandidateList> lists, std::uint32_t top_k,
+                                   espn_store_reader* reader, void* side_stream = nullptr);
+
   espn_counters counters() const;
 
  private:
@@ -294,6 +315,8 @@ class Reranker {
   std::vector<std::uint32_t> hint_ids_;   // last prefetch_hints snapshot (CSR)
   std::vector<std::uint64_t> hint_off_;
   std::vector<espn_fetch_stats> last_fs_;
+  std::uint8_t* pinned_ = nullptr;  // prefetch_from_file: record payloads (cudaHostAlloc, grown)
+  std::uint64_t pinned_cap_ = 0;
 };
 
 // QueryStats of one query exactly as the reference computes them

@@ -3,6 +3,8 @@
 // computed by libespn_gpu.so.
 #include "espn_b200.hpp"
 
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -176,9 +178,9 @@ Store Store::from_documents(const std::vector<EmbeddingMatrix>& docs, Dtype dtyp
 }
 
 Store::Store(StreamedTag, std::span<const std::uint64_t> row_ptr, std::uint32_t d, Dtype dtype, RecordLayout layout,
-             int device, std::span<const std::uint8_t> resident)
+             int device, std::span<const std::uint8_t> resident, bool disk_tier)
     : cache_(std::make_unique<WorkspaceCache>()), d_(d), dtype_(dtype), layout_(layout), device_(device),
-      row_ptr_(row_ptr.begin(), row_ptr.end()) {
+      row_ptr_(row_ptr.begin(), row_ptr.end()), resident_(resident.begin(), resident.end()) {
   if (row_ptr.size() < 2) throw InvalidInputError("empty table");
   espn_table_desc desc{};
   desc.n_docs = row_ptr.size() - 1;
@@ -187,7 +189,7 @@ Store::Store(StreamedTag, std::span<const std::uint64_t> row_ptr, std::uint32_t 
   desc.d_cls = layout.d_cls;
   desc.value_width = layout.value_width;
   desc.alignment = layout.alignment;
-  desc.flags = ESPN_TABLE_STREAMED;
+  desc.flags = ESPN_TABLE_STREAMED | (disk_tier ? ESPN_TABLE_DISK_TIER : 0u);
   desc.row_ptr = row_ptr.data();
   desc.rows = nullptr;
   desc.device = device;
@@ -199,8 +201,8 @@ Store::Store(StreamedTag, std::span<const std::uint64_t> row_ptr, std::uint32_t 
 }
 
 Store Store::streamed(std::span<const std::uint64_t> row_ptr, std::uint32_t d, Dtype dtype, RecordLayout layout,
-                      int device, std::span<const std::uint8_t> resident) {
-  return Store(StreamedTag{}, row_ptr, d, dtype, layout, device, resident);
+                      int device, std::span<const std::uint8_t> resident, bool disk_tier) {
+  return Store(StreamedTag{}, row_ptr, d, dtype, layout, device, resident, disk_tier);
 }
 
 void Store::load_rows(std::uint64_t doc_begin, std::uint64_t n_docs, std::span<const std::uint16_t> codes) {
@@ -211,7 +213,7 @@ void Store::load_rows(std::uint64_t doc_begin, std::uint64_t n_docs, std::span<c
 }
 
 Store Store::open_store(const std::string& base, Dtype dtype, int device, std::span<const std::uint8_t> resident,
-                        std::uint64_t chunk_bytes) {
+                        std::uint64_t chunk_bytes, bool disk_tier) {
   auto check_store = [](int st) {
     if (st != ESPN_OK) throw_status(st, espn_store_last_error());
   };
@@ -223,7 +225,7 @@ Store Store::open_store(const std::string& base, Dtype dtype, int device, std::s
   check_store(espn_store_records(rd, recs.data()));
   std::vector<std::uint64_t> rp(h.count + 1, 0);
   for (std::uint64_t i = 0; i < h.count; ++i) rp[i + 1] = rp[i] + recs[i].token_count;
-  Store s = streamed(rp, h.d, dtype, RecordLayout{h.d_cls, h.value_width, h.alignment}, device, resident);
+  Store s = streamed(rp, h.d, dtype, RecordLayout{h.d_cls, h.value_width, h.alignment}, device, resident, disk_tier);
   const std::uint64_t max_tok = std::max<std::uint64_t>(chunk_bytes / (2ull * h.d), 1);
   std::vector<std::uint16_t> codes;
   std::vector<std::uint64_t> lrp;
@@ -322,9 +324,10 @@ FetchResult Store::fetch_batch(std::span<const DocId> doc_ids) const {
 
 // ---------------------------------------------------------------- Reranker
 Reranker::Reranker(const Store& store, std::uint32_t max_queries, std::uint32_t max_candidates,
-                   std::uint32_t max_query_tokens)
+                   std::uint32_t max_query_tokens, std::uint64_t staging_bytes)
     : store_(&store) {
   espn_workspace_desc desc{};
+  desc.staging_bytes = staging_bytes;
   desc.max_queries = std::max(max_queries, 1u);
   desc.max_candidates = std::max(max_candidates, 1u);
   desc.max_query_tokens = max_query_tokens;
@@ -336,6 +339,55 @@ Reranker::Reranker(const Store& store, std::uint32_t max_queries, std::uint32_t 
 
 Reranker::~Reranker() {
   if (ws_) espn_gpu_workspace_destroy(ws_);
+  if (pinned_) cudaFreeHost(pinned_);
+}
+
+std::uint64_t Reranker::prefetch_from_file(std::span<const CandidateList> lists, std::uint32_t top_k,
+                                           espn_store_reader* reader, void* side_stream) {
+  if (!reader) throw InvalidInputError("prefetch_from_file: null store reader");
+  if (store_->layout().value_width != 2 || store_->dtype() != Dtype::f16)
+    throw InvalidConfigError("prefetch_from_file: the file's values must be the table's codes "
+                             "(value_width 2 store, f16 table)");
+  const std::uint32_t B = static_cast<std::uint32_t>(lists.size());
+  if (B == 0) return 0;
+  // the needed docs of each list that are not in HBM (store.hpp:91-94 order)
+  std::vector<std::uint64_t> off(B + 1, 0);
+  std::vector<std::uint32_t> ids;
+  for (std::uint32_t b = 0; b < B; ++b) {
+    const std::size_t n = lists[b].entries.size();
+    const std::size_t m = top_k ? std::min<std::size_t>(n, top_k) : n;
+    for (std::size_t j = 0; j < m; ++j) {
+      const DocId id = lists[b].entries[j].doc_id;
+      if (id < store_->n_docs() && !store_->resident(id)) ids.push_back(static_cast<std::uint32_t>(id));
+    }
+    off[b + 1] = ids.size();
+  }
+  auto check_store = [](int st) {
+    if (st != ESPN_OK) throw_status(st, espn_store_last_error());
+  };
+  const std::uint64_t n = ids.size();
+  std::vector<std::uint64_t> rec_off(n + 1, 0);
+  std::uint64_t br = 0, bl = 0;
+  double secs = 0;
+  check_store(espn_store_fetch(reader, ids.data(), n, nullptr, rec_off.data(), 0, &br, &bl, &secs));  // sizes
+  if (rec_off[n] > pinned_cap_) {
+    if (pinned_) cudaFreeHost(pinned_);
+    pinned_ = nullptr;
+    pinned_cap_ = 0;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&pinned_), rec_off[n], cudaHostAllocDefault) != cudaSuccess)
+      throw espn::Error("prefetch_from_file: pinned buffer allocation failed");
+    pinned_cap_ = rec_off[n];
+  }
+  check_store(espn_store_fetch(reader, ids.data(), n, pinned_, rec_off.data(), pinned_cap_, &br, &bl, &secs));
+  // each record is [CLS d_cls x value_width | BOW rows]: the rows follow the CLS
+  std::vector<std::uint64_t> row_off(n);
+  const std::uint64_t cls_bytes = static_cast<std::uint64_t>(store_->layout().d_cls) * store_->layout().value_width;
+  for (std::uint64_t j = 0; j < n; ++j) row_off[j] = rec_off[j] + cls_bytes;
+  check(espn_gpu_prefetch_rows(store_->handle(), ws_, B, ids.data(), off.data(), pinned_, row_off.data(), rec_off[n],
+                               side_stream));
+  hint_ids_ = std::move(ids);  // the prefetched ids of the next prefetched rerank (QueryStats)
+  hint_off_ = std::move(off);
+  return br;
 }
 
 espn_counters Reranker::counters() const {

@@ -231,6 +231,44 @@ int main() {
       CHECK(hbm.stats[b].hit_rate == 0.0, "no prefetch, hit rate 0");
     }
   }
+  // ---- the disk tier: only ~1/3 of the docs in HBM, the rest read from the file per batch ----
+  {
+    std::vector<float> rows;
+    for (const auto& m : docs) rows.insert(rows.end(), m.values.begin(), m.values.end());
+    const std::string base = "/tmp/espn_host_api_test_disk";
+    espn::gpu::build_store(base, rp, rows, d, {}, espn::gpu::RecordLayout{16, 2, 512});
+    std::vector<std::uint8_t> resident(n_docs);
+    for (std::uint32_t i = 0; i < n_docs; ++i) resident[i] = (i * 2654435761u >> 9) % 3 == 0;
+    espn::gpu::Store disk = espn::gpu::Store::open_store(base, espn::gpu::Dtype::f16, 0, resident, 64ull << 20,
+                                                         /*disk_tier=*/true);
+    espn_store_reader* rd = nullptr;
+    espn_store_header hh{};
+    CHECK(espn_store_open(base.c_str(), ESPN_READ_DIRECT, 16, &rd, &hh) == ESPN_OK, "store open (direct)");
+    espn::gpu::Reranker rd_r(disk, B, B * K, nq);
+    espn::gpu::Reranker rh(store, B, B * K, nq);
+    espn::PipelineConfig cfg;
+    cfg.rerank_count = K;
+    bool thrown = false;  // not prefetched: the rows exist only in the file
+    try { rd_r.rerank(qs, cl, cfg, espn::gpu::Kernel::tcgen05); } catch (const espn::InvalidStateError&) { thrown = true; }
+    CHECK(thrown, "disk tier without prefetch must throw InvalidStateError");
+    const std::uint64_t got_bytes = rd_r.prefetch_from_file(cl, cfg.rerank_count, rd);
+    CHECK(got_bytes > 0, "prefetch_from_file read the misses");
+    espn::BatchResult a = rd_r.rerank(qs, cl, cfg, espn::gpu::Kernel::tcgen05, /*prefetched=*/true);
+    espn::BatchResult h = rh.rerank(qs, cl, cfg, espn::gpu::Kernel::tcgen05);
+    for (std::uint32_t b = 0; b < B; ++b) {
+      CHECK(a.rankings[b].entries.size() == h.rankings[b].entries.size(), "disk ranking size q%u", b);
+      for (std::size_t j = 0; j < a.rankings[b].entries.size() && j < h.rankings[b].entries.size(); ++j)
+        CHECK(a.rankings[b].entries[j].doc_id == h.rankings[b].entries[j].doc_id &&
+                  a.rankings[b].entries[j].score == h.rankings[b].entries[j].score,
+              "disk ranking q%u pos %zu", b, j);
+      std::uint64_t miss = 0;
+      for (std::uint32_t j = 0; j < cfg.rerank_count && j < cl[b].entries.size(); ++j) miss += !resident[cl[b].entries[j].doc_id];
+      CHECK(rd_r.last_fetch_stats()[b].prefetched == miss && rd_r.last_fetch_stats()[b].missed == 0,
+            "q%u disk-tier hits %llu vs %llu", b, (unsigned long long)rd_r.last_fetch_stats()[b].prefetched,
+            (unsigned long long)miss);
+    }
+    espn_store_close(rd);
+  }
   // ---- error mapping (error.hpp:8-42) ----
   {
     espn::PipelineConfig cfg;

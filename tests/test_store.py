@@ -194,3 +194,27 @@ def test_python_wrapper_bounds_checks(tmp_path):
         api.build_store(tmp_path / "b", rp, np.zeros((5, 8), np.float32), 8, 16, cls=np.zeros((1, 16), np.float32))
     with pytest.raises(api.InvalidInputError):
         api.build_store(tmp_path / "b", np.array([1, 3], np.uint64), np.zeros((3, 8), np.float32), 8)
+
+
+@pytest.mark.parametrize("mode", ["direct", "buffered", "mmap"])
+def test_store_reader_fetch_rows(tmp_path, mode):
+    """api.StoreReader (the file-backed StoreHandle, store.hpp:56-112) -- the
+    host side of the disk tier: request order, duplicates, the BOW rows at
+    row_offsets() are the store's fp16 codes, direct-mode counters aligned."""
+    rp, codes = synth.make_table(300, 32, 1, 40, seed=4)
+    base = tmp_path / "r"
+    api.build_store(base, rp, api.decode(codes, "f16"), 32, d_cls=16, alignment=512)
+    rd = api.StoreReader(base, mode=mode, queue_depth=4)
+    ids = np.array([5, 299, 5, 0, 17], np.uint32)
+    buf, off, ctr = rd.fetch(ids)
+    roff = rd.row_offsets(off)
+    for j, i in enumerate(ids):
+        t = int(rp[i + 1] - rp[i])
+        got = np.frombuffer(buf[int(roff[j]):int(roff[j]) + t * 64].tobytes(), np.uint16)
+        assert np.array_equal(got, codes[int(rp[i]) * 32:int(rp[i + 1]) * 32])
+        assert int(off[j + 1] - off[j]) == (16 + t * 32) * 2
+    if mode == "direct":
+        assert ctr["bytes_read"] % 512 == 0 and ctr["bytes_read"] >= int(off[-1])
+    with pytest.raises(api.InvalidInputError):
+        rd.fetch(np.array([300], np.uint32))
+    rd.close()

@@ -12,7 +12,7 @@ call releases the GIL) overlaps batch n's staging and scoring -- the paper's
 prefetch-while-scoring structure.  Rankings are checked against the same
 table fully in HBM on the first batches.
 
-usage: python tools/disk_tier_bench.py [n_docs] [queue_depth] [out.json]
+usage: python tools/disk_tier_bench.py [n_docs] [queue_depth] [out.json] [alignment]
 """
 import json
 import os
@@ -30,13 +30,14 @@ from paper_2312_05417_b200 import api, synth  # noqa: E402
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 500_000
 QD = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 OUT = sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/disk_tier.json"
+ALIGN = int(sys.argv[4]) if len(sys.argv) > 4 else 4096  # store alignment (SPEC: 1, 512 or 4096)
 B, K, R, k, d = 64, 1000, 1000, 10, 32
 NB = 12  # distinct batches
 
 t0 = time.time()
 rp, codes = synth.make_table(N, d, 1, 63, seed=41)
 base = Path(os.environ.get("ESPN_DISK_DIR", "/tmp")) / "espn_disk_tier"
-api.build_store(base, rp, api.decode(codes, "f16"), d, d_cls=128, alignment=4096)
+api.build_store(base, rp, api.decode(codes, "f16"), d, d_cls=128, alignment=ALIGN)
 file_bytes = (base.with_suffix(".espn")).stat().st_size
 t_build = time.time() - t0
 resident = (np.random.default_rng(1).random(N) < 0.2).astype(np.uint8)
@@ -123,7 +124,8 @@ res_j = {
     "workload": "configs[3] on NVMe: %d docs (t~U{1..63}, d32 fp16), 20%% resident in HBM, the rest only in the "
                 ".espn file on the box's disk; batch %d x %d candidates, R=%d, top-%d" % (N, B, K, R, k),
     "store_file_bytes": file_bytes, "store_build_s": round(t_build, 1),
-    "reader": {"mode": "direct (O_DIRECT)", "queue_depth": QD, "alignment": 4096},
+    "reader": {"mode": "direct (O_DIRECT)", "queue_depth": QD, "alignment": ALIGN},
+    "payload_bytes_per_batch": float(np.mean(sizes)),
     "miss_docs_per_batch": miss_docs,
     "disk_bytes_per_batch": bytes_read / steps,
     "serial": {"ms_per_batch": serial_step * 1e3, "queries_per_s": B / serial_step,
