@@ -63,9 +63,14 @@ struct TcCfg;
 template <bool S> struct TcCfg<16, S>  { static constexpr int NQC = 128, NS = 6, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
 #ifndef ESPN_D32_NQC
 #define ESPN_D32_NQC 128
+#endif
+#ifndef ESPN_D32_NS
 #define ESPN_D32_NS 4
 #endif
-template <bool S> struct TcCfg<32, S>  { static constexpr int NQC = ESPN_D32_NQC, NS = ESPN_D32_NS, UNITMAX = 64, NU = 3; static constexpr bool REPA = false; };
+#ifndef ESPN_D32_NU
+#define ESPN_D32_NU 3
+#endif
+template <bool S> struct TcCfg<32, S>  { static constexpr int NQC = ESPN_D32_NQC, NS = S ? 4 : ESPN_D32_NS, UNITMAX = 64, NU = S ? 3 : ESPN_D32_NU; static constexpr bool REPA = false; };
 template <bool S> struct TcCfg<64, S>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = S ? 2 : 3; static constexpr bool REPA = false; };
 template <bool S> struct TcCfg<128, S> { static constexpr int NQC = 64,  NS = 2, UNITMAX = 32, NU = S ? 1 : 2; static constexpr bool REPA = true; };
 
@@ -425,9 +430,33 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
   rs.rot = (uint32_t)(((uint64_t)rs.rot + n_units) % G);
   typename L::Unit* units = S.units;
   uint8_t* smem = S.smem;
+  // ESPN_DEBUG bit 8: per warp, cycles of this batch and cycles spent waiting
+  // on mbarriers, summed over all CTAs into g_cta_prof[2 * warp + {0, 1}]
+  // (tools/role_profile.py) -- which role is the bottleneck
+#ifndef ESPN_NO_ROLE_PROFILE
+  const bool tr = (p.dbg & 8u) != 0;
+#else
+  constexpr bool tr = false;
+#endif
+  unsigned long long wacc = 0;
+  const long long tb0 = tr ? clock64() : 0;
+#define ESPN_WAIT(bar, par)                      \
+  do {                                           \
+    if (tr) {                                    \
+      const long long t0_ = clock64();           \
+      espn_ptx::mbar_wait(bar, par);             \
+      wacc += (unsigned long long)(clock64() - t0_); \
+    } else {                                     \
+      espn_ptx::mbar_wait(bar, par);             \
+    }                                            \
+  } while (0)
 
   if (warp == L::LOADER_WARP) {
     // ============================ UNIT LOADER ===================================
+    // (Software-pipelining the three dependent metadata round trips across
+    // units -- unit table of it+2, ids of it+1, row_ptr of it in one go -- was
+    // measured: the loader's busy share fell from 91 to 84 % but the step did
+    // not get faster, 37.5 vs 37.1 us; tools/role_profile.py.)
     for (uint32_t it = 0; it < cnt; ++it) {
       const uint32_t ug = first + it * G, gi = gu0 + it;
       const uint32_t us = gi % L::NU;
@@ -461,7 +490,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
           }
         }
       }
-      mbar_wait(&S.uempty_bar[us], ((gi / L::NU) & 1) ^ 1);
+      ESPN_WAIT(&S.uempty_bar[us], ((gi / L::NU) & 1) ^ 1);
       for (int i = lane; i < L::MAXW; i += 32) U.bitmap[i] = 0;
       for (int i = lane; i < L::MAX_STAGES; i += 32) {
         U.op_beg[i] = 0xFFFFFFFFu;
@@ -555,13 +584,13 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
     for (uint32_t it = 0; it < cnt; ++it) {
       const uint32_t gi = gu0 + it, us = gi % L::NU;
       const typename L::Unit& U = units[us];
-      mbar_wait(&S.ufull_bar[us], (gi / L::NU) & 1);
+      ESPN_WAIT(&S.ufull_bar[us], (gi / L::NU) & 1);
       const uint32_t Sl = U.S, npt = U.n_pt;
       const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       uint32_t pc = 0;  // next patch of the unit (patches are in stage order)
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t s = gs % L::NS;
-        mbar_wait(&S.full_bar[s], (gs / L::NS) & 1);
+        ESPN_WAIT(&S.full_bar[s], (gs / L::NS) & 1);
         uint8_t* stage = S.sB + s * L::STAGE_BYTES;
         for (;;) {
           const uint32_t i = pc + lane;
@@ -603,7 +632,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       const uint32_t ug = first + it * G, gi = gu0 + it, us = gi % L::NU;
       const uint4 ue = __ldcg(&p.unit_tab[ug]);
       const uint32_t b = ue.x, tail = ue.y >> 31;
-      mbar_wait(&S.uempty_bar[us], ((gi / L::NU) & 1) ^ 1);
+      ESPN_WAIT(&S.uempty_bar[us], ((gi / L::NU) & 1) ^ 1);
       // Query tokens -> A slot `us` (rows 96+128*us .. +32), converted to the
       // table dtype; rows >= nq stay zero.  Item e = (row i, 8-value chunk c);
       // batches of 4 items per lane keep all their loads in flight together.
@@ -678,7 +707,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
     for (uint32_t it = 0; it < cnt; ++it) {
       const uint32_t gi = gu0 + it, us = gi % L::NU;
       const typename L::Unit& U = units[us];
-      mbar_wait(&S.ufull_bar[us], (gi / L::NU) & 1);
+      ESPN_WAIT(&S.ufull_bar[us], (gi / L::NU) & 1);
       const uint32_t Sl = U.S;
       const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
@@ -686,7 +715,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
         // ops [o0, o1) of this stage (loader-planned); this warp issues parity pw
         const uint32_t o0 = U.op_beg[st], o1 = st + 1 < n_st ? U.op_beg[st + 1] : U.n_ops;
         uint32_t bytes = U.stage_tx[st][pw];
-        mbar_wait(&S.empty_bar[s], ((gs / L::NS) & 1) ^ 1);
+        ESPN_WAIT(&S.empty_bar[s], ((gs / L::NS) & 1) ^ 1);
         if (p.dbg & 4u) bytes = 0;
         if (lane == 0) mbar_arrive_expect_tx(&S.full_bar[s], bytes);
         __syncwarp();
@@ -709,13 +738,13 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
     const uint32_t a_base = smem_u32(S.sA), b_base = smem_u32(S.sB);
     for (uint32_t it = 0; it < cnt; ++it) {
       const uint32_t gi = gu0 + it, us = gi % L::NU;
-      mbar_wait(&S.ufull_bar[us], (gi / L::NU) & 1);
+      ESPN_WAIT(&S.ufull_bar[us], (gi / L::NU) & 1);
       const uint32_t Sl = units[us].S;
       const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t s = gs % L::NS, buf = gs % L::NBUF;
-        mbar_wait(&S.patched_bar[s], (gs / L::NS) & 1);  // rows landed and pads patched
-        mbar_wait(&S.tempty_bar[buf], ((gs / L::NBUF) & 1) ^ 1);
+        ESPN_WAIT(&S.patched_bar[s], (gs / L::NS) & 1);  // rows landed and pads patched
+        ESPN_WAIT(&S.tempty_bar[buf], ((gs / L::NBUF) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = S.tmem_base + buf * L::BUFC;
         const uint32_t x0 = st * L::STAGE_SLOTS;
@@ -782,13 +811,13 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
     for (uint32_t it = 0; it < cnt; ++it) {
       const uint32_t gi = gu0 + it, us = gi % L::NU;
       const typename L::Unit& U = units[us];
-      mbar_wait(&S.ufull_bar[us], (gi / L::NU) & 1);
+      ESPN_WAIT(&S.ufull_bar[us], (gi / L::NU) & 1);
       const uint32_t Sl = U.S;
       int* my_pm = reinterpret_cast<int*>(S.pm) + (us * 32 + lane) * L::PM_STRIDE;
       const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t buf = gs % L::NBUF;
-        mbar_wait(&S.tfull_bar[buf], (gs / L::NBUF) & 1);
+        ESPN_WAIT(&S.tfull_bar[buf], (gs / L::NBUF) & 1);
         tc_fence_after();
         const uint32_t xw = st * L::STAGE_SLOTS + w * L::NQC + h * L::HALF;
         const int remv = (p.dbg & 1u) ? 0 : (int)Sl - (int)xw;
@@ -865,7 +894,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
     for (uint32_t it = 0; it < cnt; ++it) {
       const uint32_t gi = gu0 + it, us = gi % L::NU;
       const typename L::Unit& U = units[us];
-      mbar_wait(&S.edone_bar[us], (gi / L::NU) & 1);
+      ESPN_WAIT(&S.edone_bar[us], (gi / L::NU) & 1);
       const uint32_t nd = U.nd, tail = U.tail;
       const uint64_t j0 = U.cfirst;
       int* pmu = reinterpret_cast<int*>(S.pm) + us * 32 * L::PM_STRIDE;
@@ -886,7 +915,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       if (ESPN_ARRIVE_ALL || lane == 0) mbar_arrive(&S.uempty_bar[us]);  // slot free
       if (fused) {
         const uint32_t j = gi % L::NB;
-        mbar_wait(&S.bfree_bar[j], ((gi / L::NB) & 1) ^ 1);
+        ESPN_WAIT(&S.bfree_bar[j], ((gi / L::NB) & 1) ^ 1);
 #pragma unroll
         for (int r = 0; r < NK; ++r) ring[j * L::UNITMAX + r * 32 + lane] = bow[r];
         __syncwarp();
@@ -944,7 +973,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
         clv[r] = k < nd ? __ldcg(&p.cand_cls[j0 + k]) : 0.0f;
       }
       const uint32_t j = gi % L::NB;
-      mbar_wait(&S.bdone_bar[j], (gi / L::NB) & 1);
+      ESPN_WAIT(&S.bdone_bar[j], (gi / L::NB) & 1);
       float bow[NK];
 #pragma unroll
       for (int r = 0; r < NK; ++r) bow[r] = ring[j * L::UNITMAX + r * 32 + lane];
@@ -1015,6 +1044,11 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       }
     }
   }
+  if (tr && lane == 0) {
+    atomicAdd(&g_cta_prof[2 * warp], (unsigned long long)(clock64() - tb0));
+    atomicAdd(&g_cta_prof[2 * warp + 1], wacc);
+  }
+#undef ESPN_WAIT
 }
 
 template <int D, bool SPLIT>

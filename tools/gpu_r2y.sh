@@ -1,0 +1,4 @@
+# stage ring depth A/B on the served C2 step (d=32 non-split kernel)
+L=paper_2312_05417_b200/lib/libespn_gpu.so
+for v in base ns5nu2 ns4nu2 base ns5nu2 ns4nu2; do cp tools/ab/libespn_gpu_$v.so $L; printf "%s " $v; timeout 300 python tools/server_knobs.py 0 on 2>&1 | tail -1; done
+cp tools/ab/libespn_gpu_base.so $L
