@@ -47,7 +47,10 @@ def build_lib(verbose: bool = False, force: bool = False) -> Path:
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [NVCC, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp), str(CSRC / "espn_gpu.cu"),
+    # ESPN_NVCC_DEFINES: extra -D flags for measurement builds (e.g. -DESPN_ROLE_PROFILE
+    # for tools/role_profile.py); production builds leave it unset
+    extra = os.environ.get("ESPN_NVCC_DEFINES", "").split()
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-o", str(tmp), str(CSRC / "espn_gpu.cu"),
            "-lcudart"]
     if verbose:
         cmd.insert(1, "-Xptxas")

@@ -64,6 +64,9 @@ template <bool S> struct TcCfg<16, S>  { static constexpr int NQC = 128, NS = 6,
 #ifndef ESPN_D32_NQC
 #define ESPN_D32_NQC 128
 #endif
+#ifndef ESPN_MMA_DESC
+#define ESPN_MMA_DESC 0  // A/B knob: 1 = descriptors stepped per quarter instead of rebuilt per MMA
+#endif
 #ifndef ESPN_D32_NS
 #define ESPN_D32_NS 4
 #endif
@@ -108,10 +111,19 @@ struct TcLayout {
   static constexpr int NPROD = 2;                  // bulk-copy producer warps
   static constexpr int PLANES = ESPN_PLANES;       // issuing lanes per producer warp
   static constexpr int NEPI = 8;                   // epilogue warps: 4 lane quarters x 2 column halves
+#ifndef ESPN_MMA_WARP_LATE
   static constexpr int MMA_WARP = NEPI;
   static constexpr int PROD_WARP0 = NEPI + 1;
   static constexpr int LOADER_WARP = PROD_WARP0 + NPROD;
   static constexpr int COMBINE_WARP = LOADER_WARP + 1;
+#else
+  // A/B knob: the MMA warp on SM sub-partition 3 (warp % 4), beside the
+  // lightest roles (query tile, epilogue quarter 3)
+  static constexpr int PROD_WARP0 = NEPI;
+  static constexpr int LOADER_WARP = PROD_WARP0 + NPROD;
+  static constexpr int MMA_WARP = LOADER_WARP + 1;
+  static constexpr int COMBINE_WARP = MMA_WARP + 1;
+#endif
   static constexpr int DEDUP_WARP = COMBINE_WARP + 1;  // fused top-k: duplicate check
   static constexpr int RANK_WARP = DEDUP_WARP + 1;     // fused top-k: keys, unit top-k
   static constexpr int QUERY_WARP = RANK_WARP + 1;     // unit query tile -> A operand slot
@@ -433,22 +445,34 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
   // ESPN_DEBUG bit 8: per warp, cycles of this batch and cycles spent waiting
   // on mbarriers, summed over all CTAs into g_cta_prof[2 * warp + {0, 1}]
   // (tools/role_profile.py) -- which role is the bottleneck
-#ifndef ESPN_NO_ROLE_PROFILE
+#ifdef ESPN_ROLE_PROFILE  // opt-in build (tools/role_profile.py): even unexecuted, it costs ~15% on C2
   const bool tr = (p.dbg & 8u) != 0;
 #else
   constexpr bool tr = false;
 #endif
   unsigned long long wacc = 0;
   const long long tb0 = tr ? clock64() : 0;
-#define ESPN_WAIT(bar, par)                      \
-  do {                                           \
-    if (tr) {                                    \
-      const long long t0_ = clock64();           \
-      espn_ptx::mbar_wait(bar, par);             \
-      wacc += (unsigned long long)(clock64() - t0_); \
-    } else {                                     \
-      espn_ptx::mbar_wait(bar, par);             \
-    }                                            \
+  // (and per barrier kind: g_cta_prof[64 + 12 * warp + kind], kind = the
+  // barrier array: full, empty, tfull, tempty, ufull, uempty, edone, bdone,
+  // bfree, patched)
+  auto bar_kind = [&](const uint64_t* bar) -> int {
+    const int i = (int)(bar - S.full_bar);
+    constexpr int e0 = L::NS, e1 = e0 + L::NS, e2 = e1 + L::NBUF, e3 = e2 + L::NBUF, e4 = e3 + L::NU,
+                  e5 = e4 + L::NU, e6 = e5 + L::NU, e7 = e6 + L::NB, e8 = e7 + L::NB;
+    return i < e0 ? 0 : i < e1 ? 1 : i < e2 ? 2 : i < e3 ? 3 : i < e4 ? 4 : i < e5 ? 5 : i < e6 ? 6 : i < e7 ? 7
+         : i < e8 ? 8 : 9;
+  };
+#define ESPN_WAIT(bar, par)                                                        \
+  do {                                                                             \
+    if (tr) {                                                                      \
+      const long long t0_ = clock64();                                             \
+      espn_ptx::mbar_wait(bar, par);                                               \
+      const unsigned long long dt_ = (unsigned long long)(clock64() - t0_);        \
+      wacc += dt_;                                                                 \
+      if (lane == 0) atomicAdd(&g_cta_prof[64 + 12 * warp + bar_kind(bar)], dt_); \
+    } else {                                                                       \
+      espn_ptx::mbar_wait(bar, par);                                               \
+    }                                                                              \
   } while (0)
 
   if (warp == L::LOADER_WARP) {
@@ -769,7 +793,36 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
                 acc = 1;
               }
             }
-        } else
+        } else {
+#if ESPN_MMA_DESC == 1
+          // descriptors stepped per quarter (A 32 rows up the block-diagonal
+          // window, B one quarter along the stage) instead of rebuilt per MMA
+          uint64_t a_desc = umma_desc_sw(a_base + (96 + 128 * us) * L::PW, 8 * L::PW, L::SWZ);
+          uint64_t b_desc = umma_desc_sw(b_base + s * L::STAGE_BYTES, 8 * L::PW, L::SWZ);
+#pragma unroll 1
+          for (int w = 0; w < 4; ++w) {
+            const int rem = (int)Sl - (int)(x0 + w * L::NQC);
+            if (rem <= 0) break;
+            const uint32_t nv = rem < L::NQC ? (uint32_t)rem : (uint32_t)L::NQC;
+            const uint32_t n_mma = (nv + 15u) & ~15u;
+            if ((p.dbg & 2u) || ((p.dbg & 64u) && w > 0)) break;
+            const uint32_t idesc = umma_idesc_f16(128, n_mma, p.bf16);
+#pragma unroll
+            for (int ks = 0; ks < L::KSTEPS; ++ks) {
+              const uint32_t kb = ks * 32;
+              const uint64_t bd = b_desc + (((kb / L::PW) * L::PANEL_BYTES + (kb % L::PW)) >> 4);
+#pragma unroll
+              for (int part = 0; part < (L::SPLIT ? 2 : 1); ++part) {
+                const uint64_t ad = a_desc + ((part * L::LO_ROWS * L::PW + (kb / L::PW) * L::A_PANEL_BYTES +
+                                               (kb % L::PW)) >> 4);
+                umma_f16_elect(d_tmem, ad, bd, idesc, acc);
+                acc = 1;
+              }
+            }
+            a_desc -= (32 * L::PW) >> 4;
+            b_desc += (L::NQC * L::PW) >> 4;
+          }
+#else
 #pragma unroll 1
           for (int w = 0; w < 4; ++w) {
             const int rem = (int)Sl - (int)(x0 + w * L::NQC);
@@ -795,6 +848,8 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
               }
             }
           }
+#endif
+        }
         umma_commit_elect(&S.empty_bar[s]);
         umma_commit_elect(&S.tfull_bar[buf]);
       }

@@ -1,7 +1,11 @@
 """Profiling experiment (not product): per warp role of the MaxSim kernel,
 the share of its time spent waiting on mbarriers (ESPN_DEBUG bit 8, summed
 over all CTAs and batches) for the served C2 step -- the role that never
-waits is the bottleneck.  usage: python tools/role_profile.py [on|off]"""
+waits is the bottleneck.  The accounting is compiled in only with
+-DESPN_ROLE_PROFILE (it costs ~15% even when not executed):
+  ESPN_NVCC_DEFINES=-DESPN_ROLE_PROFILE python -c "from paper_2312_05417_b200 import build as b; b.build_lib(force=True)"
+  python tools/role_profile.py [on|off]
+(rebuild without the define afterwards)."""
 import ctypes as C
 import os
 import sys
@@ -40,6 +44,7 @@ for _ in range(3):
 if serve:
     store.server_start(idle_us=2_000_000)
 buf = (C.c_uint64 * (8 + 1024))()
+KINDS = ["full", "empty", "tfull", "tempty", "ufull", "uempty", "edone", "bdone", "bfree", "patched"]
 
 
 def run(n):
@@ -67,5 +72,8 @@ a = np.array(buf[8:8 + 34], dtype=np.float64).reshape(17, 2)
 names = ["epi q0 h0", "epi q1 h0", "epi q2 h0", "epi q3 h0", "epi q0 h1", "epi q1 h1", "epi q2 h1", "epi q3 h1",
          "MMA", "producer 0", "producer 1", "loader", "combine", "dedup", "rank", "query tile", "pad patch"]
 print(f"server={'on' if serve else 'off'}: per warp role, busy share = 1 - waiting / total (all CTAs, 200 batches)")
-for n, (tot, w) in zip(names, a):
-    print(f"  {n:12s} total {tot / 1e9:8.3f} Gcyc  waiting {100 * w / max(tot, 1):5.1f} %  busy {100 * (1 - w / max(tot, 1)):5.1f} %")
+kb = np.array(buf[8 + 64:8 + 64 + 17 * 12], dtype=np.float64).reshape(17, 12)
+for i, (n, (tot, w)) in enumerate(zip(names, a)):
+    parts = ", ".join(f"{KINDS[j]} {100 * kb[i, j] / max(tot, 1):.1f}" for j in range(10) if kb[i, j] > 0.005 * tot)
+    print(f"  {n:12s} total {tot / 1e9:8.3f} Gcyc  waiting {100 * w / max(tot, 1):5.1f} %  busy "
+          f"{100 * (1 - w / max(tot, 1)):5.1f} %   [{parts}]")
