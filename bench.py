@@ -762,22 +762,30 @@ def run_ours(args, cfg):
     kern_name = f"rerank_small_kernel<{d}>" if small_path else f"maxsim_tc_kernel<{d}>"
     kern_label = ("single-launch small-batch kernel (CUDA cores, fp32 query, bit-exact; %s)" % args.kernel
                   if small_path else "tcgen05 (%s)" % args.kernel)
-    if serve:  # graph capture synchronises the device: capture with the server paused
-        store.server_pause()
-    for ln in lanes:
-        for db in dev_batches:
-            gr = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gr, stream=ln.stream):
-                ln.enqueue(db, torch.cuda.current_stream().cuda_stream)
-            ln.graphs.append(gr)
-    if serve:
-        torch.cuda.synchronize()
-        store.server_start(query_precision=args.query_precision, idle_us=2_000_000)  # relaunch for the replays
+    # a step is one CUDA-graph replay, or (--launch eager) one ASYNC
+    # espn_gpu_rerank call (measured equal for the served step: 1.656/1.646 M
+    # eager vs 1.661/1.650 M graphs at the same clocks)
+    use_graphs = args.launch != "eager"
+    if use_graphs:
+        if serve:  # graph capture synchronises the device: capture with the server paused
+            store.server_pause()
+        for ln in lanes:
+            for db in dev_batches:
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=ln.stream):
+                    ln.enqueue(db, torch.cuda.current_stream().cuda_stream)
+                ln.graphs.append(gr)
+        if serve:
+            torch.cuda.synchronize()
+            store.server_start(query_precision=args.query_precision, idle_us=2_000_000)  # relaunch for the replays
 
     def replay(st):
         ln = lanes[st % NL]
-        with torch.cuda.stream(ln.stream):
-            ln.graphs[st % n_batches].replay()
+        if use_graphs:
+            with torch.cuda.stream(ln.stream):
+                ln.graphs[st % n_batches].replay()
+        else:
+            ln.enqueue(dev_batches[st % n_batches], ln.stream.cuda_stream)
 
     def fork(ev_start):
         for ln in lanes:
@@ -830,16 +838,22 @@ def run_ours(args, cfg):
     barrier()
     for st in range(args.steps):
         evs[st][0].record(ln0.stream)
-        with torch.cuda.stream(ln0.stream):
-            ln0.graphs[st % n_batches].replay()
+        if use_graphs:
+            with torch.cuda.stream(ln0.stream):
+                ln0.graphs[st % n_batches].replay()
+        else:
+            ln0.enqueue(dev_batches[st % n_batches], ln0.stream.cuda_stream)
         evs[st][1].record(ln0.stream)
     barrier()
     lat = np.array([a.elapsed_time(b) for a, b in evs])
     p50, p99 = max_over_ranks(float(np.percentile(lat, 50))), max_over_ranks(float(np.percentile(lat, 99)))
 
     # ---- correctness spot check of the timed path: the source doc ranks first ----
-    with torch.cuda.stream(ln0.stream):
-        ln0.graphs[0].replay()
+    if use_graphs:
+        with torch.cuda.stream(ln0.stream):
+            ln0.graphs[0].replay()
+    else:
+        ln0.enqueue(dev_batches[0], ln0.stream.cuda_stream)
     barrier()
     top = ln0.packed.cpu().numpy()[:B_q * k].reshape(B_q, k)[:, 0].view(np.uint32)  # (plain D2H: no kernel)
     src = dev_batches[0]["glob"]["ids"].reshape(B_q, K)[:, 0]
@@ -1001,9 +1015,9 @@ def run_ours(args, cfg):
                                    + (" [ranks share GPUs: harness check, not a performance number]"
                                       if shared else "")),
                    "l2": l2_note,
-                   "launch": ("persistent tcgen05 MaxSim server (one launch) fed by a device batch queue; a step = one "
-                              "CUDA graph (plan + submit -> wait); %d batches in flight on separate streams/workspaces"
-                              % NL if serve else
+                   "launch": ("persistent tcgen05 MaxSim server (one launch) fed by a device batch queue; a step = %s "
+                              "(plan + submit -> wait); %d batches in flight on separate streams/workspaces"
+                              % ("one CUDA graph" if use_graphs else "one ASYNC espn_gpu_rerank call", NL) if serve else
                               ("one CUDA graph per batch (ONE kernel: validation, CUDA-core MaxSim, aggregate, "
                                "per-CTA top-k, last-CTA merge + duplicate check); %d batches in flight on separate "
                                "streams/workspaces" % NL) if small_path else
@@ -1168,6 +1182,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--launch", default="graph", choices=["graph", "eager"],
+                    help="a timed step = one CUDA-graph replay (default) or one ASYNC espn_gpu_rerank call")
     ap.add_argument("--kernel", default=None, choices=["auto", "tcgen05", "small"],
                     help="espn_kernel of the re-rank calls; default: small (the single-launch kernel) for "
                          "configs[0] (batch 1), auto (tcgen05) otherwise")
