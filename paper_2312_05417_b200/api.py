@@ -656,7 +656,7 @@ class Reranker:
 
     # ---- multi-GPU (espn_gpu.h "Multi-GPU") -------------------------
     def _sharded_args(self, query_tokens, cand_ids, cand_cls, cand_offsets, config, device_io, device_offsets,
-                      sync, needed_counts, query_precision, out):
+                      sync, needed_counts, query_precision, out, kernel="auto"):
         if device_offsets:
             offs_p, B = _ptr(cand_offsets), int(cand_offsets.numel()) - 1
             nc_p = _ptr(needed_counts) if needed_counts is not None else None
@@ -695,30 +695,31 @@ class Reranker:
         args = L.RerankArgs(n_queries=B, n_query_tokens=int(query_tokens.shape[1]), query_tokens=_ptr(query_tokens),
                             cand_ids=_ptr(cand_ids), cand_cls=_ptr(cand_cls), cand_offsets=offs_p,
                             rerank_count=int(config.rerank_count), final_k=k, alpha=float(config.alpha),
-                            flags=flags, kernel=L.ESPN_KERNEL_AUTO, needed_counts=nc_p)
+                            flags=flags, kernel=_KERNELS[kernel], needed_counts=nc_p)
         o = L.RerankOut(ids=_ptr(out[0]), scores=_ptr(out[1]), counts=_ptr(out[2]))
         self._keep_sh = (query_tokens, cand_ids, cand_cls, keep, out)
         return args, o, out
 
     def rerank_sharded(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig, comm: "NcclComm",
                        device_io: bool = False, device_offsets: bool = False, out=None, stream=None, sync: bool = True,
-                       needed_counts=None, query_precision: str = "auto"):
+                       needed_counts=None, query_precision: str = "auto", kernel: str = "auto"):
         """espn_gpu_rerank_sharded: every rank passes the SAME global batch
         (global doc ids) and gets the global ranked lists back; the table's
         placement (doc-id shard or full replica) decides the split.  Returns
         (ids[B,k], scores[B,k], counts[B])."""
         args, o, out = self._sharded_args(query_tokens, cand_ids, cand_cls, cand_offsets, config, device_io,
-                                          device_offsets, sync, needed_counts, query_precision, out)
+                                          device_offsets, sync, needed_counts, query_precision, out, kernel)
         _check(L.lib().espn_gpu_rerank_sharded(self.store.handle, self._h, C.byref(args), C.byref(o), comm.handle,
                                                C.c_void_p(stream) if stream else None))
         return out
 
     def shard_pack(self, query_tokens, cand_ids, cand_cls, cand_offsets, config: PipelineConfig, nranks: int,
-                   rank: int, device_io: bool = True, stream=None, query_precision: str = "auto"):
+                   rank: int, device_io: bool = True, stream=None, query_precision: str = "auto",
+                   kernel: str = "auto"):
         """Phase 1 without NCCL: this rank's packed block (device pointer, int32
         words) in the workspace's send buffer."""
         args, o, _ = self._sharded_args(query_tokens, cand_ids, cand_cls, cand_offsets, config, device_io, False,
-                                        True, None, query_precision, None)
+                                        True, None, query_precision, None, kernel)
         ptr, words = C.c_void_p(), C.c_uint64()
         _check(L.lib().espn_gpu_shard_pack(self.store.handle, self._h, C.byref(args), int(nranks), int(rank),
                                            C.c_void_p(stream) if stream else None, C.byref(ptr), C.byref(words)))

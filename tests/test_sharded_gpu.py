@@ -220,3 +220,40 @@ def test_nccl_one_rank_eager_graph_and_group(oracle, cuda_ok):
     assert np.array_equal(oi, ref[0]) and np.array_equal(osc, ref[1])
     comms[0].close()
     rr.close(); store.close()
+
+
+@pytest.mark.parametrize("placement", ["shard", "replica"])
+def test_sharded_local_pass_small_kernel_bitexact(oracle, cuda_ok, placement):
+    """The ranks' local passes through the single-launch small-batch kernel
+    (device offsets, per-query needed counts from the owner split, base
+    offsets for REPLICA query slices): exact arithmetic, so the merged global
+    lists equal the oracle's bit for bit."""
+    G = 2
+    rp, codes, q, ids, cls, off = _case(seed=40)
+    cfg = api.PipelineConfig(rerank_count=200, final_k=FINAL_K, alpha=0.5, partial_rerank_enabled=True)
+    dq, di, dc = _dev(q, ids, cls)
+    stores, rrs, blocks = [], [], []
+    for g in range(G):
+        if placement == "shard":
+            lrp, lcodes = sharding.shard_table(rp, codes, D, G, g)
+            st = api.GpuStore(lrp, lcodes, D, shard_count=G, shard_index=g)
+        else:
+            st = api.GpuStore(rp, codes, D)
+        rr = api.Reranker(st, B, int(off[-1]), 32, max_list=K)  # small kernel: lists <= 2048
+        blocks.append(rr.shard_pack(dq, di, dc, off, cfg, G, g, kernel="small"))
+        stores.append(st)
+        rrs.append(rr)
+    bq = B if placement == "shard" else -(-B // G)
+    recv = _gather_blocks(blocks, sharding.pack_words(bq, FINAL_K))
+    gi, gs, gc = (x.cpu().numpy() for x in rrs[0].shard_merge(dq, di, dc, off, cfg, recv, G))
+    ot = oracle.OracleTable(rp, codes, D)
+    st_, oi, os_, on = oracle.rerank_batch(ot, np.ascontiguousarray(q, np.float32), ids, cls, off,
+                                           cfg.rerank_count, cfg.final_k, cfg.alpha, cfg.partial_rerank_enabled)
+    assert st_ == 0
+    assert np.array_equal(gc.astype(np.int64), np.asarray(on, np.int64))
+    for b in range(B):
+        n = int(on[b])
+        assert np.array_equal(gi.view(np.uint32)[b, :n].astype(np.int64), np.asarray(oi[b, :n], np.int64)), b
+        assert np.array_equal(gs[b, :n].view(np.uint32), np.asarray(os_[b, :n], np.float32).view(np.uint32)), b
+    for rr, st in zip(rrs, stores):
+        rr.close(); st.close()
