@@ -1431,7 +1431,9 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   // the running MaxSim kernel by the plan and awaited by a one-thread kernel ----
   const bool qsplit = tc && tc_query_split(t->d, t->dtype, a->flags);
   const bool served = t->server != nullptr && tc && fused && !t->tiered && qsplit == t->server_split;
-  if (t->server && tc && !served)
+  // any other kernel would wait for SM resources the running server holds
+  // (every SM is occupied by one server CTA) until the server idles out
+  if (t->server && !served)
     return fail(ESPN_E_INVALID_STATE, "a persistent re-rank server runs on this table: only fused tcgen05 batches "
                                       "(final_k <= 32, the server's query precision) can be served; stop it first");
   if (served) {

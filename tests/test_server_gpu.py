@@ -146,6 +146,9 @@ def test_idle_exit_relaunch_errors_and_stop(cuda_ok):
     # batches the server cannot take fail cleanly instead of waiting for an SM
     with pytest.raises(api.InvalidStateError):
         rr.rerank_arrays(q, ids, cls, off, api.PipelineConfig(rerank_count=600, final_k=64))
+    for kern in ("simt", "small"):  # CUDA-core kernels need SMs the server holds
+        with pytest.raises(api.InvalidStateError):
+            rr.rerank_arrays(q[:1], ids[:int(off[1])], cls[:int(off[1])], off[:2], cfg, kernel=kern)
     store.server_stop()
     got = rr.rerank_arrays(q, ids, cls, off, api.PipelineConfig(rerank_count=600, final_k=64))
     assert got[2][0] == 64
