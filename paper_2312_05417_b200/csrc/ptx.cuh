@@ -160,6 +160,28 @@ __host__ __device__ __forceinline__ uint32_t umma_idesc_f16(uint32_t m, uint32_t
   return (1u << 4) | (bf16 << 7) | (bf16 << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
+// Paired fp32 multiply / add (sm_100 FMUL2 / FADD2), per component exactly
+// __fmul_rn / __fadd_rn.  Caution: ptxas fuses a paired multiply feeding a
+// paired add into FFMA2 (one rounding) -- with the __fmul2_rn / __fadd2_rn
+// intrinsics and with this explicit-.rn PTX alike, even under -fmad=false --
+// so bit-exact code must not chain mul2_rn into add2_rn.
+__device__ __forceinline__ unsigned long long f2_bits(float2 v) {
+  return (unsigned long long)__float_as_uint(v.x) | ((unsigned long long)__float_as_uint(v.y) << 32);
+}
+__device__ __forceinline__ float2 bits_f2(unsigned long long u) {
+  return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
+}
+__device__ __forceinline__ float2 mul2_rn(float2 a, float2 b) {
+  unsigned long long d;
+  asm volatile("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+__device__ __forceinline__ float2 add2_rn(float2 a, float2 b) {
+  unsigned long long d;
+  asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
 __device__ __forceinline__ void red_max_shared(int* addr, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(smem_u32(addr)), "r"(v) : "memory");

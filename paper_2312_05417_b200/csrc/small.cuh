@@ -44,10 +44,11 @@ constexpr int kSmallMaxChunk = 256;       // scored candidates per CTA
 constexpr int kSmallMaxList = 2048;       // scored candidates per query
 constexpr int kSmallHashSlots = 4096;     // per-query duplicate hash (2x the longest list)
 constexpr int kSmallMaxCtas = 296;        // 2 per SM
-constexpr int kSmallWarpRowBytes = 1024;  // per-warp row staging (16 rows at d=32)
-constexpr int kSmallRegionBytes = 16 * 1024;  // row staging | last CTA: the lists + level-1 merges
-constexpr int kSmallLevel1Keys = 16 * kFusedMaxK;                       // <= 16 level-1 lists of k
-constexpr int kSmallListKeys = kSmallRegionBytes / 8 - kSmallLevel1Keys;  // P x k keys merged in smem
+constexpr int kSmallLevel1Keys = 16 * kFusedMaxK;  // <= 16 level-1 lists of k
+// per-warp fp32 row staging: at least one quad of rows, within the 48 KB of
+// static shared memory next to the query (32 x d fp32)
+template <int D>
+constexpr int small_wbuf() { return D <= 32 ? 2048 : (4 * 4 * D <= 1024 ? 1024 : 2048); }
 
 struct SmallParams {
   MaxSimParams m;              // table, batch and outputs; m.unit_top = B x P x k per-CTA lists
@@ -113,8 +114,10 @@ __global__ void __launch_bounds__(small_threads<D>()) rerank_small_kernel(const 
   constexpr uint32_t NT = small_threads<D>();
   constexpr uint32_t NW = NT / 32;
   constexpr uint32_t NDR = NT / 64;                          // documents per round
-  constexpr uint32_t WBUF = kSmallWarpRowBytes;              // per-warp row staging
-  constexpr uint32_t WROWS = WBUF / (2 * D);                 // rows per staged piece
+  constexpr uint32_t WBUF = small_wbuf<D>();                 // per-warp staging
+  constexpr uint32_t WROWS = WBUF / (4 * D) / 4 * 4;         // fp32 rows per staged piece, whole quads
+  constexpr int REGION = NW * WBUF;                          // row staging | last CTA: lists + level-1 merges
+  constexpr int LIST_KEYS = REGION / 8 - kSmallLevel1Keys;   // P x k keys merged in shared memory
   constexpr uint32_t HM = kSmallHashSlots - 1;
   __shared__ __align__(16) float sq[32 * D];                 // query tokens (fp32, as given)
   __shared__ uint64_t keys[kSmallMaxChunk];                  // this CTA's candidate keys
@@ -124,9 +127,9 @@ __global__ void __launch_bounds__(small_threads<D>()) rerank_small_kernel(const 
   __shared__ float halfmax[NDR][32];                         // second half's row maxima per document
   // compute phase: NW row-staging buffers; the last CTA's merge phase reuses
   // the space for the P lists and the level-1 merges
-  __shared__ __align__(16) uint8_t region[kSmallRegionBytes];
+  __shared__ __align__(16) uint8_t region[REGION];
   __shared__ uint32_t s_last;
-  static_assert(NW * WBUF <= kSmallRegionBytes && WROWS >= 1, "row staging");
+  static_assert(WROWS >= 4 && LIST_KEYS >= 1024, "row staging / merge scratch");
   static_assert(NT >= kSmallMaxChunk, "one thread per candidate");
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t b = blockIdx.y, pc = blockIdx.x, P = sp.P;
@@ -230,59 +233,57 @@ __global__ void __launch_bounds__(small_threads<D>()) rerank_small_kernel(const 
       const uint8_t* doc = reinterpret_cast<const uint8_t*>(src);
       const uint32_t th = (t + 1) / 2;
       const uint32_t ra = half ? th : 0u, rb = half ? t : th;  // this warp's rows [ra, rb)
-      // rows in pieces of WROWS: one coalesced round trip per piece into the
-      // warp's buffer (plain rows), then every lane reads each row with
-      // broadcast 16-byte shared loads
+      // rows in pieces of WROWS: one coalesced round trip per piece; each
+      // lane converts its 16-byte chunks to fp32 once (not every lane per
+      // element) into the warp's buffer laid out [row quad][k][4 rows], so
+      // one broadcast 16-byte load feeds four rows' k-th products, computed
+      // two at a time by the paired multiply (FMUL2, per component exactly
+      // __fmul_rn) and summed per row with scalar __fadd_rn in ascending k
+      // (the reference's order).  (A paired add after the paired multiply is
+      // fused by ptxas into FFMA2 -- one rounding -- even with explicit .rn
+      // and -fmad=false, so the sums stay scalar.)
+      float* fbuf = reinterpret_cast<float*>(wbuf);
       for (uint32_t r0 = ra; r0 < rb; r0 += WROWS) {
         const uint32_t nr = min(WROWS, rb - r0);
         const uint32_t nv = nr * RL::CH;
         __syncwarp();  // the previous piece is consumed
         for (uint32_t v = lane; v < nv; v += 32) {
-          const uint32_t jr = r0 + v / RL::CH, cc = v % RL::CH;
-          *reinterpret_cast<uint4*>(wbuf + (jr - r0) * (2 * D) + cc * 16) =
-              __ldg(reinterpret_cast<const uint4*>(doc + RL::off(t, jr, cc)));
+          const uint32_t jl = v / RL::CH, cc = v % RL::CH;
+          const uint4 x = __ldg(reinterpret_cast<const uint4*>(doc + RL::off(t, r0 + jl, cc)));
+          const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+          float* dst = fbuf + ((jl >> 2) * D + cc * 8) * 4 + (jl & 3);
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh) {
+            dst[(2 * hh) * 4] = espn_ptx::code_to_f32((uint16_t)(w[hh] & 0xFFFFu), p.bf16);
+            dst[(2 * hh + 1) * 4] = espn_ptx::code_to_f32((uint16_t)(w[hh] >> 16), p.bf16);
+          }
         }
         __syncwarp();
-        // four rows at a time: independent accumulators, each summed in
-        // ascending k (the reference's order)
         uint32_t jr = 0;
-        for (; jr + 4 <= nr; jr += 4) {
-          float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (; jr + 4 <= nr; jr += 4) {  // a whole quad: two rows per paired op
+          const float4* fq = reinterpret_cast<const float4*>(fbuf) + (jr >> 2) * D;
+          float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
 #pragma unroll
-          for (int k8 = 0; k8 < D / 8; ++k8) {
-            uint4 v[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) v[r] = *reinterpret_cast<const uint4*>(wbuf + (jr + r) * (2 * D) + k8 * 16);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
-#pragma unroll
-              for (int hh = 0; hh < 4; ++hh) {
-                const float x0 = espn_ptx::code_to_f32((uint16_t)(w[hh] & 0xFFFFu), p.bf16);
-                const float x1 = espn_ptx::code_to_f32((uint16_t)(w[hh] >> 16), p.bf16);
-                acc[r] = __fadd_rn(acc[r], __fmul_rn(q[k8 * 8 + 2 * hh], x0));
-                acc[r] = __fadd_rn(acc[r], __fmul_rn(q[k8 * 8 + 2 * hh + 1], x1));
-              }
-            }
+          for (int kk = 0; kk < D; ++kk) {
+            const float4 x = fq[kk];
+            const float2 qq = make_float2(q[kk], q[kk]);
+            const float2 p01 = espn_ptx::mul2_rn(qq, make_float2(x.x, x.y));
+            const float2 p23 = espn_ptx::mul2_rn(qq, make_float2(x.z, x.w));
+            a0 = __fadd_rn(a0, p01.x);
+            a1 = __fadd_rn(a1, p01.y);
+            a2 = __fadd_rn(a2, p23.x);
+            a3 = __fadd_rn(a3, p23.y);
           }
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (acc[r] > m) m = acc[r];
+          if (a0 > m) m = a0;
+          if (a1 > m) m = a1;
+          if (a2 > m) m = a2;
+          if (a3 > m) m = a3;
         }
-        for (; jr < nr; ++jr) {
+        for (; jr < nr; ++jr) {  // the last < 4 rows, one at a time
+          const float* fr = fbuf + (jr >> 2) * D * 4 + (jr & 3);
           float acc = 0.0f;
 #pragma unroll
-          for (int k8 = 0; k8 < D / 8; ++k8) {
-            const uint4 v = *reinterpret_cast<const uint4*>(wbuf + jr * (2 * D) + k8 * 16);
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int hh = 0; hh < 4; ++hh) {
-              const float x0 = espn_ptx::code_to_f32((uint16_t)(w[hh] & 0xFFFFu), p.bf16);
-              const float x1 = espn_ptx::code_to_f32((uint16_t)(w[hh] >> 16), p.bf16);
-              acc = __fadd_rn(acc, __fmul_rn(q[k8 * 8 + 2 * hh], x0));
-              acc = __fadd_rn(acc, __fmul_rn(q[k8 * 8 + 2 * hh + 1], x1));
-            }
-          }
+          for (int kk = 0; kk < D; ++kk) acc = __fadd_rn(acc, __fmul_rn(q[kk], fr[kk * 4]));
           if (acc > m) m = acc;
         }
       }
@@ -348,11 +349,11 @@ __global__ void __launch_bounds__(small_threads<D>()) rerank_small_kernel(const 
   __threadfence();
   const unsigned long long* lists = p.unit_top + (size_t)b * P * k;
   const uint32_t nkeys = P * k;
-  if (nkeys <= (uint32_t)kSmallListKeys && P <= 32u * NW) {
+  if (nkeys <= (uint32_t)LIST_KEYS && P <= 32u * NW) {
     // the P lists -> shared memory in one round trip; warps k-way merge 32
     // lists each (level 1), warp 0 merges their results
     uint64_t* L0 = reinterpret_cast<uint64_t*>(region);
-    uint64_t* L1 = L0 + kSmallListKeys;
+    uint64_t* L1 = L0 + LIST_KEYS;
     for (uint32_t i = tid; i < nkeys; i += NT) L0[i] = __ldcg(&lists[i]);
     __syncthreads();
     const uint32_t n1 = (P + 31) / 32;
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(small_threads<D>()) rerank_small_kernel(const 
       if (lane == 0) p.out_counts[b] = cnt;
     }
   } else if (wid == 0) {  // long: the chunked k-way merge straight from the lists
-    fused_merge<kSmallListKeys>(p, b, b * P, P, reinterpret_cast<uint64_t*>(region), lane, /*kway=*/true);
+    fused_merge<LIST_KEYS>(p, b, b * P, P, reinterpret_cast<uint64_t*>(region), lane, /*kway=*/true);
   }
   // the batch is done for this query: reset its hash, empty-code flag and counter
   {
