@@ -64,6 +64,9 @@ template <bool S> struct TcCfg<16, S>  { static constexpr int NQC = 128, NS = 6,
 #ifndef ESPN_D32_NQC
 #define ESPN_D32_NQC 128
 #endif
+#ifndef ESPN_NO_PATCH
+#define ESPN_NO_PATCH 1  // 1: no pad-patch warp, the epilogue masks pad columns (C2 35.7 vs 36.5 us); 0: the 17-warp patch design
+#endif
 #ifndef ESPN_MMA_DESC
 #define ESPN_MMA_DESC 0  // A/B knob: 1 = descriptors stepped per quarter instead of rebuilt per MMA
 #endif
@@ -128,13 +131,14 @@ struct TcLayout {
   static constexpr int RANK_WARP = DEDUP_WARP + 1;     // fused top-k: keys, unit top-k
   static constexpr int QUERY_WARP = RANK_WARP + 1;     // unit query tile -> A operand slot
   static constexpr int PATCH_WARP = QUERY_WARP + 1;    // pad slots <- copies of the doc's last row
-  static constexpr int NWARPS = PATCH_WARP + 1;
+  static constexpr int NWARPS = ESPN_NO_PATCH ? PATCH_WARP : PATCH_WARP + 1;  // (no pad-patch warp: 16)
   static constexpr int NB = 8;                     // bow ring (combine -> rank) depth, in units
   static constexpr int HALF = NQC / 2;             // columns per epilogue warp per stage
   static constexpr int LW = HALF < 32 ? HALF : 32; // tcgen05.ld width (columns)
   static constexpr int NLD = HALF / LW;            // loads per epilogue warp per stage
   static constexpr int NGH = HALF / 8;             // 8-slot groups per epilogue warp per stage
   static constexpr int NTHREADS = NWARPS * 32;
+  static constexpr int MAXREG = NWARPS <= 16 ? 120 : 96;  // see maxsim_tc_kernel
 
   struct Unit {
     uint32_t b, nd, S, tail;   // tail: alpha*cls tail unit (no MaxSim)
@@ -146,6 +150,9 @@ struct TcLayout {
     // stage << 20}, in stage order.
     uint32_t pt[UNITMAX];
     uint32_t n_pt;
+#if ESPN_NO_PATCH
+    uint8_t vc[NG];             // per 8-slot group: its valid (non-pad) slots
+#endif
     // Bulk-copy plan (loader-built): one op per (doc, stage piece, K-panel)
     // {src lo, src hi, byte offset in the stage, bytes}, in stage order;
     // stage st issues ops [op_beg[st], op_beg[st+1]) (last stage: to n_ops),
@@ -556,6 +563,13 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
             const uint32_t pi = pcarry + pincl - 1;
             U.pt[pi] = (last - stl * L::STAGE_SLOTS) | ((pad - t) << 16) | (stl << 20);
           }
+#if ESPN_NO_PATCH
+          {
+            const uint32_t g0 = start >> 3, ngr = pad >> 3;
+            for (uint32_t gg = 0; gg + 1 < ngr; ++gg) U.vc[g0 + gg] = 8;
+            U.vc[g0 + ngr - 1] = (uint8_t)(t - 8 * (ngr - 1));
+          }
+#endif
           // one op per stage piece and K-panel: the piece [a, e) of the doc's
           // slots inside stage st lands at (a - x0) * PW of panel pn
           uint32_t o = ocarry + oincl - npc;
@@ -598,7 +612,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       __syncwarp();
       if (ESPN_ARRIVE_ALL || lane == 0) mbar_arrive(&S.ufull_bar[us]);  // every lane releases its own writes
     }
-  } else if (warp == L::PATCH_WARP) {
+  } else if (warp == L::PATCH_WARP && !ESPN_NO_PATCH) {
     // ============================ PAD PATCH =====================================
     // Once a stage's rows have landed, every doc whose last 8-slot group is
     // partial gets copies of its last row in its pad slots (re-swizzled for
@@ -767,7 +781,11 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
       const uint32_t n_st = (Sl + L::STAGE_SLOTS - 1) / L::STAGE_SLOTS;
       for (uint32_t st = 0; st < n_st; ++st, ++gs) {
         const uint32_t s = gs % L::NS, buf = gs % L::NBUF;
+#if ESPN_NO_PATCH
+        ESPN_WAIT(&S.full_bar[s], (gs / L::NS) & 1);  // rows landed (pads masked by the epilogue)
+#else
         ESPN_WAIT(&S.patched_bar[s], (gs / L::NS) & 1);  // rows landed and pads patched
+#endif
         ESPN_WAIT(&S.tempty_bar[buf], ((gs / L::NBUF) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = S.tmem_base + buf * L::BUFC;
@@ -908,8 +926,20 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
             for (int qq = 0; qq < GPC; ++qq) {
               const int q = c * GPC + qq;
               const float* x = &v[c][8 * qq];
+#if ESPN_NO_PATCH
+              const uint32_t nvq = U.vc[G0 + q];  // warp-uniform
+              if (nvq < 8) {
+                float y[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) y[i] = (i == 0 || (uint32_t)i < nvq) ? x[i] : -INFINITY;
+                gm[q] = fmaxf(fmax3(y[0], y[1], y[2]), fmax3(fmax3(y[3], y[4], y[5]), y[6], y[7]));
+              } else {
+                gm[q] = fmaxf(fmax3(x[0], x[1], x[2]), fmax3(fmax3(x[3], x[4], x[5]), x[6], x[7]));
+              }
+#else
               // pad columns hold copies of the doc's last row (patch warp): no masking
               gm[q] = fmaxf(fmax3(x[0], x[1], x[2]), fmax3(fmax3(x[3], x[4], x[5]), x[6], x[7]));
+#endif
             }
           }
           if (p.dbg & 32u) continue;  // profiling knob: no scan / flush
@@ -1107,7 +1137,10 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
 }
 
 template <int D, bool SPLIT>
-__global__ void __launch_bounds__(TcLayout<D, SPLIT>::NTHREADS, 1)
+// Register cap: the next batch's plan CTA (32 registers per thread) must fit
+// beside a persistent server CTA on the busiest SM sub-partition (16 K
+// registers): 4 warps x 120 with 16 warps, 5 warps x 96 with 17
+__global__ void __maxnreg__((TcLayout<D, SPLIT>::MAXREG))
 maxsim_tc_kernel(const MaxSimParams p) {
   using L = TcLayout<D, SPLIT>;
   using namespace espn_ptx;

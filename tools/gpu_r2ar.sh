@@ -1,0 +1,6 @@
+# pad-patch elimination A/B (ESPN_NO_PATCH=1: epilogue masks pad columns); parity with the variant first
+L=paper_2312_05417_b200/lib/libespn_gpu.so
+cp tools/ab/libespn_gpu_nopatch.so $L
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_server_gpu.py tests/test_fuzz_gpu.py -q -x -k "not small" > gpurun_out/pytest_ar.log 2>&1; echo pytest_nopatch=$?; tail -3 gpurun_out/pytest_ar.log
+for v in cur nopatch cur nopatch; do cp tools/ab/libespn_gpu_$v.so $L; printf "%s " $v; timeout 300 python tools/server_knobs.py 0 on 2>&1 | tail -1; done
+cp tools/ab/libespn_gpu_cur.so $L
