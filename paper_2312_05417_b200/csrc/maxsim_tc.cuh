@@ -134,7 +134,10 @@ struct TcLayout {
   static constexpr int NWARPS = ESPN_NO_PATCH ? PATCH_WARP : PATCH_WARP + 1;  // (no pad-patch warp: 16)
   static constexpr int NB = 8;                     // bow ring (combine -> rank) depth, in units
   static constexpr int HALF = NQC / 2;             // columns per epilogue warp per stage
-  static constexpr int LW = HALF < 32 ? HALF : 32; // tcgen05.ld width (columns)
+#ifndef ESPN_EPI_LW
+#define ESPN_EPI_LW 32  // A/B knob: columns per tcgen05.ld of the epilogue (64 = one load per stage half)
+#endif
+  static constexpr int LW = HALF < ESPN_EPI_LW ? HALF : ESPN_EPI_LW; // tcgen05.ld width (columns)
   static constexpr int NLD = HALF / LW;            // loads per epilogue warp per stage
   static constexpr int NGH = HALF / 8;             // 8-slot groups per epilogue warp per stage
   static constexpr int NTHREADS = NWARPS * 32;
