@@ -95,34 +95,45 @@ int check_device(int dev, int* num_sms, bool* tc_ok) {
 }
 
 constexpr int kMinUnitDocs = 8;
+constexpr int kExclusiveUnitDocs = 64;  // longest unit of a non-served tcgen05 launch
 // internal re-rank flag: device cand_offsets are a query slice of a larger
 // batch (cand_offsets[0] may be nonzero; REPLICA placement of the sharded call)
 constexpr uint32_t kFlagBaseOffsets = 0x80000000u;  // shortest work unit (small batches, see espn_gpu_rerank)
 
-template <int D>
+template <int D, bool S>
 constexpr int tc_unit_docs(uint32_t max_t) {
-  using L = TcLayout<D>;
+  using L = TcLayout<D, S>;
   const uint32_t pad = (max_t + 7u) & ~7u;
   const uint32_t u = pad ? (uint32_t)L::MAX_SLOTS / pad : 0;
   return (int)std::min<uint32_t>(u, (uint32_t)L::UNITMAX);
 }
 
-int tc_max_tokens_rt(uint32_t d) {  // longest doc one work unit holds (UNITMAX x 64 slots)
-  switch (d) {
-    case 16: return TcLayout<16>::MAX_SLOTS;
-    case 32: return TcLayout<32>::MAX_SLOTS;
-    case 64: return TcLayout<64>::MAX_SLOTS;
-    case 128: return TcLayout<128>::MAX_SLOTS;
+// longest doc one work unit holds (UNITMAX x 64 slots; the split-query layout
+// of d = 32 has shorter units than the rounded-query one)
+int tc_max_tokens_rt(uint32_t d, bool split) {
+  switch (d * 2 + (split ? 1 : 0)) {
+    case 32: return TcLayout<16, false>::MAX_SLOTS;
+    case 33: return TcLayout<16, true>::MAX_SLOTS;
+    case 64: return TcLayout<32, false>::MAX_SLOTS;
+    case 65: return TcLayout<32, true>::MAX_SLOTS;
+    case 128: return TcLayout<64, false>::MAX_SLOTS;
+    case 129: return TcLayout<64, true>::MAX_SLOTS;
+    case 256: return TcLayout<128, false>::MAX_SLOTS;
+    case 257: return TcLayout<128, true>::MAX_SLOTS;
     default: return 0;
   }
 }
 
-int tc_unit_docs_rt(uint32_t d, uint32_t max_t) {
-  switch (d) {
-    case 16: return tc_unit_docs<16>(max_t);
-    case 32: return tc_unit_docs<32>(max_t);
-    case 64: return tc_unit_docs<64>(max_t);
-    case 128: return tc_unit_docs<128>(max_t);
+int tc_unit_docs_rt(uint32_t d, uint32_t max_t, bool split) {
+  switch (d * 2 + (split ? 1 : 0)) {
+    case 32: return tc_unit_docs<16, false>(max_t);
+    case 33: return tc_unit_docs<16, true>(max_t);
+    case 64: return tc_unit_docs<32, false>(max_t);
+    case 65: return tc_unit_docs<32, true>(max_t);
+    case 128: return tc_unit_docs<64, false>(max_t);
+    case 129: return tc_unit_docs<64, true>(max_t);
+    case 256: return tc_unit_docs<128, false>(max_t);
+    case 257: return tc_unit_docs<128, true>(max_t);
     default: return 0;
   }
 }
@@ -1187,7 +1198,11 @@ int espn_gpu_workspace_create(espn_gpu_table* t, const espn_workspace_desc* desc
   al((void**)&w->needed, B * sizeof(uint32_t));
   // work-unit table capacity: every query may end in a partial unit
   {
-    int ud = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
+    // (the shorter of the two layouts' units that fit the longest doc: the
+    // query precision picks one per call)
+    const int ur = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t, false) : 0;
+    const int us = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t, true) : 0;
+    int ud = (ur > 0 && us > 0) ? std::min(ur, us) : std::max(ur, us);
     if (ud > kMinUnitDocs) ud = kMinUnitDocs;  // small batches use units down to kMinUnitDocs docs
     w->max_units = ud > 0 ? (C + ud - 1) / ud + 2 * B : 0;  // + partial units (needed, tail)
   }
@@ -1384,14 +1399,24 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
 
   // ---- kernel choice (tcgen05 when the dim has a tensor-core tiling) ----
   uint32_t kern = a->kernel;
-  int unit_docs = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t) : 0;
-  if (unit_docs > kMinUnitDocs) {
-    // small batches: shorter work units so that every SM gets one (C1: one
-    // query x 1000 candidates -> 125 units of 8 docs instead of 16 of 64)
-    const uint64_t ub = (uint64_t)a->n_queries * std::max<uint32_t>(a->rerank_count, 1u);
-    const uint64_t per_sm = (ub + t->num_sms - 1) / t->num_sms;
-    unit_docs = (int)std::max<uint64_t>(kMinUnitDocs, std::min<uint64_t>((uint64_t)unit_docs, per_sm));
-  }
+  // (the query precision the tcgen05 path would use picks the unit layout)
+  const bool split_if_tc = tc_query_split(t->d, t->dtype, a->flags);
+  const int layout_docs = t->tc_ok ? tc_unit_docs_rt(t->d, t->max_t, split_if_tc) : 0;
+  // size the units so that the batch is a whole number of rounds over the
+  // SMs: with units of at most `cap` docs, how many rounds does the batch
+  // take?  Then spread each query over as many (shorter) units as those rounds
+  // hold.  C2 (64 x 1000, 148 SMs, cap 96): 704 units of 91 docs = 4.8
+  // rounds; C1 (1 x 1000): 125 units of 8 docs, one per SM.
+  auto size_units = [&](int cap) -> int {
+    if (cap <= kMinUnitDocs || a->n_queries == 0) return cap;
+    const uint64_t Bq = a->n_queries;
+    const uint64_t per_q = std::max<uint64_t>(1, std::min<uint64_t>(std::max<uint32_t>(a->rerank_count, 1u), max_list));
+    const uint64_t sms = (uint64_t)t->num_sms;
+    const uint64_t n_long = Bq * ((per_q + cap - 1) / cap);
+    const uint64_t upq = std::max<uint64_t>(1, ((n_long + sms - 1) / sms) * sms / Bq);  // units per query
+    return (int)std::max<uint64_t>(kMinUnitDocs, std::min<uint64_t>((uint64_t)cap, (per_q + upq - 1) / upq));
+  };
+  int unit_docs = size_units(layout_docs);
   // single-launch small batches (K5, small.cuh): a few queries, short lists,
   // fused-size k, table in HBM.  Opt-in only: its CUDA-core arithmetic on the
   // fp32 query is exact, the tcgen05 path rounds the query (f16) or splits it
@@ -1408,7 +1433,7 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
   if (kern == ESPN_KERNEL_AUTO) kern = (tc_supported(t->d) && unit_docs > 0) ? ESPN_KERNEL_TCGEN05 : ESPN_KERNEL_SIMT;
   if (kern == ESPN_KERNEL_TCGEN05 && (!t->tc_ok || !tc_supported(t->d) || unit_docs <= 0))
     return fail(ESPN_E_INVALID_CONFIG, "tcgen05 MaxSim needs an sm_100 device, d in {16,32,64,128} and docs of at most " +
-                                           std::to_string(tc_max_tokens_rt(t->d)) + " tokens at d=" + std::to_string(t->d) +
+                                           std::to_string(tc_max_tokens_rt(t->d, split_if_tc)) + " tokens at d=" + std::to_string(t->d) +
                                            " (longest doc here: " + std::to_string(t->max_t) + ")");
   if (kern == ESPN_KERNEL_SIMT && !simt_supported(t->d))
     return fail(ESPN_E_INVALID_CONFIG, "CUDA-core MaxSim supports d in {8,16,32,48,64,96,128}");
@@ -1440,6 +1465,10 @@ int espn_gpu_rerank(espn_gpu_table* t, espn_gpu_workspace* w, const espn_rerank_
     const int ss = server_ensure(t, s);
     if (ss) return ss;
   }
+  // a launch of its own runs one batch alone: its last round is not hidden
+  // behind the next batch's units as in the served queue, so shorter units
+  // (C2: 46 -> 42 us per launch; served, the 96-doc units are 8% faster)
+  if (tc && !served && layout_docs > kExclusiveUnitDocs) unit_docs = size_units(kExclusiveUnitDocs);
   // dedup hash of the separate top-k kernel, sized by the longest scored list
   // (part of the graph key: a captured launch bakes it in)
   uint32_t topk_hs = 64;

@@ -74,9 +74,12 @@ template <bool S> struct TcCfg<16, S>  { static constexpr int NQC = 128, NS = 6,
 #define ESPN_D32_NS 4
 #endif
 #ifndef ESPN_D32_NU
-#define ESPN_D32_NU 3
+#define ESPN_D32_NU 3  // unit slots in flight
 #endif
-template <bool S> struct TcCfg<32, S>  { static constexpr int NQC = ESPN_D32_NQC, NS = S ? 4 : ESPN_D32_NS, UNITMAX = 64, NU = S ? 3 : ESPN_D32_NU; static constexpr bool REPA = false; };
+#ifndef ESPN_D32_UNITMAX
+#define ESPN_D32_UNITMAX 96  // docs per work unit, d = 32 rounded query (served C2: 32.9 us; 64: 35.8; 128 with NU 2: 34.0)
+#endif
+template <bool S> struct TcCfg<32, S>  { static constexpr int NQC = ESPN_D32_NQC, NS = S ? 4 : ESPN_D32_NS, UNITMAX = S ? 64 : ESPN_D32_UNITMAX, NU = S ? 3 : ESPN_D32_NU; static constexpr bool REPA = false; };
 template <bool S> struct TcCfg<64, S>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = S ? 2 : 3; static constexpr bool REPA = false; };
 template <bool S> struct TcCfg<128, S> { static constexpr int NQC = 64,  NS = 2, UNITMAX = 32, NU = S ? 1 : 2; static constexpr bool REPA = true; };
 
@@ -185,6 +188,7 @@ struct TcLayout {
   static constexpr int OFF_GATE = OFF_DESC + DESC_RING * (int)sizeof(MaxSimParams);
   static constexpr int SMEM_BYTES = OFF_GATE + 32 + 1024;  // + alignment slack
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static_assert(UNITMAX % 32 == 0, "the rank and combine warps hold UNITMAX / 32 docs per lane");
   static_assert(STAGE_BYTES % 1024 == 0 && A_BYTES % 16 == 0, "alignment");
 };
 

@@ -183,7 +183,7 @@ def test_max_length_docs(oracle, cuda_ok, d):
     # work unit) mixed with short ones, plus a batch of one query (small units)
     rng = np.random.default_rng(51)
     t = rng.integers(1, 64, 600)
-    tmax = 4096 if d == 32 else 2048  # UNITMAX x 64 slots (TcCfg)
+    tmax = 6144 if d == 32 else 2048  # UNITMAX x 64 slots (TcCfg, rounded query)
     t[[3, 77, 400]] = [tmax, tmax - 1, tmax // 2 + 1]
     rp = np.zeros(601, np.uint64)
     rp[1:] = np.cumsum(t)
@@ -213,6 +213,9 @@ def test_max_length_docs(oracle, cuda_ok, d):
     with pytest.raises(api.InvalidConfigError, match=str(tmax)):
         rr.rerank_arrays(q, ids, cls, off, cfg, kernel="tcgen05")
     rr.rerank_arrays(q, ids, cls, off, cfg)  # auto -> CUDA cores
+    if d == 32:  # the split-query layout has 64-doc units: 4096 slots
+        with pytest.raises(api.InvalidConfigError, match="4096"):
+            rr.rerank_arrays(q, ids, cls, off, cfg, kernel="tcgen05", query_precision="split")
     rr.close()
     store.close()
 
