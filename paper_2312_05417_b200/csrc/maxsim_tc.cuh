@@ -79,7 +79,7 @@ template <bool S> struct TcCfg<16, S>  { static constexpr int NQC = 128, NS = 6,
 #ifndef ESPN_D32_UNITMAX
 #define ESPN_D32_UNITMAX 96  // docs per work unit, d = 32 rounded query (served C2: 32.9 us; 64: 35.8; 128 with NU 2: 34.0)
 #endif
-template <bool S> struct TcCfg<32, S>  { static constexpr int NQC = ESPN_D32_NQC, NS = S ? 4 : ESPN_D32_NS, UNITMAX = S ? 64 : ESPN_D32_UNITMAX, NU = S ? 3 : ESPN_D32_NU; static constexpr bool REPA = false; };
+template <bool S> struct TcCfg<32, S>  { static constexpr int NQC = S ? 128 : ESPN_D32_NQC, NS = S ? 4 : ESPN_D32_NS, UNITMAX = S ? 64 : ESPN_D32_UNITMAX, NU = S ? 3 : ESPN_D32_NU; static constexpr bool REPA = false; };
 template <bool S> struct TcCfg<64, S>  { static constexpr int NQC = 64,  NS = 3, UNITMAX = 64, NU = S ? 2 : 3; static constexpr bool REPA = false; };
 template <bool S> struct TcCfg<128, S> { static constexpr int NQC = 64,  NS = 2, UNITMAX = 32, NU = S ? 1 : 2; static constexpr bool REPA = true; };
 
@@ -910,7 +910,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
           const uint32_t nv = remv < L::HALF ? (uint32_t)remv : (uint32_t)L::HALF;
           const uint32_t taddr0 = S.tmem_base + ((uint32_t)(w * 32) << 16) + buf * L::BUFC +
                                   (L::REPA ? w * L::NQC : 0) + h * L::HALF;
-          float v[L::NLD][L::LW];
+          float v[L::NLD < 2 ? L::NLD : 2][L::LW];  // two-chunk ring: chunk c in v[c & 1]
           tmem_ld_32x32b<L::LW>(taddr0, v[0]);
           const uint32_t G0 = xw >> 3;  // multiple of NGH
           const uint32_t bw = U.bitmap[G0 >> 5];
@@ -922,7 +922,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
           for (int c = 0; c < L::NLD; ++c) {
             tmem_ld_wait();
             if (c + 1 < L::NLD) {
-              if ((uint32_t)(L::LW * (c + 1)) < nv) tmem_ld_32x32b<L::LW>(taddr0 + L::LW * (c + 1), v[c + 1]);
+              if ((uint32_t)(L::LW * (c + 1)) < nv) tmem_ld_32x32b<L::LW>(taddr0 + L::LW * (c + 1), v[(c + 1) & 1]);
             } else {
               tc_fence_before();
               __syncwarp();
@@ -932,7 +932,7 @@ __device__ __forceinline__ void tc_batch(const MaxSimParams& p, const TcSmem<D, 
 #pragma unroll
             for (int qq = 0; qq < GPC; ++qq) {
               const int q = c * GPC + qq;
-              const float* x = &v[c][8 * qq];
+              const float* x = &v[c & 1][8 * qq];
 #if ESPN_NO_PATCH
               const uint32_t nvq = U.vc[G0 + q];  // warp-uniform
               if (nvq < 8) {
