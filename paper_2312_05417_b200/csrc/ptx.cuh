@@ -27,7 +27,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // try_wait with a suspend-time hint: the waiting warp sleeps in hardware until
 // the phase completes (or the hint expires) instead of spinning on issue slots
 // shared with the compute warps of its SM sub-partition.
+#ifndef ESPN_WAIT_MODE
+#define ESPN_WAIT_MODE 1  // A/B knob: 0 try_wait without a time hint, 1 try_wait with a 10 ms hint, 2 test_wait spin
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if ESPN_WAIT_MODE == 0
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra LAB_WAIT;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#elif ESPN_WAIT_MODE == 2
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra LAB_WAIT;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
@@ -35,6 +55,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra LAB_WAIT;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680)
       : "memory");
+#endif
 }
 // Arrive and add `bytes` to the barrier's expected transaction count.
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
