@@ -45,6 +45,9 @@ constexpr int kSmallMaxList = 2048;       // scored candidates per query
 constexpr int kSmallHashSlots = 4096;     // per-query duplicate hash (2x the longest list)
 constexpr int kSmallMaxCtas = 296;        // 2 per SM
 constexpr int kSmallLevel1Keys = 16 * kFusedMaxK;  // <= 16 level-1 lists of k
+#ifndef ESPN_SMALL_SELECT
+#define ESPN_SMALL_SELECT 1  // last-CTA merge by threshold select (0: two-level k-way merge only)
+#endif
 // per-warp fp32 row staging: at least one quad of rows, within the 48 KB of
 // static shared memory next to the query (32 x d fp32)
 template <int D>
@@ -128,7 +131,8 @@ __global__ void __launch_bounds__(small_threads<D>()) rerank_small_kernel(const 
   // compute phase: NW row-staging buffers; the last CTA's merge phase reuses
   // the space for the P lists and the level-1 merges
   __shared__ __align__(16) uint8_t region[REGION];
-  __shared__ uint32_t s_last;
+  __shared__ uint32_t s_last, s_ncand;
+  __shared__ uint64_t s_thr;
   static_assert(WROWS >= 4 && LIST_KEYS >= 1024, "row staging / merge scratch");
   static_assert(NT >= kSmallMaxChunk, "one thread per candidate");
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -349,13 +353,66 @@ __global__ void __launch_bounds__(small_threads<D>()) rerank_small_kernel(const 
   __threadfence();
   const unsigned long long* lists = p.unit_top + (size_t)b * P * k;
   const uint32_t nkeys = P * k;
+  bool merged = false;
   if (nkeys <= (uint32_t)LIST_KEYS && P <= 32u * NW) {
-    // the P lists -> shared memory in one round trip; warps k-way merge 32
-    // lists each (level 1), warp 0 merges their results
+    // the P lists -> shared memory in one round trip
     uint64_t* L0 = reinterpret_cast<uint64_t*>(region);
     uint64_t* L1 = L0 + LIST_KEYS;
     for (uint32_t i = tid; i < nkeys; i += NT) L0[i] = __ldcg(&lists[i]);
+    if (tid == 0) {
+      s_thr = 1ull;  // fewer than k non-empty lists: every non-empty key competes
+      s_ncand = 0u;
+    }
     __syncthreads();
+#if ESPN_SMALL_SELECT
+    // Threshold select (replaces two rounds of serial k-way merging, which
+    // took ~7 us of the 17 us batch-1 kernel, small_timeline_r2.txt): the
+    // lists are sorted and keys are unique, so with T = the k-th largest
+    // list head there are k keys >= T and the query's top k are exactly the
+    // k largest keys >= T.  Those come from the <= k lists whose head is
+    // >= T, so there are at most k * k of them; each is placed by counting
+    // the larger ones.  (Keys repeat only for duplicate ids, which fail the
+    // call; more than kSmallLevel1Keys survivors falls back to the merge.)
+    if (tid < P) {
+      const uint64_t h = L0[tid * k];
+      if (h != 0) {
+        uint32_t above = 0;
+        for (uint32_t m = 0; m < P; ++m) above += L0[m * k] > h ? 1u : 0u;
+        if (above == k - 1) s_thr = h;
+      }
+    }
+    __syncthreads();
+    const uint64_t T = s_thr;
+    for (uint32_t i = tid; i < nkeys; i += NT) {
+      const uint64_t v = L0[i];
+      if (v >= T) {
+        const uint32_t at = atomicAdd(&s_ncand, 1u);
+        if (at < (uint32_t)kSmallLevel1Keys) L1[at] = v;
+      }
+    }
+    __syncthreads();
+    const uint32_t M = s_ncand;
+    if (M <= (uint32_t)kSmallLevel1Keys) {
+      for (uint32_t i = tid; i < M; i += NT) {
+        const uint64_t v = L1[i];
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < M; ++j) r += L1[j] > v ? 1u : 0u;
+        if (r < k) {
+          p.out_ids[(size_t)b * k + r] = ~(uint32_t)(v & 0xFFFFFFFFu);
+          p.out_scores[(size_t)b * k + r] = order_float((uint32_t)(v >> 32));
+        }
+      }
+      if (tid == 0) p.out_counts[b] = min(M, k);
+      merged = true;
+    }
+#endif
+  }
+  if (merged) {
+    // (placed by the threshold select)
+  } else if (nkeys <= (uint32_t)LIST_KEYS && P <= 32u * NW) {
+    // warps k-way merge 32 lists each (level 1), warp 0 merges their results
+    uint64_t* L0 = reinterpret_cast<uint64_t*>(region);
+    uint64_t* L1 = L0 + LIST_KEYS;
     const uint32_t n1 = (P + 31) / 32;
     if (wid < n1) small_kway(L0 + (size_t)wid * 32 * k, min(32u, P - wid * 32), k, L1 + wid * k, lane);
     __syncthreads();

@@ -106,6 +106,19 @@ def test_longest_lists_and_max_batch(oracle, cuda_ok):
         _exact(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, got)
 
 
+def test_last_cta_merge_select_and_fallback(oracle, cuda_ok):
+    # final_k = 32 over 2048-candidate lists: 4 queries get 74 CTAs each (the
+    # last CTA's threshold select over 74 lists), 16 queries get 18 CTAs each
+    # (fewer lists than k: all 576 keys survive, more than the select's 512
+    # slots, so the two-level k-way merge runs instead)
+    for B, K in ((4, 2048), (16, 2048)):
+        rp, codes, q, ids, cls, off, _ = _case(40000, 32, 32, B, K, seed=B * 13 + 5)
+        cfg = api.PipelineConfig(rerank_count=K, final_k=32)
+        got, launches = _run(rp, codes, 32, "f16", q, ids, cls, off, cfg)
+        assert launches == 1
+        _exact(oracle, rp, codes, 32, "f16", q, ids, cls, off, cfg, got)
+
+
 def test_matches_simt_and_tcgen05(oracle, cuda_ok):
     rp, codes, q, ids, cls, off, _ = _case(20000, 32, 32, 2, 1000, seed=77)
     cfg = api.PipelineConfig(rerank_count=1000, final_k=10)
